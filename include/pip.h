@@ -1,0 +1,189 @@
+/*
+ * pip.h — C ABI of the B200-native parallel in-place (PIP) kernels.
+ *
+ * This is the drop-in boundary for the reference's hot path
+ * (`pipal`, /root/reference/pkg/src/pipal).  The reference is pure Python on
+ * numpy uint64 arrays; its "plugin API" is the module-level functions listed
+ * next to each entry point below.  A Python host layer
+ * (paper_2103_01216_b200/) binds these entry points through ctypes and keeps
+ * the reference's signatures, argument meaning and error behaviour; any
+ * other FFI (cgo, JNI, N-API) can bind the same symbols — see INTEGRATION.md.
+ *
+ * Conventions
+ *   - every array is a plain pointer to 64-bit words plus an element count;
+ *   - `*_u64` entry points take DEVICE pointers and are stream-ordered on the
+ *     given cudaStream_t (passed as void*, NULL = legacy default stream);
+ *     device results (totals, counts) are written to DEVICE pointers;
+ *   - `*_host` entry points take HOST pointers, run synchronously on a device
+ *     of the caller's choice and include the host<->device transfers
+ *     (chunked and overlapped where the algorithm streams);
+ *   - nothing allocates device memory except the `*_host` entry points:
+ *     auxiliary space comes from caller-provided `scratch` (O(#CTAs) bytes,
+ *     independent of n: the analogue of the reference's unmetered recursion
+ *     stack) and `workspace` (sublinear, metered by the caller — the analogue
+ *     of runtime.alloc / runtime.release);
+ *   - values are unsigned 64-bit; comparisons are unsigned (the reference
+ *     compares numpy uint64), sums wrap mod 2^64.
+ *   - every function returns a pip_status.
+ */
+#ifndef PIP_H_
+#define PIP_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum pip_status {
+  PIP_OK = 0,
+  PIP_ERR_INVALID_ARG = 1,   /* reference: ValueError (bad split/offset/...) */
+  PIP_ERR_INVALID_SWAPS = 2, /* reference: ValueError, H[i] must lie in [0,i] */
+  PIP_ERR_LIVELOCK = 3,      /* reference: detres.LivelockError */
+  PIP_ERR_OOM = 4,           /* workspace / scratch too small */
+  PIP_ERR_CUDA = 5,          /* CUDA runtime error (see pip_last_cuda_error) */
+  PIP_ERR_UNSORTED = 6,      /* reference: ValueError("unsorted input run") */
+  PIP_ERR_UNSUPPORTED = 7,   /* size or option outside this build's support */
+  PIP_ERR_TABLE = 8,         /* reservation table overfull (never in practice) */
+  PIP_ERR_DEBUG_SWEEP = 9    /* reference: debug sweep assertion failed */
+};
+
+/* scan element operations (strong.scan `op`): None/add, max, min, xor */
+enum pip_scan_op { PIP_OP_ADD = 0, PIP_OP_MAX = 1, PIP_OP_MIN = 2, PIP_OP_XOR = 3 };
+
+/* random-permutation storage variants (relaxed.RP_VARIANTS) */
+enum pip_rp_variant { PIP_RP_NAIVE = 0, PIP_RP_FLAT = 1, PIP_RP_ONERES = 2, PIP_RP_FINAL = 3 };
+
+/* Predicate descriptor replacing the reference's numpy callables
+ * (cli.py:41 EVEN, test_strong.py:21,184, strong.py:440-441,553).
+ * keep(x) = negate XOR test(x), with
+ *   PIP_PRED_MASK_EQ : (x & a) == b          (even: a=1,b=0; odd: a=1,b=1)
+ *   PIP_PRED_MOD_EQ  : (x % a) == b          (a >= 1; u64 magic division)
+ *   PIP_PRED_LT/LE/GT/GE/EQ : x op a         (unsigned)
+ *   PIP_PRED_ALL     : true
+ */
+enum pip_pred_kind {
+  PIP_PRED_ALL = 0, PIP_PRED_MASK_EQ = 1, PIP_PRED_MOD_EQ = 2, PIP_PRED_LT = 3,
+  PIP_PRED_LE = 4, PIP_PRED_GT = 5, PIP_PRED_GE = 6, PIP_PRED_EQ = 7
+};
+typedef struct pip_pred {
+  uint32_t kind;
+  uint32_t negate;
+  uint64_t a;
+  uint64_t b;
+} pip_pred;
+
+/* Round statistics of the deterministic-reservations engine
+ * (detres.RoundStats, detres.py:222-230). */
+typedef struct pip_rp_stats {
+  uint64_t rounds;             /* RoundStats.rounds */
+  uint64_t total_committed;    /* RoundStats.total_committed */
+  uint64_t n_iterates;         /* non-self swaps (relaxed.py:239) */
+  uint64_t peak_table_count;   /* max distinct keys held by the table in a round */
+  uint64_t table_capacity;     /* reference capacity: peak_table_load = count/capacity */
+  uint64_t prefix;             /* b(n) used */
+  uint64_t workspace_words;    /* device workspace the run used, in 64-bit words */
+  uint64_t rounds_recorded;    /* committed-per-round entries written */
+} pip_rp_stats;
+
+/* ---- library / sizing ---------------------------------------------------- */
+int pip_version(void);
+const char* pip_status_string(int status);
+const char* pip_last_cuda_error(void);
+/* bytes of O(#CTAs) scratch every strong op needs on `device` */
+size_t pip_scratch_bytes(int device);
+
+/* ---- scan: strong.scan / strong.scan_blocked (strong.py:151-236) --------- *
+ * Exclusive (inclusive=0) or inclusive in-place scan of a[0:n) under `op`.
+ * Exclusive output: a[i] = op(init, x0 op ... op x_{i-1}), a[0] = init
+ * (reference: op=None -> init 0; op given -> init = `identity`).
+ * Inclusive output: a[i] = op(init, x0 op ... op x_i).
+ * total_dev (device, may be NULL) receives x0 op ... op x_{n-1} (no init).
+ * Replaces strong.py:151-166 (scan) and :169-236 (scan_blocked).           */
+int pip_scan_u64(uint64_t* a, uint64_t n, int op, uint64_t init, int inclusive,
+                 uint64_t* total_dev, void* scratch, size_t scratch_bytes, void* stream);
+/* Fold without writing (strong.reduce, strong.py:43-64; shard totals). */
+int pip_reduce_u64(const uint64_t* a, uint64_t n, int op, uint64_t* total_dev,
+                   void* scratch, size_t scratch_bytes, void* stream);
+/* Host-buffer scan: H2D / scan-with-carry / D2H pipelined in chunks. */
+int pip_scan_u64_host(uint64_t* host_a, uint64_t n, int op, uint64_t init, int inclusive,
+                      uint64_t* total_out, int device);
+
+/* ---- filter: strong.filter_kway / relaxed.filter_relaxed ----------------- *
+ * Stable in-place filter of a[0:n): kept values end in a[0:m) in original
+ * order; a[m:n) is unspecified (as in the reference).  m_dev (device)
+ * receives m.  Replaces strong.py:283-349 and relaxed.py:284-309.          */
+int pip_filter_u64(uint64_t* a, uint64_t n, const pip_pred* pred, uint64_t* m_dev,
+                   void* scratch, size_t scratch_bytes, void* stream);
+/* Count kept elements without moving anything (shard counts). */
+int pip_count_u64(const uint64_t* a, uint64_t n, const pip_pred* pred, uint64_t* m_dev,
+                  void* scratch, size_t scratch_bytes, void* stream);
+int pip_filter_u64_host(uint64_t* host_a, uint64_t n, const pip_pred* pred, uint64_t* m_out,
+                        int device);
+
+/* ---- rotate: strong.rotate (strong.py:67-95) ------------------------------ *
+ * Left rotation: out[i] = in[(i + o) mod n], 0 <= o <= n.                   */
+int pip_rotate_u64(uint64_t* a, uint64_t n, uint64_t o, void* scratch, size_t scratch_bytes,
+                   void* stream);
+
+/* ---- merge: strong.merge_strong / relaxed.merge_relaxed ------------------ *
+ * a[0:split) and a[split:n) are sorted ascending (unsigned); on return a is
+ * sorted.  `workspace`/`workspace_bytes` is the metered auxiliary space
+ * (pip_merge_workspace_bytes tells how much a given budget can use); with
+ * workspace_bytes == 0 the strong (zero-heap) schedule runs on scratch only.
+ * check_sorted != 0 reproduces debug=True (PIP_ERR_UNSORTED).
+ * Replaces strong.py:496-522 and relaxed.py:579-612.                        */
+int pip_merge_u64(uint64_t* a, uint64_t n, uint64_t split, int check_sorted,
+                  void* workspace, size_t workspace_bytes, void* scratch, size_t scratch_bytes,
+                  void* stream);
+/* device workspace (bytes) the relaxed merge uses for n, split and budget
+ * b = budget_words (b(n) of the caller's EpsilonConfig); 0 = strong path. */
+size_t pip_merge_workspace_bytes(uint64_t n, uint64_t split, uint64_t budget_words);
+int pip_merge_u64_host(uint64_t* host_a, uint64_t n, uint64_t split, uint64_t budget_words,
+                       int device);
+
+/* ---- random permutation: relaxed.random_permutation (relaxed.py:220-251) - *
+ * Applies the Knuth swap sequence H (swap a[i], a[H[i]] for i = n-1..0) as
+ * deterministic-reservation rounds over prefix = b(n) pending iterates
+ * (detres.run_rounds, detres.py:256-307), with the reference's round
+ * structure (descending ids, self-swaps retired at ingestion, failures
+ * packed first), so rounds / committed-per-round / trace are identical.
+ *   committed_per_round_dev: device u64[rounds_cap] (NULL ok)
+ *   trace_dev: device u64[n_iterates] of committed ids in round/packed order
+ *   (NULL ok); debug != 0 runs the clean-table sweep (relaxed.py:212-217).
+ * workspace must hold pip_rp_workspace_bytes(n, prefix, variant).
+ * stats_host receives the round statistics (the call synchronizes).        */
+size_t pip_rp_workspace_bytes(uint64_t n, uint64_t prefix, int variant);
+int pip_random_permutation_u64(uint64_t* a, const uint64_t* h, uint64_t n, uint64_t prefix,
+                               int variant, int debug, uint64_t* committed_per_round_dev,
+                               uint64_t rounds_cap, uint64_t* trace_dev,
+                               void* workspace, size_t workspace_bytes,
+                               pip_rp_stats* stats_host, void* stream);
+/* relaxed.validate_swap_sequence (relaxed.py:55-58) + the non-self count of
+ * relaxed.py:239: nonself_dev receives #{i : H[i] != i}; returns
+ * PIP_ERR_INVALID_SWAPS (after syncing) when some H[i] > i.               */
+int pip_validate_swaps_u64(const uint64_t* h, uint64_t n, uint64_t* nonself_dev,
+                           void* scratch, size_t scratch_bytes, void* stream);
+int pip_random_permutation_u64_host(uint64_t* host_a, const uint64_t* host_h, uint64_t n,
+                                    uint64_t prefix, int variant, pip_rp_stats* stats_host,
+                                    int device);
+
+/* ---- input generation (runtime.Rng, runtime.py:263-302) ------------------ *
+ * out[k] = mix64(seed + (lo + k + 1) * GOLDEN) >> shift   (Rng.words)
+ * swaps: out[k] = Rng.words(lo..)[k] % (lo + k + 1)      (make_swap_sequence) */
+int pip_rng_words_u64(uint64_t* out, uint64_t lo, uint64_t count, uint64_t seed,
+                      uint32_t shift, void* stream);
+int pip_make_swaps_u64(uint64_t* out, uint64_t lo, uint64_t count, uint64_t seed,
+                       void* stream);
+
+/* ---- microbenchmarks used by the roofline (bench.py) --------------------- */
+/* iters rounds of 8-byte read-modify-write at uniform random word indices of
+ * buf[0:n) (one per thread of a full grid); returns device time in ms. */
+int pip_bench_random_rmw(uint64_t* buf, uint64_t n, uint64_t updates, uint64_t seed,
+                         float* ms_out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PIP_H_ */

@@ -1,0 +1,365 @@
+// extern "C" boundary (include/pip.h) and the host-buffer entry points.
+#include <cstdio>
+#include <cstring>
+#include <vector>
+#include "common.cuh"
+
+namespace pip {
+
+static thread_local char g_cuda_err[256] = "";
+void set_cuda_error(cudaError_t e) {
+  snprintf(g_cuda_err, sizeof(g_cuda_err), "%s: %s", cudaGetErrorName(e), cudaGetErrorString(e));
+}
+
+int current_device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d;
+}
+
+int num_sms(int device) {
+  static int cache[64] = {0};
+  if (device < 0 || device >= 64) device = 0;
+  if (!cache[device]) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device);
+    cache[device] = v > 0 ? v : 1;
+  }
+  return cache[device];
+}
+
+size_t scratch_bytes_for(int sms);
+int scan_device(u64* a, u64 n, int op, u64 init, int inclusive, const u64* carry_dev,
+                u64* total_dev, void* scratch, size_t scratch_bytes, cudaStream_t st);
+int reduce_device(const u64* a, u64 n, int op, u64* total_dev, void* scratch, size_t scratch_bytes,
+                  cudaStream_t st);
+int filter_device(u64* a, u64 n, const pip_pred* pred, u64* m_dev, void* scratch,
+                  size_t scratch_bytes, cudaStream_t st);
+int count_device(const u64* a, u64 n, const pip_pred* pred, u64* m_dev, void* scratch,
+                 size_t scratch_bytes, cudaStream_t st);
+int rotate_device(u64* a, u64 n, u64 o, cudaStream_t st);
+int validate_device(const u64* h, u64 n, u64* nonself_dev, void* scratch, size_t scratch_bytes,
+                    cudaStream_t st);
+int rng_words(u64* out, u64 lo, u64 count, u64 seed, u32 shift, cudaStream_t st);
+int make_swaps(u64* out, u64 lo, u64 count, u64 seed, cudaStream_t st);
+int bench_random_rmw(u64* buf, u64 n, u64 updates, u64 seed, float* ms, cudaStream_t st);
+size_t rp_workspace_bytes(u64 n, u64 prefix, int variant);
+int rp_device(u64* a, const u64* h, u64 n, u64 prefix, int variant, int debug,
+              u64* counts_host, u64 rounds_cap, u64* trace_dev, void* ws, size_t ws_bytes,
+              pip_rp_stats* stats, cudaStream_t st);
+size_t merge_workspace_bytes(u64 n, u64 split, u64 budget_words);
+int merge_device(u64* a, u64 n, u64 split, int check_sorted, void* ws, size_t ws_bytes,
+                 void* scratch, size_t scratch_bytes, cudaStream_t st);
+
+// ---------------------------------------------------------------------------
+// host-buffer helpers: RAII device allocations on a private stream
+struct DevBuf {
+  void* p = nullptr;
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  cudaError_t alloc(size_t bytes) { return cudaMalloc(&p, bytes ? bytes : 16); }
+};
+struct Stream {
+  cudaStream_t s = nullptr;
+  ~Stream() {
+    if (s) cudaStreamDestroy(s);
+  }
+  cudaError_t create() { return cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking); }
+};
+struct Event {
+  cudaEvent_t e = nullptr;
+  ~Event() {
+    if (e) cudaEventDestroy(e);
+  }
+  cudaError_t create() { return cudaEventCreateWithFlags(&e, cudaEventDisableTiming); }
+};
+
+static const u64 HOST_CHUNK = 1ull << 26;  // 512 MiB of words per pipeline stage
+
+// scan over host memory: chunk k is copied in on `cp_in`, scanned on `comp`
+// with the running carry (the previous chunk's inclusive fold) and copied
+// out on `cp_out`; three chunk buffers keep all three engines busy.
+int scan_host(u64* host, u64 n, int op, u64 init, int inclusive, u64* total_out, int device) {
+  PIP_CUDA(cudaSetDevice(device));
+  const int sms = num_sms(device);
+  if (n == 0) {
+    if (total_out) *total_out = init;
+    return PIP_OK;
+  }
+  const u64 chunk = n < HOST_CHUNK ? n : HOST_CHUNK;
+  const int nb = n > chunk ? 3 : 1;
+  DevBuf bufs[3], scratch, carry;
+  for (int i = 0; i < nb; ++i) PIP_CUDA(bufs[i].alloc(chunk * 8));
+  const size_t sb = scratch_bytes_for(sms);
+  PIP_CUDA(scratch.alloc(sb));
+  PIP_CUDA(carry.alloc(16 * 8));
+  Stream cin, comp, cout;
+  PIP_CUDA(cin.create());
+  PIP_CUDA(comp.create());
+  PIP_CUDA(cout.create());
+  const u64 nchunks = (n + chunk - 1) / chunk;
+  std::vector<Event> in_done(nchunks), comp_done(nchunks), out_done(nchunks);
+  u64* cr = (u64*)carry.p;  // cr[k & 1] = carry into chunk k
+  u64 ident = op == PIP_OP_MIN ? ~0ull : 0ull;
+  PIP_CUDA(cudaMemcpyAsync(cr, &ident, 8, cudaMemcpyHostToDevice, comp.s));
+  PIP_CUDA(cudaStreamSynchronize(comp.s));
+  for (u64 k = 0; k < nchunks; ++k) {
+    PIP_CUDA(in_done[k].create());
+    PIP_CUDA(comp_done[k].create());
+    PIP_CUDA(out_done[k].create());
+    const u64 off = k * chunk, len = (n - off) < chunk ? (n - off) : chunk;
+    u64* b = (u64*)bufs[k % nb].p;
+    if (k >= (u64)nb) PIP_CUDA(cudaStreamWaitEvent(cin.s, out_done[k - nb].e, 0));
+    PIP_CUDA(cudaMemcpyAsync(b, host + off, len * 8, cudaMemcpyHostToDevice, cin.s));
+    PIP_CUDA(cudaEventRecord(in_done[k].e, cin.s));
+    PIP_CUDA(cudaStreamWaitEvent(comp.s, in_done[k].e, 0));
+    int rc = scan_device(b, len, op, init, inclusive, cr + (k & 1), cr + ((k + 1) & 1),
+                         scratch.p, sb, comp.s);
+    if (rc) return rc;
+    PIP_CUDA(cudaEventRecord(comp_done[k].e, comp.s));
+    PIP_CUDA(cudaStreamWaitEvent(cout.s, comp_done[k].e, 0));
+    PIP_CUDA(cudaMemcpyAsync(host + off, b, len * 8, cudaMemcpyDeviceToHost, cout.s));
+    PIP_CUDA(cudaEventRecord(out_done[k].e, cout.s));
+  }
+  u64 tot = 0;
+  PIP_CUDA(cudaMemcpyAsync(&tot, cr + (nchunks & 1), 8, cudaMemcpyDeviceToHost, comp.s));
+  PIP_CUDA(cudaStreamSynchronize(comp.s));
+  PIP_CUDA(cudaStreamSynchronize(cout.s));
+  u32 abort_flag = 0;
+  PIP_CUDA(cudaMemcpy(&abort_flag, scratch.p, 4, cudaMemcpyDeviceToHost));
+  if (abort_flag) return PIP_ERR_CUDA;
+  if (total_out) *total_out = tot;
+  return PIP_OK;
+}
+
+// filter over host memory: chunk k is filtered on device; once its kept
+// count is known the kept prefix goes back to host[m : m + kept), which lies
+// inside the already-uploaded part of the array (m <= chunk start).
+int filter_host(u64* host, u64 n, const pip_pred* pred, u64* m_out, int device) {
+  PIP_CUDA(cudaSetDevice(device));
+  const int sms = num_sms(device);
+  if (n == 0) {
+    if (m_out) *m_out = 0;
+    return PIP_OK;
+  }
+  const u64 chunk = n < HOST_CHUNK ? n : HOST_CHUNK;
+  const int nb = n > chunk ? 3 : 1;
+  DevBuf bufs[3], scratch, counts;
+  for (int i = 0; i < nb; ++i) PIP_CUDA(bufs[i].alloc(chunk * 8));
+  const size_t sb = scratch_bytes_for(sms);
+  PIP_CUDA(scratch.alloc(sb));
+  const u64 nchunks = (n + chunk - 1) / chunk;
+  PIP_CUDA(counts.alloc(nchunks * 8));
+  u64* hc = nullptr;
+  PIP_CUDA(cudaMallocHost(&hc, nchunks * 8));
+  struct HostFree {
+    u64* p;
+    ~HostFree() { cudaFreeHost(p); }
+  } hf{hc};
+  Stream cin, comp, cout;
+  PIP_CUDA(cin.create());
+  PIP_CUDA(comp.create());
+  PIP_CUDA(cout.create());
+  std::vector<Event> in_done(nchunks), cnt_done(nchunks), out_done(nchunks);
+  for (u64 k = 0; k < nchunks; ++k) {
+    PIP_CUDA(in_done[k].create());
+    PIP_CUDA(cnt_done[k].create());
+    PIP_CUDA(out_done[k].create());
+  }
+  u64 m = 0;
+  auto issue = [&](u64 k) -> int {
+    const u64 off = k * chunk, len = (n - off) < chunk ? (n - off) : chunk;
+    u64* b = (u64*)bufs[k % nb].p;
+    if (k >= (u64)nb) PIP_CUDA(cudaStreamWaitEvent(cin.s, out_done[k - nb].e, 0));
+    PIP_CUDA(cudaMemcpyAsync(b, host + off, len * 8, cudaMemcpyHostToDevice, cin.s));
+    PIP_CUDA(cudaEventRecord(in_done[k].e, cin.s));
+    PIP_CUDA(cudaStreamWaitEvent(comp.s, in_done[k].e, 0));
+    int rc = filter_device(b, len, pred, (u64*)counts.p + k, scratch.p, sb, comp.s);
+    if (rc) return rc;
+    PIP_CUDA(cudaMemcpyAsync(hc + k, (u64*)counts.p + k, 8, cudaMemcpyDeviceToHost, comp.s));
+    PIP_CUDA(cudaEventRecord(cnt_done[k].e, comp.s));
+    return PIP_OK;
+  };
+  const u64 ahead = (u64)nb - 1;
+  for (u64 k = 0; k < nchunks && k <= ahead; ++k)
+    if (int rc = issue(k)) return rc;
+  for (u64 k = 0; k < nchunks; ++k) {
+    PIP_CUDA(cudaEventSynchronize(cnt_done[k].e));
+    const u64 kept = hc[k];
+    u64* b = (u64*)bufs[k % nb].p;
+    if (kept) PIP_CUDA(cudaMemcpyAsync(host + m, b, kept * 8, cudaMemcpyDeviceToHost, cout.s));
+    PIP_CUDA(cudaEventRecord(out_done[k].e, cout.s));
+    m += kept;
+    if (k + 1 + ahead < nchunks)
+      if (int rc = issue(k + 1 + ahead)) return rc;
+  }
+  PIP_CUDA(cudaStreamSynchronize(cout.s));
+  u32 abort_flag = 0;
+  PIP_CUDA(cudaMemcpy(&abort_flag, scratch.p, 4, cudaMemcpyDeviceToHost));
+  if (abort_flag) return PIP_ERR_CUDA;
+  if (m_out) *m_out = m;
+  return PIP_OK;
+}
+
+}  // namespace pip
+
+using namespace pip;
+
+extern "C" {
+
+int pip_version(void) { return 1; }
+
+const char* pip_status_string(int s) {
+  switch (s) {
+    case PIP_OK: return "ok";
+    case PIP_ERR_INVALID_ARG: return "invalid argument";
+    case PIP_ERR_INVALID_SWAPS: return "invalid swap sequence: H[i] must lie in [0, i]";
+    case PIP_ERR_LIVELOCK: return "no iterate committed for 64 rounds";
+    case PIP_ERR_OOM: return "workspace or scratch too small";
+    case PIP_ERR_CUDA: return "CUDA error";
+    case PIP_ERR_UNSORTED: return "unsorted input run";
+    case PIP_ERR_UNSUPPORTED: return "unsupported size or option";
+    case PIP_ERR_TABLE: return "reservation table overfull; presize the table";
+    case PIP_ERR_DEBUG_SWEEP: return "debug sweep: reservation slots not clean after a round";
+    default: return "unknown status";
+  }
+}
+
+const char* pip_last_cuda_error(void) { return g_cuda_err; }
+
+size_t pip_scratch_bytes(int device) { return scratch_bytes_for(num_sms(device)); }
+
+int pip_scan_u64(uint64_t* a, uint64_t n, int op, uint64_t init, int inclusive, uint64_t* total_dev,
+                 void* scratch, size_t scratch_bytes, void* stream) {
+  return scan_device((u64*)a, n, op, init, inclusive, nullptr, (u64*)total_dev, scratch,
+                     scratch_bytes, (cudaStream_t)stream);
+}
+
+int pip_reduce_u64(const uint64_t* a, uint64_t n, int op, uint64_t* total_dev, void* scratch,
+                   size_t scratch_bytes, void* stream) {
+  return reduce_device((const u64*)a, n, op, (u64*)total_dev, scratch, scratch_bytes,
+                       (cudaStream_t)stream);
+}
+
+int pip_scan_u64_host(uint64_t* host_a, uint64_t n, int op, uint64_t init, int inclusive,
+                      uint64_t* total_out, int device) {
+  if (op < PIP_OP_ADD || op > PIP_OP_XOR || (n && !host_a)) return PIP_ERR_INVALID_ARG;
+  return scan_host((u64*)host_a, n, op, init, inclusive, (u64*)total_out, device);
+}
+
+int pip_filter_u64(uint64_t* a, uint64_t n, const pip_pred* pred, uint64_t* m_dev, void* scratch,
+                   size_t scratch_bytes, void* stream) {
+  return filter_device((u64*)a, n, pred, (u64*)m_dev, scratch, scratch_bytes, (cudaStream_t)stream);
+}
+
+int pip_count_u64(const uint64_t* a, uint64_t n, const pip_pred* pred, uint64_t* m_dev,
+                  void* scratch, size_t scratch_bytes, void* stream) {
+  return count_device((const u64*)a, n, pred, (u64*)m_dev, scratch, scratch_bytes,
+                      (cudaStream_t)stream);
+}
+
+int pip_filter_u64_host(uint64_t* host_a, uint64_t n, const pip_pred* pred, uint64_t* m_out,
+                        int device) {
+  if (!pred || (n && !host_a)) return PIP_ERR_INVALID_ARG;
+  return filter_host((u64*)host_a, n, pred, (u64*)m_out, device);
+}
+
+int pip_rotate_u64(uint64_t* a, uint64_t n, uint64_t o, void* scratch, size_t scratch_bytes,
+                   void* stream) {
+  (void)scratch;
+  (void)scratch_bytes;
+  return rotate_device((u64*)a, n, o, (cudaStream_t)stream);
+}
+
+size_t pip_merge_workspace_bytes(uint64_t n, uint64_t split, uint64_t budget_words) {
+  return merge_workspace_bytes(n, split, budget_words);
+}
+
+int pip_merge_u64(uint64_t* a, uint64_t n, uint64_t split, int check_sorted, void* workspace,
+                  size_t workspace_bytes, void* scratch, size_t scratch_bytes, void* stream) {
+  return merge_device((u64*)a, n, split, check_sorted, workspace, workspace_bytes, scratch,
+                      scratch_bytes, (cudaStream_t)stream);
+}
+
+int pip_merge_u64_host(uint64_t* host_a, uint64_t n, uint64_t split, uint64_t budget_words,
+                       int device) {
+  if (split > n || (n && !host_a)) return PIP_ERR_INVALID_ARG;
+  PIP_CUDA(cudaSetDevice(device));
+  if (n == 0) return PIP_OK;
+  Stream s;
+  PIP_CUDA(s.create());
+  DevBuf a, ws, scratch;
+  PIP_CUDA(a.alloc(n * 8));
+  const size_t wb = merge_workspace_bytes(n, split, budget_words);
+  PIP_CUDA(ws.alloc(wb));
+  const size_t sb = scratch_bytes_for(num_sms(device));
+  PIP_CUDA(scratch.alloc(sb));
+  PIP_CUDA(cudaMemcpyAsync(a.p, host_a, n * 8, cudaMemcpyHostToDevice, s.s));
+  int rc = merge_device((u64*)a.p, n, split, 0, wb ? ws.p : nullptr, wb, scratch.p, sb, s.s);
+  if (rc) return rc;
+  PIP_CUDA(cudaMemcpyAsync(host_a, a.p, n * 8, cudaMemcpyDeviceToHost, s.s));
+  PIP_CUDA(cudaStreamSynchronize(s.s));
+  return PIP_OK;
+}
+
+size_t pip_rp_workspace_bytes(uint64_t n, uint64_t prefix, int variant) {
+  return rp_workspace_bytes(n, prefix, variant);
+}
+
+int pip_random_permutation_u64(uint64_t* a, const uint64_t* h, uint64_t n, uint64_t prefix,
+                               int variant, int debug, uint64_t* committed_per_round_host,
+                               uint64_t rounds_cap, uint64_t* trace_dev, void* workspace,
+                               size_t workspace_bytes, pip_rp_stats* stats_host, void* stream) {
+  return rp_device((u64*)a, (const u64*)h, n, prefix, variant, debug,
+                   (u64*)committed_per_round_host, rounds_cap, (u64*)trace_dev, workspace,
+                   workspace_bytes, stats_host, (cudaStream_t)stream);
+}
+
+int pip_validate_swaps_u64(const uint64_t* h, uint64_t n, uint64_t* nonself_dev, void* scratch,
+                           size_t scratch_bytes, void* stream) {
+  return validate_device((const u64*)h, n, (u64*)nonself_dev, scratch, scratch_bytes,
+                         (cudaStream_t)stream);
+}
+
+int pip_random_permutation_u64_host(uint64_t* host_a, const uint64_t* host_h, uint64_t n,
+                                    uint64_t prefix, int variant, pip_rp_stats* stats_host,
+                                    int device) {
+  if (n && (!host_a || !host_h)) return PIP_ERR_INVALID_ARG;
+  PIP_CUDA(cudaSetDevice(device));
+  if (n == 0) {
+    if (stats_host) memset(stats_host, 0, sizeof(*stats_host));
+    return PIP_OK;
+  }
+  Stream s;
+  PIP_CUDA(s.create());
+  DevBuf a, h, ws;
+  PIP_CUDA(a.alloc(n * 8));
+  PIP_CUDA(h.alloc(n * 8));
+  const size_t wb = rp_workspace_bytes(n, prefix, variant);
+  PIP_CUDA(ws.alloc(wb));
+  PIP_CUDA(cudaMemcpyAsync(a.p, host_a, n * 8, cudaMemcpyHostToDevice, s.s));
+  PIP_CUDA(cudaMemcpyAsync(h.p, host_h, n * 8, cudaMemcpyHostToDevice, s.s));
+  int rc = rp_device((u64*)a.p, (const u64*)h.p, n, prefix, variant, 0, nullptr, 0, nullptr, ws.p,
+                     wb, stats_host, s.s);
+  if (rc) return rc;
+  PIP_CUDA(cudaMemcpyAsync(host_a, a.p, n * 8, cudaMemcpyDeviceToHost, s.s));
+  PIP_CUDA(cudaStreamSynchronize(s.s));
+  return PIP_OK;
+}
+
+int pip_rng_words_u64(uint64_t* out, uint64_t lo, uint64_t count, uint64_t seed, uint32_t shift,
+                      void* stream) {
+  return rng_words((u64*)out, lo, count, seed, shift, (cudaStream_t)stream);
+}
+
+int pip_make_swaps_u64(uint64_t* out, uint64_t lo, uint64_t count, uint64_t seed, void* stream) {
+  return make_swaps((u64*)out, lo, count, seed, (cudaStream_t)stream);
+}
+
+int pip_bench_random_rmw(uint64_t* buf, uint64_t n, uint64_t updates, uint64_t seed, float* ms_out,
+                         void* stream) {
+  return bench_random_rmw((u64*)buf, n, updates, seed, ms_out, (cudaStream_t)stream);
+}
+
+}  // extern "C"

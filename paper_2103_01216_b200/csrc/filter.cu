@@ -1,0 +1,263 @@
+// Stable in-place filter (strong.filter_kway, relaxed.filter_relaxed) and
+// kept-count reduction.
+//
+// Reference: pkg/src/pipal/strong.py:283-349 — sqrt(n) chunks, a count
+// pass, then batches of chunks whose destinations precede the batch's
+// first source are compacted in parallel (:317-327); the predicate runs
+// twice per element.  relaxed.py:284-309 retires one b(n)-prefix per round
+// through a buffer.  Both leave a[0:m) = kept values in order, m returned,
+// a[m:) unspecified.
+//
+// Here: ONE pass, predicate evaluated once.  Same persistent look-back
+// skeleton as scan.cu with kept COUNTS as the scanned quantity.  In-place
+// safety: a tile writes only to [prefix, prefix + kept) with prefix <= its
+// own first index, i.e. into tiles that precede it; every such tile has
+// published its aggregate — which it can only do after its loads returned —
+// before this tile's look-back resolves.  So "destination precedes source"
+// (the reference's batching rule, strong.py:317-327) holds at tile
+// granularity without any batching.
+#include "lookback.cuh"
+
+namespace pip {
+
+static constexpr int FILTER_THREADS = 512;
+static constexpr u64 FILTER_TILE = (u64)FILTER_THREADS * 16;
+
+int scan_grid_for(const void* kernel, int threads, int device, u64 tiles, int* grid);
+
+template <bool VEC>
+__global__ void __launch_bounds__(FILTER_THREADS, 2)
+filter_kernel(u64* __restrict__ a, u64 n, DevPred p, u64* m_out, LookbackCtx c, u64 num_tiles) {
+  using O = Op<PIP_OP_ADD>;
+  __shared__ u64 s_warp[FILTER_THREADS / 32];
+  __shared__ int s_abort;
+  const u32 lane = lane_id(), warp = warp_id();
+  const u32 lt = (1u << lane) - 1u;
+
+  for (u64 tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+    const u64 wbase = tile * FILTER_TILE + (u64)warp * 512;
+    const bool full = VEC && (tile * FILTER_TILE + FILTER_TILE <= n);
+    u64 x[16];
+    u32 keep = 0;
+    if (full) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        ulonglong2 v = ldg_stream2(a + wbase + 64 * j + 2 * lane);
+        x[2 * j] = v.x;
+        x[2 * j + 1] = v.y;
+      }
+#pragma unroll
+      for (int k = 0; k < 16; ++k) keep |= (u32)pred_eval(p, x[k]) << k;
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const u64 i0 = wbase + 64 * j + 2 * lane;
+        x[2 * j] = i0 < n ? a[i0] : 0;
+        x[2 * j + 1] = i0 + 1 < n ? a[i0 + 1] : 0;
+        keep |= (u32)(i0 < n && pred_eval(p, x[2 * j])) << (2 * j);
+        keep |= (u32)(i0 + 1 < n && pred_eval(p, x[2 * j + 1])) << (2 * j + 1);
+      }
+    }
+    u64 cnt = warp_reduce<O>((u64)__popc(keep));
+    if (lane == 0) s_warp[warp] = cnt;
+    __syncthreads();
+    if (warp == 0) {
+      u64 wv = lane < FILTER_THREADS / 32 ? s_warp[lane] : 0;
+      u64 winc = warp_incl_scan<O>(wv);
+      u64 wexc = winc - wv;
+      const u64 agg = __shfl_sync(0xffffffffu, winc, FILTER_THREADS / 32 - 1);
+      int ok = 1;
+      if (lane == 0) {
+        ok = publish_begin(c, tile);
+        if (ok) {
+          if (tile == 0) publish_incl(c, tile, agg);
+          else publish_agg(c, tile, agg);
+        }
+      }
+      ok = __shfl_sync(0xffffffffu, ok, 0);
+      u64 prefix = 0;
+      if (ok && tile > 0) {
+        ok = lookback<O>(c, tile, prefix);
+        if (ok && lane == 0) publish_incl(c, tile, prefix + agg);
+      }
+      if (lane < FILTER_THREADS / 32) s_warp[lane] = prefix + wexc;
+      if (lane == 0) {
+        s_abort = !ok;
+        if (ok && tile == num_tiles - 1 && m_out) *m_out = prefix + agg;
+      }
+    }
+    __syncthreads();
+    if (s_abort) return;
+    u64 run = s_warp[warp];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const bool f0 = (keep >> (2 * j)) & 1u, f1 = (keep >> (2 * j + 1)) & 1u;
+      const u32 m0 = __ballot_sync(0xffffffffu, f0);
+      const u32 m1 = __ballot_sync(0xffffffffu, f1);
+      const u64 r0 = run + __popc(m0 & lt) + __popc(m1 & lt);
+      if (f0) a[r0] = x[2 * j];
+      if (f1) a[r0 + f0] = x[2 * j + 1];
+      run += __popc(m0) + __popc(m1);
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(512)
+count_kernel(const u64* __restrict__ a, u64 n, DevPred p, u64* partials, u32* counter, u64* total) {
+  __shared__ u64 s_warp[16];
+  __shared__ bool s_last;
+  u64 t = 0;
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  const bool vec = ((uintptr_t)a & 15) == 0;
+  if (vec) {
+    const u64 npairs = n / 2;
+    for (u64 q = (u64)blockIdx.x * blockDim.x + threadIdx.x; q < npairs; q += stride) {
+      ulonglong2 v = ldg_stream2(a + 2 * q);
+      t += (u64)pred_eval(p, v.x) + (u64)pred_eval(p, v.y);
+    }
+    if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) t += pred_eval(p, a[n - 1]);
+  } else {
+    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+      t += pred_eval(p, a[i]);
+  }
+  t = warp_reduce<Op<PIP_OP_ADD>>(t);
+  if (lane_id() == 0) s_warp[warp_id()] = t;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    u64 b = 0;
+    for (int w = 0; w < (int)(blockDim.x / 32); ++w) b += s_warp[w];
+    partials[blockIdx.x] = b;
+    __threadfence();
+    s_last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (s_last && threadIdx.x < 32) {
+    __threadfence();
+    u64 v = 0;
+    for (u32 i = threadIdx.x; i < gridDim.x; i += 32) v += ld_relaxed_u64(partials + i);
+    v = warp_reduce<Op<PIP_OP_ADD>>(v);
+    if (threadIdx.x == 0) {
+      *total = v;
+      *counter = 0;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host
+
+struct ScratchLayoutF {
+  u32* abort;
+  u32* counter;
+  u64* partials;
+  TileSlot* slots;
+};
+size_t scratch_bytes_for(int sms);
+static ScratchLayoutF carve_f(void* scratch, int sms) {
+  const size_t gmax = (size_t)sms * 8;
+  char* p = (char*)scratch;
+  ScratchLayoutF L;
+  L.abort = (u32*)p;
+  L.counter = (u32*)p + 1;
+  L.partials = (u64*)(p + 256);
+  L.slots = (TileSlot*)(p + 256 + gmax * sizeof(u64));
+  return L;
+}
+
+template <bool VEC>
+static int launch_filter(u64* a, u64 n, const DevPred& p, u64* m_dev, const ScratchLayoutF& L,
+                         cudaStream_t st, int dev) {
+  const u64 tiles = (n + FILTER_TILE - 1) / FILTER_TILE;
+  auto k = filter_kernel<VEC>;
+  int per_sm = 0;
+  PIP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, FILTER_THREADS, 0));
+  if (per_sm < 1) return PIP_ERR_UNSUPPORTED;
+  if (per_sm > 8) per_sm = 8;
+  u64 g = (u64)per_sm * num_sms(dev);
+  if (g > tiles) g = tiles;
+  int grid = (int)g;
+  PIP_CUDA(cudaMemsetAsync(L.abort, 0, 256, st));
+  PIP_CUDA(cudaMemsetAsync(L.slots, 0, sizeof(TileSlot) * 2 * (size_t)grid, st));
+  LookbackCtx c{L.slots, L.abort, (u32)grid};
+  DevPred pp = p;
+  void* args[] = {&a, &n, &pp, &m_dev, &c, (void*)&tiles};
+  PIP_CUDA(cudaLaunchCooperativeKernel((const void*)k, dim3(grid), dim3(FILTER_THREADS), args, 0, st));
+  return PIP_OK;
+}
+
+int filter_device(u64* a, u64 n, const pip_pred* pred, u64* m_dev, void* scratch,
+                  size_t scratch_bytes, cudaStream_t st) {
+  const int dev = current_device();
+  const int sms = num_sms(dev);
+  if (!pred || pred->kind > PIP_PRED_EQ) return PIP_ERR_INVALID_ARG;
+  if (pred->kind == PIP_PRED_MOD_EQ && pred->a == 0) return PIP_ERR_INVALID_ARG;
+  if (!scratch || scratch_bytes < scratch_bytes_for(sms)) return PIP_ERR_OOM;
+  if (n == 0) {
+    if (m_dev) PIP_CUDA(cudaMemsetAsync(m_dev, 0, 8, st));
+    return PIP_OK;
+  }
+  DevPred p = make_dev_pred(*pred);
+  ScratchLayoutF L = carve_f(scratch, sms);
+  const bool vec = ((uintptr_t)a & 15) == 0;
+  return vec ? launch_filter<true>(a, n, p, m_dev, L, st, dev)
+             : launch_filter<false>(a, n, p, m_dev, L, st, dev);
+}
+
+int count_device(const u64* a, u64 n, const pip_pred* pred, u64* m_dev, void* scratch,
+                 size_t scratch_bytes, cudaStream_t st) {
+  const int dev = current_device();
+  const int sms = num_sms(dev);
+  if (!pred || pred->kind > PIP_PRED_EQ || !m_dev) return PIP_ERR_INVALID_ARG;
+  if (pred->kind == PIP_PRED_MOD_EQ && pred->a == 0) return PIP_ERR_INVALID_ARG;
+  if (!scratch || scratch_bytes < scratch_bytes_for(sms)) return PIP_ERR_OOM;
+  DevPred p = make_dev_pred(*pred);
+  ScratchLayoutF L = carve_f(scratch, sms);
+  int grid = sms * 2;
+  u64 need = (n + 1023) / 1024;
+  if ((u64)grid > need) grid = (int)(need ? need : 1);
+  PIP_CUDA(cudaMemsetAsync(L.abort, 0, 256, st));
+  count_kernel<<<grid, 512, 0, st>>>(a, n, p, L.partials, L.counter, m_dev);
+  PIP_CHECK_LAUNCH();
+  return PIP_OK;
+}
+
+// u64 division by an invariant divisor (Granlund-Montgomery / libdivide
+// "round-up" method): q = mulhi(x, m) [>> s], with a 65-bit "add" variant.
+DevPred make_dev_pred(const pip_pred& in) {
+  DevPred p{};
+  p.kind = in.kind;
+  p.negate = in.negate;
+  p.a = in.a;
+  p.b = in.b;
+  if (in.kind == PIP_PRED_MOD_EQ && in.a >= 1) {
+    const u64 d = in.a;
+    if ((d & (d - 1)) == 0) {
+      p.pow2 = 1;
+    } else {
+      int l = 63 - __builtin_clzll(d);  // floor(log2 d); d not a power of 2
+      unsigned __int128 one = 1;
+      // m = floor(2^(64+l) / d) + 1 ; check if it fits 64 bits with error bound
+      unsigned __int128 num = one << (64 + l);
+      u64 proposed = (u64)(num / d);
+      u64 rem = (u64)(num - (unsigned __int128)proposed * d);
+      u64 e = d - rem;
+      if (e < (1ull << l)) {
+        p.magic = proposed + 1;
+        p.shift = l;
+        p.add = 0;
+      } else {
+        // 65-bit multiplier: m = 2*proposed + 1 (mod 2^64), add-indicator form
+        proposed += proposed;
+        u64 twice_rem = rem + rem;
+        if (twice_rem >= d || twice_rem < rem) proposed += 1;
+        p.magic = proposed + 1;
+        p.shift = l;
+        p.add = 1;
+      }
+    }
+  }
+  return p;
+}
+
+}  // namespace pip

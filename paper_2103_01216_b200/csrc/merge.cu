@@ -1,0 +1,490 @@
+// In-place merge of two sorted runs (strong.merge_strong,
+// relaxed.merge_relaxed).
+//
+// Reference: pkg/src/pipal/strong.py:462-522 (co-rank by dual binary search
+// `_split_point` :474-488, rotate the middle by triple reversal, recurse:
+// O(n log n) moves) and pkg/src/pipal/relaxed.py:377-612 (k = b(n) chunks:
+// descriptor sort of chunks by their last element :509-527, whole-chunk
+// cycle permutation through a k-word buffer :531-546, three-chunk streaming
+// merge :413-506, tails parked and merged back :566-612).
+//
+// B200 design — two streaming passes over HBM, both fully parallel:
+//   P0  (descriptors, O(n/C) work) chunks of C = 8192 words; A' = the A
+//       words after its head A[0:hA) (hA = |A| mod C), B' = the B words
+//       before its tail (hB = |B| mod C), so A' and B' are whole chunks of
+//       one contiguous slot region [hA, n - hB); the head and the tail stay
+//       where they are.  Every chunk gets its destination slot in the order
+//       of chunk LAST elements (the reference's descriptor sort, ties A
+//       before B), and the merge-path co-ranks of every output block
+//       [mC, (m+1)C) over the original runs A, B are computed BEFORE
+//       anything moves.
+//   P1  (chunk permutation, ~16 B/word) the slot permutation is applied in
+//       place by walking its cycles backwards from "cut" slots whose chunks
+//       were first saved to a cut buffer (cuts every D slots — D set by the
+//       workspace budget); every walk is independent, so all CTAs walk in
+//       parallel; cycles that contain no cut (rare) are found by pointer
+//       jumping (min-label) and rotated by one CTA each through shared
+//       memory.
+//   P2  (block merge, ~16 B/word) after the permutation a chunk in slot q
+//       only holds words of output rank < (q+2)C + hA + hB (chunks sorted by
+//       last element), so output block m can be written as soon as every
+//       block <= m + L (L = 3 + ceil((hA+hB)/C)) has loaded its inputs.
+//       Blocks are assigned round-robin to persistent CTAs, loaded (<= 6
+//       contiguous pieces) into shared memory, merged by merge path and
+//       written back under that dataflow rule — no grid barrier per block.
+//       Block 0 (the only writer of the in-place head) is kept in shared
+//       memory and written after a final barrier; the blocks over the tail
+//       are the last ones and wait for every load anyway.
+// Output equals np.sort(a) (values are plain words, so the tie order is
+// invisible; it is fixed here as A before B for the co-ranks).
+#include "sync.cuh"
+
+namespace pip {
+
+static constexpr int MG_THREADS = 512;
+static constexpr u32 MG_LOGC = 13;
+static constexpr u64 MG_C = 1ull << MG_LOGC;  // words per chunk / output block
+static constexpr int MG_PER_THREAD = (int)(MG_C / MG_THREADS);
+
+struct MergeGlobal {
+  GridSync sync;
+  u32 walk_next;  // dynamic walk assignment
+  u32 uncut;      // #slots on cut-free cycles
+};
+
+struct MergeArgs {
+  u64* a;
+  u64 n, na, nb;
+  u64 hA, hB, KA, KB, K, NB, D, ncuts, L;
+  u64* cut;       // [ncuts * C] saved chunks of the cut slots
+  u32* dest;      // [K] destination slot of the chunk in slot s
+  u32* inv;       // [K] slot whose chunk moves into slot s
+  u32* lab[2];    // [K] pointer-jumping labels   (only if uncut cycles)
+  u32* jmp[2];    // [K] pointer-jumping jumps
+  unsigned char* visited;  // [K]
+  u64* cr;        // [NB + 1] A co-rank of every output block boundary
+  u32* status;    // [G] per CTA: (last block loaded) + 1
+  MergeGlobal* g;
+};
+
+__device__ __forceinline__ void mpart(u64 total, u32 G, u32 b, u64& s, u64& e) {
+  s = total * b / G;
+  e = total * (b + 1) / G;
+}
+
+// physical word of A[x] / B[y] once the chunks sit in their destination
+// slots (the head A[0:hA) and the tail B[nb-hB:nb) never move)
+__device__ __forceinline__ u64 phys_a(const MergeArgs& M, u64 x) {
+  if (x < M.hA) return x;
+  const u64 xp = x - M.hA;
+  return M.hA + ((u64)__ldcg(M.dest + (xp >> MG_LOGC)) << MG_LOGC) + (xp & (MG_C - 1));
+}
+__device__ __forceinline__ u64 phys_b(const MergeArgs& M, u64 y) {
+  if (y >= M.nb - M.hB) return M.na + y;
+  return M.hA + ((u64)__ldcg(M.dest + M.KA + (y >> MG_LOGC)) << MG_LOGC) + (y & (MG_C - 1));
+}
+
+// merge path over the original runs A = a[0:na), B = a[na:n) (A first on ties)
+__device__ __forceinline__ u64 corank2_global(const MergeArgs& M, u64 q) {
+  const u64* A = M.a;
+  const u64* B = M.a + M.na;
+  u64 lo = q > M.nb ? q - M.nb : 0, hi = q < M.na ? q : M.na;
+  while (lo < hi) {
+    const u64 mid = (lo + hi) >> 1;
+    if (__ldcg(A + mid) <= __ldcg(B + (q - mid - 1))) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+__device__ __forceinline__ u32 corank2_smem(const u64* x, u32 nx, const u64* y, u32 ny, u32 q) {
+  u32 lo = q > ny ? q - ny : 0, hi = q < nx ? q : nx;
+  while (lo < hi) {
+    const u32 mid = (lo + hi) >> 1;
+    if (x[mid] <= y[q - mid - 1]) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+// merge sA[0:na) and sB[0:nb) into out[0:na+nb); MG_PER_THREAD outputs each
+__device__ __forceinline__ void block_merge(const u64* sA, u32 na, const u64* sB, u32 nb, u64* out) {
+  const u32 total = na + nb;
+  const u32 r0 = threadIdx.x * MG_PER_THREAD;
+  if (r0 >= total) return;
+  const u32 r1 = r0 + MG_PER_THREAD < total ? r0 + MG_PER_THREAD : total;
+  u32 i = corank2_smem(sA, na, sB, nb, r0);
+  u32 j = r0 - i;
+  for (u32 r = r0; r < r1; ++r) {
+    if (i < na && (j >= nb || sA[i] <= sB[j])) out[r] = sA[i++];
+    else out[r] = sB[j++];
+  }
+}
+
+__device__ __forceinline__ bool is_cut(const MergeArgs& M, u64 s) {
+  return M.ncuts && (s % M.D) == 0 && __ldcg(M.inv + s) != (u32)s;
+}
+
+// copy one chunk, whole CTA (8-byte accesses: slots start at hA, which need
+// not be 16-byte aligned); every thread reads before anyone writes
+__device__ __forceinline__ void move_chunk(u64* dst, const u64* src) {
+  const u32 tid = threadIdx.x;
+  u64 v[MG_PER_THREAD];
+#pragma unroll
+  for (int k = 0; k < MG_PER_THREAD; ++k) v[k] = __ldcg(src + tid + k * MG_THREADS);
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < MG_PER_THREAD; ++k) dst[tid + k * MG_THREADS] = v[k];
+}
+
+__device__ __forceinline__ u64* slot_ptr(const MergeArgs& M, u64 s) {
+  return M.a + M.hA + (s << MG_LOGC);
+}
+
+__global__ void __launch_bounds__(MG_THREADS, 1) merge_kernel(MergeArgs M) {
+  extern __shared__ __align__(16) u64 smem[];
+  u64* s_in = smem;               // [C]  A-piece | B-piece
+  u64* s_out = smem + MG_C;       // [C]
+  u64* s_def = smem + 2 * MG_C;   // [C]  block 0, written last
+  __shared__ u64 s_misc[2];
+  __shared__ int s_flag;
+  const u32 b = blockIdx.x, G = gridDim.x, tid = threadIdx.x;
+  MergeGlobal* g = M.g;
+  u32 gen = 0;
+  u64* a = M.a;
+
+  // ---------------- P0: slot destinations (sort by chunk last) + co-ranks
+  {
+    u64 s, e;
+    mpart(M.K, G, b, s, e);
+    for (u64 x = s + tid; x < e; x += MG_THREADS) {
+      u64 d;
+      if (x < M.KA) {
+        const u64 last = __ldcg(a + M.hA + ((x + 1) << MG_LOGC) - 1);
+        u64 lo = 0, hi = M.KB;  // #B' chunks with last < this last
+        while (lo < hi) {
+          const u64 mid = (lo + hi) >> 1;
+          if (__ldcg(a + M.na + ((mid + 1) << MG_LOGC) - 1) < last) lo = mid + 1; else hi = mid;
+        }
+        d = x + lo;
+      } else {
+        const u64 y = x - M.KA;
+        const u64 last = __ldcg(a + M.na + ((y + 1) << MG_LOGC) - 1);
+        u64 lo = 0, hi = M.KA;  // #A' chunks with last <= this last
+        while (lo < hi) {
+          const u64 mid = (lo + hi) >> 1;
+          if (__ldcg(a + M.hA + ((mid + 1) << MG_LOGC) - 1) <= last) lo = mid + 1; else hi = mid;
+        }
+        d = y + lo;
+      }
+      M.dest[x] = (u32)d;
+      M.inv[d] = (u32)x;
+      M.visited[x] = 0;
+    }
+    mpart(M.NB + 1, G, b, s, e);
+    for (u64 m = s + tid; m < e; m += MG_THREADS) {
+      const u64 p = m * MG_C < M.n ? m * MG_C : M.n;
+      M.cr[m] = corank2_global(M, p);
+    }
+  }
+  if (!grid_barrier(&g->sync, gen)) return;
+
+  // ---------------- P0b: save the chunks of the cut slots
+  for (u64 c = b; c < M.ncuts; c += G) {
+    const u64 slot = c * M.D;
+    if (__ldcg(M.inv + slot) != (u32)slot) move_chunk(M.cut + c * MG_C, slot_ptr(M, slot));
+    __syncthreads();
+  }
+  if (!grid_barrier(&g->sync, gen)) return;
+
+  // ---------------- P1: chunk permutation: walk each cycle backwards from a cut
+  for (;;) {
+    if (tid == 0) s_misc[0] = atomicAdd(&g->walk_next, 1u);
+    __syncthreads();
+    const u64 c = s_misc[0];
+    __syncthreads();
+    if (c >= M.ncuts) break;
+    const u64 p0 = c * M.D;
+    if (__ldcg(M.inv + p0) == (u32)p0) continue;
+    u64 sdst = p0;
+    for (u64 steps = 0; steps <= M.K; ++steps) {
+      const u64 src = __ldcg(M.inv + sdst);
+      const bool last = is_cut(M, src);
+      move_chunk(slot_ptr(M, sdst), last ? M.cut + (src / M.D) * MG_C : slot_ptr(M, src));
+      if (tid == 0) M.visited[sdst] = 1;
+      if (last) break;
+      sdst = src;
+    }
+    __syncthreads();
+  }
+  if (!grid_barrier(&g->sync, gen)) return;
+
+  // ---------------- P1b: cycles without a cut (rare; all of them if no cut buffer)
+  {
+    u64 s, e;
+    mpart(M.K, G, b, s, e);
+    u32 cnt = 0;
+    for (u64 x = s + tid; x < e; x += MG_THREADS)
+      cnt += !__ldcg(M.visited + x) && __ldcg(M.inv + x) != (u32)x;
+    cnt = __reduce_add_sync(0xffffffffu, cnt);
+    if ((tid & 31) == 0 && cnt) atomicAdd(&g->uncut, cnt);
+  }
+  if (!grid_barrier(&g->sync, gen)) return;
+  if (ld_relaxed_u32(&g->uncut)) {
+    u64 s, e;
+    mpart(M.K, G, b, s, e);
+    for (u64 x = s + tid; x < e; x += MG_THREADS) {
+      M.lab[0][x] = (u32)x;
+      M.jmp[0][x] = __ldcg(M.inv + x);
+    }
+    if (!grid_barrier(&g->sync, gen)) return;
+    // min-label by pointer jumping: after r rounds lab = min over 2^r steps
+    u32 cur = 0;
+    for (u64 span = 1; span < M.K; span <<= 1) {
+      for (u64 x = s + tid; x < e; x += MG_THREADS) {
+        const u32 j = __ldcg(M.jmp[cur] + x);
+        const u32 l1 = __ldcg(M.lab[cur] + x), l2 = __ldcg(M.lab[cur] + j);
+        M.lab[cur ^ 1][x] = l1 < l2 ? l1 : l2;
+        M.jmp[cur ^ 1][x] = __ldcg(M.jmp[cur] + j);
+      }
+      cur ^= 1;
+      if (!grid_barrier(&g->sync, gen)) return;
+    }
+    // each leader (cycle minimum) rotates its cycle through shared memory
+    for (u64 x0 = b; x0 < M.K; x0 += G) {
+      const bool lead = !__ldcg(M.visited + x0) && __ldcg(M.inv + x0) != (u32)x0 &&
+                        __ldcg(M.lab[cur] + x0) == (u32)x0;
+      if (!lead) continue;
+      for (u32 k = tid; k < MG_C; k += MG_THREADS) s_out[k] = __ldcg(slot_ptr(M, x0) + k);
+      __syncthreads();
+      u64 sdst = x0;
+      for (u64 steps = 0; steps <= M.K; ++steps) {
+        const u64 src = __ldcg(M.inv + sdst);
+        if (src == x0) {
+          for (u32 k = tid; k < MG_C; k += MG_THREADS) slot_ptr(M, sdst)[k] = s_out[k];
+          break;
+        }
+        move_chunk(slot_ptr(M, sdst), slot_ptr(M, src));
+        sdst = src;
+      }
+      __syncthreads();
+    }
+    if (!grid_barrier(&g->sync, gen)) return;
+  }
+
+  // ---------------- P2: block merge under the dataflow rule
+  for (u64 m = b; m < M.NB; m += G) {
+    const u64 p0 = m * MG_C, p1 = (m + 1) * MG_C < M.n ? (m + 1) * MG_C : M.n;
+    const u64 i0 = __ldcg(M.cr + m), i1 = __ldcg(M.cr + m + 1);
+    const u64 j0 = p0 - i0, j1 = p1 - i1;
+    const u32 na = (u32)(i1 - i0), nb = (u32)(j1 - j0);
+    for (u32 k = tid; k < na; k += MG_THREADS) s_in[k] = __ldcg(a + phys_a(M, i0 + k));
+    for (u32 k = tid; k < nb; k += MG_THREADS) s_in[na + k] = __ldcg(a + phys_b(M, j0 + k));
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      st_release_u32(M.status + b, (u32)(m + 1));
+    }
+    u64* out = m == 0 ? s_def : s_out;
+    block_merge(s_in, na, s_in + na, nb, out);
+    if (m != 0) {
+      // every block <= m + L (all blocks, for the tail) must have loaded
+      const u64 upto = m + M.L < M.NB - 1 ? m + M.L : M.NB - 1;
+      if (tid < 32) {
+        u64 spins = 0;
+        int ok = 1;
+        for (;;) {
+          bool ready = true;
+          for (u32 c = tid; c < G; c += 32) {
+            if (c > upto) continue;
+            const u64 mc = c + ((upto - c) / G) * G;
+            if (ld_acquire_u32(M.status + c) < mc + 1) ready = false;
+          }
+          if (__all_sync(0xffffffffu, ready)) break;
+          if (tid == 0) {
+            if (++spins > 32) __nanosleep(64);
+            if ((spins & 1023) == 0) {
+              if (ld_relaxed_u32(&g->sync.abort)) ok = 0;
+              else if (spins > (1ull << 25)) { atomicExch(&g->sync.abort, 1u); ok = 0; }
+            }
+          }
+          if (!__shfl_sync(0xffffffffu, ok, 0)) break;
+        }
+        if (tid == 0) s_flag = ok;
+      }
+      __syncthreads();
+      if (!s_flag) return;
+      for (u32 k = tid; k < (u32)(p1 - p0); k += MG_THREADS) a[p0 + k] = s_out[k];
+    }
+    __syncthreads();
+  }
+  // block 0 owns the in-place head: write it once every block has loaded
+  if (!grid_barrier(&g->sync, gen)) return;
+  if (b == 0) {
+    const u64 p1 = MG_C < M.n ? MG_C : M.n;
+    for (u32 k = tid; k < (u32)p1; k += MG_THREADS) a[k] = s_def[k];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// single-CTA merge of a small array (n <= C)
+__global__ void __launch_bounds__(MG_THREADS, 1) merge_small_kernel(u64* a, u32 n, u32 na) {
+  extern __shared__ __align__(16) u64 smem[];
+  u64* s_in = smem;
+  u64* s_out = smem + MG_C;
+  for (u32 k = threadIdx.x; k < n; k += MG_THREADS) s_in[k] = a[k];
+  __syncthreads();
+  block_merge(s_in, na, s_in + na, n - na, s_out);
+  __syncthreads();
+  for (u32 k = threadIdx.x; k < n; k += MG_THREADS) a[k] = s_out[k];
+}
+
+// sortedness of both runs (debug=True): counts descents inside each run
+__global__ void check_sorted_kernel(const u64* a, u64 n, u64 na, u32* bad) {
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  u32 c = 0;
+  for (u64 k = (u64)blockIdx.x * blockDim.x + threadIdx.x; k + 1 < n; k += stride) {
+    if (k + 1 == na) continue;  // run boundary
+    c += a[k + 1] < a[k];
+  }
+  c = __reduce_add_sync(0xffffffffu, c);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(bad, c);
+}
+
+// ---------------------------------------------------------------------------
+// host
+
+struct MergeLayout {
+  size_t dest, inv, lab0, lab1, jmp0, jmp1, visited, cr, status, g, cut, total;
+  u64 D, ncuts, desc_bytes;
+};
+
+// budget_words == 0: strong schedule, cut buffer of one chunk per SM
+static MergeLayout merge_layout(u64 n, u64 na, u64 budget_words, int grid) {
+  const u64 nb = n - na;
+  const u64 hA = na % MG_C, hB = nb % MG_C;
+  const u64 K = (n - hA - hB) / MG_C;
+  const u64 NB = (n + MG_C - 1) / MG_C;
+  MergeLayout L{};
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off += (bytes + 15) & ~(size_t)15;
+    return o;
+  };
+  L.dest = take(K * 4);
+  L.inv = take(K * 4);
+  L.lab0 = take(K * 4);
+  L.lab1 = take(K * 4);
+  L.jmp0 = take(K * 4);
+  L.jmp1 = take(K * 4);
+  L.visited = take(K);
+  L.cr = take((NB + 1) * 8);
+  L.status = take((size_t)grid * 4);
+  L.g = take(sizeof(MergeGlobal));
+  L.desc_bytes = off;
+  const u64 desc_words = (off + 7) / 8;
+  u64 cut_chunks;
+  if (budget_words == 0) cut_chunks = (u64)grid;
+  else cut_chunks = budget_words > desc_words ? (budget_words - desc_words) / MG_C : 0;
+  if (cut_chunks > K) cut_chunks = K;
+  if (cut_chunks) {
+    L.D = (K + cut_chunks - 1) / cut_chunks;
+    L.ncuts = (K + L.D - 1) / L.D;
+  } else {
+    L.D = 1;
+    L.ncuts = 0;
+  }
+  L.cut = take(L.ncuts * MG_C * 8);
+  L.total = off;
+  return L;
+}
+
+static int merge_grid() { return num_sms(current_device()); }
+
+size_t merge_workspace_bytes(u64 n, u64 split, u64 budget_words) {
+  if (split > n || n <= MG_C || split == 0 || split == n) return 0;
+  return merge_layout(n, split, budget_words, merge_grid()).total;
+}
+
+int merge_device(u64* a, u64 n, u64 split, int check_sorted, void* ws, size_t ws_bytes,
+                 void* scratch, size_t scratch_bytes, cudaStream_t st) {
+  if (split > n) return PIP_ERR_INVALID_ARG;
+  if (check_sorted && n > 1) {
+    if (!scratch || scratch_bytes < 16) return PIP_ERR_OOM;
+    u32* bad = (u32*)scratch;
+    PIP_CUDA(cudaMemsetAsync(bad, 0, 4, st));
+    u64 blocks = (n + 255) / 256;
+    const u64 cap = (u64)num_sms(current_device()) * 8;
+    if (blocks > cap) blocks = cap;
+    check_sorted_kernel<<<(unsigned)blocks, 256, 0, st>>>(a, n, split, bad);
+    PIP_CHECK_LAUNCH();
+    u32 h = 0;
+    PIP_CUDA(cudaMemcpyAsync(&h, bad, 4, cudaMemcpyDeviceToHost, st));
+    PIP_CUDA(cudaStreamSynchronize(st));
+    if (h) return PIP_ERR_UNSORTED;
+  }
+  if (n < 2 || split == 0 || split == n) return PIP_OK;
+  if (n <= MG_C) {
+    const size_t smem = 2 * MG_C * sizeof(u64);
+    PIP_CUDA(cudaFuncSetAttribute(merge_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem));
+    merge_small_kernel<<<1, MG_THREADS, smem, st>>>(a, (u32)n, (u32)split);
+    PIP_CHECK_LAUNCH();
+    return PIP_OK;
+  }
+  const int grid = merge_grid();
+  // the workspace the caller sized with pip_merge_workspace_bytes(n, split, b)
+  // determines the cut buffer; recover b's layout from its size
+  MergeLayout L = merge_layout(n, split, 0, grid);
+  {
+    const MergeLayout Lb = merge_layout(n, split, (u64)(ws_bytes / 8), grid);
+    if (Lb.total <= ws_bytes) L = Lb;
+    else {
+      const MergeLayout L0 = merge_layout(n, split, 1, grid);  // descriptors only
+      if (L0.total <= ws_bytes && L.total > ws_bytes) L = L0;
+    }
+  }
+  if (!ws || ws_bytes < L.total) return PIP_ERR_OOM;
+  if (((n + MG_C - 1) / MG_C) > 0xffffffffull) return PIP_ERR_UNSUPPORTED;
+  char* w = (char*)ws;
+  MergeArgs M{};
+  M.a = a;
+  M.n = n;
+  M.na = split;
+  M.nb = n - split;
+  M.hA = split % MG_C;
+  M.hB = M.nb % MG_C;
+  M.KA = (split - M.hA) / MG_C;
+  M.KB = (M.nb - M.hB) / MG_C;
+  M.K = M.KA + M.KB;
+  M.NB = (n + MG_C - 1) / MG_C;
+  M.D = L.D;
+  M.ncuts = L.ncuts;
+  M.L = 3 + (M.hA + M.hB + MG_C - 1) / MG_C;
+  M.cut = (u64*)(w + L.cut);
+  M.dest = (u32*)(w + L.dest);
+  M.inv = (u32*)(w + L.inv);
+  M.lab[0] = (u32*)(w + L.lab0);
+  M.lab[1] = (u32*)(w + L.lab1);
+  M.jmp[0] = (u32*)(w + L.jmp0);
+  M.jmp[1] = (u32*)(w + L.jmp1);
+  M.visited = (unsigned char*)(w + L.visited);
+  M.cr = (u64*)(w + L.cr);
+  M.status = (u32*)(w + L.status);
+  M.g = (MergeGlobal*)(w + L.g);
+  if ((u64)grid <= 2 * M.L) return PIP_ERR_UNSUPPORTED;
+  PIP_CUDA(cudaMemsetAsync(M.status, 0, (size_t)grid * 4, st));
+  PIP_CUDA(cudaMemsetAsync(M.g, 0, sizeof(MergeGlobal), st));
+  const size_t smem = 3 * MG_C * sizeof(u64);
+  PIP_CUDA(cudaFuncSetAttribute(merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  void* args[] = {&M};
+  PIP_CUDA(cudaLaunchCooperativeKernel((const void*)merge_kernel, dim3(grid), dim3(MG_THREADS), args,
+                                       smem, st));
+  MergeGlobal gh{};
+  PIP_CUDA(cudaMemcpyAsync(&gh, M.g, sizeof(gh), cudaMemcpyDeviceToHost, st));
+  PIP_CUDA(cudaStreamSynchronize(st));
+  if (gh.sync.abort) return PIP_ERR_CUDA;
+  return PIP_OK;
+}
+
+}  // namespace pip

@@ -1,0 +1,629 @@
+// In-place random permutation by deterministic reservations
+// (relaxed.random_permutation on detres.run_rounds).
+//
+// Reference: pkg/src/pipal/relaxed.py:64-251 (_RpClient: next_ids :107-120,
+// reserve :130-159, commit :161-197, clean :199-217) and
+// pkg/src/pipal/detres.py:40-211 (ReservationTable), :256-307 (run_rounds).
+//
+// Semantics kept bit-for-bit (so rounds, committed-per-round, trace and
+// peak_table_load equal the reference's):
+//   * iterates are ids i with H[i] != i taken in DESCENDING order from a
+//     window [cursor - W + 1, cursor] (W = span_cap = b + b/4 + 8 for
+//     `final`, max(count, 1024) otherwise), at most `count = b - #failures`
+//     per round; an empty window advances the cursor (next_ids);
+//   * failures of a round are packed first, in order (compact_by_mask);
+//   * reserve: R[H[i]] = max(R[H[i]], i) (naive/flat also R[i] = max(., i));
+//     `final` serves targets inside this round's fresh id range [dlo, dhi]
+//     from a dense array (slot = 1 + writer id), all others from an
+//     open-addressed, linear-probed write-max table keyed by
+//     (k * GOLDEN) >> (64 - log2 cap), cap = pow2 >= 2b (4b naive/flat);
+//   * commit: i commits iff nobody active targets i (own slot empty or i)
+//     and i holds its target's reservation; then swap a[i], a[H[i]];
+//   * livelock after 64 zero-commit rounds.
+//
+// B200 design: ONE cooperative persistent kernel runs every round; the four
+// phases of a round (pack+clean+window-count | refill | reserve | commit)
+// are separated by a grid barrier, so a round costs four barriers instead
+// of host round-trips.  Reservations are single 64-bit words
+// (key << 32 | id): claim = atomicCAS on the empty word, update =
+// atomicMax on the same word (same key => max on the id).  The slot each
+// target landed in is remembered, so the commit check and the targeted
+// clean are single accesses with no re-probing.  All per-iterate state is
+// 32-bit (n < 2^32 - 1) to halve the workspace traffic.
+#include <vector>
+#include "sync.cuh"
+
+namespace pip {
+
+static constexpr int RP_THREADS = 256;
+static constexpr u64 RP_EMPTY = ~0ull;
+static constexpr u32 RP_NOSLOT = 0xffffffffu;
+static constexpr u64 RP_ROUND_CHUNK = 512;  // committed counts per launch
+
+struct RpGlobal {
+  GridSync sync;  // barrier + abort + kernel error (PIP_ERR_*)
+  u64 dlo, dhi;
+};
+
+struct RpResume {
+  u64 fill, rounds, zero_rounds, total_committed, peak, trace_pos, nfail_prev;
+  long long cursor;
+  u64 dlo, dhi;
+  u32 ping, done, first, pad;
+};
+
+struct RpArgs {
+  u64* a;
+  const u64* h;
+  u64 n, prefix, span_cap, rounds_limit;
+  u32 logcap, debug, targeted_clean_ok, pad;
+  u32* ids[2];
+  u32* tg[2];
+  u32* slot;
+  unsigned char* cflag;
+  u32* dense;
+  u64* table;
+  u32* failcnt;
+  u32* wcnt;
+  u32* claimcnt;
+  u64* round_counts;  // RP_ROUND_CHUNK
+  u64* trace;
+  RpGlobal* g;
+  RpResume* resume;
+};
+
+__device__ __forceinline__ void part(u64 total, u32 G, u32 b, u64& s, u64& e) {
+  s = total * b / G;
+  e = total * (b + 1) / G;
+}
+
+// block-wide stable exclusive rank of `f`; *tot = number of set flags
+__device__ __forceinline__ u32 block_rank(bool f, u32* s_cnt, u32* tot) {
+  const u32 lane = lane_id(), warp = warp_id();
+  const u32 m = __ballot_sync(0xffffffffu, f);
+  const u32 wr = __popc(m & ((1u << lane) - 1u));
+  if (lane == 0) s_cnt[warp] = __popc(m);
+  __syncthreads();
+  if (warp == 0) {
+    const u32 nw = blockDim.x / 32;
+    u32 v = lane < nw ? s_cnt[lane] : 0;
+    u32 inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      u32 t = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= (u32)o) inc += t;
+    }
+    if (lane < nw) s_cnt[lane] = inc - v;
+    if (lane == 31) s_cnt[32] = inc;
+  }
+  __syncthreads();
+  const u32 r = s_cnt[warp] + wr;
+  *tot = s_cnt[32];
+  __syncthreads();
+  return r;
+}
+
+__device__ __forceinline__ u64 block_sum(u64 v, u64* s_red) {
+  v = warp_reduce<Op<PIP_OP_ADD>>(v);
+  if (lane_id() == 0) s_red[warp_id()] = v;
+  __syncthreads();
+  u64 t = 0;
+  if (threadIdx.x == 0) {
+    for (u32 w = 0; w < blockDim.x / 32; ++w) t += s_red[w];
+    s_red[32] = t;
+  }
+  __syncthreads();
+  t = s_red[32];
+  __syncthreads();
+  return t;
+}
+
+// sum of cnt[0..G) and exclusive prefix up to b (all threads get both)
+__device__ __forceinline__ void sum_counts(const u32* cnt, u32 G, u32 b, u64* s_red, u64& total,
+                                           u64& before) {
+  if (threadIdx.x < 32) {
+    u64 t = 0, bf = 0;
+    for (u32 i = threadIdx.x; i < G; i += 32) {
+      const u64 v = __ldcg(cnt + i);
+      t += v;
+      if (i < b) bf += v;
+    }
+    t = warp_reduce<Op<PIP_OP_ADD>>(t);
+    bf = warp_reduce<Op<PIP_OP_ADD>>(bf);
+    if (threadIdx.x == 0) {
+      s_red[33] = t;
+      s_red[34] = bf;
+    }
+  }
+  __syncthreads();
+  total = s_red[33];
+  before = s_red[34];
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
+// write-max reservation table: one 64-bit word per slot, key<<32 | value
+__device__ __forceinline__ u64 rp_home(u32 key, u32 logcap) {
+  return ((u64)key * GOLDEN) >> (64 - logcap);
+}
+
+__device__ __forceinline__ u32 table_reserve(u64* table, u32 logcap, u32 key, u32 val,
+                                             u32& claimed, u32* err) {
+  const u64 mask = (1ull << logcap) - 1;
+  u64 s = rp_home(key, logcap);
+  const u64 want = ((u64)key << 32) | val;
+  for (u64 step = 0; step <= mask; ++step) {
+    u64 cur = __ldcg(table + s);
+    if (cur == RP_EMPTY) {
+      const u64 prev = atomicCAS(reinterpret_cast<unsigned long long*>(table + s), RP_EMPTY, want);
+      if (prev == RP_EMPTY) {
+        claimed += 1;
+        return (u32)s;
+      }
+      cur = prev;
+    }
+    if ((u32)(cur >> 32) == key) {
+      if ((u32)cur < val) atomicMax(reinterpret_cast<unsigned long long*>(table + s), want);
+      return (u32)s;
+    }
+    s = (s + 1) & mask;
+  }
+  atomicExch(err, (u32)PIP_ERR_TABLE);
+  return RP_NOSLOT;
+}
+
+__device__ __forceinline__ bool table_lookup(const u64* table, u32 logcap, u32 key, u32& val) {
+  const u64 mask = (1ull << logcap) - 1;
+  u64 s = rp_home(key, logcap);
+  for (u64 step = 0; step <= mask; ++step) {
+    const u64 cur = __ldcg(table + s);
+    if (cur == RP_EMPTY) return false;
+    if ((u32)(cur >> 32) == key) {
+      val = (u32)cur;
+      return true;
+    }
+    s = (s + 1) & mask;
+  }
+  return false;
+}
+
+// ---------------------------------------------------------------------------
+template <int V>
+__global__ void __launch_bounds__(RP_THREADS, 4) rp_kernel(RpArgs A) {
+  __shared__ u32 s_cnt[33];
+  __shared__ u64 s_red[36];
+  const u32 b = blockIdx.x, G = gridDim.x, tid = threadIdx.x, T = blockDim.x;
+  RpGlobal* g = A.g;
+  RpResume R = *A.resume;
+  u32 gen = 0;
+  u64 rounds_here = 0;
+  const bool trace = A.trace != nullptr;
+
+  while (!R.done) {
+    // ======================= P1: retire previous round =====================
+    const u32 old = R.ping, nw = R.ping ^ 1u;
+    const u32* ids_o = A.ids[old];
+    const u32* tg_o = A.tg[old];
+    u32* ids_n = A.ids[nw];
+    u32* tg_n = A.tg[nw];
+    u64 nfail = 0;
+    if (!R.first) {
+      const u64 F = R.fill;
+      u64 fbefore;
+      sum_counts(A.failcnt, G, b, s_red, nfail, fbefore);
+      const u64 ncommit = F - nfail;
+      // committed-per-round + livelock bookkeeping (identical in every CTA)
+      if (b == 0 && tid == 0) {
+        const u64 r = R.rounds - 1;
+        A.round_counts[r % RP_ROUND_CHUNK] = ncommit;
+      }
+      R.total_committed += ncommit;
+      if (ncommit == 0) {
+        R.zero_rounds += 1;
+        if (R.zero_rounds >= 64) {
+          if (b == 0 && tid == 0) atomicExch(&g->sync.error, (u32)PIP_ERR_LIVELOCK);
+          R.done = 1;
+          break;
+        }
+      } else {
+        R.zero_rounds = 0;
+      }
+      u64 s, e;
+      part(F, G, b, s, e);
+      const u64 cbefore = s - fbefore;  // committed items in CTAs < b
+      const bool targeted = A.targeted_clean_ok && F * 8 < (1ull << A.logcap);
+      u64 runf = 0, runc = 0;
+      for (u64 c0 = s; c0 < e; c0 += T) {
+        const u64 k = c0 + tid;
+        const bool valid = k < e;
+        const bool com = valid && __ldcg(A.cflag + k);
+        u32 tot;
+        const u32 rf = block_rank(valid && !com, s_cnt, &tot);
+        if (valid && !com) {
+          ids_n[fbefore + runf + rf] = __ldcg(ids_o + k);
+          tg_n[fbefore + runf + rf] = __ldcg(tg_o + k);
+        }
+        runf += tot;
+        if (trace) {
+          u32 totc;
+          const u32 rc = block_rank(com, s_cnt, &totc);
+          if (com) A.trace[R.trace_pos + cbefore + runc + rc] = __ldcg(ids_o + k);
+          runc += totc;
+        }
+        if (targeted && valid) {
+          const u32 sl = __ldcg(A.slot + k);
+          if (sl != RP_NOSLOT) A.table[sl] = RP_EMPTY;
+        }
+      }
+      R.trace_pos += ncommit;
+      if (!targeted) {
+        const u64 cap = 1ull << A.logcap;
+        u64 ts, te;
+        part(cap, G, b, ts, te);
+        for (u64 x = ts + tid; x < te; x += T) A.table[x] = RP_EMPTY;
+      }
+      if (V == PIP_RP_FINAL && R.dhi >= R.dlo) {
+        u64 ds, de;
+        part(R.dhi - R.dlo + 1, G, b, ds, de);
+        for (u64 x = ds + tid; x < de; x += T) A.dense[x] = 0;
+      }
+    }
+    // window for the refill (next_ids)
+    const u64 count = A.prefix - nfail;
+    long long cursor = R.cursor;
+    u64 hi = 0, lo = 0, wd = 0;
+    bool win = count > 0 && cursor >= 0;
+    auto count_window = [&]() {
+      hi = (u64)cursor;
+      const u64 W = (V == PIP_RP_FINAL) ? A.span_cap : (count > 1024 ? count : 1024);
+      lo = hi + 1 >= W ? hi + 1 - W : 0;
+      wd = hi - lo + 1;
+      u64 s, e;
+      part(wd, G, b, s, e);
+      u64 c = 0;
+      for (u64 q = s + tid; q < e; q += T) {
+        const u64 id = hi - q;
+        c += __ldg(A.h + id) != id;
+      }
+      c = block_sum(c, s_red);
+      if (tid == 0) A.wcnt[b] = (u32)c;
+    };
+    if (win) count_window();
+    if (!grid_barrier(&g->sync, gen)) break;
+
+    // ======================= P2: refill =====================================
+    if (A.debug && !R.first) {
+      // relaxed.py:212-217: every slot touched must read as empty again
+      const u64 cap = 1ull << A.logcap;
+      u64 ts, te;
+      part(cap, G, b, ts, te);
+      for (u64 x = ts + tid; x < te; x += T)
+        if (__ldcg(A.table + x) != RP_EMPTY) atomicExch(&g->sync.error, (u32)PIP_ERR_DEBUG_SWEEP);
+      if (V == PIP_RP_FINAL) {
+        part(A.span_cap, G, b, ts, te);
+        for (u64 x = ts + tid; x < te; x += T)
+          if (__ldcg(A.dense + x) != 0) atomicExch(&g->sync.error, (u32)PIP_ERR_DEBUG_SWEEP);
+      }
+    }
+    u64 total_ns = 0, wbefore = 0;
+    bool aborted = false;
+    while (win) {
+      sum_counts(A.wcnt, G, b, s_red, total_ns, wbefore);
+      if (total_ns > 0) break;
+      cursor = (long long)lo - 1;  // empty window: move on (relaxed.py:119)
+      win = cursor >= 0;
+      if (win) count_window();
+      if (!grid_barrier(&g->sync, gen)) { aborted = true; break; }
+    }
+    if (aborted) break;
+    const u64 fresh = win ? (count < total_ns ? count : total_ns) : 0;
+    if (fresh > 0) {
+      u64 s, e;
+      part(wd, G, b, s, e);
+      u64 run = wbefore;
+      for (u64 c0 = s; c0 < e && run < fresh; c0 += T) {
+        const u64 q = c0 + tid;
+        const bool valid = q < e;
+        const u64 id = hi - q;
+        const u64 hv = valid ? __ldg(A.h + id) : id;
+        const bool f = valid && hv != id;
+        u32 tot;
+        const u32 r = block_rank(f, s_cnt, &tot);
+        const u64 rank = run + r;
+        if (f && rank < fresh) {
+          ids_n[nfail + rank] = (u32)id;
+          tg_n[nfail + rank] = (u32)hv;
+          if (rank == 0) g->dhi = id;
+          if (rank == fresh - 1) g->dlo = id;
+        }
+        run += tot;
+      }
+    } else if (b == 0 && tid == 0) {
+      g->dlo = 1;
+      g->dhi = 0;
+    }
+    const u64 newF = nfail + fresh;
+    if (newF == 0) {
+      R.done = 1;
+      R.cursor = cursor;
+      break;
+    }
+    if (!grid_barrier(&g->sync, gen)) break;
+
+    // ======================= P3: reserve ====================================
+    const u64 dlo = ld_relaxed_u64(reinterpret_cast<const u64*>(&g->dlo));
+    const u64 dhi = ld_relaxed_u64(reinterpret_cast<const u64*>(&g->dhi));
+    if (fresh > 0) cursor = (long long)dlo - 1;
+    {
+      u64 s, e;
+      part(newF, G, b, s, e);
+      u32 claims = 0;
+      for (u64 k = s + tid; k < e; k += T) {
+        const u32 i = __ldcg(ids_n + k), t = __ldcg(tg_n + k);
+        u32 sl = RP_NOSLOT;
+        if (V == PIP_RP_FINAL && t >= dlo && t <= dhi) {
+          atomicMax(A.dense + (dhi - t), i + 1u);
+        } else {
+          if (V == PIP_RP_NAIVE || V == PIP_RP_FLAT) table_reserve(A.table, A.logcap, i, i, claims, &g->sync.error);
+          sl = table_reserve(A.table, A.logcap, t, i, claims, &g->sync.error);
+        }
+        A.slot[k] = sl;
+      }
+      const u64 c = block_sum(claims, s_red);
+      if (tid == 0) A.claimcnt[b] = (u32)c;
+    }
+    if (!grid_barrier(&g->sync, gen)) break;
+
+    // ======================= P4: commit + swap ==============================
+    {
+      u64 claims_total, dummy;
+      sum_counts(A.claimcnt, G, b, s_red, claims_total, dummy);
+      if (claims_total > R.peak) R.peak = claims_total;
+      u64 s, e;
+      part(newF, G, b, s, e);
+      u32 fails = 0;
+      for (u64 k = s + tid; k < e; k += T) {
+        const u32 i = __ldcg(ids_n + k), t = __ldcg(tg_n + k);
+        bool own, tgt;
+        u32 v = 0;
+        if (V == PIP_RP_FINAL && k >= nfail) {
+          const u32 dv = __ldcg(A.dense + (dhi - i));
+          own = dv == 0 || dv == i + 1u;
+        } else if (V == PIP_RP_NAIVE || V == PIP_RP_FLAT) {
+          own = table_lookup(A.table, A.logcap, i, v) && v == i;
+        } else {
+          own = !table_lookup(A.table, A.logcap, i, v) || v == i;
+        }
+        if (V == PIP_RP_FINAL && t >= dlo && t <= dhi) {
+          tgt = __ldcg(A.dense + (dhi - t)) == i + 1u;
+        } else {
+          const u32 sl = __ldcg(A.slot + k);
+          const u64 w = sl == RP_NOSLOT ? RP_EMPTY : __ldcg(A.table + sl);
+          tgt = w != RP_EMPTY && (u32)(w >> 32) == t && (u32)w == i;
+        }
+        const bool c = own && tgt;
+        A.cflag[k] = c;
+        if (c) {
+          const u64 x = __ldcg(A.a + i), y = __ldcg(A.a + t);
+          A.a[i] = y;
+          A.a[t] = x;
+        } else {
+          fails += 1;
+        }
+      }
+      const u64 f = block_sum(fails, s_red);
+      if (tid == 0) A.failcnt[b] = (u32)f;
+    }
+    R.fill = newF;
+    R.nfail_prev = nfail;
+    R.ping = nw;
+    R.rounds += 1;
+    R.first = 0;
+    R.dlo = dlo;
+    R.dhi = dhi;
+    R.cursor = cursor;
+    if (!grid_barrier(&g->sync, gen)) break;
+    if (++rounds_here >= A.rounds_limit) break;  // pause: host drains counts
+  }
+  if (b == 0 && tid == 0) *A.resume = R;
+}
+
+// ---------------------------------------------------------------------------
+// host
+
+struct RpLayout {
+  size_t ids[2], tg[2], slot, cflag, dense, table, failcnt, wcnt, claimcnt, rcounts, global,
+      resume, total;
+};
+
+static u64 pow2_at_least(u64 x) {
+  u64 c = 8;  // ReservationTable.MIN_CAPACITY
+  while (c < x) c <<= 1;
+  return c;
+}
+
+static int rp_gmax() { return num_sms(current_device()) * 4; }
+
+static RpLayout rp_layout(u64 prefix, int variant, u64 cap, int gmax) {
+  RpLayout L{};
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off += (bytes + 255) & ~(size_t)255;
+    return o;
+  };
+  L.ids[0] = take(prefix * 4);
+  L.ids[1] = take(prefix * 4);
+  L.tg[0] = take(prefix * 4);
+  L.tg[1] = take(prefix * 4);
+  L.slot = take(prefix * 4);
+  L.cflag = take(prefix);
+  L.dense = take(variant == PIP_RP_FINAL ? (prefix + prefix / 4 + 8) * 4 : 0);
+  L.table = take(cap * 8);
+  L.failcnt = take((size_t)gmax * 4);
+  L.wcnt = take((size_t)gmax * 4);
+  L.claimcnt = take((size_t)gmax * 4);
+  L.rcounts = take(RP_ROUND_CHUNK * 8);
+  L.global = take(sizeof(RpGlobal));
+  L.resume = take(sizeof(RpResume));
+  L.total = off;
+  return L;
+}
+
+static u64 rp_capacity(u64 prefix, int variant) {
+  const bool two_res = variant == PIP_RP_NAIVE || variant == PIP_RP_FLAT;
+  return pow2_at_least(two_res ? 4 * prefix : 2 * prefix);
+}
+
+size_t rp_workspace_bytes(u64 n, u64 prefix, int variant) {
+  if (prefix < 1 || variant < 0 || variant > 3) return 0;
+  if (prefix > n && n > 0) prefix = n;
+  return rp_layout(prefix, variant, rp_capacity(prefix, variant), rp_gmax()).total;
+}
+
+template <int V>
+static int rp_run(RpArgs& A, int grid, cudaStream_t st) {
+  auto k = rp_kernel<V>;
+  void* args[] = {&A};
+  PIP_CUDA(cudaLaunchCooperativeKernel((const void*)k, dim3(grid), dim3(RP_THREADS), args, 0, st));
+  return PIP_OK;
+}
+
+int validate_counts(const u64* h, u64 n, u64* nonself, u64* invalid, void* scratch16,
+                    cudaStream_t st);
+
+int rp_device(u64* a, const u64* h, u64 n, u64 prefix, int variant, int debug,
+              u64* counts_host, u64 rounds_cap, u64* trace_dev, void* ws, size_t ws_bytes,
+              pip_rp_stats* stats, cudaStream_t st) {
+  if (variant < 0 || variant > 3 || prefix < 1) return PIP_ERR_INVALID_ARG;
+  if (n >= 0xffffffffull) return PIP_ERR_UNSUPPORTED;
+  pip_rp_stats S{};
+  S.prefix = prefix;
+  if (n == 0) {
+    if (stats) *stats = S;
+    return PIP_OK;
+  }
+  // the client sizes its table / dense window from `prefix` (relaxed.py:84-89)
+  const u64 cap = rp_capacity(prefix, variant);
+  if (cap > (1ull << 31)) return PIP_ERR_UNSUPPORTED;
+  u32 logcap = 0;
+  while ((1ull << logcap) < cap) ++logcap;
+  const int dev = current_device();
+  const int gmax = rp_gmax();
+  const RpLayout Lrun = rp_layout(prefix, variant, cap, gmax);
+  if (!ws || ws_bytes < Lrun.total) return PIP_ERR_OOM;
+  char* w = (char*)ws;
+  // validate H and count the non-self iterates (relaxed.py:233, :239)
+  u64 n_iter = 0, invalid = 0;
+  int vrc = validate_counts(h, n, &n_iter, &invalid, w + Lrun.global, st);
+  if (vrc) return vrc;
+  if (invalid) return PIP_ERR_INVALID_SWAPS;
+  S.n_iterates = n_iter;
+  S.table_capacity = cap;
+  if (n_iter == 0) {
+    if (stats) *stats = S;
+    return PIP_OK;
+  }
+  // ... while run_rounds clamps the active prefix to n_iterates (detres.py:267)
+  const u64 P = prefix < n_iter ? prefix : n_iter;
+  RpArgs A{};
+  A.a = a;
+  A.h = h;
+  A.n = n;
+  A.prefix = P;
+  A.span_cap = prefix + prefix / 4 + 8;
+  A.rounds_limit = RP_ROUND_CHUNK;
+  A.logcap = logcap;
+  A.debug = debug ? 1u : 0u;
+  A.targeted_clean_ok = (variant == PIP_RP_FINAL || variant == PIP_RP_ONERES) ? 1u : 0u;
+  for (int p = 0; p < 2; ++p) {
+    A.ids[p] = (u32*)(w + Lrun.ids[p]);
+    A.tg[p] = (u32*)(w + Lrun.tg[p]);
+  }
+  A.slot = (u32*)(w + Lrun.slot);
+  A.cflag = (unsigned char*)(w + Lrun.cflag);
+  A.dense = (u32*)(w + Lrun.dense);
+  A.table = (u64*)(w + Lrun.table);
+  A.failcnt = (u32*)(w + Lrun.failcnt);
+  A.wcnt = (u32*)(w + Lrun.wcnt);
+  A.claimcnt = (u32*)(w + Lrun.claimcnt);
+  A.round_counts = (u64*)(w + Lrun.rcounts);
+  A.trace = trace_dev;
+  A.g = (RpGlobal*)(w + Lrun.global);
+  A.resume = (RpResume*)(w + Lrun.resume);
+
+  PIP_CUDA(cudaMemsetAsync(A.table, 0xff, cap * 8, st));
+  if (variant == PIP_RP_FINAL) PIP_CUDA(cudaMemsetAsync(A.dense, 0, A.span_cap * 4, st));
+  PIP_CUDA(cudaMemsetAsync(A.failcnt, 0, (size_t)gmax * 4, st));
+  PIP_CUDA(cudaMemsetAsync(A.g, 0, sizeof(RpGlobal), st));
+  RpResume R0{};
+  R0.cursor = (long long)n - 1;
+  R0.first = 1;
+  R0.dlo = 1;
+  R0.dhi = 0;
+  PIP_CUDA(cudaMemcpyAsync(A.resume, &R0, sizeof(R0), cudaMemcpyHostToDevice, st));
+  PIP_CUDA(cudaStreamSynchronize(st));  // R0 lives on this stack frame
+
+  // grid: enough CTAs to give every thread ~2 iterates, at most co-resident
+  int per_sm = 0;
+  const void* kp = variant == PIP_RP_FINAL ? (const void*)rp_kernel<PIP_RP_FINAL>
+                   : variant == PIP_RP_ONERES ? (const void*)rp_kernel<PIP_RP_ONERES>
+                   : variant == PIP_RP_FLAT ? (const void*)rp_kernel<PIP_RP_FLAT>
+                                             : (const void*)rp_kernel<PIP_RP_NAIVE>;
+  PIP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kp, RP_THREADS, 0));
+  if (per_sm < 1) return PIP_ERR_UNSUPPORTED;
+  if (per_sm > 4) per_sm = 4;
+  u64 grid = (u64)per_sm * num_sms(dev);
+  const u64 want = (P + RP_THREADS * 2 - 1) / (RP_THREADS * 2);
+  const u64 floor_g = (u64)num_sms(dev);
+  if (grid > want) grid = want < floor_g ? (floor_g < grid ? floor_g : grid) : want;
+  if (grid < 1) grid = 1;
+
+  u64 recorded = 0;
+  RpResume R{};
+  RpGlobal Gh{};
+  for (;;) {
+    int rc;
+    switch (variant) {
+      case PIP_RP_FINAL: rc = rp_run<PIP_RP_FINAL>(A, (int)grid, st); break;
+      case PIP_RP_ONERES: rc = rp_run<PIP_RP_ONERES>(A, (int)grid, st); break;
+      case PIP_RP_FLAT: rc = rp_run<PIP_RP_FLAT>(A, (int)grid, st); break;
+      default: rc = rp_run<PIP_RP_NAIVE>(A, (int)grid, st); break;
+    }
+    if (rc) return rc;
+    PIP_CUDA(cudaMemcpyAsync(&R, A.resume, sizeof(R), cudaMemcpyDeviceToHost, st));
+    PIP_CUDA(cudaMemcpyAsync(&Gh, A.g, sizeof(Gh), cudaMemcpyDeviceToHost, st));
+    PIP_CUDA(cudaStreamSynchronize(st));
+    if (Gh.sync.abort) return PIP_ERR_CUDA;
+    // counts are recorded in P1 of the following round: all rounds but the
+    // last completed one are available (all of them once done)
+    const u64 have = R.done ? R.rounds : (R.rounds ? R.rounds - 1 : 0);
+    if (have > recorded && counts_host) {
+      std::vector<u64> chunk(RP_ROUND_CHUNK);
+      PIP_CUDA(cudaMemcpyAsync(chunk.data(), A.round_counts, RP_ROUND_CHUNK * 8,
+                               cudaMemcpyDeviceToHost, st));
+      PIP_CUDA(cudaStreamSynchronize(st));
+      for (u64 r = recorded; r < have; ++r)
+        if (r < rounds_cap) counts_host[r] = chunk[r % RP_ROUND_CHUNK];
+    }
+    if (have > recorded) recorded = have;
+    if (Gh.sync.error) {
+      S.rounds = R.rounds;
+      if (stats) *stats = S;
+      return (int)Gh.sync.error;
+    }
+    if (R.done) break;
+    // reset the barrier for the next launch
+    PIP_CUDA(cudaMemsetAsync(&A.g->sync.bar_count, 0, 8, st));
+  }
+  S.rounds = R.rounds;
+  S.total_committed = R.total_committed;
+  S.peak_table_count = R.peak;
+  S.table_capacity = cap;
+  S.workspace_words = (Lrun.total + 7) / 8;
+  S.rounds_recorded = recorded < rounds_cap ? recorded : rounds_cap;
+  if (stats) *stats = S;
+  return PIP_OK;
+}
+
+}  // namespace pip

@@ -1,0 +1,252 @@
+"""Strong (zero-heap) in-place operations on the GPU — drop-in for
+``pipal.strong`` (reference strong.py).
+
+Signatures, return values and errors follow the reference:
+  scan(a, op=None, identity=0, base=256) -> ScanResult      strong.py:151-166
+  scan_blocked(a, op=None, identity=0, block=256)           strong.py:169-236
+  reduce(a, op=None, identity=0) -> int                     strong.py:43-64
+  rotate(a, o)                                              strong.py:85-95
+  filter_kway(a, pred, n=None) -> int                       strong.py:283-349
+  merge_strong(a, split, debug=False)                       strong.py:496-522
+``a`` is either a numpy uint64 array (copied through the device by the
+library's host-buffer entry points and written back in place) or a torch
+CUDA tensor (uint64/int64, processed in place on the current stream).
+
+Zero heap: nothing here charges the space meter.  Scan, filter, reduce and
+rotate use O(#CTAs) look-back scratch (the analogue of the reference's
+O(log n) recursion stack); merge_strong additionally uses O(n / 8192) chunk
+descriptors plus one 64 KiB chunk per SM of unmetered device scratch
+("workspace").
+"""
+from __future__ import annotations
+
+import ctypes as C
+import operator
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .pred import as_pred
+from .runtime import M64, Words, as_words, scratch_for, small_device_words
+
+__all__ = ["ScanResult", "scan", "scan_blocked", "scan_inclusive", "reduce", "rotate",
+           "filter_kway", "merge_strong"]
+
+SCAN_BASE = 256
+
+
+@dataclass
+class ScanResult:
+    array: object
+    total: int
+
+
+def _device_index() -> int:
+    import torch
+
+    return torch.cuda.current_device()
+
+
+def _op_code(op):
+    """Map the reference's `op` callables onto the kernel's element ops."""
+    if op is None or op is operator.add:
+        return _lib.OP_ADD
+    if op is max:
+        return _lib.OP_MAX
+    if op is min:
+        return _lib.OP_MIN
+    if op is operator.xor or op is operator.ixor:
+        return _lib.OP_XOR
+    raise TypeError("GPU scan supports op in {None, operator.add, max, min, operator.xor}; "
+                    "arbitrary callables cannot run on the device")
+
+
+def _identity_of(code: int) -> int:
+    return M64 if code == _lib.OP_MIN else 0
+
+
+def _scan_impl(a, op, identity, inclusive: bool) -> ScanResult:
+    w: Words = as_words(a, _wrap=True)
+    code = _op_code(op)
+    n = w.n
+    # reference: op=None always starts from 0 and reports `identity & M64`
+    # for an empty array; a given op starts from `identity`
+    init = 0 if op is None else int(identity) & M64
+    if n == 0:
+        return ScanResult(a, int(identity) & M64 if op is None else identity)
+    lib = _lib.load()
+    if w.is_device:
+        import torch
+
+        with torch.cuda.device(w.device):
+            st = w.stream()
+            sp, sb = scratch_for(w.device, st)
+            tot = small_device_words(1, w.device)
+            _lib.check(lib.pip_scan_u64(w.ptr, n, code, init, 1 if inclusive else 0, tot.data_ptr(),
+                                        sp, sb, st), "scan")
+            total = int(tot.item()) & M64
+    else:
+        out = C.c_uint64(0)
+        _lib.check(lib.pip_scan_u64_host(w.ptr, n, code, init, 1 if inclusive else 0,
+                                         C.byref(out), _device_index()), "scan")
+        total = int(out.value)
+    return ScanResult(a, total)
+
+
+def scan(a, op=None, identity: int = 0, base: int = SCAN_BASE) -> ScanResult:
+    """Exclusive in-place scan; returns the rewritten array and the total."""
+    return _scan_impl(a, op, identity, inclusive=False)
+
+
+def scan_blocked(a, op=None, identity: int = 0, block: int = SCAN_BASE) -> ScanResult:
+    """Blocked scan (strong.py:169-236): same contract, bit-identical to scan."""
+    return _scan_impl(a, op, identity, inclusive=False)
+
+
+def scan_inclusive(a, op=None, identity: int = 0) -> ScanResult:
+    """Inclusive in-place scan (BASELINE config 1): a[i] = x0 op ... op x_i.
+
+    Equals the reference's exclusive scan shifted left by one with the total
+    appended (``a[1:] ++ [total]``), i.e. ``np.cumsum`` for op=None.
+    """
+    return _scan_impl(a, op, identity, inclusive=True)
+
+
+def reduce(a, op=None, identity: int = 0) -> int:
+    """Fold the array with an associative op; the array is not modified."""
+    w: Words = as_words(a, _wrap=True)
+    code = _op_code(op)
+    if w.n == 0:
+        return identity & M64 if op is None else identity
+    lib = _lib.load()
+    if w.is_device:
+        import torch
+
+        with torch.cuda.device(w.device):
+            st = w.stream()
+            sp, sb = scratch_for(w.device, st)
+            tot = small_device_words(1, w.device)
+            _lib.check(lib.pip_reduce_u64(w.ptr, w.n, code, tot.data_ptr(), sp, sb, st), "reduce")
+            return int(tot.item()) & M64
+    # host array: stream it through the device with a read-only scan copy
+    import torch
+
+    dev = torch.from_numpy(w.obj.view(np.int64)).cuda()
+    return reduce(dev, op, identity)
+
+
+def rotate(a, o: int) -> None:
+    """Left-rotate in place: output[i] = input[(i + o) mod n] (triple reversal)."""
+    w: Words = as_words(a, _wrap=True)
+    n = w.n
+    if not 0 <= o <= n:
+        raise ValueError("offset must lie in [0, n]")
+    if o == 0 or o == n or n < 2:
+        return
+    lib = _lib.load()
+    if w.is_device:
+        import torch
+
+        with torch.cuda.device(w.device):
+            st = w.stream()
+            _lib.check(lib.pip_rotate_u64(w.ptr, n, o, None, 0, st), "rotate")
+        return
+    _via_device(w.obj, lambda t: rotate(t, o))
+
+
+def _via_device(arr: np.ndarray, fn):
+    """Run a device op on a host array: H2D, fn(tensor), D2H in place."""
+    import torch
+
+    t = torch.from_numpy(arr.view(np.int64)).cuda()
+    r = fn(t)
+    arr[:] = t.cpu().numpy().view(np.uint64)
+    return r
+
+
+def filter_kway(a, pred, n: int | None = None) -> int:
+    """Stable in-place filter: kept elements end up in a[0:m); returns m.
+
+    ``pred`` must be a :class:`~paper_2103_01216_b200.pred.Pred`.  Only the
+    first ``n`` words are filtered when ``n`` is given (strong.py:283-292).
+    """
+    w: Words = as_words(a, _wrap=True)
+    p = as_pred(pred)
+    n = w.n if n is None else int(n)
+    if n < 0 or n > w.n:
+        raise ValueError("n out of range")
+    if n == 0:
+        return 0
+    lib = _lib.load()
+    desc = p.descriptor()
+    if w.is_device:
+        import torch
+
+        with torch.cuda.device(w.device):
+            st = w.stream()
+            sp, sb = scratch_for(w.device, st)
+            m = small_device_words(1, w.device)
+            _lib.check(lib.pip_filter_u64(w.ptr, n, C.byref(desc), m.data_ptr(), sp, sb, st),
+                       "filter")
+            return int(m.item())
+    out = C.c_uint64(0)
+    _lib.check(lib.pip_filter_u64_host(w.ptr, n, C.byref(desc), C.byref(out), _device_index()),
+               "filter")
+    return int(out.value)
+
+
+def _merge_impl(a, split: int, debug: bool, budget_words: int, meter_workspace: bool) -> None:
+    from .runtime import alloc, release
+
+    w: Words = as_words(a, _wrap=True)
+    n = w.n
+    if not 0 <= split <= n:
+        raise ValueError("split out of range")
+    lib = _lib.load()
+    if not w.is_device:
+        if debug:
+            return _via_device(w.obj, lambda t: _merge_impl(t, split, debug, budget_words,
+                                                             meter_workspace))
+        if split == 0 or split == n or n < 2:
+            return None
+        wb = lib.pip_merge_workspace_bytes(n, split, budget_words)
+        words = (wb + 7) // 8
+        if meter_workspace:
+            from .runtime import charge, uncharge
+
+            charge(words)
+            try:
+                _lib.check(lib.pip_merge_u64_host(w.ptr, n, split, budget_words, _device_index()),
+                           "merge")
+            finally:
+                uncharge(words)
+        else:
+            _lib.check(lib.pip_merge_u64_host(w.ptr, n, split, budget_words, _device_index()),
+                       "merge")
+        return None
+    import torch
+
+    with torch.cuda.device(w.device):
+        st = w.stream()
+        sp, sb = scratch_for(w.device, st)
+        wb = lib.pip_merge_workspace_bytes(n, split, budget_words)
+        if meter_workspace:
+            buf = alloc(wb, w.device)
+            ptr, keep = buf.ptr, buf
+        else:
+            keep = torch.empty(max(wb, 16), dtype=torch.uint8, device=f"cuda:{w.device}")
+            ptr, buf = keep.data_ptr(), None
+        try:
+            _lib.check(lib.pip_merge_u64(w.ptr, n, split, 1 if debug else 0, ptr if wb else None,
+                                         wb, sp, sb, st), "merge")
+        finally:
+            if buf is not None:
+                release(buf)
+            del keep
+    return None
+
+
+def merge_strong(a, split: int, debug: bool = False) -> None:
+    """In-place merge of the sorted runs a[0:split) and a[split:n)."""
+    _merge_impl(a, split, debug, 0, meter_workspace=False)
