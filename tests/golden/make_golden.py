@@ -1,0 +1,151 @@
+"""Generate the golden fixtures from the reference `pipal` itself.
+
+Run in the build container (the reference is importable there, not on the
+GPU box):  PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py
+
+Every fixture is produced by calling the reference's own public functions on
+seeded inputs (the same seeds its tests use where they have one), so the GPU
+parity tests compare against the reference's outputs, not a restatement.
+"""
+from __future__ import annotations
+
+import sys
+from pathlib import Path
+
+import numpy as np
+
+sys.dont_write_bytecode = True
+sys.path.insert(0, "/root/reference/pkg/src")
+
+from pipal import baselines as bl  # noqa: E402
+from pipal import relaxed, strong  # noqa: E402
+from pipal.runtime import EpsilonConfig, Rng, WORD  # noqa: E402
+
+OUT = Path(__file__).resolve().parent
+
+
+def rand_words(seed, n, hi=None):
+    rng = np.random.default_rng(seed)
+    if hi is None:
+        return rng.integers(0, 1 << 64, size=n, dtype=np.uint64)
+    return rng.integers(0, hi, size=n, dtype=np.uint64)
+
+
+def make_scan():
+    d = {}
+    cases = {
+        "one": np.array([7], dtype=np.uint64),
+        "ones": np.array([1, 1, 1, 1], dtype=np.uint64),
+        "pi": np.array([3, 1, 4, 1, 5, 9, 2, 6], dtype=np.uint64),
+        "wrap": np.array([(1 << 64) - 1, 5], dtype=np.uint64),
+    }
+    for n in [2, 3, 255, 256, 257, 1000, 4096, 12345]:  # test_strong.py:96-101
+        cases[f"rand{n}"] = rand_words(n, n)
+    cases["c1like"] = Rng(1).words(0, 70_000) >> WORD(44)  # BASELINE config 1 values
+    for name, x in cases.items():
+        a = x.copy()
+        r = strong.scan(a)  # the reference's in-place Alg. 3
+        d["in_" + name] = x
+        d["out_" + name] = a
+        d["tot_" + name] = np.array([r.total], dtype=np.uint64)
+    np.savez_compressed(OUT / "scan.npz", **d)
+
+
+def make_filter():
+    d = {}
+    preds = {
+        "even": lambda b: (b & WORD(1)) == 0,        # cli.py:41
+        "odd": lambda b: (b & WORD(1)) == 1,         # test_strong.py:184
+        "mod3": lambda b: (b % WORD(3)) == 0,        # BASELINE config 2
+    }
+    inputs = {str(n): rand_words(n + 17, n) for n in [0, 1, 10, 1000, 9999, 20000]}
+    inputs["c2like"] = Rng(1).words(0, 20_000) >> WORD(1)  # config 2 value distribution
+    for name, x in inputs.items():
+        d[f"in_{name}"] = x
+        for pname, p in preds.items():
+            a = x.copy()
+            m = strong.filter_kway(a, p)  # test_strong.py:170-176
+            d[f"out_{pname}_{name}"] = a[:m].copy()
+    np.savez_compressed(OUT / "filter.npz", **d)
+
+
+def make_merge():
+    d = {}
+    pairs = [(1, 1), (5, 3), (100, 1), (1, 100), (1000, 1000), (4096, 999)]  # test_strong.py:248
+    for na, nb in pairs:
+        rng = np.random.default_rng(na * 7919 + nb)
+        x = np.sort(rng.integers(0, 50, size=na, dtype=np.uint64))
+        y = np.sort(rng.integers(0, 50, size=nb, dtype=np.uint64))
+        a = np.concatenate([x, y])
+        strong.merge_strong(a, na)
+        d[f"in_small{na}_{nb}"] = np.concatenate([x, y])
+        d[f"split_small{na}_{nb}"] = np.array([na], dtype=np.uint64)
+        d[f"out_small{na}_{nb}"] = a
+    for na, nb, eps in [(10_000, 3777, 0.5), (999, 65_536, 0.3), (20_000, 20_000, 0.7)]:
+        rng = np.random.default_rng(na * 131 + nb)  # test_relaxed_seq.py:36-40
+        x = np.sort(rng.integers(0, 2000, size=na, dtype=np.uint64))
+        y = np.sort(rng.integers(0, 2000, size=nb, dtype=np.uint64))
+        a = np.concatenate([x, y])
+        relaxed.merge_relaxed(a, na, EpsilonConfig(eps, 1e-12))
+        d[f"in_relaxed{na}_{nb}"] = np.concatenate([x, y])
+        d[f"split_relaxed{na}_{nb}"] = np.array([na], dtype=np.uint64)
+        d[f"out_relaxed{na}_{nb}"] = a
+    # config-3-like: heavy duplicates, values < 2^30
+    x = np.sort(Rng(1).words(0, 40_000) >> WORD(34))
+    y = np.sort(Rng(2).words(0, 40_000) >> WORD(34))
+    a = np.concatenate([x, y])
+    strong.merge_strong(a, len(x))
+    d["in_c3like"] = np.concatenate([x, y])
+    d["split_c3like"] = np.array([len(x)], dtype=np.uint64)
+    d["out_c3like"] = a
+    np.savez_compressed(OUT / "merge.npz", **d)
+
+
+def make_rp():
+    d = {}
+    cases = [
+        ("fig3", np.array([0, 0, 1, 3, 1, 2, 3, 1], dtype=np.uint64), 0.5, 1.0),
+        ("n10000_s177", relaxed.make_swap_sequence(10_000, Rng(177)), 0.5, 0.02),
+        ("n3000_s9", relaxed.make_swap_sequence(3000, Rng(9)), 0.5, 0.02),
+        ("n5000_s21", relaxed.make_swap_sequence(5000, Rng(21)), 0.5, 0.02),
+        ("n4001_pure03", relaxed.make_swap_sequence(4001, Rng(4)), 0.3, 1e-12),
+        ("n20000_pure07", relaxed.make_swap_sequence(20_000, Rng(3)), 0.7, 1e-12),
+    ]
+    for name, h, eps, frac in cases:
+        for variant in relaxed.RP_VARIANTS:
+            n = len(h)
+            a = np.arange(n, dtype=np.uint64)
+            tr = []
+            st = relaxed.random_permutation(a, h, variant, EpsilonConfig(eps, frac), trace=tr)
+            ref = np.arange(n, dtype=np.uint64)
+            bl.seq_knuth_shuffle(ref, h)
+            assert np.array_equal(a, ref)
+            key = f"{name}_{variant}"
+            d[key + "__h"] = h
+            d[key + "__budget"] = np.array([eps, frac], dtype=np.float64)
+            d[key + "__variant"] = np.array([variant])
+            d[key + "__rounds"] = np.array([st.rounds], dtype=np.uint64)
+            d[key + "__committed"] = np.array(st.committed_per_round, dtype=np.uint64)
+            d[key + "__peak"] = np.array([st.peak_table_load], dtype=np.float64)
+            d[key + "__trace"] = (np.concatenate(tr) if tr else np.empty(0, np.uint64)).astype(np.uint64)
+            d[key + "__out"] = a
+    np.savez_compressed(OUT / "rp.npz", **d)
+
+
+def make_rng():
+    d = {}
+    for seed in (0, 1, 177, (1 << 64) - 1):
+        r = Rng(seed)
+        d[f"words_{seed}"] = r.words(5, 5000)
+        d[f"swaps_{seed}"] = relaxed.make_swap_sequence(3000, r)
+    np.savez_compressed(OUT / "rng.npz", **d)
+
+
+if __name__ == "__main__":
+    make_scan()
+    make_filter()
+    make_merge()
+    make_rp()
+    make_rng()
+    for p in sorted(OUT.glob("*.npz")):
+        print(p.name, p.stat().st_size)
