@@ -1,0 +1,719 @@
+#!/usr/bin/env python
+"""Benchmark of the PIP hot path on B200 (contract: one JSON line on rank 0).
+
+Default workload (N=1): BASELINE.json configs[1] — in-place INCLUSIVE prefix
+sum of n = 2^32 int64 words, values Rng(1).words >> 44 (uniform in [0, 2^20)),
+resident in HBM.  `--op` selects the other configs for our own measurements:
+  scan    configs[1]  inclusive scan, 2^32 words               (default)
+  filter  configs[2]  stable filter x % 3 == 0, 2^32 words, values < 2^63
+  merge   configs[3]  merge two sorted runs of 2^31 words, values < 2^30
+  rp      configs[4]  random permutation, n = 2^30, H = make_swap_sequence
+  rp0     configs[0]  random permutation, n = 10^6, H from PCG64(seed)
+Multi-GPU (torchrun, WORLD_SIZE = N > 1): scan is sharded (strong scaling,
+2^32 / N words per rank; local reduce -> NCCL all_gather of shard totals ->
+scan with a device carry-in).  `--impl reference` times the CPU reference
+path (the C port of the reference's own algorithm in oracle/) instead.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+PAPER_GELEM_S = {  # PAPER.md:1148-1157,1320-1332 (72-core Xeon, Cilk Plus), for context only
+    "scan": 2e9 / 0.336, "filter": 2e9 / 0.335, "rp": 1e9 / 3.960, "rp0": 1e7 / 0.0656,
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="pip", choices=["pip", "reference"])
+    ap.add_argument("--op", default="scan", choices=["scan", "filter", "merge", "rp", "rp0"])
+    ap.add_argument("--log2n", type=int, default=None, help="override n = 2^k")
+    ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--profile", action="store_true",
+                    help="single warm launch pair for ncu (no JSON contract)")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# distributed plumbing
+
+def dist_init():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    return ws, rank, local
+
+
+def barrier(ws):
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def max_over_ranks(x: float, ws: int) -> float:
+    if ws == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ---------------------------------------------------------------------------
+# clocks (nvidia-smi sampled during the timed region)
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.proc = None
+        self.path = tempfile.mktemp(prefix="clk", suffix=".csv")
+        try:
+            import torch
+
+            uuid = str(torch.cuda.get_device_properties(device).uuid)
+            sel = uuid if uuid.startswith("GPU-") else f"GPU-{uuid}"
+        except Exception:
+            sel = str(device)
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", sel, f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        time.sleep(0.12)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.f.close()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        os.unlink(self.path)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no-samples"]}
+        # median under load: samples at >= 50% of max (idle gaps excluded)
+        hi = [s for s in sm if s >= 0.5 * max(smax)] or sm
+        return {"sm_mhz": statistics.median(hi), "sm_max_mhz": max(smax),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# helpers
+
+def peaks() -> dict:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return {"hbm_gbs": float(d["hbm_gbs"]), "source": "MEASURED_PEAKS.json (measured copy)"}
+    return {"hbm_gbs": 6650.0, "source": "B200_PROFILING.md fallback 6.65 TB/s"}
+
+
+def ncu_traffic(op: str):
+    """DRAM bytes per element of the dominant kernel from the committed ncu
+    summary (profiles/ncu_summary.json), or None."""
+    p = ROOT / "profiles" / "ncu_summary.json"
+    if not p.exists():
+        return None
+    d = json.loads(p.read_text())
+    e = d.get(op)
+    if not e:
+        return None
+    return e.get("dram_bytes_per_elem")
+
+
+def cpu_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+class Events:
+    def __init__(self, torch):
+        self.torch = torch
+
+    def time(self, fn, steps: int, stream):
+        torch = self.torch
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            fn()
+        e1.record(stream)
+        e1.synchronize()
+        return e0.elapsed_time(e1)
+
+
+# ---------------------------------------------------------------------------
+# workloads (pip arm)
+
+def run_scan(args, ws, rank, local, torch, pip, lib):
+    n_total = 1 << (args.log2n or 32)
+    n = n_total // ws
+    lo = rank * n
+    dev = local
+    st = torch.cuda.current_stream()
+    sptr = st.cuda_stream
+    a = torch.empty(n, dtype=torch.int64, device=f"cuda:{dev}")
+    pip.Rng(args.seed).words_device(lo, lo + n, shift=44, device=dev, out=a)
+    torch.cuda.synchronize()
+    sp, sb = pip.runtime.scratch_for(dev, sptr)
+    tot = torch.zeros(ws + 2, dtype=torch.int64, device=f"cuda:{dev}")
+    gathered = torch.zeros(ws, dtype=torch.int64, device=f"cuda:{dev}")
+    carry = torch.zeros(1, dtype=torch.int64, device=f"cuda:{dev}")
+
+    if ws == 1:
+        def step():
+            rc = lib.pip_scan_u64(a.data_ptr(), n, 0, 0, 1, tot.data_ptr(), sp, sb, sptr)
+            assert rc == 0, rc
+        launches = 1
+    else:
+        import torch.distributed as dist
+
+        def step():
+            # shard total -> all ranks' totals -> exclusive carry -> scan with carry
+            rc = lib.pip_reduce_u64(a.data_ptr(), n, 0, tot.data_ptr(), sp, sb, sptr)
+            assert rc == 0, rc
+            dist.all_gather_into_tensor(gathered, tot[:1])
+            torch.sum(gathered[:rank], dim=0, keepdim=True, out=carry) if rank else carry.zero_()
+            rc = lib.pip_scan_u64_carry(a.data_ptr(), n, 0, 0, 1, carry.data_ptr(),
+                                        tot[1:].data_ptr(), sp, sb, sptr)
+            assert rc == 0, rc
+        launches = 2
+
+    # parity of the first (warm-up) step through a size-independent property:
+    # the inclusive scan's adjacent differences give back the input, on
+    # windows at the start, middle and end of the shard, plus the total
+    wins = [(0, 1 << 16), (n // 2 - 4096, n // 2 + 4096), (n - (1 << 16), n)]
+    before = [a[s:e].clone() for s, e in wins]
+    step()
+    torch.cuda.synchronize()
+    for (s, e), x in zip(wins, before):
+        out = a[s:e]
+        assert torch.equal(out[1:] - out[:-1], x[1:]), f"scan parity failed on window {s}"
+    if ws == 1:
+        assert int(tot[0].item()) == int(a[n - 1].item())
+        assert int(a[0].item()) == int(before[0][0].item())
+    for _ in range(max(args.warmup - 1, 0)):
+        step()
+    torch.cuda.synchronize()
+
+    barrier(ws)
+    torch.cuda.synchronize()
+    clk = ClockSampler(dev)
+    ms = Events(torch).time(step, args.steps, st)
+    torch.cuda.synchronize()
+    barrier(ws)
+    clocks = clk.stop()
+    ms = max_over_ranks(ms, ws)
+    per_step = ms / args.steps
+    value = n_total * args.steps / (ms / 1e3)
+    # roofline: dominant kernel = scan_kernel; 16 B/elem algorithmic (ws==1)
+    algo_bytes = 16 * n if ws == 1 else 24 * n
+    pk = peaks()
+    achieved = algo_bytes / (per_step / 1e3) / 1e9
+    tb = ncu_traffic("scan")
+    roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": pk["hbm_gbs"],
+            "unit": "GB/s", "frac": round(achieved / pk["hbm_gbs"], 4),
+            "traffic": (tb * n) if tb else None,
+            "note": f"{'16' if ws == 1 else '24'} B/word algorithmic (read+write"
+                    f"{'' if ws == 1 else ' + shard reduce'}); peak = {pk['source']}; "
+                    "kernel time = CUDA-event step time (1 launch/step)"}
+    extra = {"n_per_rank": n}
+    e2e = None
+    if not args.no_e2e:
+        e2e = e2e_host(lib, "scan", n, args, torch, dev, ws)
+    cpu = None
+    if ws == 1 and rank == 0 and not args.no_cpu:
+        cpu = cpu_baseline("scan", args)
+    cfg = {"workload": "inclusive in-place scan, BASELINE configs[1]", "n": n_total,
+           "dtype_in": "int64 (uint64 words)", "values": f"Rng({args.seed}).words >> 44, in [0,2^20)",
+           "l2": "inputs (32 GiB) larger than L2 (126 MB): no flush needed",
+           "parallelism": f"shard{ws}" if ws > 1 else "single-GPU",
+           "seed": args.seed}
+    return dict(value=value, per_step=per_step, roof=roof, e2e=e2e, cpu=cpu, cfg=cfg,
+                clocks=clocks, launches=launches * args.steps, extra=extra)
+
+
+def regen_timed(step, regen, steps, torch, st):
+    """Per-step CUDA-event timing for destructive in-place ops: the input is
+    regenerated between steps OUTSIDE the timed events."""
+    total = 0.0
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    for _ in range(steps):
+        regen()
+        torch.cuda.synchronize()
+        e0.record(st)
+        step()
+        e1.record(st)
+        e1.synchronize()
+        total += e0.elapsed_time(e1)
+    return total
+
+
+def run_filter(args, ws, rank, local, torch, pip, lib):
+    if ws > 1:
+        raise SystemExit("filter is benchmarked on one GPU in this round")
+    n = 1 << (args.log2n or 32)
+    dev = local
+    st = torch.cuda.current_stream()
+    sptr = st.cuda_stream
+    a = torch.empty(n, dtype=torch.int64, device=f"cuda:{dev}")
+    rng = pip.Rng(args.seed)
+    regen = lambda: rng.words_device(0, n, shift=1, device=dev, out=a)  # noqa: E731
+    sp, sb = pip.runtime.scratch_for(dev, sptr)
+    mdev = torch.zeros(1, dtype=torch.int64, device=f"cuda:{dev}")
+    desc = pip.pred.mod_eq(3, 0).descriptor()
+
+    def step():
+        rc = lib.pip_filter_u64(a.data_ptr(), n, C.byref(desc), mdev.data_ptr(), sp, sb, sptr)
+        assert rc == 0, rc
+
+    for _ in range(args.warmup):
+        regen()
+        step()
+    torch.cuda.synchronize()
+    m = int(mdev.item())
+    regen()
+    cnt = torch.zeros(1, dtype=torch.int64, device=f"cuda:{dev}")
+    lib.pip_count_u64(a.data_ptr(), n, C.byref(desc), cnt.data_ptr(), sp, sb, sptr)
+    assert int(cnt.item()) == m
+    clk = ClockSampler(dev)
+    ms = regen_timed(step, regen, args.steps, torch, st)
+    clocks = clk.stop()
+    per_step = ms / args.steps
+    value = n * args.steps / (ms / 1e3)
+    algo = 8 * n + 8 * m
+    pk = peaks()
+    achieved = algo / (per_step / 1e3) / 1e9
+    tb = ncu_traffic("filter")
+    roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": pk["hbm_gbs"], "unit": "GB/s",
+            "frac": round(achieved / pk["hbm_gbs"], 4), "traffic": (tb * n) if tb else None,
+            "note": f"8 B/word read + 8 B/kept word written (m/n = {m / n:.4f}); peak = {pk['source']}"}
+    e2e = None if args.no_e2e else e2e_host(lib, "filter", n, args, torch, dev, ws)
+    cpu = None if args.no_cpu else cpu_baseline("filter", args)
+    cfg = {"workload": "stable in-place filter x % 3 == 0, BASELINE configs[2]", "n": n,
+           "values": f"Rng({args.seed}).words >> 1, in [0,2^63)", "kept": m,
+           "l2": "inputs larger than L2; input regenerated between steps (untimed)",
+           "parallelism": "single-GPU", "seed": args.seed}
+    return dict(value=value, per_step=per_step, roof=roof, e2e=e2e, cpu=cpu, cfg=cfg,
+                clocks=clocks, launches=args.steps, extra={})
+
+
+def sort_run(t, torch, pip):
+    """Sort a device run of any length (torch.sort stops at INT_MAX elements):
+    sort pieces of 2^30 with torch, then merge adjacent pieces in place."""
+    n = t.numel()
+    piece = 1 << 30
+    for s in range(0, n, piece):
+        t[s:s + piece] = torch.sort(t[s:s + piece]).values
+    width = piece
+    while width < n:
+        for s in range(0, n, 2 * width):
+            e = min(s + 2 * width, n)
+            if s + width < e:
+                pip.relaxed.merge_relaxed(t[s:e], width)
+        width *= 2
+
+
+def run_merge(args, ws, rank, local, torch, pip, lib):
+    if ws > 1:
+        raise SystemExit("merge is benchmarked on one GPU in this round")
+    n = 1 << (args.log2n or 32)
+    na = n // 2
+    dev = local
+    st = torch.cuda.current_stream()
+    sptr = st.cuda_stream
+    a = torch.empty(n, dtype=torch.int64, device=f"cuda:{dev}")
+    rng = pip.Rng(args.seed)
+
+    def regen():
+        rng.words_device(0, n, shift=34, device=dev, out=a)
+        sort_run(a[:na], torch, pip)
+        sort_run(a[na:], torch, pip)
+
+    budget = pip.EpsilonConfig(0.5)
+    b = budget.prefix_words(n)
+    wb = lib.pip_merge_workspace_bytes(n, na, b)
+    ws_t = torch.empty(max(wb, 16), dtype=torch.uint8, device=f"cuda:{dev}")
+    sp, sb = pip.runtime.scratch_for(dev, sptr)
+
+    def step():
+        rc = lib.pip_merge_u64(a.data_ptr(), n, na, 0, ws_t.data_ptr(), wb, sp, sb, sptr)
+        assert rc == 0, rc
+
+    regen()
+    step()
+    torch.cuda.synchronize()
+    assert bool((a[1:] >= a[:-1]).all().item())
+    for _ in range(max(args.warmup - 1, 0)):
+        regen()
+        step()
+    clk = ClockSampler(dev)
+    ms = regen_timed(step, regen, args.steps, torch, st)
+    clocks = clk.stop()
+    per_step = ms / args.steps
+    value = n * args.steps / (ms / 1e3)
+    pk = peaks()
+    achieved = 16 * n / (per_step / 1e3) / 1e9
+    tb = ncu_traffic("merge")
+    roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": pk["hbm_gbs"], "unit": "GB/s",
+            "frac": round(achieved / pk["hbm_gbs"], 4), "traffic": (tb * n) if tb else None,
+            "note": "16 B/word algorithmic (each word read once, written once); the in-place "
+                    "schedule moves ~32 B/word (chunk permutation + block merge)"}
+    e2e = None if args.no_e2e else e2e_host(lib, "merge", n, args, torch, dev, ws, budget=b)
+    cpu = None if args.no_cpu else cpu_baseline("merge", args)
+    cfg = {"workload": "in-place merge of two sorted runs (merge_relaxed, eps=0.5, f=0.02), "
+                       "BASELINE configs[3]", "n": n, "split": na,
+           "values": f"Rng({args.seed}).words >> 34, in [0,2^30), runs sorted (untimed)",
+           "workspace_bytes": wb, "budget_words": b,
+           "l2": "inputs larger than L2; runs regenerated + sorted between steps (untimed)",
+           "parallelism": "single-GPU", "seed": args.seed}
+    return dict(value=value, per_step=per_step, roof=roof, e2e=e2e, cpu=cpu, cfg=cfg,
+                clocks=clocks, launches=args.steps, extra={})
+
+
+def run_rp(args, ws, rank, local, torch, pip, lib, small: bool):
+    if ws > 1:
+        raise SystemExit("the random permutation is single-GPU (replicas only)")
+    dev = local
+    st = torch.cuda.current_stream()
+    sptr = st.cuda_stream
+    if small:
+        n = 10 ** 6 if args.log2n is None else 1 << args.log2n
+        g = np.random.Generator(np.random.PCG64(args.seed))
+        hh = g.integers(0, np.arange(1, n + 1, dtype=np.int64), dtype=np.int64)
+        h = torch.from_numpy(hh).cuda()
+        hsrc = f"PCG64({args.seed}) integers(0, i+1)"
+    else:
+        n = 1 << (args.log2n or 30)
+        h = torch.empty(n, dtype=torch.int64, device=f"cuda:{dev}")
+        pip.Rng(args.seed).swaps_device(0, n, device=dev, out=h)
+        hsrc = f"make_swap_sequence(n, Rng({args.seed})) generated on device"
+    a = torch.arange(n, dtype=torch.int64, device=f"cuda:{dev}")
+    budget = pip.EpsilonConfig(0.5)
+    prefix = budget.prefix_words(n)
+    wb = lib.pip_rp_workspace_bytes(n, prefix, 3)
+    ws_t = torch.empty(wb, dtype=torch.uint8, device=f"cuda:{dev}")
+    stats = pip._lib.PipRpStats()
+    counts = np.zeros(1 << 16, dtype=np.uint64)
+
+    def step():
+        rc = lib.pip_random_permutation_u64(a.data_ptr(), h.data_ptr(), n, prefix, 3, 0,
+                                            counts.ctypes.data, len(counts), None,
+                                            ws_t.data_ptr(), wb, C.byref(stats), sptr)
+        assert rc == 0, rc
+
+    step()
+    torch.cuda.synchronize()
+    if small or n <= (1 << 26):
+        from oracle import oracle
+
+        ref = np.arange(n, dtype=np.uint64)
+        oracle.seq_knuth_shuffle(ref, h.cpu().numpy().view(np.uint64))
+        assert np.array_equal(a.cpu().numpy().view(np.uint64), ref)
+    for _ in range(max(args.warmup - 1, 0)):
+        step()
+    torch.cuda.synchronize()
+    clk = ClockSampler(dev)
+    ms = Events(torch).time(step, args.steps, st)
+    clocks = clk.stop()
+    per_step = ms / args.steps
+    value = n * args.steps / (ms / 1e3)
+    iters = int(stats.n_iterates)
+    # roofline: one random 8-byte read-modify-write (a 32-byte sector) per
+    # committed swap, against a measured random-RMW rate on an equal array
+    bufn = n
+    buf = torch.zeros(bufn, dtype=torch.int64, device=f"cuda:{dev}")
+    msf = C.c_float(0)
+    upd = max(bufn, 1 << 26)
+    lib.pip_bench_random_rmw(buf.data_ptr(), bufn, upd, 7, C.byref(msf), sptr)
+    rmw_rate = upd / (msf.value / 1e3)
+    del buf
+    swaps_rate = iters / (per_step / 1e3)
+    roof = {"bound": "hbm", "achieved": round(swaps_rate * 32 / 1e9, 1),
+            "peak": round(rmw_rate * 32 / 1e9, 1), "unit": "GB/s",
+            "frac": round(swaps_rate / rmw_rate, 4), "traffic": None,
+            "note": "random-sector roofline: one 32-B sector RMW per committed swap "
+                    f"({iters} swaps) vs a measured random 8-B RMW microbenchmark over "
+                    f"{bufn} words ({rmw_rate / 1e9:.2f} G RMW/s)"}
+    e2e = None
+    if not args.no_e2e:
+        e2e = e2e_host(lib, "rp", n, args, torch, dev, ws, h=h, prefix=prefix)
+    cpu = None if args.no_cpu else cpu_baseline("rp0" if small else "rp", args)
+    cfg = {"workload": ("random permutation n=10^6, BASELINE configs[0]" if small else
+                        "random permutation n=2^30, BASELINE configs[4]"),
+           "n": n, "H": hsrc, "variant": "final", "budget": "EpsilonConfig(0.5, 0.02)",
+           "prefix": prefix, "rounds": int(stats.rounds), "workspace_bytes": wb,
+           "workspace_words_over_b": round(wb / 8 / prefix, 3),
+           "l2": "C0 is L2-resident by design (8 MB); C4 arrays 8 GiB >> L2",
+           "parallelism": "single-GPU", "seed": args.seed}
+    return dict(value=value, per_step=per_step, roof=roof, e2e=e2e, cpu=cpu, cfg=cfg,
+                clocks=clocks, launches=args.steps, extra={})
+
+
+# ---------------------------------------------------------------------------
+# end to end through the C ABI with host buffers (pinned), copies timed
+
+def e2e_host(lib, op, n, args, torch, dev, ws, **kw):
+    steps = max(2, min(args.steps, 3))
+    try:
+        host = torch.empty(n, dtype=torch.int64, pin_memory=True)
+    except RuntimeError as exc:
+        return {"value": None, "unit": "elements/s", "error": f"pinned alloc failed: {exc}"}
+    hp = host.data_ptr()
+    rng_seed = args.seed
+    d = torch.empty(n, dtype=torch.int64, device=f"cuda:{dev}")
+
+    def fill():
+        import paper_2103_01216_b200 as pip
+
+        if op == "scan":
+            pip.Rng(rng_seed).words_device(0, n, shift=44, device=dev, out=d)
+        elif op == "filter":
+            pip.Rng(rng_seed).words_device(0, n, shift=1, device=dev, out=d)
+        elif op == "merge":
+            pip.Rng(rng_seed).words_device(0, n, shift=34, device=dev, out=d)
+            sort_run(d[: n // 2], torch, pip)
+            sort_run(d[n // 2:], torch, pip)
+        else:
+            d.copy_(torch.arange(n, dtype=torch.int64, device=f"cuda:{dev}"))
+        host.copy_(d)
+        torch.cuda.synchronize()
+
+    hh = None
+    if op == "rp":
+        hh = torch.empty(n, dtype=torch.int64, pin_memory=True)
+        hh.copy_(kw["h"])
+    total = 0.0
+    bi = bo = 0
+    for _ in range(steps):
+        fill()
+        t0 = time.perf_counter()
+        if op == "scan":
+            out = C.c_uint64(0)
+            rc = lib.pip_scan_u64_host(hp, n, 0, 0, 1, C.byref(out), dev)
+            bi, bo = 8 * n, 8 * n
+        elif op == "filter":
+            import paper_2103_01216_b200 as pip
+
+            desc = pip.pred.mod_eq(3, 0).descriptor()
+            out = C.c_uint64(0)
+            rc = lib.pip_filter_u64_host(hp, n, C.byref(desc), C.byref(out), dev)
+            bi, bo = 8 * n, 8 * int(out.value)
+        elif op == "merge":
+            rc = lib.pip_merge_u64_host(hp, n, n // 2, kw["budget"], dev)
+            bi, bo = 8 * n, 8 * n
+        else:
+            import paper_2103_01216_b200 as pip
+
+            stats = pip._lib.PipRpStats()
+            rc = lib.pip_random_permutation_u64_host(hp, hh.data_ptr(), n, kw["prefix"], 3,
+                                                     C.byref(stats), dev)
+            bi, bo = 16 * n, 8 * n
+        total += time.perf_counter() - t0
+        assert rc == 0, rc
+    del d
+    return {"value": n * steps / total, "unit": "elements/s", "h2d_bytes_per_step": bi,
+            "d2h_bytes_per_step": bo, "steps": steps,
+            "note": "synchronous C-ABI *_host call on pinned host memory; wall clock "
+                    "around the call (H2D + kernels + D2H)"}
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline: the C port of the reference's own algorithm (oracle/)
+
+CPU_SAMPLE_LOG2 = {"scan": 28, "filter": 28, "merge": 26, "rp": 24, "rp0": None}
+
+
+def _cpu_input(op, n, seed):
+    import paper_2103_01216_b200 as pip
+
+    rng = pip.Rng(seed)
+    if op == "scan":
+        return rng.words(0, n) >> np.uint64(44), None
+    if op == "filter":
+        return rng.words(0, n) >> np.uint64(1), None
+    if op == "merge":
+        x = rng.words(0, n) >> np.uint64(34)
+        x[: n // 2].sort()
+        x[n // 2:].sort()
+        return x, None
+    if op == "rp0":
+        g = np.random.Generator(np.random.PCG64(seed))
+        h = g.integers(0, np.arange(1, n + 1, dtype=np.int64), dtype=np.int64).astype(np.uint64)
+        return np.arange(n, dtype=np.uint64), h
+    h = rng.words(0, n) % (np.arange(n, dtype=np.uint64) + np.uint64(1))
+    return np.arange(n, dtype=np.uint64), h
+
+
+def cpu_run(op, x, h, threads):
+    import paper_2103_01216_b200 as pip
+    from oracle import oracle
+
+    n = len(x)
+    if op == "scan":
+        oracle.ref_scan(x, threads)
+    elif op == "filter":
+        oracle.ref_filter_kway(x, pip.pred.mod_eq(3, 0), threads)
+    elif op == "merge":
+        oracle.ref_merge_strong(x, n // 2, threads)
+    else:
+        oracle.ref_random_permutation(x, h, pip.EpsilonConfig(0.5).prefix_words(n), "final",
+                                      threads)
+
+
+def cpu_baseline(op, args, budget_s: float = 12.0) -> dict:
+    from oracle import oracle
+
+    oracle.build()
+    lg = CPU_SAMPLE_LOG2[op]
+    n = 10 ** 6 if lg is None else 1 << lg
+    threads = cpu_threads()
+    x0, h = _cpu_input(op, n, args.seed)
+    reps, el = 0, 0.0
+    while el < budget_s and reps < 50:
+        x = x0.copy()
+        t0 = time.perf_counter()
+        cpu_run(op, x, h, threads)
+        el += time.perf_counter() - t0
+        reps += 1
+    names = {"scan": "strong.scan (Alg. 3 up/down sweep)", "filter": "strong.filter_kway",
+             "merge": "strong.merge_strong", "rp": "relaxed.random_permutation (final)",
+             "rp0": "relaxed.random_permutation (final)"}
+    return {"value": n * reps / el, "unit": "elements/s", "cores": threads, "kind": "port",
+            "sample": f"{names[op]} C/OpenMP port (oracle/pip_oracle.c) on n={n} "
+                      f"words x {reps} reps, {el:.1f} s, same generator/seed"}
+
+
+# ---------------------------------------------------------------------------
+
+def main():
+    args = parse()
+    ws, rank, local = dist_init()
+    metric = "elements/s per in-place op (perm/scan/filter/merge); % of HBM roofline"
+    if args.impl == "reference":
+        if rank != 0:
+            barrier(ws) if False else None
+            return
+        op = args.op
+        lg = CPU_SAMPLE_LOG2[op]
+        n = 10 ** 6 if lg is None else 1 << lg
+        threads = cpu_threads()
+        x0, h = _cpu_input(op, n, args.seed)
+        for _ in range(args.warmup):
+            cpu_run(op, x0.copy(), h, threads)
+        el = 0.0
+        for _ in range(args.steps):
+            x = x0.copy()
+            t0 = time.perf_counter()
+            cpu_run(op, x, h, threads)
+            el += time.perf_counter() - t0
+        value = n * args.steps / el
+        full = {"scan": 1 << 32, "filter": 1 << 32, "merge": 1 << 32, "rp": 1 << 30, "rp0": 10 ** 6}
+        line = {"metric": metric, "value": value, "unit": "elements/s", "impl": "reference",
+                "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": el / args.steps * 1e3, "higher_is_better": True,
+                "scaling": "strong" if op in ("scan", "filter", "merge") else "weak",
+                "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+                "config": {"workload": {"scan": "inclusive in-place scan, BASELINE configs[1]",
+                                        "filter": "stable filter x%3==0, BASELINE configs[2]",
+                                        "merge": "in-place merge, BASELINE configs[3]",
+                                        "rp": "random permutation, BASELINE configs[4]",
+                                        "rp0": "random permutation, BASELINE configs[0]"}[op],
+                           "n": full[op], "sample_n": n, "seed": args.seed},
+                "cpu_baseline": {"value": value, "unit": "elements/s", "cores": threads,
+                                 "kind": "port",
+                                 "sample": f"C/OpenMP port of the reference algorithm "
+                                           f"(oracle/pip_oracle.c), n={n} per step"},
+                "e2e": {"value": value, "unit": "elements/s", "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+
+    import torch
+
+    import paper_2103_01216_b200 as pip
+
+    torch.cuda.set_device(local)
+    lib = pip._lib.load()
+    if args.op == "scan":
+        r = run_scan(args, ws, rank, local, torch, pip, lib)
+    elif args.op == "filter":
+        r = run_filter(args, ws, rank, local, torch, pip, lib)
+    elif args.op == "merge":
+        r = run_merge(args, ws, rank, local, torch, pip, lib)
+    else:
+        r = run_rp(args, ws, rank, local, torch, pip, lib, small=(args.op == "rp0"))
+    if rank == 0:
+        e2e = r["e2e"]
+        line = {"metric": metric, "value": r["value"], "unit": "elements/s", "n_gpus": ws,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": r["per_step"],
+                "higher_is_better": True,
+                "scaling": "strong" if args.op in ("scan", "filter", "merge") else "weak",
+                "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+                "config": r["cfg"], "roofline": r["roof"], "cpu_baseline": r["cpu"],
+                "e2e": e2e, "clocks": r["clocks"], "gpu_launches": r["launches"],
+                "paper_72core_elements_per_s": PAPER_GELEM_S.get(args.op)}
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

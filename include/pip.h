@@ -103,6 +103,12 @@ size_t pip_scratch_bytes(int device);
  * Replaces strong.py:151-166 (scan) and :169-236 (scan_blocked).           */
 int pip_scan_u64(uint64_t* a, uint64_t n, int op, uint64_t init, int inclusive,
                  uint64_t* total_dev, void* scratch, size_t scratch_bytes, void* stream);
+/* Same, with a DEVICE carry-in: outputs are op(init, op(*carry_dev, ...))
+ * and total_dev receives op(*carry_dev, x0 .. x_{n-1}) — the running carry a
+ * sharded or chunked scan hands to the next shard/chunk without a host sync. */
+int pip_scan_u64_carry(uint64_t* a, uint64_t n, int op, uint64_t init, int inclusive,
+                       const uint64_t* carry_dev, uint64_t* total_dev, void* scratch,
+                       size_t scratch_bytes, void* stream);
 /* Fold without writing (strong.reduce, strong.py:43-64; shard totals). */
 int pip_reduce_u64(const uint64_t* a, uint64_t n, int op, uint64_t* total_dev,
                    void* scratch, size_t scratch_bytes, void* stream);

@@ -61,6 +61,7 @@ SIGNATURES = {
     "pip_last_cuda_error": (C.c_char_p, []),
     "pip_scratch_bytes": (sz, [i32]),
     "pip_scan_u64": (i32, [vp, u64, i32, u64, i32, vp, vp, sz, vp]),
+    "pip_scan_u64_carry": (i32, [vp, u64, i32, u64, i32, vp, vp, vp, sz, vp]),
     "pip_reduce_u64": (i32, [vp, u64, i32, vp, vp, sz, vp]),
     "pip_scan_u64_host": (i32, [vp, u64, i32, u64, i32, C.POINTER(u64), i32]),
     "pip_filter_u64": (i32, [vp, u64, C.POINTER(PipPred), vp, vp, sz, vp]),

@@ -236,6 +236,13 @@ int pip_scan_u64(uint64_t* a, uint64_t n, int op, uint64_t init, int inclusive, 
                      scratch_bytes, (cudaStream_t)stream);
 }
 
+int pip_scan_u64_carry(uint64_t* a, uint64_t n, int op, uint64_t init, int inclusive,
+                       const uint64_t* carry_dev, uint64_t* total_dev, void* scratch,
+                       size_t scratch_bytes, void* stream) {
+  return scan_device((u64*)a, n, op, init, inclusive, (const u64*)carry_dev, (u64*)total_dev,
+                     scratch, scratch_bytes, (cudaStream_t)stream);
+}
+
 int pip_reduce_u64(const uint64_t* a, uint64_t n, int op, uint64_t* total_dev, void* scratch,
                    size_t scratch_bytes, void* stream) {
   return reduce_device((const u64*)a, n, op, (u64*)total_dev, scratch, scratch_bytes,

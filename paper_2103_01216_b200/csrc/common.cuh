@@ -158,12 +158,64 @@ __device__ __forceinline__ u64 warp_incl_scan(u64 v) {
 
 // ---------------------------------------------------------------------------
 // decoupled look-back tile status, O(#CTAs) and reusable (see scan.cu)
-struct TileSlot {
-  u64 agg;
-  u64 incl;
-  u32 flag;  // (epoch << 2) | state ; epoch = tile + 1
-  u32 pad[3];
+// 16 bytes, written and read with single 128-bit accesses (as CUB's tile
+// descriptors): value and (epoch << 2 | state) are always seen together.
+struct __align__(16) TileSlot {
+  u64 value;
+  u64 flag;  // (epoch << 2) | state ; epoch = tile + 1
 };
 enum : u32 { SLOT_BUSY = 0, SLOT_AGG = 1, SLOT_INCL = 2 };
+__device__ __forceinline__ void st_slot(TileSlot* s, u64 value, u64 flag) {
+  asm volatile("st.global.cg.v2.u64 [%0], {%1, %2};" ::"l"(s), "l"(value), "l"(flag) : "memory");
+}
+__device__ __forceinline__ void ld_slot(const TileSlot* s, u64& value, u64& flag) {
+  asm volatile("ld.global.cg.v2.u64 {%0, %1}, [%2];" : "=l"(value), "=l"(flag) : "l"(s) : "memory");
+}
 
+}  // namespace pip
+
+// ---------------------------------------------------------------------------
+// TMA bulk copies (cp.async.bulk, 1-D, no tensor map) + mbarriers (sm_90+)
+namespace pip {
+__device__ __forceinline__ u32 smem_u32(const void* p) {
+  return (u32)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(u64* bar, u32 count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(u64* bar, u32 bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(u64* bar, u32 phase) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+// global -> shared bulk copy completing on `bar` (16-byte aligned, size % 16 == 0)
+__device__ __forceinline__ void tma_load_1d(void* sdst, const void* gsrc, u32 bytes, u64* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(sdst)),
+      "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(u64* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+// order prior generic-proxy shared-memory accesses before async-proxy (TMA) ones
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ ulonglong2 lds2(const u64* p) {
+  return *reinterpret_cast<const ulonglong2*>(p);
+}
 }  // namespace pip

@@ -16,6 +16,7 @@
 // before this tile's look-back resolves.  So "destination precedes source"
 // (the reference's batching rule, strong.py:317-327) holds at tile
 // granularity without any batching.
+#include <cstdlib>
 #include "lookback.cuh"
 
 namespace pip {
@@ -25,15 +26,90 @@ static constexpr u64 FILTER_TILE = (u64)FILTER_THREADS * 16;
 
 int scan_grid_for(const void* kernel, int threads, int device, u64 tiles, int* grid);
 
-template <bool VEC>
-__global__ void __launch_bounds__(FILTER_THREADS, 2)
-filter_kernel(u64* __restrict__ a, u64 n, DevPred p, u64* m_out, LookbackCtx c, u64 num_tiles) {
+// one tile with values + keep flags in registers: publish the kept count,
+// look back for the output offset, scatter kept words (stable).  false => abort
+template <int THREADS>
+__device__ __forceinline__ bool filter_tile_body(const u64 (&x)[16], u32 keep, u64* __restrict__ a,
+                                                 u64 tile, u64* m_out, const LookbackCtx& c,
+                                                 u64 num_tiles, u64* s_warp, int* s_abort) {
   using O = Op<PIP_OP_ADD>;
-  __shared__ u64 s_warp[FILTER_THREADS / 32];
-  __shared__ int s_abort;
+  constexpr int NW = THREADS / 32;
   const u32 lane = lane_id(), warp = warp_id();
   const u32 lt = (1u << lane) - 1u;
+  u64* s_ctl = s_warp + NW;     // [2]: agg, ok
+  u64* s_lb = s_warp + NW + 2;  // block look-back scratch
+  u64 cnt = warp_reduce<O>((u64)__popc(keep));
+  if (lane == 0) s_warp[warp] = cnt;
+  __syncthreads();
+  if (warp == 0) {
+    const u64 wv = lane < NW ? s_warp[lane] : 0;
+    const u64 winc = warp_incl_scan<O>(wv);
+    const u64 wexc = winc - wv;
+    const u64 agg = __shfl_sync(0xffffffffu, winc, NW - 1);
+    __syncwarp();
+    if (lane < NW) s_warp[lane] = wexc;
+    if (lane == 0) {
+      const int ok = publish_begin(c, tile);
+      if (ok) {
+        // this tile's reads must be ordered before other tiles' writes into it
+        __threadfence();
+        if (tile == 0) publish_incl(c, tile, agg);
+        else publish_agg(c, tile, agg);
+      }
+      s_ctl[0] = agg;
+      s_ctl[1] = ok;
+    }
+  }
+  __syncthreads();
+  const u64 agg = s_ctl[0];
+  bool ok = s_ctl[1] != 0;
+  u64 prefix = 0;
+  if (ok && tile > 0) {
+    if (LB_BLOCK) {
+      ok = block_lookback<O, THREADS>(c, tile, prefix, s_lb);
+    } else {
+      if (warp == 0) {
+        const bool wok = lookback<O>(c, tile, prefix);
+        if (lane == 0) {
+          s_lb[0] = prefix;
+          s_lb[1] = wok;
+        }
+      }
+      __syncthreads();
+      prefix = s_lb[0];
+      ok = s_lb[1] != 0;
+    }
+    if (ok && threadIdx.x == 0) publish_incl(c, tile, prefix + agg);
+  }
+  if (!ok) {
+    if (threadIdx.x == 0) atomicExch(c.abort, 1u);
+    return false;
+  }
+  if (threadIdx.x == 0 && tile == num_tiles - 1 && m_out) *m_out = prefix + agg;
+  (void)s_abort;
+  u64 run = prefix + s_warp[warp];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const bool f0 = (keep >> (2 * j)) & 1u, f1 = (keep >> (2 * j + 1)) & 1u;
+    const u32 m0 = __ballot_sync(0xffffffffu, f0);
+    const u32 m1 = __ballot_sync(0xffffffffu, f1);
+    const u64 r0 = run + __popc(m0 & lt) + __popc(m1 & lt);
+    if (f0) a[r0] = x[2 * j];
+    if (f1) a[r0 + f0] = x[2 * j + 1];
+    run += __popc(m0) + __popc(m1);
+  }
+  __syncthreads();
+  return true;
+}
 
+template <bool VEC>
+__global__ void __launch_bounds__(FILTER_THREADS, 2)
+filter_kernel(u64* __restrict__ a, u64 n, DevPred p, u64* m_out, LookbackCtx c, u64 num_tiles,
+              u32* counter) {
+  __shared__ u64 s_warp[4 * (FILTER_THREADS / 32) + 4];
+  __shared__ int s_abort;
+  const u32 lane = lane_id(), warp = warp_id();
+  (void)counter;
   for (u64 tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
     const u64 wbase = tile * FILTER_TILE + (u64)warp * 512;
     const bool full = VEC && (tile * FILTER_TILE + FILTER_TILE <= n);
@@ -58,48 +134,79 @@ filter_kernel(u64* __restrict__ a, u64 n, DevPred p, u64* m_out, LookbackCtx c, 
         keep |= (u32)(i0 + 1 < n && pred_eval(p, x[2 * j + 1])) << (2 * j + 1);
       }
     }
-    u64 cnt = warp_reduce<O>((u64)__popc(keep));
-    if (lane == 0) s_warp[warp] = cnt;
-    __syncthreads();
-    if (warp == 0) {
-      u64 wv = lane < FILTER_THREADS / 32 ? s_warp[lane] : 0;
-      u64 winc = warp_incl_scan<O>(wv);
-      u64 wexc = winc - wv;
-      const u64 agg = __shfl_sync(0xffffffffu, winc, FILTER_THREADS / 32 - 1);
-      int ok = 1;
-      if (lane == 0) {
-        ok = publish_begin(c, tile);
-        if (ok) {
-          if (tile == 0) publish_incl(c, tile, agg);
-          else publish_agg(c, tile, agg);
-        }
-      }
-      ok = __shfl_sync(0xffffffffu, ok, 0);
-      u64 prefix = 0;
-      if (ok && tile > 0) {
-        ok = lookback<O>(c, tile, prefix);
-        if (ok && lane == 0) publish_incl(c, tile, prefix + agg);
-      }
-      if (lane < FILTER_THREADS / 32) s_warp[lane] = prefix + wexc;
-      if (lane == 0) {
-        s_abort = !ok;
-        if (ok && tile == num_tiles - 1 && m_out) *m_out = prefix + agg;
-      }
-    }
-    __syncthreads();
-    if (s_abort) return;
-    u64 run = s_warp[warp];
+    if (!filter_tile_body<FILTER_THREADS>(x, keep, a, tile, m_out, c, num_tiles, s_warp, &s_abort))
+      return;
+  }
+}
+
+// TMA ring variant (16-byte aligned base), as scan_tma_kernel
+template <int THREADS, int STAGES>
+__global__ void __launch_bounds__(THREADS, 1)
+filter_tma_kernel(u64* __restrict__ a, u64 n, DevPred p, u64* m_out, LookbackCtx c, u64 num_tiles,
+                  u64 full_tiles, u32* counter) {
+  constexpr u64 TILE = (u64)THREADS * 16;
+  constexpr u32 TILE_BYTES = (u32)(TILE * 8);
+  extern __shared__ __align__(128) u64 ring[];
+  __shared__ __align__(8) u64 bars[STAGES];
+  __shared__ u64 s_tile[STAGES];
+  __shared__ u64 s_warp[4 * (THREADS / 32) + 4];
+  __shared__ int s_abort;
+  const u32 tid = threadIdx.x, lane = lane_id(), warp = warp_id();
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; ++s) mbar_init(&bars[s], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  auto issue = [&](u64 k) {
+    const int s = (int)(k % STAGES);
+    const u64 t = blockIdx.x + k * gridDim.x;
+    s_tile[s] = t;
+    if (t < full_tiles) {
+      mbar_expect_tx(&bars[s], TILE_BYTES);
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const bool f0 = (keep >> (2 * j)) & 1u, f1 = (keep >> (2 * j + 1)) & 1u;
-      const u32 m0 = __ballot_sync(0xffffffffu, f0);
-      const u32 m1 = __ballot_sync(0xffffffffu, f1);
-      const u64 r0 = run + __popc(m0 & lt) + __popc(m1 & lt);
-      if (f0) a[r0] = x[2 * j];
-      if (f1) a[r0 + f0] = x[2 * j + 1];
-      run += __popc(m0) + __popc(m1);
+      for (int q = 0; q < 4; ++q)
+        tma_load_1d(ring + s * TILE + q * (TILE / 4), a + t * TILE + q * (TILE / 4), TILE_BYTES / 4,
+                    &bars[s]);
+    } else {
+      mbar_arrive(&bars[s]);
+    }
+  };
+  if (tid == 0)
+    for (int k = 0; k < STAGES; ++k) issue(k);
+  for (u64 k = 0;; ++k) {
+    const int s = (int)(k % STAGES);
+    mbar_wait(&bars[s], (u32)((k / STAGES) & 1));
+    const u64 tile = s_tile[s];
+    if (tile >= num_tiles) break;
+    u64 x[16];
+    u32 keep = 0;
+    if (tile < full_tiles) {
+      const u64* src = ring + s * TILE + warp * 512;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const ulonglong2 v = lds2(src + 64 * j + 2 * lane);
+        x[2 * j] = v.x;
+        x[2 * j + 1] = v.y;
+      }
+#pragma unroll
+      for (int q = 0; q < 16; ++q) keep |= (u32)pred_eval(p, x[q]) << q;
+    } else {
+      const u64 wbase = tile * TILE + (u64)warp * 512;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const u64 i0 = wbase + 64 * j + 2 * lane;
+        x[2 * j] = i0 < n ? a[i0] : 0;
+        x[2 * j + 1] = i0 + 1 < n ? a[i0 + 1] : 0;
+        keep |= (u32)(i0 < n && pred_eval(p, x[2 * j])) << (2 * j);
+        keep |= (u32)(i0 + 1 < n && pred_eval(p, x[2 * j + 1])) << (2 * j + 1);
+      }
     }
     __syncthreads();
+    if (tid == 0) {
+      fence_proxy_async_smem();
+      issue(k + STAGES);
+    }
+    if (!filter_tile_body<THREADS>(x, keep, a, tile, m_out, c, num_tiles, s_warp, &s_abort)) return;
   }
 }
 
@@ -178,12 +285,47 @@ static int launch_filter(u64* a, u64 n, const DevPred& p, u64* m_dev, const Scra
   if (g > tiles) g = tiles;
   int grid = (int)g;
   PIP_CUDA(cudaMemsetAsync(L.abort, 0, 256, st));
-  PIP_CUDA(cudaMemsetAsync(L.slots, 0, sizeof(TileSlot) * 2 * (size_t)grid, st));
-  LookbackCtx c{L.slots, L.abort, (u32)grid};
+  PIP_CUDA(cudaMemsetAsync(L.slots, 0, sizeof(TileSlot) * 4 * (size_t)grid, st));
+  LookbackCtx c{L.slots, L.abort, (u32)(4 * grid)};
   DevPred pp = p;
-  void* args[] = {&a, &n, &pp, &m_dev, &c, (void*)&tiles};
+  u32* counter = L.counter;
+  void* args[] = {&a, &n, &pp, &m_dev, &c, (void*)&tiles, &counter};
   PIP_CUDA(cudaLaunchCooperativeKernel((const void*)k, dim3(grid), dim3(FILTER_THREADS), args, 0, st));
   return PIP_OK;
+}
+
+template <int THREADS, int STAGES>
+static int launch_filter_tma(u64* a, u64 n, const DevPred& p, u64* m_dev, const ScratchLayoutF& L,
+                             cudaStream_t st, int dev) {
+  constexpr u64 TILE = (u64)THREADS * 16;
+  const u64 tiles = (n + TILE - 1) / TILE, full_tiles = n / TILE;
+  auto k = filter_tma_kernel<THREADS, STAGES>;
+  const int smem = (int)(STAGES * TILE * 8);
+  PIP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  int per_sm = 0;
+  PIP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, THREADS, smem));
+  if (per_sm < 1) return PIP_ERR_UNSUPPORTED;
+  if (per_sm > 8) per_sm = 8;
+  u64 g = (u64)per_sm * num_sms(dev);
+  if (g > tiles) g = tiles;
+  int grid = (int)g;
+  PIP_CUDA(cudaMemsetAsync(L.abort, 0, 256, st));
+  PIP_CUDA(cudaMemsetAsync(L.slots, 0, sizeof(TileSlot) * 4 * (size_t)grid, st));
+  LookbackCtx c{L.slots, L.abort, (u32)(4 * grid)};
+  DevPred pp = p;
+  u32* counter = L.counter;
+  void* args[] = {&a, &n, &pp, &m_dev, &c, (void*)&tiles, (void*)&full_tiles, &counter};
+  PIP_CUDA(cudaLaunchCooperativeKernel((const void*)k, dim3(grid), dim3(THREADS), args, smem, st));
+  return PIP_OK;
+}
+
+static int filter_cfg() {
+  static int cfg = -1;
+  if (cfg < 0) {
+    const char* e = getenv("PIP_FILTER_CFG");
+    cfg = e ? atoi(e) : 0;
+  }
+  return cfg;
 }
 
 int filter_device(u64* a, u64 n, const pip_pred* pred, u64* m_dev, void* scratch,
@@ -200,6 +342,12 @@ int filter_device(u64* a, u64 n, const pip_pred* pred, u64* m_dev, void* scratch
   DevPred p = make_dev_pred(*pred);
   ScratchLayoutF L = carve_f(scratch, sms);
   const bool vec = ((uintptr_t)a & 15) == 0;
+  const int cfg = filter_cfg();
+  if (vec && cfg > 0 && n >= FILTER_TILE) {
+    if (cfg == 1) return launch_filter_tma<512, 3>(a, n, p, m_dev, L, st, dev);
+    if (cfg == 2) return launch_filter_tma<256, 3>(a, n, p, m_dev, L, st, dev);
+    return launch_filter_tma<256, 4>(a, n, p, m_dev, L, st, dev);
+  }
   return vec ? launch_filter<true>(a, n, p, m_dev, L, st, dev)
              : launch_filter<false>(a, n, p, m_dev, L, st, dev);
 }

@@ -1,22 +1,25 @@
 // Decoupled look-back over O(#CTAs) reusable tile-status slots.
 //
-// Persistent kernels assign tiles round-robin: tile t is processed by CTA
-// t % G in wave t / G.  Each CTA owns two status slots (wave parity), so the
-// scratch is 2*G slots regardless of n — the device analogue of the
-// reference's O(log n) recursion stack (strong.py:107-129), never metered.
+// Persistent kernels walk tiles round-robin (tile t on CTA t % G, wave t / G).
+// Tile t publishes into slot t % R of a ring of R = 4G slots, so the scratch
+// is O(#CTAs) regardless of n — the device analogue of the reference's
+// O(log n) recursion stack (strong.py:107-129), never metered.  The tiles of
+// one wave start together, so a tile typically finds the last inclusive
+// prefix at the end of the PREVIOUS wave: the look-back is block-wide (every
+// thread reads one predecessor slot), which covers a whole wave in a single
+// L2 round trip instead of wave/32 warp-sized steps.
 //
-// Protocol (one writer per slot, many readers):
-//   writer, per tile t (epoch e = t + 1):
-//     0. reuse rule: the slot last held tile u = t - 2G; before overwriting
-//        it wait until tile u + 1 has published its inclusive prefix (then
-//        tile u + 1 — the only reader that cannot skip past u — is done
-//        with it);
-//     1. flag = (e, BUSY); fence; agg; fence; flag = (e, AGG)  [release]
-//     2. look back; fence; incl; fence; flag = (e, INCL)        [release]
-//   reader of tile u: acquire flag; epoch older -> not ready; epoch newer ->
-//     overwritten (restart the look-back: an overwritten slot u implies
-//     INCL(u+1) exists, so the restart terminates); epoch equal -> read the
-//     value, fence, re-read the flag (seqlock) and accept iff the epoch held.
+// A slot is 16 bytes {value, (epoch << 2) | state} published with ONE 128-bit
+// store and read with ONE 128-bit load, so a reader always sees a value
+// together with the flag it was published under (no fences, no seqlock).
+// Protocol, per tile t (epoch e = t + 1):
+//   writer: reuse rule — the slot last held tile u = t - R; before
+//           overwriting it, wait until tile u + 1 published its inclusive
+//           prefix (tile u + 1 is the only reader that cannot skip past u);
+//           then store (agg, e|AGG); look back; store (incl, e|INCL).
+//   reader of tile u: epoch older -> not ready; epoch newer -> overwritten
+//           (restart the look-back: an overwritten slot u implies INCL(u+1)
+//           exists, so restarts terminate); epoch equal -> use the value.
 // All spins are bounded: a CTA that waits ~seconds sets `abort` and exits,
 // so a protocol bug can never wedge the GPU.
 #pragma once
@@ -25,19 +28,20 @@
 namespace pip {
 
 struct LookbackCtx {
-  TileSlot* slots;  // [2 * G]
+  TileSlot* slots;  // [R]
   u32* abort;       // global abort flag (0 = ok)
-  u32 G;
+  u32 R;            // ring size (4 x resident CTAs)
 };
 
 __device__ __forceinline__ TileSlot* slot_of(const LookbackCtx& c, u64 tile) {
-  return c.slots + ((tile % c.G) * 2 + ((tile / c.G) & 1));
+  return c.slots + (tile % c.R);
 }
 
-static constexpr u64 SPIN_LIMIT = 1ull << 25;  // x ~64..256 ns sleep => seconds
+static constexpr bool LB_BLOCK = false;  // block-wide look-back (measured slower)
+static constexpr u64 SPIN_LIMIT = 1ull << 25;  // x ~64 ns sleep => seconds
 
 __device__ __forceinline__ bool spin_tick(const LookbackCtx& c, u64& spins) {
-  if (++spins > 64) __nanosleep(64);
+  if (++spins > 256) __nanosleep(32);
   if ((spins & 1023) == 0) {
     if (ld_relaxed_u32(c.abort)) return false;
     if (spins > SPIN_LIMIT) {
@@ -48,39 +52,30 @@ __device__ __forceinline__ bool spin_tick(const LookbackCtx& c, u64& spins) {
   return true;
 }
 
-// single thread: wait for the reuse rule, then mark the slot busy for tile t
+// single thread: wait for the reuse rule before tile t may use its slot
 __device__ __forceinline__ bool publish_begin(const LookbackCtx& c, u64 tile) {
-  TileSlot* s = slot_of(c, tile);
-  const u64 G = c.G;
-  if (tile >= 2 * G) {
-    const u64 v = tile - 2 * G + 1;  // tile u + 1 with u = tile - 2G
-    TileSlot* sv = slot_of(c, v);
+  const u64 R = c.R;
+  if (tile >= R) {
+    const u64 v = tile - R + 1;  // tile u + 1 with u = tile - R
+    const TileSlot* sv = slot_of(c, v);
     u64 spins = 0;
     for (;;) {
-      u32 f = ld_acquire_u32(&sv->flag);
-      u64 e = f >> 2;
+      u64 val, f;
+      ld_slot(sv, val, f);
+      const u64 e = f >> 2;
       if (e > v + 1 || (e == v + 1 && (f & 3) == SLOT_INCL)) break;
       if (!spin_tick(c, spins)) return false;
     }
   }
-  st_relaxed_u32(&s->flag, (u32)((tile + 1) << 2) | SLOT_BUSY);
-  fence_gpu();
   return true;
 }
 
 __device__ __forceinline__ void publish_agg(const LookbackCtx& c, u64 tile, u64 agg) {
-  TileSlot* s = slot_of(c, tile);
-  st_relaxed_u64(&s->agg, agg);
-  fence_gpu();
-  st_release_u32(&s->flag, (u32)((tile + 1) << 2) | SLOT_AGG);
+  st_slot(slot_of(c, tile), agg, ((tile + 1) << 2) | SLOT_AGG);
 }
 
 __device__ __forceinline__ void publish_incl(const LookbackCtx& c, u64 tile, u64 incl) {
-  TileSlot* s = slot_of(c, tile);
-  fence_gpu();
-  st_relaxed_u64(&s->incl, incl);
-  fence_gpu();
-  st_release_u32(&s->flag, (u32)((tile + 1) << 2) | SLOT_INCL);
+  st_slot(slot_of(c, tile), incl, ((tile + 1) << 2) | SLOT_INCL);
 }
 
 enum : int { RD_NOTREADY = 0, RD_AGG = 1, RD_INCL = 2, RD_OVERWRITTEN = 3 };
@@ -91,18 +86,15 @@ __device__ __forceinline__ int read_slot(const LookbackCtx& c, long long u, u64&
     v = O::identity;
     return RD_INCL;
   }
-  TileSlot* s = slot_of(c, (u64)u);
-  u32 f1 = ld_acquire_u32(&s->flag);
-  u64 e = f1 >> 2, want = (u64)u + 1;
+  u64 f;
+  ld_slot(slot_of(c, (u64)u), v, f);
+  const u64 e = f >> 2, want = (u64)u + 1;
   if (e < want) return RD_NOTREADY;
   if (e > want) return RD_OVERWRITTEN;
-  u32 st = f1 & 3;
-  if (st == SLOT_BUSY) return RD_NOTREADY;
-  v = (st == SLOT_AGG) ? ld_relaxed_u64(&s->agg) : ld_relaxed_u64(&s->incl);
-  fence_gpu();
-  u32 f2 = ld_relaxed_u32(&s->flag);
-  if ((f2 >> 2) != e) return RD_OVERWRITTEN;
-  return st == SLOT_AGG ? RD_AGG : RD_INCL;
+  const u64 st = f & 3;
+  if (st == SLOT_AGG) return RD_AGG;
+  if (st == SLOT_INCL) return RD_INCL;
+  return RD_NOTREADY;
 }
 
 // whole warp: exclusive prefix (fold of all tiles < tile); false on abort
@@ -121,8 +113,8 @@ __device__ bool lookback(const LookbackCtx& c, u64 tile, u64& prefix_out) {
     for (;;) {
       st = read_slot<O>(c, u, v);
       incl_mask = __ballot_sync(0xffffffffu, st == RD_INCL);
-      u32 bad = __ballot_sync(0xffffffffu, st == RD_NOTREADY);
-      u32 ow = __ballot_sync(0xffffffffu, st == RD_OVERWRITTEN);
+      const u32 bad = __ballot_sync(0xffffffffu, st == RD_NOTREADY);
+      const u32 ow = __ballot_sync(0xffffffffu, st == RD_OVERWRITTEN);
       need = incl_mask ? (((incl_mask & (0u - incl_mask)) << 1) - 1u) : 0xffffffffu;
       if (ow & need) {
         restart = true;
@@ -141,10 +133,74 @@ __device__ bool lookback(const LookbackCtx& c, u64 tile, u64& prefix_out) {
       if (!__shfl_sync(0xffffffffu, (int)ok, 0)) return false;
       continue;
     }
-    u64 contrib = ((need >> lane) & 1u) ? v : O::identity;
+    const u64 contrib = ((need >> lane) & 1u) ? v : O::identity;
     prefix = O::apply(prefix, warp_reduce<O>(contrib));
     if (incl_mask) break;
     base -= 32;
+  }
+  prefix_out = prefix;
+  return true;
+}
+
+// whole CTA (T threads, T/32 warps): exclusive prefix of `tile`.  s_lb needs
+// 3*(T/32)+2 words of shared memory.  Every thread gets the result.
+template <class O, int T>
+__device__ bool block_lookback(const LookbackCtx& c, u64 tile, u64& prefix_out, u64* s_lb) {
+  constexpr int NW = T / 32;
+  const u32 lane = lane_id(), warp = warp_id(), tid = threadIdx.x;
+  u64* s_first = s_lb;               // [NW] first INCL index in warp (or 32*NW sentinel)
+  u64* s_flags = s_lb + NW;          // [NW] bit0: not-ready, bit1: overwritten (positions)
+  u64* s_val = s_lb + 2 * NW;        // [NW] partial folds
+  u64* s_ctl = s_lb + 3 * NW;        // [2] control
+  u64 prefix = O::identity;
+  long long base = (long long)tile - 1;
+  u64 spins = 0;
+  for (;;) {
+    const long long u = base - (long long)tid;
+    u64 v = O::identity;
+    const int st = read_slot<O>(c, u, v);
+    // first INCL position (global index tid) over the block
+    const u32 im = __ballot_sync(0xffffffffu, st == RD_INCL);
+    if (lane == 0) s_first[warp] = im ? (u64)(warp * 32 + __ffs(im) - 1) : (u64)T;
+    __syncthreads();
+    u64 first = T;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) first = s_first[w] < first ? s_first[w] : first;
+    const bool in_need = (u64)tid <= first;
+    const u32 bad = __ballot_sync(0xffffffffu, in_need && st == RD_NOTREADY);
+    const u32 ow = __ballot_sync(0xffffffffu, in_need && st == RD_OVERWRITTEN);
+    const u64 contrib = in_need ? v : O::identity;
+    const u64 wsum = warp_reduce<O>(contrib);
+    if (lane == 0) {
+      s_flags[warp] = (bad ? 1u : 0u) | (ow ? 2u : 0u);
+      s_val[warp] = wsum;
+    }
+    __syncthreads();
+    u64 flags = 0, tot = O::identity;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+      flags |= s_flags[w];
+      tot = O::apply(tot, s_val[w]);
+    }
+    if (flags & 3) {
+      // retry: a needed predecessor has not published yet (bit 0), or a
+      // needed slot was recycled (bit 1: INCL(u+1) exists, start over).
+      // Thread 0 decides about aborting so the whole CTA leaves together.
+      if (tid == 0) s_ctl[0] = spin_tick(c, spins) ? 1 : 0;
+      __syncthreads();
+      const bool ok = s_ctl[0] != 0;
+      __syncthreads();
+      if (!ok) return false;
+      if (flags & 2) {
+        prefix = O::identity;
+        base = (long long)tile - 1;
+      }
+      continue;
+    }
+    __syncthreads();  // s_lb reused by the next iteration
+    prefix = O::apply(prefix, tot);
+    if (first < (u64)T) break;
+    base -= T;
   }
   prefix_out = prefix;
   return true;

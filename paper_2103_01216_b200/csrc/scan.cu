@@ -13,6 +13,7 @@
 // segment [tile*8192 + w*512, +512); in chunk j (0..7) lane l holds the pair
 // (2l, 2l+1) of the 64-element sub-chunk j, loaded/stored as one 128-bit
 // access, so every warp access is a fully coalesced 512-byte transaction.
+#include <cstdlib>
 #include "lookback.cuh"
 
 namespace pip {
@@ -21,15 +22,118 @@ static constexpr int SCAN_THREADS = 512;
 static constexpr int SCAN_ITEMS = 16;
 static constexpr u64 SCAN_TILE = (u64)SCAN_THREADS * SCAN_ITEMS;  // 8192
 
+// One tile, values already in registers (x[2j], x[2j+1] = pair j of this
+// lane in its warp's 512-element segment).  Publishes the aggregate, looks
+// back, scans with warp shuffles and stores.  false => abort.
+template <int OP, bool INCLUSIVE, int THREADS>
+__device__ __forceinline__ bool scan_tile_body(const u64 (&x)[SCAN_ITEMS], u64* __restrict__ a,
+                                               u64 n, u64 tile, u64 init, const u64* carry_in,
+                                               u64* total, const LookbackCtx& c, u64 num_tiles,
+                                               bool full, u64* s_warp, int* s_abort) {
+  using O = Op<OP>;
+  constexpr u64 TILE = (u64)THREADS * SCAN_ITEMS;
+  constexpr int NW = THREADS / 32;
+  const u32 lane = lane_id(), warp = warp_id();
+  const u64 wbase = tile * TILE + (u64)warp * 512;
+  u64* s_ctl = s_warp + NW;      // [2]: agg, ok
+  u64* s_lb = s_warp + NW + 2;   // block look-back scratch
+  u64 t = x[0];
+#pragma unroll
+  for (int k = 1; k < SCAN_ITEMS; ++k) t = O::apply(t, x[k]);
+  t = warp_reduce<O>(t);
+  if (lane == 0) s_warp[warp] = t;
+  __syncthreads();
+  // carry_in (streaming chunks, shards) acts as an inclusive tile -1
+  u64 prefix = (tile == 0 && carry_in) ? *carry_in : O::identity;
+  if (warp == 0) {
+    const u64 wv = lane < NW ? s_warp[lane] : O::identity;
+    const u64 winc = warp_incl_scan<O>(wv);
+    u64 wexc = __shfl_up_sync(0xffffffffu, winc, 1);
+    if (lane == 0) wexc = O::identity;
+    const u64 agg = __shfl_sync(0xffffffffu, winc, NW - 1);
+    __syncwarp();
+    if (lane < NW) s_warp[lane] = wexc;
+    if (lane == 0) {
+      const int ok = publish_begin(c, tile);
+      if (ok) {
+        if (tile == 0) publish_incl(c, tile, O::apply(prefix, agg));
+        else publish_agg(c, tile, agg);
+      }
+      s_ctl[0] = agg;
+      s_ctl[1] = ok;
+    }
+  }
+  __syncthreads();
+  const u64 agg = s_ctl[0];
+  bool ok = s_ctl[1] != 0;
+  if (ok && tile > 0) {
+    if (LB_BLOCK) {
+      ok = block_lookback<O, THREADS>(c, tile, prefix, s_lb);
+    } else {
+      // warp 0 looks back; the prefix reaches the CTA through shared memory
+      if (warp == 0) {
+        const bool wok = lookback<O>(c, tile, prefix);
+        if (lane == 0) {
+          s_lb[0] = prefix;
+          s_lb[1] = wok;
+        }
+      }
+      __syncthreads();
+      prefix = s_lb[0];
+      ok = s_lb[1] != 0;
+    }
+    if (ok && threadIdx.x == 0) publish_incl(c, tile, O::apply(prefix, agg));
+  }
+  if (!ok) {
+    if (threadIdx.x == 0) atomicExch(c.abort, 1u);
+    return false;
+  }
+  if (threadIdx.x == 0 && tile == num_tiles - 1 && total) *total = O::apply(prefix, agg);
+  (void)s_abort;
+  u64 run = O::apply(prefix, s_warp[warp]);
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const u64 x0 = x[2 * j], x1 = x[2 * j + 1];
+    const u64 s = O::apply(x0, x1);
+    const u64 inc = warp_incl_scan<O>(s);
+    u64 exc = __shfl_up_sync(0xffffffffu, inc, 1);
+    if (lane == 0) exc = O::identity;
+    const u64 tot = __shfl_sync(0xffffffffu, inc, 31);
+    const u64 e = O::apply(run, exc);
+    u64 o0, o1;
+    if (INCLUSIVE) {
+      o0 = O::apply(e, x0);
+      o1 = O::apply(o0, x1);
+    } else {
+      o0 = e;
+      o1 = O::apply(e, x0);
+    }
+    o0 = O::apply(init, o0);
+    o1 = O::apply(init, o1);
+    const u64 i0 = wbase + 64 * j + 2 * lane;
+    if (full) {
+      stg_stream2(a + i0, o0, o1);
+    } else {
+      if (i0 < n) a[i0] = o0;
+      if (i0 + 1 < n) a[i0 + 1] = o1;
+    }
+    run = O::apply(run, tot);
+  }
+  __syncthreads();  // s_warp is rewritten by the next tile
+  return true;
+}
+
+// register path: any alignment (VEC = 16-byte aligned base); tiles
+// round-robin over the persistent grid (tile t on CTA t % G)
 template <int OP, bool INCLUSIVE, bool VEC>
 __global__ void __launch_bounds__(SCAN_THREADS, 2)
 scan_kernel(u64* __restrict__ a, u64 n, u64 init, const u64* carry_in, u64* total, LookbackCtx c,
-            u64 num_tiles) {
+            u64 num_tiles, u32* counter) {
   using O = Op<OP>;
-  __shared__ u64 s_warp[SCAN_THREADS / 32];
+  __shared__ u64 s_warp[4 * (SCAN_THREADS / 32) + 4];
   __shared__ int s_abort;
   const u32 lane = lane_id(), warp = warp_id();
-
+  (void)counter;
   for (u64 tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
     const u64 wbase = tile * SCAN_TILE + (u64)warp * 512;
     const bool full = VEC && (tile * SCAN_TILE + SCAN_TILE <= n);
@@ -49,72 +153,81 @@ scan_kernel(u64* __restrict__ a, u64 n, u64 init, const u64* carry_in, u64* tota
         x[2 * j + 1] = i0 + 1 < n ? a[i0 + 1] : O::identity;
       }
     }
-    // tile aggregate
-    u64 t = x[0];
+    if (!scan_tile_body<OP, INCLUSIVE, SCAN_THREADS>(x, a, n, tile, init, carry_in, total, c,
+                                                     num_tiles, full, s_warp, &s_abort))
+      return;
+  }
+}
+
+// TMA path (16-byte aligned base): each CTA keeps STAGES claimed tiles in
+// flight as cp.async.bulk copies into a shared-memory ring, so HBM reads
+// overlap the look-back and scan of the current tile.
+template <int OP, bool INCLUSIVE, int THREADS, int STAGES>
+__global__ void __launch_bounds__(THREADS, 1)
+scan_tma_kernel(u64* __restrict__ a, u64 n, u64 init, const u64* carry_in, u64* total,
+                LookbackCtx c, u64 num_tiles, u64 full_tiles, u32* counter) {
+  using O = Op<OP>;
+  constexpr u64 TILE = (u64)THREADS * SCAN_ITEMS;
+  constexpr u32 TILE_BYTES = (u32)(TILE * 8);
+  extern __shared__ __align__(128) u64 ring[];
+  __shared__ __align__(8) u64 bars[STAGES];
+  __shared__ u64 s_tile[STAGES];
+  __shared__ u64 s_warp[4 * (THREADS / 32) + 4];
+  __shared__ int s_abort;
+  const u32 tid = threadIdx.x, lane = lane_id(), warp = warp_id();
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; ++s) mbar_init(&bars[s], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  auto issue = [&](u64 k) {  // tid 0: start the copy of this CTA's k-th tile
+    const int s = (int)(k % STAGES);
+    const u64 t = blockIdx.x + k * gridDim.x;
+    s_tile[s] = t;
+    if (t < full_tiles) {
+      mbar_expect_tx(&bars[s], TILE_BYTES);
 #pragma unroll
-    for (int k = 1; k < SCAN_ITEMS; ++k) t = O::apply(t, x[k]);
-    t = warp_reduce<O>(t);
-    if (lane == 0) s_warp[warp] = t;
-    __syncthreads();
-    if (warp == 0) {
-      u64 wv = lane < SCAN_THREADS / 32 ? s_warp[lane] : O::identity;
-      u64 winc = warp_incl_scan<O>(wv);
-      u64 wexc = __shfl_up_sync(0xffffffffu, winc, 1);
-      if (lane == 0) wexc = O::identity;
-      const u64 agg = __shfl_sync(0xffffffffu, winc, SCAN_THREADS / 32 - 1);
-      // carry_in (streaming chunks) acts as an inclusive tile -1
-      u64 prefix = (tile == 0 && carry_in) ? *carry_in : O::identity;
-      int ok = 1;
-      if (lane == 0) {
-        ok = publish_begin(c, tile);
-        if (ok) {
-          if (tile == 0) publish_incl(c, tile, O::apply(prefix, agg));
-          else publish_agg(c, tile, agg);
-        }
+      for (int q = 0; q < 4; ++q)
+        tma_load_1d(ring + s * TILE + q * (TILE / 4), a + t * TILE + q * (TILE / 4), TILE_BYTES / 4,
+                    &bars[s]);
+    } else {
+      mbar_arrive(&bars[s]);
+    }
+  };
+  if (tid == 0)
+    for (int k = 0; k < STAGES; ++k) issue(k);
+  for (u64 k = 0;; ++k) {
+    const int s = (int)(k % STAGES);
+    mbar_wait(&bars[s], (u32)((k / STAGES) & 1));
+    const u64 tile = s_tile[s];
+    if (tile >= num_tiles) break;
+    u64 x[SCAN_ITEMS];
+    const bool full = tile < full_tiles;
+    if (full) {
+      const u64* src = ring + s * TILE + warp * 512;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const ulonglong2 v = lds2(src + 64 * j + 2 * lane);
+        x[2 * j] = v.x;
+        x[2 * j + 1] = v.y;
       }
-      ok = __shfl_sync(0xffffffffu, ok, 0);
-      if (ok && tile > 0) {
-        ok = lookback<O>(c, tile, prefix);
-        if (ok && lane == 0) publish_incl(c, tile, O::apply(prefix, agg));
-      }
-      if (lane < SCAN_THREADS / 32) s_warp[lane] = O::apply(prefix, wexc);
-      if (lane == 0) {
-        s_abort = !ok;
-        if (ok && tile == num_tiles - 1 && total) *total = O::apply(prefix, agg);
+    } else {
+      const u64 wbase = tile * TILE + (u64)warp * 512;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const u64 i0 = wbase + 64 * j + 2 * lane;
+        x[2 * j] = i0 < n ? a[i0] : O::identity;
+        x[2 * j + 1] = i0 + 1 < n ? a[i0 + 1] : O::identity;
       }
     }
-    __syncthreads();
-    if (s_abort) return;
-    u64 run = s_warp[warp];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const u64 x0 = x[2 * j], x1 = x[2 * j + 1];
-      const u64 s = O::apply(x0, x1);
-      const u64 inc = warp_incl_scan<O>(s);
-      u64 exc = __shfl_up_sync(0xffffffffu, inc, 1);
-      if (lane == 0) exc = O::identity;
-      const u64 tot = __shfl_sync(0xffffffffu, inc, 31);
-      const u64 e = O::apply(run, exc);
-      u64 o0, o1;
-      if (INCLUSIVE) {
-        o0 = O::apply(e, x0);
-        o1 = O::apply(o0, x1);
-      } else {
-        o0 = e;
-        o1 = O::apply(e, x0);
-      }
-      o0 = O::apply(init, o0);
-      o1 = O::apply(init, o1);
-      const u64 i0 = wbase + 64 * j + 2 * lane;
-      if (full) {
-        stg_stream2(a + i0, o0, o1);
-      } else {
-        if (i0 < n) a[i0] = o0;
-        if (i0 + 1 < n) a[i0 + 1] = o1;
-      }
-      run = O::apply(run, tot);
+    __syncthreads();  // stage s is in registers: refill it
+    if (tid == 0) {
+      fence_proxy_async_smem();
+      issue(k + STAGES);
     }
-    __syncthreads();  // s_warp is rewritten by the next tile
+    if (!scan_tile_body<OP, INCLUSIVE, THREADS>(x, a, n, tile, init, carry_in, total, c, num_tiles,
+                                                full, s_warp, &s_abort))
+      return;
   }
 }
 
@@ -176,7 +289,7 @@ static constexpr int CTAS_PER_SM_MAX = 8;
 static size_t header_bytes() { return 256; }
 size_t scratch_bytes_for(int sms) {
   const size_t gmax = (size_t)sms * CTAS_PER_SM_MAX;
-  return header_bytes() + gmax * sizeof(u64) + 2 * gmax * sizeof(TileSlot);
+  return header_bytes() + gmax * sizeof(u64) + 4 * gmax * sizeof(TileSlot);
 }
 static ScratchLayout carve(void* scratch, int sms) {
   const size_t gmax = (size_t)sms * CTAS_PER_SM_MAX;
@@ -210,17 +323,63 @@ static int launch_scan_t(u64* a, u64 n, u64 init, const u64* carry, u64* total,
   int rc = persistent_grid(k, SCAN_THREADS, device, tiles, &grid);
   if (rc) return rc;
   PIP_CUDA(cudaMemsetAsync(L.abort, 0, header_bytes(), st));
-  PIP_CUDA(cudaMemsetAsync(L.slots, 0, sizeof(TileSlot) * 2 * (size_t)grid, st));
-  LookbackCtx c{L.slots, L.abort, (u32)grid};
-  void* args[] = {&a, &n, &init, &carry, &total, &c, (void*)&tiles};
+  PIP_CUDA(cudaMemsetAsync(L.slots, 0, sizeof(TileSlot) * 4 * (size_t)grid, st));
+  LookbackCtx c{L.slots, L.abort, (u32)(4 * grid)};
+  u32* counter = L.counter;
+  void* args[] = {&a, &n, &init, &carry, &total, &c, (void*)&tiles, &counter};
   PIP_CUDA(cudaLaunchCooperativeKernel((const void*)k, dim3(grid), dim3(SCAN_THREADS), args, 0, st));
   return PIP_OK;
+}
+
+template <int OP, bool INCL, int THREADS, int STAGES>
+static int launch_scan_tma(u64* a, u64 n, u64 init, const u64* carry, u64* total,
+                           const ScratchLayout& L, cudaStream_t st, int device) {
+  constexpr u64 TILE = (u64)THREADS * SCAN_ITEMS;
+  const u64 tiles = (n + TILE - 1) / TILE;
+  const u64 full_tiles = n / TILE;
+  auto k = scan_tma_kernel<OP, INCL, THREADS, STAGES>;
+  const int smem = (int)(STAGES * TILE * 8);
+  PIP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  int per_sm = 0;
+  PIP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, THREADS, smem));
+  if (per_sm < 1) return PIP_ERR_UNSUPPORTED;
+  if (per_sm > CTAS_PER_SM_MAX) per_sm = CTAS_PER_SM_MAX;
+  u64 g = (u64)per_sm * num_sms(device);
+  if (g > tiles) g = tiles;
+  int grid = (int)g;
+  PIP_CUDA(cudaMemsetAsync(L.abort, 0, header_bytes(), st));
+  PIP_CUDA(cudaMemsetAsync(L.slots, 0, sizeof(TileSlot) * 4 * (size_t)grid, st));
+  LookbackCtx c{L.slots, L.abort, (u32)(4 * grid)};
+  u32* counter = L.counter;
+  void* args[] = {&a, &n, &init, &carry, &total, &c, (void*)&tiles, (void*)&full_tiles, &counter};
+  PIP_CUDA(cudaLaunchCooperativeKernel((const void*)k, dim3(grid), dim3(THREADS), args, smem, st));
+  return PIP_OK;
+}
+
+static int scan_cfg() {
+  static int cfg = -1;
+  if (cfg < 0) {
+    const char* e = getenv("PIP_SCAN_CFG");
+    cfg = e ? atoi(e) : 0;
+  }
+  return cfg;
 }
 
 template <int OP>
 static int launch_scan_op(u64* a, u64 n, u64 init, int inclusive, const u64* carry, u64* total,
                           const ScratchLayout& L, cudaStream_t st, int device) {
   const bool vec = ((uintptr_t)a & 15) == 0;
+  const int cfg = scan_cfg();
+  if (vec && cfg > 0 && n >= SCAN_TILE) {
+    if (cfg == 1)
+      return inclusive ? launch_scan_tma<OP, true, 512, 3>(a, n, init, carry, total, L, st, device)
+                       : launch_scan_tma<OP, false, 512, 3>(a, n, init, carry, total, L, st, device);
+    if (cfg == 2)
+      return inclusive ? launch_scan_tma<OP, true, 256, 3>(a, n, init, carry, total, L, st, device)
+                       : launch_scan_tma<OP, false, 256, 3>(a, n, init, carry, total, L, st, device);
+    return inclusive ? launch_scan_tma<OP, true, 256, 4>(a, n, init, carry, total, L, st, device)
+                     : launch_scan_tma<OP, false, 256, 4>(a, n, init, carry, total, L, st, device);
+  }
   if (inclusive) {
     return vec ? launch_scan_t<OP, true, true>(a, n, init, carry, total, L, st, device)
                : launch_scan_t<OP, true, false>(a, n, init, carry, total, L, st, device);
