@@ -31,7 +31,8 @@ int scan_grid_for(const void* kernel, int threads, int device, u64 tiles, int* g
 template <int THREADS>
 __device__ __forceinline__ bool filter_tile_body(const u64 (&x)[16], u32 keep, u64* __restrict__ a,
                                                  u64 tile, u64* m_out, const LookbackCtx& c,
-                                                 u64 num_tiles, u64* s_warp, int* s_abort) {
+                                                 u64 num_tiles, u64* s_warp, int* s_abort,
+                                                 const u64* carry_in) {
   using O = Op<PIP_OP_ADD>;
   constexpr int NW = THREADS / 32;
   const u32 lane = lane_id(), warp = warp_id();
@@ -53,7 +54,7 @@ __device__ __forceinline__ bool filter_tile_body(const u64 (&x)[16], u32 keep, u
       if (ok) {
         // this tile's reads must be ordered before other tiles' writes into it
         __threadfence();
-        if (tile == 0) publish_incl(c, tile, agg);
+        if (tile == 0) publish_incl(c, tile, (carry_in ? *carry_in : 0) + agg);
         else publish_agg(c, tile, agg);
       }
       s_ctl[0] = agg;
@@ -63,7 +64,7 @@ __device__ __forceinline__ bool filter_tile_body(const u64 (&x)[16], u32 keep, u
   __syncthreads();
   const u64 agg = s_ctl[0];
   bool ok = s_ctl[1] != 0;
-  u64 prefix = 0;
+  u64 prefix = (tile == 0 && carry_in) ? *carry_in : 0;
   if (ok && tile > 0) {
     if (LB_BLOCK) {
       ok = block_lookback<O, THREADS>(c, tile, prefix, s_lb);
@@ -105,7 +106,7 @@ __device__ __forceinline__ bool filter_tile_body(const u64 (&x)[16], u32 keep, u
 template <bool VEC>
 __global__ void __launch_bounds__(FILTER_THREADS, 2)
 filter_kernel(u64* __restrict__ a, u64 n, DevPred p, u64* m_out, LookbackCtx c, u64 num_tiles,
-              u32* counter) {
+              u32* counter, const u64* carry_in, u64* out) {
   __shared__ u64 s_warp[4 * (FILTER_THREADS / 32) + 4];
   __shared__ int s_abort;
   const u32 lane = lane_id(), warp = warp_id();
@@ -134,7 +135,8 @@ filter_kernel(u64* __restrict__ a, u64 n, DevPred p, u64* m_out, LookbackCtx c, 
         keep |= (u32)(i0 + 1 < n && pred_eval(p, x[2 * j + 1])) << (2 * j + 1);
       }
     }
-    if (!filter_tile_body<FILTER_THREADS>(x, keep, a, tile, m_out, c, num_tiles, s_warp, &s_abort))
+    if (!filter_tile_body<FILTER_THREADS>(x, keep, out, tile, m_out, c, num_tiles, s_warp, &s_abort,
+                                          carry_in))
       return;
   }
 }
@@ -206,7 +208,132 @@ filter_tma_kernel(u64* __restrict__ a, u64 n, DevPred p, u64* m_out, LookbackCtx
       fence_proxy_async_smem();
       issue(k + STAGES);
     }
-    if (!filter_tile_body<THREADS>(x, keep, a, tile, m_out, c, num_tiles, s_warp, &s_abort)) return;
+    if (!filter_tile_body<THREADS>(x, keep, a, tile, m_out, c, num_tiles, s_warp, &s_abort, nullptr))
+      return;
+  }
+}
+
+// Aggregate-ahead pipeline (see scan_ahead_kernel in scan.cu): the next
+// tile's kept count is published before this tile looks back, so the
+// look-back never waits on a predecessor's HBM load.  In-place safety is
+// unchanged: a tile publishes its count only after its data sits in shared
+// memory, and writes only below its own end.
+template <int THREADS, int STAGES>
+__global__ void __launch_bounds__(THREADS, 1)
+filter_ahead_kernel(u64* __restrict__ a, DevPred p, u64* m_out, LookbackCtx c, u64 num_tiles) {
+  using O = Op<PIP_OP_ADD>;
+  constexpr int NW = THREADS / 32;
+  constexpr u64 TILE = (u64)THREADS * 16;
+  constexpr u32 TILE_BYTES = (u32)(TILE * 8);
+  extern __shared__ __align__(128) u64 ring[];
+  __shared__ __align__(8) u64 bars[STAGES];
+  __shared__ u64 s_wexc[STAGES][NW];
+  __shared__ u64 s_agg[STAGES];
+  __shared__ u64 s_tmp[NW + 4];
+  const u32 tid = threadIdx.x, lane = lane_id(), warp = warp_id();
+  const u32 lt = (1u << lane) - 1u;
+  const u64 G = gridDim.x;
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; ++s) mbar_init(&bars[s], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  auto issue = [&](u64 k) {
+    const u64 t = blockIdx.x + k * G;
+    if (t < num_tiles) {
+      const int s = (int)(k % STAGES);
+      mbar_expect_tx(&bars[s], TILE_BYTES);
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        tma_load_1d(ring + s * TILE + q * (TILE / 4), a + t * TILE + q * (TILE / 4), TILE_BYTES / 4,
+                    &bars[s]);
+    }
+  };
+  auto reduce_stage = [&](u64 k) {
+    const int s = (int)(k % STAGES);
+    mbar_wait(&bars[s], (u32)((k / STAGES) & 1));
+    const u64* src = ring + s * TILE + warp * 512;
+    u32 cnt = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const ulonglong2 v = lds2(src + 64 * j + 2 * lane);
+      cnt += (u32)pred_eval(p, v.x) + (u32)pred_eval(p, v.y);
+    }
+    const u64 t = warp_reduce<O>((u64)cnt);
+    if (lane == 0) s_tmp[warp] = t;
+    __syncthreads();
+    if (warp == 0) {
+      const u64 wv = lane < NW ? s_tmp[lane] : 0;
+      const u64 winc = warp_incl_scan<O>(wv);
+      if (lane < NW) s_wexc[s][lane] = winc - wv;
+      if (lane == NW - 1) s_agg[s] = winc;
+    }
+    __syncthreads();
+  };
+  if (tid == 0)
+    for (int k = 0; k < STAGES; ++k) issue(k);
+  if ((u64)blockIdx.x >= num_tiles) return;
+  reduce_stage(0);
+  if (tid == 0) {
+    const u64 t0 = blockIdx.x;
+    const int ok = publish_begin(c, t0);
+    if (ok) {
+      if (t0 == 0) publish_incl(c, 0, s_agg[0]);
+      else publish_agg(c, t0, s_agg[0]);
+    }
+    s_tmp[NW] = ok;
+  }
+  __syncthreads();
+  if (!s_tmp[NW]) return;
+  for (u64 k = 0;; ++k) {
+    const u64 tile = blockIdx.x + k * G;
+    if (tile >= num_tiles) break;
+    const int s = (int)(k % STAGES);
+    const u64 tn = tile + G;
+    if (tn < num_tiles) {
+      reduce_stage(k + 1);
+      if (tid == 0) {
+        const int ok = publish_begin(c, tn);
+        if (ok) publish_agg(c, tn, s_agg[(k + 1) % STAGES]);
+        s_tmp[NW] = ok;
+      }
+    }
+    if (warp == 0) {
+      u64 prefix = 0;
+      bool ok = true;
+      if (tile > 0) {
+        ok = lookback<O>(c, tile, prefix);
+        if (ok && lane == 0) publish_incl(c, tile, prefix + s_agg[s]);
+      }
+      if (lane == 0) {
+        s_tmp[NW + 1] = prefix;
+        s_tmp[NW + 2] = ok;
+        if (ok && tile == num_tiles - 1 && m_out) *m_out = prefix + s_agg[s];
+      }
+    }
+    __syncthreads();
+    if (!s_tmp[NW + 2] || (tn < num_tiles && !s_tmp[NW])) {
+      if (tid == 0) atomicExch(c.abort, 1u);
+      return;
+    }
+    u64 run = s_tmp[NW + 1] + s_wexc[s][warp];
+    const u64* src = ring + s * TILE + warp * 512;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const ulonglong2 v = lds2(src + 64 * j + 2 * lane);
+      const bool f0 = pred_eval(p, v.x), f1 = pred_eval(p, v.y);
+      const u32 m0 = __ballot_sync(0xffffffffu, f0);
+      const u32 m1 = __ballot_sync(0xffffffffu, f1);
+      const u64 r0 = run + __popc(m0 & lt) + __popc(m1 & lt);
+      if (f0) a[r0] = v.x;
+      if (f1) a[r0 + f0] = v.y;
+      run += __popc(m0) + __popc(m1);
+    }
+    __syncthreads();
+    if (tid == 0) {
+      fence_proxy_async_smem();
+      issue(k + STAGES);
+    }
   }
 }
 
@@ -257,6 +384,7 @@ count_kernel(const u64* __restrict__ a, u64 n, DevPred p, u64* partials, u32* co
 struct ScratchLayoutF {
   u32* abort;
   u32* counter;
+  u64* carry;
   u64* partials;
   TileSlot* slots;
 };
@@ -267,6 +395,7 @@ static ScratchLayoutF carve_f(void* scratch, int sms) {
   ScratchLayoutF L;
   L.abort = (u32*)p;
   L.counter = (u32*)p + 1;
+  L.carry = (u64*)(p + 128);
   L.partials = (u64*)(p + 256);
   L.slots = (TileSlot*)(p + 256 + gmax * sizeof(u64));
   return L;
@@ -274,7 +403,9 @@ static ScratchLayoutF carve_f(void* scratch, int sms) {
 
 template <bool VEC>
 static int launch_filter(u64* a, u64 n, const DevPred& p, u64* m_dev, const ScratchLayoutF& L,
-                         cudaStream_t st, int dev) {
+                         cudaStream_t st, int dev, const u64* carry_in = nullptr,
+                         u64* out = nullptr) {
+  if (!out) out = a;
   const u64 tiles = (n + FILTER_TILE - 1) / FILTER_TILE;
   auto k = filter_kernel<VEC>;
   int per_sm = 0;
@@ -284,12 +415,12 @@ static int launch_filter(u64* a, u64 n, const DevPred& p, u64* m_dev, const Scra
   u64 g = (u64)per_sm * num_sms(dev);
   if (g > tiles) g = tiles;
   int grid = (int)g;
-  PIP_CUDA(cudaMemsetAsync(L.abort, 0, 256, st));
+  PIP_CUDA(cudaMemsetAsync(L.abort, 0, 64, st));
   PIP_CUDA(cudaMemsetAsync(L.slots, 0, sizeof(TileSlot) * 4 * (size_t)grid, st));
   LookbackCtx c{L.slots, L.abort, (u32)(4 * grid)};
   DevPred pp = p;
   u32* counter = L.counter;
-  void* args[] = {&a, &n, &pp, &m_dev, &c, (void*)&tiles, &counter};
+  void* args[] = {&a, &n, &pp, &m_dev, &c, (void*)&tiles, &counter, &carry_in, &out};
   PIP_CUDA(cudaLaunchCooperativeKernel((const void*)k, dim3(grid), dim3(FILTER_THREADS), args, 0, st));
   return PIP_OK;
 }
@@ -309,7 +440,7 @@ static int launch_filter_tma(u64* a, u64 n, const DevPred& p, u64* m_dev, const 
   u64 g = (u64)per_sm * num_sms(dev);
   if (g > tiles) g = tiles;
   int grid = (int)g;
-  PIP_CUDA(cudaMemsetAsync(L.abort, 0, 256, st));
+  PIP_CUDA(cudaMemsetAsync(L.abort, 0, 64, st));
   PIP_CUDA(cudaMemsetAsync(L.slots, 0, sizeof(TileSlot) * 4 * (size_t)grid, st));
   LookbackCtx c{L.slots, L.abort, (u32)(4 * grid)};
   DevPred pp = p;
@@ -319,9 +450,40 @@ static int launch_filter_tma(u64* a, u64 n, const DevPred& p, u64* m_dev, const 
   return PIP_OK;
 }
 
+template <int THREADS, int STAGES>
+static int launch_filter_ahead(u64* a, u64 n, const DevPred& p, u64* m_dev,
+                               const ScratchLayoutF& L, cudaStream_t st, int dev) {
+  constexpr u64 TILE = (u64)THREADS * 16;
+  const u64 full_tiles = n / TILE, rem = n - full_tiles * TILE;
+  auto k = filter_ahead_kernel<THREADS, STAGES>;
+  const int smem = (int)(STAGES * TILE * 8);
+  PIP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  int per_sm = 0;
+  PIP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, THREADS, smem));
+  if (per_sm < 1) return PIP_ERR_UNSUPPORTED;
+  if (per_sm > 8) per_sm = 8;
+  u64 g = (u64)per_sm * num_sms(dev);
+  if (g > full_tiles) g = full_tiles;
+  int grid = (int)g;
+  u64* mid = rem ? L.carry : m_dev;
+  PIP_CUDA(cudaMemsetAsync(L.abort, 0, 64, st));
+  PIP_CUDA(cudaMemsetAsync(L.slots, 0, sizeof(TileSlot) * 4 * (size_t)grid, st));
+  LookbackCtx c{L.slots, L.abort, (u32)(4 * grid)};
+  DevPred pp = p;
+  void* args[] = {&a, &pp, &mid, &c, (void*)&full_tiles};
+  PIP_CUDA(cudaLaunchCooperativeKernel((const void*)k, dim3(grid), dim3(THREADS), args, smem, st));
+  if (rem) {
+    // tail: kept words continue at a[m_full ...]; the tail sits 16-byte aligned
+    return launch_filter<true>(a + full_tiles * TILE, rem, p, m_dev, L, st, dev, L.carry, a);
+  }
+  return PIP_OK;
+}
+
 static int filter_cfg() {
   static int cfg = -1;
   if (cfg < 0) {
+    // 0 = register path (best measured: the predicate runs once per word);
+    // 4/5 = aggregate-ahead TMA pipeline (evaluates the predicate twice)
     const char* e = getenv("PIP_FILTER_CFG");
     cfg = e ? atoi(e) : 0;
   }
@@ -343,7 +505,11 @@ int filter_device(u64* a, u64 n, const pip_pred* pred, u64* m_dev, void* scratch
   ScratchLayoutF L = carve_f(scratch, sms);
   const bool vec = ((uintptr_t)a & 15) == 0;
   const int cfg = filter_cfg();
-  if (vec && cfg > 0 && n >= FILTER_TILE) {
+  if (vec && cfg >= 4 && n >= 4 * FILTER_TILE) {
+    if (cfg == 4) return launch_filter_ahead<512, 3>(a, n, p, m_dev, L, st, dev);
+    return launch_filter_ahead<256, 3>(a, n, p, m_dev, L, st, dev);
+  }
+  if (vec && cfg > 0 && cfg < 4 && n >= FILTER_TILE) {
     if (cfg == 1) return launch_filter_tma<512, 3>(a, n, p, m_dev, L, st, dev);
     if (cfg == 2) return launch_filter_tma<256, 3>(a, n, p, m_dev, L, st, dev);
     return launch_filter_tma<256, 4>(a, n, p, m_dev, L, st, dev);
@@ -364,7 +530,7 @@ int count_device(const u64* a, u64 n, const pip_pred* pred, u64* m_dev, void* sc
   int grid = sms * 2;
   u64 need = (n + 1023) / 1024;
   if ((u64)grid > need) grid = (int)(need ? need : 1);
-  PIP_CUDA(cudaMemsetAsync(L.abort, 0, 256, st));
+  PIP_CUDA(cudaMemsetAsync(L.abort, 0, 64, st));
   count_kernel<<<grid, 512, 0, st>>>(a, n, p, L.partials, L.counter, m_dev);
   PIP_CHECK_LAUNCH();
   return PIP_OK;

@@ -231,6 +231,153 @@ scan_tma_kernel(u64* __restrict__ a, u64 n, u64 init, const u64* carry_in, u64* 
   }
 }
 
+// Aggregate-ahead pipeline (16-byte aligned base, whole tiles only):
+// every CTA keeps STAGES of its tiles in flight as cp.async.bulk copies into
+// a shared-memory ring and, before it looks back for tile k, reduces tile
+// k+1 (already in shared memory) and publishes that aggregate.  So when any
+// tile looks back, the tiles of its wave published their aggregates one
+// iteration earlier: the look-back never waits for a predecessor's HBM load,
+// only for L2 round trips.  (The measured bottleneck of the plain kernel was
+// exactly that wait: 51% of warp stalls at the CTA barrier behind warp 0's
+// look-back, profiles/r01_scan_v1_lookback_stall.ncu-rep.)
+template <int OP, bool INCLUSIVE, int THREADS, int STAGES>
+__global__ void __launch_bounds__(THREADS, 1)
+scan_ahead_kernel(u64* __restrict__ a, u64 init, const u64* carry_in, u64* total, LookbackCtx c,
+                  u64 num_tiles) {
+  using O = Op<OP>;
+  constexpr int NW = THREADS / 32;
+  constexpr u64 TILE = (u64)THREADS * SCAN_ITEMS;
+  constexpr u32 TILE_BYTES = (u32)(TILE * 8);
+  static_assert(STAGES >= 2, "need a stage for the tile ahead");
+  extern __shared__ __align__(128) u64 ring[];
+  __shared__ __align__(8) u64 bars[STAGES];
+  __shared__ u64 s_wexc[STAGES][NW];
+  __shared__ u64 s_agg[STAGES];
+  __shared__ u64 s_tmp[NW + 4];
+  const u32 tid = threadIdx.x, lane = lane_id(), warp = warp_id();
+  const u64 G = gridDim.x;
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; ++s) mbar_init(&bars[s], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  auto issue = [&](u64 k) {
+    const u64 t = blockIdx.x + k * G;
+    if (t < num_tiles) {
+      const int s = (int)(k % STAGES);
+      mbar_expect_tx(&bars[s], TILE_BYTES);
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        tma_load_1d(ring + s * TILE + q * (TILE / 4), a + t * TILE + q * (TILE / 4), TILE_BYTES / 4,
+                    &bars[s]);
+    }
+  };
+  // wait for the k-th tile, fold it: s_agg[stage], s_wexc[stage][warp]
+  auto reduce_stage = [&](u64 k) {
+    const int s = (int)(k % STAGES);
+    mbar_wait(&bars[s], (u32)((k / STAGES) & 1));
+    const u64* src = ring + s * TILE + warp * 512;
+    u64 t = O::identity;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const ulonglong2 v = lds2(src + 64 * j + 2 * lane);
+      t = O::apply(t, O::apply(v.x, v.y));
+    }
+    t = warp_reduce<O>(t);
+    if (lane == 0) s_tmp[warp] = t;
+    __syncthreads();
+    if (warp == 0) {
+      const u64 wv = lane < NW ? s_tmp[lane] : O::identity;
+      const u64 winc = warp_incl_scan<O>(wv);
+      u64 wexc = __shfl_up_sync(0xffffffffu, winc, 1);
+      if (lane == 0) wexc = O::identity;
+      if (lane < NW) s_wexc[s][lane] = wexc;
+      if (lane == NW - 1) s_agg[s] = winc;
+    }
+    __syncthreads();
+  };
+  if (tid == 0)
+    for (int k = 0; k < STAGES; ++k) issue(k);
+  if ((u64)blockIdx.x >= num_tiles) return;
+  // first tile: publish its aggregate (tile 0: its inclusive prefix)
+  reduce_stage(0);
+  if (tid == 0) {
+    const u64 t0 = blockIdx.x;
+    const int ok = publish_begin(c, t0);
+    if (ok) {
+      if (t0 == 0) publish_incl(c, 0, O::apply(carry_in ? *carry_in : O::identity, s_agg[0]));
+      else publish_agg(c, t0, s_agg[0]);
+    }
+    s_tmp[NW] = ok;
+  }
+  __syncthreads();
+  if (!s_tmp[NW]) return;
+  for (u64 k = 0;; ++k) {
+    const u64 tile = blockIdx.x + k * G;
+    if (tile >= num_tiles) break;
+    const int s = (int)(k % STAGES);
+    const u64 tn = tile + G;
+    // (1) the next tile's aggregate goes out before we wait on anyone
+    if (tn < num_tiles) {
+      reduce_stage(k + 1);
+      if (tid == 0) {
+        const int ok = publish_begin(c, tn);
+        if (ok) publish_agg(c, tn, s_agg[(k + 1) % STAGES]);
+        s_tmp[NW] = ok;
+      }
+    }
+    // (2) this tile's prefix
+    if (warp == 0) {
+      u64 prefix = (tile == 0 && carry_in) ? *carry_in : O::identity;
+      bool ok = true;
+      if (tile > 0) {
+        ok = lookback<O>(c, tile, prefix);
+        if (ok && lane == 0) publish_incl(c, tile, O::apply(prefix, s_agg[s]));
+      }
+      if (lane == 0) {
+        s_tmp[NW + 1] = prefix;
+        s_tmp[NW + 2] = ok;
+        if (ok && tile == num_tiles - 1 && total) *total = O::apply(prefix, s_agg[s]);
+      }
+    }
+    __syncthreads();
+    if (!s_tmp[NW + 2] || (tn < num_tiles && !s_tmp[NW])) {
+      if (tid == 0) atomicExch(c.abort, 1u);
+      return;
+    }
+    // (3) scan the tile out of shared memory and store it
+    u64 run = O::apply(s_tmp[NW + 1], s_wexc[s][warp]);
+    const u64* src = ring + s * TILE + warp * 512;
+    const u64 wbase = tile * TILE + (u64)warp * 512;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const ulonglong2 v = lds2(src + 64 * j + 2 * lane);
+      const u64 x0 = v.x, x1 = v.y;
+      const u64 inc = warp_incl_scan<O>(O::apply(x0, x1));
+      u64 exc = __shfl_up_sync(0xffffffffu, inc, 1);
+      if (lane == 0) exc = O::identity;
+      const u64 tot = __shfl_sync(0xffffffffu, inc, 31);
+      const u64 e = O::apply(run, exc);
+      u64 o0, o1;
+      if (INCLUSIVE) {
+        o0 = O::apply(e, x0);
+        o1 = O::apply(o0, x1);
+      } else {
+        o0 = e;
+        o1 = O::apply(e, x0);
+      }
+      stg_stream2(a + wbase + 64 * j + 2 * lane, O::apply(init, o0), O::apply(init, o1));
+      run = O::apply(run, tot);
+    }
+    // (4) release the stage
+    __syncthreads();
+    if (tid == 0) {
+      fence_proxy_async_smem();
+      issue(k + STAGES);
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // reduce: grid-stride fold, per-CTA partials, last CTA folds the partials.
 template <int OP>
@@ -282,6 +429,7 @@ reduce_kernel(const u64* __restrict__ a, u64 n, u64* partials, u32* counter, u64
 struct ScratchLayout {
   u32* abort;       // [0]
   u32* counter;     // [1]
+  u64* carry;       // header byte 128: hand-off between the two launches of a scan
   u64* partials;    // G_MAX
   TileSlot* slots;  // 2 * G_MAX
 };
@@ -297,6 +445,7 @@ static ScratchLayout carve(void* scratch, int sms) {
   ScratchLayout L;
   L.abort = (u32*)p;
   L.counter = (u32*)p + 1;
+  L.carry = (u64*)(p + 128);
   L.partials = (u64*)(p + header_bytes());
   L.slots = (TileSlot*)(p + header_bytes() + gmax * sizeof(u64));
   return L;
@@ -322,7 +471,7 @@ static int launch_scan_t(u64* a, u64 n, u64 init, const u64* carry, u64* total,
   int grid = 0;
   int rc = persistent_grid(k, SCAN_THREADS, device, tiles, &grid);
   if (rc) return rc;
-  PIP_CUDA(cudaMemsetAsync(L.abort, 0, header_bytes(), st));
+  PIP_CUDA(cudaMemsetAsync(L.abort, 0, 64, st));
   PIP_CUDA(cudaMemsetAsync(L.slots, 0, sizeof(TileSlot) * 4 * (size_t)grid, st));
   LookbackCtx c{L.slots, L.abort, (u32)(4 * grid)};
   u32* counter = L.counter;
@@ -347,7 +496,7 @@ static int launch_scan_tma(u64* a, u64 n, u64 init, const u64* carry, u64* total
   u64 g = (u64)per_sm * num_sms(device);
   if (g > tiles) g = tiles;
   int grid = (int)g;
-  PIP_CUDA(cudaMemsetAsync(L.abort, 0, header_bytes(), st));
+  PIP_CUDA(cudaMemsetAsync(L.abort, 0, 64, st));
   PIP_CUDA(cudaMemsetAsync(L.slots, 0, sizeof(TileSlot) * 4 * (size_t)grid, st));
   LookbackCtx c{L.slots, L.abort, (u32)(4 * grid)};
   u32* counter = L.counter;
@@ -356,11 +505,43 @@ static int launch_scan_tma(u64* a, u64 n, u64 init, const u64* carry, u64* total
   return PIP_OK;
 }
 
+template <int OP, bool INCL, int THREADS, int STAGES>
+static int launch_scan_ahead(u64* a, u64 n, u64 init, const u64* carry, u64* total,
+                             const ScratchLayout& L, cudaStream_t st, int device) {
+  constexpr u64 TILE = (u64)THREADS * SCAN_ITEMS;
+  const u64 full_tiles = n / TILE;
+  const u64 rem = n - full_tiles * TILE;
+  auto k = scan_ahead_kernel<OP, INCL, THREADS, STAGES>;
+  const int smem = (int)(STAGES * TILE * 8);
+  PIP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  int per_sm = 0;
+  PIP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, THREADS, smem));
+  if (per_sm < 1) return PIP_ERR_UNSUPPORTED;
+  if (per_sm > CTAS_PER_SM_MAX) per_sm = CTAS_PER_SM_MAX;
+  u64 g = (u64)per_sm * num_sms(device);
+  if (g > full_tiles) g = full_tiles;
+  int grid = (int)g;
+  // the whole-tile part writes its inclusive fold to `mid` when a tail follows
+  u64* mid = rem ? L.carry : total;
+  PIP_CUDA(cudaMemsetAsync(L.abort, 0, 64, st));
+  PIP_CUDA(cudaMemsetAsync(L.slots, 0, sizeof(TileSlot) * 4 * (size_t)grid, st));
+  LookbackCtx c{L.slots, L.abort, (u32)(4 * grid)};
+  void* args[] = {&a, &init, &carry, &mid, &c, (void*)&full_tiles};
+  PIP_CUDA(cudaLaunchCooperativeKernel((const void*)k, dim3(grid), dim3(THREADS), args, smem, st));
+  if (rem) {
+    u64* tail = a + full_tiles * TILE;
+    return launch_scan_t<OP, INCL, true>(tail, rem, init, L.carry, total, L, st, device);
+  }
+  return PIP_OK;
+}
+
 static int scan_cfg() {
   static int cfg = -1;
   if (cfg < 0) {
+    // 5 = aggregate-ahead TMA pipeline, 256 threads x 3 stages (best measured,
+    // profiles/README.md); 0 = register path; 1-3 = plain TMA rings
     const char* e = getenv("PIP_SCAN_CFG");
-    cfg = e ? atoi(e) : 0;
+    cfg = e ? atoi(e) : 5;
   }
   return cfg;
 }
@@ -370,7 +551,14 @@ static int launch_scan_op(u64* a, u64 n, u64 init, int inclusive, const u64* car
                           const ScratchLayout& L, cudaStream_t st, int device) {
   const bool vec = ((uintptr_t)a & 15) == 0;
   const int cfg = scan_cfg();
-  if (vec && cfg > 0 && n >= SCAN_TILE) {
+  if (vec && cfg >= 4 && n >= 4 * SCAN_TILE) {
+    if (cfg == 4)
+      return inclusive ? launch_scan_ahead<OP, true, 512, 3>(a, n, init, carry, total, L, st, device)
+                       : launch_scan_ahead<OP, false, 512, 3>(a, n, init, carry, total, L, st, device);
+    return inclusive ? launch_scan_ahead<OP, true, 256, 3>(a, n, init, carry, total, L, st, device)
+                     : launch_scan_ahead<OP, false, 256, 3>(a, n, init, carry, total, L, st, device);
+  }
+  if (vec && cfg > 0 && cfg < 4 && n >= SCAN_TILE) {
     if (cfg == 1)
       return inclusive ? launch_scan_tma<OP, true, 512, 3>(a, n, init, carry, total, L, st, device)
                        : launch_scan_tma<OP, false, 512, 3>(a, n, init, carry, total, L, st, device);
@@ -425,7 +613,7 @@ static int launch_reduce(const u64* a, u64 n, u64* total, const ScratchLayout& L
   int grid = sms * 2;
   u64 need = (n + 1023) / 1024;
   if ((u64)grid > need) grid = (int)(need ? need : 1);
-  PIP_CUDA(cudaMemsetAsync(L.abort, 0, header_bytes(), st));
+  PIP_CUDA(cudaMemsetAsync(L.abort, 0, 64, st));
   reduce_kernel<OP><<<grid, 512, 0, st>>>(a, n, L.partials, L.counter, total);
   PIP_CHECK_LAUNCH();
   return PIP_OK;
