@@ -1,5 +1,6 @@
 // extern "C" boundary (include/pip.h) and the host-buffer entry points.
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 #include "common.cuh"
@@ -9,6 +10,15 @@ namespace pip {
 static thread_local char g_cuda_err[256] = "";
 void set_cuda_error(cudaError_t e) {
   snprintf(g_cuda_err, sizeof(g_cuda_err), "%s: %s", cudaGetErrorName(e), cudaGetErrorString(e));
+}
+
+bool timing_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("PIP_TIMING");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
 }
 
 int current_device() {

@@ -134,6 +134,13 @@ __host__ __device__ __forceinline__ u64 mix64(u64 z) {
   return z ^ (z >> 31);
 }
 
+__device__ __forceinline__ u64 globaltimer_ns() {
+  u64 t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+bool timing_enabled();  // env PIP_TIMING=1: per-phase timers printed to stderr
+
 // ---------------------------------------------------------------------------
 // warp helpers
 __device__ __forceinline__ u32 lane_id() { return threadIdx.x & 31; }

@@ -37,22 +37,34 @@
 //       are the last ones and wait for every load anyway.
 // Output equals np.sort(a) (values are plain words, so the tie order is
 // invisible; it is fixed here as A before B for the co-ranks).
+#include <cstdio>
+#include <cstdlib>
 #include "sync.cuh"
 
 namespace pip {
 
 static constexpr int MG_THREADS = 512;
+static constexpr int MG_CTAS_PER_SM = 1;
 static constexpr u32 MG_LOGC = 13;
 static constexpr u64 MG_C = 1ull << MG_LOGC;  // words per chunk / output block
 static constexpr int MG_PER_THREAD = (int)(MG_C / MG_THREADS);
+// shared-memory padding: merge-path readers sit ~8 words apart and writers
+// exactly 16 words apart, which on 8-byte words means 16- and 32-way bank
+// conflicts; one pad word per 8 (inputs) / per 16 (outputs) spreads them
+__device__ __forceinline__ u32 SI(u32 l) { return l + (l >> 3); }
+__device__ __forceinline__ u32 SO(u32 r) { return r + (r >> 4); }
+static constexpr u32 MG_IN_WORDS = (u32)(MG_C + MG_C / 8);
+static constexpr u32 MG_OUT_WORDS = (u32)(MG_C + MG_C / 16);
 
 struct MergeGlobal {
   GridSync sync;
   u32 walk_next;  // dynamic walk assignment
   u32 uncut;      // #slots on cut-free cycles
+  u64 t[8];       // %globaltimer at phase boundaries (CTA 0)
 };
 
 struct MergeArgs {
+  u32 dbg;  // profiling knobs (PIP_MERGE_DBG): bit0 skip the dataflow wait, bit1 copy instead of merge
   u64* a;
   u64 n, na, nb;
   u64 hA, hB, KA, KB, K, NB, D, ncuts, L;
@@ -63,6 +75,7 @@ struct MergeArgs {
   u32* jmp[2];    // [K] pointer-jumping jumps
   unsigned char* visited;  // [K]
   u64* cr;        // [NB + 1] A co-rank of every output block boundary
+  ulonglong4* plan;  // [NB] {i0, i1, dest slots of the <= 2 A' and <= 2 B' chunks}
   u32* status;    // [G] per CTA: (last block loaded) + 1
   MergeGlobal* g;
 };
@@ -97,26 +110,39 @@ __device__ __forceinline__ u64 corank2_global(const MergeArgs& M, u64 q) {
   return lo;
 }
 
-__device__ __forceinline__ u32 corank2_smem(const u64* x, u32 nx, const u64* y, u32 ny, u32 q) {
-  u32 lo = q > ny ? q - ny : 0, hi = q < nx ? q : nx;
+// merge path over the padded input buffer: A = logical [0, na), B = [na, na + nb)
+__device__ __forceinline__ u32 corank2_smem(const u64* s, u32 na, u32 nb, u32 q) {
+  u32 lo = q > nb ? q - nb : 0, hi = q < na ? q : na;
   while (lo < hi) {
     const u32 mid = (lo + hi) >> 1;
-    if (x[mid] <= y[q - mid - 1]) lo = mid + 1; else hi = mid;
+    if (s[SI(mid)] <= s[SI(na + q - mid - 1)]) lo = mid + 1; else hi = mid;
   }
   return lo;
 }
 
-// merge sA[0:na) and sB[0:nb) into out[0:na+nb); MG_PER_THREAD outputs each
-__device__ __forceinline__ void block_merge(const u64* sA, u32 na, const u64* sB, u32 nb, u64* out) {
+// merge A and B of the padded input `s` into the padded output `out`;
+// MG_PER_THREAD outputs per thread from its merge-path co-rank; one shared
+// load per output (the consumed side's next key), no data-dependent branches
+__device__ __forceinline__ void block_merge(const u64* s, u32 na, u32 nb, u64* out) {
   const u32 total = na + nb;
   const u32 r0 = threadIdx.x * MG_PER_THREAD;
   if (r0 >= total) return;
-  const u32 r1 = r0 + MG_PER_THREAD < total ? r0 + MG_PER_THREAD : total;
-  u32 i = corank2_smem(sA, na, sB, nb, r0);
+  u32 i = corank2_smem(s, na, nb, r0);
   u32 j = r0 - i;
+  u64 ka = i < na ? s[SI(i)] : ~0ull;
+  u64 kb = j < nb ? s[SI(na + j)] : ~0ull;
+  const u32 r1 = r0 + MG_PER_THREAD < total ? r0 + MG_PER_THREAD : total;
+#pragma unroll 4
   for (u32 r = r0; r < r1; ++r) {
-    if (i < na && (j >= nb || sA[i] <= sB[j])) out[r] = sA[i++];
-    else out[r] = sB[j++];
+    const bool pa = (j >= nb) || (i < na && ka <= kb);  // ties from A
+    out[SO(r)] = pa ? ka : kb;
+    const u32 ni = i + (pa ? 1u : 0u), nj = j + (pa ? 0u : 1u);
+    const bool more = pa ? (ni < na) : (nj < nb);
+    const u64 nk = more ? s[SI(pa ? ni : na + nj)] : ~0ull;
+    ka = pa ? nk : ka;
+    kb = pa ? kb : nk;
+    i = ni;
+    j = nj;
   }
 }
 
@@ -140,17 +166,19 @@ __device__ __forceinline__ u64* slot_ptr(const MergeArgs& M, u64 s) {
   return M.a + M.hA + (s << MG_LOGC);
 }
 
-__global__ void __launch_bounds__(MG_THREADS, 1) merge_kernel(MergeArgs M) {
+__global__ void __launch_bounds__(MG_THREADS, MG_CTAS_PER_SM) merge_kernel(MergeArgs M) {
   extern __shared__ __align__(16) u64 smem[];
-  u64* s_in = smem;               // [C]  A-piece | B-piece
-  u64* s_out = smem + MG_C;       // [C]
-  u64* s_def = smem + 2 * MG_C;   // [C]  block 0, written last
+  u64* s_in = smem;                                  // padded input (A | B)
+  u64* s_def = smem + MG_IN_WORDS;                   // 2nd input buffer / block 0's output
+  u64* s_out = smem + 2 * MG_IN_WORDS;               // padded output
   __shared__ u64 s_misc[2];
   __shared__ int s_flag;
   const u32 b = blockIdx.x, G = gridDim.x, tid = threadIdx.x;
   MergeGlobal* g = M.g;
   u32 gen = 0;
   u64* a = M.a;
+  const bool tm = b == 0 && tid == 0;
+  if (tm) g->t[0] = globaltimer_ns();
 
   // ---------------- P0: slot destinations (sort by chunk last) + co-ranks
   {
@@ -187,14 +215,38 @@ __global__ void __launch_bounds__(MG_THREADS, 1) merge_kernel(MergeArgs M) {
     }
   }
   if (!grid_barrier(&g->sync, gen)) return;
+  if (tm) g->t[1] = globaltimer_ns();
 
-  // ---------------- P0b: save the chunks of the cut slots
+  // ---------------- P0b: per-block load plans; save the chunks of the cut slots
+  {
+    u64 s, e;
+    mpart(M.NB, G, b, s, e);
+    const u64 lb = M.nb - M.hB;
+    for (u64 m = s + tid; m < e; m += MG_THREADS) {
+      const u64 p0 = m * MG_C, p1 = (m + 1) * MG_C < M.n ? (m + 1) * MG_C : M.n;
+      const u64 i0 = __ldcg(M.cr + m), i1 = __ldcg(M.cr + m + 1);
+      const u64 j0 = p0 - i0, j1 = p1 - i1;
+      u32 da0 = 0, da1 = 0, db0 = 0, db1 = 0;
+      const u64 xs = i0 > M.hA ? i0 : M.hA;
+      if (xs < i1) {
+        da0 = __ldcg(M.dest + ((xs - M.hA) >> MG_LOGC));
+        da1 = __ldcg(M.dest + ((i1 - 1 - M.hA) >> MG_LOGC));
+      }
+      const u64 ye = j1 < lb ? j1 : lb;
+      if (j0 < ye) {
+        db0 = __ldcg(M.dest + M.KA + (j0 >> MG_LOGC));
+        db1 = __ldcg(M.dest + M.KA + ((ye - 1) >> MG_LOGC));
+      }
+      M.plan[m] = make_ulonglong4(i0, i1, ((u64)da1 << 32) | da0, ((u64)db1 << 32) | db0);
+    }
+  }
   for (u64 c = b; c < M.ncuts; c += G) {
     const u64 slot = c * M.D;
     if (__ldcg(M.inv + slot) != (u32)slot) move_chunk(M.cut + c * MG_C, slot_ptr(M, slot));
     __syncthreads();
   }
   if (!grid_barrier(&g->sync, gen)) return;
+  if (tm) g->t[2] = globaltimer_ns();
 
   // ---------------- P1: chunk permutation: walk each cycle backwards from a cut
   for (;;) {
@@ -217,6 +269,7 @@ __global__ void __launch_bounds__(MG_THREADS, 1) merge_kernel(MergeArgs M) {
     __syncthreads();
   }
   if (!grid_barrier(&g->sync, gen)) return;
+  if (tm) g->t[3] = globaltimer_ns();
 
   // ---------------- P1b: cycles without a cut (rare; all of them if no cut buffer)
   {
@@ -271,57 +324,207 @@ __global__ void __launch_bounds__(MG_THREADS, 1) merge_kernel(MergeArgs M) {
     if (!grid_barrier(&g->sync, gen)) return;
   }
 
+  if (tm) g->t[4] = globaltimer_ns();
   // ---------------- P2: block merge under the dataflow rule
-  for (u64 m = b; m < M.NB; m += G) {
+  // The inputs of block m are <= 6 contiguous segments (A head in place, <= 2
+  // permuted A' chunks, <= 2 permuted B' chunks, B tail in place).  Each
+  // thread gathers MG_PER_THREAD input words into registers with independent
+  // loads, issued one block ahead so HBM latency overlaps the merge.
+  if (tm) g->t[4] = globaltimer_ns();
+  u64 regs[MG_PER_THREAD];
+  u32 nxt_na = 0, nxt_nb = 0;
+  auto plan_and_load = [&](u64 m, u32& na_out, u32& nb_out) {
     const u64 p0 = m * MG_C, p1 = (m + 1) * MG_C < M.n ? (m + 1) * MG_C : M.n;
-    const u64 i0 = __ldcg(M.cr + m), i1 = __ldcg(M.cr + m + 1);
+    const ulonglong2 pa = __ldcg(reinterpret_cast<const ulonglong2*>(M.plan + m));
+    const ulonglong2 pb = __ldcg(reinterpret_cast<const ulonglong2*>(M.plan + m) + 1);
+    const ulonglong4 pl = make_ulonglong4(pa.x, pa.y, pb.x, pb.y);
+    const u64 i0 = pl.x, i1 = pl.y;
     const u64 j0 = p0 - i0, j1 = p1 - i1;
-    const u32 na = (u32)(i1 - i0), nb = (u32)(j1 - j0);
-    for (u32 k = tid; k < na; k += MG_THREADS) s_in[k] = __ldcg(a + phys_a(M, i0 + k));
-    for (u32 k = tid; k < nb; k += MG_THREADS) s_in[na + k] = __ldcg(a + phys_b(M, j0 + k));
+    const u32 da[2] = {(u32)pl.z, (u32)(pl.z >> 32)};
+    const u32 db[2] = {(u32)pl.w, (u32)(pl.w >> 32)};
+    na_out = (u32)(i1 - i0);
+    nb_out = (u32)(j1 - j0);
+    // <= 6 segments as scalars: loQ = first block index, phQ = physical word
+    u32 lo1 = ~0u, lo2 = ~0u, lo3 = ~0u, lo4 = ~0u, lo5 = ~0u;
+    u64 ph0 = 0, ph1 = 0, ph2 = 0, ph3 = 0, ph4 = 0, ph5 = 0;
+    int ns = 0;
+    u32 pos = 0;
+    auto put = [&](u64 ph, u32 len) {
+      switch (ns) {
+        case 0: ph0 = ph; break;
+        case 1: lo1 = pos; ph1 = ph; break;
+        case 2: lo2 = pos; ph2 = ph; break;
+        case 3: lo3 = pos; ph3 = ph; break;
+        case 4: lo4 = pos; ph4 = ph; break;
+        default: lo5 = pos; ph5 = ph; break;
+      }
+      ++ns;
+      pos += len;
+    };
+    {  // A: head in place, then <= 2 chunk pieces
+      u64 x = i0;
+      const u64 xh = i1 < M.hA ? i1 : M.hA;
+      if (x < xh) { put(x, (u32)(xh - x)); x = xh; }
+      int q = 0;
+      while (x < i1) {
+        const u64 ce = M.hA + (((x - M.hA) >> MG_LOGC) + 1) * MG_C;
+        const u64 e = ce < i1 ? ce : i1;
+        put(M.hA + ((u64)da[q & 1] << MG_LOGC) + ((x - M.hA) & (MG_C - 1)), (u32)(e - x));
+        x = e;
+        ++q;
+      }
+    }
+    {  // B: <= 2 chunk pieces, then the tail in place
+      const u64 lb = M.nb - M.hB;
+      u64 y = j0;
+      int q = 0;
+      while (y < j1 && y < lb) {
+        const u64 ce = ((y >> MG_LOGC) + 1) * MG_C;
+        u64 e = ce < j1 ? ce : j1;
+        if (e > lb) e = lb;
+        put(M.hA + ((u64)db[q & 1] << MG_LOGC) + (y & (MG_C - 1)), (u32)(e - y));
+        y = e;
+        ++q;
+      }
+      if (y < j1) put(M.na + y, (u32)(j1 - y));
+    }
+#pragma unroll
+    for (int r = 0; r < MG_PER_THREAD; ++r) {
+      const u32 k = tid + r * MG_THREADS;
+      u64 ph = ph0;
+      u32 lo = 0;
+      if (k >= lo1) { ph = ph1; lo = lo1; }
+      if (k >= lo2) { ph = ph2; lo = lo2; }
+      if (k >= lo3) { ph = ph3; lo = lo3; }
+      if (k >= lo4) { ph = ph4; lo = lo4; }
+      if (k >= lo5) { ph = ph5; lo = lo5; }
+      regs[r] = k < pos ? __ldcg(a + ph + (k - lo)) : 0ull;
+    }
+  };
+  // wait until every block <= upto has reported loaded
+  auto wait_loaded = [&](u64 upto) -> bool {
+    if (tid < 32) {
+      u64 spins = 0;
+      int ok = 1;
+      for (;;) {
+        bool ready = true;
+        for (u32 c = tid; c < G; c += 32) {
+          if (c > upto) continue;
+          const u64 mc = c + ((upto - c) / G) * G;
+          if (ld_acquire_u32(M.status + c) < mc + 1) ready = false;
+        }
+        if (__all_sync(0xffffffffu, ready)) break;
+        if (tid == 0) {
+          if (++spins > 32) __nanosleep(64);
+          if ((spins & 1023) == 0) {
+            if (ld_relaxed_u32(&g->sync.abort)) ok = 0;
+            else if (spins > (1ull << 25)) { atomicExch(&g->sync.abort, 1u); ok = 0; }
+          }
+        }
+        if (!__shfl_sync(0xffffffffu, ok, 0)) break;
+      }
+      if (tid == 0) s_flag = ok;
+    }
+    __syncthreads();
+    return s_flag != 0;
+  };
+  auto store_block = [&](u64 m, const u64* src) {
+    const u64 p0 = m * MG_C, p1 = (m + 1) * MG_C < M.n ? (m + 1) * MG_C : M.n;
+    const u32 len = (u32)(p1 - p0);
+    if (len == MG_C && (((uintptr_t)(a + p0)) & 15) == 0) {
+      ulonglong2* dst = reinterpret_cast<ulonglong2*>(a + p0);
+#pragma unroll
+      for (int r = 0; r < MG_PER_THREAD / 2; ++r) {
+        const u32 k = tid + r * MG_THREADS;
+        stg_stream2(reinterpret_cast<u64*>(dst + k), src[SO(2 * k)], src[SO(2 * k + 1)]);
+      }
+    } else {
+      for (u32 k = tid; k < len; k += MG_THREADS) a[p0 + k] = src[SO(k)];
+    }
+  };
+  auto publish_loaded = [&](u64 m) {
     __syncthreads();
     if (tid == 0) {
       __threadfence();
       st_release_u32(M.status + b, (u32)(m + 1));
     }
-    u64* out = m == 0 ? s_def : s_out;
-    block_merge(s_in, na, s_in + na, nb, out);
-    if (m != 0) {
-      // every block <= m + L (all blocks, for the tail) must have loaded
-      const u64 upto = m + M.L < M.NB - 1 ? m + M.L : M.NB - 1;
-      if (tid < 32) {
-        u64 spins = 0;
-        int ok = 1;
-        for (;;) {
-          bool ready = true;
-          for (u32 c = tid; c < G; c += 32) {
-            if (c > upto) continue;
-            const u64 mc = c + ((upto - c) / G) * G;
-            if (ld_acquire_u32(M.status + c) < mc + 1) ready = false;
-          }
-          if (__all_sync(0xffffffffu, ready)) break;
-          if (tid == 0) {
-            if (++spins > 32) __nanosleep(64);
-            if ((spins & 1023) == 0) {
-              if (ld_relaxed_u32(&g->sync.abort)) ok = 0;
-              else if (spins > (1ull << 25)) { atomicExch(&g->sync.abort, 1u); ok = 0; }
-            }
-          }
-          if (!__shfl_sync(0xffffffffu, ok, 0)) break;
-        }
-        if (tid == 0) s_flag = ok;
+  };
+  auto stage = [&](u64* dst, u32 cnt) {
+#pragma unroll
+    for (int r = 0; r < MG_PER_THREAD; ++r) {
+      const u32 k = tid + r * MG_THREADS;
+      if (k < cnt) dst[SI(k)] = regs[r];
+    }
+  };
+
+  if (M.hA == 0) {
+    // no in-place head: double-buffered inputs (s_in, s_def), the NEXT block
+    // reports loaded before this block waits to write
+    u64* buf[2] = {s_in, s_def};
+    int cur = 0;
+    u64 m = b;
+    u32 na = 0, nb = 0;
+    if (m < M.NB) {
+      plan_and_load(m, na, nb);
+      stage(buf[0], na + nb);
+      publish_loaded(m);
+      if (m + G < M.NB) plan_and_load(m + G, nxt_na, nxt_nb);
+    }
+    for (; m < M.NB; m += G) {
+      if (M.dbg & 2) {
+        for (u32 k = tid; k < na + nb; k += MG_THREADS) s_out[SO(k)] = buf[cur][SI(k)];
+      } else {
+        block_merge(buf[cur], na, nb, s_out);
       }
+      const bool has_next = m + G < M.NB;
+      if (has_next) {
+        stage(buf[cur ^ 1], nxt_na + nxt_nb);
+        publish_loaded(m + G);
+        if (m + 2 * G < M.NB) {
+          const u32 pa = nxt_na, pb = nxt_nb;
+          plan_and_load(m + 2 * G, nxt_na, nxt_nb);
+          na = pa;
+          nb = pb;
+        } else {
+          na = nxt_na;
+          nb = nxt_nb;
+        }
+      }
+      const u64 upto = m + M.L < M.NB - 1 ? m + M.L : M.NB - 1;
+      if (!(M.dbg & 1) && !wait_loaded(upto)) return;
+      store_block(m, s_out);
       __syncthreads();
-      if (!s_flag) return;
-      for (u32 k = tid; k < (u32)(p1 - p0); k += MG_THREADS) a[p0 + k] = s_out[k];
+      cur ^= 1;
+    }
+    if (tm) g->t[5] = globaltimer_ns();
+    return;
+  }
+
+  // in-place head present: block 0 (the only writer of [0, hA)) is kept in
+  // s_def and written after a final barrier
+  u64 m = b;
+  u32 na = 0, nb = 0;
+  if (m < M.NB) plan_and_load(m, nxt_na, nxt_nb);
+  for (; m < M.NB; m += G) {
+    na = nxt_na;
+    nb = nxt_nb;
+    stage(s_in, na + nb);
+    publish_loaded(m);
+    if (m + G < M.NB) plan_and_load(m + G, nxt_na, nxt_nb);
+    u64* out = m == 0 ? s_def : s_out;
+    block_merge(s_in, na, nb, out);
+    if (m != 0) {
+      const u64 upto = m + M.L < M.NB - 1 ? m + M.L : M.NB - 1;
+      if (!wait_loaded(upto)) return;
+      store_block(m, s_out);
     }
     __syncthreads();
   }
-  // block 0 owns the in-place head: write it once every block has loaded
   if (!grid_barrier(&g->sync, gen)) return;
+  if (tm) g->t[5] = globaltimer_ns();
   if (b == 0) {
     const u64 p1 = MG_C < M.n ? MG_C : M.n;
-    for (u32 k = tid; k < (u32)p1; k += MG_THREADS) a[k] = s_def[k];
+    for (u32 k = tid; k < (u32)p1; k += MG_THREADS) a[k] = s_def[SO(k)];
   }
 }
 
@@ -330,12 +533,12 @@ __global__ void __launch_bounds__(MG_THREADS, 1) merge_kernel(MergeArgs M) {
 __global__ void __launch_bounds__(MG_THREADS, 1) merge_small_kernel(u64* a, u32 n, u32 na) {
   extern __shared__ __align__(16) u64 smem[];
   u64* s_in = smem;
-  u64* s_out = smem + MG_C;
-  for (u32 k = threadIdx.x; k < n; k += MG_THREADS) s_in[k] = a[k];
+  u64* s_out = smem + MG_IN_WORDS;
+  for (u32 k = threadIdx.x; k < n; k += MG_THREADS) s_in[SI(k)] = a[k];
   __syncthreads();
-  block_merge(s_in, na, s_in + na, n - na, s_out);
+  block_merge(s_in, na, n - na, s_out);
   __syncthreads();
-  for (u32 k = threadIdx.x; k < n; k += MG_THREADS) a[k] = s_out[k];
+  for (u32 k = threadIdx.x; k < n; k += MG_THREADS) a[k] = s_out[SO(k)];
 }
 
 // sortedness of both runs (debug=True): counts descents inside each run
@@ -354,7 +557,7 @@ __global__ void check_sorted_kernel(const u64* a, u64 n, u64 na, u32* bad) {
 // host
 
 struct MergeLayout {
-  size_t dest, inv, lab0, lab1, jmp0, jmp1, visited, cr, status, g, cut, total;
+  size_t dest, inv, lab0, lab1, jmp0, jmp1, visited, cr, plan, status, g, cut, total;
   u64 D, ncuts, desc_bytes;
 };
 
@@ -379,6 +582,7 @@ static MergeLayout merge_layout(u64 n, u64 na, u64 budget_words, int grid) {
   L.jmp1 = take(K * 4);
   L.visited = take(K);
   L.cr = take((NB + 1) * 8);
+  L.plan = take(NB * 32);
   L.status = take((size_t)grid * 4);
   L.g = take(sizeof(MergeGlobal));
   L.desc_bytes = off;
@@ -399,7 +603,7 @@ static MergeLayout merge_layout(u64 n, u64 na, u64 budget_words, int grid) {
   return L;
 }
 
-static int merge_grid() { return num_sms(current_device()); }
+static int merge_grid() { return num_sms(current_device()) * MG_CTAS_PER_SM; }
 
 size_t merge_workspace_bytes(u64 n, u64 split, u64 budget_words) {
   if (split > n || n <= MG_C || split == 0 || split == n) return 0;
@@ -425,7 +629,7 @@ int merge_device(u64* a, u64 n, u64 split, int check_sorted, void* ws, size_t ws
   }
   if (n < 2 || split == 0 || split == n) return PIP_OK;
   if (n <= MG_C) {
-    const size_t smem = 2 * MG_C * sizeof(u64);
+    const size_t smem = (MG_IN_WORDS + MG_OUT_WORDS) * sizeof(u64);
     PIP_CUDA(cudaFuncSetAttribute(merge_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)smem));
     merge_small_kernel<<<1, MG_THREADS, smem, st>>>(a, (u32)n, (u32)split);
@@ -448,6 +652,10 @@ int merge_device(u64* a, u64 n, u64 split, int check_sorted, void* ws, size_t ws
   if (((n + MG_C - 1) / MG_C) > 0xffffffffull) return PIP_ERR_UNSUPPORTED;
   char* w = (char*)ws;
   MergeArgs M{};
+  {
+    const char* e = getenv("PIP_MERGE_DBG");
+    M.dbg = e ? (u32)atoi(e) : 0u;
+  }
   M.a = a;
   M.n = n;
   M.na = split;
@@ -470,12 +678,13 @@ int merge_device(u64* a, u64 n, u64 split, int check_sorted, void* ws, size_t ws
   M.jmp[1] = (u32*)(w + L.jmp1);
   M.visited = (unsigned char*)(w + L.visited);
   M.cr = (u64*)(w + L.cr);
+  M.plan = (ulonglong4*)(w + L.plan);
   M.status = (u32*)(w + L.status);
   M.g = (MergeGlobal*)(w + L.g);
   if ((u64)grid <= 2 * M.L) return PIP_ERR_UNSUPPORTED;
   PIP_CUDA(cudaMemsetAsync(M.status, 0, (size_t)grid * 4, st));
   PIP_CUDA(cudaMemsetAsync(M.g, 0, sizeof(MergeGlobal), st));
-  const size_t smem = 3 * MG_C * sizeof(u64);
+  const size_t smem = (2 * MG_IN_WORDS + MG_OUT_WORDS) * sizeof(u64);
   PIP_CUDA(cudaFuncSetAttribute(merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   void* args[] = {&M};
   PIP_CUDA(cudaLaunchCooperativeKernel((const void*)merge_kernel, dim3(grid), dim3(MG_THREADS), args,
@@ -484,6 +693,14 @@ int merge_device(u64* a, u64 n, u64 split, int check_sorted, void* ws, size_t ws
   PIP_CUDA(cudaMemcpyAsync(&gh, M.g, sizeof(gh), cudaMemcpyDeviceToHost, st));
   PIP_CUDA(cudaStreamSynchronize(st));
   if (gh.sync.abort) return PIP_ERR_CUDA;
+  if (timing_enabled())
+    fprintf(stderr,
+            "[pip merge] n=%llu K=%llu ncuts=%llu D=%llu uncut=%u  P0 %.3f ms | cuts %.3f | "
+            "walks %.3f | uncut %.3f | block-merge %.3f ms\n",
+            (unsigned long long)n, (unsigned long long)M.K, (unsigned long long)M.ncuts,
+            (unsigned long long)M.D, gh.uncut, (gh.t[1] - gh.t[0]) * 1e-6,
+            (gh.t[2] - gh.t[1]) * 1e-6, (gh.t[3] - gh.t[2]) * 1e-6, (gh.t[4] - gh.t[3]) * 1e-6,
+            (gh.t[5] - gh.t[4]) * 1e-6);
   return PIP_OK;
 }
 

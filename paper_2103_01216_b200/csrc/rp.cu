@@ -30,6 +30,7 @@
 // target landed in is remembered, so the commit check and the targeted
 // clean are single accesses with no re-probing.  All per-iterate state is
 // 32-bit (n < 2^32 - 1) to halve the workspace traffic.
+#include <cstdio>
 #include <vector>
 #include "sync.cuh"
 
@@ -43,6 +44,7 @@ static constexpr u64 RP_ROUND_CHUNK = 512;  // committed counts per launch
 struct RpGlobal {
   GridSync sync;  // barrier + abort + kernel error (PIP_ERR_*)
   u64 dlo, dhi;
+  u64 t[4];       // ns accumulated per phase by CTA 0 (P1 retire, P2 refill, P3 reserve, P4 commit)
 };
 
 struct RpResume {
@@ -198,6 +200,16 @@ __global__ void __launch_bounds__(RP_THREADS, 4) rp_kernel(RpArgs A) {
   u32 gen = 0;
   u64 rounds_here = 0;
   const bool trace = A.trace != nullptr;
+  const bool tm = b == 0 && tid == 0;
+  u64 tacc[4] = {0, 0, 0, 0};
+  u64 tlast = tm ? globaltimer_ns() : 0;
+  auto tick = [&](int ph) {
+    if (tm) {
+      const u64 now = globaltimer_ns();
+      tacc[ph] += now - tlast;
+      tlast = now;
+    }
+  };
 
   while (!R.done) {
     // ======================= P1: retire previous round =====================
@@ -290,6 +302,7 @@ __global__ void __launch_bounds__(RP_THREADS, 4) rp_kernel(RpArgs A) {
     };
     if (win) count_window();
     if (!grid_barrier(&g->sync, gen)) break;
+    tick(0);
 
     // ======================= P2: refill =====================================
     if (A.debug && !R.first) {
@@ -349,6 +362,7 @@ __global__ void __launch_bounds__(RP_THREADS, 4) rp_kernel(RpArgs A) {
       break;
     }
     if (!grid_barrier(&g->sync, gen)) break;
+    tick(1);
 
     // ======================= P3: reserve ====================================
     const u64 dlo = ld_relaxed_u64(reinterpret_cast<const u64*>(&g->dlo));
@@ -364,7 +378,8 @@ __global__ void __launch_bounds__(RP_THREADS, 4) rp_kernel(RpArgs A) {
         if (V == PIP_RP_FINAL && t >= dlo && t <= dhi) {
           atomicMax(A.dense + (dhi - t), i + 1u);
         } else {
-          if (V == PIP_RP_NAIVE || V == PIP_RP_FLAT) table_reserve(A.table, A.logcap, i, i, claims, &g->sync.error);
+          if (V == PIP_RP_NAIVE || V == PIP_RP_FLAT)
+            table_reserve(A.table, A.logcap, i, i, claims, &g->sync.error);
           sl = table_reserve(A.table, A.logcap, t, i, claims, &g->sync.error);
         }
         A.slot[k] = sl;
@@ -373,6 +388,7 @@ __global__ void __launch_bounds__(RP_THREADS, 4) rp_kernel(RpArgs A) {
       if (tid == 0) A.claimcnt[b] = (u32)c;
     }
     if (!grid_barrier(&g->sync, gen)) break;
+    tick(2);
 
     // ======================= P4: commit + swap ==============================
     {
@@ -423,9 +439,13 @@ __global__ void __launch_bounds__(RP_THREADS, 4) rp_kernel(RpArgs A) {
     R.dhi = dhi;
     R.cursor = cursor;
     if (!grid_barrier(&g->sync, gen)) break;
+    tick(3);
     if (++rounds_here >= A.rounds_limit) break;  // pause: host drains counts
   }
-  if (b == 0 && tid == 0) *A.resume = R;
+  if (b == 0 && tid == 0) {
+    *A.resume = R;
+    for (int i = 0; i < 4; ++i) g->t[i] += tacc[i];
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -616,6 +636,13 @@ int rp_device(u64* a, const u64* h, u64 n, u64 prefix, int variant, int debug,
     // reset the barrier for the next launch
     PIP_CUDA(cudaMemsetAsync(&A.g->sync.bar_count, 0, 8, st));
   }
+  if (timing_enabled())
+    fprintf(stderr,
+            "[pip rp] n=%llu prefix=%llu rounds=%llu grid=%llu  retire+clean+window %.3f ms | "
+            "refill %.3f | reserve %.3f | commit+swap %.3f ms\n",
+            (unsigned long long)n, (unsigned long long)P, (unsigned long long)R.rounds,
+            (unsigned long long)grid, Gh.t[0] * 1e-6, Gh.t[1] * 1e-6, Gh.t[2] * 1e-6,
+            Gh.t[3] * 1e-6);
   S.rounds = R.rounds;
   S.total_committed = R.total_committed;
   S.peak_table_count = R.peak;
