@@ -92,7 +92,12 @@ struct DevPred {
   u32 shift;   // MOD_EQ: post shift
   u32 add;     // MOD_EQ: 65-bit "add" form
   u32 pow2;    // MOD_EQ: divisor is a power of two (use mask a-1)
+  u32 tz;      // MOD_EQ: trailing zeros of the divisor d = 2^tz * d_odd
+  u64 inv;     // MOD_EQ: d_odd^-1 mod 2^64
+  u64 lim;     // MOD_EQ: floor((2^64 - 1) / d_odd)
 };
+// predicate classes the filter kernels are specialised on
+enum : int { PC_MASK = 0, PC_MOD = 1, PC_GEN = 2 };
 DevPred make_dev_pred(const pip_pred& p);
 
 __device__ __forceinline__ u64 fast_div(u64 x, const DevPred& p) {
@@ -121,6 +126,25 @@ __device__ __forceinline__ bool pred_eval(const DevPred& p, u64 x) {
     case PIP_PRED_GE: r = x >= p.a; break;
     case PIP_PRED_EQ: r = x == p.a; break;
     default: r = true; break;
+  }
+  return r != (p.negate != 0);
+}
+
+// class-specialised predicate.  PC_MOD tests x % d == r by divisibility:
+// (x - r) is a multiple of d = 2^tz * d_odd iff its low tz bits are zero and
+// ((x - r) >> tz) * d_odd^-1 (mod 2^64) <= (2^64 - 1) / d_odd — one 64-bit
+// multiply-low and a compare (Granlund & Montgomery).  r < d is guaranteed
+// by the host (r >= d never matches and is mapped to PC_MASK false).
+template <int PC>
+__device__ __forceinline__ bool pred_eval_t(const DevPred& p, u64 x) {
+  bool r;
+  if (PC == PC_MASK) {
+    r = (x & p.a) == p.b;
+  } else if (PC == PC_MOD) {
+    const u64 y = x - p.b;
+    r = (x >= p.b) && ((y & ((1ull << p.tz) - 1ull)) == 0) && ((y >> p.tz) * p.inv <= p.lim);
+  } else {
+    return pred_eval(p, x);
   }
   return r != (p.negate != 0);
 }
@@ -214,6 +238,10 @@ __device__ __forceinline__ void tma_load_1d(void* sdst, const void* gsrc, u32 by
           smem_u32(sdst)),
       "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
+}
+// named barrier over a subset of the CTA's warps (id 1..15)
+__device__ __forceinline__ void named_bar(u32 id, u32 threads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
 __device__ __forceinline__ void mbar_arrive(u64* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");

@@ -103,7 +103,7 @@ __device__ __forceinline__ bool filter_tile_body(const u64 (&x)[16], u32 keep, u
   return true;
 }
 
-template <bool VEC>
+template <bool VEC, int PC>
 __global__ void __launch_bounds__(FILTER_THREADS, 2)
 filter_kernel(u64* __restrict__ a, u64 n, DevPred p, u64* m_out, LookbackCtx c, u64 num_tiles,
               u32* counter, const u64* carry_in, u64* out) {
@@ -124,15 +124,15 @@ filter_kernel(u64* __restrict__ a, u64 n, DevPred p, u64* m_out, LookbackCtx c, 
         x[2 * j + 1] = v.y;
       }
 #pragma unroll
-      for (int k = 0; k < 16; ++k) keep |= (u32)pred_eval(p, x[k]) << k;
+      for (int k = 0; k < 16; ++k) keep |= (u32)pred_eval_t<PC>(p, x[k]) << k;
     } else {
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         const u64 i0 = wbase + 64 * j + 2 * lane;
         x[2 * j] = i0 < n ? a[i0] : 0;
         x[2 * j + 1] = i0 + 1 < n ? a[i0 + 1] : 0;
-        keep |= (u32)(i0 < n && pred_eval(p, x[2 * j])) << (2 * j);
-        keep |= (u32)(i0 + 1 < n && pred_eval(p, x[2 * j + 1])) << (2 * j + 1);
+        keep |= (u32)(i0 < n && pred_eval_t<PC>(p, x[2 * j])) << (2 * j);
+        keep |= (u32)(i0 + 1 < n && pred_eval_t<PC>(p, x[2 * j + 1])) << (2 * j + 1);
       }
     }
     if (!filter_tile_body<FILTER_THREADS>(x, keep, out, tile, m_out, c, num_tiles, s_warp, &s_abort,
@@ -337,6 +337,214 @@ filter_ahead_kernel(u64* __restrict__ a, DevPred p, u64* m_out, LookbackCtx c, u
   }
 }
 
+// Warp-specialized pipeline (see scan_ws_kernel in scan.cu): warp 0 streams
+// tiles in with cp.async.bulk and runs publish / look-back for tile k while
+// the compute warps count tile k (keeping each lane's keep bits) and scatter
+// tile k-1.  The predicate runs once per word.  In-place safety is the same
+// argument as above: a tile's count is published only after its words sit
+// in shared memory, and a tile writes only below its own end.
+template <int NWC, int S, int PC, bool DYN, bool AHEAD = false>
+__global__ void __launch_bounds__(32 * (NWC + 1), 1)
+filter_ws_kernel(u64* __restrict__ a, DevPred p, u64* m_out, LookbackCtx c, u64 num_tiles,
+                 u32* counter) {
+  using O = Op<PIP_OP_ADD>;
+  constexpr u64 TILE = (u64)NWC * 512;
+  constexpr u32 TILE_BYTES = (u32)(TILE * 8);
+  extern __shared__ __align__(128) u64 ring[];
+  __shared__ __align__(8) u64 full[S], reduced[S], pready[S], empty[S];
+  __shared__ u64 s_wtot[S][NWC];
+  __shared__ u64 s_wexc[S][NWC];
+  __shared__ u64 s_agg[S];
+  __shared__ u64 s_prefix[S];
+  __shared__ u32 s_keep[S][NWC * 32];
+  __shared__ int s_abort;
+  __shared__ u64 s_tile[S];  // DYN: tile id of each stage (claimed at issue)
+  const u32 tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const u32 lt = (1u << lane) - 1u;
+  const u64 G = gridDim.x, B = blockIdx.x;
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&reduced[s], 1);
+      mbar_init(&pready[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    s_abort = 0;
+    mbar_fence_init();
+  }
+  __syncthreads();
+  auto issue = [&](u64 k) {
+    const int s = (int)(k % S);
+    const u64 t = DYN ? (u64)atomicAdd(counter, 1u) : B + k * G;
+    s_tile[s] = t;
+    if (DYN && t >= num_tiles) {
+      mbar_arrive(&full[s]);
+      return;
+    }
+    mbar_expect_tx(&full[s], TILE_BYTES);
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      tma_load_1d(ring + s * TILE + q * (TILE / 4), a + t * TILE + q * (TILE / 4), TILE_BYTES / 4,
+                  &full[s]);
+  };
+  if (warp == 0) {
+    if (lane == 0)
+      for (u64 k = 0; k + 1 < (u64)S; ++k)
+        if (DYN || B + k * G < num_tiles) issue(k);
+    __syncwarp();
+    for (u64 k = 0;; ++k) {
+      const int s = (int)(k % S);
+      if (DYN) mbar_wait(&full[s], (u32)((k / S) & 1));  // s_tile[s] is set
+      const u64 t = DYN ? s_tile[s] : B + k * G;
+      if (t >= num_tiles) break;
+      if (AHEAD) {
+        // the aggregate of tile k+1 goes out before tile k looks back
+        const u64 kn = k + 1, tn = DYN ? 0 : B + kn * G;
+        int okn = 1;
+        if (tn < num_tiles) {
+          const int sn = (int)(kn % S);
+          mbar_wait(&reduced[sn], (u32)((kn / S) & 1));
+          if (lane == 0) {
+            okn = publish_begin(c, tn);
+            if (okn) { __threadfence(); publish_agg(c, tn, s_agg[sn]); };
+          }
+          okn = __shfl_sync(0xffffffffu, okn, 0);
+        }
+        if (!okn) {
+          if (lane == 0) {
+            s_abort = 1;
+            mbar_arrive(&pready[s]);
+          }
+          return;
+        }
+      }
+      mbar_wait(&reduced[s], (u32)((k / S) & 1));
+      const u64 agg = s_agg[s];
+      u64 prefix = 0;
+      int ok = 1;
+      if (lane == 0 && (!AHEAD || k == 0)) {
+        ok = publish_begin(c, t);
+        if (ok) {
+          __threadfence();
+          if (t == 0) publish_incl(c, 0, agg);
+          else publish_agg(c, t, agg);
+        }
+      }
+      ok = __shfl_sync(0xffffffffu, ok, 0);
+      if (ok && t > 0) {
+        ok = lookback<O>(c, t, prefix);
+        if (ok && lane == 0) publish_incl(c, t, prefix + agg);
+      }
+      if (lane == 0) {
+        s_prefix[s] = prefix;
+        if (!ok) s_abort = 1;
+        if (ok && t == num_tiles - 1 && m_out) *m_out = prefix + agg;
+        mbar_arrive(&pready[s]);
+      }
+      if (!ok) return;
+      const u64 kk = k + S - 1;
+      if (DYN || B + kk * G < num_tiles) {
+        if (kk >= (u64)S) mbar_wait(&empty[kk % S], (u32)(((kk / S) - 1) & 1));
+        if (lane == 0) {
+          fence_proxy_async_smem();
+          issue(kk);
+        }
+      }
+      __syncwarp();
+    }
+    return;
+  }
+  const u32 w = warp - 1;
+  auto scatter = [&](u64 k) -> bool {
+    const int s = (int)(k % S);
+    mbar_wait(&pready[s], (u32)((k / S) & 1));
+    if (s_abort) return false;
+    u64 run = s_prefix[s] + s_wexc[s][w];
+    const u32 keep = s_keep[s][w * 32 + lane];
+    const u64* src = ring + s * TILE + w * 512;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const bool f0 = (keep >> (2 * j)) & 1u, f1 = (keep >> (2 * j + 1)) & 1u;
+      const u32 m0 = __ballot_sync(0xffffffffu, f0);
+      const u32 m1 = __ballot_sync(0xffffffffu, f1);
+      const u64 r0 = run + __popc(m0 & lt) + __popc(m1 & lt);
+      if (f0 | f1) {
+        const ulonglong2 v = lds2(src + 64 * j + 2 * lane);
+        if (f0) a[r0] = v.x;
+        if (f1) a[r0 + f0] = v.y;
+      }
+      run += __popc(m0) + __popc(m1);
+    }
+    named_bar(1, NWC * 32);
+    if (w == 0 && lane == 0) mbar_arrive(&empty[s]);
+    return true;
+  };
+  auto reduce_tile = [&](u64 k) {
+    const int s = (int)(k % S);
+    mbar_wait(&full[s], (u32)((k / S) & 1));
+    const u64* src = ring + s * TILE + w * 512;
+    u32 keep = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const ulonglong2 v = lds2(src + 64 * j + 2 * lane);
+      keep |= ((u32)pred_eval_t<PC>(p, v.x) << (2 * j)) | ((u32)pred_eval_t<PC>(p, v.y) << (2 * j + 1));
+    }
+    s_keep[s][w * 32 + lane] = keep;
+    const u64 cnt = warp_reduce<O>((u64)__popc(keep));
+    if (lane == 0) s_wtot[s][w] = cnt;
+    named_bar(1, NWC * 32);
+    if (w == 0) {
+      const u64 wv = lane < (u32)NWC ? s_wtot[s][lane] : 0;
+      const u64 winc = warp_incl_scan<O>(wv);
+      if (lane < (u32)NWC) s_wexc[s][lane] = winc - wv;
+      if (lane == NWC - 1) s_agg[s] = winc;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&reduced[s]);
+    }
+  };
+  if (AHEAD && !DYN) {
+    // compute warps run two tiles ahead in reducing: reduce(k+2) after store(k)
+    if (B < num_tiles) reduce_tile(0);
+    if (B + G < num_tiles) reduce_tile(1);
+    for (u64 k = 0; B + k * G < num_tiles; ++k) {
+      if (!scatter(k)) return;
+      if (B + (k + 2) * G < num_tiles) reduce_tile(k + 2);
+    }
+    return;
+  }
+  for (u64 k = 0;; ++k) {
+    const int s = (int)(k % S);
+    if (DYN) mbar_wait(&full[s], (u32)((k / S) & 1));
+    const u64 t = DYN ? s_tile[s] : B + k * G;
+    if (t >= num_tiles) {
+      if (k > 0) scatter(k - 1);
+      break;
+    }
+    if (!DYN) mbar_wait(&full[s], (u32)((k / S) & 1));
+    const u64* src = ring + s * TILE + w * 512;
+    u32 keep = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const ulonglong2 v = lds2(src + 64 * j + 2 * lane);
+      keep |= ((u32)pred_eval_t<PC>(p, v.x) << (2 * j)) | ((u32)pred_eval_t<PC>(p, v.y) << (2 * j + 1));
+    }
+    s_keep[s][w * 32 + lane] = keep;
+    const u64 cnt = warp_reduce<O>((u64)__popc(keep));
+    if (lane == 0) s_wtot[s][w] = cnt;
+    named_bar(1, NWC * 32);
+    if (w == 0) {
+      const u64 wv = lane < (u32)NWC ? s_wtot[s][lane] : 0;
+      const u64 winc = warp_incl_scan<O>(wv);
+      if (lane < (u32)NWC) s_wexc[s][lane] = winc - wv;
+      if (lane == NWC - 1) s_agg[s] = winc;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&reduced[s]);
+    }
+    if (k > 0 && !scatter(k - 1)) return;
+  }
+}
+
+template <int PC>
 __global__ void __launch_bounds__(512)
 count_kernel(const u64* __restrict__ a, u64 n, DevPred p, u64* partials, u32* counter, u64* total) {
   __shared__ u64 s_warp[16];
@@ -348,12 +556,12 @@ count_kernel(const u64* __restrict__ a, u64 n, DevPred p, u64* partials, u32* co
     const u64 npairs = n / 2;
     for (u64 q = (u64)blockIdx.x * blockDim.x + threadIdx.x; q < npairs; q += stride) {
       ulonglong2 v = ldg_stream2(a + 2 * q);
-      t += (u64)pred_eval(p, v.x) + (u64)pred_eval(p, v.y);
+      t += (u64)pred_eval_t<PC>(p, v.x) + (u64)pred_eval_t<PC>(p, v.y);
     }
-    if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) t += pred_eval(p, a[n - 1]);
+    if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) t += pred_eval_t<PC>(p, a[n - 1]);
   } else {
     for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
-      t += pred_eval(p, a[i]);
+      t += pred_eval_t<PC>(p, a[i]);
   }
   t = warp_reduce<Op<PIP_OP_ADD>>(t);
   if (lane_id() == 0) s_warp[warp_id()] = t;
@@ -401,13 +609,33 @@ static ScratchLayoutF carve_f(void* scratch, int sms) {
   return L;
 }
 
+static int pred_class(const DevPred& p) {
+  if (p.kind == PIP_PRED_MASK_EQ) return PC_MASK;
+  if (p.kind == PIP_PRED_MOD_EQ) return PC_MOD;
+  return PC_GEN;
+}
+
+template <bool VEC, int PC>
+static int launch_filter_pc(u64* a, u64 n, const DevPred& p, u64* m_dev, const ScratchLayoutF& L,
+                            cudaStream_t st, int dev, const u64* carry_in, u64* out);
+
 template <bool VEC>
 static int launch_filter(u64* a, u64 n, const DevPred& p, u64* m_dev, const ScratchLayoutF& L,
                          cudaStream_t st, int dev, const u64* carry_in = nullptr,
                          u64* out = nullptr) {
   if (!out) out = a;
+  switch (pred_class(p)) {
+    case PC_MASK: return launch_filter_pc<VEC, PC_MASK>(a, n, p, m_dev, L, st, dev, carry_in, out);
+    case PC_MOD: return launch_filter_pc<VEC, PC_MOD>(a, n, p, m_dev, L, st, dev, carry_in, out);
+    default: return launch_filter_pc<VEC, PC_GEN>(a, n, p, m_dev, L, st, dev, carry_in, out);
+  }
+}
+
+template <bool VEC, int PC>
+static int launch_filter_pc(u64* a, u64 n, const DevPred& p, u64* m_dev, const ScratchLayoutF& L,
+                            cudaStream_t st, int dev, const u64* carry_in, u64* out) {
   const u64 tiles = (n + FILTER_TILE - 1) / FILTER_TILE;
-  auto k = filter_kernel<VEC>;
+  auto k = filter_kernel<VEC, PC>;
   int per_sm = 0;
   PIP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, FILTER_THREADS, 0));
   if (per_sm < 1) return PIP_ERR_UNSUPPORTED;
@@ -479,13 +707,51 @@ static int launch_filter_ahead(u64* a, u64 n, const DevPred& p, u64* m_dev,
   return PIP_OK;
 }
 
+template <int NWC, int S, int PC, bool DYN, bool AHEAD = false>
+static int launch_filter_ws_pc(u64* a, u64 n, const DevPred& p, u64* m_dev,
+                               const ScratchLayoutF& L, cudaStream_t st, int dev) {
+  constexpr u64 TILE = (u64)NWC * 512;
+  constexpr int THREADS = 32 * (NWC + 1);
+  const u64 full_tiles = n / TILE, rem = n - full_tiles * TILE;
+  auto k = filter_ws_kernel<NWC, S, PC, DYN, AHEAD>;
+  const int smem = (int)(S * TILE * 8);
+  PIP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  int per_sm = 0;
+  PIP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, THREADS, smem));
+  if (per_sm < 1) return PIP_ERR_UNSUPPORTED;
+  if (per_sm > 8) per_sm = 8;
+  u64 g = (u64)per_sm * num_sms(dev);
+  if (g > full_tiles) g = full_tiles;
+  int grid = (int)g;
+  u64* mid = rem ? L.carry : m_dev;
+  PIP_CUDA(cudaMemsetAsync(L.abort, 0, 64, st));
+  PIP_CUDA(cudaMemsetAsync(L.slots, 0, sizeof(TileSlot) * 4 * (size_t)grid, st));
+  LookbackCtx c{L.slots, L.abort, (u32)(4 * grid)};
+  DevPred pp = p;
+  u32* counter = L.counter;
+  void* args[] = {&a, &pp, &mid, &c, (void*)&full_tiles, &counter};
+  PIP_CUDA(cudaLaunchCooperativeKernel((const void*)k, dim3(grid), dim3(THREADS), args, smem, st));
+  if (rem) return launch_filter<true>(a + full_tiles * TILE, rem, p, m_dev, L, st, dev, L.carry, a);
+  return PIP_OK;
+}
+
+template <int NWC, int S, bool DYN = false, bool AHEAD = false>
+static int launch_filter_ws(u64* a, u64 n, const DevPred& p, u64* m_dev, const ScratchLayoutF& L,
+                            cudaStream_t st, int dev) {
+  switch (pred_class(p)) {
+    case PC_MASK: return launch_filter_ws_pc<NWC, S, PC_MASK, DYN, AHEAD>(a, n, p, m_dev, L, st, dev);
+    case PC_MOD: return launch_filter_ws_pc<NWC, S, PC_MOD, DYN, AHEAD>(a, n, p, m_dev, L, st, dev);
+    default: return launch_filter_ws_pc<NWC, S, PC_GEN, DYN, AHEAD>(a, n, p, m_dev, L, st, dev);
+  }
+}
+
 static int filter_cfg() {
   static int cfg = -1;
   if (cfg < 0) {
-    // 0 = register path (best measured: the predicate runs once per word);
-    // 4/5 = aggregate-ahead TMA pipeline (evaluates the predicate twice)
+    // 8 = warp-specialized pipeline, 16 compute warps x 3 stages (best
+    // measured); 0 = register path; 4/5 = aggregate-ahead TMA pipeline
     const char* e = getenv("PIP_FILTER_CFG");
-    cfg = e ? atoi(e) : 0;
+    cfg = e ? atoi(e) : 8;
   }
   return cfg;
 }
@@ -505,6 +771,13 @@ int filter_device(u64* a, u64 n, const pip_pred* pred, u64* m_dev, void* scratch
   ScratchLayoutF L = carve_f(scratch, sms);
   const bool vec = ((uintptr_t)a & 15) == 0;
   const int cfg = filter_cfg();
+  if (vec && cfg >= 6 && n >= 8 * FILTER_TILE) {
+    if (cfg == 6) return launch_filter_ws<8, 4>(a, n, p, m_dev, L, st, dev);
+    if (cfg == 7) return launch_filter_ws<8, 3>(a, n, p, m_dev, L, st, dev);
+    if (cfg == 9) return launch_filter_ws<16, 3, true>(a, n, p, m_dev, L, st, dev);
+    if (cfg == 10) return launch_filter_ws<12, 4, false, true>(a, n, p, m_dev, L, st, dev);
+    return launch_filter_ws<16, 3>(a, n, p, m_dev, L, st, dev);
+  }
   if (vec && cfg >= 4 && n >= 4 * FILTER_TILE) {
     if (cfg == 4) return launch_filter_ahead<512, 3>(a, n, p, m_dev, L, st, dev);
     return launch_filter_ahead<256, 3>(a, n, p, m_dev, L, st, dev);
@@ -531,7 +804,11 @@ int count_device(const u64* a, u64 n, const pip_pred* pred, u64* m_dev, void* sc
   u64 need = (n + 1023) / 1024;
   if ((u64)grid > need) grid = (int)(need ? need : 1);
   PIP_CUDA(cudaMemsetAsync(L.abort, 0, 64, st));
-  count_kernel<<<grid, 512, 0, st>>>(a, n, p, L.partials, L.counter, m_dev);
+  switch (pred_class(p)) {
+    case PC_MASK: count_kernel<PC_MASK><<<grid, 512, 0, st>>>(a, n, p, L.partials, L.counter, m_dev); break;
+    case PC_MOD: count_kernel<PC_MOD><<<grid, 512, 0, st>>>(a, n, p, L.partials, L.counter, m_dev); break;
+    default: count_kernel<PC_GEN><<<grid, 512, 0, st>>>(a, n, p, L.partials, L.counter, m_dev); break;
+  }
   PIP_CHECK_LAUNCH();
   return PIP_OK;
 }
@@ -544,6 +821,21 @@ DevPred make_dev_pred(const pip_pred& in) {
   p.negate = in.negate;
   p.a = in.a;
   p.b = in.b;
+  if (in.kind == PIP_PRED_MOD_EQ && in.a >= 1) {
+    if (in.b >= in.a) {  // x % d == r with r >= d never holds
+      p.kind = PIP_PRED_MASK_EQ;
+      p.a = 0;
+      p.b = 1;
+      return p;
+    }
+    u64 d = in.a;
+    p.tz = (u32)__builtin_ctzll(d);
+    const u64 dodd = d >> p.tz;
+    u64 inv = dodd;  // Newton: inv <- inv * (2 - d * inv), 6 steps >= 64 bits
+    for (int i = 0; i < 6; ++i) inv *= 2 - dodd * inv;
+    p.inv = inv;
+    p.lim = ~0ull / dodd;
+  }
   if (in.kind == PIP_PRED_MOD_EQ && in.a >= 1) {
     const u64 d = in.a;
     if ((d & (d - 1)) == 0) {

@@ -378,6 +378,227 @@ scan_ahead_kernel(u64* __restrict__ a, u64 init, const u64* carry_in, u64* total
   }
 }
 
+// Warp-specialized pipeline (16-byte aligned base, whole tiles only).
+// Warp 0 is the producer / look-back warp: it keeps S-1 tiles ahead in flight
+// as cp.async.bulk copies, and for tile k publishes the aggregate, looks back
+// and publishes the inclusive prefix; the NWC compute warps meanwhile reduce
+// tile k and scan + store tile k-1.  The look-back's L2 round trips (the
+// barrier stall of every single-role kernel above, profiles/
+// r01_scan_ahead_summary.txt) leave the compute warps' critical path.
+// Hand-offs are mbarriers: full (TMA bytes landed), reduced (tile aggregate
+// in smem), pready (prefix in smem), empty (stage stored, may be refilled).
+template <int OP, bool INCLUSIVE, int NWC, int S, bool DYN, bool AHEAD = false>
+__global__ void __launch_bounds__(32 * (NWC + 1), 1)
+scan_ws_kernel(u64* __restrict__ a, u64 init, const u64* carry_in, u64* total, LookbackCtx c,
+               u64 num_tiles, u32* counter) {
+  using O = Op<OP>;
+  constexpr u64 TILE = (u64)NWC * 512;
+  constexpr u32 TILE_BYTES = (u32)(TILE * 8);
+  extern __shared__ __align__(128) u64 ring[];
+  __shared__ __align__(8) u64 full[S], reduced[S], pready[S], empty[S];
+  __shared__ u64 s_wtot[S][NWC];
+  __shared__ u64 s_wexc[S][NWC];
+  __shared__ u64 s_agg[S];
+  __shared__ u64 s_prefix[S];
+  __shared__ int s_abort;
+  __shared__ u64 s_tile[S];  // DYN: tile id of each stage (claimed at issue)
+  const u32 tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const u64 G = gridDim.x, B = blockIdx.x;
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&reduced[s], 1);
+      mbar_init(&pready[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    s_abort = 0;
+    mbar_fence_init();
+  }
+  __syncthreads();
+  auto issue = [&](u64 k) {  // one thread: TMA tile k into stage k % S
+    const int s = (int)(k % S);
+    const u64 t = DYN ? (u64)atomicAdd(counter, 1u) : B + k * G;
+    s_tile[s] = t;
+    if (DYN && t >= num_tiles) {
+      mbar_arrive(&full[s]);
+      return;
+    }
+    mbar_expect_tx(&full[s], TILE_BYTES);
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      tma_load_1d(ring + s * TILE + q * (TILE / 4), a + t * TILE + q * (TILE / 4), TILE_BYTES / 4,
+                  &full[s]);
+  };
+
+  if (warp == 0) {
+    // ------------------------------------------------ producer / look-back
+    if (lane == 0)
+      for (u64 k = 0; k + 1 < (u64)S; ++k)
+        if (DYN || B + k * G < num_tiles) issue(k);
+    __syncwarp();
+    for (u64 k = 0;; ++k) {
+      const int s = (int)(k % S);
+      if (DYN) mbar_wait(&full[s], (u32)((k / S) & 1));  // s_tile[s] is set
+      const u64 t = DYN ? s_tile[s] : B + k * G;
+      if (t >= num_tiles) break;
+      if (AHEAD) {
+        // the aggregate of tile k+1 goes out before tile k looks back
+        const u64 kn = k + 1, tn = DYN ? 0 : B + kn * G;
+        int okn = 1;
+        if (tn < num_tiles) {
+          const int sn = (int)(kn % S);
+          mbar_wait(&reduced[sn], (u32)((kn / S) & 1));
+          if (lane == 0) {
+            okn = publish_begin(c, tn);
+            if (okn) publish_agg(c, tn, s_agg[sn]);
+          }
+          okn = __shfl_sync(0xffffffffu, okn, 0);
+        }
+        if (!okn) {
+          if (lane == 0) {
+            s_abort = 1;
+            mbar_arrive(&pready[s]);
+          }
+          return;
+        }
+      }
+      mbar_wait(&reduced[s], (u32)((k / S) & 1));
+      const u64 agg = s_agg[s];
+      u64 prefix = (t == 0 && carry_in) ? *carry_in : O::identity;
+      int ok = 1;
+      if (lane == 0 && (!AHEAD || k == 0)) {
+        ok = publish_begin(c, t);
+        if (ok) {
+          if (t == 0) publish_incl(c, 0, O::apply(prefix, agg));
+          else publish_agg(c, t, agg);
+        }
+      }
+      ok = __shfl_sync(0xffffffffu, ok, 0);
+      if (ok && t > 0) {
+        ok = lookback<O>(c, t, prefix);
+        if (ok && lane == 0) publish_incl(c, t, O::apply(prefix, agg));
+      }
+      if (lane == 0) {
+        s_prefix[s] = prefix;
+        if (!ok) s_abort = 1;
+        if (ok && t == num_tiles - 1 && total) *total = O::apply(prefix, agg);
+        mbar_arrive(&pready[s]);
+      }
+      if (!ok) return;
+      // refill: tile k+S-1 goes into the stage of tile k-1 once that is stored
+      const u64 kk = k + S - 1;
+      if (DYN || B + kk * G < num_tiles) {
+        if (kk >= (u64)S) mbar_wait(&empty[kk % S], (u32)(((kk / S) - 1) & 1));
+        if (lane == 0) {
+          fence_proxy_async_smem();
+          issue(kk);
+        }
+      }
+      __syncwarp();
+    }
+    return;
+  }
+
+  // ---------------------------------------------------- compute warps
+  const u32 w = warp - 1;
+  auto scan_store = [&](u64 k) -> bool {
+    const int s = (int)(k % S);
+    mbar_wait(&pready[s], (u32)((k / S) & 1));
+    if (s_abort) return false;
+    u64 run = O::apply(s_prefix[s], s_wexc[s][w]);
+    const u64* src = ring + s * TILE + w * 512;
+    const u64 wbase = (DYN ? s_tile[s] : B + k * G) * TILE + (u64)w * 512;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const ulonglong2 v = lds2(src + 64 * j + 2 * lane);
+      const u64 x0 = v.x, x1 = v.y;
+      const u64 inc = warp_incl_scan<O>(O::apply(x0, x1));
+      u64 exc = __shfl_up_sync(0xffffffffu, inc, 1);
+      if (lane == 0) exc = O::identity;
+      const u64 tot = __shfl_sync(0xffffffffu, inc, 31);
+      const u64 e = O::apply(run, exc);
+      u64 o0, o1;
+      if (INCLUSIVE) {
+        o0 = O::apply(e, x0);
+        o1 = O::apply(o0, x1);
+      } else {
+        o0 = e;
+        o1 = O::apply(e, x0);
+      }
+      stg_stream2(a + wbase + 64 * j + 2 * lane, O::apply(init, o0), O::apply(init, o1));
+      run = O::apply(run, tot);
+    }
+    named_bar(1, NWC * 32);  // every compute warp has read stage s
+    if (w == 0 && lane == 0) mbar_arrive(&empty[s]);
+    return true;
+  };
+  auto reduce_tile = [&](u64 k) {
+    const int s = (int)(k % S);
+    mbar_wait(&full[s], (u32)((k / S) & 1));
+    const u64* src = ring + s * TILE + w * 512;
+    u64 acc = O::identity;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const ulonglong2 v = lds2(src + 64 * j + 2 * lane);
+      acc = O::apply(acc, O::apply(v.x, v.y));
+    }
+    acc = warp_reduce<O>(acc);
+    if (lane == 0) s_wtot[s][w] = acc;
+    named_bar(1, NWC * 32);
+    if (w == 0) {
+      const u64 wv = lane < (u32)NWC ? s_wtot[s][lane] : O::identity;
+      const u64 winc = warp_incl_scan<O>(wv);
+      u64 wexc = __shfl_up_sync(0xffffffffu, winc, 1);
+      if (lane == 0) wexc = O::identity;
+      if (lane < (u32)NWC) s_wexc[s][lane] = wexc;
+      if (lane == NWC - 1) s_agg[s] = winc;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&reduced[s]);
+    }
+  };
+  if (AHEAD && !DYN) {
+    // compute warps run two tiles ahead in reducing: reduce(k+2) after store(k)
+    if (B < num_tiles) reduce_tile(0);
+    if (B + G < num_tiles) reduce_tile(1);
+    for (u64 k = 0; B + k * G < num_tiles; ++k) {
+      if (!scan_store(k)) return;
+      if (B + (k + 2) * G < num_tiles) reduce_tile(k + 2);
+    }
+    return;
+  }
+  for (u64 k = 0;; ++k) {
+    const int s = (int)(k % S);
+    if (DYN) mbar_wait(&full[s], (u32)((k / S) & 1));
+    const u64 t = DYN ? s_tile[s] : B + k * G;
+    if (t >= num_tiles) {
+      if (k > 0) scan_store(k - 1);
+      break;
+    }
+    if (!DYN) mbar_wait(&full[s], (u32)((k / S) & 1));
+    const u64* src = ring + s * TILE + w * 512;
+    u64 acc = O::identity;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const ulonglong2 v = lds2(src + 64 * j + 2 * lane);
+      acc = O::apply(acc, O::apply(v.x, v.y));
+    }
+    acc = warp_reduce<O>(acc);
+    if (lane == 0) s_wtot[s][w] = acc;
+    named_bar(1, NWC * 32);
+    if (w == 0) {
+      const u64 wv = lane < (u32)NWC ? s_wtot[s][lane] : O::identity;
+      const u64 winc = warp_incl_scan<O>(wv);
+      u64 wexc = __shfl_up_sync(0xffffffffu, winc, 1);
+      if (lane == 0) wexc = O::identity;
+      if (lane < (u32)NWC) s_wexc[s][lane] = wexc;
+      if (lane == NWC - 1) s_agg[s] = winc;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&reduced[s]);
+    }
+    if (k > 0 && !scan_store(k - 1)) return;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // reduce: grid-stride fold, per-CTA partials, last CTA folds the partials.
 template <int OP>
@@ -535,13 +756,45 @@ static int launch_scan_ahead(u64* a, u64 n, u64 init, const u64* carry, u64* tot
   return PIP_OK;
 }
 
+template <int OP, bool INCL, int NWC, int S, bool DYN = false, bool AHEAD = false>
+static int launch_scan_ws(u64* a, u64 n, u64 init, const u64* carry, u64* total,
+                          const ScratchLayout& L, cudaStream_t st, int device) {
+  constexpr u64 TILE = (u64)NWC * 512;
+  constexpr int THREADS = 32 * (NWC + 1);
+  const u64 full_tiles = n / TILE;
+  const u64 rem = n - full_tiles * TILE;
+  auto k = scan_ws_kernel<OP, INCL, NWC, S, DYN, AHEAD>;
+  const int smem = (int)(S * TILE * 8);
+  PIP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  int per_sm = 0;
+  PIP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, THREADS, smem));
+  if (per_sm < 1) return PIP_ERR_UNSUPPORTED;
+  if (per_sm > CTAS_PER_SM_MAX) per_sm = CTAS_PER_SM_MAX;
+  u64 g = (u64)per_sm * num_sms(device);
+  if (g > full_tiles) g = full_tiles;
+  int grid = (int)g;
+  u64* mid = rem ? L.carry : total;
+  PIP_CUDA(cudaMemsetAsync(L.abort, 0, 64, st));
+  PIP_CUDA(cudaMemsetAsync(L.slots, 0, sizeof(TileSlot) * 4 * (size_t)grid, st));
+  LookbackCtx c{L.slots, L.abort, (u32)(4 * grid)};
+  u32* counter = L.counter;
+  void* args[] = {&a, &init, &carry, &mid, &c, (void*)&full_tiles, &counter};
+  PIP_CUDA(cudaLaunchCooperativeKernel((const void*)k, dim3(grid), dim3(THREADS), args, smem, st));
+  if (rem) {
+    u64* tail = a + full_tiles * TILE;
+    return launch_scan_t<OP, INCL, true>(tail, rem, init, L.carry, total, L, st, device);
+  }
+  return PIP_OK;
+}
+
 static int scan_cfg() {
   static int cfg = -1;
   if (cfg < 0) {
-    // 5 = aggregate-ahead TMA pipeline, 256 threads x 3 stages (best measured,
-    // profiles/README.md); 0 = register path; 1-3 = plain TMA rings
+    // 8 = warp-specialized pipeline, 16 compute warps x 3 stages of 64 KiB
+    // (best measured, profiles/r01_scan_ws_summary.txt); 6/7 = smaller WS
+    // variants; 4/5 = aggregate-ahead TMA; 1-3 = plain TMA rings; 0 = registers
     const char* e = getenv("PIP_SCAN_CFG");
-    cfg = e ? atoi(e) : 5;
+    cfg = e ? atoi(e) : 8;
   }
   return cfg;
 }
@@ -551,6 +804,23 @@ static int launch_scan_op(u64* a, u64 n, u64 init, int inclusive, const u64* car
                           const ScratchLayout& L, cudaStream_t st, int device) {
   const bool vec = ((uintptr_t)a & 15) == 0;
   const int cfg = scan_cfg();
+  if (vec && cfg >= 6 && n >= 8 * SCAN_TILE) {
+    if (cfg == 6)
+      return inclusive ? launch_scan_ws<OP, true, 8, 4>(a, n, init, carry, total, L, st, device)
+                       : launch_scan_ws<OP, false, 8, 4>(a, n, init, carry, total, L, st, device);
+    if (cfg == 7)
+      return inclusive ? launch_scan_ws<OP, true, 8, 3>(a, n, init, carry, total, L, st, device)
+                       : launch_scan_ws<OP, false, 8, 3>(a, n, init, carry, total, L, st, device);
+    if (cfg == 9)
+      return inclusive ? launch_scan_ws<OP, true, 16, 3, true>(a, n, init, carry, total, L, st, device)
+                       : launch_scan_ws<OP, false, 16, 3, true>(a, n, init, carry, total, L, st, device);
+    if (cfg == 10)
+      return inclusive
+                 ? launch_scan_ws<OP, true, 12, 4, false, true>(a, n, init, carry, total, L, st, device)
+                 : launch_scan_ws<OP, false, 12, 4, false, true>(a, n, init, carry, total, L, st, device);
+    return inclusive ? launch_scan_ws<OP, true, 16, 3>(a, n, init, carry, total, L, st, device)
+                     : launch_scan_ws<OP, false, 16, 3>(a, n, init, carry, total, L, st, device);
+  }
   if (vec && cfg >= 4 && n >= 4 * SCAN_TILE) {
     if (cfg == 4)
       return inclusive ? launch_scan_ahead<OP, true, 512, 3>(a, n, init, carry, total, L, st, device)
