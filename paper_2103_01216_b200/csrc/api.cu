@@ -85,7 +85,21 @@ struct Event {
   cudaError_t create() { return cudaEventCreateWithFlags(&e, cudaEventDisableTiming); }
 };
 
-static const u64 HOST_CHUNK = 1ull << 26;  // 512 MiB of words per pipeline stage
+// words per pipeline stage of the host-buffer entry points (PIP_HOST_CHUNK_LOG2)
+static u64 host_chunk() {
+  static u64 c = 0;
+  if (!c) {
+    const char* e = getenv("PIP_HOST_CHUNK_LOG2");
+    const int lg = e ? atoi(e) : 24;
+    c = 1ull << (lg >= 16 && lg <= 30 ? lg : 26);
+  }
+  return c;
+}
+static int host_nbuf() {
+  const char* e = getenv("PIP_HOST_NBUF");
+  const int v = e ? atoi(e) : 4;  // 2^24-word chunks x 4 buffers: best measured
+  return v >= 2 && v <= 8 ? v : 4;
+}
 
 // scan over host memory: chunk k is copied in on `cp_in`, scanned on `comp`
 // with the running carry (the previous chunk's inclusive fold) and copied
@@ -97,9 +111,10 @@ int scan_host(u64* host, u64 n, int op, u64 init, int inclusive, u64* total_out,
     if (total_out) *total_out = init;
     return PIP_OK;
   }
+  const u64 HOST_CHUNK = host_chunk();
   const u64 chunk = n < HOST_CHUNK ? n : HOST_CHUNK;
-  const int nb = n > chunk ? 3 : 1;
-  DevBuf bufs[3], scratch, carry;
+  const int nb = n > chunk ? host_nbuf() : 1;
+  DevBuf bufs[8], scratch, carry;
   for (int i = 0; i < nb; ++i) PIP_CUDA(bufs[i].alloc(chunk * 8));
   const size_t sb = scratch_bytes_for(sms);
   PIP_CUDA(scratch.alloc(sb));
@@ -153,9 +168,10 @@ int filter_host(u64* host, u64 n, const pip_pred* pred, u64* m_out, int device) 
     if (m_out) *m_out = 0;
     return PIP_OK;
   }
+  const u64 HOST_CHUNK = host_chunk();
   const u64 chunk = n < HOST_CHUNK ? n : HOST_CHUNK;
-  const int nb = n > chunk ? 3 : 1;
-  DevBuf bufs[3], scratch, counts;
+  const int nb = n > chunk ? host_nbuf() : 1;
+  DevBuf bufs[8], scratch, counts;
   for (int i = 0; i < nb; ++i) PIP_CUDA(bufs[i].alloc(chunk * 8));
   const size_t sb = scratch_bytes_for(sms);
   PIP_CUDA(scratch.alloc(sb));

@@ -130,11 +130,19 @@ int make_swaps(u64* out, u64 lo, u64 count, u64 seed, cudaStream_t st) {
 // ---------------------------------------------------------------------------
 // random 8-byte read-modify-write microbenchmark (the RP roofline: the swap
 // phase touches 2 random 32-byte sectors per committed swap)
-__global__ void random_rmw_kernel(u64* __restrict__ buf, u64 n, u64 updates, u64 seed) {
+__global__ void __launch_bounds__(256)
+random_rmw_kernel(u64* __restrict__ buf, u64 n, u64 updates, u64 seed) {
+  // 8 independent read-modify-writes in flight per thread; index by
+  // multiply-high range reduction (no 64-bit division on the critical path)
   const u64 stride = (u64)gridDim.x * blockDim.x;
-  for (u64 k = (u64)blockIdx.x * blockDim.x + threadIdx.x; k < updates; k += stride) {
-    const u64 i = mix64(seed + k * GOLDEN) % n;
-    buf[i] += 1;
+  for (u64 k = (u64)blockIdx.x * blockDim.x + threadIdx.x; k * 8 < updates; k += stride) {
+    u64 idx[8], v[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) idx[q] = __umul64hi(mix64(seed + (k * 8 + q) * GOLDEN), n);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) v[q] = __ldcg(buf + idx[q]);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) buf[idx[q]] = v[q] + 1;
   }
 }
 
