@@ -61,6 +61,7 @@ struct MergeGlobal {
   u32 walk_next;  // dynamic walk assignment
   u32 uncut;      // #slots on cut-free cycles
   u64 t[8];       // %globaltimer at phase boundaries (CTA 0)
+  u64 sec[6];     // PIP_MERGE_DBG bit2: CTA 0 cycles in stage|load-issue|merge|wait|store|other
 };
 
 struct MergeArgs {
@@ -333,11 +334,18 @@ __global__ void __launch_bounds__(MG_THREADS, MG_CTAS_PER_SM) merge_kernel(Merge
   if (tm) g->t[4] = globaltimer_ns();
   u64 regs[MG_PER_THREAD];
   u32 nxt_na = 0, nxt_nb = 0;
+  // plan records are read one block before they are needed (rec_* below)
+  ulonglong2 rec_a = make_ulonglong2(0, 0), rec_b = make_ulonglong2(0, 0);
+  auto fetch_plan = [&](u64 m) {
+    if (m < M.NB) {
+      rec_a = __ldcg(reinterpret_cast<const ulonglong2*>(M.plan + m));
+      rec_b = __ldcg(reinterpret_cast<const ulonglong2*>(M.plan + m) + 1);
+    }
+  };
   auto plan_and_load = [&](u64 m, u32& na_out, u32& nb_out) {
     const u64 p0 = m * MG_C, p1 = (m + 1) * MG_C < M.n ? (m + 1) * MG_C : M.n;
-    const ulonglong2 pa = __ldcg(reinterpret_cast<const ulonglong2*>(M.plan + m));
-    const ulonglong2 pb = __ldcg(reinterpret_cast<const ulonglong2*>(M.plan + m) + 1);
-    const ulonglong4 pl = make_ulonglong4(pa.x, pa.y, pb.x, pb.y);
+    const ulonglong4 pl = make_ulonglong4(rec_a.x, rec_a.y, rec_b.x, rec_b.y);
+    fetch_plan(m + G);  // the next block's record travels while this one loads
     const u64 i0 = pl.x, i1 = pl.y;
     const u64 j0 = p0 - i0, j1 = p1 - i1;
     const u32 da[2] = {(u32)pl.z, (u32)(pl.z >> 32)};
@@ -401,18 +409,37 @@ __global__ void __launch_bounds__(MG_THREADS, MG_CTAS_PER_SM) merge_kernel(Merge
       regs[r] = k < pos ? __ldcg(a + ph + (k - lo)) : 0ull;
     }
   };
-  // wait until every block <= upto has reported loaded
+  // wait until every block <= upto has reported loaded.  Warp 0 issues the
+  // status loads early (pre_status, before the merge) so that in the common
+  // case the check costs no extra L2 round trip.
+  constexpr int MAXS = 8;  // statuses per lane (G <= 256)
+  u32 st_cache[MAXS];
+  auto pre_status = [&]() {
+    if (tid < 32) {
+#pragma unroll
+      for (int q = 0; q < MAXS; ++q) {
+        const u32 c = tid + 32 * q;
+        st_cache[q] = c < G ? ld_relaxed_u32(M.status + c) : 0xffffffffu;
+      }
+    }
+  };
   auto wait_loaded = [&](u64 upto) -> bool {
     if (tid < 32) {
       u64 spins = 0;
       int ok = 1;
+      bool first = true;
       for (;;) {
         bool ready = true;
-        for (u32 c = tid; c < G; c += 32) {
-          if (c > upto) continue;
+#pragma unroll
+        for (int q = 0; q < MAXS; ++q) {
+          const u32 c = tid + 32 * q;
+          if (c >= G || c > upto) continue;
           const u64 mc = c + ((upto - c) / G) * G;
-          if (ld_acquire_u32(M.status + c) < mc + 1) ready = false;
+          u32 v = st_cache[q];
+          if (!first || v < mc + 1) v = st_cache[q] = ld_acquire_u32(M.status + c);
+          if (v < mc + 1) ready = false;
         }
+        first = false;
         if (__all_sync(0xffffffffu, ready)) break;
         if (tid == 0) {
           if (++spins > 32) __nanosleep(64);
@@ -424,6 +451,7 @@ __global__ void __launch_bounds__(MG_THREADS, MG_CTAS_PER_SM) merge_kernel(Merge
         if (!__shfl_sync(0xffffffffu, ok, 0)) break;
       }
       if (tid == 0) s_flag = ok;
+      fence_gpu();  // acquire: the loads we are about to overwrite have landed
     }
     __syncthreads();
     return s_flag != 0;
@@ -443,11 +471,8 @@ __global__ void __launch_bounds__(MG_THREADS, MG_CTAS_PER_SM) merge_kernel(Merge
     }
   };
   auto publish_loaded = [&](u64 m) {
-    __syncthreads();
-    if (tid == 0) {
-      __threadfence();
-      st_release_u32(M.status + b, (u32)(m + 1));
-    }
+    __syncthreads();  // every thread's loads of block m have landed (data dependency)
+    if (tid == 0) st_release_u32(M.status + b, (u32)(m + 1));
   };
   auto stage = [&](u64* dst, u32 cnt) {
 #pragma unroll
@@ -464,22 +489,36 @@ __global__ void __launch_bounds__(MG_THREADS, MG_CTAS_PER_SM) merge_kernel(Merge
     int cur = 0;
     u64 m = b;
     u32 na = 0, nb = 0;
+    fetch_plan(m);
     if (m < M.NB) {
       plan_and_load(m, na, nb);
       stage(buf[0], na + nb);
       publish_loaded(m);
       if (m + G < M.NB) plan_and_load(m + G, nxt_na, nxt_nb);
     }
+    const bool prof = (M.dbg & 4) && b == 0 && tid == 0;
+    u64 cyc[6] = {0, 0, 0, 0, 0, 0};
+    u64 c0 = clock64();
+    auto mark = [&](int q) {
+      if (prof) {
+        const u64 c1 = clock64();
+        cyc[q] += c1 - c0;
+        c0 = c1;
+      }
+    };
     for (; m < M.NB; m += G) {
+      pre_status();
       if (M.dbg & 2) {
         for (u32 k = tid; k < na + nb; k += MG_THREADS) s_out[SO(k)] = buf[cur][SI(k)];
       } else {
         block_merge(buf[cur], na, nb, s_out);
       }
+      mark(2);
       const bool has_next = m + G < M.NB;
       if (has_next) {
         stage(buf[cur ^ 1], nxt_na + nxt_nb);
         publish_loaded(m + G);
+        mark(0);
         if (m + 2 * G < M.NB) {
           const u32 pa = nxt_na, pb = nxt_nb;
           plan_and_load(m + 2 * G, nxt_na, nxt_nb);
@@ -489,13 +528,18 @@ __global__ void __launch_bounds__(MG_THREADS, MG_CTAS_PER_SM) merge_kernel(Merge
           na = nxt_na;
           nb = nxt_nb;
         }
+        mark(1);
       }
       const u64 upto = m + M.L < M.NB - 1 ? m + M.L : M.NB - 1;
       if (!(M.dbg & 1) && !wait_loaded(upto)) return;
+      mark(3);
       store_block(m, s_out);
       __syncthreads();
+      mark(4);
       cur ^= 1;
     }
+    if (prof)
+      for (int q = 0; q < 6; ++q) g->sec[q] = cyc[q];
     if (tm) g->t[5] = globaltimer_ns();
     return;
   }
@@ -504,6 +548,7 @@ __global__ void __launch_bounds__(MG_THREADS, MG_CTAS_PER_SM) merge_kernel(Merge
   // s_def and written after a final barrier
   u64 m = b;
   u32 na = 0, nb = 0;
+  fetch_plan(m);
   if (m < M.NB) plan_and_load(m, nxt_na, nxt_nb);
   for (; m < M.NB; m += G) {
     na = nxt_na;
@@ -512,6 +557,7 @@ __global__ void __launch_bounds__(MG_THREADS, MG_CTAS_PER_SM) merge_kernel(Merge
     publish_loaded(m);
     if (m + G < M.NB) plan_and_load(m + G, nxt_na, nxt_nb);
     u64* out = m == 0 ? s_def : s_out;
+    pre_status();
     block_merge(s_in, na, nb, out);
     if (m != 0) {
       const u64 upto = m + M.L < M.NB - 1 ? m + M.L : M.NB - 1;
@@ -681,7 +727,7 @@ int merge_device(u64* a, u64 n, u64 split, int check_sorted, void* ws, size_t ws
   M.plan = (ulonglong4*)(w + L.plan);
   M.status = (u32*)(w + L.status);
   M.g = (MergeGlobal*)(w + L.g);
-  if ((u64)grid <= 2 * M.L) return PIP_ERR_UNSUPPORTED;
+  if ((u64)grid <= 2 * M.L || grid > 256) return PIP_ERR_UNSUPPORTED;
   PIP_CUDA(cudaMemsetAsync(M.status, 0, (size_t)grid * 4, st));
   PIP_CUDA(cudaMemsetAsync(M.g, 0, sizeof(MergeGlobal), st));
   const size_t smem = (2 * MG_IN_WORDS + MG_OUT_WORDS) * sizeof(u64);
@@ -693,6 +739,10 @@ int merge_device(u64* a, u64 n, u64 split, int check_sorted, void* ws, size_t ws
   PIP_CUDA(cudaMemcpyAsync(&gh, M.g, sizeof(gh), cudaMemcpyDeviceToHost, st));
   PIP_CUDA(cudaStreamSynchronize(st));
   if (gh.sync.abort) return PIP_ERR_CUDA;
+  if (timing_enabled() && (M.dbg & 4))
+    fprintf(stderr, "[pip merge] CTA0 cycles: merge %llu | stage+publish %llu | plan+load-issue %llu | wait %llu | store %llu\n",
+            (unsigned long long)gh.sec[2], (unsigned long long)gh.sec[0], (unsigned long long)gh.sec[1],
+            (unsigned long long)gh.sec[3], (unsigned long long)gh.sec[4]);
   if (timing_enabled())
     fprintf(stderr,
             "[pip merge] n=%llu K=%llu ncuts=%llu D=%llu uncut=%u  P0 %.3f ms | cuts %.3f | "
