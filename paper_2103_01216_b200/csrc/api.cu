@@ -2,6 +2,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <vector>
 #include "common.cuh"
 
@@ -62,13 +63,62 @@ int merge_device(u64* a, u64 n, u64 split, int check_sorted, void* ws, size_t ws
                  void* scratch, size_t scratch_bytes, cudaStream_t st);
 
 // ---------------------------------------------------------------------------
-// host-buffer helpers: RAII device allocations on a private stream
+// host-buffer helpers: device buffers come from a small per-device caching
+// pool (the *_host entry points would otherwise pay cudaMalloc/cudaFree on
+// every call, which dominates small inputs); RAII returns them to the pool.
+struct PoolBlock {
+  int dev;
+  size_t bytes;
+  void* p;
+};
+static std::mutex g_pool_mu;
+static std::vector<PoolBlock> g_pool;
+static const size_t POOL_KEEP = 16;
+
+static cudaError_t pool_get(size_t bytes, void** out) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  {
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    size_t best = (size_t)-1, bi = 0;
+    for (size_t i = 0; i < g_pool.size(); ++i)
+      if (g_pool[i].dev == dev && g_pool[i].bytes >= bytes && g_pool[i].bytes < best &&
+          g_pool[i].bytes <= 4 * bytes + (1u << 20)) {
+        best = g_pool[i].bytes;
+        bi = i;
+      }
+    if (best != (size_t)-1) {
+      *out = g_pool[bi].p;
+      g_pool.erase(g_pool.begin() + bi);
+      return cudaSuccess;
+    }
+  }
+  return cudaMalloc(out, bytes);
+}
+static void pool_put(void* p, size_t bytes) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  g_pool.push_back({dev, bytes, p});
+  while (g_pool.size() > POOL_KEEP) {  // drop the largest
+    size_t bi = 0;
+    for (size_t i = 1; i < g_pool.size(); ++i)
+      if (g_pool[i].bytes > g_pool[bi].bytes) bi = i;
+    cudaFree(g_pool[bi].p);
+    g_pool.erase(g_pool.begin() + bi);
+  }
+}
+
 struct DevBuf {
   void* p = nullptr;
+  size_t bytes = 0;
   ~DevBuf() {
-    if (p) cudaFree(p);
+    if (p) pool_put(p, bytes);
   }
-  cudaError_t alloc(size_t bytes) { return cudaMalloc(&p, bytes ? bytes : 16); }
+  cudaError_t alloc(size_t b) {
+    bytes = b ? b : 16;
+    return pool_get(bytes, &p);
+  }
 };
 struct Stream {
   cudaStream_t s = nullptr;
