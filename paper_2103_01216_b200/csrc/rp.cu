@@ -52,7 +52,7 @@ struct RpResume {
   u64 fill, rounds, zero_rounds, total_committed, peak, trace_pos, nfail_prev;
   long long cursor;
   u64 dlo, dhi;
-  u32 ping, done, first, pad;
+  u32 ping, done, first, logcap_c;  // logcap_c: BM collided-table size of the last round
 };
 
 struct RpArgs {
@@ -74,7 +74,9 @@ struct RpArgs {
   RpGlobal* g;
   RpResume* resume;
   u32* bmB;  // BM: bit t set <=> some active iterate targets t this round
-  u32* bmC;  // BM: bit t set <=> at least two active iterates target t
+  u32* bmC;  // BM 1: bit t set <=> at least two active iterates target t
+  u32* lc;   // BM 2: per-CTA lists of iterates whose target was already marked
+  u32* lccnt;  // BM: list lengths [G]
   u64 bm_words;
 };
 
@@ -194,13 +196,14 @@ __device__ __forceinline__ bool table_lookup(const u64* table, u32 logcap, u32 k
 }
 
 // ---------------------------------------------------------------------------
-// BM (final variant, budget permitting): reservations by bitmaps.  Almost
-// every target of a round is hit by exactly one iterate; B[t] records "t is
-// targeted" (own check: i may commit only if !B[i]) and C[t] "targeted at
-// least twice".  Only iterates on C targets go through the write-max table,
-// which is therefore small and L2-resident; the target check of everybody
-// else is just !C[t].  Same commit rule, so the same rounds as the reference.
-template <int V, bool BM>
+// BM (final variant, budget permitting): reservations by a bitmap.  Almost
+// every target of a round is hit by exactly one iterate.  B[t] records "t is
+// targeted" (own check: i may commit only if !B[i]); an iterate whose
+// atomicOr finds B[t] already set goes to a per-CTA list, and only those
+// iterates (plus the first marker of their targets) use the write-max table,
+// sized per round for them alone so that it stays L2-resident.  Same commit
+// rule, so the same rounds as the reference.
+template <int V, int BM>
 __global__ void __launch_bounds__(RP_THREADS, 4) rp_kernel(RpArgs A) {
   __shared__ u32 s_cnt[33];
   __shared__ u64 s_red[36];
@@ -272,14 +275,14 @@ __global__ void __launch_bounds__(RP_THREADS, 4) rp_kernel(RpArgs A) {
           if (com) A.trace[R.trace_pos + cbefore + runc + rc] = __ldcg(ids_o + k);
           runc += totc;
         }
-        if ((targeted || BM) && valid) {
+        if ((BM == 1 || (!BM && targeted)) && valid) {
           const u32 sl = __ldcg(A.slot + k);
           if (sl != RP_NOSLOT) A.table[sl] = RP_EMPTY;
         }
         if (BM && valid && F * 256 < A.n) {  // sparse round: clear the touched words
           const u32 t = __ldcg(tg_o + k);
           A.bmB[t >> 5] = 0u;
-          A.bmC[t >> 5] = 0u;
+          if (BM == 1) A.bmC[t >> 5] = 0u;
         }
       }
       R.trace_pos += ncommit;
@@ -288,8 +291,13 @@ __global__ void __launch_bounds__(RP_THREADS, 4) rp_kernel(RpArgs A) {
         part(A.bm_words, G, b, ts, te);
         for (u64 x = ts + tid; x < te; x += T) {
           A.bmB[x] = 0u;
-          A.bmC[x] = 0u;
+          if (BM == 1) A.bmC[x] = 0u;
         }
+      }
+      if (BM == 2 && R.logcap_c) {  // the collided table used only its first 2^logcap_c slots
+        u64 ts, te;
+        part(1ull << R.logcap_c, G, b, ts, te);
+        for (u64 x = ts + tid; x < te; x += T) A.table[x] = RP_EMPTY;
       }
       if (!targeted && !BM) {
         const u64 cap = 1ull << A.logcap;
@@ -343,7 +351,7 @@ __global__ void __launch_bounds__(RP_THREADS, 4) rp_kernel(RpArgs A) {
       if (BM) {
         part(A.bm_words, G, b, ts, te);
         for (u64 x = ts + tid; x < te; x += T)
-          if (__ldcg(A.bmB + x) | __ldcg(A.bmC + x)) atomicExch(&g->sync.error, (u32)PIP_ERR_DEBUG_SWEEP);
+          if (__ldcg(A.bmB + x) | (BM == 1 ? __ldcg(A.bmC + x) : 0u)) atomicExch(&g->sync.error, (u32)PIP_ERR_DEBUG_SWEEP);
       }
     }
     u64 total_ns = 0, wbefore = 0;
@@ -400,10 +408,7 @@ __global__ void __launch_bounds__(RP_THREADS, 4) rp_kernel(RpArgs A) {
       u64 s, e;
       part(newF, G, b, s, e);
       u32 claims = 0;
-      if (BM) {
-        // mark: first toucher of t sets B[t]; later ones also set C[t].  The
-        // reference's table holds the distinct out-of-window targets: count
-        // first touches outside [dlo, dhi] (peak_table_load).
+      if (BM == 1) {
         for (u64 k = s + tid; k < e; k += T) {
           const u32 t = __ldcg(tg_n + k);
           const u32 bit = 1u << (t & 31);
@@ -412,6 +417,23 @@ __global__ void __launch_bounds__(RP_THREADS, 4) rp_kernel(RpArgs A) {
           else if (t < dlo || t > dhi) claims += 1;
           A.slot[k] = RP_NOSLOT;
         }
+      } else if (BM == 2) {
+        // mark: first toucher of t sets B[t]; later ones go to the list.  The
+        // reference's table holds the distinct out-of-window targets: count
+        // first touches outside [dlo, dhi] (peak_table_load).
+        if (tid == 0) s_cnt[32] = 0;
+        __syncthreads();
+        for (u64 k = s + tid; k < e; k += T) {
+          const u32 t = __ldcg(tg_n + k);
+          const u32 bit = 1u << (t & 31);
+          const u32 old = atomicOr(A.bmB + (t >> 5), bit);
+          const bool coll = old & bit;
+          if (coll) A.lc[s + atomicAdd(s_cnt + 32, 1u)] = (u32)(k - s);
+          else if (t < dlo || t > dhi) claims += 1;
+          A.cflag[k] = coll ? 2 : 0;
+        }
+        __syncthreads();
+        if (tid == 0) A.lccnt[b] = s_cnt[32];
       } else {
       for (u64 k = s + tid; k < e; k += T) {
         const u32 i = __ldcg(ids_n + k), t = __ldcg(tg_n + k);
@@ -429,20 +451,126 @@ __global__ void __launch_bounds__(RP_THREADS, 4) rp_kernel(RpArgs A) {
       const u64 c = block_sum(claims, s_red);
       if (tid == 0) A.claimcnt[b] = (u32)c;
     }
-    if (BM) {
-      // collided targets only: write-max reservations in the (small) table
+    if (BM == 1) {
+      // P3b: iterates on targets hit once (no C bit) are their target's only
+      // reserver and commit now; the few on C targets reserve in the
+      // write-max table and are resolved in P4 (cflag 2).
       if (!grid_barrier(&g->sync, gen)) break;
+      tick(2);
+      u64 claims_total, dummy;
+      sum_counts(A.claimcnt, G, b, s_red, claims_total, dummy);
+      if (claims_total > R.peak) R.peak = claims_total;
       u64 s, e;
       part(newF, G, b, s, e);
-      u32 dummy = 0;
+      u32 fails = 0, dclaim = 0;
       for (u64 k = s + tid; k < e; k += T) {
-        const u32 t = __ldcg(tg_n + k);
+        const u32 t = __ldcg(tg_n + k), i = __ldcg(ids_n + k);
         if ((__ldcg(A.bmC + (t >> 5)) >> (t & 31)) & 1u) {
-          const u32 i = __ldcg(ids_n + k);
-          A.slot[k] = table_reserve(A.table, A.logcap, t, i, dummy, &g->sync.error);
+          A.slot[k] = table_reserve(A.table, A.logcap, t, i, dclaim, &g->sync.error);
+          A.cflag[k] = 2;
+        } else {
+          const bool c = !((__ldcg(A.bmB + (i >> 5)) >> (i & 31)) & 1u);
+          A.cflag[k] = c;
+          if (c) {
+            const u64 x = __ldcg(A.a + i), y = __ldcg(A.a + t);
+            A.a[i] = y;
+            A.a[t] = x;
+          } else {
+            fails += 1;
+          }
         }
       }
-    }
+      if (!grid_barrier(&g->sync, gen)) break;
+      for (u64 k = s + tid; k < e; k += T) {
+        if (__ldcg(A.cflag + k) != 2) continue;
+        const u32 t = __ldcg(tg_n + k), i = __ldcg(ids_n + k);
+        const bool own = !((__ldcg(A.bmB + (i >> 5)) >> (i & 31)) & 1u);
+        const u32 sl = __ldcg(A.slot + k);
+        const u64 w = sl == RP_NOSLOT ? RP_EMPTY : __ldcg(A.table + sl);
+        const bool c = own && w != RP_EMPTY && (u32)(w >> 32) == t && (u32)w == i;
+        A.cflag[k] = c;
+        if (c) {
+          const u64 x = __ldcg(A.a + i), y = __ldcg(A.a + t);
+          A.a[i] = y;
+          A.a[t] = x;
+        } else {
+          fails += 1;
+        }
+      }
+      const u64 f = block_sum(fails, s_red);
+      if (tid == 0) A.failcnt[b] = (u32)f;
+    } else if (BM == 2) {
+      // P3b: the iterates that found their target already marked (list lc)
+      // reserve in a write-max table sized for them alone (L2-resident);
+      // then every first marker looks its target up there: absent => it is
+      // the only reserver and commits right away, present => it joins the
+      // write-max and is resolved in the short P4 with the others (cflag 2).
+      if (!grid_barrier(&g->sync, gen)) break;
+      tick(2);
+      u64 claims_total, dummy, lc_total, lc_before;
+      sum_counts(A.claimcnt, G, b, s_red, claims_total, dummy);
+      if (claims_total > R.peak) R.peak = claims_total;
+      sum_counts(A.lccnt, G, b, s_red, lc_total, lc_before);
+      u32 lg = 0;
+      if (lc_total) {
+        lg = 8;
+        while ((1ull << lg) < 2 * lc_total) ++lg;
+        if (lg > A.logcap) lg = A.logcap;
+      }
+      R.logcap_c = lg;
+      u64 s, e;
+      part(newF, G, b, s, e);
+      u32 dclaim = 0;
+      if (lc_total) {
+        const u32 mine = __ldcg(A.lccnt + b);
+        for (u32 q = tid; q < mine; q += T) {
+          const u64 k = s + __ldcg(A.lc + s + q);
+          table_reserve(A.table, lg, __ldcg(tg_n + k), __ldcg(ids_n + k), dclaim, &g->sync.error);
+        }
+        if (!grid_barrier(&g->sync, gen)) break;
+      }
+      u32 fails = 0;
+      for (u64 k = s + tid; k < e; k += T) {
+        if (__ldcg(A.cflag + k)) continue;
+        const u32 t = __ldcg(tg_n + k), i = __ldcg(ids_n + k);
+        u32 v;
+        if (lc_total && table_lookup(A.table, lg, t, v)) {
+          table_reserve(A.table, lg, t, i, dclaim, &g->sync.error);
+          A.cflag[k] = 2;
+          continue;
+        }
+        const bool c = !((__ldcg(A.bmB + (i >> 5)) >> (i & 31)) & 1u);
+        A.cflag[k] = c;
+        if (c) {
+          const u64 x = __ldcg(A.a + i), y = __ldcg(A.a + t);
+          A.a[i] = y;
+          A.a[t] = x;
+        } else {
+          fails += 1;
+        }
+      }
+      if (lc_total) {
+        if (!grid_barrier(&g->sync, gen)) break;
+        // P4: iterates on collided targets
+        for (u64 k = s + tid; k < e; k += T) {
+          if (__ldcg(A.cflag + k) != 2) continue;
+          const u32 t = __ldcg(tg_n + k), i = __ldcg(ids_n + k);
+          const bool own = !((__ldcg(A.bmB + (i >> 5)) >> (i & 31)) & 1u);
+          u32 v = 0;
+          const bool c = own && table_lookup(A.table, lg, t, v) && v == i;
+          A.cflag[k] = c;
+          if (c) {
+            const u64 x = __ldcg(A.a + i), y = __ldcg(A.a + t);
+            A.a[i] = y;
+            A.a[t] = x;
+          } else {
+            fails += 1;
+          }
+        }
+      }
+      const u64 f = block_sum(fails, s_red);
+      if (tid == 0) A.failcnt[b] = (u32)f;
+    } else {
     if (!grid_barrier(&g->sync, gen)) break;
     tick(2);
 
@@ -458,16 +586,7 @@ __global__ void __launch_bounds__(RP_THREADS, 4) rp_kernel(RpArgs A) {
         const u32 i = __ldcg(ids_n + k), t = __ldcg(tg_n + k);
         bool own, tgt;
         u32 v = 0;
-        if (BM) {
-          own = !((__ldcg(A.bmB + (i >> 5)) >> (i & 31)) & 1u);
-          if ((__ldcg(A.bmC + (t >> 5)) >> (t & 31)) & 1u) {
-            const u32 sl = __ldcg(A.slot + k);
-            const u64 w = sl == RP_NOSLOT ? RP_EMPTY : __ldcg(A.table + sl);
-            tgt = w != RP_EMPTY && (u32)(w >> 32) == t && (u32)w == i;
-          } else {
-            tgt = true;
-          }
-        } else if (V == PIP_RP_FINAL && k >= nfail) {
+        if (V == PIP_RP_FINAL && k >= nfail) {
           const u32 dv = __ldcg(A.dense + (dhi - i));
           own = dv == 0 || dv == i + 1u;
         } else if (V == PIP_RP_NAIVE || V == PIP_RP_FLAT) {
@@ -475,8 +594,7 @@ __global__ void __launch_bounds__(RP_THREADS, 4) rp_kernel(RpArgs A) {
         } else {
           own = !table_lookup(A.table, A.logcap, i, v) || v == i;
         }
-        if (BM) {
-        } else if (V == PIP_RP_FINAL && t >= dlo && t <= dhi) {
+        if (V == PIP_RP_FINAL && t >= dlo && t <= dhi) {
           tgt = __ldcg(A.dense + (dhi - t)) == i + 1u;
         } else {
           const u32 sl = __ldcg(A.slot + k);
@@ -495,6 +613,7 @@ __global__ void __launch_bounds__(RP_THREADS, 4) rp_kernel(RpArgs A) {
       }
       const u64 f = block_sum(fails, s_red);
       if (tid == 0) A.failcnt[b] = (u32)f;
+    }
     }
     R.fill = newF;
     R.nfail_prev = nfail;
@@ -519,9 +638,9 @@ __global__ void __launch_bounds__(RP_THREADS, 4) rp_kernel(RpArgs A) {
 
 struct RpLayout {
   size_t ids[2], tg[2], slot, cflag, dense, table, failcnt, wcnt, claimcnt, rcounts, global,
-      resume, bmB, bmC, total;
+      resume, bmB, bmC, lc, lccnt, total;
   u64 bm_words;
-  bool bm;
+  int bm;  // 0 table (+dense window), 1 bitmaps B and C, 2 bitmap B + collided lists
 };
 
 static u64 pow2_at_least(u64 x) {
@@ -532,7 +651,7 @@ static u64 pow2_at_least(u64 x) {
 
 static int rp_gmax() { return num_sms(current_device()) * 4; }
 
-static RpLayout rp_layout_mode(u64 n, u64 prefix, int variant, u64 cap, int gmax, bool bm) {
+static RpLayout rp_layout_mode(u64 n, u64 prefix, int variant, u64 cap, int gmax, int bm) {
   RpLayout L{};
   L.bm = bm;
   size_t off = 0;
@@ -545,7 +664,7 @@ static RpLayout rp_layout_mode(u64 n, u64 prefix, int variant, u64 cap, int gmax
   L.ids[1] = take(prefix * 4);
   L.tg[0] = take(prefix * 4);
   L.tg[1] = take(prefix * 4);
-  L.slot = take(prefix * 4);
+  L.slot = take(bm == 2 ? 0 : prefix * 4);
   L.cflag = take(prefix);
   L.dense = take(variant == PIP_RP_FINAL && !bm ? (prefix + prefix / 4 + 8) * 4 : 0);
   L.table = take(cap * 8);
@@ -557,7 +676,9 @@ static RpLayout rp_layout_mode(u64 n, u64 prefix, int variant, u64 cap, int gmax
   L.resume = take(sizeof(RpResume));
   L.bm_words = bm ? (n + 31) / 32 : 0;
   L.bmB = take(L.bm_words * 4);
-  L.bmC = take(L.bm_words * 4);
+  L.bmC = take(bm == 1 ? L.bm_words * 4 : 0);
+  L.lc = take(bm == 2 ? prefix * 4 : 0);
+  L.lccnt = take(bm == 2 ? (size_t)gmax * 4 : 0);
   L.total = off;
   return L;
 }
@@ -568,15 +689,22 @@ static u64 rp_capacity(u64 prefix, int variant) {
 }
 
 // bitmap reservations for `final` whenever they fit the acceptance gate
-// (workspace <= 8 b(n) words, test_acceptance.py:257); PIP_RP_BM=0/1 forces
+// (workspace <= 8 b(n) words, test_acceptance.py:257).  Mode 1 (bitmaps B
+// and C) while C is small enough to live in L2 (n <= 2^28: one phase less per
+// round); mode 2 (B + collided lists, L2-resident per-round table) above
+// that, where the random C reads would go to HBM.  PIP_RP_BM=0/1/2 forces.
 static RpLayout rp_layout(u64 n, u64 prefix, int variant, u64 cap, int gmax) {
   if (variant == PIP_RP_FINAL) {
-    const RpLayout Lb = rp_layout_mode(n, prefix, variant, cap, gmax, true);
-    bool use = (Lb.total + 7) / 8 <= 8 * prefix;
-    if (const char* e = getenv("PIP_RP_BM")) use = atoi(e) != 0;
-    if (use) return Lb;
+    int want = n <= (1ull << 28) ? 1 : 2;
+    if (const char* e = getenv("PIP_RP_BM")) want = atoi(e);
+    if (want == 1 || want == 2) {
+      const RpLayout Lb = rp_layout_mode(n, prefix, variant, cap, gmax, want);
+      if ((Lb.total + 7) / 8 <= 8 * prefix || getenv("PIP_RP_BM")) return Lb;
+      const RpLayout Lo = rp_layout_mode(n, prefix, variant, cap, gmax, 3 - want);
+      if ((Lo.total + 7) / 8 <= 8 * prefix) return Lo;
+    }
   }
-  return rp_layout_mode(n, prefix, variant, cap, gmax, false);
+  return rp_layout_mode(n, prefix, variant, cap, gmax, 0);
 }
 
 size_t rp_workspace_bytes(u64 n, u64 prefix, int variant) {
@@ -585,7 +713,7 @@ size_t rp_workspace_bytes(u64 n, u64 prefix, int variant) {
   return rp_layout(n, prefix, variant, rp_capacity(prefix, variant), rp_gmax()).total;
 }
 
-template <int V, bool BM = false>
+template <int V, int BM = 0>
 static int rp_run(RpArgs& A, int grid, cudaStream_t st) {
   auto k = rp_kernel<V, BM>;
   void* args[] = {&A};
@@ -657,13 +785,15 @@ int rp_device(u64* a, const u64* h, u64 n, u64 prefix, int variant, int debug,
   A.resume = (RpResume*)(w + Lrun.resume);
   A.bm_words = Lrun.bm_words;
   A.bmB = Lrun.bm ? (u32*)(w + Lrun.bmB) : nullptr;
-  A.bmC = Lrun.bm ? (u32*)(w + Lrun.bmC) : nullptr;
+  A.bmC = Lrun.bm == 1 ? (u32*)(w + Lrun.bmC) : nullptr;
+  A.lc = Lrun.bm == 2 ? (u32*)(w + Lrun.lc) : nullptr;
+  A.lccnt = Lrun.bm == 2 ? (u32*)(w + Lrun.lccnt) : nullptr;
 
   PIP_CUDA(cudaMemsetAsync(A.table, 0xff, cap * 8, st));
   if (variant == PIP_RP_FINAL && !Lrun.bm) PIP_CUDA(cudaMemsetAsync(A.dense, 0, A.span_cap * 4, st));
   if (Lrun.bm) {
     PIP_CUDA(cudaMemsetAsync(A.bmB, 0, Lrun.bm_words * 4, st));
-    PIP_CUDA(cudaMemsetAsync(A.bmC, 0, Lrun.bm_words * 4, st));
+    if (Lrun.bm == 1) PIP_CUDA(cudaMemsetAsync(A.bmC, 0, Lrun.bm_words * 4, st));
   }
   PIP_CUDA(cudaMemsetAsync(A.failcnt, 0, (size_t)gmax * 4, st));
   PIP_CUDA(cudaMemsetAsync(A.g, 0, sizeof(RpGlobal), st));
@@ -677,11 +807,12 @@ int rp_device(u64* a, const u64* h, u64 n, u64 prefix, int variant, int debug,
 
   // grid: enough CTAs to give every thread ~2 iterates, at most co-resident
   int per_sm = 0;
-  const void* kp = variant == PIP_RP_FINAL ? (Lrun.bm ? (const void*)rp_kernel<PIP_RP_FINAL, true>
-                                                      : (const void*)rp_kernel<PIP_RP_FINAL, false>)
-                   : variant == PIP_RP_ONERES ? (const void*)rp_kernel<PIP_RP_ONERES, false>
-                   : variant == PIP_RP_FLAT ? (const void*)rp_kernel<PIP_RP_FLAT, false>
-                                             : (const void*)rp_kernel<PIP_RP_NAIVE, false>;
+  const void* kp = variant == PIP_RP_FINAL ? (Lrun.bm == 1   ? (const void*)rp_kernel<PIP_RP_FINAL, 1>
+                                                 : Lrun.bm == 2 ? (const void*)rp_kernel<PIP_RP_FINAL, 2>
+                                                                : (const void*)rp_kernel<PIP_RP_FINAL, 0>)
+                   : variant == PIP_RP_ONERES ? (const void*)rp_kernel<PIP_RP_ONERES, 0>
+                   : variant == PIP_RP_FLAT ? (const void*)rp_kernel<PIP_RP_FLAT, 0>
+                                             : (const void*)rp_kernel<PIP_RP_NAIVE, 0>;
   PIP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kp, RP_THREADS, 0));
   if (per_sm < 1) return PIP_ERR_UNSUPPORTED;
   if (per_sm > 4) per_sm = 4;
@@ -701,8 +832,9 @@ int rp_device(u64* a, const u64* h, u64 n, u64 prefix, int variant, int debug,
     int rc;
     switch (variant) {
       case PIP_RP_FINAL:
-        rc = Lrun.bm ? rp_run<PIP_RP_FINAL, true>(A, (int)grid, st)
-                     : rp_run<PIP_RP_FINAL, false>(A, (int)grid, st);
+        rc = Lrun.bm == 1   ? rp_run<PIP_RP_FINAL, 1>(A, (int)grid, st)
+             : Lrun.bm == 2 ? rp_run<PIP_RP_FINAL, 2>(A, (int)grid, st)
+                            : rp_run<PIP_RP_FINAL, 0>(A, (int)grid, st);
         break;
       case PIP_RP_ONERES: rc = rp_run<PIP_RP_ONERES>(A, (int)grid, st); break;
       case PIP_RP_FLAT: rc = rp_run<PIP_RP_FLAT>(A, (int)grid, st); break;

@@ -296,3 +296,24 @@ def test_merge_full_range_unsigned(pip):
     t = dev(a)
     pip.relaxed.merge_relaxed(t, len(x))
     assert np.array_equal(host(t), np.sort(a))
+
+
+@pytest.mark.parametrize("mode", ["0", "1", "2"])
+@pytest.mark.parametrize("n,seed,frac,debug", [(100_000, 55, 0.02, False), (1_000_000, 1, 0.02, False),
+                                               (20_000, 3, 1e-12, True), (3000, 0, 0.05, True)])
+def test_rp_reservation_modes(pip, orc, monkeypatch, mode, n, seed, frac, debug):
+    # PIP_RP_BM forces the device reservation scheme: 0 hash table + dense
+    # window, 1 bitmaps B/C, 2 bitmap B + collided lists.  All must reproduce
+    # the reference's rounds exactly (relaxed.py:176-227).
+    monkeypatch.setenv("PIP_RP_BM", mode)
+    h = (np.zeros(n, dtype=np.uint64) if seed == 0
+         else pip.relaxed.make_swap_sequence(n, pip.Rng(seed)))
+    budget = pip.EpsilonConfig(0.5, frac)
+    a = dev(np.arange(n, dtype=np.uint64))
+    st = pip.relaxed.random_permutation(a, dev(h), "final", budget, debug=debug)
+    b = np.arange(n, dtype=np.uint64)
+    ref = orc.ref_random_permutation(b, h, budget.prefix_words(n), "final", threads=8)
+    assert np.array_equal(host(a), b)
+    assert st.rounds == ref["rounds"]
+    assert st.committed_per_round == ref["committed_per_round"]
+    assert st.peak_table_load == ref["peak_count"] / ref["capacity"]
