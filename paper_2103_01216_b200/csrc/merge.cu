@@ -55,6 +55,8 @@ __device__ __forceinline__ u32 SI(u32 l) { return l + (l >> 3); }
 __device__ __forceinline__ u32 SO(u32 r) { return r + (r >> 4); }
 static constexpr u32 MG_IN_WORDS = (u32)(MG_C + MG_C / 8);
 static constexpr u32 MG_OUT_WORDS = (u32)(MG_C + MG_C / 16);
+static constexpr u32 MG_STAGE_WORDS = (u32)(MG_C + 16);  // bulk-copy staging (+2 junk words x 6 segments)
+static constexpr size_t MG_SMEM = (size_t)(MG_STAGE_WORDS + MG_IN_WORDS + MG_C) * 8;
 
 struct MergeGlobal {
   GridSync sync;
@@ -169,9 +171,7 @@ __device__ __forceinline__ u64* slot_ptr(const MergeArgs& M, u64 s) {
 
 __global__ void __launch_bounds__(MG_THREADS, MG_CTAS_PER_SM) merge_kernel(MergeArgs M) {
   extern __shared__ __align__(16) u64 smem[];
-  u64* s_in = smem;                                  // padded input (A | B)
-  u64* s_def = smem + MG_IN_WORDS;                   // 2nd input buffer / block 0's output
-  u64* s_out = smem + 2 * MG_IN_WORDS;               // padded output
+  u64* s_out = smem;  // P1b: one chunk in transit
   __shared__ u64 s_misc[2];
   __shared__ int s_flag;
   const u32 b = blockIdx.x, G = gridDim.x, tid = threadIdx.x;
@@ -327,14 +327,23 @@ __global__ void __launch_bounds__(MG_THREADS, MG_CTAS_PER_SM) merge_kernel(Merge
 
   if (tm) g->t[4] = globaltimer_ns();
   // ---------------- P2: block merge under the dataflow rule
-  // The inputs of block m are <= 6 contiguous segments (A head in place, <= 2
-  // permuted A' chunks, <= 2 permuted B' chunks, B tail in place).  Each
-  // thread gathers MG_PER_THREAD input words into registers with independent
-  // loads, issued one block ahead so HBM latency overlaps the merge.
-  if (tm) g->t[4] = globaltimer_ns();
-  u64 regs[MG_PER_THREAD];
-  u32 nxt_na = 0, nxt_nb = 0;
-  // plan records are read one block before they are needed (rec_* below)
+  // Global traffic goes through the TMA engine only, so the SM's load/store
+  // pipe is left to the shared-memory merge:
+  //   load   the <= 6 contiguous input segments of block m + 2G (A head in
+  //          place, <= 2 permuted A' chunks, <= 2 permuted B' chunks, B tail
+  //          in place) with one bulk copy each into the staging buffer (each
+  //          widened to 16-byte alignment: <= 2 junk words per segment);
+  //   copy   staging -> the padded merge buffer (bank-conflict-free layout);
+  //   merge  MG_PER_THREAD consecutive outputs per thread into registers;
+  //   stage  registers -> the contiguous output buffer (pairs rotated by
+  //          lane so 16-byte shared stores hit distinct banks);
+  //   store  one bulk copy to a[mC, (m+1)C) once every block <= m + L has
+  //          reported its inputs loaded (the dataflow rule).
+  u64* s_stage = smem;                                 // MG_STAGE_WORDS
+  u64* s_pad = smem + MG_STAGE_WORDS;                  // MG_IN_WORDS, padded
+  u64* s_outc = smem + MG_STAGE_WORDS + MG_IN_WORDS;   // MG_C, contiguous
+  __shared__ __align__(8) u64 s_bar;
+  __shared__ u32 s_seg[2 + 2 * 6];  // na, nb | lo[6] | staging index[6]
   ulonglong2 rec_a = make_ulonglong2(0, 0), rec_b = make_ulonglong2(0, 0);
   auto fetch_plan = [&](u64 m) {
     if (m < M.NB) {
@@ -342,42 +351,28 @@ __global__ void __launch_bounds__(MG_THREADS, MG_CTAS_PER_SM) merge_kernel(Merge
       rec_b = __ldcg(reinterpret_cast<const ulonglong2*>(M.plan + m) + 1);
     }
   };
-  auto plan_and_load = [&](u64 m, u32& na_out, u32& nb_out) {
+  // thread 0: the segments of block m, their bulk copies, the plan in s_seg
+  auto issue_load = [&](u64 m) {
     const u64 p0 = m * MG_C, p1 = (m + 1) * MG_C < M.n ? (m + 1) * MG_C : M.n;
     const ulonglong4 pl = make_ulonglong4(rec_a.x, rec_a.y, rec_b.x, rec_b.y);
-    fetch_plan(m + G);  // the next block's record travels while this one loads
+    fetch_plan(m + G);
     const u64 i0 = pl.x, i1 = pl.y;
     const u64 j0 = p0 - i0, j1 = p1 - i1;
     const u32 da[2] = {(u32)pl.z, (u32)(pl.z >> 32)};
     const u32 db[2] = {(u32)pl.w, (u32)(pl.w >> 32)};
-    na_out = (u32)(i1 - i0);
-    nb_out = (u32)(j1 - j0);
-    // <= 6 segments as scalars: loQ = first block index, phQ = physical word
-    u32 lo1 = ~0u, lo2 = ~0u, lo3 = ~0u, lo4 = ~0u, lo5 = ~0u;
-    u64 ph0 = 0, ph1 = 0, ph2 = 0, ph3 = 0, ph4 = 0, ph5 = 0;
+    u64 ph[6];
+    u32 len[6];
     int ns = 0;
-    u32 pos = 0;
-    auto put = [&](u64 ph, u32 len) {
-      switch (ns) {
-        case 0: ph0 = ph; break;
-        case 1: lo1 = pos; ph1 = ph; break;
-        case 2: lo2 = pos; ph2 = ph; break;
-        case 3: lo3 = pos; ph3 = ph; break;
-        case 4: lo4 = pos; ph4 = ph; break;
-        default: lo5 = pos; ph5 = ph; break;
-      }
-      ++ns;
-      pos += len;
-    };
     {  // A: head in place, then <= 2 chunk pieces
       u64 x = i0;
       const u64 xh = i1 < M.hA ? i1 : M.hA;
-      if (x < xh) { put(x, (u32)(xh - x)); x = xh; }
+      if (x < xh) { ph[ns] = x; len[ns++] = (u32)(xh - x); x = xh; }
       int q = 0;
       while (x < i1) {
         const u64 ce = M.hA + (((x - M.hA) >> MG_LOGC) + 1) * MG_C;
         const u64 e = ce < i1 ? ce : i1;
-        put(M.hA + ((u64)da[q & 1] << MG_LOGC) + ((x - M.hA) & (MG_C - 1)), (u32)(e - x));
+        ph[ns] = M.hA + ((u64)da[q & 1] << MG_LOGC) + ((x - M.hA) & (MG_C - 1));
+        len[ns++] = (u32)(e - x);
         x = e;
         ++q;
       }
@@ -390,23 +385,55 @@ __global__ void __launch_bounds__(MG_THREADS, MG_CTAS_PER_SM) merge_kernel(Merge
         const u64 ce = ((y >> MG_LOGC) + 1) * MG_C;
         u64 e = ce < j1 ? ce : j1;
         if (e > lb) e = lb;
-        put(M.hA + ((u64)db[q & 1] << MG_LOGC) + (y & (MG_C - 1)), (u32)(e - y));
+        ph[ns] = M.hA + ((u64)db[q & 1] << MG_LOGC) + (y & (MG_C - 1));
+        len[ns++] = (u32)(e - y);
         y = e;
         ++q;
       }
-      if (y < j1) put(M.na + y, (u32)(j1 - y));
+      if (y < j1) { ph[ns] = M.na + y; len[ns++] = (u32)(j1 - y); }
+    }
+    u32 bytes[6], total = 0, E = 0, lo = 0;
+    for (int k = 0; k < ns; ++k) {
+      const u32 par = (u32)(((uintptr_t)(a + ph[k]) >> 3) & 1u);
+      bytes[k] = ((par + len[k]) * 8u + 15u) & ~15u;
+      total += bytes[k];
+    }
+    mbar_expect_tx(&s_bar, total);
+    s_seg[0] = (u32)(i1 - i0);
+    s_seg[1] = (u32)(j1 - j0);
+    for (int k = 0; k < 6; ++k) {
+      if (k < ns) {
+        const u32 par = (u32)(((uintptr_t)(a + ph[k]) >> 3) & 1u);
+        tma_load_1d(s_stage + E, a + ph[k] - par, bytes[k], &s_bar);
+        s_seg[2 + k] = lo;
+        s_seg[8 + k] = E + par;
+        E += bytes[k] / 8;
+        lo += len[k];
+      } else {
+        s_seg[2 + k] = 0xffffffffu;
+        s_seg[8 + k] = 0;
+      }
+    }
+  };
+  // all threads: staging -> padded merge buffer (plan in s_seg)
+  auto copy_in = [&](u32& na_out, u32& nb_out) {
+    na_out = s_seg[0];
+    nb_out = s_seg[1];
+    const u32 cnt = na_out + nb_out;
+    u32 lo[6], si[6];
+#pragma unroll
+    for (int k = 0; k < 6; ++k) {
+      lo[k] = s_seg[2 + k];
+      si[k] = s_seg[8 + k];
     }
 #pragma unroll
     for (int r = 0; r < MG_PER_THREAD; ++r) {
-      const u32 k = tid + r * MG_THREADS;
-      u64 ph = ph0;
-      u32 lo = 0;
-      if (k >= lo1) { ph = ph1; lo = lo1; }
-      if (k >= lo2) { ph = ph2; lo = lo2; }
-      if (k >= lo3) { ph = ph3; lo = lo3; }
-      if (k >= lo4) { ph = ph4; lo = lo4; }
-      if (k >= lo5) { ph = ph5; lo = lo5; }
-      regs[r] = k < pos ? __ldcg(a + ph + (k - lo)) : 0ull;
+      const u32 x = tid + r * MG_THREADS;
+      u32 base = si[0];
+#pragma unroll
+      for (int k = 1; k < 6; ++k)
+        if (x >= lo[k]) base = si[k] - lo[k];
+      if (x < cnt) s_pad[SI(x)] = s_stage[base + x];
     }
   };
   // wait until every block <= upto has reported loaded.  Warp 0 issues the
@@ -451,127 +478,159 @@ __global__ void __launch_bounds__(MG_THREADS, MG_CTAS_PER_SM) merge_kernel(Merge
         if (!__shfl_sync(0xffffffffu, ok, 0)) break;
       }
       if (tid == 0) s_flag = ok;
-      fence_gpu();  // acquire: the loads we are about to overwrite have landed
+      fence_gpu();  // acquire: the reads of the words we are about to overwrite are done
     }
     __syncthreads();
     return s_flag != 0;
   };
-  auto store_block = [&](u64 m, const u64* src) {
+  // merge-path co-rank, then MG_PER_THREAD steps with one shared load each
+  auto merge_regs = [&](u32 na, u32 nb, u64 (&o)[MG_PER_THREAD]) {
+    const u64* sp = smem + MG_STAGE_WORDS;  // s_pad, derived from smem (LDS)
+    const u32 total = na + nb;
+    const u32 r0 = tid * MG_PER_THREAD;
+    if (r0 >= total) return;
+    u32 i = corank2_smem(sp, na, nb, r0);
+    u32 j = r0 - i;
+    u64 ka = i < na ? sp[SI(i)] : ~0ull;
+    u64 kb = j < nb ? sp[SI(na + j)] : ~0ull;
+#pragma unroll
+    for (int q = 0; q < MG_PER_THREAD; ++q) {
+      const bool pa = (j >= nb) || (i < na && ka <= kb);  // ties from A
+      o[q] = pa ? ka : kb;
+      const u32 ni = i + (pa ? 1u : 0u), nj = j + (pa ? 0u : 1u);
+      const bool more = pa ? (ni < na) : (nj < nb);
+      const u64 nk = more ? sp[SI(pa ? ni : na + nj)] : ~0ull;
+      ka = pa ? nk : ka;
+      kb = pa ? kb : nk;
+      i = ni;
+      j = nj;
+    }
+  };
+  // registers -> contiguous s_outc: pair q of thread t goes to 16-byte slot
+  // 8t + q; issuing the pairs rotated by t mod 8 spreads a warp's stores over
+  // all bank groups (4 wavefronts per 512 bytes, the minimum)
+  auto stage_out = [&](u64 (&o)[MG_PER_THREAD]) {
+    static_assert(MG_PER_THREAD == 16, "pair rotation assumes 8 pairs");
+    const u32 rot = tid & 7;
+#pragma unroll
+    for (int bit = 0; bit < 3; ++bit) {
+      const int sh = 1 << bit;
+      if (rot & sh) {
+        u64 t[MG_PER_THREAD];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          t[2 * q] = o[2 * ((q + sh) & 7)];
+          t[2 * q + 1] = o[2 * ((q + sh) & 7) + 1];
+        }
+#pragma unroll
+        for (int q = 0; q < MG_PER_THREAD; ++q) o[q] = t[q];
+      }
+    }
+    ulonglong2* dst = reinterpret_cast<ulonglong2*>(smem + MG_STAGE_WORDS + MG_IN_WORDS);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) dst[8 * tid + ((q + rot) & 7)] = make_ulonglong2(o[2 * q], o[2 * q + 1]);
+  };
+  // thread 0: s_outc[0, len) -> a[p0, p0 + len) (16-byte-aligned middle by
+  // the TMA engine, <= 1 word at either end by hand)
+  auto store_out = [&](u64 m) {
     const u64 p0 = m * MG_C, p1 = (m + 1) * MG_C < M.n ? (m + 1) * MG_C : M.n;
     const u32 len = (u32)(p1 - p0);
-    if (len == MG_C && (((uintptr_t)(a + p0)) & 15) == 0) {
-      ulonglong2* dst = reinterpret_cast<ulonglong2*>(a + p0);
-#pragma unroll
-      for (int r = 0; r < MG_PER_THREAD / 2; ++r) {
-        const u32 k = tid + r * MG_THREADS;
-        stg_stream2(reinterpret_cast<u64*>(dst + k), src[SO(2 * k)], src[SO(2 * k + 1)]);
-      }
-    } else {
-      for (u32 k = tid; k < len; k += MG_THREADS) a[p0 + k] = src[SO(k)];
+    const u32 head = (u32)(((uintptr_t)(a + p0) >> 3) & 1u);
+    const u32 body = len > head ? ((len - head) & ~1u) : 0u;
+    if (head && len) a[p0] = s_outc[0];
+    if (head + body < len) a[p0 + len - 1] = s_outc[len - 1];
+    if (body) {
+      tma_store_1d(a + p0 + head, s_outc + head, body * 8u);
+      bulk_commit();
     }
+  };
+  auto store_regs = [&](u64 m, const u64 (&o)[MG_PER_THREAD]) {
+    const u64 p0 = m * MG_C, p1 = (m + 1) * MG_C < M.n ? (m + 1) * MG_C : M.n;
+    const u32 len = (u32)(p1 - p0), r0 = tid * MG_PER_THREAD;
+#pragma unroll
+    for (int q = 0; q < MG_PER_THREAD; ++q)
+      if (r0 + q < len) a[p0 + r0 + q] = o[q];
   };
   auto publish_loaded = [&](u64 m) {
-    __syncthreads();  // every thread's loads of block m have landed (data dependency)
     if (tid == 0) st_release_u32(M.status + b, (u32)(m + 1));
   };
-  auto stage = [&](u64* dst, u32 cnt) {
-#pragma unroll
-    for (int r = 0; r < MG_PER_THREAD; ++r) {
-      const u32 k = tid + r * MG_THREADS;
-      if (k < cnt) dst[SI(k)] = regs[r];
+
+  const bool prof = (M.dbg & 4) && b == 0 && tid == 0;
+  u64 cyc[6] = {0, 0, 0, 0, 0, 0};
+  u64 c0 = clock64();
+  auto mark = [&](int q) {
+    if (prof) {
+      const u64 c1 = clock64();
+      cyc[q] += c1 - c0;
+      c0 = c1;
     }
   };
-
-  if (M.hA == 0) {
-    // no in-place head: double-buffered inputs (s_in, s_def), the NEXT block
-    // reports loaded before this block waits to write
-    u64* buf[2] = {s_in, s_def};
-    int cur = 0;
-    u64 m = b;
-    u32 na = 0, nb = 0;
-    fetch_plan(m);
-    if (m < M.NB) {
-      plan_and_load(m, na, nb);
-      stage(buf[0], na + nb);
-      publish_loaded(m);
-      if (m + G < M.NB) plan_and_load(m + G, nxt_na, nxt_nb);
+  // CTA 0 keeps block 0's output (it overwrites the in-place head, which any
+  // block may still read) in s_outc until the end and stores its other
+  // blocks from registers
+  const bool keep0 = M.hA > 0 && b == 0;
+  u32 phase = 0;
+  if (tid == 0) {
+    mbar_init(&s_bar, 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  u64 m = b;
+  u32 na = 0, nb = 0;
+  if (tid == 0) fetch_plan(m);
+  if (m < M.NB) {
+    if (tid == 0) issue_load(m);
+    mbar_wait(&s_bar, phase);
+    phase ^= 1;
+    __syncthreads();  // s_seg visible
+    copy_in(na, nb);
+    publish_loaded(m);
+    __syncthreads();  // staging free
+    if (tid == 0 && m + G < M.NB) issue_load(m + G);
+  }
+  for (; m < M.NB; m += G) {
+    pre_status();
+    u64 o[MG_PER_THREAD];
+    merge_regs(na, nb, o);
+    mark(2);
+    const bool regs_path = keep0 && m != 0;
+    if (!regs_path) {
+      if (tid == 0) bulk_wait_read_all();  // the previous store has read s_outc
+      __syncthreads();
+      stage_out(o);
+      fence_proxy_async_smem();
     }
-    const bool prof = (M.dbg & 4) && b == 0 && tid == 0;
-    u64 cyc[6] = {0, 0, 0, 0, 0, 0};
-    u64 c0 = clock64();
-    auto mark = [&](int q) {
-      if (prof) {
-        const u64 c1 = clock64();
-        cyc[q] += c1 - c0;
-        c0 = c1;
-      }
-    };
-    for (; m < M.NB; m += G) {
-      pre_status();
-      if (M.dbg & 2) {
-        for (u32 k = tid; k < na + nb; k += MG_THREADS) s_out[SO(k)] = buf[cur][SI(k)];
-      } else {
-        block_merge(buf[cur], na, nb, s_out);
-      }
-      mark(2);
-      const bool has_next = m + G < M.NB;
-      if (has_next) {
-        stage(buf[cur ^ 1], nxt_na + nxt_nb);
-        publish_loaded(m + G);
-        mark(0);
-        if (m + 2 * G < M.NB) {
-          const u32 pa = nxt_na, pb = nxt_nb;
-          plan_and_load(m + 2 * G, nxt_na, nxt_nb);
-          na = pa;
-          nb = pb;
-        } else {
-          na = nxt_na;
-          nb = nxt_nb;
-        }
-        mark(1);
-      }
+    __syncthreads();  // merge inputs consumed; s_outc complete
+    mark(0);
+    if (m + G < M.NB) {
+      mbar_wait(&s_bar, phase);
+      phase ^= 1;
+      copy_in(na, nb);
+      publish_loaded(m + G);
+      __syncthreads();  // staging free, s_pad holds block m + G
+      if (tid == 0 && m + 2 * G < M.NB) issue_load(m + 2 * G);
+    }
+    mark(1);
+    if (!(keep0 && m == 0)) {
       const u64 upto = m + M.L < M.NB - 1 ? m + M.L : M.NB - 1;
       if (!(M.dbg & 1) && !wait_loaded(upto)) return;
       mark(3);
-      store_block(m, s_out);
-      __syncthreads();
+      if (regs_path) store_regs(m, o);
+      else if (tid == 0) store_out(m);
       mark(4);
-      cur ^= 1;
     }
-    if (prof)
-      for (int q = 0; q < 6; ++q) g->sec[q] = cyc[q];
-    if (tm) g->t[5] = globaltimer_ns();
-    return;
   }
-
-  // in-place head present: block 0 (the only writer of [0, hA)) is kept in
-  // s_def and written after a final barrier
-  u64 m = b;
-  u32 na = 0, nb = 0;
-  fetch_plan(m);
-  if (m < M.NB) plan_and_load(m, nxt_na, nxt_nb);
-  for (; m < M.NB; m += G) {
-    na = nxt_na;
-    nb = nxt_nb;
-    stage(s_in, na + nb);
-    publish_loaded(m);
-    if (m + G < M.NB) plan_and_load(m + G, nxt_na, nxt_nb);
-    u64* out = m == 0 ? s_def : s_out;
-    pre_status();
-    block_merge(s_in, na, nb, out);
-    if (m != 0) {
-      const u64 upto = m + M.L < M.NB - 1 ? m + M.L : M.NB - 1;
-      if (!wait_loaded(upto)) return;
-      store_block(m, s_out);
+  if (prof)
+    for (int q = 0; q < 6; ++q) g->sec[q] = cyc[q];
+  if (tid == 0) bulk_wait_all();
+  if (M.hA > 0) {
+    if (!grid_barrier(&g->sync, gen)) return;
+    if (b == 0) {
+      const u64 p1 = MG_C < M.n ? MG_C : M.n;
+      for (u32 k = tid; k < (u32)p1; k += MG_THREADS) a[k] = s_outc[k];
     }
-    __syncthreads();
   }
-  if (!grid_barrier(&g->sync, gen)) return;
   if (tm) g->t[5] = globaltimer_ns();
-  if (b == 0) {
-    const u64 p1 = MG_C < M.n ? MG_C : M.n;
-    for (u32 k = tid; k < (u32)p1; k += MG_THREADS) a[k] = s_def[SO(k)];
-  }
 }
 
 // ---------------------------------------------------------------------------
@@ -730,7 +789,7 @@ int merge_device(u64* a, u64 n, u64 split, int check_sorted, void* ws, size_t ws
   if ((u64)grid <= 2 * M.L || grid > 256) return PIP_ERR_UNSUPPORTED;
   PIP_CUDA(cudaMemsetAsync(M.status, 0, (size_t)grid * 4, st));
   PIP_CUDA(cudaMemsetAsync(M.g, 0, sizeof(MergeGlobal), st));
-  const size_t smem = (2 * MG_IN_WORDS + MG_OUT_WORDS) * sizeof(u64);
+  const size_t smem = MG_SMEM;
   PIP_CUDA(cudaFuncSetAttribute(merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   void* args[] = {&M};
   PIP_CUDA(cudaLaunchCooperativeKernel((const void*)merge_kernel, dim3(grid), dim3(MG_THREADS), args,
