@@ -28,7 +28,12 @@
 //   P2  (block merge, ~16 B/word) after the permutation a chunk in slot q
 //       only holds words of output rank < (q+2)C + hA + hB (chunks sorted by
 //       last element), so output block m can be written as soon as every
-//       block <= m + L (L = 3 + ceil((hA+hB)/C)) has loaded its inputs.
+//       block <= m + L (L = 1 + ceil((hA+hB)/C)) has loaded its inputs.
+//       (Block m's region overlaps slots <= m; a word of the chunk in slot q
+//       has fewer than qC + C + C + hA + hB words before it in the merged
+//       order — the q chunks of smaller-or-equal last, its own chunk, one
+//       partial chunk of the other run, head and tail — so it belongs to a
+//       block <= q + 1 + ceil((hA+hB)/C).)
 //       Blocks are assigned round-robin to persistent CTAs, loaded (<= 6
 //       contiguous pieces) into shared memory, merged by merge path and
 //       written back under that dataflow rule — no grid barrier per block.
@@ -351,89 +356,94 @@ __global__ void __launch_bounds__(MG_THREADS, MG_CTAS_PER_SM) merge_kernel(Merge
       rec_b = __ldcg(reinterpret_cast<const ulonglong2*>(M.plan + m) + 1);
     }
   };
-  // thread 0: the segments of block m, their bulk copies, the plan in s_seg
+  // warp 0: the segments of block m (lane k computes segment k: 0 A head,
+  // 1-2 A' pieces, 3-4 B' pieces, 5 B tail), one bulk copy per lane, and the
+  // plan for copy_in in s_seg.  The plan record was fetched one block ahead.
   auto issue_load = [&](u64 m) {
+    const u32 lane = tid;  // warp 0 only
     const u64 p0 = m * MG_C, p1 = (m + 1) * MG_C < M.n ? (m + 1) * MG_C : M.n;
-    const ulonglong4 pl = make_ulonglong4(rec_a.x, rec_a.y, rec_b.x, rec_b.y);
+    const u64 i0 = rec_a.x, i1 = rec_a.y;
+    const u32 da0 = (u32)rec_b.x, da1 = (u32)(rec_b.x >> 32);
+    const u32 db0 = (u32)rec_b.y, db1 = (u32)(rec_b.y >> 32);
     fetch_plan(m + G);
-    const u64 i0 = pl.x, i1 = pl.y;
     const u64 j0 = p0 - i0, j1 = p1 - i1;
-    const u32 da[2] = {(u32)pl.z, (u32)(pl.z >> 32)};
-    const u32 db[2] = {(u32)pl.w, (u32)(pl.w >> 32)};
-    u64 ph[6];
-    u32 len[6];
-    int ns = 0;
-    {  // A: head in place, then <= 2 chunk pieces
-      u64 x = i0;
+    u64 ph = 0, len = 0;
+    if (lane == 0) {  // A head [i0, min(i1, hA))
       const u64 xh = i1 < M.hA ? i1 : M.hA;
-      if (x < xh) { ph[ns] = x; len[ns++] = (u32)(xh - x); x = xh; }
-      int q = 0;
-      while (x < i1) {
-        const u64 ce = M.hA + (((x - M.hA) >> MG_LOGC) + 1) * MG_C;
-        const u64 e = ce < i1 ? ce : i1;
-        ph[ns] = M.hA + ((u64)da[q & 1] << MG_LOGC) + ((x - M.hA) & (MG_C - 1));
-        len[ns++] = (u32)(e - x);
-        x = e;
-        ++q;
+      if (i0 < xh) { ph = i0; len = xh - i0; }
+    } else if (lane == 1 || lane == 2) {  // A' pieces
+      const u64 xs = i0 > M.hA ? i0 : M.hA;
+      if (xs < i1) {
+        const u64 ce = M.hA + (((xs - M.hA) >> MG_LOGC) + 1) * MG_C;  // end of first chunk
+        const u64 s0 = lane == 1 ? xs : ce, e0 = lane == 1 ? (ce < i1 ? ce : i1) : i1;
+        if (s0 < e0) {
+          ph = M.hA + ((u64)(lane == 1 ? da0 : da1) << MG_LOGC) + ((s0 - M.hA) & (MG_C - 1));
+          len = e0 - s0;
+        }
       }
-    }
-    {  // B: <= 2 chunk pieces, then the tail in place
+    } else if (lane == 3 || lane == 4) {  // B' pieces
       const u64 lb = M.nb - M.hB;
-      u64 y = j0;
-      int q = 0;
-      while (y < j1 && y < lb) {
-        const u64 ce = ((y >> MG_LOGC) + 1) * MG_C;
-        u64 e = ce < j1 ? ce : j1;
-        if (e > lb) e = lb;
-        ph[ns] = M.hA + ((u64)db[q & 1] << MG_LOGC) + (y & (MG_C - 1));
-        len[ns++] = (u32)(e - y);
-        y = e;
-        ++q;
+      const u64 ye = j1 < lb ? j1 : lb;
+      if (j0 < ye) {
+        const u64 ce = ((j0 >> MG_LOGC) + 1) * MG_C;
+        const u64 s0 = lane == 3 ? j0 : ce, e0 = lane == 3 ? (ce < ye ? ce : ye) : ye;
+        if (s0 < e0) {
+          ph = M.hA + ((u64)(lane == 3 ? db0 : db1) << MG_LOGC) + (s0 & (MG_C - 1));
+          len = e0 - s0;
+        }
       }
-      if (y < j1) { ph[ns] = M.na + y; len[ns++] = (u32)(j1 - y); }
+    } else if (lane == 5) {  // B tail
+      const u64 lb = M.nb - M.hB;
+      const u64 ys = j0 > lb ? j0 : lb;
+      if (ys < j1) { ph = M.na + ys; len = j1 - ys; }
     }
-    u32 bytes[6], total = 0, E = 0, lo = 0;
-    for (int k = 0; k < ns; ++k) {
-      const u32 par = (u32)(((uintptr_t)(a + ph[k]) >> 3) & 1u);
-      bytes[k] = ((par + len[k]) * 8u + 15u) & ~15u;
-      total += bytes[k];
+    const u32 par = (u32)(((uintptr_t)(a + ph) >> 3) & 1u);
+    const u32 bytes = len ? ((par + (u32)len) * 8u + 15u) & ~15u : 0u;
+    // exclusive prefix sums over lanes 0..5 of len (logical start) and bytes
+    u32 lo = (u32)len, bo = bytes;
+#pragma unroll
+    for (int o = 1; o < 8; o <<= 1) {
+      const u32 l2 = __shfl_up_sync(0xffffffffu, lo, o), b2 = __shfl_up_sync(0xffffffffu, bo, o);
+      if (lane >= (u32)o) { lo += l2; bo += b2; }
     }
-    mbar_expect_tx(&s_bar, total);
-    s_seg[0] = (u32)(i1 - i0);
-    s_seg[1] = (u32)(j1 - j0);
-    for (int k = 0; k < 6; ++k) {
-      if (k < ns) {
-        const u32 par = (u32)(((uintptr_t)(a + ph[k]) >> 3) & 1u);
-        tma_load_1d(s_stage + E, a + ph[k] - par, bytes[k], &s_bar);
-        s_seg[2 + k] = lo;
-        s_seg[8 + k] = E + par;
-        E += bytes[k] / 8;
-        lo += len[k];
-      } else {
-        s_seg[2 + k] = 0xffffffffu;
-        s_seg[8 + k] = 0;
-      }
+    const u32 total = __shfl_sync(0xffffffffu, bo, 7);
+    lo -= (u32)len;
+    bo -= bytes;
+    if (lane == 0) {
+      mbar_expect_tx(&s_bar, total);
+      s_seg[0] = (u32)(i1 - i0);
+      s_seg[1] = (u32)(j1 - j0);
+    }
+    __syncwarp();
+    if (lane < 6) {
+      if (len) tma_load_1d(s_stage + bo / 8, a + ph - par, bytes, &s_bar);
+      s_seg[2 + lane] = len ? lo : 0xffffffffu;
+      s_seg[8 + lane] = bo / 8 + par;
     }
   };
-  // all threads: staging -> padded merge buffer (plan in s_seg)
+  // all threads: staging -> padded merge buffer, segment by segment
   auto copy_in = [&](u32& na_out, u32& nb_out) {
     na_out = s_seg[0];
     nb_out = s_seg[1];
     const u32 cnt = na_out + nb_out;
-    u32 lo[6], si[6];
+    u32 lo[7], si[6];
 #pragma unroll
     for (int k = 0; k < 6; ++k) {
       lo[k] = s_seg[2 + k];
       si[k] = s_seg[8 + k];
     }
+    lo[6] = cnt;
+    u64* sp = smem + MG_STAGE_WORDS;
 #pragma unroll
-    for (int r = 0; r < MG_PER_THREAD; ++r) {
-      const u32 x = tid + r * MG_THREADS;
-      u32 base = si[0];
+    for (int k = 0; k < 6; ++k) {
+      if (lo[k] == 0xffffffffu) continue;
+      u32 e = cnt;  // end = start of the next present segment
 #pragma unroll
-      for (int k = 1; k < 6; ++k)
-        if (x >= lo[k]) base = si[k] - lo[k];
-      if (x < cnt) s_pad[SI(x)] = s_stage[base + x];
+      for (int k2 = 6; k2 > k; --k2)
+        if (lo[k2] != 0xffffffffu) e = lo[k2];
+      const u64* src = smem + si[k] - lo[k];
+#pragma unroll 4
+      for (u32 x = lo[k] + tid; x < e; x += MG_THREADS) sp[SI(x)] = src[x];
     }
   };
   // wait until every block <= upto has reported loaded.  Warp 0 issues the
@@ -461,7 +471,7 @@ __global__ void __launch_bounds__(MG_THREADS, MG_CTAS_PER_SM) merge_kernel(Merge
         for (int q = 0; q < MAXS; ++q) {
           const u32 c = tid + 32 * q;
           if (c >= G || c > upto) continue;
-          const u64 mc = c + ((upto - c) / G) * G;
+          const u32 mc = c + (((u32)upto - c) / G) * G;  // 32-bit: NB < 2^32
           u32 v = st_cache[q];
           if (!first || v < mc + 1) v = st_cache[q] = ld_acquire_u32(M.status + c);
           if (v < mc + 1) ready = false;
@@ -477,8 +487,9 @@ __global__ void __launch_bounds__(MG_THREADS, MG_CTAS_PER_SM) merge_kernel(Merge
         }
         if (!__shfl_sync(0xffffffffu, ok, 0)) break;
       }
+      // the acquire loads order this CTA's later writes after the readers'
+      // releases (published once their bulk reads had landed)
       if (tid == 0) s_flag = ok;
-      fence_gpu();  // acquire: the reads of the words we are about to overwrite are done
     }
     __syncthreads();
     return s_flag != 0;
@@ -498,8 +509,9 @@ __global__ void __launch_bounds__(MG_THREADS, MG_CTAS_PER_SM) merge_kernel(Merge
       const bool pa = (j >= nb) || (i < na && ka <= kb);  // ties from A
       o[q] = pa ? ka : kb;
       const u32 ni = i + (pa ? 1u : 0u), nj = j + (pa ? 0u : 1u);
-      const bool more = pa ? (ni < na) : (nj < nb);
-      const u64 nk = more ? sp[SI(pa ? ni : na + nj)] : ~0ull;
+      // unconditional load (index <= na + nb: one slot past the data, still
+      // inside shared memory), then select: no divergent branch per step
+      const u64 nk = sp[SI(pa ? ni : na + nj)];
       ka = pa ? nk : ka;
       kb = pa ? kb : nk;
       i = ni;
@@ -513,18 +525,17 @@ __global__ void __launch_bounds__(MG_THREADS, MG_CTAS_PER_SM) merge_kernel(Merge
     static_assert(MG_PER_THREAD == 16, "pair rotation assumes 8 pairs");
     const u32 rot = tid & 7;
 #pragma unroll
-    for (int bit = 0; bit < 3; ++bit) {
+    for (int bit = 0; bit < 3; ++bit) {  // branch-free: lanes differ in rot
       const int sh = 1 << bit;
-      if (rot & sh) {
-        u64 t[MG_PER_THREAD];
+      const bool on = (rot >> bit) & 1u;
+      u64 t[MG_PER_THREAD];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          t[2 * q] = o[2 * ((q + sh) & 7)];
-          t[2 * q + 1] = o[2 * ((q + sh) & 7) + 1];
-        }
-#pragma unroll
-        for (int q = 0; q < MG_PER_THREAD; ++q) o[q] = t[q];
+      for (int q = 0; q < 8; ++q) {
+        t[2 * q] = on ? o[2 * ((q + sh) & 7)] : o[2 * q];
+        t[2 * q + 1] = on ? o[2 * ((q + sh) & 7) + 1] : o[2 * q + 1];
       }
+#pragma unroll
+      for (int q = 0; q < MG_PER_THREAD; ++q) o[q] = t[q];
     }
     ulonglong2* dst = reinterpret_cast<ulonglong2*>(smem + MG_STAGE_WORDS + MG_IN_WORDS);
 #pragma unroll
@@ -577,47 +588,48 @@ __global__ void __launch_bounds__(MG_THREADS, MG_CTAS_PER_SM) merge_kernel(Merge
   __syncthreads();
   u64 m = b;
   u32 na = 0, nb = 0;
-  if (tid == 0) fetch_plan(m);
+  if (tid < 32) fetch_plan(m);
   if (m < M.NB) {
-    if (tid == 0) issue_load(m);
+    if (tid < 32) issue_load(m);
     mbar_wait(&s_bar, phase);
     phase ^= 1;
     __syncthreads();  // s_seg visible
     copy_in(na, nb);
     publish_loaded(m);
     __syncthreads();  // staging free
-    if (tid == 0 && m + G < M.NB) issue_load(m + G);
+    if (tid < 32 && m + G < M.NB) issue_load(m + G);
   }
   for (; m < M.NB; m += G) {
     pre_status();
     u64 o[MG_PER_THREAD];
     merge_regs(na, nb, o);
-    mark(2);
+    mark(0);
     const bool regs_path = keep0 && m != 0;
     if (!regs_path) {
       if (tid == 0) bulk_wait_read_all();  // the previous store has read s_outc
       __syncthreads();
+      mark(1);
       stage_out(o);
       fence_proxy_async_smem();
     }
     __syncthreads();  // merge inputs consumed; s_outc complete
-    mark(0);
+    mark(2);
     if (m + G < M.NB) {
       mbar_wait(&s_bar, phase);
       phase ^= 1;
+      mark(3);
       copy_in(na, nb);
       publish_loaded(m + G);
       __syncthreads();  // staging free, s_pad holds block m + G
-      if (tid == 0 && m + 2 * G < M.NB) issue_load(m + 2 * G);
+      if (tid < 32 && m + 2 * G < M.NB) issue_load(m + 2 * G);
     }
-    mark(1);
+    mark(4);
     if (!(keep0 && m == 0)) {
       const u64 upto = m + M.L < M.NB - 1 ? m + M.L : M.NB - 1;
       if (!(M.dbg & 1) && !wait_loaded(upto)) return;
-      mark(3);
       if (regs_path) store_regs(m, o);
       else if (tid == 0) store_out(m);
-      mark(4);
+      mark(5);
     }
   }
   if (prof)
@@ -773,7 +785,7 @@ int merge_device(u64* a, u64 n, u64 split, int check_sorted, void* ws, size_t ws
   M.NB = (n + MG_C - 1) / MG_C;
   M.D = L.D;
   M.ncuts = L.ncuts;
-  M.L = 3 + (M.hA + M.hB + MG_C - 1) / MG_C;
+  M.L = 1 + (M.hA + M.hB + MG_C - 1) / MG_C;
   M.cut = (u64*)(w + L.cut);
   M.dest = (u32*)(w + L.dest);
   M.inv = (u32*)(w + L.inv);
@@ -799,9 +811,10 @@ int merge_device(u64* a, u64 n, u64 split, int check_sorted, void* ws, size_t ws
   PIP_CUDA(cudaStreamSynchronize(st));
   if (gh.sync.abort) return PIP_ERR_CUDA;
   if (timing_enabled() && (M.dbg & 4))
-    fprintf(stderr, "[pip merge] CTA0 cycles: merge %llu | stage+publish %llu | plan+load-issue %llu | wait %llu | store %llu\n",
-            (unsigned long long)gh.sec[2], (unsigned long long)gh.sec[0], (unsigned long long)gh.sec[1],
-            (unsigned long long)gh.sec[3], (unsigned long long)gh.sec[4]);
+    fprintf(stderr, "[pip merge] CTA0 thread-0 cycles: merge %llu | merge imbalance + store-read wait %llu | "
+            "stage %llu | load wait %llu | copy-in + issue %llu | dataflow wait + store %llu\n",
+            (unsigned long long)gh.sec[0], (unsigned long long)gh.sec[1], (unsigned long long)gh.sec[2],
+            (unsigned long long)gh.sec[3], (unsigned long long)gh.sec[4], (unsigned long long)gh.sec[5]);
   if (timing_enabled())
     fprintf(stderr,
             "[pip merge] n=%llu K=%llu ncuts=%llu D=%llu uncut=%u  P0 %.3f ms | cuts %.3f | "
