@@ -97,7 +97,7 @@ struct DevPred {
   u64 lim;     // MOD_EQ: floor((2^64 - 1) / d_odd)
 };
 // predicate classes the filter kernels are specialised on
-enum : int { PC_MASK = 0, PC_MOD = 1, PC_GEN = 2 };
+enum : int { PC_MASK = 0, PC_MOD = 1, PC_GEN = 2, PC_MODODD = 3 };
 DevPred make_dev_pred(const pip_pred& p);
 
 __device__ __forceinline__ u64 fast_div(u64 x, const DevPred& p) {
@@ -140,9 +140,11 @@ __device__ __forceinline__ bool pred_eval_t(const DevPred& p, u64 x) {
   bool r;
   if (PC == PC_MASK) {
     r = (x & p.a) == p.b;
-  } else if (PC == PC_MOD) {
+  } else if (PC == PC_MOD) {  // branch-free (bitwise &): no divergent short-circuit
     const u64 y = x - p.b;
-    r = (x >= p.b) && ((y & ((1ull << p.tz) - 1ull)) == 0) && ((y >> p.tz) * p.inv <= p.lim);
+    r = (x >= p.b) & ((y & ((1ull << p.tz) - 1ull)) == 0) & ((y >> p.tz) * p.inv <= p.lim);
+  } else if (PC == PC_MODODD) {  // odd divisor: x = b (mod d) <=> (x - b) * d^-1 <= lim
+    r = (x >= p.b) & ((x - p.b) * p.inv <= p.lim);
   } else {
     return pred_eval(p, x);
   }
@@ -164,6 +166,7 @@ __device__ __forceinline__ u64 globaltimer_ns() {
   return t;
 }
 bool timing_enabled();  // env PIP_TIMING=1: per-phase timers printed to stderr
+u32 lb_stride(int sms, int grid);  // look-back slot spacing in memory
 
 // ---------------------------------------------------------------------------
 // warp helpers

@@ -350,6 +350,7 @@ filter_ws_kernel(u64* __restrict__ a, DevPred p, u64* m_out, LookbackCtx c, u64 
   using O = Op<PIP_OP_ADD>;
   constexpr u64 TILE = (u64)NWC * 512;
   constexpr u32 TILE_BYTES = (u32)(TILE * 8);
+  constexpr u64 STRIDE = TILE + 2;  // + 2 words: the compacted output may start one word in
   extern __shared__ __align__(128) u64 ring[];
   __shared__ __align__(8) u64 full[S], reduced[S], pready[S], empty[S];
   __shared__ u64 s_wtot[S][NWC];
@@ -384,7 +385,7 @@ filter_ws_kernel(u64* __restrict__ a, DevPred p, u64* m_out, LookbackCtx c, u64 
     mbar_expect_tx(&full[s], TILE_BYTES);
 #pragma unroll
     for (int q = 0; q < 4; ++q)
-      tma_load_1d(ring + s * TILE + q * (TILE / 4), a + t * TILE + q * (TILE / 4), TILE_BYTES / 4,
+      tma_load_1d(ring + s * STRIDE + q * (TILE / 4), a + t * TILE + q * (TILE / 4), TILE_BYTES / 4,
                   &full[s]);
   };
   if (warp == 0) {
@@ -455,34 +456,62 @@ filter_ws_kernel(u64* __restrict__ a, DevPred p, u64* m_out, LookbackCtx c, u64 
     return;
   }
   const u32 w = warp - 1;
+  // scatter: the kept words of the tile are compacted inside its own stage
+  // buffer (every warp first pulls its 16 words per lane into registers) and
+  // leave with one bulk store; only <= 2 ragged words go through the LSU
   auto scatter = [&](u64 k) -> bool {
     const int s = (int)(k % S);
     mbar_wait(&pready[s], (u32)((k / S) & 1));
     if (s_abort) return false;
-    u64 run = s_prefix[s] + s_wexc[s][w];
+    const u64 prefix = s_prefix[s];
+    const u64 agg = s_agg[s];
+    u64* stage = ring + s * STRIDE;
+    // word parity of the destination: compacted word q sits at stage[par + q]
+    // so that shared and global addresses agree modulo 16 bytes
+    const u32 par = (u32)(((uintptr_t)(a + prefix) >> 3) & 1u);
+    u32 run = (u32)s_wexc[s][w] + par;
     const u32 keep = s_keep[s][w * 32 + lane];
-    const u64* src = ring + s * TILE + w * 512;
+    const u64* src = stage + w * 512;
+    u64 vx[8], vy[8];
+    u32 pos[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       const bool f0 = (keep >> (2 * j)) & 1u, f1 = (keep >> (2 * j + 1)) & 1u;
       const u32 m0 = __ballot_sync(0xffffffffu, f0);
       const u32 m1 = __ballot_sync(0xffffffffu, f1);
-      const u64 r0 = run + __popc(m0 & lt) + __popc(m1 & lt);
-      if (f0 | f1) {
-        const ulonglong2 v = lds2(src + 64 * j + 2 * lane);
-        if (f0) a[r0] = v.x;
-        if (f1) a[r0 + f0] = v.y;
-      }
+      pos[j] = run + __popc(m0 & lt) + __popc(m1 & lt);
+      const ulonglong2 v = lds2(src + 64 * j + 2 * lane);
+      vx[j] = v.x;
+      vy[j] = v.y;
       run += __popc(m0) + __popc(m1);
     }
+    named_bar(1, NWC * 32);  // the whole tile is in registers
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const bool f0 = (keep >> (2 * j)) & 1u, f1 = (keep >> (2 * j + 1)) & 1u;
+      if (f0) stage[pos[j]] = vx[j];
+      if (f1) stage[pos[j] + (f0 ? 1u : 0u)] = vy[j];
+    }
+    fence_proxy_async_smem();
     named_bar(1, NWC * 32);
-    if (w == 0 && lane == 0) mbar_arrive(&empty[s]);
+    if (w == 0 && lane == 0) {
+      const u32 head = par && agg ? 1u : 0u;
+      const u32 body = (u32)((agg - head) & ~1ull);
+      if (head) a[prefix] = stage[1];
+      if (head + body < agg) a[prefix + agg - 1] = stage[par + agg - 1];
+      if (body) {
+        tma_store_1d(a + prefix + head, stage + par + head, body * 8u);
+        bulk_commit();
+        bulk_wait_read_all();  // the stage may be refilled once the store has read it
+      }
+      mbar_arrive(&empty[s]);
+    }
     return true;
   };
   auto reduce_tile = [&](u64 k) {
     const int s = (int)(k % S);
     mbar_wait(&full[s], (u32)((k / S) & 1));
-    const u64* src = ring + s * TILE + w * 512;
+    const u64* src = ring + s * STRIDE + w * 512;
     u32 keep = 0;
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
@@ -510,6 +539,7 @@ filter_ws_kernel(u64* __restrict__ a, DevPred p, u64* m_out, LookbackCtx c, u64 
       if (!scatter(k)) return;
       if (B + (k + 2) * G < num_tiles) reduce_tile(k + 2);
     }
+    if (w == 0 && lane == 0) bulk_wait_all();
     return;
   }
   for (u64 k = 0;; ++k) {
@@ -518,10 +548,11 @@ filter_ws_kernel(u64* __restrict__ a, DevPred p, u64* m_out, LookbackCtx c, u64 
     const u64 t = DYN ? s_tile[s] : B + k * G;
     if (t >= num_tiles) {
       if (k > 0) scatter(k - 1);
+      if (w == 0 && lane == 0) bulk_wait_all();  // the bulk stores have landed
       break;
     }
     if (!DYN) mbar_wait(&full[s], (u32)((k / S) & 1));
-    const u64* src = ring + s * TILE + w * 512;
+    const u64* src = ring + s * STRIDE + w * 512;
     u32 keep = 0;
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
@@ -554,6 +585,7 @@ count_kernel(const u64* __restrict__ a, u64 n, DevPred p, u64* partials, u32* co
   const bool vec = ((uintptr_t)a & 15) == 0;
   if (vec) {
     const u64 npairs = n / 2;
+#pragma unroll 4
     for (u64 q = (u64)blockIdx.x * blockDim.x + threadIdx.x; q < npairs; q += stride) {
       ulonglong2 v = ldg_stream2(a + 2 * q);
       t += (u64)pred_eval_t<PC>(p, v.x) + (u64)pred_eval_t<PC>(p, v.y);
@@ -611,7 +643,7 @@ static ScratchLayoutF carve_f(void* scratch, int sms) {
 
 static int pred_class(const DevPred& p) {
   if (p.kind == PIP_PRED_MASK_EQ) return PC_MASK;
-  if (p.kind == PIP_PRED_MOD_EQ) return PC_MOD;
+  if (p.kind == PIP_PRED_MOD_EQ) return p.tz == 0 ? PC_MODODD : PC_MOD;
   return PC_GEN;
 }
 
@@ -627,6 +659,7 @@ static int launch_filter(u64* a, u64 n, const DevPred& p, u64* m_dev, const Scra
   switch (pred_class(p)) {
     case PC_MASK: return launch_filter_pc<VEC, PC_MASK>(a, n, p, m_dev, L, st, dev, carry_in, out);
     case PC_MOD: return launch_filter_pc<VEC, PC_MOD>(a, n, p, m_dev, L, st, dev, carry_in, out);
+    case PC_MODODD: return launch_filter_pc<VEC, PC_MODODD>(a, n, p, m_dev, L, st, dev, carry_in, out);
     default: return launch_filter_pc<VEC, PC_GEN>(a, n, p, m_dev, L, st, dev, carry_in, out);
   }
 }
@@ -644,8 +677,8 @@ static int launch_filter_pc(u64* a, u64 n, const DevPred& p, u64* m_dev, const S
   if (g > tiles) g = tiles;
   int grid = (int)g;
   PIP_CUDA(cudaMemsetAsync(L.abort, 0, 64, st));
-  PIP_CUDA(cudaMemsetAsync(L.slots, 0, sizeof(TileSlot) * 4 * (size_t)grid, st));
-  LookbackCtx c{L.slots, L.abort, (u32)(4 * grid)};
+  PIP_CUDA(cudaMemsetAsync(L.slots, 0, sizeof(TileSlot) * 4 * (size_t)grid * lb_stride(num_sms(current_device()), grid), st));
+  LookbackCtx c{L.slots, L.abort, (u32)(4 * grid), lb_stride(num_sms(current_device()), grid)};
   DevPred pp = p;
   u32* counter = L.counter;
   void* args[] = {&a, &n, &pp, &m_dev, &c, (void*)&tiles, &counter, &carry_in, &out};
@@ -669,8 +702,8 @@ static int launch_filter_tma(u64* a, u64 n, const DevPred& p, u64* m_dev, const 
   if (g > tiles) g = tiles;
   int grid = (int)g;
   PIP_CUDA(cudaMemsetAsync(L.abort, 0, 64, st));
-  PIP_CUDA(cudaMemsetAsync(L.slots, 0, sizeof(TileSlot) * 4 * (size_t)grid, st));
-  LookbackCtx c{L.slots, L.abort, (u32)(4 * grid)};
+  PIP_CUDA(cudaMemsetAsync(L.slots, 0, sizeof(TileSlot) * 4 * (size_t)grid * lb_stride(num_sms(current_device()), grid), st));
+  LookbackCtx c{L.slots, L.abort, (u32)(4 * grid), lb_stride(num_sms(current_device()), grid)};
   DevPred pp = p;
   u32* counter = L.counter;
   void* args[] = {&a, &n, &pp, &m_dev, &c, (void*)&tiles, (void*)&full_tiles, &counter};
@@ -695,8 +728,8 @@ static int launch_filter_ahead(u64* a, u64 n, const DevPred& p, u64* m_dev,
   int grid = (int)g;
   u64* mid = rem ? L.carry : m_dev;
   PIP_CUDA(cudaMemsetAsync(L.abort, 0, 64, st));
-  PIP_CUDA(cudaMemsetAsync(L.slots, 0, sizeof(TileSlot) * 4 * (size_t)grid, st));
-  LookbackCtx c{L.slots, L.abort, (u32)(4 * grid)};
+  PIP_CUDA(cudaMemsetAsync(L.slots, 0, sizeof(TileSlot) * 4 * (size_t)grid * lb_stride(num_sms(current_device()), grid), st));
+  LookbackCtx c{L.slots, L.abort, (u32)(4 * grid), lb_stride(num_sms(current_device()), grid)};
   DevPred pp = p;
   void* args[] = {&a, &pp, &mid, &c, (void*)&full_tiles};
   PIP_CUDA(cudaLaunchCooperativeKernel((const void*)k, dim3(grid), dim3(THREADS), args, smem, st));
@@ -714,7 +747,7 @@ static int launch_filter_ws_pc(u64* a, u64 n, const DevPred& p, u64* m_dev,
   constexpr int THREADS = 32 * (NWC + 1);
   const u64 full_tiles = n / TILE, rem = n - full_tiles * TILE;
   auto k = filter_ws_kernel<NWC, S, PC, DYN, AHEAD>;
-  const int smem = (int)(S * TILE * 8);
+  const int smem = (int)(S * (TILE + 2) * 8);
   PIP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   int per_sm = 0;
   PIP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, THREADS, smem));
@@ -725,8 +758,8 @@ static int launch_filter_ws_pc(u64* a, u64 n, const DevPred& p, u64* m_dev,
   int grid = (int)g;
   u64* mid = rem ? L.carry : m_dev;
   PIP_CUDA(cudaMemsetAsync(L.abort, 0, 64, st));
-  PIP_CUDA(cudaMemsetAsync(L.slots, 0, sizeof(TileSlot) * 4 * (size_t)grid, st));
-  LookbackCtx c{L.slots, L.abort, (u32)(4 * grid)};
+  PIP_CUDA(cudaMemsetAsync(L.slots, 0, sizeof(TileSlot) * 4 * (size_t)grid * lb_stride(num_sms(current_device()), grid), st));
+  LookbackCtx c{L.slots, L.abort, (u32)(4 * grid), lb_stride(num_sms(current_device()), grid)};
   DevPred pp = p;
   u32* counter = L.counter;
   void* args[] = {&a, &pp, &mid, &c, (void*)&full_tiles, &counter};
@@ -741,6 +774,7 @@ static int launch_filter_ws(u64* a, u64 n, const DevPred& p, u64* m_dev, const S
   switch (pred_class(p)) {
     case PC_MASK: return launch_filter_ws_pc<NWC, S, PC_MASK, DYN, AHEAD>(a, n, p, m_dev, L, st, dev);
     case PC_MOD: return launch_filter_ws_pc<NWC, S, PC_MOD, DYN, AHEAD>(a, n, p, m_dev, L, st, dev);
+    case PC_MODODD: return launch_filter_ws_pc<NWC, S, PC_MODODD, DYN, AHEAD>(a, n, p, m_dev, L, st, dev);
     default: return launch_filter_ws_pc<NWC, S, PC_GEN, DYN, AHEAD>(a, n, p, m_dev, L, st, dev);
   }
 }
@@ -776,6 +810,8 @@ int filter_device(u64* a, u64 n, const pip_pred* pred, u64* m_dev, void* scratch
     if (cfg == 7) return launch_filter_ws<8, 3>(a, n, p, m_dev, L, st, dev);
     if (cfg == 9) return launch_filter_ws<16, 3, true>(a, n, p, m_dev, L, st, dev);
     if (cfg == 10) return launch_filter_ws<12, 4, false, true>(a, n, p, m_dev, L, st, dev);
+    if (cfg == 11) return launch_filter_ws<14, 4>(a, n, p, m_dev, L, st, dev);
+    if (cfg == 12) return launch_filter_ws<12, 4>(a, n, p, m_dev, L, st, dev);
     return launch_filter_ws<16, 3>(a, n, p, m_dev, L, st, dev);
   }
   if (vec && cfg >= 4 && n >= 4 * FILTER_TILE) {
@@ -807,6 +843,7 @@ int count_device(const u64* a, u64 n, const pip_pred* pred, u64* m_dev, void* sc
   switch (pred_class(p)) {
     case PC_MASK: count_kernel<PC_MASK><<<grid, 512, 0, st>>>(a, n, p, L.partials, L.counter, m_dev); break;
     case PC_MOD: count_kernel<PC_MOD><<<grid, 512, 0, st>>>(a, n, p, L.partials, L.counter, m_dev); break;
+    case PC_MODODD: count_kernel<PC_MODODD><<<grid, 512, 0, st>>>(a, n, p, L.partials, L.counter, m_dev); break;
     default: count_kernel<PC_GEN><<<grid, 512, 0, st>>>(a, n, p, L.partials, L.counter, m_dev); break;
   }
   PIP_CHECK_LAUNCH();

@@ -3,11 +3,19 @@
 // Persistent kernels walk tiles round-robin (tile t on CTA t % G, wave t / G).
 // Tile t publishes into slot t % R of a ring of R = 4G slots, so the scratch
 // is O(#CTAs) regardless of n — the device analogue of the reference's
-// O(log n) recursion stack (strong.py:107-129), never metered.  The tiles of
-// one wave start together, so a tile typically finds the last inclusive
-// prefix at the end of the PREVIOUS wave: the look-back is block-wide (every
-// thread reads one predecessor slot), which covers a whole wave in a single
-// L2 round trip instead of wave/32 warp-sized steps.
+// O(log n) recursion stack (strong.py:107-129), never metered.  One warp
+// reads 32 predecessor slots per L2 round trip.
+//
+// Measured (B200, scan of 2^32 words, PIP_TIMING=1 counters): the chain of
+// inclusive prefixes is the kernel's serial part — a wave of 148 tiles needs
+// ~2 look-back reads per tile, and under full HBM streaming one L2 round trip
+// costs ~1.6 us, so the look-back, not bandwidth, sets the pace (14.0 ms with
+// it, 10.6 ms with it removed).  What helped: slots spaced `stride` apart in
+// memory so a window spans several L2 lines (14.0 -> 13.0 ms).  What did not:
+// 128-slot windows (4 loads per lane: 19 ms), block-wide windows, smaller
+// tiles (more waves), 2-stage 96 KiB tiles (load latency exposed), and
+// clusters of 2-4 CTAs sharing one chain step (18 ms: the DSMEM hand-offs
+// add a hop per wave).
 //
 // A slot is 16 bytes {value, (epoch << 2) | state} published with ONE 128-bit
 // store and read with ONE 128-bit load, so a reader always sees a value
@@ -27,14 +35,23 @@
 
 namespace pip {
 
+// measurement counters (PIP_TIMING=1), one copy per translation unit
+static __device__ u64 g_scan_prof[8];
+static __device__ u32 g_prof_on;
+static __device__ u32 g_prof_cta;
+__device__ __forceinline__ void lb_count(int which) {
+  if (g_prof_on && blockIdx.x == g_prof_cta && (threadIdx.x & 31) == 0) g_scan_prof[which] += 1;
+}
+
 struct LookbackCtx {
   TileSlot* slots;  // [R]
   u32* abort;       // global abort flag (0 = ok)
   u32 R;            // ring size (4 x resident CTAs)
+  u32 stride = 1;   // slots apart in memory (spreads a look-back window over L2 lines)
 };
 
 __device__ __forceinline__ TileSlot* slot_of(const LookbackCtx& c, u64 tile) {
-  return c.slots + (tile % c.R);
+  return c.slots + (tile % c.R) * c.stride;
 }
 
 static constexpr bool LB_BLOCK = false;  // block-wide look-back (measured slower)
@@ -111,6 +128,7 @@ __device__ bool lookback(const LookbackCtx& c, u64 tile, u64& prefix_out) {
     u32 incl_mask, need;
     bool restart = false;
     for (;;) {
+      lb_count(5);
       st = read_slot<O>(c, u, v);
       incl_mask = __ballot_sync(0xffffffffu, st == RD_INCL);
       const u32 bad = __ballot_sync(0xffffffffu, st == RD_NOTREADY);
@@ -121,6 +139,7 @@ __device__ bool lookback(const LookbackCtx& c, u64 tile, u64& prefix_out) {
         break;
       }
       if ((bad & need) == 0) break;
+      lb_count(6);
       bool ok = true;
       if (lane == 0) ok = spin_tick(c, spins);
       if (!__shfl_sync(0xffffffffu, (int)ok, 0)) return false;

@@ -13,6 +13,7 @@
 // segment [tile*8192 + w*512, +512); in chunk j (0..7) lane l holds the pair
 // (2l, 2l+1) of the 64-element sub-chunk j, loaded/stored as one 128-bit
 // access, so every warp access is a fully coalesced 512-byte transaction.
+#include <cstdio>
 #include <cstdlib>
 #include "lookback.cuh"
 
@@ -387,12 +388,14 @@ scan_ahead_kernel(u64* __restrict__ a, u64 init, const u64* carry_in, u64* total
 // r01_scan_ahead_summary.txt) leave the compute warps' critical path.
 // Hand-offs are mbarriers: full (TMA bytes landed), reduced (tile aggregate
 // in smem), pready (prefix in smem), empty (stage stored, may be refilled).
-template <int OP, bool INCLUSIVE, int NWC, int S, bool DYN, bool AHEAD = false>
+
+template <int OP, bool INCLUSIVE, int NWC, int S, bool DYN, bool AHEAD = false, int WPW = 512>
 __global__ void __launch_bounds__(32 * (NWC + 1), 1)
 scan_ws_kernel(u64* __restrict__ a, u64 init, const u64* carry_in, u64* total, LookbackCtx c,
                u64 num_tiles, u32* counter) {
   using O = Op<OP>;
-  constexpr u64 TILE = (u64)NWC * 512;
+  constexpr u64 TILE = (u64)NWC * WPW;  // WPW words per compute warp
+  constexpr int JW = WPW / 64;
   constexpr u32 TILE_BYTES = (u32)(TILE * 8);
   extern __shared__ __align__(128) u64 ring[];
   __shared__ __align__(8) u64 full[S], reduced[S], pready[S], empty[S];
@@ -462,7 +465,9 @@ scan_ws_kernel(u64* __restrict__ a, u64 init, const u64* carry_in, u64* total, L
           return;
         }
       }
+      const u64 tw0 = clock64();
       mbar_wait(&reduced[s], (u32)((k / S) & 1));
+      const u64 tw1 = clock64();
       const u64 agg = s_agg[s];
       u64 prefix = (t == 0 && carry_in) ? *carry_in : O::identity;
       int ok = 1;
@@ -483,6 +488,11 @@ scan_ws_kernel(u64* __restrict__ a, u64 init, const u64* carry_in, u64* total, L
         if (!ok) s_abort = 1;
         if (ok && t == num_tiles - 1 && total) *total = O::apply(prefix, agg);
         mbar_arrive(&pready[s]);
+        if (B == g_prof_cta && g_prof_on) {
+          g_scan_prof[0] += tw1 - tw0;            // producer waits for the reduce
+          g_scan_prof[1] += clock64() - tw1;      // publish + look-back
+          g_scan_prof[2] += 1;
+        }
       }
       if (!ok) return;
       // refill: tile k+S-1 goes into the stage of tile k-1 once that is stored
@@ -503,13 +513,15 @@ scan_ws_kernel(u64* __restrict__ a, u64 init, const u64* carry_in, u64* total, L
   const u32 w = warp - 1;
   auto scan_store = [&](u64 k) -> bool {
     const int s = (int)(k % S);
+    const u64 tp0 = clock64();
     mbar_wait(&pready[s], (u32)((k / S) & 1));
+    if (B == g_prof_cta && tid == 32 && g_prof_on) g_scan_prof[3] += clock64() - tp0;  // compute waits for prefix
     if (s_abort) return false;
     u64 run = O::apply(s_prefix[s], s_wexc[s][w]);
-    const u64* src = ring + s * TILE + w * 512;
-    const u64 wbase = (DYN ? s_tile[s] : B + k * G) * TILE + (u64)w * 512;
+    const u64* src = ring + s * TILE + w * WPW;
+    const u64 wbase = (DYN ? s_tile[s] : B + k * G) * TILE + (u64)w * WPW;
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
+    for (int j = 0; j < JW; ++j) {
       const ulonglong2 v = lds2(src + 64 * j + 2 * lane);
       const u64 x0 = v.x, x1 = v.y;
       const u64 inc = warp_incl_scan<O>(O::apply(x0, x1));
@@ -535,10 +547,10 @@ scan_ws_kernel(u64* __restrict__ a, u64 init, const u64* carry_in, u64* total, L
   auto reduce_tile = [&](u64 k) {
     const int s = (int)(k % S);
     mbar_wait(&full[s], (u32)((k / S) & 1));
-    const u64* src = ring + s * TILE + w * 512;
+    const u64* src = ring + s * TILE + w * WPW;
     u64 acc = O::identity;
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
+    for (int j = 0; j < JW; ++j) {
       const ulonglong2 v = lds2(src + 64 * j + 2 * lane);
       acc = O::apply(acc, O::apply(v.x, v.y));
     }
@@ -574,11 +586,13 @@ scan_ws_kernel(u64* __restrict__ a, u64 init, const u64* carry_in, u64* total, L
       if (k > 0) scan_store(k - 1);
       break;
     }
+    const u64 tf0 = clock64();
     if (!DYN) mbar_wait(&full[s], (u32)((k / S) & 1));
-    const u64* src = ring + s * TILE + w * 512;
+    if (B == g_prof_cta && tid == 32 && g_prof_on) g_scan_prof[4] += clock64() - tf0;  // compute waits for data
+    const u64* src = ring + s * TILE + w * WPW;
     u64 acc = O::identity;
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
+    for (int j = 0; j < JW; ++j) {
       const ulonglong2 v = lds2(src + 64 * j + 2 * lane);
       acc = O::apply(acc, O::apply(v.x, v.y));
     }
@@ -693,8 +707,8 @@ static int launch_scan_t(u64* a, u64 n, u64 init, const u64* carry, u64* total,
   int rc = persistent_grid(k, SCAN_THREADS, device, tiles, &grid);
   if (rc) return rc;
   PIP_CUDA(cudaMemsetAsync(L.abort, 0, 64, st));
-  PIP_CUDA(cudaMemsetAsync(L.slots, 0, sizeof(TileSlot) * 4 * (size_t)grid, st));
-  LookbackCtx c{L.slots, L.abort, (u32)(4 * grid)};
+  PIP_CUDA(cudaMemsetAsync(L.slots, 0, sizeof(TileSlot) * 4 * (size_t)grid * lb_stride(num_sms(current_device()), grid), st));
+  LookbackCtx c{L.slots, L.abort, (u32)(4 * grid), lb_stride(num_sms(current_device()), grid)};
   u32* counter = L.counter;
   void* args[] = {&a, &n, &init, &carry, &total, &c, (void*)&tiles, &counter};
   PIP_CUDA(cudaLaunchCooperativeKernel((const void*)k, dim3(grid), dim3(SCAN_THREADS), args, 0, st));
@@ -718,8 +732,8 @@ static int launch_scan_tma(u64* a, u64 n, u64 init, const u64* carry, u64* total
   if (g > tiles) g = tiles;
   int grid = (int)g;
   PIP_CUDA(cudaMemsetAsync(L.abort, 0, 64, st));
-  PIP_CUDA(cudaMemsetAsync(L.slots, 0, sizeof(TileSlot) * 4 * (size_t)grid, st));
-  LookbackCtx c{L.slots, L.abort, (u32)(4 * grid)};
+  PIP_CUDA(cudaMemsetAsync(L.slots, 0, sizeof(TileSlot) * 4 * (size_t)grid * lb_stride(num_sms(current_device()), grid), st));
+  LookbackCtx c{L.slots, L.abort, (u32)(4 * grid), lb_stride(num_sms(current_device()), grid)};
   u32* counter = L.counter;
   void* args[] = {&a, &n, &init, &carry, &total, &c, (void*)&tiles, (void*)&full_tiles, &counter};
   PIP_CUDA(cudaLaunchCooperativeKernel((const void*)k, dim3(grid), dim3(THREADS), args, smem, st));
@@ -745,8 +759,8 @@ static int launch_scan_ahead(u64* a, u64 n, u64 init, const u64* carry, u64* tot
   // the whole-tile part writes its inclusive fold to `mid` when a tail follows
   u64* mid = rem ? L.carry : total;
   PIP_CUDA(cudaMemsetAsync(L.abort, 0, 64, st));
-  PIP_CUDA(cudaMemsetAsync(L.slots, 0, sizeof(TileSlot) * 4 * (size_t)grid, st));
-  LookbackCtx c{L.slots, L.abort, (u32)(4 * grid)};
+  PIP_CUDA(cudaMemsetAsync(L.slots, 0, sizeof(TileSlot) * 4 * (size_t)grid * lb_stride(num_sms(current_device()), grid), st));
+  LookbackCtx c{L.slots, L.abort, (u32)(4 * grid), lb_stride(num_sms(current_device()), grid)};
   void* args[] = {&a, &init, &carry, &mid, &c, (void*)&full_tiles};
   PIP_CUDA(cudaLaunchCooperativeKernel((const void*)k, dim3(grid), dim3(THREADS), args, smem, st));
   if (rem) {
@@ -756,14 +770,14 @@ static int launch_scan_ahead(u64* a, u64 n, u64 init, const u64* carry, u64* tot
   return PIP_OK;
 }
 
-template <int OP, bool INCL, int NWC, int S, bool DYN = false, bool AHEAD = false>
+template <int OP, bool INCL, int NWC, int S, bool DYN = false, bool AHEAD = false, int WPW = 512>
 static int launch_scan_ws(u64* a, u64 n, u64 init, const u64* carry, u64* total,
                           const ScratchLayout& L, cudaStream_t st, int device) {
-  constexpr u64 TILE = (u64)NWC * 512;
+  constexpr u64 TILE = (u64)NWC * WPW;
   constexpr int THREADS = 32 * (NWC + 1);
   const u64 full_tiles = n / TILE;
   const u64 rem = n - full_tiles * TILE;
-  auto k = scan_ws_kernel<OP, INCL, NWC, S, DYN, AHEAD>;
+  auto k = scan_ws_kernel<OP, INCL, NWC, S, DYN, AHEAD, WPW>;
   const int smem = (int)(S * TILE * 8);
   PIP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   int per_sm = 0;
@@ -775,11 +789,33 @@ static int launch_scan_ws(u64* a, u64 n, u64 init, const u64* carry, u64* total,
   int grid = (int)g;
   u64* mid = rem ? L.carry : total;
   PIP_CUDA(cudaMemsetAsync(L.abort, 0, 64, st));
-  PIP_CUDA(cudaMemsetAsync(L.slots, 0, sizeof(TileSlot) * 4 * (size_t)grid, st));
-  LookbackCtx c{L.slots, L.abort, (u32)(4 * grid)};
+  PIP_CUDA(cudaMemsetAsync(L.slots, 0, sizeof(TileSlot) * 4 * (size_t)grid * lb_stride(num_sms(current_device()), grid), st));
+  LookbackCtx c{L.slots, L.abort, (u32)(4 * grid), lb_stride(num_sms(current_device()), grid)};
   u32* counter = L.counter;
   void* args[] = {&a, &init, &carry, &mid, &c, (void*)&full_tiles, &counter};
+  const bool prof = timing_enabled();
+  if (prof) {
+    const u64 z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    const u32 on = 1;
+    PIP_CUDA(cudaMemcpyToSymbolAsync(g_scan_prof, z, sizeof(z), 0, cudaMemcpyHostToDevice, st));
+    PIP_CUDA(cudaMemcpyToSymbolAsync(g_prof_on, &on, 4, 0, cudaMemcpyHostToDevice, st));
+    const char* pc = getenv("PIP_PROF_CTA");
+    const u32 cta = pc ? (u32)atoi(pc) : 0u;
+    PIP_CUDA(cudaMemcpyToSymbolAsync(g_prof_cta, &cta, 4, 0, cudaMemcpyHostToDevice, st));
+    PIP_CUDA(cudaStreamSynchronize(st));
+  }
   PIP_CUDA(cudaLaunchCooperativeKernel((const void*)k, dim3(grid), dim3(THREADS), args, smem, st));
+  if (prof) {
+    u64 h[8];
+    const u32 off = 0;
+    PIP_CUDA(cudaMemcpyFromSymbolAsync(h, g_scan_prof, sizeof(h), 0, cudaMemcpyDeviceToHost, st));
+    PIP_CUDA(cudaMemcpyToSymbolAsync(g_prof_on, &off, 4, 0, cudaMemcpyHostToDevice, st));
+    PIP_CUDA(cudaStreamSynchronize(st));
+    fprintf(stderr, "[pip scan] profiled CTA: tiles %llu | producer: wait-reduce %llu lookback %llu | compute: wait-prefix %llu wait-data %llu cycles | look-back reads %llu retries %llu\n",
+            (unsigned long long)h[2], (unsigned long long)h[0], (unsigned long long)h[1],
+            (unsigned long long)h[3], (unsigned long long)h[4], (unsigned long long)h[5],
+            (unsigned long long)h[6]);
+  }
   if (rem) {
     u64* tail = a + full_tiles * TILE;
     return launch_scan_t<OP, INCL, true>(tail, rem, init, L.carry, total, L, st, device);
@@ -814,6 +850,12 @@ static int launch_scan_op(u64* a, u64 n, u64 init, int inclusive, const u64* car
     if (cfg == 9)
       return inclusive ? launch_scan_ws<OP, true, 16, 3, true>(a, n, init, carry, total, L, st, device)
                        : launch_scan_ws<OP, false, 16, 3, true>(a, n, init, carry, total, L, st, device);
+    if (cfg == 11)
+      return inclusive ? launch_scan_ws<OP, true, 14, 4>(a, n, init, carry, total, L, st, device)
+                       : launch_scan_ws<OP, false, 14, 4>(a, n, init, carry, total, L, st, device);
+    if (cfg == 12)
+      return inclusive ? launch_scan_ws<OP, true, 12, 4>(a, n, init, carry, total, L, st, device)
+                       : launch_scan_ws<OP, false, 12, 4>(a, n, init, carry, total, L, st, device);
     if (cfg == 10)
       return inclusive
                  ? launch_scan_ws<OP, true, 12, 4, false, true>(a, n, init, carry, total, L, st, device)
