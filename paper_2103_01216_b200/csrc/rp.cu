@@ -111,6 +111,39 @@ __device__ __forceinline__ u32 block_rank(bool f, u32* s_cnt, u32* tot) {
   return r;
 }
 
+// block-wide exclusive prefix of per-thread counts v (< 2^16 each); *tot = sum
+__device__ __forceinline__ u32 block_excl_sum(u32 v, u32* s_cnt, u32* tot) {
+  const u32 lane = lane_id(), warp = warp_id();
+  u32 inc = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const u32 t = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= (u32)o) inc += t;
+  }
+  if (lane == 31) s_cnt[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    const u32 nw = blockDim.x / 32;
+    const u32 w = lane < nw ? s_cnt[lane] : 0;
+    u32 wi = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const u32 t = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= (u32)o) wi += t;
+    }
+    if (lane < nw) s_cnt[lane] = wi - w;
+    if (lane == 31) s_cnt[32] = wi;
+  }
+  __syncthreads();
+  const u32 r = s_cnt[warp] + inc - v;
+  *tot = s_cnt[32];
+  __syncthreads();
+  return r;
+}
+
+// items per thread per pass in the latency-bound loops (independent loads in flight)
+static constexpr int RB = 4;
+
 __device__ __forceinline__ u64 block_sum(u64 v, u64* s_red) {
   v = warp_reduce<Op<PIP_OP_ADD>>(v);
   if (lane_id() == 0) s_red[warp_id()] = v;
@@ -258,31 +291,52 @@ __global__ void __launch_bounds__(RP_THREADS, 4) rp_kernel(RpArgs A) {
       const u64 cbefore = s - fbefore;  // committed items in CTAs < b
       const bool targeted = A.targeted_clean_ok && F * 8 < (1ull << A.logcap);
       u64 runf = 0, runc = 0;
-      for (u64 c0 = s; c0 < e; c0 += T) {
-        const u64 k = c0 + tid;
-        const bool valid = k < e;
-        const bool com = valid && __ldcg(A.cflag + k);
-        u32 tot;
-        const u32 rf = block_rank(valid && !com, s_cnt, &tot);
-        if (valid && !com) {
-          ids_n[fbefore + runf + rf] = __ldcg(ids_o + k);
-          tg_n[fbefore + runf + rf] = __ldcg(tg_o + k);
+      // RB consecutive items per thread: failures keep their order
+      for (u64 c0 = s; c0 < e; c0 += (u64)RB * T) {
+        const u64 kb = c0 + (u64)RB * tid;
+        u32 fm = 0, cm = 0, iv[RB], tv[RB];
+#pragma unroll
+        for (int q = 0; q < RB; ++q) {
+          const u64 k = kb + q;
+          iv[q] = tv[q] = 0;
+          if (k < e) {
+            const bool com = __ldcg(A.cflag + k);
+            iv[q] = __ldcg(ids_o + k);
+            tv[q] = __ldcg(tg_o + k);
+            if (com) cm |= 1u << q;
+            else fm |= 1u << q;
+          }
         }
+        u32 tot;
+        u64 pos = fbefore + runf + block_excl_sum(__popc(fm), s_cnt, &tot);
+#pragma unroll
+        for (int q = 0; q < RB; ++q)
+          if ((fm >> q) & 1u) {
+            ids_n[pos] = iv[q];
+            tg_n[pos] = tv[q];
+            ++pos;
+          }
         runf += tot;
         if (trace) {
           u32 totc;
-          const u32 rc = block_rank(com, s_cnt, &totc);
-          if (com) A.trace[R.trace_pos + cbefore + runc + rc] = __ldcg(ids_o + k);
+          u64 cp = R.trace_pos + cbefore + runc + block_excl_sum(__popc(cm), s_cnt, &totc);
+#pragma unroll
+          for (int q = 0; q < RB; ++q)
+            if ((cm >> q) & 1u) A.trace[cp++] = iv[q];
           runc += totc;
         }
-        if ((BM == 1 || (!BM && targeted)) && valid) {
-          const u32 sl = __ldcg(A.slot + k);
-          if (sl != RP_NOSLOT) A.table[sl] = RP_EMPTY;
-        }
-        if (BM && valid && F * 256 < A.n) {  // sparse round: clear the touched words
-          const u32 t = __ldcg(tg_o + k);
-          A.bmB[t >> 5] = 0u;
-          if (BM == 1) A.bmC[t >> 5] = 0u;
+#pragma unroll
+        for (int q = 0; q < RB; ++q) {
+          const u64 k = kb + q;
+          if (k >= e) continue;
+          if (BM == 1 || (!BM && targeted)) {
+            const u32 sl = __ldcg(A.slot + k);
+            if (sl != RP_NOSLOT) A.table[sl] = RP_EMPTY;
+          }
+          if (BM && F * 256 < A.n) {  // sparse round: clear the touched words
+            A.bmB[tv[q] >> 5] = 0u;
+            if (BM == 1) A.bmC[tv[q] >> 5] = 0u;
+          }
         }
       }
       R.trace_pos += ncommit;
@@ -324,6 +378,7 @@ __global__ void __launch_bounds__(RP_THREADS, 4) rp_kernel(RpArgs A) {
       u64 s, e;
       part(wd, G, b, s, e);
       u64 c = 0;
+#pragma unroll 4
       for (u64 q = s + tid; q < e; q += T) {
         const u64 id = hi - q;
         c += __ldg(A.h + id) != id;
@@ -370,21 +425,33 @@ __global__ void __launch_bounds__(RP_THREADS, 4) rp_kernel(RpArgs A) {
       u64 s, e;
       part(wd, G, b, s, e);
       u64 run = wbefore;
-      for (u64 c0 = s; c0 < e && run < fresh; c0 += T) {
-        const u64 q = c0 + tid;
-        const bool valid = q < e;
-        const u64 id = hi - q;
-        const u64 hv = valid ? __ldg(A.h + id) : id;
-        const bool f = valid && hv != id;
-        u32 tot;
-        const u32 r = block_rank(f, s_cnt, &tot);
-        const u64 rank = run + r;
-        if (f && rank < fresh) {
-          ids_n[nfail + rank] = (u32)id;
-          tg_n[nfail + rank] = (u32)hv;
-          if (rank == 0) g->dhi = id;
-          if (rank == fresh - 1) g->dlo = id;
+      for (u64 c0 = s; c0 < e && run < fresh; c0 += (u64)RB * T) {
+        const u64 qb = c0 + (u64)RB * tid;
+        u64 hv[RB];
+        u32 fm = 0;
+#pragma unroll
+        for (int q = 0; q < RB; ++q) {
+          hv[q] = 0;
+          if (qb + q < e) {
+            const u64 id = hi - (qb + q);
+            hv[q] = __ldg(A.h + id);
+            if (hv[q] != id) fm |= 1u << q;
+          }
         }
+        u32 tot;
+        u64 rank = run + block_excl_sum(__popc(fm), s_cnt, &tot);
+#pragma unroll
+        for (int q = 0; q < RB; ++q)
+          if ((fm >> q) & 1u) {
+            if (rank < fresh) {
+              const u64 id = hi - (qb + q);
+              ids_n[nfail + rank] = (u32)id;
+              tg_n[nfail + rank] = (u32)hv[q];
+              if (rank == 0) g->dhi = id;
+              if (rank == fresh - 1) g->dlo = id;
+            }
+            ++rank;
+          }
         run += tot;
       }
     } else if (b == 0 && tid == 0) {
@@ -409,13 +476,22 @@ __global__ void __launch_bounds__(RP_THREADS, 4) rp_kernel(RpArgs A) {
       part(newF, G, b, s, e);
       u32 claims = 0;
       if (BM == 1) {
-        for (u64 k = s + tid; k < e; k += T) {
-          const u32 t = __ldcg(tg_n + k);
-          const u32 bit = 1u << (t & 31);
-          const u32 old = atomicOr(A.bmB + (t >> 5), bit);
-          if (old & bit) atomicOr(A.bmC + (t >> 5), bit);
-          else if (t < dlo || t > dhi) claims += 1;
-          A.slot[k] = RP_NOSLOT;
+        for (u64 k0 = s + tid; k0 < e; k0 += (u64)RB * T) {
+          u32 t[RB], old[RB];
+#pragma unroll
+          for (int q = 0; q < RB; ++q) t[q] = k0 + q * T < e ? __ldcg(tg_n + k0 + q * T) : 0u;
+#pragma unroll
+          for (int q = 0; q < RB; ++q)
+            old[q] = k0 + q * T < e ? atomicOr(A.bmB + (t[q] >> 5), 1u << (t[q] & 31)) : 0u;
+#pragma unroll
+          for (int q = 0; q < RB; ++q) {
+            const u64 k = k0 + q * T;
+            if (k >= e) continue;
+            const u32 bit = 1u << (t[q] & 31);
+            if (old[q] & bit) atomicOr(A.bmC + (t[q] >> 5), bit);
+            else if (t[q] < dlo || t[q] > dhi) claims += 1;
+            A.slot[k] = RP_NOSLOT;
+          }
         }
       } else if (BM == 2) {
         // mark: first toucher of t sets B[t]; later ones go to the list.  The
@@ -423,14 +499,22 @@ __global__ void __launch_bounds__(RP_THREADS, 4) rp_kernel(RpArgs A) {
         // first touches outside [dlo, dhi] (peak_table_load).
         if (tid == 0) s_cnt[32] = 0;
         __syncthreads();
-        for (u64 k = s + tid; k < e; k += T) {
-          const u32 t = __ldcg(tg_n + k);
-          const u32 bit = 1u << (t & 31);
-          const u32 old = atomicOr(A.bmB + (t >> 5), bit);
-          const bool coll = old & bit;
-          if (coll) A.lc[s + atomicAdd(s_cnt + 32, 1u)] = (u32)(k - s);
-          else if (t < dlo || t > dhi) claims += 1;
-          A.cflag[k] = coll ? 2 : 0;
+        for (u64 k0 = s + tid; k0 < e; k0 += (u64)RB * T) {
+          u32 t[RB], old[RB];
+#pragma unroll
+          for (int q = 0; q < RB; ++q) t[q] = k0 + q * T < e ? __ldcg(tg_n + k0 + q * T) : 0u;
+#pragma unroll
+          for (int q = 0; q < RB; ++q)
+            old[q] = k0 + q * T < e ? atomicOr(A.bmB + (t[q] >> 5), 1u << (t[q] & 31)) : 0u;
+#pragma unroll
+          for (int q = 0; q < RB; ++q) {
+            const u64 k = k0 + q * T;
+            if (k >= e) continue;
+            const bool coll = (old[q] >> (t[q] & 31)) & 1u;
+            if (coll) A.lc[s + atomicAdd(s_cnt + 32, 1u)] = (u32)(k - s);
+            else if (t[q] < dlo || t[q] > dhi) claims += 1;
+            A.cflag[k] = coll ? 2 : 0;
+          }
         }
         __syncthreads();
         if (tid == 0) A.lccnt[b] = s_cnt[32];
@@ -514,7 +598,7 @@ __global__ void __launch_bounds__(RP_THREADS, 4) rp_kernel(RpArgs A) {
       u32 lg = 0;
       if (lc_total) {
         lg = 8;
-        while ((1ull << lg) < 2 * lc_total) ++lg;
+        while ((1ull << lg) < 4 * lc_total) ++lg;  // load <= 1/4: short probes
         if (lg > A.logcap) lg = A.logcap;
       }
       R.logcap_c = lg;
@@ -530,6 +614,9 @@ __global__ void __launch_bounds__(RP_THREADS, 4) rp_kernel(RpArgs A) {
         if (!grid_barrier(&g->sync, gen)) break;
       }
       u32 fails = 0;
+      // (one item per thread per step: the random swaps are throughput-bound,
+      // and 4 CTAs/SM of 64 registers beat 2 CTAs/SM with 4-item batches,
+      // measured 110 vs 175 ms at 2^30)
       for (u64 k = s + tid; k < e; k += T) {
         if (__ldcg(A.cflag + k)) continue;
         const u32 t = __ldcg(tg_n + k), i = __ldcg(ids_n + k);
