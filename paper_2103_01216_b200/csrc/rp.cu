@@ -614,19 +614,35 @@ __global__ void __launch_bounds__(RP_THREADS, 4) rp_kernel(RpArgs A) {
         if (!grid_barrier(&g->sync, gen)) break;
       }
       u32 fails = 0;
-      // (one item per thread per step: the random swaps are throughput-bound,
-      // and 4 CTAs/SM of 64 registers beat 2 CTAs/SM with 4-item batches,
-      // measured 110 vs 175 ms at 2^30)
-      for (u64 k = s + tid; k < e; k += T) {
-        if (__ldcg(A.cflag + k)) continue;
-        const u32 t = __ldcg(tg_n + k), i = __ldcg(ids_n + k);
+      // One item per thread per step (4 CTAs/SM of 64 registers beat 2 CTAs/SM
+      // with 4-item batches: 110 vs 175 ms at 2^30), but the step's loads are
+      // issued in two waves instead of a chain: {cflag, target, id} of the
+      // next item travel while this one finishes (software pipeline), and the
+      // table probe and the own-check word go out together.
+      u64 k = s + tid;
+      u32 ncf = 1, nt = 0, ni = 0;
+      if (k < e) {
+        ncf = __ldcg(A.cflag + k);
+        nt = __ldcg(tg_n + k);
+        ni = __ldcg(ids_n + k);
+      }
+      for (; k < e; k += T) {
+        const u32 cf = ncf, t = nt, i = ni;
+        if (k + T < e) {
+          ncf = __ldcg(A.cflag + k + T);
+          nt = __ldcg(tg_n + k + T);
+          ni = __ldcg(ids_n + k + T);
+        }
+        if (cf) continue;
+        const u64 w0 = lc_total ? __ldcg(A.table + rp_home(t, lg)) : RP_EMPTY;
+        const u32 bw = __ldcg(A.bmB + (i >> 5));
         u32 v;
-        if (lc_total && table_lookup(A.table, lg, t, v)) {
+        if (w0 != RP_EMPTY && ((u32)(w0 >> 32) == t || table_lookup(A.table, lg, t, v))) {
           table_reserve(A.table, lg, t, i, dclaim, &g->sync.error);
           A.cflag[k] = 2;
           continue;
         }
-        const bool c = !((__ldcg(A.bmB + (i >> 5)) >> (i & 31)) & 1u);
+        const bool c = !((bw >> (i & 31)) & 1u);
         A.cflag[k] = c;
         if (c) {
           const u64 x = __ldcg(A.a + i), y = __ldcg(A.a + t);
