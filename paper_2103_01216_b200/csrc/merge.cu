@@ -61,7 +61,7 @@ __device__ __forceinline__ u32 SO(u32 r) { return r + (r >> 4); }
 static constexpr u32 MG_IN_WORDS = (u32)(MG_C + MG_C / 8);
 static constexpr u32 MG_OUT_WORDS = (u32)(MG_C + MG_C / 16);
 static constexpr u32 MG_STAGE_WORDS = (u32)(MG_C + 16);  // bulk-copy staging (+2 junk words x 6 segments)
-static constexpr size_t MG_SMEM = (size_t)(MG_STAGE_WORDS + MG_IN_WORDS + MG_C) * 8;
+static constexpr size_t MG_SMEM = (size_t)(2 * MG_STAGE_WORDS + MG_C) * 8;
 
 struct MergeGlobal {
   GridSync sync;
@@ -332,23 +332,24 @@ __global__ void __launch_bounds__(MG_THREADS, MG_CTAS_PER_SM) merge_kernel(Merge
 
   if (tm) g->t[4] = globaltimer_ns();
   // ---------------- P2: block merge under the dataflow rule
-  // Global traffic goes through the TMA engine only, so the SM's load/store
-  // pipe is left to the shared-memory merge:
-  //   load   the <= 6 contiguous input segments of block m + 2G (A head in
+  // Global traffic goes through the TMA engine only:
+  //   load   the <= 6 contiguous input segments of block m + G (A head in
   //          place, <= 2 permuted A' chunks, <= 2 permuted B' chunks, B tail
-  //          in place) with one bulk copy each into the staging buffer (each
-  //          widened to 16-byte alignment: <= 2 junk words per segment);
-  //   copy   staging -> the padded merge buffer (bank-conflict-free layout);
-  //   merge  MG_PER_THREAD consecutive outputs per thread into registers;
-  //   stage  registers -> the contiguous output buffer (pairs rotated by
-  //          lane so 16-byte shared stores hit distinct banks);
+  //          in place), one bulk copy each, into one of two staging buffers
+  //          (each copy widened to 16-byte alignment: <= 2 junk words per
+  //          segment), while block m is merged out of the other buffer;
+  //   merge  straight from staging through the segment map (logical A/B
+  //          index -> staging word), a merge-path range of 16-17 consecutive
+  //          outputs per thread into registers.  The ranges start at
+  //          16t + (lane >> 1), which spreads a warp's reads and writes over
+  //          all shared-memory banks even for perfectly interleaved runs;
+  //   stage  registers -> the contiguous output buffer;
   //   store  one bulk copy to a[mC, (m+1)C) once every block <= m + L has
   //          reported its inputs loaded (the dataflow rule).
-  u64* s_stage = smem;                                 // MG_STAGE_WORDS
-  u64* s_pad = smem + MG_STAGE_WORDS;                  // MG_IN_WORDS, padded
-  u64* s_outc = smem + MG_STAGE_WORDS + MG_IN_WORDS;   // MG_C, contiguous
-  __shared__ __align__(8) u64 s_bar;
-  __shared__ u32 s_seg[2 + 2 * 6];  // na, nb | lo[6] | staging index[6]
+  constexpr int MO = MG_PER_THREAD + 1;  // outputs per thread, at most
+  u64* s_outc = smem + 2 * MG_STAGE_WORDS;  // MG_C, contiguous
+  __shared__ __align__(8) u64 s_bar[2];
+  __shared__ u32 s_seg[2][2 + 2 * 6];  // per buffer: na, nb | lo[6] | staging index[6]
   ulonglong2 rec_a = make_ulonglong2(0, 0), rec_b = make_ulonglong2(0, 0);
   auto fetch_plan = [&](u64 m) {
     if (m < M.NB) {
@@ -357,10 +358,12 @@ __global__ void __launch_bounds__(MG_THREADS, MG_CTAS_PER_SM) merge_kernel(Merge
     }
   };
   // warp 0: the segments of block m (lane k computes segment k: 0 A head,
-  // 1-2 A' pieces, 3-4 B' pieces, 5 B tail), one bulk copy per lane, and the
-  // plan for copy_in in s_seg.  The plan record was fetched one block ahead.
-  auto issue_load = [&](u64 m) {
+  // 1-2 A' pieces, 3-4 B' pieces, 5 B tail), one bulk copy per lane into
+  // staging buffer `sb`, the segment map in s_seg[sb].  The plan record was
+  // fetched one block ahead.
+  auto issue_load = [&](u64 m, int sb) {
     const u32 lane = tid;  // warp 0 only
+    u64* stage = smem + sb * MG_STAGE_WORDS;
     const u64 p0 = m * MG_C, p1 = (m + 1) * MG_C < M.n ? (m + 1) * MG_C : M.n;
     const u64 i0 = rec_a.x, i1 = rec_a.y;
     const u32 da0 = (u32)rec_b.x, da1 = (u32)(rec_b.x >> 32);
@@ -410,40 +413,15 @@ __global__ void __launch_bounds__(MG_THREADS, MG_CTAS_PER_SM) merge_kernel(Merge
     lo -= (u32)len;
     bo -= bytes;
     if (lane == 0) {
-      mbar_expect_tx(&s_bar, total);
-      s_seg[0] = (u32)(i1 - i0);
-      s_seg[1] = (u32)(j1 - j0);
+      mbar_expect_tx(&s_bar[sb], total);
+      s_seg[sb][0] = (u32)(i1 - i0);
+      s_seg[sb][1] = (u32)(j1 - j0);
     }
     __syncwarp();
     if (lane < 6) {
-      if (len) tma_load_1d(s_stage + bo / 8, a + ph - par, bytes, &s_bar);
-      s_seg[2 + lane] = len ? lo : 0xffffffffu;
-      s_seg[8 + lane] = bo / 8 + par;
-    }
-  };
-  // all threads: staging -> padded merge buffer, segment by segment
-  auto copy_in = [&](u32& na_out, u32& nb_out) {
-    na_out = s_seg[0];
-    nb_out = s_seg[1];
-    const u32 cnt = na_out + nb_out;
-    u32 lo[7], si[6];
-#pragma unroll
-    for (int k = 0; k < 6; ++k) {
-      lo[k] = s_seg[2 + k];
-      si[k] = s_seg[8 + k];
-    }
-    lo[6] = cnt;
-    u64* sp = smem + MG_STAGE_WORDS;
-#pragma unroll
-    for (int k = 0; k < 6; ++k) {
-      if (lo[k] == 0xffffffffu) continue;
-      u32 e = cnt;  // end = start of the next present segment
-#pragma unroll
-      for (int k2 = 6; k2 > k; --k2)
-        if (lo[k2] != 0xffffffffu) e = lo[k2];
-      const u64* src = smem + si[k] - lo[k];
-#pragma unroll 4
-      for (u32 x = lo[k] + tid; x < e; x += MG_THREADS) sp[SI(x)] = src[x];
+      if (len) tma_load_1d(stage + bo / 8, a + ph - par, bytes, &s_bar[sb]);
+      s_seg[sb][2 + lane] = len ? lo : 0xffffffffu;
+      s_seg[sb][8 + lane] = bo / 8 + par;
     }
   };
   // wait until every block <= upto has reported loaded.  Warp 0 issues the
@@ -473,7 +451,7 @@ __global__ void __launch_bounds__(MG_THREADS, MG_CTAS_PER_SM) merge_kernel(Merge
           if (c >= G || c > upto) continue;
           const u32 mc = c + (((u32)upto - c) / G) * G;  // 32-bit: NB < 2^32
           u32 v = st_cache[q];
-          if (!first || v < mc + 1) v = st_cache[q] = ld_acquire_u32(M.status + c);
+          if (!first || v < mc + 1) v = st_cache[q] = ld_relaxed_u32(M.status + c);
           if (v < mc + 1) ready = false;
         }
         first = false;
@@ -487,59 +465,62 @@ __global__ void __launch_bounds__(MG_THREADS, MG_CTAS_PER_SM) merge_kernel(Merge
         }
         if (!__shfl_sync(0xffffffffu, ok, 0)) break;
       }
-      // the acquire loads order this CTA's later writes after the readers'
-      // releases (published once their bulk reads had landed)
+      // WAR only: the writes below are issued after these loads returned the
+      // flags, and a flag goes up only after its reader's bulk loads landed
       if (tid == 0) s_flag = ok;
     }
     __syncthreads();
     return s_flag != 0;
   };
-  // merge-path co-rank, then MG_PER_THREAD steps with one shared load each
-  auto merge_regs = [&](u32 na, u32 nb, u64 (&o)[MG_PER_THREAD]) {
-    const u64* sp = smem + MG_STAGE_WORDS;  // s_pad, derived from smem (LDS)
+  // this thread's output range [r0, r1) of the block
+  const u32 lane_t = tid & 31;
+  const u32 r0_all = tid * MG_PER_THREAD + (lane_t >> 1);
+  const u32 r1_all = lane_t == 31 ? (tid + 1) * MG_PER_THREAD : r0_all + MG_PER_THREAD + (((lane_t + 1) >> 1) - (lane_t >> 1));
+  // merge path over staging buffer `sb` through its segment map
+  auto merge_regs = [&](int sb, u32 na, u32 nb, u32& r0, u32& r1, u64 (&o)[MO]) {
+    const u64* sp = smem + sb * MG_STAGE_WORDS;
     const u32 total = na + nb;
-    const u32 r0 = tid * MG_PER_THREAD;
-    if (r0 >= total) return;
-    u32 i = corank2_smem(sp, na, nb, r0);
-    u32 j = r0 - i;
-    u64 ka = i < na ? sp[SI(i)] : ~0ull;
-    u64 kb = j < nb ? sp[SI(na + j)] : ~0ull;
+    r0 = r0_all < total ? r0_all : total;
+    r1 = r1_all < total ? r1_all : total;
+    // A side: segments 0..2, B side: 3..5 (lo = logical start, 0xffffffff if absent)
+    const u32 la1 = s_seg[sb][3], la2 = s_seg[sb][4];
+    const u32 oa0 = s_seg[sb][2] == 0xffffffffu ? 0u : s_seg[sb][8] - s_seg[sb][2];
+    const u32 oa1 = s_seg[sb][9] - la1, oa2 = s_seg[sb][10] - la2;
+    const u32 lb4 = s_seg[sb][6], lb5 = s_seg[sb][7];
+    const u32 ob3 = s_seg[sb][5] == 0xffffffffu ? 0u : s_seg[sb][11] - s_seg[sb][5];
+    const u32 ob4 = s_seg[sb][12] - lb4, ob5 = s_seg[sb][13] - lb5;
+    auto mapA = [&](u32 x) -> u32 { return x + (x >= la2 ? oa2 : (x >= la1 ? oa1 : oa0)); };
+    auto mapB = [&](u32 x) -> u32 { return x + (x >= lb5 ? ob5 : (x >= lb4 ? ob4 : ob3)); };
+    if (r0 >= r1) return;
+    u32 lo = r0 > nb ? r0 - nb : 0, hi = r0 < na ? r0 : na;
+    while (lo < hi) {
+      const u32 mid = (lo + hi) >> 1;
+      if (sp[mapA(mid)] <= sp[mapB(na + r0 - mid - 1)]) lo = mid + 1;
+      else hi = mid;
+    }
+    u32 i = lo, j = r0 - lo;
+    u64 ka = sp[mapA(i)];
+    u64 kb = sp[mapB(na + j)];
 #pragma unroll
-    for (int q = 0; q < MG_PER_THREAD; ++q) {
+    for (int q = 0; q < MO; ++q) {
       const bool pa = (j >= nb) || (i < na && ka <= kb);  // ties from A
       o[q] = pa ? ka : kb;
       const u32 ni = i + (pa ? 1u : 0u), nj = j + (pa ? 0u : 1u);
-      // unconditional load (index <= na + nb: one slot past the data, still
-      // inside shared memory), then select: no divergent branch per step
-      const u64 nk = sp[SI(pa ? ni : na + nj)];
+      // unconditional load (one word past a side's end is still staging
+      // memory), then select: no divergent branch per step
+      const u64 nk = sp[pa ? mapA(ni) : mapB(na + nj)];
       ka = pa ? nk : ka;
       kb = pa ? kb : nk;
       i = ni;
       j = nj;
     }
   };
-  // registers -> contiguous s_outc: pair q of thread t goes to 16-byte slot
-  // 8t + q; issuing the pairs rotated by t mod 8 spreads a warp's stores over
-  // all bank groups (4 wavefronts per 512 bytes, the minimum)
-  auto stage_out = [&](u64 (&o)[MG_PER_THREAD]) {
-    static_assert(MG_PER_THREAD == 16, "pair rotation assumes 8 pairs");
-    const u32 rot = tid & 7;
+  // registers -> s_outc[r0, r1): lanes sit 16.5 words apart, so each 8-byte
+  // store of a warp covers all bank pairs twice (the minimum)
+  auto stage_out = [&](u32 r0, u32 r1, const u64 (&o)[MO]) {
 #pragma unroll
-    for (int bit = 0; bit < 3; ++bit) {  // branch-free: lanes differ in rot
-      const int sh = 1 << bit;
-      const bool on = (rot >> bit) & 1u;
-      u64 t[MG_PER_THREAD];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        t[2 * q] = on ? o[2 * ((q + sh) & 7)] : o[2 * q];
-        t[2 * q + 1] = on ? o[2 * ((q + sh) & 7) + 1] : o[2 * q + 1];
-      }
-#pragma unroll
-      for (int q = 0; q < MG_PER_THREAD; ++q) o[q] = t[q];
-    }
-    ulonglong2* dst = reinterpret_cast<ulonglong2*>(smem + MG_STAGE_WORDS + MG_IN_WORDS);
-#pragma unroll
-    for (int q = 0; q < 8; ++q) dst[8 * tid + ((q + rot) & 7)] = make_ulonglong2(o[2 * q], o[2 * q + 1]);
+    for (int q = 0; q < MO; ++q)
+      if (r0 + q < r1) s_outc[r0 + q] = o[q];
   };
   // thread 0: s_outc[0, len) -> a[p0, p0 + len) (16-byte-aligned middle by
   // the TMA engine, <= 1 word at either end by hand)
@@ -555,15 +536,16 @@ __global__ void __launch_bounds__(MG_THREADS, MG_CTAS_PER_SM) merge_kernel(Merge
       bulk_commit();
     }
   };
-  auto store_regs = [&](u64 m, const u64 (&o)[MG_PER_THREAD]) {
-    const u64 p0 = m * MG_C, p1 = (m + 1) * MG_C < M.n ? (m + 1) * MG_C : M.n;
-    const u32 len = (u32)(p1 - p0), r0 = tid * MG_PER_THREAD;
+  auto store_regs = [&](u64 m, u32 r0, u32 r1, const u64 (&o)[MO]) {
+    const u64 p0 = m * MG_C;
 #pragma unroll
-    for (int q = 0; q < MG_PER_THREAD; ++q)
-      if (r0 + q < len) a[p0 + r0 + q] = o[q];
+    for (int q = 0; q < MO; ++q)
+      if (r0 + q < r1) a[p0 + r0 + q] = o[q];
   };
+  // a plain flag store by a thread with no global stores in flight (thread 0
+  // issues the block stores; a release here would wait for them)
   auto publish_loaded = [&](u64 m) {
-    if (tid == 0) st_release_u32(M.status + b, (u32)(m + 1));
+    if (tid == 32) st_relaxed_u32(M.status + b, (u32)(m + 1));
   };
 
   const bool prof = (M.dbg & 4) && b == 0 && tid == 0;
@@ -580,57 +562,62 @@ __global__ void __launch_bounds__(MG_THREADS, MG_CTAS_PER_SM) merge_kernel(Merge
   // block may still read) in s_outc until the end and stores its other
   // blocks from registers
   const bool keep0 = M.hA > 0 && b == 0;
-  u32 phase = 0;
+  u32 phase[2] = {0, 0};
   if (tid == 0) {
-    mbar_init(&s_bar, 1);
+    mbar_init(&s_bar[0], 1);
+    mbar_init(&s_bar[1], 1);
     mbar_fence_init();
   }
   __syncthreads();
   u64 m = b;
-  u32 na = 0, nb = 0;
+  int cur = 0;
   if (tid < 32) fetch_plan(m);
   if (m < M.NB) {
-    if (tid < 32) issue_load(m);
-    mbar_wait(&s_bar, phase);
-    phase ^= 1;
-    __syncthreads();  // s_seg visible
-    copy_in(na, nb);
+    if (tid < 32) issue_load(m, 0);
+    mbar_wait(&s_bar[0], phase[0]);
+    phase[0] ^= 1;
     publish_loaded(m);
-    __syncthreads();  // staging free
-    if (tid < 32 && m + G < M.NB) issue_load(m + G);
+    if (tid < 32 && m + G < M.NB) issue_load(m + G, 1);
+    __syncthreads();  // s_seg[0] visible
   }
   for (; m < M.NB; m += G) {
     pre_status();
-    u64 o[MG_PER_THREAD];
-    merge_regs(na, nb, o);
+    const u32 na = s_seg[cur][0], nb = s_seg[cur][1];
+    u64 o[MO];
+    u32 r0, r1;
+    merge_regs(cur, na, nb, r0, r1, o);
     mark(0);
     const bool regs_path = keep0 && m != 0;
     if (!regs_path) {
       if (tid == 0) bulk_wait_read_all();  // the previous store has read s_outc
       __syncthreads();
       mark(1);
-      stage_out(o);
+      stage_out(r0, r1, o);
       fence_proxy_async_smem();
     }
-    __syncthreads();  // merge inputs consumed; s_outc complete
+    __syncthreads();  // buffer `cur` consumed; s_outc complete
     mark(2);
     if (m + G < M.NB) {
-      mbar_wait(&s_bar, phase);
-      phase ^= 1;
+      mbar_wait(&s_bar[cur ^ 1], phase[cur ^ 1]);  // block m + G has landed
+      phase[cur ^ 1] ^= 1;
       mark(3);
-      copy_in(na, nb);
       publish_loaded(m + G);
-      __syncthreads();  // staging free, s_pad holds block m + G
-      if (tid < 32 && m + 2 * G < M.NB) issue_load(m + 2 * G);
+      if (tid < 32 && m + 2 * G < M.NB) {
+        fence_proxy_async_smem();
+        issue_load(m + 2 * G, cur);
+      }
     }
     mark(4);
     if (!(keep0 && m == 0)) {
       const u64 upto = m + M.L < M.NB - 1 ? m + M.L : M.NB - 1;
-      if (!(M.dbg & 1) && !wait_loaded(upto)) return;
-      if (regs_path) store_regs(m, o);
+      if (!(M.dbg & 1) && !wait_loaded(upto)) return;  // (its __syncthreads also
+      if (regs_path) store_regs(m, r0, r1, o);         //  publishes s_seg[cur])
       else if (tid == 0) store_out(m);
       mark(5);
+    } else {
+      __syncthreads();  // s_seg[cur] (block 2G) visible before the next merge
     }
+    cur ^= 1;
   }
   if (prof)
     for (int q = 0; q < 6; ++q) g->sec[q] = cyc[q];
@@ -812,7 +799,7 @@ int merge_device(u64* a, u64 n, u64 split, int check_sorted, void* ws, size_t ws
   if (gh.sync.abort) return PIP_ERR_CUDA;
   if (timing_enabled() && (M.dbg & 4))
     fprintf(stderr, "[pip merge] CTA0 thread-0 cycles: merge %llu | merge imbalance + store-read wait %llu | "
-            "stage %llu | load wait %llu | copy-in + issue %llu | dataflow wait + store %llu\n",
+            "stage %llu | load wait %llu | publish + issue %llu | dataflow wait + store %llu\n",
             (unsigned long long)gh.sec[0], (unsigned long long)gh.sec[1], (unsigned long long)gh.sec[2],
             (unsigned long long)gh.sec[3], (unsigned long long)gh.sec[4], (unsigned long long)gh.sec[5]);
   if (timing_enabled())
