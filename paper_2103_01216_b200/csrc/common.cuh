@@ -234,6 +234,18 @@ __device__ __forceinline__ void mbar_wait(u64* bar, u32 phase) {
       "r"(phase)
       : "memory");
 }
+// one non-blocking probe of the phase with parity `phase`
+__device__ __forceinline__ bool mbar_try(u64* bar, u32 phase) {
+  u32 ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(phase)
+      : "memory");
+  return ok != 0;
+}
 // global -> shared bulk copy completing on `bar` (16-byte aligned, size % 16 == 0)
 __device__ __forceinline__ void tma_load_1d(void* sdst, const void* gsrc, u32 bytes, u64* bar) {
   asm volatile(

@@ -332,223 +332,52 @@ __global__ void __launch_bounds__(MG_THREADS, MG_CTAS_PER_SM) merge_kernel(Merge
 
   if (tm) g->t[4] = globaltimer_ns();
   // ---------------- P2: block merge under the dataflow rule
-  // Global traffic goes through the TMA engine only:
-  //   load   the <= 6 contiguous input segments of block m + G (A head in
-  //          place, <= 2 permuted A' chunks, <= 2 permuted B' chunks, B tail
-  //          in place), one bulk copy each, into one of two staging buffers
-  //          (each copy widened to 16-byte alignment: <= 2 junk words per
-  //          segment), while block m is merged out of the other buffer;
-  //   merge  straight from staging through the segment map (logical A/B
-  //          index -> staging word), a merge-path range of 16-17 consecutive
-  //          outputs per thread into registers.  The ranges start at
-  //          16t + (lane >> 1), which spreads a warp's reads and writes over
-  //          all shared-memory banks even for perfectly interleaved runs;
-  //   stage  registers -> the contiguous output buffer;
-  //   store  one bulk copy to a[mC, (m+1)C) once every block <= m + L has
-  //          reported its inputs loaded (the dataflow rule).
-  constexpr int MO = MG_PER_THREAD + 1;  // outputs per thread, at most
-  u64* s_outc = smem + 2 * MG_STAGE_WORDS;  // MG_C, contiguous
-  __shared__ __align__(8) u64 s_bar[2];
+  // Warp-specialized: warp 0 is the control warp, warps 1..15 merge.
+  //   load   (control) the <= 6 contiguous input segments of a block (A head
+  //          in place, <= 2 permuted A' chunks, <= 2 permuted B' chunks, B
+  //          tail in place), one bulk copy each into one of two staging
+  //          buffers, widened to 16-byte alignment (<= 2 junk words per
+  //          segment); "loaded" is published as soon as the bytes land;
+  //   merge  (merge warps) straight from staging through the segment map,
+  //          a merge-path range of 17-18 consecutive outputs per thread into
+  //          registers (ranges start at t*8192/480, not a multiple of 16
+  //          words, so a warp's shared accesses spread over the banks even
+  //          for perfectly interleaved runs); the staging buffer is handed
+  //          back at once, the registers go to the output buffer as soon as
+  //          the previous block's store has read it;
+  //   store  (control) one bulk copy of the output buffer to a[mC, (m+1)C)
+  //          once every block <= m + L has loaded (the dataflow rule).
+  // The dataflow wait of block m overlaps the merge of block m + G.
+  constexpr u32 NMW = MG_THREADS - 32;  // merge threads
+  constexpr int MO = (int)((MG_C + NMW - 1) / NMW) + 1;  // outputs per thread, at most
+  static_assert((2 * MG_STAGE_WORDS + MG_C) * 8 <= MG_SMEM, "two staging buffers + output");
+  u64* s_obuf = smem + 2 * MG_STAGE_WORDS;
+  __shared__ __align__(8) u64 s_full[2], s_sfree[2], s_ofull, s_ofree;
   __shared__ u32 s_seg[2][2 + 2 * 6];  // per buffer: na, nb | lo[6] | staging index[6]
-  ulonglong2 rec_a = make_ulonglong2(0, 0), rec_b = make_ulonglong2(0, 0);
-  auto fetch_plan = [&](u64 m) {
-    if (m < M.NB) {
-      rec_a = __ldcg(reinterpret_cast<const ulonglong2*>(M.plan + m));
-      rec_b = __ldcg(reinterpret_cast<const ulonglong2*>(M.plan + m) + 1);
-    }
+  // CTA 0 keeps block 0's output (it overwrites the in-place head, which any
+  // block may still read) in s_obuf to the end; its later blocks are written
+  // back into their own staging buffer and stored from there
+  const bool keep0 = M.hA > 0 && b == 0;
+  const u64 nblk = b < M.NB ? (M.NB - 1 - b) / G + 1 : 0;  // blocks of this CTA
+  auto in_place = [&](u64 j) { return keep0 && j > 0; };
+  auto wait_or_abort = [&](u64* bar, u32 ph) -> bool {
+    u32 n = 0;
+    while (!mbar_try(bar, ph))
+      if ((++n & 255) == 0 && ld_relaxed_u32(&g->sync.abort)) return false;
+    return true;
   };
-  // warp 0: the segments of block m (lane k computes segment k: 0 A head,
-  // 1-2 A' pieces, 3-4 B' pieces, 5 B tail), one bulk copy per lane into
-  // staging buffer `sb`, the segment map in s_seg[sb].  The plan record was
-  // fetched one block ahead.
-  auto issue_load = [&](u64 m, int sb) {
-    const u32 lane = tid;  // warp 0 only
-    u64* stage = smem + sb * MG_STAGE_WORDS;
-    const u64 p0 = m * MG_C, p1 = (m + 1) * MG_C < M.n ? (m + 1) * MG_C : M.n;
-    const u64 i0 = rec_a.x, i1 = rec_a.y;
-    const u32 da0 = (u32)rec_b.x, da1 = (u32)(rec_b.x >> 32);
-    const u32 db0 = (u32)rec_b.y, db1 = (u32)(rec_b.y >> 32);
-    fetch_plan(m + G);
-    const u64 j0 = p0 - i0, j1 = p1 - i1;
-    u64 ph = 0, len = 0;
-    if (lane == 0) {  // A head [i0, min(i1, hA))
-      const u64 xh = i1 < M.hA ? i1 : M.hA;
-      if (i0 < xh) { ph = i0; len = xh - i0; }
-    } else if (lane == 1 || lane == 2) {  // A' pieces
-      const u64 xs = i0 > M.hA ? i0 : M.hA;
-      if (xs < i1) {
-        const u64 ce = M.hA + (((xs - M.hA) >> MG_LOGC) + 1) * MG_C;  // end of first chunk
-        const u64 s0 = lane == 1 ? xs : ce, e0 = lane == 1 ? (ce < i1 ? ce : i1) : i1;
-        if (s0 < e0) {
-          ph = M.hA + ((u64)(lane == 1 ? da0 : da1) << MG_LOGC) + ((s0 - M.hA) & (MG_C - 1));
-          len = e0 - s0;
-        }
-      }
-    } else if (lane == 3 || lane == 4) {  // B' pieces
-      const u64 lb = M.nb - M.hB;
-      const u64 ye = j1 < lb ? j1 : lb;
-      if (j0 < ye) {
-        const u64 ce = ((j0 >> MG_LOGC) + 1) * MG_C;
-        const u64 s0 = lane == 3 ? j0 : ce, e0 = lane == 3 ? (ce < ye ? ce : ye) : ye;
-        if (s0 < e0) {
-          ph = M.hA + ((u64)(lane == 3 ? db0 : db1) << MG_LOGC) + (s0 & (MG_C - 1));
-          len = e0 - s0;
-        }
-      }
-    } else if (lane == 5) {  // B tail
-      const u64 lb = M.nb - M.hB;
-      const u64 ys = j0 > lb ? j0 : lb;
-      if (ys < j1) { ph = M.na + ys; len = j1 - ys; }
+  if (tid == 0) {
+    for (int q = 0; q < 2; ++q) {
+      mbar_init(&s_full[q], 1);
+      mbar_init(&s_sfree[q], 1);
     }
-    const u32 par = (u32)(((uintptr_t)(a + ph) >> 3) & 1u);
-    const u32 bytes = len ? ((par + (u32)len) * 8u + 15u) & ~15u : 0u;
-    // exclusive prefix sums over lanes 0..5 of len (logical start) and bytes
-    u32 lo = (u32)len, bo = bytes;
-#pragma unroll
-    for (int o = 1; o < 8; o <<= 1) {
-      const u32 l2 = __shfl_up_sync(0xffffffffu, lo, o), b2 = __shfl_up_sync(0xffffffffu, bo, o);
-      if (lane >= (u32)o) { lo += l2; bo += b2; }
-    }
-    const u32 total = __shfl_sync(0xffffffffu, bo, 7);
-    lo -= (u32)len;
-    bo -= bytes;
-    if (lane == 0) {
-      mbar_expect_tx(&s_bar[sb], total);
-      s_seg[sb][0] = (u32)(i1 - i0);
-      s_seg[sb][1] = (u32)(j1 - j0);
-    }
-    __syncwarp();
-    if (lane < 6) {
-      if (len) tma_load_1d(stage + bo / 8, a + ph - par, bytes, &s_bar[sb]);
-      s_seg[sb][2 + lane] = len ? lo : 0xffffffffu;
-      s_seg[sb][8 + lane] = bo / 8 + par;
-    }
-  };
-  // wait until every block <= upto has reported loaded.  Warp 0 issues the
-  // status loads early (pre_status, before the merge) so that in the common
-  // case the check costs no extra L2 round trip.
-  constexpr int MAXS = 8;  // statuses per lane (G <= 256)
-  u32 st_cache[MAXS];
-  auto pre_status = [&]() {
-    if (tid < 32) {
-#pragma unroll
-      for (int q = 0; q < MAXS; ++q) {
-        const u32 c = tid + 32 * q;
-        st_cache[q] = c < G ? ld_relaxed_u32(M.status + c) : 0xffffffffu;
-      }
-    }
-  };
-  auto wait_loaded = [&](u64 upto) -> bool {
-    if (tid < 32) {
-      u64 spins = 0;
-      int ok = 1;
-      bool first = true;
-      for (;;) {
-        bool ready = true;
-#pragma unroll
-        for (int q = 0; q < MAXS; ++q) {
-          const u32 c = tid + 32 * q;
-          if (c >= G || c > upto) continue;
-          const u32 mc = c + (((u32)upto - c) / G) * G;  // 32-bit: NB < 2^32
-          u32 v = st_cache[q];
-          if (!first || v < mc + 1) v = st_cache[q] = ld_relaxed_u32(M.status + c);
-          if (v < mc + 1) ready = false;
-        }
-        first = false;
-        if (__all_sync(0xffffffffu, ready)) break;
-        if (tid == 0) {
-          if (++spins > 32) __nanosleep(64);
-          if ((spins & 1023) == 0) {
-            if (ld_relaxed_u32(&g->sync.abort)) ok = 0;
-            else if (spins > (1ull << 25)) { atomicExch(&g->sync.abort, 1u); ok = 0; }
-          }
-        }
-        if (!__shfl_sync(0xffffffffu, ok, 0)) break;
-      }
-      // WAR only: the writes below are issued after these loads returned the
-      // flags, and a flag goes up only after its reader's bulk loads landed
-      if (tid == 0) s_flag = ok;
-    }
-    __syncthreads();
-    return s_flag != 0;
-  };
-  // this thread's output range [r0, r1) of the block
-  const u32 lane_t = tid & 31;
-  const u32 r0_all = tid * MG_PER_THREAD + (lane_t >> 1);
-  const u32 r1_all = lane_t == 31 ? (tid + 1) * MG_PER_THREAD : r0_all + MG_PER_THREAD + (((lane_t + 1) >> 1) - (lane_t >> 1));
-  // merge path over staging buffer `sb` through its segment map
-  auto merge_regs = [&](int sb, u32 na, u32 nb, u32& r0, u32& r1, u64 (&o)[MO]) {
-    const u64* sp = smem + sb * MG_STAGE_WORDS;
-    const u32 total = na + nb;
-    r0 = r0_all < total ? r0_all : total;
-    r1 = r1_all < total ? r1_all : total;
-    // A side: segments 0..2, B side: 3..5 (lo = logical start, 0xffffffff if absent)
-    const u32 la1 = s_seg[sb][3], la2 = s_seg[sb][4];
-    const u32 oa0 = s_seg[sb][2] == 0xffffffffu ? 0u : s_seg[sb][8] - s_seg[sb][2];
-    const u32 oa1 = s_seg[sb][9] - la1, oa2 = s_seg[sb][10] - la2;
-    const u32 lb4 = s_seg[sb][6], lb5 = s_seg[sb][7];
-    const u32 ob3 = s_seg[sb][5] == 0xffffffffu ? 0u : s_seg[sb][11] - s_seg[sb][5];
-    const u32 ob4 = s_seg[sb][12] - lb4, ob5 = s_seg[sb][13] - lb5;
-    auto mapA = [&](u32 x) -> u32 { return x + (x >= la2 ? oa2 : (x >= la1 ? oa1 : oa0)); };
-    auto mapB = [&](u32 x) -> u32 { return x + (x >= lb5 ? ob5 : (x >= lb4 ? ob4 : ob3)); };
-    if (r0 >= r1) return;
-    u32 lo = r0 > nb ? r0 - nb : 0, hi = r0 < na ? r0 : na;
-    while (lo < hi) {
-      const u32 mid = (lo + hi) >> 1;
-      if (sp[mapA(mid)] <= sp[mapB(na + r0 - mid - 1)]) lo = mid + 1;
-      else hi = mid;
-    }
-    u32 i = lo, j = r0 - lo;
-    u64 ka = sp[mapA(i)];
-    u64 kb = sp[mapB(na + j)];
-#pragma unroll
-    for (int q = 0; q < MO; ++q) {
-      const bool pa = (j >= nb) || (i < na && ka <= kb);  // ties from A
-      o[q] = pa ? ka : kb;
-      const u32 ni = i + (pa ? 1u : 0u), nj = j + (pa ? 0u : 1u);
-      // unconditional load (one word past a side's end is still staging
-      // memory), then select: no divergent branch per step
-      const u64 nk = sp[pa ? mapA(ni) : mapB(na + nj)];
-      ka = pa ? nk : ka;
-      kb = pa ? kb : nk;
-      i = ni;
-      j = nj;
-    }
-  };
-  // registers -> s_outc[r0, r1): lanes sit 16.5 words apart, so each 8-byte
-  // store of a warp covers all bank pairs twice (the minimum)
-  auto stage_out = [&](u32 r0, u32 r1, const u64 (&o)[MO]) {
-#pragma unroll
-    for (int q = 0; q < MO; ++q)
-      if (r0 + q < r1) s_outc[r0 + q] = o[q];
-  };
-  // thread 0: s_outc[0, len) -> a[p0, p0 + len) (16-byte-aligned middle by
-  // the TMA engine, <= 1 word at either end by hand)
-  auto store_out = [&](u64 m) {
-    const u64 p0 = m * MG_C, p1 = (m + 1) * MG_C < M.n ? (m + 1) * MG_C : M.n;
-    const u32 len = (u32)(p1 - p0);
-    const u32 head = (u32)(((uintptr_t)(a + p0) >> 3) & 1u);
-    const u32 body = len > head ? ((len - head) & ~1u) : 0u;
-    if (head && len) a[p0] = s_outc[0];
-    if (head + body < len) a[p0 + len - 1] = s_outc[len - 1];
-    if (body) {
-      tma_store_1d(a + p0 + head, s_outc + head, body * 8u);
-      bulk_commit();
-    }
-  };
-  auto store_regs = [&](u64 m, u32 r0, u32 r1, const u64 (&o)[MO]) {
-    const u64 p0 = m * MG_C;
-#pragma unroll
-    for (int q = 0; q < MO; ++q)
-      if (r0 + q < r1) a[p0 + r0 + q] = o[q];
-  };
-  // a plain flag store by a thread with no global stores in flight (thread 0
-  // issues the block stores; a release here would wait for them)
-  auto publish_loaded = [&](u64 m) {
-    if (tid == 32) st_relaxed_u32(M.status + b, (u32)(m + 1));
-  };
+    mbar_init(&s_ofull, 1);
+    mbar_init(&s_ofree, 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
 
-  const bool prof = (M.dbg & 4) && b == 0 && tid == 0;
+  const bool prof = (M.dbg & 4) && b == 0 && (tid == 0 || tid == 32);
   u64 cyc[6] = {0, 0, 0, 0, 0, 0};
   u64 c0 = clock64();
   auto mark = [&](int q) {
@@ -558,75 +387,250 @@ __global__ void __launch_bounds__(MG_THREADS, MG_CTAS_PER_SM) merge_kernel(Merge
       c0 = c1;
     }
   };
-  // CTA 0 keeps block 0's output (it overwrites the in-place head, which any
-  // block may still read) in s_outc until the end and stores its other
-  // blocks from registers
-  const bool keep0 = M.hA > 0 && b == 0;
-  u32 phase[2] = {0, 0};
-  if (tid == 0) {
-    mbar_init(&s_bar[0], 1);
-    mbar_init(&s_bar[1], 1);
-    mbar_fence_init();
-  }
-  __syncthreads();
-  u64 m = b;
-  int cur = 0;
-  if (tid < 32) fetch_plan(m);
-  if (m < M.NB) {
-    if (tid < 32) issue_load(m, 0);
-    mbar_wait(&s_bar[0], phase[0]);
-    phase[0] ^= 1;
-    publish_loaded(m);
-    if (tid < 32 && m + G < M.NB) issue_load(m + G, 1);
-    __syncthreads();  // s_seg[0] visible
-  }
-  for (; m < M.NB; m += G) {
-    pre_status();
-    const u32 na = s_seg[cur][0], nb = s_seg[cur][1];
-    u64 o[MO];
-    u32 r0, r1;
-    merge_regs(cur, na, nb, r0, r1, o);
-    mark(0);
-    const bool regs_path = keep0 && m != 0;
-    if (!regs_path) {
-      if (tid == 0) bulk_wait_read_all();  // the previous store has read s_outc
-      __syncthreads();
-      mark(1);
-      stage_out(r0, r1, o);
-      fence_proxy_async_smem();
-    }
-    __syncthreads();  // buffer `cur` consumed; s_outc complete
-    mark(2);
-    if (m + G < M.NB) {
-      mbar_wait(&s_bar[cur ^ 1], phase[cur ^ 1]);  // block m + G has landed
-      phase[cur ^ 1] ^= 1;
-      mark(3);
-      publish_loaded(m + G);
-      if (tid < 32 && m + 2 * G < M.NB) {
-        fence_proxy_async_smem();
-        issue_load(m + 2 * G, cur);
+
+  if (tid < 32) {
+    // ================================================= control warp
+    const u32 lane = tid;
+    ulonglong2 rec_a = make_ulonglong2(0, 0), rec_b = make_ulonglong2(0, 0);
+    auto fetch_plan = [&](u64 m) {
+      if (m < M.NB) {
+        rec_a = __ldcg(reinterpret_cast<const ulonglong2*>(M.plan + m));
+        rec_b = __ldcg(reinterpret_cast<const ulonglong2*>(M.plan + m) + 1);
       }
-    }
-    mark(4);
-    if (!(keep0 && m == 0)) {
+    };
+    // lane k computes segment k: 0 A head, 1-2 A' pieces, 3-4 B' pieces, 5 B tail
+    auto issue_load = [&](u64 m, int sb) {
+      u64* stage = smem + sb * MG_STAGE_WORDS;
+      const u64 p0 = m * MG_C, p1 = (m + 1) * MG_C < M.n ? (m + 1) * MG_C : M.n;
+      const u64 i0 = rec_a.x, i1 = rec_a.y;
+      const u32 da0 = (u32)rec_b.x, da1 = (u32)(rec_b.x >> 32);
+      const u32 db0 = (u32)rec_b.y, db1 = (u32)(rec_b.y >> 32);
+      fetch_plan(m + G);
+      const u64 j0 = p0 - i0, j1 = p1 - i1;
+      u64 ph = 0, len = 0;
+      if (lane == 0) {  // A head [i0, min(i1, hA))
+        const u64 xh = i1 < M.hA ? i1 : M.hA;
+        if (i0 < xh) { ph = i0; len = xh - i0; }
+      } else if (lane == 1 || lane == 2) {  // A' pieces
+        const u64 xs = i0 > M.hA ? i0 : M.hA;
+        if (xs < i1) {
+          const u64 ce = M.hA + (((xs - M.hA) >> MG_LOGC) + 1) * MG_C;  // end of first chunk
+          const u64 s0 = lane == 1 ? xs : ce, e0 = lane == 1 ? (ce < i1 ? ce : i1) : i1;
+          if (s0 < e0) {
+            ph = M.hA + ((u64)(lane == 1 ? da0 : da1) << MG_LOGC) + ((s0 - M.hA) & (MG_C - 1));
+            len = e0 - s0;
+          }
+        }
+      } else if (lane == 3 || lane == 4) {  // B' pieces
+        const u64 lb = M.nb - M.hB;
+        const u64 ye = j1 < lb ? j1 : lb;
+        if (j0 < ye) {
+          const u64 ce = ((j0 >> MG_LOGC) + 1) * MG_C;
+          const u64 s0 = lane == 3 ? j0 : ce, e0 = lane == 3 ? (ce < ye ? ce : ye) : ye;
+          if (s0 < e0) {
+            ph = M.hA + ((u64)(lane == 3 ? db0 : db1) << MG_LOGC) + (s0 & (MG_C - 1));
+            len = e0 - s0;
+          }
+        }
+      } else if (lane == 5) {  // B tail
+        const u64 lb = M.nb - M.hB;
+        const u64 ys = j0 > lb ? j0 : lb;
+        if (ys < j1) { ph = M.na + ys; len = j1 - ys; }
+      }
+      const u32 par = (u32)(((uintptr_t)(a + ph) >> 3) & 1u);
+      const u32 bytes = len ? ((par + (u32)len) * 8u + 15u) & ~15u : 0u;
+      u32 lo = (u32)len, bo = bytes;  // exclusive prefix sums over lanes 0..5
+#pragma unroll
+      for (int o = 1; o < 8; o <<= 1) {
+        const u32 l2 = __shfl_up_sync(0xffffffffu, lo, o), b2 = __shfl_up_sync(0xffffffffu, bo, o);
+        if (lane >= (u32)o) { lo += l2; bo += b2; }
+      }
+      const u32 total = __shfl_sync(0xffffffffu, bo, 7);
+      lo -= (u32)len;
+      bo -= bytes;
+      if (lane < 6) {
+        s_seg[sb][2 + lane] = len ? lo : 0xffffffffu;
+        s_seg[sb][8 + lane] = bo / 8 + par;
+      }
+      if (lane == 0) {
+        s_seg[sb][0] = (u32)(i1 - i0);
+        s_seg[sb][1] = (u32)(j1 - j0);
+      }
+      __syncwarp();
+      // the expect_tx arrive releases the map above to whoever observes the flip
+      if (lane == 0) mbar_expect_tx(&s_full[sb], total);
+      __syncwarp();
+      if (lane < 6 && len) tma_load_1d(stage + bo / 8, a + ph - par, bytes, &s_full[sb]);
+    };
+    // every block <= upto has reported loaded (lanes poll 8 CTAs each).
+    // WAR only: the store is issued after these loads returned the flags, and
+    // a flag goes up only after its reader's bulk loads landed.
+    constexpr int MAXS = 8;  // G <= 256
+    auto wait_loaded = [&](u64 upto) -> bool {
+      u64 spins = 0;
+      for (;;) {
+        bool ready = true;
+#pragma unroll
+        for (int q = 0; q < MAXS; ++q) {
+          const u32 c = lane + 32 * q;
+          if (c >= G || c > upto) continue;
+          const u32 mc = c + (((u32)upto - c) / G) * G;  // 32-bit: NB < 2^32
+          if (ld_relaxed_u32(M.status + c) < mc + 1) ready = false;
+        }
+        // WAR only: the store below is issued after these loads returned the
+        // flags, and a flag goes up only after its reader's bulk loads landed
+        if (__all_sync(0xffffffffu, ready)) return true;
+        int ok = 1;
+        if (lane == 0) {
+          if (++spins > 32) __nanosleep(64);
+          if ((spins & 1023) == 0) {
+            if (ld_relaxed_u32(&g->sync.abort)) ok = 0;
+            else if (spins > (1ull << 25)) { atomicExch(&g->sync.abort, 1u); ok = 0; }
+          }
+        }
+        if (!__shfl_sync(0xffffffffu, ok, 0)) return false;
+      }
+    };
+    fetch_plan(b);
+    for (u64 j = 0; j < nblk && j < 2; ++j) issue_load(b + j * G, (int)j);
+    // (an event loop that polls loads, refills and the dataflow rule without
+    // blocking measured slower: 38 vs 32 ms at 2^32 — the status poll is an
+    // L2 round trip on every pass)
+    bool ok = true;
+    for (u64 j = 0; j < nblk; ++j) {
+      const u64 m = b + j * G;
+      const int sb = (int)(j & 1);
+      const u32 use = (u32)(j >> 1);
+      if (j == 0) {  // publish block 0's load
+        if (!wait_or_abort(&s_full[0], 0)) { ok = false; break; }
+        if (lane == 0) st_relaxed_u32(M.status + b, (u32)(m + 1));
+      }
+      // the merge warps have read block j: its staging buffer takes block j+2
+      if (!in_place(j)) {
+        if (!wait_or_abort(&s_sfree[sb], use & 1)) { ok = false; break; }
+        if (j + 2 < nblk) {
+          if (lane == 0) fence_proxy_async_smem();
+          __syncwarp();
+          issue_load(m + 2 * G, sb);
+        }
+      }
+      // publish block j+1's load as soon as it has landed
+      if (j + 1 < nblk) {
+        if (!wait_or_abort(&s_full[sb ^ 1], ((j + 1) >> 1) & 1)) { ok = false; break; }
+        if (lane == 0) st_relaxed_u32(M.status + b, (u32)(m + G + 1));
+      }
+      mark(0);
+      if (!wait_or_abort(&s_ofull, (u32)(j & 1))) { ok = false; break; }  // output written
+      mark(1);
+      if (keep0 && j == 0) continue;  // block 0 is written after the final barrier
       const u64 upto = m + M.L < M.NB - 1 ? m + M.L : M.NB - 1;
-      if (!(M.dbg & 1) && !wait_loaded(upto)) return;  // (its __syncthreads also
-      if (regs_path) store_regs(m, r0, r1, o);         //  publishes s_seg[cur])
-      else if (tid == 0) store_out(m);
-      mark(5);
-    } else {
-      __syncthreads();  // s_seg[cur] (block 2G) visible before the next merge
+      if (!(M.dbg & 1) && !wait_loaded(upto)) { ok = false; break; }
+      mark(2);
+      const u64* out = in_place(j) ? smem + sb * MG_STAGE_WORDS : s_obuf;
+      if (lane == 0) {
+        const u64 p0 = m * MG_C, p1 = (m + 1) * MG_C < M.n ? (m + 1) * MG_C : M.n;
+        const u32 len = (u32)(p1 - p0);
+        const u32 head = (u32)(((uintptr_t)(a + p0) >> 3) & 1u);
+        const u32 body = len > head ? ((len - head) & ~1u) : 0u;
+        if (head && len) a[p0] = out[0];
+        if (head + body < len) a[p0 + len - 1] = out[len - 1];
+        if (body) {
+          tma_store_1d(a + p0 + head, out + head, body * 8u);
+          bulk_commit();
+          bulk_wait_read_all();  // the buffer may be rewritten
+        }
+        if (!in_place(j)) mbar_arrive(&s_ofree);
+      }
+      __syncwarp();
+      if (in_place(j) && j + 2 < nblk) {  // the store has read it: refill
+        if (lane == 0) fence_proxy_async_smem();
+        __syncwarp();
+        issue_load(m + 2 * G, sb);
+      }
+      mark(3);
     }
-    cur ^= 1;
+    if (lane == 0) bulk_wait_all();
+    if (!ok && lane == 0) atomicExch(&g->sync.abort, 1u);
+  } else {
+    // ================================================= merge warps
+    const u32 t = tid - 32;
+    const u32 r0_all = (u32)(((u64)t * MG_C) / NMW), r1_all = (u32)(((u64)(t + 1) * MG_C) / NMW);
+    u32 ofree_uses = 0;  // completed phases of s_ofree
+    for (u64 j = 0; j < nblk; ++j) {
+      const int sb = (int)(j & 1);
+      if (!wait_or_abort(&s_full[sb], (u32)((j >> 1) & 1))) break;
+      u64* sp = smem + sb * MG_STAGE_WORDS;
+      const u32 na = s_seg[sb][0], nb = s_seg[sb][1], total = na + nb;
+      const u32 r0 = r0_all < total ? r0_all : total, r1 = r1_all < total ? r1_all : total;
+      // segment map: A side segments 0..2, B side 3..5 (lo = logical start,
+      // 0xffffffff if absent); staging word = logical + offset of its segment
+      const u32 la1 = s_seg[sb][3], la2 = s_seg[sb][4];
+      const u32 oa0 = s_seg[sb][2] == 0xffffffffu ? 0u : s_seg[sb][8] - s_seg[sb][2];
+      const u32 oa1 = s_seg[sb][9] - la1, oa2 = s_seg[sb][10] - la2;
+      const u32 lb4 = s_seg[sb][6], lb5 = s_seg[sb][7];
+      const u32 ob3 = s_seg[sb][5] == 0xffffffffu ? 0u : s_seg[sb][11] - s_seg[sb][5];
+      const u32 ob4 = s_seg[sb][12] - lb4, ob5 = s_seg[sb][13] - lb5;
+      auto mapA = [&](u32 x) -> u32 { return x + (x >= la2 ? oa2 : (x >= la1 ? oa1 : oa0)); };
+      auto mapB = [&](u32 x) -> u32 { return x + (x >= lb5 ? ob5 : (x >= lb4 ? ob4 : ob3)); };
+      u64 o[MO];
+      if (r0 < r1) {
+        u32 lo = r0 > nb ? r0 - nb : 0, hi = r0 < na ? r0 : na;
+        while (lo < hi) {
+          const u32 mid = (lo + hi) >> 1;
+          if (sp[mapA(mid)] <= sp[mapB(na + r0 - mid - 1)]) lo = mid + 1;
+          else hi = mid;
+        }
+        u32 i = lo, jj = r0 - lo;
+        u64 ka = sp[mapA(i)];
+        u64 kb = sp[mapB(na + jj)];
+#pragma unroll
+        for (int q = 0; q < MO; ++q) {
+          const bool pa = (jj >= nb) || (i < na && ka <= kb);  // ties from A
+          o[q] = pa ? ka : kb;
+          const u32 ni = i + (pa ? 1u : 0u), nj = jj + (pa ? 0u : 1u);
+          // unconditional load (one word past a side's end is still staging
+          // memory), then select: no divergent branch per step
+          const u64 nk = sp[pa ? mapA(ni) : mapB(na + nj)];
+          ka = pa ? nk : ka;
+          kb = pa ? kb : nk;
+          i = ni;
+          jj = nj;
+        }
+      }
+      mark(0);
+      named_bar(1, NMW);  // every merge warp is done reading the staging buffer
+      u64* out = s_obuf;
+      if (in_place(j)) {
+        out = sp;
+      } else {
+        if (t == 0) mbar_arrive(&s_sfree[sb]);
+        if (j > 0 && !(keep0)) {  // the previous block's store has read s_obuf
+          if (!wait_or_abort(&s_ofree, ofree_uses & 1)) break;
+          ++ofree_uses;
+        }
+      }
+      mark(1);
+#pragma unroll
+      for (int q = 0; q < MO; ++q)
+        if (r0 + q < r1) out[r0 + q] = o[q];
+      fence_proxy_async_smem();
+      named_bar(1, NMW);
+      if (t == 0) mbar_arrive(&s_ofull);
+      mark(2);
+    }
   }
-  if (prof)
-    for (int q = 0; q < 6; ++q) g->sec[q] = cyc[q];
-  if (tid == 0) bulk_wait_all();
+  if (prof && tid == 32)
+    for (int q = 0; q < 3; ++q) g->sec[q] = cyc[q];
+  if (prof && tid == 0) {
+    g->sec[3] = cyc[0] + cyc[1];  // waiting for loads to land / for the merge warps
+    g->sec[4] = cyc[2];           // dataflow rule
+    g->sec[5] = cyc[3];           // store (+ refill issue)
+  }
   if (M.hA > 0) {
     if (!grid_barrier(&g->sync, gen)) return;
     if (b == 0) {
       const u64 p1 = MG_C < M.n ? MG_C : M.n;
-      for (u32 k = tid; k < (u32)p1; k += MG_THREADS) a[k] = s_outc[k];
+      for (u32 k = tid; k < (u32)p1; k += MG_THREADS) a[k] = s_obuf[k];
     }
   }
   if (tm) g->t[5] = globaltimer_ns();
@@ -798,8 +802,8 @@ int merge_device(u64* a, u64 n, u64 split, int check_sorted, void* ws, size_t ws
   PIP_CUDA(cudaStreamSynchronize(st));
   if (gh.sync.abort) return PIP_ERR_CUDA;
   if (timing_enabled() && (M.dbg & 4))
-    fprintf(stderr, "[pip merge] CTA0 thread-0 cycles: merge %llu | merge imbalance + store-read wait %llu | "
-            "stage %llu | load wait %llu | publish + issue %llu | dataflow wait + store %llu\n",
+    fprintf(stderr, "[pip merge] CTA0 cycles: merge warps: merge (+ wait data) %llu | wait output buffer %llu | write-out %llu ; "
+            "control: loads/merge wait %llu | dataflow wait %llu | store %llu\n",
             (unsigned long long)gh.sec[0], (unsigned long long)gh.sec[1], (unsigned long long)gh.sec[2],
             (unsigned long long)gh.sec[3], (unsigned long long)gh.sec[4], (unsigned long long)gh.sec[5]);
   if (timing_enabled())
