@@ -13,9 +13,10 @@
 // it, 10.6 ms with it removed).  What helped: slots spaced `stride` apart in
 // memory so a window spans several L2 lines (14.0 -> 13.0 ms).  What did not:
 // 128-slot windows (4 loads per lane: 19 ms), block-wide windows, smaller
-// tiles (more waves), 2-stage 96 KiB tiles (load latency exposed), and
-// clusters of 2-4 CTAs sharing one chain step (18 ms: the DSMEM hand-offs
-// add a hop per wave).
+// tiles (more waves), 2-stage 96 KiB tiles (load latency exposed), clusters
+// of 2-4 CTAs sharing one chain step (18 ms: the DSMEM hand-offs add a hop
+// per wave), and pairs of tiles per chain step with separate producer /
+// look-back warps (13.9 ms: less overlap between look-back and compute).
 //
 // A slot is 16 bytes {value, (epoch << 2) | state} published with ONE 128-bit
 // store and read with ONE 128-bit load, so a reader always sees a value
