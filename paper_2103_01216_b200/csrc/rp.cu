@@ -300,9 +300,9 @@ __global__ void __launch_bounds__(RP_THREADS, 4) rp_kernel(RpArgs A) {
           const u64 k = kb + q;
           iv[q] = tv[q] = 0;
           if (k < e) {
-            const bool com = __ldcg(A.cflag + k);
-            iv[q] = __ldcg(ids_o + k);
-            tv[q] = __ldcg(tg_o + k);
+            const bool com = __ldcs(A.cflag + k);
+            iv[q] = __ldcs(ids_o + k);
+            tv[q] = __ldcs(tg_o + k);
             if (com) cm |= 1u << q;
             else fm |= 1u << q;
           }
@@ -381,7 +381,7 @@ __global__ void __launch_bounds__(RP_THREADS, 4) rp_kernel(RpArgs A) {
 #pragma unroll 4
       for (u64 q = s + tid; q < e; q += T) {
         const u64 id = hi - q;
-        c += __ldg(A.h + id) != id;
+        c += __ldcs(A.h + id) != id;
       }
       c = block_sum(c, s_red);
       if (tid == 0) A.wcnt[b] = (u32)c;
@@ -434,7 +434,7 @@ __global__ void __launch_bounds__(RP_THREADS, 4) rp_kernel(RpArgs A) {
           hv[q] = 0;
           if (qb + q < e) {
             const u64 id = hi - (qb + q);
-            hv[q] = __ldg(A.h + id);
+            hv[q] = __ldcs(A.h + id);
             if (hv[q] != id) fm |= 1u << q;
           }
         }
@@ -479,7 +479,7 @@ __global__ void __launch_bounds__(RP_THREADS, 4) rp_kernel(RpArgs A) {
         for (u64 k0 = s + tid; k0 < e; k0 += (u64)RB * T) {
           u32 t[RB], old[RB];
 #pragma unroll
-          for (int q = 0; q < RB; ++q) t[q] = k0 + q * T < e ? __ldcg(tg_n + k0 + q * T) : 0u;
+          for (int q = 0; q < RB; ++q) t[q] = k0 + q * T < e ? __ldcs(tg_n + k0 + q * T) : 0u;
 #pragma unroll
           for (int q = 0; q < RB; ++q)
             old[q] = k0 + q * T < e ? atomicOr(A.bmB + (t[q] >> 5), 1u << (t[q] & 31)) : 0u;
@@ -502,7 +502,7 @@ __global__ void __launch_bounds__(RP_THREADS, 4) rp_kernel(RpArgs A) {
         for (u64 k0 = s + tid; k0 < e; k0 += (u64)RB * T) {
           u32 t[RB], old[RB];
 #pragma unroll
-          for (int q = 0; q < RB; ++q) t[q] = k0 + q * T < e ? __ldcg(tg_n + k0 + q * T) : 0u;
+          for (int q = 0; q < RB; ++q) t[q] = k0 + q * T < e ? __ldcs(tg_n + k0 + q * T) : 0u;
 #pragma unroll
           for (int q = 0; q < RB; ++q)
             old[q] = k0 + q * T < e ? atomicOr(A.bmB + (t[q] >> 5), 1u << (t[q] & 31)) : 0u;
@@ -520,7 +520,7 @@ __global__ void __launch_bounds__(RP_THREADS, 4) rp_kernel(RpArgs A) {
         if (tid == 0) A.lccnt[b] = s_cnt[32];
       } else {
       for (u64 k = s + tid; k < e; k += T) {
-        const u32 i = __ldcg(ids_n + k), t = __ldcg(tg_n + k);
+        const u32 i = __ldcs(ids_n + k), t = __ldcs(tg_n + k);
         u32 sl = RP_NOSLOT;
         if (V == PIP_RP_FINAL && t >= dlo && t <= dhi) {
           atomicMax(A.dense + (dhi - t), i + 1u);
@@ -548,7 +548,7 @@ __global__ void __launch_bounds__(RP_THREADS, 4) rp_kernel(RpArgs A) {
       part(newF, G, b, s, e);
       u32 fails = 0, dclaim = 0;
       for (u64 k = s + tid; k < e; k += T) {
-        const u32 t = __ldcg(tg_n + k), i = __ldcg(ids_n + k);
+        const u32 t = __ldcs(tg_n + k), i = __ldcs(ids_n + k);
         if ((__ldcg(A.bmC + (t >> 5)) >> (t & 31)) & 1u) {
           A.slot[k] = table_reserve(A.table, A.logcap, t, i, dclaim, &g->sync.error);
           A.cflag[k] = 2;
@@ -566,8 +566,8 @@ __global__ void __launch_bounds__(RP_THREADS, 4) rp_kernel(RpArgs A) {
       }
       if (!grid_barrier(&g->sync, gen)) break;
       for (u64 k = s + tid; k < e; k += T) {
-        if (__ldcg(A.cflag + k) != 2) continue;
-        const u32 t = __ldcg(tg_n + k), i = __ldcg(ids_n + k);
+        if (__ldcs(A.cflag + k) != 2) continue;
+        const u32 t = __ldcs(tg_n + k), i = __ldcs(ids_n + k);
         const bool own = !((__ldcg(A.bmB + (i >> 5)) >> (i & 31)) & 1u);
         const u32 sl = __ldcg(A.slot + k);
         const u64 w = sl == RP_NOSLOT ? RP_EMPTY : __ldcg(A.table + sl);
@@ -609,7 +609,7 @@ __global__ void __launch_bounds__(RP_THREADS, 4) rp_kernel(RpArgs A) {
         const u32 mine = __ldcg(A.lccnt + b);
         for (u32 q = tid; q < mine; q += T) {
           const u64 k = s + __ldcg(A.lc + s + q);
-          table_reserve(A.table, lg, __ldcg(tg_n + k), __ldcg(ids_n + k), dclaim, &g->sync.error);
+          table_reserve(A.table, lg, __ldcs(tg_n + k), __ldcs(ids_n + k), dclaim, &g->sync.error);
         }
         if (!grid_barrier(&g->sync, gen)) break;
       }
@@ -622,16 +622,16 @@ __global__ void __launch_bounds__(RP_THREADS, 4) rp_kernel(RpArgs A) {
       u64 k = s + tid;
       u32 ncf = 1, nt = 0, ni = 0;
       if (k < e) {
-        ncf = __ldcg(A.cflag + k);
-        nt = __ldcg(tg_n + k);
-        ni = __ldcg(ids_n + k);
+        ncf = __ldcs(A.cflag + k);
+        nt = __ldcs(tg_n + k);
+        ni = __ldcs(ids_n + k);
       }
       for (; k < e; k += T) {
         const u32 cf = ncf, t = nt, i = ni;
         if (k + T < e) {
-          ncf = __ldcg(A.cflag + k + T);
-          nt = __ldcg(tg_n + k + T);
-          ni = __ldcg(ids_n + k + T);
+          ncf = __ldcs(A.cflag + k + T);
+          nt = __ldcs(tg_n + k + T);
+          ni = __ldcs(ids_n + k + T);
         }
         if (cf) continue;
         const u64 w0 = lc_total ? __ldcg(A.table + rp_home(t, lg)) : RP_EMPTY;
@@ -656,8 +656,8 @@ __global__ void __launch_bounds__(RP_THREADS, 4) rp_kernel(RpArgs A) {
         if (!grid_barrier(&g->sync, gen)) break;
         // P4: iterates on collided targets
         for (u64 k = s + tid; k < e; k += T) {
-          if (__ldcg(A.cflag + k) != 2) continue;
-          const u32 t = __ldcg(tg_n + k), i = __ldcg(ids_n + k);
+          if (__ldcs(A.cflag + k) != 2) continue;
+          const u32 t = __ldcs(tg_n + k), i = __ldcs(ids_n + k);
           const bool own = !((__ldcg(A.bmB + (i >> 5)) >> (i & 31)) & 1u);
           u32 v = 0;
           const bool c = own && table_lookup(A.table, lg, t, v) && v == i;
@@ -686,7 +686,7 @@ __global__ void __launch_bounds__(RP_THREADS, 4) rp_kernel(RpArgs A) {
       part(newF, G, b, s, e);
       u32 fails = 0;
       for (u64 k = s + tid; k < e; k += T) {
-        const u32 i = __ldcg(ids_n + k), t = __ldcg(tg_n + k);
+        const u32 i = __ldcs(ids_n + k), t = __ldcs(tg_n + k);
         bool own, tgt;
         u32 v = 0;
         if (V == PIP_RP_FINAL && k >= nfail) {
