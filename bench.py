@@ -483,9 +483,10 @@ def run_rp(args, ws, rank, local, torch, pip, lib, small: bool):
     rmw_rate = upd / (msf.value / 1e3)
     del buf
     swaps_rate = iters / (per_step / 1e3)
+    tb = None if small else ncu_traffic("rp")
     roof = {"bound": "hbm", "achieved": round(swaps_rate * 32 / 1e9, 1),
             "peak": round(rmw_rate * 32 / 1e9, 1), "unit": "GB/s",
-            "frac": round(swaps_rate / rmw_rate, 4), "traffic": None,
+            "frac": round(swaps_rate / rmw_rate, 4), "traffic": (tb * n) if tb else None,
             "note": "random-sector roofline: one 32-B sector RMW per committed swap "
                     f"({iters} swaps) vs a measured random 8-B RMW microbenchmark over "
                     f"{bufn} words ({rmw_rate / 1e9:.2f} G RMW/s)"}
