@@ -112,6 +112,9 @@ class ClockSampler:
                 ["nvidia-smi", "-i", sel, f"--query-gpu={self.FIELDS}",
                  "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=self.f, stderr=subprocess.DEVNULL)
+            # nvidia-smi takes a moment to start (and may buffer its output):
+            # give it time to be sampling before a short timed region begins
+            time.sleep(0.6)
         except Exception:
             self.proc = None
 
@@ -540,7 +543,7 @@ def e2e_host(lib, op, n, args, torch, dev, ws, **kw):
         hh.copy_(kw["h"])
     total = 0.0
     bi = bo = 0
-    for _ in range(steps):
+    for it in range(steps + 1):  # the first call is an untimed warm-up (pools, pinned staging)
         fill()
         t0 = time.perf_counter()
         if op == "scan":
@@ -564,7 +567,8 @@ def e2e_host(lib, op, n, args, torch, dev, ws, **kw):
             rc = lib.pip_random_permutation_u64_host(hp, hh.data_ptr(), n, kw["prefix"], 3,
                                                      C.byref(stats), dev)
             bi, bo = 16 * n, 8 * n
-        total += time.perf_counter() - t0
+        if it > 0:
+            total += time.perf_counter() - t0
         assert rc == 0, rc
     del d
     return {"value": n * steps / total, "unit": "elements/s", "h2d_bytes_per_step": bi,
