@@ -575,6 +575,180 @@ filter_ws_kernel(u64* __restrict__ a, DevPred p, u64* m_out, LookbackCtx c, u64 
   }
 }
 
+// Split-role pipeline (see scan_ws2_kernel): warp 0 streams tiles in, LBW
+// look-back warps take tiles round-robin so consecutive look-backs overlap,
+// NWC compute warps count tile k and compact + store tile k - D.
+template <int NWC, int S, int PC, int LBW, int D>
+__global__ void __launch_bounds__(32 * (NWC + 1 + LBW), 1)
+filter_ws2_kernel(u64* __restrict__ a, DevPred p, u64* m_out, LookbackCtx c, u64 num_tiles) {
+  using O = Op<PIP_OP_ADD>;
+  constexpr u64 TILE = (u64)NWC * 512;
+  constexpr u32 TILE_BYTES = (u32)(TILE * 8);
+  constexpr u64 STRIDE = TILE + 2;  // + 2 words: the compacted output may start one word in
+  static_assert(S >= D + 2, "stages");
+  extern __shared__ __align__(128) u64 ring[];
+  __shared__ __align__(8) u64 full[S], reduced[S], pready[S], empty[S];
+  __shared__ u64 s_wtot[S][NWC];
+  __shared__ u64 s_wexc[S][NWC];
+  __shared__ u64 s_agg[S];
+  __shared__ u64 s_prefix[S];
+  __shared__ u32 s_keep[S][NWC * 32];
+  __shared__ volatile int s_abort;
+  const u32 tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const u32 lt = (1u << lane) - 1u;
+  const u64 G = gridDim.x, B = blockIdx.x;
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&reduced[s], 1);
+      mbar_init(&pready[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    s_abort = 0;
+    mbar_fence_init();
+  }
+  __syncthreads();
+  auto ph = [&](u64 k) { return (u32)((k / S) & 1); };
+  auto wait_or_abort = [&](u64* bar, u32 phase) -> bool {
+    while (!mbar_try(bar, phase))
+      if (s_abort) return false;
+    return true;
+  };
+  if (warp == 0) {
+    // ------------------------------------------------------------ producer
+    for (u64 k = 0; B + k * G < num_tiles; ++k) {
+      const int s = (int)(k % S);
+      if (k >= (u64)S && !wait_or_abort(&empty[s], (u32)(((k / S) - 1) & 1))) return;
+      if (lane == 0) {
+        fence_proxy_async_smem();
+        const u64 t = B + k * G;
+        mbar_expect_tx(&full[s], TILE_BYTES);
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          tma_load_1d(ring + s * STRIDE + q * (TILE / 4), a + t * TILE + q * (TILE / 4), TILE_BYTES / 4,
+                      &full[s]);
+      }
+      __syncwarp();
+    }
+    return;
+  }
+  if (warp <= (u32)LBW) {
+    // ------------------------------------------------ look-back, k = warp-1 mod LBW
+    for (u64 k = warp - 1; B + k * G < num_tiles; k += LBW) {
+      const int s = (int)(k % S);
+      const u64 t = B + k * G;
+      if (!wait_or_abort(&reduced[s], ph(k))) return;
+      const u64 agg = s_agg[s];
+      u64 prefix = 0;
+      int ok = 1;
+      if (lane == 0) {
+        ok = publish_begin(c, t);
+        if (ok) {
+          __threadfence();
+          if (t == 0) publish_incl(c, 0, agg);
+          else publish_agg(c, t, agg);
+        }
+      }
+      ok = __shfl_sync(0xffffffffu, ok, 0);
+      if (ok && t > 0) {
+        ok = lookback<O>(c, t, prefix);
+        if (ok && lane == 0) publish_incl(c, t, prefix + agg);
+      }
+      if (lane == 0) {
+        s_prefix[s] = prefix;
+        if (!ok) s_abort = 1;
+        if (ok && t == num_tiles - 1 && m_out) *m_out = prefix + agg;
+        mbar_arrive(&pready[s]);
+      }
+      if (!ok) return;
+    }
+    return;
+  }
+  // ---------------------------------------------------------------- compute
+  const u32 w = warp - 1 - LBW;
+  // the kept words of a tile are compacted inside its own stage buffer (every
+  // warp first pulls its 16 words per lane into registers) and leave with one
+  // bulk store; only <= 2 ragged words go through the LSU
+  auto scatter = [&](u64 k) -> bool {
+    const int s = (int)(k % S);
+    if (!wait_or_abort(&pready[s], ph(k))) return false;
+    const u64 prefix = s_prefix[s];
+    const u64 agg = s_agg[s];
+    u64* stage = ring + s * STRIDE;
+    // word parity of the destination: compacted word q sits at stage[par + q]
+    // so that shared and global addresses agree modulo 16 bytes
+    const u32 par = (u32)(((uintptr_t)(a + prefix) >> 3) & 1u);
+    u32 run = (u32)s_wexc[s][w] + par;
+    const u32 keep = s_keep[s][w * 32 + lane];
+    const u64* src = stage + w * 512;
+    u64 vx[8], vy[8];
+    u32 pos[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const bool f0 = (keep >> (2 * j)) & 1u, f1 = (keep >> (2 * j + 1)) & 1u;
+      const u32 m0 = __ballot_sync(0xffffffffu, f0);
+      const u32 m1 = __ballot_sync(0xffffffffu, f1);
+      pos[j] = run + __popc(m0 & lt) + __popc(m1 & lt);
+      const ulonglong2 v = lds2(src + 64 * j + 2 * lane);
+      vx[j] = v.x;
+      vy[j] = v.y;
+      run += __popc(m0) + __popc(m1);
+    }
+    named_bar(1, NWC * 32);  // the whole tile is in registers
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const bool f0 = (keep >> (2 * j)) & 1u, f1 = (keep >> (2 * j + 1)) & 1u;
+      if (f0) stage[pos[j]] = vx[j];
+      if (f1) stage[pos[j] + (f0 ? 1u : 0u)] = vy[j];
+    }
+    fence_proxy_async_smem();
+    named_bar(1, NWC * 32);
+    if (w == 0 && lane == 0) {
+      const u32 head = par && agg ? 1u : 0u;
+      const u32 body = (u32)((agg - head) & ~1ull);
+      if (head) a[prefix] = stage[1];
+      if (head + body < agg) a[prefix + agg - 1] = stage[par + agg - 1];
+      if (body) {
+        tma_store_1d(a + prefix + head, stage + par + head, body * 8u);
+        bulk_commit();
+        bulk_wait_read_all();  // the stage may be refilled once the store has read it
+      }
+      mbar_arrive(&empty[s]);
+    }
+    return true;
+  };
+  for (u64 k = 0;; ++k) {
+    const int s = (int)(k % S);
+    if (B + k * G >= num_tiles) {
+      for (u64 q = k > (u64)D ? k - D : 0; q < k; ++q)
+        if (!scatter(q)) break;
+      break;
+    }
+    if (!wait_or_abort(&full[s], ph(k))) break;
+    const u64* src = ring + s * STRIDE + w * 512;
+    u32 keep = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const ulonglong2 v = lds2(src + 64 * j + 2 * lane);
+      keep |= ((u32)pred_eval_t<PC>(p, v.x) << (2 * j)) | ((u32)pred_eval_t<PC>(p, v.y) << (2 * j + 1));
+    }
+    s_keep[s][w * 32 + lane] = keep;
+    const u64 cnt = warp_reduce<O>((u64)__popc(keep));
+    if (lane == 0) s_wtot[s][w] = cnt;
+    named_bar(1, NWC * 32);
+    if (w == 0) {
+      const u64 wv = lane < (u32)NWC ? s_wtot[s][lane] : 0;
+      const u64 winc = warp_incl_scan<O>(wv);
+      if (lane < (u32)NWC) s_wexc[s][lane] = winc - wv;
+      if (lane == NWC - 1) s_agg[s] = winc;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&reduced[s]);
+    }
+    if (k >= (u64)D && !scatter(k - D)) break;
+  }
+  if (w == 0 && lane == 0) bulk_wait_all();  // the bulk stores have landed
+}
+
 template <int PC>
 __global__ void __launch_bounds__(512)
 count_kernel(const u64* __restrict__ a, u64 n, DevPred p, u64* partials, u32* counter, u64* total) {
@@ -768,6 +942,45 @@ static int launch_filter_ws_pc(u64* a, u64 n, const DevPred& p, u64* m_dev,
   return PIP_OK;
 }
 
+template <int NWC, int S, int PC, int LBW, int D>
+static int launch_filter_ws2_pc(u64* a, u64 n, const DevPred& p, u64* m_dev,
+                                const ScratchLayoutF& L, cudaStream_t st, int dev) {
+  constexpr u64 TILE = (u64)NWC * 512;
+  constexpr int THREADS = 32 * (NWC + 1 + LBW);
+  const u64 full_tiles = n / TILE, rem = n - full_tiles * TILE;
+  auto k = filter_ws2_kernel<NWC, S, PC, LBW, D>;
+  const int smem = (int)(S * (TILE + 2) * 8);
+  PIP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  int per_sm = 0;
+  PIP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, THREADS, smem));
+  if (per_sm < 1) return PIP_ERR_UNSUPPORTED;
+  if (per_sm > 8) per_sm = 8;
+  u64 g = (u64)per_sm * num_sms(dev);
+  if (g > full_tiles) g = full_tiles;
+  int grid = (int)g;
+  u64* mid = rem ? L.carry : m_dev;
+  const u32 stride = lb_stride(num_sms(dev), grid);
+  PIP_CUDA(cudaMemsetAsync(L.abort, 0, 64, st));
+  PIP_CUDA(cudaMemsetAsync(L.slots, 0, sizeof(TileSlot) * 4 * (size_t)grid * stride, st));
+  LookbackCtx c{L.slots, L.abort, (u32)(4 * grid), stride};
+  DevPred pp = p;
+  void* args[] = {&a, &pp, &mid, &c, (void*)&full_tiles};
+  PIP_CUDA(cudaLaunchCooperativeKernel((const void*)k, dim3(grid), dim3(THREADS), args, smem, st));
+  if (rem) return launch_filter<true>(a + full_tiles * TILE, rem, p, m_dev, L, st, dev, L.carry, a);
+  return PIP_OK;
+}
+
+template <int NWC, int S, int LBW, int D>
+static int launch_filter_ws2(u64* a, u64 n, const DevPred& p, u64* m_dev, const ScratchLayoutF& L,
+                             cudaStream_t st, int dev) {
+  switch (pred_class(p)) {
+    case PC_MASK: return launch_filter_ws2_pc<NWC, S, PC_MASK, LBW, D>(a, n, p, m_dev, L, st, dev);
+    case PC_MOD: return launch_filter_ws2_pc<NWC, S, PC_MOD, LBW, D>(a, n, p, m_dev, L, st, dev);
+    case PC_MODODD: return launch_filter_ws2_pc<NWC, S, PC_MODODD, LBW, D>(a, n, p, m_dev, L, st, dev);
+    default: return launch_filter_ws2_pc<NWC, S, PC_GEN, LBW, D>(a, n, p, m_dev, L, st, dev);
+  }
+}
+
 template <int NWC, int S, bool DYN = false, bool AHEAD = false>
 static int launch_filter_ws(u64* a, u64 n, const DevPred& p, u64* m_dev, const ScratchLayoutF& L,
                             cudaStream_t st, int dev) {
@@ -782,10 +995,12 @@ static int launch_filter_ws(u64* a, u64 n, const DevPred& p, u64* m_dev, const S
 static int filter_cfg() {
   static int cfg = -1;
   if (cfg < 0) {
-    // 8 = warp-specialized pipeline, 16 compute warps x 3 stages (best
-    // measured); 0 = register path; 4/5 = aggregate-ahead TMA pipeline
+    // 17 = filter_ws2_kernel<13 compute warps, 4 stages, 3 look-back warps,
+    // compaction 2 tiles behind the count> (best measured: 10.36 ms at 2^32;
+    // cfg 8 = filter_ws_kernel<16,3> 12.5 ms; <12,4,3,2> 10.66; <13,4,4,2>
+    // 10.39; <16,3,3,1> 11.04); 0 = register path; 4/5 = aggregate-ahead TMA
     const char* e = getenv("PIP_FILTER_CFG");
-    cfg = e ? atoi(e) : 8;
+    cfg = e ? atoi(e) : 17;
   }
   return cfg;
 }
@@ -810,6 +1025,9 @@ int filter_device(u64* a, u64 n, const pip_pred* pred, u64* m_dev, void* scratch
     if (cfg == 7) return launch_filter_ws<8, 3>(a, n, p, m_dev, L, st, dev);
     if (cfg == 9) return launch_filter_ws<16, 3, true>(a, n, p, m_dev, L, st, dev);
     if (cfg == 10) return launch_filter_ws<12, 4, false, true>(a, n, p, m_dev, L, st, dev);
+    if (cfg == 17) return launch_filter_ws2<13, 4, 3, 2>(a, n, p, m_dev, L, st, dev);  // default
+    if (cfg == 18) return launch_filter_ws2<12, 4, 3, 2>(a, n, p, m_dev, L, st, dev);
+
     if (cfg == 11) return launch_filter_ws<14, 4>(a, n, p, m_dev, L, st, dev);
     if (cfg == 12) return launch_filter_ws<12, 4>(a, n, p, m_dev, L, st, dev);
     return launch_filter_ws<16, 3>(a, n, p, m_dev, L, st, dev);

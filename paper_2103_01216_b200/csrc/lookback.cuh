@@ -7,16 +7,18 @@
 // reads 32 predecessor slots per L2 round trip.
 //
 // Measured (B200, scan of 2^32 words, PIP_TIMING=1 counters): the chain of
-// inclusive prefixes is the kernel's serial part — a wave of 148 tiles needs
-// ~2 look-back reads per tile, and under full HBM streaming one L2 round trip
-// costs ~1.6 us, so the look-back, not bandwidth, sets the pace (14.0 ms with
-// it, 10.6 ms with it removed).  What helped: slots spaced `stride` apart in
-// memory so a window spans several L2 lines (14.0 -> 13.0 ms).  What did not:
-// 128-slot windows (4 loads per lane: 19 ms), block-wide windows, smaller
-// tiles (more waves), 2-stage 96 KiB tiles (load latency exposed), clusters
-// of 2-4 CTAs sharing one chain step (18 ms: the DSMEM hand-offs add a hop
-// per wave), and pairs of tiles per chain step with separate producer /
-// look-back warps (13.9 ms: less overlap between look-back and compute).
+// inclusive prefixes is the kernels' serial part — ~2 look-back reads per
+// tile, and under full HBM streaming one L2 round trip costs ~1.6 us; with a
+// single look-back warp that also streams the tiles in, that warp was busy
+// 84% of the time and set the pace (14.0 ms; 10.6 ms with the look-back
+// removed, measurement only).  What helped: slots spaced `stride` apart in
+// memory (14.0 -> 12.9 ms); a separate producer warp plus several look-back
+// warps taking tiles round-robin, so consecutive look-backs of a CTA overlap,
+// with the compute warps two tiles ahead of the stores (scan_ws2_kernel,
+// filter_ws2_kernel: 12.9 -> 11.2 ms, filter 12.5 -> 10.4 ms).  What did
+// not: 128-slot windows (4 loads per lane: 19 ms), block-wide windows,
+// smaller tiles (more waves), 2-stage 96 KiB tiles, clusters of 2-4 CTAs
+// sharing one chain step (18 ms), pairs of tiles per chain step (13.9 ms).
 //
 // A slot is 16 bytes {value, (epoch << 2) | state} published with ONE 128-bit
 // store and read with ONE 128-bit load, so a reader always sees a value

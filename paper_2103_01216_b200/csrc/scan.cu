@@ -614,6 +614,160 @@ scan_ws_kernel(u64* __restrict__ a, u64 init, const u64* carry_in, u64* total, L
 }
 
 // ---------------------------------------------------------------------------
+// Same pipeline with the roles split across more warps: warp 0 only streams
+// tiles in, LBW look-back warps take tiles round-robin (warp 1 + (k % LBW)),
+// so the look-backs of consecutive tiles of this CTA overlap instead of
+// queueing behind one another (the single look-back warp of scan_ws_kernel
+// is busy ~84% of the time at 2^32).
+template <int OP, bool INCLUSIVE, int NWC, int S, int LBW, int D = 1>
+__global__ void __launch_bounds__(32 * (NWC + 1 + LBW), 1)
+scan_ws2_kernel(u64* __restrict__ a, u64 init, const u64* carry_in, u64* total, LookbackCtx c,
+                u64 num_tiles) {
+  using O = Op<OP>;
+  constexpr u64 TILE = (u64)NWC * 512;
+  constexpr u32 TILE_BYTES = (u32)(TILE * 8);
+  extern __shared__ __align__(128) u64 ring[];
+  __shared__ __align__(8) u64 full[S], reduced[S], pready[S], empty[S];
+  __shared__ u64 s_wtot[S][NWC];
+  __shared__ u64 s_wexc[S][NWC];
+  __shared__ u64 s_agg[S];
+  __shared__ u64 s_prefix[S];
+  __shared__ volatile int s_abort;
+  const u32 tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const u64 G = gridDim.x, B = blockIdx.x;
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&reduced[s], 1);
+      mbar_init(&pready[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    s_abort = 0;
+    mbar_fence_init();
+  }
+  __syncthreads();
+  auto ph = [&](u64 k) { return (u32)((k / S) & 1); };
+  auto wait_or_abort = [&](u64* bar, u32 phase) -> bool {
+    while (!mbar_try(bar, phase))
+      if (s_abort) return false;
+    return true;
+  };
+  if (warp == 0) {
+    // ------------------------------------------------------------ producer
+    for (u64 k = 0; B + k * G < num_tiles; ++k) {
+      const int s = (int)(k % S);
+      if (k >= (u64)S && !wait_or_abort(&empty[s], (u32)(((k / S) - 1) & 1))) return;
+      if (lane == 0) {
+        fence_proxy_async_smem();
+        const u64 t = B + k * G;
+        mbar_expect_tx(&full[s], TILE_BYTES);
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          tma_load_1d(ring + s * TILE + q * (TILE / 4), a + t * TILE + q * (TILE / 4), TILE_BYTES / 4,
+                      &full[s]);
+      }
+      __syncwarp();
+    }
+    return;
+  }
+  if (warp <= (u32)LBW) {
+    // ------------------------------------------------ look-back, k = warp-1 mod LBW
+    for (u64 k = warp - 1; B + k * G < num_tiles; k += LBW) {
+      const int s = (int)(k % S);
+      const u64 t = B + k * G;
+      if (!wait_or_abort(&reduced[s], ph(k))) return;
+      const u64 agg = s_agg[s];
+      u64 prefix = (t == 0 && carry_in) ? *carry_in : O::identity;
+      int ok = 1;
+      if (lane == 0) {
+        ok = publish_begin(c, t);
+        if (ok) {
+          if (t == 0) publish_incl(c, 0, O::apply(prefix, agg));
+          else publish_agg(c, t, agg);
+        }
+      }
+      ok = __shfl_sync(0xffffffffu, ok, 0);
+      if (ok && t > 0) {
+        ok = lookback<O>(c, t, prefix);
+        if (ok && lane == 0) publish_incl(c, t, O::apply(prefix, agg));
+      }
+      if (lane == 0) {
+        s_prefix[s] = prefix;
+        if (!ok) s_abort = 1;
+        if (ok && t == num_tiles - 1 && total) *total = O::apply(prefix, agg);
+        mbar_arrive(&pready[s]);
+      }
+      if (!ok) return;
+    }
+    return;
+  }
+  // ---------------------------------------------------------------- compute
+  const u32 w = warp - 1 - LBW;
+  auto scan_store = [&](u64 k) -> bool {
+    const int s = (int)(k % S);
+    if (!wait_or_abort(&pready[s], ph(k))) return false;
+    u64 run = O::apply(s_prefix[s], s_wexc[s][w]);
+    const u64* src = ring + s * TILE + w * 512;
+    const u64 wbase = (B + k * G) * TILE + (u64)w * 512;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const ulonglong2 v = lds2(src + 64 * j + 2 * lane);
+      const u64 x0 = v.x, x1 = v.y;
+      const u64 inc = warp_incl_scan<O>(O::apply(x0, x1));
+      u64 exc = __shfl_up_sync(0xffffffffu, inc, 1);
+      if (lane == 0) exc = O::identity;
+      const u64 tot = __shfl_sync(0xffffffffu, inc, 31);
+      const u64 e = O::apply(run, exc);
+      u64 o0, o1;
+      if (INCLUSIVE) {
+        o0 = O::apply(e, x0);
+        o1 = O::apply(o0, x1);
+      } else {
+        o0 = e;
+        o1 = O::apply(e, x0);
+      }
+      stg_stream2(a + wbase + 64 * j + 2 * lane, O::apply(init, o0), O::apply(init, o1));
+      run = O::apply(run, tot);
+    }
+    named_bar(1, NWC * 32);  // every compute warp has read stage s
+    if (w == 0 && lane == 0) mbar_arrive(&empty[s]);
+    return true;
+  };
+  // compute runs D tiles ahead of the stores (S >= D + 2 stages)
+  static_assert(S >= D + 2, "stages");
+  for (u64 k = 0;; ++k) {
+    const int s = (int)(k % S);
+    if (B + k * G >= num_tiles) {
+      for (u64 q = k > (u64)D ? k - D : 0; q < k; ++q)
+        if (!scan_store(q)) return;
+      break;
+    }
+    if (!wait_or_abort(&full[s], ph(k))) return;
+    const u64* src = ring + s * TILE + w * 512;
+    u64 acc = O::identity;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const ulonglong2 v = lds2(src + 64 * j + 2 * lane);
+      acc = O::apply(acc, O::apply(v.x, v.y));
+    }
+    acc = warp_reduce<O>(acc);
+    if (lane == 0) s_wtot[s][w] = acc;
+    named_bar(1, NWC * 32);
+    if (w == 0) {
+      const u64 wv = lane < (u32)NWC ? s_wtot[s][lane] : O::identity;
+      const u64 winc = warp_incl_scan<O>(wv);
+      u64 wexc = __shfl_up_sync(0xffffffffu, winc, 1);
+      if (lane == 0) wexc = O::identity;
+      if (lane < (u32)NWC) s_wexc[s][lane] = wexc;
+      if (lane == NWC - 1) s_agg[s] = winc;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&reduced[s]);
+    }
+    if (k >= (u64)D && !scan_store(k - D)) return;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // reduce: grid-stride fold, per-CTA partials, last CTA folds the partials.
 template <int OP>
 __global__ void __launch_bounds__(512)
@@ -823,14 +977,45 @@ static int launch_scan_ws(u64* a, u64 n, u64 init, const u64* carry, u64* total,
   return PIP_OK;
 }
 
+template <int OP, bool INCL, int NWC, int S, int LBW, int D = 1>
+static int launch_scan_ws2(u64* a, u64 n, u64 init, const u64* carry, u64* total,
+                           const ScratchLayout& L, cudaStream_t st, int device) {
+  constexpr u64 TILE = (u64)NWC * 512;
+  constexpr int THREADS = 32 * (NWC + 1 + LBW);
+  const u64 full_tiles = n / TILE;
+  const u64 rem = n - full_tiles * TILE;
+  auto k = scan_ws2_kernel<OP, INCL, NWC, S, LBW, D>;
+  const int smem = (int)(S * TILE * 8);
+  PIP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  int per_sm = 0;
+  PIP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, THREADS, smem));
+  if (per_sm < 1) return PIP_ERR_UNSUPPORTED;
+  if (per_sm > CTAS_PER_SM_MAX) per_sm = CTAS_PER_SM_MAX;
+  u64 g = (u64)per_sm * num_sms(device);
+  if (g > full_tiles) g = full_tiles;
+  int grid = (int)g;
+  u64* mid = rem ? L.carry : total;
+  const u32 stride = lb_stride(num_sms(device), grid);
+  PIP_CUDA(cudaMemsetAsync(L.abort, 0, 64, st));
+  PIP_CUDA(cudaMemsetAsync(L.slots, 0, sizeof(TileSlot) * 4 * (size_t)grid * stride, st));
+  LookbackCtx c{L.slots, L.abort, (u32)(4 * grid), stride};
+  void* args[] = {&a, &init, &carry, &mid, &c, (void*)&full_tiles};
+  PIP_CUDA(cudaLaunchCooperativeKernel((const void*)k, dim3(grid), dim3(THREADS), args, smem, st));
+  if (rem) return launch_scan_t<OP, INCL, true>(a + full_tiles * TILE, rem, init, L.carry, total, L, st, device);
+  return PIP_OK;
+}
+
 static int scan_cfg() {
   static int cfg = -1;
   if (cfg < 0) {
-    // 8 = warp-specialized pipeline, 16 compute warps x 3 stages of 64 KiB
-    // (best measured, profiles/r01_scan_ws_summary.txt); 6/7 = smaller WS
-    // variants; 4/5 = aggregate-ahead TMA; 1-3 = plain TMA rings; 0 = registers
+    // 17 = scan_ws2_kernel<13 compute warps, 4 stages of 52 KiB, 3 look-back
+    // warps, compute 2 tiles ahead> (best measured: 11.2 ms at 2^32; with one
+    // look-back warp doing the streaming too — cfg 8, scan_ws_kernel<16,3> —
+    // 12.9 ms; 2 look-back warps, 3 stages: 12.2; <12,4,2,2>: 11.6;
+    // <10,5,3,3>: 11.7); 6/7/9-12 = other scan_ws variants; 4/5 =
+    // aggregate-ahead TMA; 1-3 = plain TMA rings; 0 = registers
     const char* e = getenv("PIP_SCAN_CFG");
-    cfg = e ? atoi(e) : 8;
+    cfg = e ? atoi(e) : 17;
   }
   return cfg;
 }
@@ -850,6 +1035,9 @@ static int launch_scan_op(u64* a, u64 n, u64 init, int inclusive, const u64* car
     if (cfg == 9)
       return inclusive ? launch_scan_ws<OP, true, 16, 3, true>(a, n, init, carry, total, L, st, device)
                        : launch_scan_ws<OP, false, 16, 3, true>(a, n, init, carry, total, L, st, device);
+    if (cfg == 17)  // default: producer warp, 3 look-back warps, 13 compute warps 2 tiles ahead
+      return inclusive ? launch_scan_ws2<OP, true, 13, 4, 3, 2>(a, n, init, carry, total, L, st, device)
+                       : launch_scan_ws2<OP, false, 13, 4, 3, 2>(a, n, init, carry, total, L, st, device);
     if (cfg == 11)
       return inclusive ? launch_scan_ws<OP, true, 14, 4>(a, n, init, carry, total, L, st, device)
                        : launch_scan_ws<OP, false, 14, 4>(a, n, init, carry, total, L, st, device);
