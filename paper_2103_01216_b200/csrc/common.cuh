@@ -97,7 +97,7 @@ struct DevPred {
   u64 lim;     // MOD_EQ: floor((2^64 - 1) / d_odd)
 };
 // predicate classes the filter kernels are specialised on
-enum : int { PC_MASK = 0, PC_MOD = 1, PC_GEN = 2, PC_MODODD = 3 };
+enum : int { PC_MASK = 0, PC_MOD = 1, PC_GEN = 2, PC_MODODD = 3, PC_MODODD0 = 4 };
 DevPred make_dev_pred(const pip_pred& p);
 
 __device__ __forceinline__ u64 fast_div(u64 x, const DevPred& p) {
@@ -145,6 +145,8 @@ __device__ __forceinline__ bool pred_eval_t(const DevPred& p, u64 x) {
     r = (x >= p.b) & ((y & ((1ull << p.tz) - 1ull)) == 0) & ((y >> p.tz) * p.inv <= p.lim);
   } else if (PC == PC_MODODD) {  // odd divisor: x = b (mod d) <=> (x - b) * d^-1 <= lim
     r = (x >= p.b) & ((x - p.b) * p.inv <= p.lim);
+  } else if (PC == PC_MODODD0) {  // odd divisor, remainder 0
+    r = x * p.inv <= p.lim;
   } else {
     return pred_eval(p, x);
   }

@@ -643,8 +643,7 @@ filter_ws2_kernel(u64* __restrict__ a, DevPred p, u64* m_out, LookbackCtx c, u64
       int ok = 1;
       if (lane == 0) {
         ok = publish_begin(c, t);
-        if (ok) {
-          __threadfence();
+        if (ok) {  // (the tile's bulk reads completed before it was reduced)
           if (t == 0) publish_incl(c, 0, agg);
           else publish_agg(c, t, agg);
         }
@@ -817,7 +816,7 @@ static ScratchLayoutF carve_f(void* scratch, int sms) {
 
 static int pred_class(const DevPred& p) {
   if (p.kind == PIP_PRED_MASK_EQ) return PC_MASK;
-  if (p.kind == PIP_PRED_MOD_EQ) return p.tz == 0 ? PC_MODODD : PC_MOD;
+  if (p.kind == PIP_PRED_MOD_EQ) return p.tz == 0 ? (p.b == 0 ? PC_MODODD0 : PC_MODODD) : PC_MOD;
   return PC_GEN;
 }
 
@@ -834,6 +833,7 @@ static int launch_filter(u64* a, u64 n, const DevPred& p, u64* m_dev, const Scra
     case PC_MASK: return launch_filter_pc<VEC, PC_MASK>(a, n, p, m_dev, L, st, dev, carry_in, out);
     case PC_MOD: return launch_filter_pc<VEC, PC_MOD>(a, n, p, m_dev, L, st, dev, carry_in, out);
     case PC_MODODD: return launch_filter_pc<VEC, PC_MODODD>(a, n, p, m_dev, L, st, dev, carry_in, out);
+    case PC_MODODD0: return launch_filter_pc<VEC, PC_MODODD0>(a, n, p, m_dev, L, st, dev, carry_in, out);
     default: return launch_filter_pc<VEC, PC_GEN>(a, n, p, m_dev, L, st, dev, carry_in, out);
   }
 }
@@ -977,6 +977,7 @@ static int launch_filter_ws2(u64* a, u64 n, const DevPred& p, u64* m_dev, const 
     case PC_MASK: return launch_filter_ws2_pc<NWC, S, PC_MASK, LBW, D>(a, n, p, m_dev, L, st, dev);
     case PC_MOD: return launch_filter_ws2_pc<NWC, S, PC_MOD, LBW, D>(a, n, p, m_dev, L, st, dev);
     case PC_MODODD: return launch_filter_ws2_pc<NWC, S, PC_MODODD, LBW, D>(a, n, p, m_dev, L, st, dev);
+    case PC_MODODD0: return launch_filter_ws2_pc<NWC, S, PC_MODODD0, LBW, D>(a, n, p, m_dev, L, st, dev);
     default: return launch_filter_ws2_pc<NWC, S, PC_GEN, LBW, D>(a, n, p, m_dev, L, st, dev);
   }
 }
@@ -988,6 +989,7 @@ static int launch_filter_ws(u64* a, u64 n, const DevPred& p, u64* m_dev, const S
     case PC_MASK: return launch_filter_ws_pc<NWC, S, PC_MASK, DYN, AHEAD>(a, n, p, m_dev, L, st, dev);
     case PC_MOD: return launch_filter_ws_pc<NWC, S, PC_MOD, DYN, AHEAD>(a, n, p, m_dev, L, st, dev);
     case PC_MODODD: return launch_filter_ws_pc<NWC, S, PC_MODODD, DYN, AHEAD>(a, n, p, m_dev, L, st, dev);
+    case PC_MODODD0: return launch_filter_ws_pc<NWC, S, PC_MODODD0, DYN, AHEAD>(a, n, p, m_dev, L, st, dev);
     default: return launch_filter_ws_pc<NWC, S, PC_GEN, DYN, AHEAD>(a, n, p, m_dev, L, st, dev);
   }
 }
@@ -1062,6 +1064,7 @@ int count_device(const u64* a, u64 n, const pip_pred* pred, u64* m_dev, void* sc
     case PC_MASK: count_kernel<PC_MASK><<<grid, 512, 0, st>>>(a, n, p, L.partials, L.counter, m_dev); break;
     case PC_MOD: count_kernel<PC_MOD><<<grid, 512, 0, st>>>(a, n, p, L.partials, L.counter, m_dev); break;
     case PC_MODODD: count_kernel<PC_MODODD><<<grid, 512, 0, st>>>(a, n, p, L.partials, L.counter, m_dev); break;
+    case PC_MODODD0: count_kernel<PC_MODODD0><<<grid, 512, 0, st>>>(a, n, p, L.partials, L.counter, m_dev); break;
     default: count_kernel<PC_GEN><<<grid, 512, 0, st>>>(a, n, p, L.partials, L.counter, m_dev); break;
   }
   PIP_CHECK_LAUNCH();

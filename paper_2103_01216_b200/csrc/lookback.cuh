@@ -42,9 +42,6 @@ namespace pip {
 static __device__ u64 g_scan_prof[8];
 static __device__ u32 g_prof_on;
 static __device__ u32 g_prof_cta;
-__device__ __forceinline__ void lb_count(int which) {
-  if (g_prof_on && blockIdx.x == g_prof_cta && (threadIdx.x & 31) == 0) g_scan_prof[which] += 1;
-}
 
 struct LookbackCtx {
   TileSlot* slots;  // [R]
@@ -131,7 +128,6 @@ __device__ bool lookback(const LookbackCtx& c, u64 tile, u64& prefix_out) {
     u32 incl_mask, need;
     bool restart = false;
     for (;;) {
-      lb_count(5);
       st = read_slot<O>(c, u, v);
       incl_mask = __ballot_sync(0xffffffffu, st == RD_INCL);
       const u32 bad = __ballot_sync(0xffffffffu, st == RD_NOTREADY);
@@ -142,7 +138,6 @@ __device__ bool lookback(const LookbackCtx& c, u64 tile, u64& prefix_out) {
         break;
       }
       if ((bad & need) == 0) break;
-      lb_count(6);
       bool ok = true;
       if (lane == 0) ok = spin_tick(c, spins);
       if (!__shfl_sync(0xffffffffu, (int)ok, 0)) return false;

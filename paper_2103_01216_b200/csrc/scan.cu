@@ -965,10 +965,9 @@ static int launch_scan_ws(u64* a, u64 n, u64 init, const u64* carry, u64* total,
     PIP_CUDA(cudaMemcpyFromSymbolAsync(h, g_scan_prof, sizeof(h), 0, cudaMemcpyDeviceToHost, st));
     PIP_CUDA(cudaMemcpyToSymbolAsync(g_prof_on, &off, 4, 0, cudaMemcpyHostToDevice, st));
     PIP_CUDA(cudaStreamSynchronize(st));
-    fprintf(stderr, "[pip scan] profiled CTA: tiles %llu | producer: wait-reduce %llu lookback %llu | compute: wait-prefix %llu wait-data %llu cycles | look-back reads %llu retries %llu\n",
+    fprintf(stderr, "[pip scan] profiled CTA: tiles %llu | producer: wait-reduce %llu lookback %llu | compute: wait-prefix %llu wait-data %llu cycles\n",
             (unsigned long long)h[2], (unsigned long long)h[0], (unsigned long long)h[1],
-            (unsigned long long)h[3], (unsigned long long)h[4], (unsigned long long)h[5],
-            (unsigned long long)h[6]);
+            (unsigned long long)h[3], (unsigned long long)h[4]);
   }
   if (rem) {
     u64* tail = a + full_tiles * TILE;
