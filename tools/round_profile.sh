@@ -18,8 +18,8 @@ full() {  # op log2n kernel-regex
   ncu --set full --clock-control none --import-source on -k regex:$3 -s 1 -c 1 \
       -o $out/full_$1 $cmd > $out/ncu_full_$1.log 2>&1
 }
-full scan 28 scan_ws
-full filter 28 filter_ws
+full scan 28 scan_ws2
+full filter 28 filter_ws2
 full merge 28 merge_kernel
 full rp 26 rp_kernel
 ls -la $out
