@@ -497,6 +497,15 @@ __global__ void __launch_bounds__(MG_THREADS, MG_CTAS_PER_SM) merge_kernel(Merge
     // blocking measured slower: 38 vs 32 ms at 2^32 — the status poll is an
     // L2 round trip on every pass)
     bool ok = true;
+    bool owe_ofree = false;  // a store's read of s_obuf is still in flight
+    auto settle_ofree = [&]() {
+      if (owe_ofree && lane == 0) {
+        bulk_wait_read_all();
+        mbar_arrive(&s_ofree);
+      }
+      owe_ofree = false;
+      __syncwarp();
+    };
     for (u64 j = 0; j < nblk; ++j) {
       const u64 m = b + j * G;
       const int sb = (int)(j & 1);
@@ -520,6 +529,9 @@ __global__ void __launch_bounds__(MG_THREADS, MG_CTAS_PER_SM) merge_kernel(Merge
         if (lane == 0) st_relaxed_u32(M.status + b, (u32)(m + G + 1));
       }
       mark(0);
+      // the merge warps need s_obuf back before they can finish block j: the
+      // previous store's read is waited for only now, not right after issue
+      settle_ofree();
       if (!wait_or_abort(&s_ofull, (u32)(j & 1))) { ok = false; break; }  // output written
       mark(1);
       if (keep0 && j == 0) continue;  // block 0 is written after the final barrier
@@ -537,10 +549,10 @@ __global__ void __launch_bounds__(MG_THREADS, MG_CTAS_PER_SM) merge_kernel(Merge
         if (body) {
           tma_store_1d(a + p0 + head, out + head, body * 8u);
           bulk_commit();
-          bulk_wait_read_all();  // the buffer may be rewritten
         }
-        if (!in_place(j)) mbar_arrive(&s_ofree);
+        if (in_place(j)) bulk_wait_read_all();  // the staging buffer is refilled below
       }
+      owe_ofree = !in_place(j);  // settled (read waited, s_ofree arrived) next iteration
       __syncwarp();
       if (in_place(j) && j + 2 < nblk) {  // the store has read it: refill
         if (lane == 0) fence_proxy_async_smem();
@@ -549,6 +561,7 @@ __global__ void __launch_bounds__(MG_THREADS, MG_CTAS_PER_SM) merge_kernel(Merge
       }
       mark(3);
     }
+    settle_ofree();
     if (lane == 0) bulk_wait_all();
     if (!ok && lane == 0) atomicExch(&g->sync.abort, 1u);
   } else {
