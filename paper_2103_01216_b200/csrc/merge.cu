@@ -523,15 +523,15 @@ __global__ void __launch_bounds__(MG_THREADS, MG_CTAS_PER_SM) merge_kernel(Merge
           issue_load(m + 2 * G, sb);
         }
       }
+      // the merge warps need s_obuf back before they can finish block j: the
+      // previous store's read is waited for only now, not right after issue
+      settle_ofree();
       // publish block j+1's load as soon as it has landed
       if (j + 1 < nblk) {
         if (!wait_or_abort(&s_full[sb ^ 1], ((j + 1) >> 1) & 1)) { ok = false; break; }
         if (lane == 0) st_relaxed_u32(M.status + b, (u32)(m + G + 1));
       }
       mark(0);
-      // the merge warps need s_obuf back before they can finish block j: the
-      // previous store's read is waited for only now, not right after issue
-      settle_ofree();
       if (!wait_or_abort(&s_ofull, (u32)(j & 1))) { ok = false; break; }  // output written
       mark(1);
       if (keep0 && j == 0) continue;  // block 0 is written after the final barrier
