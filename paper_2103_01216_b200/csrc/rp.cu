@@ -53,6 +53,7 @@ struct RpResume {
   long long cursor;
   u64 dlo, dhi;
   u32 ping, done, first, logcap_c;  // logcap_c: BM collided-table size of the last round
+  u32 wpre, pad;                     // wpre: wcnt already holds the counts of the window at `cursor`
 };
 
 struct RpArgs {
@@ -386,8 +387,21 @@ __global__ void __launch_bounds__(RP_THREADS, 4) rp_kernel(RpArgs A) {
       c = block_sum(c, s_red);
       if (tid == 0) A.wcnt[b] = (u32)c;
     };
-    if (win) count_window();
-    if (!grid_barrier(&g->sync, gen)) break;
+    // `final` windows do not depend on the failures, so the previous round
+    // counted this one already and retire + refill share one phase (the
+    // refill writes past nfail, the retire below it; nfail comes from the
+    // previous round's counts)
+    const bool fused = V == PIP_RP_FINAL && R.wpre && !A.debug;
+    if (fused) {
+      if (win) {
+        hi = (u64)cursor;
+        lo = hi + 1 >= A.span_cap ? hi + 1 - A.span_cap : 0;
+        wd = hi - lo + 1;
+      }
+    } else {
+      if (win) count_window();
+      if (!grid_barrier(&g->sync, gen)) break;
+    }
     tick(0);
 
     // ======================= P2: refill =====================================
@@ -726,6 +740,23 @@ __global__ void __launch_bounds__(RP_THREADS, 4) rp_kernel(RpArgs A) {
     R.dlo = dlo;
     R.dhi = dhi;
     R.cursor = cursor;
+    R.wpre = 0;
+    if (V == PIP_RP_FINAL && cursor >= 0) {  // count the next round's window now
+      hi = (u64)cursor;
+      lo = hi + 1 >= A.span_cap ? hi + 1 - A.span_cap : 0;
+      wd = hi - lo + 1;
+      u64 ws, we;
+      part(wd, G, b, ws, we);
+      u64 c = 0;
+#pragma unroll 4
+      for (u64 q = ws + tid; q < we; q += T) {
+        const u64 id = hi - q;
+        c += __ldcs(A.h + id) != id;
+      }
+      c = block_sum(c, s_red);
+      if (tid == 0) A.wcnt[b] = (u32)c;
+      R.wpre = 1;
+    }
     if (!grid_barrier(&g->sync, gen)) break;
     tick(3);
     if (++rounds_here >= A.rounds_limit) break;  // pause: host drains counts
