@@ -11,34 +11,37 @@ struct GridSync {
 };
 
 // ---------------------------------------------------------------------------
-// grid barrier (co-residency guaranteed by the cooperative launch)
+// grid barrier (co-residency guaranteed by the cooperative launch).  The
+// arrival counter only grows (barrier k of a launch completes when it reaches
+// k * gridDim.x), so the last arriver has nothing to reset or publish: one
+// acq_rel add per CTA, then acquire polls of the same word.  `bar_count` is
+// zeroed before every launch.
+__device__ __forceinline__ u32 atom_add_acq_rel_u32(u32* p, u32 v) {
+  u32 old;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+
 __device__ __forceinline__ bool grid_barrier(GridSync* g, u32& gen) {
   __syncthreads();
   __shared__ int s_ok;
   if (threadIdx.x == 0) {
     int ok = 1;
-    __threadfence();
-    const u32 arrived = atomicAdd(&g->bar_count, 1u);
-    if (arrived == gridDim.x - 1) {
-      atomicExch(&g->bar_count, 0u);
-      __threadfence();
-      st_release_u32(&g->bar_gen, gen + 1);
-    } else {
-      u64 spins = 0;
-      while (ld_acquire_u32(&g->bar_gen) == gen) {
-        if (++spins > 32) __nanosleep(32);
-        if ((spins & 1023) == 0) {
-          if (ld_relaxed_u32(&g->abort)) { ok = 0; break; }
-          if (spins > (1ull << 26)) { atomicExch(&g->abort, 1u); ok = 0; break; }
-        }
+    const u32 target = (gen + 1) * gridDim.x;
+    u32 v = atom_add_acq_rel_u32(&g->bar_count, 1u) + 1u;
+    u64 spins = 0;
+    while ((int)(v - target) < 0) {
+      if (++spins > 16) __nanosleep(32);
+      if ((spins & 1023) == 0) {
+        if (ld_relaxed_u32(&g->abort)) { ok = 0; break; }
+        if (spins > (1ull << 26)) { atomicExch(&g->abort, 1u); ok = 0; break; }
       }
+      v = ld_acquire_u32(&g->bar_count);
     }
     gen += 1;
-    __threadfence();
     s_ok = ok;
   }
   __syncthreads();
-  // propagate gen to all threads (only thread 0 uses it, but keep uniform)
   return s_ok;
 }
 
