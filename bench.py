@@ -620,7 +620,7 @@ def cpu_run(op, x, h, threads):
                                       threads)
 
 
-def cpu_baseline(op, args, budget_s: float = 12.0) -> dict:
+def cpu_baseline(op, args, budget_s: float = 10.0) -> dict:
     from oracle import oracle
 
     oracle.build()
@@ -629,7 +629,7 @@ def cpu_baseline(op, args, budget_s: float = 12.0) -> dict:
     threads = cpu_threads()
     x0, h = _cpu_input(op, n, args.seed)
     reps, el = 0, 0.0
-    while el < budget_s and reps < 50:
+    while el < budget_s and reps < 2000:  # about 10 s of CPU work (time-bounded sample)
         x = x0.copy()
         t0 = time.perf_counter()
         cpu_run(op, x, h, threads)
