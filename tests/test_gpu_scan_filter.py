@@ -277,3 +277,33 @@ def test_filter_relaxed_equals_kway(pip):
         sink = []
         m2 = pip.relaxed.filter_relaxed(a2, P.even(), pip.EpsilonConfig(0.5, 1e-12), stats_sink=sink)
         assert m1 == m2 and np.array_equal(a1[:m1], a2[:m2])
+
+
+# Tile geometry of the default split-role kernels: 13 compute warps x 512 words
+# = 6656-word tiles, 4 stages, one CTA per SM; sizes around whole waves of
+# tiles (148 x 6656) and single tiles exercise the tail hand-off to the
+# register kernel and the carry between them.
+WS2_TILE = 13 * 512
+
+
+@pytest.mark.parametrize("n", [8 * WS2_TILE - 1, 8 * WS2_TILE, 8 * WS2_TILE + 1,
+                               148 * WS2_TILE, 148 * WS2_TILE + 7, 3 * 148 * WS2_TILE - 1])
+def test_scan_ws2_tile_boundaries(pip, orc, n):
+    x = rand_words(n + 1, n, hi=1 << 40)
+    for inclusive in (False, True):
+        want, tot = orc.seq_scan(x, inclusive=inclusive)
+        t = dev(x)
+        r = (pip.strong.scan_inclusive if inclusive else pip.strong.scan)(t)
+        assert np.array_equal(host(t), want) and r.total == tot, (n, inclusive)
+
+
+@pytest.mark.parametrize("n", [8 * WS2_TILE - 1, 8 * WS2_TILE + 1, 148 * WS2_TILE + 7,
+                               2 * 148 * WS2_TILE - 3])
+def test_filter_ws2_tile_boundaries(pip, orc, n):
+    P = pip.pred
+    x = rand_words(n + 2, n)
+    for p in (P.mod_eq(3, 0), P.mod_eq(5, 2), P.mod_eq(8, 1), P.always(), ~P.always(), P.lt(1 << 62)):
+        want = orc.seq_filter(x, p)
+        t = dev(x)
+        m = pip.strong.filter_kway(t, p)
+        assert m == len(want) and np.array_equal(host(t)[:m], want), (n, p)
