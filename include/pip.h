@@ -138,7 +138,9 @@ int pip_rotate_u64(uint64_t* a, uint64_t n, uint64_t o, void* scratch, size_t sc
  * sorted.  `workspace`/`workspace_bytes` is the metered auxiliary space
  * (pip_merge_workspace_bytes tells how much a given budget can use); with
  * workspace_bytes == 0 the strong (zero-heap) schedule runs on scratch only.
- * check_sorted != 0 reproduces debug=True (PIP_ERR_UNSORTED).
+ * check_sorted != 0 reproduces debug=True (PIP_ERR_UNSORTED).  `scratch`
+ * (pip_scratch_bytes, required for n > 8192) holds the block phase's
+ * per-CTA load-status words: O(#SMs), independent of n, unmetered.
  * Replaces strong.py:496-522 and relaxed.py:579-612.                        */
 int pip_merge_u64(uint64_t* a, uint64_t n, uint64_t split, int check_sorted,
                   void* workspace, size_t workspace_bytes, void* scratch, size_t scratch_bytes,

@@ -48,11 +48,12 @@
 
 namespace pip {
 
-static constexpr int MG_THREADS = 512;
+static constexpr int MG_THREADS = 544;  // block phase: loader + watcher + 15 merge warps
+static constexpr int MG_CP = 512;       // threads that move chunks (P1) / small merges
 static constexpr int MG_CTAS_PER_SM = 1;
 static constexpr u32 MG_LOGC = 13;
 static constexpr u64 MG_C = 1ull << MG_LOGC;  // words per chunk / output block
-static constexpr int MG_PER_THREAD = (int)(MG_C / MG_THREADS);
+static constexpr int MG_PER_THREAD = (int)(MG_C / MG_CP);
 // shared-memory padding: merge-path readers sit ~8 words apart and writers
 // exactly 16 words apart, which on 8-byte words means 16- and 32-way bank
 // conflicts; one pad word per 8 (inputs) / per 16 (outputs) spreads them
@@ -61,18 +62,23 @@ __device__ __forceinline__ u32 SO(u32 r) { return r + (r >> 4); }
 static constexpr u32 MG_IN_WORDS = (u32)(MG_C + MG_C / 8);
 static constexpr u32 MG_OUT_WORDS = (u32)(MG_C + MG_C / 16);
 static constexpr u32 MG_STAGE_WORDS = (u32)(MG_C + 16);  // bulk-copy staging (+2 junk words x 6 segments)
-static constexpr size_t MG_SMEM = (size_t)(2 * MG_STAGE_WORDS + MG_C) * 8;
+// per merge warp: a transpose tile for its <= 32 * 8192 / 480 + 1 outputs
+static constexpr u32 MG_SCR = (u32)((32 * MG_C) / (MG_THREADS - 64) + 2);
+// per-CTA load status words one L2 line apart: every CTA polls its
+// neighbours' words, and packed words made a few lines a hot spot
+static constexpr u32 MG_SST = 32;
+static constexpr size_t MG_SMEM = (size_t)(2 * MG_STAGE_WORDS + (MG_THREADS / 32 - 2) * MG_SCR) * 8;
 
 struct MergeGlobal {
   GridSync sync;
   u32 walk_next;  // dynamic walk assignment
   u32 uncut;      // #slots on cut-free cycles
   u64 t[8];       // %globaltimer at phase boundaries (CTA 0)
-  u64 sec[6];     // PIP_MERGE_DBG bit2: CTA 0 cycles in stage|load-issue|merge|wait|store|other
+  u64 sec[8];     // PIP_MERGE_DBG bit2: CTA 0 cycles (merge warps: data wait|merge|ofree wait|write-out; control: loads|dataflow|store)
 };
 
 struct MergeArgs {
-  u32 dbg;  // profiling knobs (PIP_MERGE_DBG): bit0 skip the dataflow wait, bit1 copy instead of merge
+  u32 dbg;  // profiling knobs (PIP_MERGE_DBG): bit0 skip the dataflow wait, bit1 no merge, bit2 CTA 0 cycle counters
   u64* a;
   u64 n, na, nb;
   u64 hA, hB, KA, KB, K, NB, D, ncuts, L;
@@ -82,9 +88,12 @@ struct MergeArgs {
   u32* lab[2];    // [K] pointer-jumping labels   (only if uncut cycles)
   u32* jmp[2];    // [K] pointer-jumping jumps
   unsigned char* visited;  // [K]
+  u32* rlo;       // [K] first / last output block that reads the chunk in slot s
+  u32* rhi;       //     (after the permutation); rlo = ~0 if none
   u64* cr;        // [NB + 1] A co-rank of every output block boundary
   ulonglong4* plan;  // [NB] {i0, i1, dest slots of the <= 2 A' and <= 2 B' chunks}
-  u32* status;    // [G] per CTA: (last block loaded) + 1
+  u32* status;    // [G * MG_SST] per CTA: (last block loaded) + 1
+  u64* head_save; // [C] block 0's output while the in-place head may still be read
   MergeGlobal* g;
 };
 
@@ -163,11 +172,15 @@ __device__ __forceinline__ bool is_cut(const MergeArgs& M, u64 s) {
 __device__ __forceinline__ void move_chunk(u64* dst, const u64* src) {
   const u32 tid = threadIdx.x;
   u64 v[MG_PER_THREAD];
+  if (tid < MG_CP) {
 #pragma unroll
-  for (int k = 0; k < MG_PER_THREAD; ++k) v[k] = __ldcg(src + tid + k * MG_THREADS);
+    for (int k = 0; k < MG_PER_THREAD; ++k) v[k] = __ldcg(src + tid + k * MG_CP);
+  }
   __syncthreads();
+  if (tid < MG_CP) {
 #pragma unroll
-  for (int k = 0; k < MG_PER_THREAD; ++k) dst[tid + k * MG_THREADS] = v[k];
+    for (int k = 0; k < MG_PER_THREAD; ++k) dst[tid + k * MG_CP] = v[k];
+  }
 }
 
 __device__ __forceinline__ u64* slot_ptr(const MergeArgs& M, u64 s) {
@@ -213,6 +226,8 @@ __global__ void __launch_bounds__(MG_THREADS, MG_CTAS_PER_SM) merge_kernel(Merge
       M.dest[x] = (u32)d;
       M.inv[d] = (u32)x;
       M.visited[x] = 0;
+      M.rlo[x] = 0xffffffffu;
+      M.rhi[x] = 0;
     }
     mpart(M.NB + 1, G, b, s, e);
     for (u64 m = s + tid; m < e; m += MG_THREADS) {
@@ -244,6 +259,15 @@ __global__ void __launch_bounds__(MG_THREADS, MG_CTAS_PER_SM) merge_kernel(Merge
         db1 = __ldcg(M.dest + M.KA + ((ye - 1) >> MG_LOGC));
       }
       M.plan[m] = make_ulonglong4(i0, i1, ((u64)da1 << 32) | da0, ((u64)db1 << 32) | db0);
+      // reader ranges of the slots this block loads from (the rule in P2)
+      if (xs < i1) {
+        atomicMin(M.rlo + da0, (u32)m); atomicMax(M.rhi + da0, (u32)m);
+        atomicMin(M.rlo + da1, (u32)m); atomicMax(M.rhi + da1, (u32)m);
+      }
+      if (j0 < ye) {
+        atomicMin(M.rlo + db0, (u32)m); atomicMax(M.rhi + db0, (u32)m);
+        atomicMin(M.rlo + db1, (u32)m); atomicMax(M.rhi + db1, (u32)m);
+      }
     }
   }
   for (u64 c = b; c < M.ncuts; c += G) {
@@ -332,34 +356,38 @@ __global__ void __launch_bounds__(MG_THREADS, MG_CTAS_PER_SM) merge_kernel(Merge
 
   if (tm) g->t[4] = globaltimer_ns();
   // ---------------- P2: block merge under the dataflow rule
-  // Warp-specialized: warp 0 is the control warp, warps 1..15 merge.
+  // Warp-specialized: warp 0 loads, warp 1 watches the dataflow rule, warps
+  // 2..16 merge and store.
   //   load   (control) the <= 6 contiguous input segments of a block (A head
   //          in place, <= 2 permuted A' chunks, <= 2 permuted B' chunks, B
   //          tail in place), one bulk copy each into one of two staging
-  //          buffers, widened to 16-byte alignment (<= 2 junk words per
-  //          segment); "loaded" is published as soon as the bytes land;
-  //   merge  (merge warps) straight from staging through the segment map,
-  //          a merge-path range of 17-18 consecutive outputs per thread into
-  //          registers (ranges start at t*8192/480, not a multiple of 16
-  //          words, so a warp's shared accesses spread over the banks even
-  //          for perfectly interleaved runs); the staging buffer is handed
-  //          back at once, the registers go to the output buffer as soon as
-  //          the previous block's store has read it;
-  //   store  (control) one bulk copy of the output buffer to a[mC, (m+1)C)
-  //          once every block <= m + L has loaded (the dataflow rule).
-  // The dataflow wait of block m overlaps the merge of block m + G.
-  constexpr u32 NMW = MG_THREADS - 32;  // merge threads
+  //          buffers (widened to 16-byte alignment); "loaded" is published as
+  //          soon as the bytes land;
+  //   rule   (watcher) block m may be written once every block <= m + L has
+  //          loaded: polled ahead of the merge warps, announced to them
+  //          through a monotone shared counter;
+  //   merge  (merge warps) a merge-path range of 17-18 consecutive outputs per
+  //          thread into registers, straight from staging (each side one
+  //          contiguous range when the chunk grid is 16-byte aligned, else
+  //          through a segment map); every warp hands the staging buffer back
+  //          on its own (mbarrier, 15 arrivals) — no CTA-wide barrier;
+  //   store  (merge warps) each warp transposes its ~546 outputs through a
+  //          private shared-memory tile and writes them with coalesced
+  //          stores once the rule allows: no output buffer shared by the
+  //          CTA, so no block waits for the previous block's store.
+  constexpr u32 NMW = MG_THREADS - 64;  // merge threads
   constexpr int MO = (int)((MG_C + NMW - 1) / NMW) + 1;  // outputs per thread, at most
-  static_assert((2 * MG_STAGE_WORDS + MG_C) * 8 <= MG_SMEM, "two staging buffers + output");
-  u64* s_obuf = smem + 2 * MG_STAGE_WORDS;
-  __shared__ __align__(8) u64 s_full[2], s_sfree[2], s_ofull, s_ofree;
+  u64* s_scr = smem + 2 * MG_STAGE_WORDS;  // per merge warp: MG_SCR words
+  __shared__ __align__(8) u64 s_full[2], s_sfree[2];
   __shared__ u32 s_seg[2][2 + 2 * 6];  // per buffer: na, nb | lo[6] | staging index[6]
-  // CTA 0 keeps block 0's output (it overwrites the in-place head, which any
-  // block may still read) in s_obuf to the end; its later blocks are written
-  // back into their own staging buffer and stored from there
+  __shared__ u32 s_dfdone;  // blocks (of this CTA) whose dataflow rule holds
+  // CTA 0 writes block 0 (it overwrites the in-place head, which any block
+  // may still read) to M.head_save; it is copied home after a final barrier
   const bool keep0 = M.hA > 0 && b == 0;
+  // interior piece boundaries of every block sit at a + hA + s*C (chunk
+  // starts, hA, the tail start): contiguous staging iff that is 16-byte aligned
+  const bool contig = ((((uintptr_t)(a + M.hA)) >> 3) & 1u) == 0 && !(M.dbg & 8);
   const u64 nblk = b < M.NB ? (M.NB - 1 - b) / G + 1 : 0;  // blocks of this CTA
-  auto in_place = [&](u64 j) { return keep0 && j > 0; };
   auto wait_or_abort = [&](u64* bar, u32 ph) -> bool {
     u32 n = 0;
     while (!mbar_try(bar, ph))
@@ -369,15 +397,14 @@ __global__ void __launch_bounds__(MG_THREADS, MG_CTAS_PER_SM) merge_kernel(Merge
   if (tid == 0) {
     for (int q = 0; q < 2; ++q) {
       mbar_init(&s_full[q], 1);
-      mbar_init(&s_sfree[q], 1);
+      mbar_init(&s_sfree[q], NMW / 32);
     }
-    mbar_init(&s_ofull, 1);
-    mbar_init(&s_ofree, 1);
+    s_dfdone = 0;
     mbar_fence_init();
   }
   __syncthreads();
 
-  const bool prof = (M.dbg & 4) && b == 0 && (tid == 0 || tid == 32);
+  const bool prof = (M.dbg & 4) && b == 0 && (tid == 0 || (tid >= 32 && tid < 64) || tid == 64);
   u64 cyc[6] = {0, 0, 0, 0, 0, 0};
   u64 c0 = clock64();
   auto mark = [&](int q) {
@@ -445,12 +472,33 @@ __global__ void __launch_bounds__(MG_THREADS, MG_CTAS_PER_SM) merge_kernel(Merge
         const u32 l2 = __shfl_up_sync(0xffffffffu, lo, o), b2 = __shfl_up_sync(0xffffffffu, bo, o);
         if (lane >= (u32)o) { lo += l2; bo += b2; }
       }
-      const u32 total = __shfl_sync(0xffffffffu, bo, 7);
       lo -= (u32)len;
       bo -= bytes;
-      if (lane < 6) {
-        s_seg[sb][2 + lane] = len ? lo : 0xffffffffu;
-        s_seg[sb][8 + lane] = bo / 8 + par;
+      u32 total;
+      if (contig) {
+        // every piece after the first of its side starts (and the one before
+        // it ends) 16-byte aligned, so each side is one contiguous range of
+        // staging: A at sA = parity of its first word, B from the next even
+        // word after A (+ its first word's parity); copies never overlap
+        const u32 na_b = (u32)(i1 - i0);
+        const unsigned pres = __ballot_sync(0xffffffffu, lane < 6 && len != 0);
+        const unsigned presA = pres & 7u, presB = pres & 0x38u;
+        const u32 parA = presA ? (u32)__shfl_sync(0xffffffffu, par, __ffs(presA) - 1) : 0u;
+        const u32 parB = presB ? (u32)__shfl_sync(0xffffffffu, par, __ffs(presB) - 1) : 0u;
+        const u32 sA = parA, sB = ((sA + na_b + 1u) & ~1u) + parB;
+        const u32 st = lane < 3 ? sA + lo : sB + (lo - na_b);  // staging word of this piece
+        bo = (st - par) * 8u;
+        total = __reduce_add_sync(0xffffffffu, lane < 6 ? bytes : 0u);
+        if (lane == 0) {
+          s_seg[sb][2] = sA;
+          s_seg[sb][3] = sB;
+        }
+      } else {
+        total = __shfl_sync(0xffffffffu, bo + bytes, 7);
+        if (lane < 6) {
+          s_seg[sb][2 + lane] = len ? lo : 0xffffffffu;
+          s_seg[sb][8 + lane] = bo / 8 + par;
+        }
       }
       if (lane == 0) {
         s_seg[sb][0] = (u32)(i1 - i0);
@@ -462,9 +510,47 @@ __global__ void __launch_bounds__(MG_THREADS, MG_CTAS_PER_SM) merge_kernel(Merge
       __syncwarp();
       if (lane < 6 && len) tma_load_1d(stage + bo / 8, a + ph - par, bytes, &s_full[sb]);
     };
+    fetch_plan(b);
+    for (u64 j = 0; j < nblk && j < 2; ++j) issue_load(b + j * G, (int)j);
+    bool ok = true;
+    for (u64 j = 0; j < nblk && ok; ++j) {
+      const u64 m = b + j * G;
+      const int sb = (int)(j & 1);
+      const u32 use = (u32)(j >> 1);
+      if (j == 0) {  // publish block 0's load
+        if (!wait_or_abort(&s_full[0], 0)) { ok = false; break; }
+        if (lane == 0) st_relaxed_u32(M.status + MG_SST * b, (u32)(m + 1));
+      }
+      // two local events, whichever comes first: the merge warps have read
+      // block j (its staging buffer takes block j+2) / block j+1 has landed
+      // (publish it for the other CTAs' dataflow rule)
+      bool iss = true, pub = j + 1 < nblk;
+      u32 spins = 0;
+      while (iss || pub) {
+        if (iss && __shfl_sync(0xffffffffu, (int)mbar_try(&s_sfree[sb], use & 1), 0)) {
+          iss = false;
+          if (j + 2 < nblk) {
+            if (lane == 0) fence_proxy_async_smem();
+            __syncwarp();
+            issue_load(m + 2 * G, sb);
+          }
+          mark(0);
+        }
+        if (pub && __shfl_sync(0xffffffffu, (int)mbar_try(&s_full[sb ^ 1], ((j + 1) >> 1) & 1), 0)) {
+          pub = false;
+          if (lane == 0) st_relaxed_u32(M.status + MG_SST * b, (u32)(m + G + 1));
+          mark(1);
+        }
+        if ((++spins & 255) == 0 && ld_relaxed_u32(&g->sync.abort)) { ok = false; break; }
+      }
+    }
+    if (!ok && lane == 0) atomicExch(&g->sync.abort, 1u);
+  } else if (tid < 64) {
+    // ================================================= dataflow watcher
+    const u32 lane = tid & 31;
     // every block <= upto has reported loaded (lanes poll 8 CTAs each).
-    // WAR only: the store is issued after these loads returned the flags, and
-    // a flag goes up only after its reader's bulk loads landed.
+    // WAR only: the merge warps store after these loads returned the flags,
+    // and a flag goes up only after its reader's bulk loads landed.
     constexpr int MAXS = 8;  // G <= 256
     auto wait_loaded = [&](u64 upto) -> bool {
       u64 spins = 0;
@@ -475,10 +561,8 @@ __global__ void __launch_bounds__(MG_THREADS, MG_CTAS_PER_SM) merge_kernel(Merge
           const u32 c = lane + 32 * q;
           if (c >= G || c > upto) continue;
           const u32 mc = c + (((u32)upto - c) / G) * G;  // 32-bit: NB < 2^32
-          if (ld_relaxed_u32(M.status + c) < mc + 1) ready = false;
+          if (ld_relaxed_u32(M.status + MG_SST * c) < mc + 1) ready = false;
         }
-        // WAR only: the store below is issued after these loads returned the
-        // flags, and a flag goes up only after its reader's bulk loads landed
         if (__all_sync(0xffffffffu, ready)) return true;
         int ok = 1;
         if (lane == 0) {
@@ -491,159 +575,215 @@ __global__ void __launch_bounds__(MG_THREADS, MG_CTAS_PER_SM) merge_kernel(Merge
         if (!__shfl_sync(0xffffffffu, ok, 0)) return false;
       }
     };
-    fetch_plan(b);
-    for (u64 j = 0; j < nblk && j < 2; ++j) issue_load(b + j * G, (int)j);
-    // (an event loop that polls loads, refills and the dataflow rule without
-    // blocking measured slower: 38 vs 32 ms at 2^32 — the status poll is an
-    // L2 round trip on every pass)
+    // the precise form of the rule: block m overwrites (parts of) slots
+    // q_lo..q_hi, whose chunks are read by the blocks rlo..rhi (computed in
+    // P0b; rhi <= m + L) — only those must have loaded.  Blocks over the tail
+    // use the global form (every block <= m + L).  Lane k watches block
+    // jb + k of a 32-block window: one round of status loads checks all 32,
+    // and the announced count is the prefix of satisfied blocks — the
+    // watcher is not a chain of dependent L2 round trips per block.
+    const u64 tail_blk = M.hB ? (M.n - M.hB) / MG_C : M.NB;  // first block over the tail
     bool ok = true;
-    bool owe_ofree = false;  // a store's read of s_obuf is still in flight
-    auto settle_ofree = [&]() {
-      if (owe_ofree && lane == 0) {
-        bulk_wait_read_all();
-        mbar_arrive(&s_ofree);
-      }
-      owe_ofree = false;
-      __syncwarp();
-    };
-    for (u64 j = 0; j < nblk; ++j) {
+    for (u64 jb = 0; jb < nblk && ok; jb += 32) {
+      const u64 j = jb + lane;
       const u64 m = b + j * G;
-      const int sb = (int)(j & 1);
-      const u32 use = (u32)(j >> 1);
-      if (j == 0) {  // publish block 0's load
-        if (!wait_or_abort(&s_full[0], 0)) { ok = false; break; }
-        if (lane == 0) st_relaxed_u32(M.status + b, (u32)(m + 1));
-      }
-      // the merge warps have read block j: its staging buffer takes block j+2
-      if (!in_place(j)) {
-        if (!wait_or_abort(&s_sfree[sb], use & 1)) { ok = false; break; }
-        if (j + 2 < nblk) {
-          if (lane == 0) fence_proxy_async_smem();
-          __syncwarp();
-          issue_load(m + 2 * G, sb);
+      int mode = 0;  // 0 nothing to wait for, 1 blocks lo..hi, 2 every block <= hi
+      u32 lo = 1, hi = 0;
+      if (j < nblk && !(keep0 && j == 0) && !(M.dbg & 1)) {
+        if (m >= tail_blk || (M.dbg & 16)) {
+          mode = 2;
+          hi = (u32)(m + M.L < M.NB - 1 ? m + M.L : M.NB - 1);
+        } else {
+          const u64 p0 = m * MG_C;
+          const u64 qlo = p0 >= M.hA ? (p0 - M.hA) >> MG_LOGC : 0;
+          const u64 qe = (p0 + MG_C - 1 >= M.hA ? ((p0 + MG_C - 1 - M.hA) >> MG_LOGC) : 0);
+          const u64 qhi = qe < M.K - 1 ? qe : M.K - 1;
+          lo = 0xffffffffu;
+          for (u64 q = qlo; q <= qhi && q < M.K; ++q) {
+            const u32 l1 = __ldcg(M.rlo + q), h1 = __ldcg(M.rhi + q);
+            if (l1 <= h1) {  // the chunk in slot q has readers
+              lo = l1 < lo ? l1 : lo;
+              hi = h1 > hi ? h1 : hi;
+            }
+          }
+          if (lo <= hi) mode = ((u64)hi - lo + 1 >= G) ? 2 : 1;
         }
       }
-      // the merge warps need s_obuf back before they can finish block j: the
-      // previous store's read is waited for only now, not right after issue
-      settle_ofree();
-      // publish block j+1's load as soon as it has landed
-      if (j + 1 < nblk) {
-        if (!wait_or_abort(&s_full[sb ^ 1], ((j + 1) >> 1) & 1)) { ok = false; break; }
-        if (lane == 0) st_relaxed_u32(M.status + b, (u32)(m + G + 1));
+      bool sat = mode == 0;
+      u64 spins = 0;
+      for (;;) {
+        // only the first few unsatisfied blocks of the window poll
+        const unsigned bal0 = __ballot_sync(0xffffffffu, sat);
+        const u32 k0 = bal0 == 0xffffffffu ? 32u : (u32)(__ffs(~bal0) - 1);
+        if (!sat && mode == 1 && lane < k0 + 2) {
+          // up to 4 readers with independent loads in flight (one round trip)
+          u32 v[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const u32 x = lo + q <= hi ? lo + q : hi;
+            v[q] = ld_relaxed_u32(M.status + MG_SST * (x % G));
+          }
+          bool r = true;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const u32 x = lo + q <= hi ? lo + q : hi;
+            if (v[q] < x + 1u) r = false;
+          }
+          for (u32 x = lo + 4; x <= hi; ++x)
+            if (ld_relaxed_u32(M.status + MG_SST * (x % G)) < x + 1u) r = false;
+          if (prof && !r && lane == 0) cyc[4] += 1;  // unsatisfied polls of the window's first block
+          sat = r;
+        }
+        if (prof && lane == 0) cyc[5] += 1;
+        const unsigned bal = __ballot_sync(0xffffffffu, sat);
+        const u32 k = bal == 0xffffffffu ? 32u : (u32)(__ffs(~bal) - 1);
+        if (k > 0 && lane == 0) {
+          __threadfence_block();
+          *(volatile u32*)&s_dfdone = (u32)(jb + k);
+        }
+        if (k == 32) break;
+        if (__shfl_sync(0xffffffffu, mode, k) == 2) {  // cooperative global wait
+          const u32 upto = __shfl_sync(0xffffffffu, hi, k);
+          if (!wait_loaded(upto)) { ok = false; break; }
+          if (lane == k) sat = true;
+          continue;
+        }
+        int go = 1;
+        if (lane == 0) {
+          if (++spins > 4) __nanosleep(128);
+          if ((spins & 1023) == 0) {
+            if (ld_relaxed_u32(&g->sync.abort)) go = 0;
+            else if (spins > (1ull << 25)) { atomicExch(&g->sync.abort, 1u); go = 0; }
+          }
+        }
+        if (!__shfl_sync(0xffffffffu, go, 0)) { ok = false; break; }
       }
-      mark(0);
-      if (!wait_or_abort(&s_ofull, (u32)(j & 1))) { ok = false; break; }  // output written
-      mark(1);
-      if (keep0 && j == 0) continue;  // block 0 is written after the final barrier
-      const u64 upto = m + M.L < M.NB - 1 ? m + M.L : M.NB - 1;
-      if (!(M.dbg & 1) && !wait_loaded(upto)) { ok = false; break; }
       mark(2);
-      const u64* out = in_place(j) ? smem + sb * MG_STAGE_WORDS : s_obuf;
-      if (lane == 0) {
-        const u64 p0 = m * MG_C, p1 = (m + 1) * MG_C < M.n ? (m + 1) * MG_C : M.n;
-        const u32 len = (u32)(p1 - p0);
-        const u32 head = (u32)(((uintptr_t)(a + p0) >> 3) & 1u);
-        const u32 body = len > head ? ((len - head) & ~1u) : 0u;
-        if (head && len) a[p0] = out[0];
-        if (head + body < len) a[p0 + len - 1] = out[len - 1];
-        if (body) {
-          tma_store_1d(a + p0 + head, out + head, body * 8u);
-          bulk_commit();
-        }
-        if (in_place(j)) bulk_wait_read_all();  // the staging buffer is refilled below
-      }
-      owe_ofree = !in_place(j);  // settled (read waited, s_ofree arrived) next iteration
-      __syncwarp();
-      if (in_place(j) && j + 2 < nblk) {  // the store has read it: refill
-        if (lane == 0) fence_proxy_async_smem();
-        __syncwarp();
-        issue_load(m + 2 * G, sb);
-      }
-      mark(3);
     }
-    settle_ofree();
-    if (lane == 0) bulk_wait_all();
     if (!ok && lane == 0) atomicExch(&g->sync.abort, 1u);
   } else {
     // ================================================= merge warps
-    const u32 t = tid - 32;
+    const u32 t = tid - 64, w = t >> 5, lane = t & 31;
     const u32 r0_all = (u32)(((u64)t * MG_C) / NMW), r1_all = (u32)(((u64)(t + 1) * MG_C) / NMW);
-    u32 ofree_uses = 0;  // completed phases of s_ofree
+    const u32 wr0 = (u32)(((u64)(w * 32) * MG_C) / NMW), wr1 = (u32)(((u64)(w * 32 + 32) * MG_C) / NMW);
+    u64* scr = s_scr + w * MG_SCR - wr0;  // indexed by block-relative output rank
     for (u64 j = 0; j < nblk; ++j) {
+      const u64 m = b + j * G;
       const int sb = (int)(j & 1);
       if (!wait_or_abort(&s_full[sb], (u32)((j >> 1) & 1))) break;
+      mark(3);
       u64* sp = smem + sb * MG_STAGE_WORDS;
       const u32 na = s_seg[sb][0], nb = s_seg[sb][1], total = na + nb;
       const u32 r0 = r0_all < total ? r0_all : total, r1 = r1_all < total ? r1_all : total;
-      // segment map: A side segments 0..2, B side 3..5 (lo = logical start,
-      // 0xffffffff if absent); staging word = logical + offset of its segment
-      const u32 la1 = s_seg[sb][3], la2 = s_seg[sb][4];
-      const u32 oa0 = s_seg[sb][2] == 0xffffffffu ? 0u : s_seg[sb][8] - s_seg[sb][2];
-      const u32 oa1 = s_seg[sb][9] - la1, oa2 = s_seg[sb][10] - la2;
-      const u32 lb4 = s_seg[sb][6], lb5 = s_seg[sb][7];
-      const u32 ob3 = s_seg[sb][5] == 0xffffffffu ? 0u : s_seg[sb][11] - s_seg[sb][5];
-      const u32 ob4 = s_seg[sb][12] - lb4, ob5 = s_seg[sb][13] - lb5;
-      auto mapA = [&](u32 x) -> u32 { return x + (x >= la2 ? oa2 : (x >= la1 ? oa1 : oa0)); };
-      auto mapB = [&](u32 x) -> u32 { return x + (x >= lb5 ? ob5 : (x >= lb4 ? ob4 : ob3)); };
       u64 o[MO];
-      if (r0 < r1) {
-        u32 lo = r0 > nb ? r0 - nb : 0, hi = r0 < na ? r0 : na;
-        while (lo < hi) {
-          const u32 mid = (lo + hi) >> 1;
-          if (sp[mapA(mid)] <= sp[mapB(na + r0 - mid - 1)]) lo = mid + 1;
-          else hi = mid;
-        }
-        u32 i = lo, jj = r0 - lo;
-        u64 ka = sp[mapA(i)];
-        u64 kb = sp[mapB(na + jj)];
+      if (M.dbg & 2) {  // profiling: no merge (outputs are garbage)
 #pragma unroll
-        for (int q = 0; q < MO; ++q) {
-          const bool pa = (jj >= nb) || (i < na && ka <= kb);  // ties from A
-          o[q] = pa ? ka : kb;
-          const u32 ni = i + (pa ? 1u : 0u), nj = jj + (pa ? 0u : 1u);
-          // unconditional load (one word past a side's end is still staging
-          // memory), then select: no divergent branch per step
-          const u64 nk = sp[pa ? mapA(ni) : mapB(na + nj)];
-          ka = pa ? nk : ka;
-          kb = pa ? kb : nk;
-          i = ni;
-          jj = nj;
+        for (int q = 0; q < MO; ++q) o[q] = sp[(r0 + q) & (MG_C - 1)];
+      } else if (contig) {
+        const u32 sA = s_seg[sb][2], sB = s_seg[sb][3];
+        if (r0 < r1) {
+          u32 lo = r0 > nb ? r0 - nb : 0, hi = r0 < na ? r0 : na;
+          const u32 bq = sB + r0 - 1;  // B word of merge-path step mid: bq - mid
+          while (lo < hi) {
+            const u32 mid = (lo + hi) >> 1;
+            if (sp[sA + mid] <= sp[bq - mid]) lo = mid + 1;
+            else hi = mid;
+          }
+          // absolute staging indices; the word one past either side's end is
+          // still staging memory, so the next-key load is unconditional
+          u32 ai = sA + lo, bi = sB + (r0 - lo);
+          const u32 ae = sA + na, be = sB + nb;
+          u64 ka = sp[ai], kb = sp[bi];
+#pragma unroll
+          for (int q = 0; q < MO; ++q) {
+            const bool pa = (bi >= be) || (ai < ae && ka <= kb);  // ties from A
+            o[q] = pa ? ka : kb;
+            ai += pa ? 1u : 0u;
+            bi += pa ? 0u : 1u;
+            const u64 nk = sp[pa ? ai : bi];
+            ka = pa ? nk : ka;
+            kb = pa ? kb : nk;
+          }
+        }
+      } else {
+        // segment map: A side segments 0..2, B side 3..5 (lo = logical start,
+        // 0xffffffff if absent); staging word = logical + offset of its segment
+        const u32 la1 = s_seg[sb][3], la2 = s_seg[sb][4];
+        const u32 oa0 = s_seg[sb][2] == 0xffffffffu ? 0u : s_seg[sb][8] - s_seg[sb][2];
+        const u32 oa1 = s_seg[sb][9] - la1, oa2 = s_seg[sb][10] - la2;
+        const u32 lb4 = s_seg[sb][6], lb5 = s_seg[sb][7];
+        const u32 ob3 = s_seg[sb][5] == 0xffffffffu ? 0u : s_seg[sb][11] - s_seg[sb][5];
+        const u32 ob4 = s_seg[sb][12] - lb4, ob5 = s_seg[sb][13] - lb5;
+        auto mapA = [&](u32 x) -> u32 { return x + (x >= la2 ? oa2 : (x >= la1 ? oa1 : oa0)); };
+        auto mapB = [&](u32 x) -> u32 { return x + (x >= lb5 ? ob5 : (x >= lb4 ? ob4 : ob3)); };
+        if (r0 < r1) {
+          u32 lo = r0 > nb ? r0 - nb : 0, hi = r0 < na ? r0 : na;
+          while (lo < hi) {
+            const u32 mid = (lo + hi) >> 1;
+            if (sp[mapA(mid)] <= sp[mapB(na + r0 - mid - 1)]) lo = mid + 1;
+            else hi = mid;
+          }
+          u32 i = lo, jj = r0 - lo;
+          u64 ka = sp[mapA(i)];
+          u64 kb = sp[mapB(na + jj)];
+#pragma unroll
+          for (int q = 0; q < MO; ++q) {
+            const bool pa = (jj >= nb) || (i < na && ka <= kb);  // ties from A
+            o[q] = pa ? ka : kb;
+            const u32 ni = i + (pa ? 1u : 0u), nj = jj + (pa ? 0u : 1u);
+            // unconditional load (one word past a side's end is still staging
+            // memory), then select: no divergent branch per step
+            const u64 nk = sp[pa ? mapA(ni) : mapB(na + nj)];
+            ka = pa ? nk : ka;
+            kb = pa ? kb : nk;
+            i = ni;
+            jj = nj;
+          }
         }
       }
       mark(0);
-      named_bar(1, NMW);  // every merge warp is done reading the staging buffer
-      u64* out = s_obuf;
-      if (in_place(j)) {
-        out = sp;
-      } else {
-        if (t == 0) mbar_arrive(&s_sfree[sb]);
-        if (j > 0 && !(keep0)) {  // the previous block's store has read s_obuf
-          if (!wait_or_abort(&s_ofree, ofree_uses & 1)) break;
-          ++ofree_uses;
+      // this warp is done with the staging buffer
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&s_sfree[sb]);
+      // the dataflow rule (announced by the watcher warp)
+      {
+        // sleep between polls: 15 spinning warps would take the issue slots
+        // and the shared-memory pipe the loader and the watcher need
+        u32 n = 0;
+        while (*(volatile u32*)&s_dfdone < (u32)(j + 1)) {
+          __nanosleep(128);
+          if ((++n & 255) == 0 && ld_relaxed_u32(&g->sync.abort)) break;
         }
+        __threadfence_block();
       }
       mark(1);
+      // transpose through the warp's tile, then coalesced stores
 #pragma unroll
       for (int q = 0; q < MO; ++q)
-        if (r0 + q < r1) out[r0 + q] = o[q];
-      fence_proxy_async_smem();
-      named_bar(1, NMW);
-      if (t == 0) mbar_arrive(&s_ofull);
+        if (r0 + q < r1) scr[r0 + q] = o[q];
+      __syncwarp();
+      const u32 we = wr1 < total ? wr1 : total;
+      u64* dst = (keep0 && j == 0) ? M.head_save : a + m * MG_C;
+      for (u32 r = wr0 + lane; r < we; r += 32) __stcs(dst + r, scr[r]);
+      __syncwarp();
       mark(2);
     }
   }
-  if (prof && tid == 32)
-    for (int q = 0; q < 3; ++q) g->sec[q] = cyc[q];
-  if (prof && tid == 0) {
-    g->sec[3] = cyc[0] + cyc[1];  // waiting for loads to land / for the merge warps
-    g->sec[4] = cyc[2];           // dataflow rule
-    g->sec[5] = cyc[3];           // store (+ refill issue)
+  if (prof && tid == 64) {
+    g->sec[0] = cyc[3];  // waiting for the block's loads to land
+    for (int q = 0; q < 3; ++q) g->sec[1 + q] = cyc[q];
+  }
+  if (prof && tid == 0) g->sec[4] = cyc[0] + cyc[1];  // loader: refills + publishes
+  if (prof && tid == 32) g->sec[5] = cyc[2];          // watcher: dataflow rule
+  if ((M.dbg & 4) && b == 0 && tid < 64 && tid >= 32) {  // watcher lanes: missing-reader polls
+    atomicAdd((unsigned long long*)&g->sec[6], (unsigned long long)cyc[4]);
+    atomicAdd((unsigned long long*)&g->sec[7], (unsigned long long)cyc[5]);  // polls
   }
   if (M.hA > 0) {
     if (!grid_barrier(&g->sync, gen)) return;
     if (b == 0) {
       const u64 p1 = MG_C < M.n ? MG_C : M.n;
-      for (u32 k = tid; k < (u32)p1; k += MG_THREADS) a[k] = s_obuf[k];
+      for (u32 k = tid; k < (u32)p1; k += MG_THREADS) a[k] = __ldcg(M.head_save + k);
     }
   }
   if (tm) g->t[5] = globaltimer_ns();
@@ -651,15 +791,15 @@ __global__ void __launch_bounds__(MG_THREADS, MG_CTAS_PER_SM) merge_kernel(Merge
 
 // ---------------------------------------------------------------------------
 // single-CTA merge of a small array (n <= C)
-__global__ void __launch_bounds__(MG_THREADS, 1) merge_small_kernel(u64* a, u32 n, u32 na) {
+__global__ void __launch_bounds__(MG_CP, 1) merge_small_kernel(u64* a, u32 n, u32 na) {
   extern __shared__ __align__(16) u64 smem[];
   u64* s_in = smem;
   u64* s_out = smem + MG_IN_WORDS;
-  for (u32 k = threadIdx.x; k < n; k += MG_THREADS) s_in[SI(k)] = a[k];
+  for (u32 k = threadIdx.x; k < n; k += MG_CP) s_in[SI(k)] = a[k];
   __syncthreads();
   block_merge(s_in, na, n - na, s_out);
   __syncthreads();
-  for (u32 k = threadIdx.x; k < n; k += MG_THREADS) a[k] = s_out[SO(k)];
+  for (u32 k = threadIdx.x; k < n; k += MG_CP) a[k] = s_out[SO(k)];
 }
 
 // sortedness of both runs (debug=True): counts descents inside each run
@@ -678,7 +818,7 @@ __global__ void check_sorted_kernel(const u64* a, u64 n, u64 na, u32* bad) {
 // host
 
 struct MergeLayout {
-  size_t dest, inv, lab0, lab1, jmp0, jmp1, visited, cr, plan, status, g, cut, total;
+  size_t dest, inv, lab0, lab1, jmp0, jmp1, visited, rlo, rhi, cr, plan, head, g, cut, total;
   u64 D, ncuts, desc_bytes;
 };
 
@@ -702,9 +842,10 @@ static MergeLayout merge_layout(u64 n, u64 na, u64 budget_words, int grid) {
   L.jmp0 = take(K * 4);
   L.jmp1 = take(K * 4);
   L.visited = take(K);
+  L.rlo = take(K * 4);
+  L.rhi = take(K * 4);
   L.cr = take((NB + 1) * 8);
   L.plan = take(NB * 32);
-  L.status = take((size_t)grid * 4);
   L.g = take(sizeof(MergeGlobal));
   L.desc_bytes = off;
   const u64 desc_words = (off + 7) / 8;
@@ -720,6 +861,12 @@ static MergeLayout merge_layout(u64 n, u64 na, u64 budget_words, int grid) {
     L.ncuts = 0;
   }
   L.cut = take(L.ncuts * MG_C * 8);
+  // block 0's deferred output (only if there is an in-place head): the cut
+  // buffer or the pointer-jumping arrays are dead by the block phase; only a
+  // small array with a budget below one chunk needs C words of its own
+  if (hA == 0 || L.ncuts > 0) L.head = L.cut;
+  else if (L.visited - L.lab0 >= MG_C * 8) L.head = L.lab0;
+  else L.head = take(MG_C * 8);
   L.total = off;
   return L;
 }
@@ -753,7 +900,7 @@ int merge_device(u64* a, u64 n, u64 split, int check_sorted, void* ws, size_t ws
     const size_t smem = (MG_IN_WORDS + MG_OUT_WORDS) * sizeof(u64);
     PIP_CUDA(cudaFuncSetAttribute(merge_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)smem));
-    merge_small_kernel<<<1, MG_THREADS, smem, st>>>(a, (u32)n, (u32)split);
+    merge_small_kernel<<<1, MG_CP, smem, st>>>(a, (u32)n, (u32)split);
     PIP_CHECK_LAUNCH();
     return PIP_OK;
   }
@@ -798,12 +945,19 @@ int merge_device(u64* a, u64 n, u64 split, int check_sorted, void* ws, size_t ws
   M.jmp[0] = (u32*)(w + L.jmp0);
   M.jmp[1] = (u32*)(w + L.jmp1);
   M.visited = (unsigned char*)(w + L.visited);
+  M.rlo = (u32*)(w + L.rlo);
+  M.rhi = (u32*)(w + L.rhi);
   M.cr = (u64*)(w + L.cr);
   M.plan = (ulonglong4*)(w + L.plan);
-  M.status = (u32*)(w + L.status);
+  // the per-CTA load status words live in the caller's O(#CTAs) device
+  // scratch (like the scan look-back ring), not in the metered workspace
+  const size_t status_off = 128, status_bytes = (size_t)grid * 4 * MG_SST;
+  if (!scratch || scratch_bytes < status_off + status_bytes) return PIP_ERR_OOM;
+  M.status = (u32*)((char*)scratch + status_off);
+  M.head_save = (u64*)(w + L.head);
   M.g = (MergeGlobal*)(w + L.g);
   if ((u64)grid <= 2 * M.L || grid > 256) return PIP_ERR_UNSUPPORTED;
-  PIP_CUDA(cudaMemsetAsync(M.status, 0, (size_t)grid * 4, st));
+  PIP_CUDA(cudaMemsetAsync(M.status, 0, status_bytes, st));
   PIP_CUDA(cudaMemsetAsync(M.g, 0, sizeof(MergeGlobal), st));
   const size_t smem = MG_SMEM;
   PIP_CUDA(cudaFuncSetAttribute(merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -815,10 +969,11 @@ int merge_device(u64* a, u64 n, u64 split, int check_sorted, void* ws, size_t ws
   PIP_CUDA(cudaStreamSynchronize(st));
   if (gh.sync.abort) return PIP_ERR_CUDA;
   if (timing_enabled() && (M.dbg & 4))
-    fprintf(stderr, "[pip merge] CTA0 cycles: merge warps: merge (+ wait data) %llu | wait output buffer %llu | write-out %llu ; "
-            "control: loads/merge wait %llu | dataflow wait %llu | store %llu\n",
+    fprintf(stderr, "[pip merge] CTA0 cycles: merge warps: wait data %llu | merge %llu | wait output buffer %llu | write-out %llu ; "
+            "loader: refills/publishes %llu | watcher: dataflow wait %llu | missing-reader polls after m %llu before m %llu\n",
             (unsigned long long)gh.sec[0], (unsigned long long)gh.sec[1], (unsigned long long)gh.sec[2],
-            (unsigned long long)gh.sec[3], (unsigned long long)gh.sec[4], (unsigned long long)gh.sec[5]);
+            (unsigned long long)gh.sec[3], (unsigned long long)gh.sec[4], (unsigned long long)gh.sec[5],
+            (unsigned long long)gh.sec[6], (unsigned long long)gh.sec[7]);
   if (timing_enabled())
     fprintf(stderr,
             "[pip merge] n=%llu K=%llu ncuts=%llu D=%llu uncut=%u  P0 %.3f ms | cuts %.3f | "

@@ -317,3 +317,27 @@ def test_rp_reservation_modes(pip, orc, monkeypatch, mode, n, seed, frac, debug)
     assert st.rounds == ref["rounds"]
     assert st.committed_per_round == ref["committed_per_round"]
     assert st.peak_table_load == ref["peak_count"] / ref["capacity"]
+
+
+@pytest.mark.parametrize("na,nb", [(8192 * 5, 8192 * 4 + 17), (20_000, 13_001), (300_000, 290_000),
+                                   (65_536, 65_536), (8193, 30_001)])
+@pytest.mark.parametrize("mode", ["offset_view", "mapped_staging", "global_rule"])
+def test_merge_staging_layouts(pip, orc, monkeypatch, na, nb, mode):
+    """Both staging layouts of the block phase: contiguous sides (interior
+    piece boundaries 16-byte aligned) and the segment map (odd word offset of
+    the chunk grid, or forced with PIP_MERGE_DBG bit 3); and the global form
+    of the dataflow rule (PIP_MERGE_DBG bit 4) beside the per-slot one."""
+    x = np.sort(rand_words(na + 3 * nb, na, 1 << 20))
+    y = np.sort(rand_words(na + 5 * nb, nb, 1 << 20))
+    want = orc.seq_merge(x, y)
+    a = np.concatenate([x, y])
+    if mode == "offset_view":
+        buf = dev(np.concatenate([np.zeros(1, dtype=np.uint64), a]))
+        t = buf[1:]
+    else:
+        monkeypatch.setenv("PIP_MERGE_DBG", "8" if mode == "mapped_staging" else "16")
+        t = dev(a)
+    pip.relaxed.merge_relaxed(t, na)
+    assert np.array_equal(host(t), want)
+    if mode == "offset_view":
+        assert int(buf[0].item()) == 0

@@ -14,6 +14,7 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import torch  # noqa: E402
 
 import paper_2103_01216_b200 as pip  # noqa: E402
+from bench import sort_run  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--op", default="scan")
@@ -41,8 +42,8 @@ elif args.op == "merge":
     ws = torch.empty(wb, dtype=torch.uint8, device="cuda")
     for _ in range(args.reps):
         pip.Rng(1).words_device(0, n, shift=34, out=a)
-        a[:na] = torch.sort(a[:na]).values
-        a[na:] = torch.sort(a[na:]).values
+        sort_run(a[:na], torch, pip)
+        sort_run(a[na:], torch, pip)
         assert lib.pip_merge_u64(a.data_ptr(), n, na, 0, ws.data_ptr(), wb, sp, sb, st) == 0
 elif args.op == "rp":
     h = pip.Rng(1).swaps_device(0, n)
