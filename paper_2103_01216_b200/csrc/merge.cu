@@ -63,10 +63,12 @@ static constexpr u32 MG_IN_WORDS = (u32)(MG_C + MG_C / 8);
 static constexpr u32 MG_OUT_WORDS = (u32)(MG_C + MG_C / 16);
 static constexpr u32 MG_STAGE_WORDS = (u32)(MG_C + 16);  // bulk-copy staging (+2 junk words x 6 segments)
 // per merge warp: a transpose tile for its <= 32 * 8192 / 480 + 1 outputs
-static constexpr u32 MG_SCR = (u32)((32 * MG_C) / (MG_THREADS - 64) + 2);
+static constexpr u32 MG_SCR = (u32)((32 * MG_C) / (MG_THREADS - 64) + 4);
 // per-CTA load status words one L2 line apart: every CTA polls its
 // neighbours' words, and packed words made a few lines a hot spot
 static constexpr u32 MG_SST = 32;
+// at most this many slots on cut-free cycles: one CTA rotates them serially
+static constexpr u32 MG_UNCUT_SERIAL = 2048;
 static constexpr size_t MG_SMEM = (size_t)(2 * MG_STAGE_WORDS + (MG_THREADS / 32 - 2) * MG_SCR) * 8;
 
 struct MergeGlobal {
@@ -78,7 +80,8 @@ struct MergeGlobal {
 };
 
 struct MergeArgs {
-  u32 dbg;  // profiling knobs (PIP_MERGE_DBG): bit0 skip the dataflow wait, bit1 no merge, bit2 CTA 0 cycle counters
+  u32 dbg;  // PIP_MERGE_DBG: bit0 skip the dataflow wait (profiling), bit1 no merge (profiling), bit2 CTA 0 cycle counters,
+            // bit3 mapped staging, bit4 global dataflow rule, bit5 pointer jumping for cut-free cycles (tests)
   u64* a;
   u64 n, na, nb;
   u64 hA, hB, KA, KB, K, NB, D, ncuts, L;
@@ -312,7 +315,48 @@ __global__ void __launch_bounds__(MG_THREADS, MG_CTAS_PER_SM) merge_kernel(Merge
     if ((tid & 31) == 0 && cnt) atomicAdd(&g->uncut, cnt);
   }
   if (!grid_barrier(&g->sync, gen)) return;
-  if (ld_relaxed_u32(&g->uncut)) {
+  const u32 n_uncut = ld_relaxed_u32(&g->uncut);
+  if (n_uncut && n_uncut <= MG_UNCUT_SERIAL && !(M.dbg & 32)) {
+    // few slots (the usual case with a cut buffer): CTA 0 collects them and
+    // rotates each cycle through shared memory — no pointer-jumping rounds
+    if (b == 0) {
+      __shared__ u32 s_ucnt;
+      u32* s_list = reinterpret_cast<u32*>(smem + MG_C);
+      if (tid == 0) s_ucnt = 0;
+      __syncthreads();
+      for (u64 x = tid; x < M.K; x += MG_THREADS)
+        if (!__ldcg(M.visited + x) && __ldcg(M.inv + x) != (u32)x) {
+          const u32 i = atomicAdd(&s_ucnt, 1u);
+          if (i < MG_UNCUT_SERIAL) s_list[i] = (u32)x;
+        }
+      __syncthreads();
+      const u32 cnt = s_ucnt < MG_UNCUT_SERIAL ? s_ucnt : MG_UNCUT_SERIAL;
+      for (u32 c = 0; c < cnt; ++c) {
+        const u64 x0 = s_list[c];
+        // thread 0 alone reads and writes `visited` here (program order)
+        if (tid == 0) s_flag = !__ldcg(M.visited + x0);
+        __syncthreads();
+        const bool lead = s_flag != 0;
+        __syncthreads();
+        if (!lead) continue;
+        for (u32 k = tid; k < MG_C; k += MG_THREADS) s_out[k] = __ldcg(slot_ptr(M, x0) + k);
+        __syncthreads();
+        u64 sdst = x0;
+        for (u64 steps = 0; steps <= M.K; ++steps) {
+          if (tid == 0) M.visited[sdst] = 1;
+          const u64 src = __ldcg(M.inv + sdst);
+          if (src == x0) {
+            for (u32 k = tid; k < MG_C; k += MG_THREADS) slot_ptr(M, sdst)[k] = s_out[k];
+            break;
+          }
+          move_chunk(slot_ptr(M, sdst), slot_ptr(M, src));
+          sdst = src;
+        }
+        __syncthreads();
+      }
+    }
+    if (!grid_barrier(&g->sync, gen)) return;
+  } else if (n_uncut) {
     u64 s, e;
     mpart(M.K, G, b, s, e);
     for (u64 x = s + tid; x < e; x += MG_THREADS) {
@@ -666,7 +710,6 @@ __global__ void __launch_bounds__(MG_THREADS, MG_CTAS_PER_SM) merge_kernel(Merge
     const u32 t = tid - 64, w = t >> 5, lane = t & 31;
     const u32 r0_all = (u32)(((u64)t * MG_C) / NMW), r1_all = (u32)(((u64)(t + 1) * MG_C) / NMW);
     const u32 wr0 = (u32)(((u64)(w * 32) * MG_C) / NMW), wr1 = (u32)(((u64)(w * 32 + 32) * MG_C) / NMW);
-    u64* scr = s_scr + w * MG_SCR - wr0;  // indexed by block-relative output rank
     for (u64 j = 0; j < nblk; ++j) {
       const u64 m = b + j * G;
       const int sb = (int)(j & 1);
@@ -694,15 +737,19 @@ __global__ void __launch_bounds__(MG_THREADS, MG_CTAS_PER_SM) merge_kernel(Merge
           u32 ai = sA + lo, bi = sB + (r0 - lo);
           const u32 ae = sA + na, be = sB + nb;
           u64 ka = sp[ai], kb = sp[bi];
+          // (a second, bounds-free copy of this loop for threads whose range
+          // cannot exhaust a side measured slower: 16.0 vs 14.0 ms at 2^32)
+          {
 #pragma unroll
-          for (int q = 0; q < MO; ++q) {
-            const bool pa = (bi >= be) || (ai < ae && ka <= kb);  // ties from A
-            o[q] = pa ? ka : kb;
-            ai += pa ? 1u : 0u;
-            bi += pa ? 0u : 1u;
-            const u64 nk = sp[pa ? ai : bi];
-            ka = pa ? nk : ka;
-            kb = pa ? kb : nk;
+            for (int q = 0; q < MO; ++q) {
+              const bool pa = (bi >= be) || (ai < ae && ka <= kb);  // ties from A
+              o[q] = pa ? ka : kb;
+              ai += pa ? 1u : 0u;
+              bi += pa ? 0u : 1u;
+              const u64 nk = sp[pa ? ai : bi];
+              ka = pa ? nk : ka;
+              kb = pa ? kb : nk;
+            }
           }
         }
       } else {
@@ -757,14 +804,27 @@ __global__ void __launch_bounds__(MG_THREADS, MG_CTAS_PER_SM) merge_kernel(Merge
         __threadfence_block();
       }
       mark(1);
-      // transpose through the warp's tile, then coalesced stores
+      // transpose through the warp's tile (placed at the 16-byte parity of
+      // the destination), then coalesced 16-byte stores
+      u64* gd = ((keep0 && j == 0) ? M.head_save : a + m * MG_C) + wr0;
+      const u32 head = (u32)(((uintptr_t)gd >> 3) & 1u);
+      u64* scr = s_scr + w * MG_SCR + head - wr0;  // indexed by block-relative rank
 #pragma unroll
       for (int q = 0; q < MO; ++q)
         if (r0 + q < r1) scr[r0 + q] = o[q];
       __syncwarp();
-      const u32 we = wr1 < total ? wr1 : total;
-      u64* dst = (keep0 && j == 0) ? M.head_save : a + m * MG_C;
-      for (u32 r = wr0 + lane; r < we; r += 32) __stcs(dst + r, scr[r]);
+      const u32 cnt = (wr1 < total ? wr1 : total) - (wr0 < total ? wr0 : total);
+      const u64* sw = scr + wr0;  // sw[k] = output word gd[k]; gd + k, sw + k 16-byte aligned iff k = head mod 2
+      if (M.dbg & 64) {
+        for (u32 k = lane; k < cnt; k += 32) gd[k] = sw[k];
+      } else {
+        for (u32 k = head + 2 * lane; k + 1 < cnt; k += 64)
+          __stcs(reinterpret_cast<ulonglong2*>(gd + k), *reinterpret_cast<const ulonglong2*>(sw + k));
+        if (lane == 0 && cnt) {
+          if (head) __stcs(gd, sw[0]);
+          if (((cnt - head) & 1u) && cnt - 1 >= head) __stcs(gd + cnt - 1, sw[cnt - 1]);
+        }
+      }
       __syncwarp();
       mark(2);
     }

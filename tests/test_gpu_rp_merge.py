@@ -321,12 +321,13 @@ def test_rp_reservation_modes(pip, orc, monkeypatch, mode, n, seed, frac, debug)
 
 @pytest.mark.parametrize("na,nb", [(8192 * 5, 8192 * 4 + 17), (20_000, 13_001), (300_000, 290_000),
                                    (65_536, 65_536), (8193, 30_001)])
-@pytest.mark.parametrize("mode", ["offset_view", "mapped_staging", "global_rule"])
+@pytest.mark.parametrize("mode", ["offset_view", "mapped_staging", "global_rule", "pointer_jumping"])
 def test_merge_staging_layouts(pip, orc, monkeypatch, na, nb, mode):
     """Both staging layouts of the block phase: contiguous sides (interior
     piece boundaries 16-byte aligned) and the segment map (odd word offset of
     the chunk grid, or forced with PIP_MERGE_DBG bit 3); and the global form
-    of the dataflow rule (PIP_MERGE_DBG bit 4) beside the per-slot one."""
+    of the dataflow rule (PIP_MERGE_DBG bit 4) beside the per-slot one; and
+    pointer jumping for cut-free cycles (bit 5) beside the serial rotation."""
     x = np.sort(rand_words(na + 3 * nb, na, 1 << 20))
     y = np.sort(rand_words(na + 5 * nb, nb, 1 << 20))
     want = orc.seq_merge(x, y)
@@ -335,7 +336,8 @@ def test_merge_staging_layouts(pip, orc, monkeypatch, na, nb, mode):
         buf = dev(np.concatenate([np.zeros(1, dtype=np.uint64), a]))
         t = buf[1:]
     else:
-        monkeypatch.setenv("PIP_MERGE_DBG", "8" if mode == "mapped_staging" else "16")
+        monkeypatch.setenv("PIP_MERGE_DBG", {"mapped_staging": "8", "global_rule": "16",
+                                             "pointer_jumping": "32"}[mode])
         t = dev(a)
     pip.relaxed.merge_relaxed(t, na)
     assert np.array_equal(host(t), want)
