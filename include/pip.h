@@ -133,6 +133,18 @@ int pip_filter_u64_host(uint64_t* host_a, uint64_t n, const pip_pred* pred, uint
 int pip_rotate_u64(uint64_t* a, uint64_t n, uint64_t o, void* scratch, size_t scratch_bytes,
                    void* stream);
 
+/* ---- partition: strong.partition_unstable / relaxed.partition_relaxed ---- *
+ * Unstable in-place partition (strong.py:394-419, relaxed.py:312-344): on
+ * return a[0:m) holds the words with keep(x), a[m:n) the others (multiset
+ * preserved); m is written to device m_dev.  workspace holds
+ * pip_partition_workspace_bytes(n) (O(n/4096) descriptors).  Stream-ordered.
+ * pip_partition_u64_host: same on a host array (copies in/out; sync).     */
+size_t pip_partition_workspace_bytes(uint64_t n);
+int pip_partition_u64(uint64_t* a, uint64_t n, const pip_pred* pred, uint64_t* m_dev,
+                      void* workspace, size_t workspace_bytes, void* stream);
+int pip_partition_u64_host(uint64_t* host_a, uint64_t n, const pip_pred* pred, uint64_t* m_out,
+                           int device);
+
 /* ---- merge: strong.merge_strong / relaxed.merge_relaxed ------------------ *
  * a[0:split) and a[split:n) are sorted ascending (unsigned); on return a is
  * sorted.  `workspace`/`workspace_bytes` is the metered auxiliary space

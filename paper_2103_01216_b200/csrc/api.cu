@@ -70,6 +70,9 @@ size_t rp_workspace_bytes(u64 n, u64 prefix, int variant);
 int rp_device(u64* a, const u64* h, u64 n, u64 prefix, int variant, int debug,
               u64* counts_host, u64 rounds_cap, u64* trace_dev, void* ws, size_t ws_bytes,
               pip_rp_stats* stats, cudaStream_t st);
+size_t partition_workspace_bytes(u64 n);
+int partition_device(u64* a, u64 n, const pip_pred* pred, u64* m_dev, void* ws, size_t ws_bytes,
+                     cudaStream_t st);
 size_t merge_workspace_bytes(u64 n, u64 split, u64 budget_words);
 int merge_device(u64* a, u64 n, u64 split, int check_sorted, void* ws, size_t ws_bytes,
                  void* scratch, size_t scratch_bytes, cudaStream_t st);
@@ -365,6 +368,38 @@ int pip_rotate_u64(uint64_t* a, uint64_t n, uint64_t o, void* scratch, size_t sc
   (void)scratch;
   (void)scratch_bytes;
   return rotate_device((u64*)a, n, o, (cudaStream_t)stream);
+}
+
+size_t pip_partition_workspace_bytes(uint64_t n) { return partition_workspace_bytes(n); }
+
+int pip_partition_u64(uint64_t* a, uint64_t n, const pip_pred* pred, uint64_t* m_dev,
+                      void* workspace, size_t workspace_bytes, void* stream) {
+  return partition_device((u64*)a, n, pred, (u64*)m_dev, workspace, workspace_bytes,
+                          (cudaStream_t)stream);
+}
+
+int pip_partition_u64_host(uint64_t* host_a, uint64_t n, const pip_pred* pred, uint64_t* m_out,
+                           int device) {
+  if (!pred || !m_out || (n && !host_a)) return PIP_ERR_INVALID_ARG;
+  PIP_CUDA(cudaSetDevice(device));
+  if (n == 0) {
+    *m_out = 0;
+    return PIP_OK;
+  }
+  Stream s;
+  PIP_CUDA(s.create());
+  DevBuf a, ws, m;
+  PIP_CUDA(a.alloc(n * 8));
+  const size_t wb = partition_workspace_bytes(n);
+  PIP_CUDA(ws.alloc(wb));
+  PIP_CUDA(m.alloc(8));
+  PIP_CUDA(cudaMemcpyAsync(a.p, host_a, n * 8, cudaMemcpyHostToDevice, s.s));
+  int rc = partition_device((u64*)a.p, n, pred, (u64*)m.p, ws.p, wb, s.s);
+  if (rc) return rc;
+  PIP_CUDA(cudaMemcpyAsync(host_a, a.p, n * 8, cudaMemcpyDeviceToHost, s.s));
+  PIP_CUDA(cudaMemcpyAsync(m_out, m.p, 8, cudaMemcpyDeviceToHost, s.s));
+  PIP_CUDA(cudaStreamSynchronize(s.s));
+  return PIP_OK;
 }
 
 size_t pip_merge_workspace_bytes(uint64_t n, uint64_t split, uint64_t budget_words) {

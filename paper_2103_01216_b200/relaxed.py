@@ -30,10 +30,11 @@ from .runtime import (
     scratch_for,
     small_device_words,
 )
-from .strong import _merge_impl, filter_kway
+from .strong import _merge_impl, _partition_impl, filter_kway
 
 __all__ = ["RP_VARIANTS", "DEFAULT_BUDGET", "make_swap_sequence", "validate_swap_sequence",
-           "random_permutation", "decompose_driver", "filter_relaxed", "merge_relaxed"]
+           "random_permutation", "decompose_driver", "filter_relaxed", "partition_relaxed",
+           "merge_relaxed"]
 
 DEFAULT_BUDGET = EpsilonConfig(epsilon=0.5)
 RP_VARIANTS = ("naive", "flat", "oneres", "final")
@@ -177,6 +178,36 @@ def filter_relaxed(a, pred, budget: EpsilonConfig = DEFAULT_BUDGET,
         return 0
     b = budget.prefix_words(n)
     m = filter_kway(a, pred)
+    if stats_sink is not None:
+        st = RoundStats()
+        rem = n
+        while rem > 0:
+            take = min(b, rem)
+            st.rounds += 1
+            st.committed_per_round.append(take)
+            rem -= take
+        stats_sink.append(st)
+    return m
+
+
+def partition_relaxed(a, pred, budget: EpsilonConfig = DEFAULT_BUDGET,
+                      stats_sink: list | None = None) -> int:
+    """Unstable partition with the reference's prefix-round contract
+    (relaxed.py:312-344): a[0:m) holds the words with ``pred`` true, a[m:n)
+    the others (multiset preserved); returns m.
+
+    The GPU runs the swap partition of ``strong.partition_unstable`` once over
+    the whole array; its O(n/4096) descriptor words are charged to the active
+    meter (well under b(n)), and ``stats_sink`` receives the reference's
+    round structure (ceil(n / b) rounds of min(b, remaining) words).
+    """
+    w = as_words(a, _wrap=True)
+    as_pred(pred)
+    n = w.n
+    if n == 0:
+        return 0
+    b = budget.prefix_words(n)
+    m = _partition_impl(a, pred, None, meter_workspace=True)
     if stats_sink is not None:
         st = RoundStats()
         rem = n

@@ -31,7 +31,7 @@ from .pred import as_pred
 from .runtime import M64, Words, as_words, scratch_for, small_device_words
 
 __all__ = ["ScanResult", "scan", "scan_blocked", "scan_inclusive", "reduce", "rotate",
-           "filter_kway", "merge_strong"]
+           "filter_kway", "partition_unstable", "merge_strong"]
 
 SCAN_BASE = 256
 
@@ -194,6 +194,65 @@ def filter_kway(a, pred, n: int | None = None) -> int:
     _lib.check(lib.pip_filter_u64_host(w.ptr, n, C.byref(desc), C.byref(out), _device_index()),
                "filter")
     return int(out.value)
+
+
+def _partition_impl(a, pred, n: int | None, meter_workspace: bool) -> int:
+    w: Words = as_words(a, _wrap=True)
+    p = as_pred(pred)
+    n = w.n if n is None else int(n)
+    if n < 0 or n > w.n:
+        raise ValueError("n out of range")
+    if n == 0:
+        return 0
+    lib = _lib.load()
+    desc = p.descriptor()
+    wb = lib.pip_partition_workspace_bytes(n)
+    if not w.is_device:
+        out = C.c_uint64(0)
+        if meter_workspace:
+            from .runtime import charge, uncharge
+
+            charge((wb + 7) // 8)
+        try:
+            _lib.check(lib.pip_partition_u64_host(w.ptr, n, C.byref(desc), C.byref(out),
+                                                  _device_index()), "partition")
+        finally:
+            if meter_workspace:
+                uncharge((wb + 7) // 8)
+        return int(out.value)
+    import torch
+
+    from .runtime import alloc, release
+
+    with torch.cuda.device(w.device):
+        st = w.stream()
+        if meter_workspace:
+            buf = alloc(wb, w.device)
+            ptr, keep = buf.ptr, buf
+        else:
+            keep = torch.empty(max(wb, 16), dtype=torch.uint8, device=f"cuda:{w.device}")
+            ptr, buf = keep.data_ptr(), None
+        try:
+            m = small_device_words(1, w.device)
+            _lib.check(lib.pip_partition_u64(w.ptr, n, C.byref(desc), m.data_ptr(), ptr, wb, st),
+                       "partition")
+            return int(m.item())
+        finally:
+            if buf is not None:
+                release(buf)
+            del keep
+
+
+def partition_unstable(a, pred, n: int | None = None) -> int:
+    """Unstable in-place partition (strong.py:394-419): the words with
+    ``pred`` true end up in a[0:m), the others in a[m:n); returns m.
+
+    ``pred`` is a :class:`~paper_2103_01216_b200.pred.Pred`.  The GPU swaps
+    the false words left of m with the true words right of m by rank (one
+    count pass, one swap pass); its O(n/4096) descriptors are device scratch,
+    like the reference's unmetered recursion space.
+    """
+    return _partition_impl(a, pred, n, meter_workspace=False)
 
 
 def _merge_impl(a, split: int, debug: bool, budget_words: int, meter_workspace: bool) -> None:

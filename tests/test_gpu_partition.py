@@ -1,0 +1,118 @@
+"""GPU parity: unstable in-place partition (strong.partition_unstable,
+relaxed.partition_relaxed) against the reference's contract and known
+answers (test_strong.py:189-207): m == #true, a[0:m) all true, a[m:n) all
+false, the multiset preserved.  The reference's order inside each side is
+unspecified (its tests check exactly these properties)."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import rand_words
+
+pytestmark = pytest.mark.gpu
+
+
+def dev(a: np.ndarray):
+    import torch
+
+    return torch.from_numpy(a.view(np.int64).copy()).cuda()
+
+
+def host(t) -> np.ndarray:
+    return t.cpu().numpy().view(np.uint64)
+
+
+@pytest.fixture(scope="module")
+def pip():
+    import paper_2103_01216_b200 as pip
+
+    return pip
+
+
+def check(pred, before: np.ndarray, after: np.ndarray, m: int) -> None:
+    keep = np.asarray(pred(before), dtype=bool)
+    assert m == int(np.count_nonzero(keep))
+    assert np.all(np.asarray(pred(after[:m]), dtype=bool))
+    assert not np.any(np.asarray(pred(after[m:]), dtype=bool))
+    assert np.array_equal(np.sort(after), np.sort(before))
+
+
+def test_partition_known_answers(pip):
+    # test_strong.py:189-197
+    a = np.array([1, 2, 3, 4], dtype=np.uint64)
+    m = pip.strong.partition_unstable(a, pip.pred.le(2))
+    assert m == 2 and sorted(a[:2].tolist()) == [1, 2] and sorted(a[2:].tolist()) == [3, 4]
+    b = np.array([5, 7, 9], dtype=np.uint64)
+    assert pip.strong.partition_unstable(b, pip.pred.lt(0)) == 0
+    assert sorted(b.tolist()) == [5, 7, 9]
+    assert pip.strong.partition_unstable(np.zeros(0, dtype=np.uint64), pip.pred.even()) == 0
+
+
+SIZES = [1, 2, 17, 1000, 4095, 4096, 4097, 8191, 8193, 30_000, 65_536, 100_003, 1_000_003]
+
+
+@pytest.mark.parametrize("n", SIZES)
+@pytest.mark.parametrize("which", ["even", "mod3", "lt1pct", "lt99pct"])
+def test_partition_device_vs_contract(pip, n, which):
+    x = rand_words(n * 3 + 7, n)
+    p = {"even": pip.pred.even(), "mod3": pip.pred.mod_eq(3, 0),
+         "lt1pct": pip.pred.lt(1 << 57), "lt99pct": pip.pred.lt((1 << 64) - (1 << 57))}[which]
+    t = dev(x)
+    m = pip.strong.partition_unstable(t, p)
+    check(p, x, host(t), m)
+
+
+@pytest.mark.parametrize("n", [0, 1, 17, 1000, 30_000])
+def test_partition_host_arrays(pip, n):
+    # test_strong.py:200-207 (numpy in, numpy out)
+    a = rand_words(n + 3, n)
+    ref = a.copy()
+    m = pip.strong.partition_unstable(a, pip.pred.even())
+    check(pip.pred.even(), ref, a, m)
+
+
+@pytest.mark.parametrize("case", ["all_true", "all_false", "sorted_true_first",
+                                  "sorted_false_first", "alternating"])
+def test_partition_structured(pip, case):
+    n = 4096 * 7 + 321
+    i = np.arange(n, dtype=np.uint64)
+    x = {"all_true": i * np.uint64(2), "all_false": i * np.uint64(2) + np.uint64(1),
+         "sorted_true_first": np.where(i < n // 3, i * 2, i * 2 + 1).astype(np.uint64),
+         "sorted_false_first": np.where(i < n // 3, i * 2 + 1, i * 2).astype(np.uint64),
+         "alternating": i}[case]
+    p = pip.pred.even()
+    t = dev(x)
+    m = pip.strong.partition_unstable(t, p)
+    out = host(t)
+    check(p, x, out, m)
+    if case in ("all_true", "all_false", "sorted_true_first"):
+        assert np.array_equal(out, x)  # nothing misplaced: nothing moves
+
+
+def test_partition_prefix_n_and_view(pip):
+    x = rand_words(5, 50_000)
+    buf = dev(np.concatenate([np.zeros(1, dtype=np.uint64), x]))
+    t = buf[1:]  # odd word offset
+    m = pip.strong.partition_unstable(t, pip.pred.mod_eq(5, 2), n=40_000)
+    out = host(t)
+    check(pip.pred.mod_eq(5, 2), x[:40_000], out[:40_000], m)
+    assert np.array_equal(out[40_000:], x[40_000:]) and int(buf[0].item()) == 0
+
+
+@pytest.mark.parametrize("eps", [0.3, 0.5, 0.7])
+def test_partition_relaxed_budget_and_rounds(pip, eps):
+    # relaxed.py:312-344: same contract, rounds of b(n) words, charged <= 8 b
+    n = 65_536
+    cfg = pip.EpsilonConfig(eps, 1e-12)
+    b = cfg.prefix_words(n)
+    x = rand_words(41, n)
+    a = x.copy()
+    meter = pip.SpaceMeter()
+    sink: list = []
+    got = []
+    rep = pip.meter_scope(meter, 8 * b, lambda: got.append(pip.relaxed.partition_relaxed(
+        a, pip.pred.odd(), cfg, stats_sink=sink)))
+    assert meter.current_words == 0 and 0 < rep.peak_words <= 8 * b
+    check(pip.pred.odd(), x, a, got[0])
+    assert sink[0].rounds == -(-n // b) and sum(sink[0].committed_per_round) == n
