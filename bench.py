@@ -9,6 +9,8 @@ resident in HBM.  `--op` selects the other configs for our own measurements:
   merge   configs[3]  merge two sorted runs of 2^31 words, values < 2^30
   rp      configs[4]  random permutation, n = 2^30, H = make_swap_sequence
   rp0     configs[0]  random permutation, n = 10^6, H from PCG64(seed)
+  partition  SURVEY 8(f) row 3 (not a BASELINE config): unstable in-place
+          partition, 2^32 words with the configs[2] inputs and predicate
 Multi-GPU (torchrun, WORLD_SIZE = N > 1): scan is sharded (strong scaling,
 2^32 / N words per rank; local reduce -> NCCL all_gather of shard totals ->
 scan with a device carry-in).  `--impl reference` times the CPU reference
@@ -44,7 +46,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="pip", choices=["pip", "reference"])
-    ap.add_argument("--op", default="scan", choices=["scan", "filter", "merge", "rp", "rp0"])
+    ap.add_argument("--op", default="scan",
+                    choices=["scan", "filter", "merge", "rp", "rp0", "partition"])
     ap.add_argument("--log2n", type=int, default=None, help="override n = 2^k")
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--no-e2e", action="store_true")
@@ -371,6 +374,61 @@ def sort_run(t, torch, pip):
         width *= 2
 
 
+def run_partition(args, ws, rank, local, torch, pip, lib):
+    if ws > 1:
+        raise SystemExit("partition is benchmarked on one GPU")
+    n = 1 << (args.log2n or 32)
+    dev = local
+    st = torch.cuda.current_stream()
+    sptr = st.cuda_stream
+    a = torch.empty(n, dtype=torch.int64, device=f"cuda:{dev}")
+    rng = pip.Rng(args.seed)
+    regen = lambda: rng.words_device(0, n, shift=1, device=dev, out=a)  # noqa: E731
+    mdev = torch.zeros(1, dtype=torch.int64, device=f"cuda:{dev}")
+    p = pip.pred.mod_eq(3, 0)
+    desc = p.descriptor()
+    wb = lib.pip_partition_workspace_bytes(n)
+    wst = torch.empty(max(wb, 16), dtype=torch.uint8, device=f"cuda:{dev}")
+
+    def step():
+        rc = lib.pip_partition_u64(a.data_ptr(), n, C.byref(desc), mdev.data_ptr(), wst.data_ptr(),
+                                   wb, sptr)
+        assert rc == 0, rc
+
+    for _ in range(args.warmup):
+        regen()
+        step()
+    torch.cuda.synchronize()
+    m = int(mdev.item())
+    # size-independent checks: prefix all true, suffix all false (x % 3 == 0)
+    assert bool(((a[:m].view(torch.int64) % 3) == 0).all())
+    assert not bool(((a[m:].view(torch.int64) % 3) == 0).any())
+    # misfits of this input: false words left of m (= true words right of m)
+    regen()
+    X = int(((a[:m] % 3) != 0).sum().item())
+    clk = ClockSampler(dev)
+    ms = regen_timed(step, regen, args.steps, torch, st)
+    clocks = clk.stop()
+    per_step = ms / args.steps
+    value = n * args.steps / (ms / 1e3)
+    algo = 8 * n + 16 * X  # every word read once, every misplaced word written once
+    pk = peaks()
+    achieved = algo / (per_step / 1e3) / 1e9
+    roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": pk["hbm_gbs"], "unit": "GB/s",
+            "frac": round(achieved / pk["hbm_gbs"], 4), "traffic": None,
+            "note": f"8 B/word read + 16 B per misfit pair (X/n = {X / n:.4f}); kernels: count, "
+                    f"plan, bounds, swap; peak = {pk['source']}"}
+    e2e = None if args.no_e2e else e2e_host(lib, "partition", n, args, torch, dev, ws)
+    cpu = None if args.no_cpu else cpu_baseline("partition", args)
+    cfg = {"workload": "unstable in-place partition x % 3 == 0 (SURVEY 8(f) row 3; configs[2] "
+                       "inputs)", "n": n, "values": f"Rng({args.seed}).words >> 1, in [0,2^63)",
+           "kept": m, "misfit_pairs": X,
+           "l2": "inputs larger than L2; input regenerated between steps (untimed)",
+           "parallelism": "single-GPU", "seed": args.seed}
+    return dict(value=value, per_step=per_step, roof=roof, e2e=e2e, cpu=cpu, cfg=cfg,
+                clocks=clocks, launches=4 * args.steps, extra={})
+
+
 def run_merge(args, ws, rank, local, torch, pip, lib):
     if ws > 1:
         raise SystemExit("merge is benchmarked on one GPU in this round")
@@ -526,7 +584,7 @@ def e2e_host(lib, op, n, args, torch, dev, ws, **kw):
 
         if op == "scan":
             pip.Rng(rng_seed).words_device(0, n, shift=44, device=dev, out=d)
-        elif op == "filter":
+        elif op in ("filter", "partition"):
             pip.Rng(rng_seed).words_device(0, n, shift=1, device=dev, out=d)
         elif op == "merge":
             pip.Rng(rng_seed).words_device(0, n, shift=34, device=dev, out=d)
@@ -560,6 +618,13 @@ def e2e_host(lib, op, n, args, torch, dev, ws, **kw):
         elif op == "merge":
             rc = lib.pip_merge_u64_host(hp, n, n // 2, kw["budget"], dev)
             bi, bo = 8 * n, 8 * n
+        elif op == "partition":
+            import paper_2103_01216_b200 as pip
+
+            desc = pip.pred.mod_eq(3, 0).descriptor()
+            out = C.c_uint64(0)
+            rc = lib.pip_partition_u64_host(hp, n, C.byref(desc), C.byref(out), dev)
+            bi, bo = 8 * n, 8 * n
         else:
             import paper_2103_01216_b200 as pip
 
@@ -580,7 +645,7 @@ def e2e_host(lib, op, n, args, torch, dev, ws, **kw):
 # ---------------------------------------------------------------------------
 # CPU baseline: the C port of the reference's own algorithm (oracle/)
 
-CPU_SAMPLE_LOG2 = {"scan": 28, "filter": 28, "merge": 26, "rp": 24, "rp0": None}
+CPU_SAMPLE_LOG2 = {"scan": 28, "filter": 28, "merge": 26, "rp": 24, "rp0": None, "partition": 26}
 
 
 def _cpu_input(op, n, seed):
@@ -589,7 +654,7 @@ def _cpu_input(op, n, seed):
     rng = pip.Rng(seed)
     if op == "scan":
         return rng.words(0, n) >> np.uint64(44), None
-    if op == "filter":
+    if op in ("filter", "partition"):
         return rng.words(0, n) >> np.uint64(1), None
     if op == "merge":
         x = rng.words(0, n) >> np.uint64(34)
@@ -615,6 +680,8 @@ def cpu_run(op, x, h, threads):
         oracle.ref_filter_kway(x, pip.pred.mod_eq(3, 0), threads)
     elif op == "merge":
         oracle.ref_merge_strong(x, n // 2, threads)
+    elif op == "partition":
+        oracle.ref_partition_unstable(x, pip.pred.mod_eq(3, 0))  # sequential, as the reference
     else:
         oracle.ref_random_permutation(x, h, pip.EpsilonConfig(0.5).prefix_words(n), "final",
                                       threads)
@@ -637,7 +704,10 @@ def cpu_baseline(op, args, budget_s: float = 10.0) -> dict:
         reps += 1
     names = {"scan": "strong.scan (Alg. 3 up/down sweep)", "filter": "strong.filter_kway",
              "merge": "strong.merge_strong", "rp": "relaxed.random_permutation (final)",
-             "rp0": "relaxed.random_permutation (final)"}
+             "rp0": "relaxed.random_permutation (final)",
+             "partition": "strong.partition_unstable (sequential, as the reference)"}
+    if op == "partition":
+        threads = 1
     return {"value": n * reps / el, "unit": "elements/s", "cores": threads, "kind": "port",
             "sample": f"{names[op]} C/OpenMP port (oracle/pip_oracle.c) on n={n} "
                       f"words x {reps} reps, {el:.1f} s, same generator/seed"}
@@ -667,7 +737,8 @@ def main():
             cpu_run(op, x, h, threads)
             el += time.perf_counter() - t0
         value = n * args.steps / el
-        full = {"scan": 1 << 32, "filter": 1 << 32, "merge": 1 << 32, "rp": 1 << 30, "rp0": 10 ** 6}
+        full = {"scan": 1 << 32, "filter": 1 << 32, "merge": 1 << 32, "rp": 1 << 30, "rp0": 10 ** 6,
+                "partition": 1 << 32}
         line = {"metric": metric, "value": value, "unit": "elements/s", "impl": "reference",
                 "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
                 "ms_per_step": el / args.steps * 1e3, "higher_is_better": True,
@@ -677,7 +748,9 @@ def main():
                                         "filter": "stable filter x%3==0, BASELINE configs[2]",
                                         "merge": "in-place merge, BASELINE configs[3]",
                                         "rp": "random permutation, BASELINE configs[4]",
-                                        "rp0": "random permutation, BASELINE configs[0]"}[op],
+                                        "rp0": "random permutation, BASELINE configs[0]",
+                                        "partition": "unstable in-place partition x%3==0 "
+                                                     "(SURVEY 8(f) row 3)"}[op],
                            "n": full[op], "sample_n": n, "seed": args.seed},
                 "cpu_baseline": {"value": value, "unit": "elements/s", "cores": threads,
                                  "kind": "port",
@@ -700,6 +773,8 @@ def main():
         r = run_filter(args, ws, rank, local, torch, pip, lib)
     elif args.op == "merge":
         r = run_merge(args, ws, rank, local, torch, pip, lib)
+    elif args.op == "partition":
+        r = run_partition(args, ws, rank, local, torch, pip, lib)
     else:
         r = run_rp(args, ws, rank, local, torch, pip, lib, small=(args.op == "rp0"))
     if rank == 0:

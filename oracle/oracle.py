@@ -37,6 +37,7 @@ _SIGS = {
     "oracle_seq_merge": (None, [vp, u64, vp, u64, vp]),
     "oracle_ref_scan": (u64, [vp, u64, i32]),
     "oracle_ref_filter_kway": (u64, [vp, u64, u32, u32, u64, u64, i32]),
+    "oracle_ref_partition_unstable": (u64, [vp, u64, u32, u32, u64, u64]),
     "oracle_ref_rotate": (None, [vp, u64, u64]),
     "oracle_ref_merge_strong": (None, [vp, u64, u64, i32]),
     "oracle_ref_random_permutation": (
@@ -117,6 +118,12 @@ def ref_scan(a: np.ndarray, threads: int = 1) -> int:
 def ref_filter_kway(a: np.ndarray, pred, threads: int = 1) -> int:
     return int(load().oracle_ref_filter_kway(_w(a).ctypes.data, len(a), pred.kind,
                                              int(pred.negate), pred.a, pred.b, threads))
+
+
+def ref_partition_unstable(a: np.ndarray, pred) -> int:
+    """strong.partition_unstable (strong.py:352-419), same output order."""
+    return int(load().oracle_ref_partition_unstable(_w(a).ctypes.data, len(a), pred.kind,
+                                                    int(pred.negate), pred.a, pred.b))
 
 
 def ref_rotate(a: np.ndarray, o: int) -> None:

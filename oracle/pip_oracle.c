@@ -252,6 +252,68 @@ static void rotate_range(u64* a, u64 s, u64 t, u64 o) {
 }
 void oracle_ref_rotate(u64* a, u64 n, u64 o) { rotate_range(a, 0, n, o); }
 
+/* strong.py:352-419 partition_unstable: blocks of SCRATCH_WORDS (256)
+ * partitioned through a scratch copy (true words first, both sides in
+ * order, :352-363), true prefixes folded leftward by range swaps (:366-373)
+ * or rotations (:376-391); outer chunks of max(ceil(n / ceil(sqrt n)), 256)
+ * words folded the same way (:394-419).  Sequential, like the reference. */
+#define PART_SCRATCH 256
+static u64 block_partition(u64* a, u64 s, u64 e, u32 kind, u32 neg, u64 pa, u64 pb) {
+  u64 tmp[PART_SCRATCH];
+  const u64 len = e - s;
+  u64 t = 0;
+  for (u64 i = 0; i < len; ++i) t += pred_eval(kind, neg, pa, pb, a[s + i]);
+  if (t == len) return t;
+  memcpy(tmp, a + s, len * 8);
+  u64 wt = s, wf = s + t;
+  for (u64 i = 0; i < len; ++i) {
+    if (pred_eval(kind, neg, pa, pb, tmp[i])) a[wt++] = tmp[i];
+    else a[wf++] = tmp[i];
+  }
+  return t;
+}
+static void swap_ranges(u64* a, u64 p, u64 q, u64 cnt) {
+  for (u64 i = 0; i < cnt; ++i) {
+    const u64 x = a[p + i];
+    a[p + i] = a[q + i];
+    a[q + i] = x;
+  }
+}
+static u64 partition_range(u64* a, u64 lo, u64 hi, u32 kind, u32 neg, u64 pa, u64 pb) {
+  u64 w = lo, s = lo;
+  while (s < hi) {
+    const u64 e = (s + PART_SCRATCH < hi) ? s + PART_SCRATCH : hi;
+    const u64 t = block_partition(a, s, e, kind, neg, pa, pb);
+    if (t) {
+      if (w + t <= s) swap_ranges(a, w, s, t);
+      else if (w < s) rotate_range(a, w, s + t, s - w);
+      w += t;
+    }
+    s = e;
+  }
+  return w - lo;
+}
+u64 oracle_ref_partition_unstable(u64* a, u64 n, u32 kind, u32 neg, u64 pa, u64 pb) {
+  if (n == 0) return 0;
+  u64 r = 0;
+  while ((r + 1) * (r + 1) <= n) ++r;
+  const u64 k = (r * r < n) ? r + 1 : r;
+  u64 chunk = (n + k - 1) / k;
+  if (chunk < PART_SCRATCH) chunk = PART_SCRATCH;
+  u64 m = 0, s = 0;
+  while (s < n) {
+    const u64 e = (s + chunk < n) ? s + chunk : n;
+    const u64 t = partition_range(a, s, e, kind, neg, pa, pb);
+    if (t) {
+      if (m + t <= s) swap_ranges(a, m, s, t);
+      else if (m < s) rotate_range(a, m, s + t, s - m);
+      m += t;
+    }
+    s = e;
+  }
+  return m;
+}
+
 /* strong.py:474-488 _split_point */
 static u64 split_point(const u64* a, u64 lo, u64 mid, u64 hi, u64 h) {
   const u64 na = mid - lo, nb = hi - mid;

@@ -69,6 +69,24 @@ def make_filter():
     np.savez_compressed(OUT / "filter.npz", **d)
 
 
+def make_partition():
+    d = {}
+    preds = {
+        "even": lambda b: (b & WORD(1)) == 0,        # test_strong.py:204
+        "mod3": lambda b: (b % WORD(3)) == 0,        # the config-2 predicate
+        "le2e62": lambda b: b <= WORD(1 << 62),      # pivot-style (quicksort_strong)
+    }
+    inputs = {str(n): rand_words(n + 3, n) for n in [0, 1, 17, 1000, 30_000]}  # test_strong.py:200
+    for name, x in inputs.items():
+        d[f"in_{name}"] = x
+        for pname, p in preds.items():
+            a = x.copy()
+            m = strong.partition_unstable(a, p)
+            d[f"out_{pname}_{name}"] = a
+            d[f"m_{pname}_{name}"] = np.array([m], dtype=np.uint64)
+    np.savez_compressed(OUT / "partition.npz", **d)
+
+
 def make_merge():
     d = {}
     pairs = [(1, 1), (5, 3), (100, 1), (1, 100), (1000, 1000), (4096, 999)]  # test_strong.py:248
@@ -144,6 +162,7 @@ def make_rng():
 if __name__ == "__main__":
     make_scan()
     make_filter()
+    make_partition()
     make_merge()
     make_rp()
     make_rng()

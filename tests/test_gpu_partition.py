@@ -8,7 +8,7 @@ from __future__ import annotations
 import numpy as np
 import pytest
 
-from conftest import rand_words
+from conftest import golden, rand_words
 
 pytestmark = pytest.mark.gpu
 
@@ -116,3 +116,21 @@ def test_partition_relaxed_budget_and_rounds(pip, eps):
     assert meter.current_words == 0 and 0 < rep.peak_words <= 8 * b
     check(pip.pred.odd(), x, a, got[0])
     assert sink[0].rounds == -(-n // b) and sum(sink[0].committed_per_round) == n
+
+
+def test_partition_golden(pip):
+    # the reference's own outputs (tests/golden/make_golden.py): same m, same
+    # multiset on each side
+    g = golden("partition")
+    preds = {"even": pip.pred.even(), "mod3": pip.pred.mod_eq(3, 0), "le2e62": pip.pred.le(1 << 62)}
+    for key in g.files:
+        if key.startswith("out_"):
+            pname, name = key[4:].split("_", 1)
+            x = g["in_" + name]
+            m_ref = int(g[f"m_{pname}_{name}"][0])
+            t = dev(x)
+            m = pip.strong.partition_unstable(t, preds[pname])
+            out = host(t)
+            assert m == m_ref
+            assert np.array_equal(np.sort(out[:m]), np.sort(g[key][:m]))
+            assert np.array_equal(np.sort(out[m:]), np.sort(g[key][m:]))

@@ -42,6 +42,18 @@ def test_oracle_filter_golden(orc):
             assert m == len(g[key]) and np.array_equal(a[:m], g[key])
 
 
+def test_oracle_partition_golden(orc):
+    # the C port reproduces the reference's partition_unstable word for word
+    g = golden("partition")
+    preds = {"even": P.even(), "mod3": P.mod_eq(3, 0), "le2e62": P.le(1 << 62)}
+    for key in g.files:
+        if key.startswith("out_"):
+            pname, name = key[4:].split("_", 1)
+            a = g["in_" + name].copy()
+            m = orc.ref_partition_unstable(a, preds[pname])
+            assert m == int(g[f"m_{pname}_{name}"][0]) and np.array_equal(a, g[key])
+
+
 def test_oracle_merge_golden(orc):
     g = golden("merge")
     for key in g.files:
