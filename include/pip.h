@@ -145,6 +145,14 @@ int pip_partition_u64(uint64_t* a, uint64_t n, const pip_pred* pred, uint64_t* m
 int pip_partition_u64_host(uint64_t* host_a, uint64_t n, const pip_pred* pred, uint64_t* m_out,
                            int device);
 
+/* ---- quicksort leaves: the base case of strong.quicksort_strong /
+ * relaxed.quicksort_relaxed (strong.py:453-454, relaxed.py:370-371):
+ * sorts a[seg_lo[g] : seg_lo[g] + seg_len[g]) ascending (unsigned) for every
+ * g < nseg; seg_len[g] <= 8192, segments disjoint; device arrays.  The
+ * recursion above it partitions with pip_partition_u64.                   */
+int pip_sort_segments_u64(uint64_t* a, const uint64_t* seg_lo_dev, const uint32_t* seg_len_dev,
+                          uint64_t nseg, void* stream);
+
 /* ---- merge: strong.merge_strong / relaxed.merge_relaxed ------------------ *
  * a[0:split) and a[split:n) are sorted ascending (unsigned); on return a is
  * sorted.  `workspace`/`workspace_bytes` is the metered auxiliary space

@@ -71,6 +71,7 @@ int rp_device(u64* a, const u64* h, u64 n, u64 prefix, int variant, int debug,
               u64* counts_host, u64 rounds_cap, u64* trace_dev, void* ws, size_t ws_bytes,
               pip_rp_stats* stats, cudaStream_t st);
 size_t partition_workspace_bytes(u64 n);
+int sort_segments_device(u64* a, const u64* seg_lo, const u32* seg_len, u64 nseg, cudaStream_t st);
 int partition_device(u64* a, u64 n, const pip_pred* pred, u64* m_dev, void* ws, size_t ws_bytes,
                      cudaStream_t st);
 size_t merge_workspace_bytes(u64 n, u64 split, u64 budget_words);
@@ -371,6 +372,12 @@ int pip_rotate_u64(uint64_t* a, uint64_t n, uint64_t o, void* scratch, size_t sc
 }
 
 size_t pip_partition_workspace_bytes(uint64_t n) { return partition_workspace_bytes(n); }
+
+int pip_sort_segments_u64(uint64_t* a, const uint64_t* seg_lo_dev, const uint32_t* seg_len_dev,
+                          uint64_t nseg, void* stream) {
+  return sort_segments_device((u64*)a, (const u64*)seg_lo_dev, seg_len_dev, nseg,
+                              (cudaStream_t)stream);
+}
 
 int pip_partition_u64(uint64_t* a, uint64_t n, const pip_pred* pred, uint64_t* m_dev,
                       void* workspace, size_t workspace_bytes, void* stream) {

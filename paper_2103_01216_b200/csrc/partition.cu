@@ -385,6 +385,54 @@ __global__ void __launch_bounds__(PT_THREADS) part_swap_kernel(u64* a, u64 n, De
   }
 }
 
+// ---------------------------------------------------------------- leaf sort
+// quicksort leaves (strong.quicksort_strong's base case a[lo:hi].sort(),
+// strong.py:453-454): one CTA per segment of <= 8192 words, bitonic sort in
+// shared memory (padded to a power of two with 2^64-1: ties are invisible)
+static constexpr u32 SEG_MAX = 8192;
+
+__global__ void __launch_bounds__(1024) segsort_kernel(u64* a, const u64* __restrict__ seg_lo,
+                                                       const u32* __restrict__ seg_len, u64 nseg) {
+  extern __shared__ __align__(16) u64 ss[];
+  const u32 tid = threadIdx.x;
+  for (u64 g = blockIdx.x; g < nseg; g += gridDim.x) {
+    const u32 L = seg_len[g];
+    u64* base = a + seg_lo[g];
+    u32 P = 2;
+    while (P < L) P <<= 1;
+    for (u32 i = tid; i < P; i += 1024) ss[i] = i < L ? base[i] : ~0ull;
+    __syncthreads();
+    for (u32 k = 2; k <= P; k <<= 1) {
+      for (u32 j = k >> 1; j > 0; j >>= 1) {
+        for (u32 i = tid; i < P / 2; i += 1024) {
+          const u32 l = 2 * i - (i & (j - 1)), r = l + j;
+          const bool up = (l & k) == 0;
+          const u64 x = ss[l], y = ss[r];
+          if ((x > y) == up) {
+            ss[l] = y;
+            ss[r] = x;
+          }
+        }
+        __syncthreads();
+      }
+    }
+    for (u32 i = tid; i < L; i += 1024) base[i] = ss[i];
+    __syncthreads();
+  }
+}
+
+int sort_segments_device(u64* a, const u64* seg_lo, const u32* seg_len, u64 nseg, cudaStream_t st) {
+  if (nseg == 0) return PIP_OK;
+  if (!a || !seg_lo || !seg_len) return PIP_ERR_INVALID_ARG;
+  const size_t smem = SEG_MAX * 8;
+  PIP_CUDA(cudaFuncSetAttribute(segsort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int sms = num_sms(current_device());
+  const u64 g = nseg < (u64)sms * 3 ? nseg : (u64)sms * 3;
+  segsort_kernel<<<(unsigned)g, 1024, smem, st>>>(a, seg_lo, seg_len, nseg);
+  PIP_CHECK_LAUNCH();
+  return PIP_OK;
+}
+
 // ---------------------------------------------------------------- host
 // groups of tiles for the plan: one per 64 tiles, at most PL_GROUPS
 static u64 part_groups(u64 ntiles) {

@@ -30,11 +30,11 @@ from .runtime import (
     scratch_for,
     small_device_words,
 )
-from .strong import _merge_impl, _partition_impl, filter_kway
+from .strong import _merge_impl, _partition_impl, _quicksort_impl, filter_kway
 
 __all__ = ["RP_VARIANTS", "DEFAULT_BUDGET", "make_swap_sequence", "validate_swap_sequence",
            "random_permutation", "decompose_driver", "filter_relaxed", "partition_relaxed",
-           "merge_relaxed"]
+           "quicksort_relaxed", "merge_relaxed"]
 
 DEFAULT_BUDGET = EpsilonConfig(epsilon=0.5)
 RP_VARIANTS = ("naive", "flat", "oneres", "final")
@@ -218,6 +218,14 @@ def partition_relaxed(a, pred, budget: EpsilonConfig = DEFAULT_BUDGET,
             rem -= take
         stats_sink.append(st)
     return m
+
+
+def quicksort_relaxed(a, rng, budget: EpsilonConfig = DEFAULT_BUDGET) -> None:
+    """Quicksort over the relaxed partition (relaxed.py:347-371): segments run
+    one at a time, so the charged footprint is one partition's descriptors
+    (O(n/2048) words); pivots use the reference's rule with salt 0."""
+    as_words(a, _wrap=True)
+    _quicksort_impl(a, rng, lambda depth: 0, meter_workspace=True)
 
 
 def merge_relaxed(a, split: int, budget: EpsilonConfig = DEFAULT_BUDGET,

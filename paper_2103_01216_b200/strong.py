@@ -31,7 +31,7 @@ from .pred import as_pred
 from .runtime import M64, Words, as_words, scratch_for, small_device_words
 
 __all__ = ["ScanResult", "scan", "scan_blocked", "scan_inclusive", "reduce", "rotate",
-           "filter_kway", "partition_unstable", "merge_strong"]
+           "filter_kway", "partition_unstable", "quicksort_strong", "merge_strong"]
 
 SCAN_BASE = 256
 
@@ -253,6 +253,92 @@ def partition_unstable(a, pred, n: int | None = None) -> int:
     like the reference's unmetered recursion space.
     """
     return _partition_impl(a, pred, n, meter_workspace=False)
+
+
+QS_LEAF = 8192  # leaves: one CTA sorts each in shared memory (pip_sort_segments_u64)
+
+
+def _quicksort_impl(a, rng, salt_of, meter_workspace: bool) -> None:
+    """Quicksort over the GPU partition (strong.py:422-454, relaxed.py:347-371):
+    segments longer than QS_LEAF words are split around a pivot picked with
+    the reference's rule (a[lo + rng.word(((lo << 21) ^ hi) + salt) % (hi -
+    lo)]) by two partitions (< pivot, == pivot); the leaves are sorted by one
+    launch.  The output is the sorted array whatever the pivots."""
+    import torch
+
+    w: Words = as_words(a, _wrap=True)
+    n = w.n
+    if n < 2:
+        return None
+    if not w.is_device:
+        return _via_device(w.obj, lambda t: _quicksort_impl(t, rng, salt_of, meter_workspace))
+    from .pred import eq, lt
+    from .runtime import alloc, release
+
+    lib = _lib.load()
+    with torch.cuda.device(w.device):
+        st = w.stream()
+        wb = lib.pip_partition_workspace_bytes(n)
+        if meter_workspace:
+            buf = alloc(wb, w.device)
+            ws_ptr, keep = buf.ptr, buf
+        else:
+            keep = torch.empty(max(wb, 16), dtype=torch.uint8, device=f"cuda:{w.device}")
+            ws_ptr, buf = keep.data_ptr(), None
+        try:
+            m = small_device_words(1, w.device)
+            words = w.obj.view(torch.int64) if w.obj.dtype != torch.int64 else w.obj
+
+            def part(lo: int, hi: int, p) -> int:
+                d = p.descriptor()
+                _lib.check(lib.pip_partition_u64(w.ptr + 8 * lo, hi - lo, C.byref(d), m.data_ptr(),
+                                                 ws_ptr, wb, st), "partition")
+                return int(m.item())
+
+            leaves_lo: list[int] = []
+            leaves_len: list[int] = []
+            stack = [(0, n, 0)]
+            while stack:
+                lo, hi, depth = stack.pop()
+                while hi - lo > QS_LEAF:
+                    salt = salt_of(depth)
+                    pv = int(words[lo + rng.word(((lo << 21) ^ hi) + salt) % (hi - lo)].item()) & M64
+                    less = part(lo, hi, lt(pv))
+                    equal = part(lo + less, hi, eq(pv))
+                    left_hi, right_lo = lo + less, lo + less + equal
+                    depth += 1
+                    if left_hi - lo < hi - right_lo:
+                        stack.append((right_lo, hi, depth))
+                        hi = left_hi
+                    else:
+                        stack.append((lo, left_hi, depth))
+                        lo = right_lo
+                if hi - lo > 1:
+                    leaves_lo.append(lo)
+                    leaves_len.append(hi - lo)
+            if leaves_lo:
+                dev = f"cuda:{w.device}"
+                slo = torch.tensor(leaves_lo, dtype=torch.int64, device=dev)
+                sln = torch.tensor(leaves_len, dtype=torch.int32, device=dev)
+                _lib.check(lib.pip_sort_segments_u64(w.ptr, slo.data_ptr(), sln.data_ptr(),
+                                                     len(leaves_lo), st), "sort")
+                torch.cuda.current_stream(w.device).synchronize()
+        finally:
+            if buf is not None:
+                release(buf)
+            del keep
+    return None
+
+
+def quicksort_strong(a, rng) -> None:
+    """In-place quicksort over the unstable partition (strong.py:422-454).
+
+    ``rng`` is a :class:`~paper_2103_01216_b200.runtime.Rng`; pivots follow
+    the reference's rule (its depth-cap restarts only change pivots, never
+    the sorted output).  Leaves of <= 8192 words are sorted on the GPU in
+    shared memory (the reference's base case is ``a[lo:hi].sort()``).
+    """
+    _quicksort_impl(a, rng, lambda depth: 0, meter_workspace=False)
 
 
 def _merge_impl(a, split: int, debug: bool, budget_words: int, meter_workspace: bool) -> None:

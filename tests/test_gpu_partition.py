@@ -134,3 +134,50 @@ def test_partition_golden(pip):
             assert m == m_ref
             assert np.array_equal(np.sort(out[:m]), np.sort(g[key][:m]))
             assert np.array_equal(np.sort(out[m:]), np.sort(g[key][m:]))
+
+
+# ----------------------------------------------------------------- quicksort
+
+@pytest.mark.parametrize("n", [0, 1, 3, 100, 10_000, 50_000])
+def test_quicksort_strong_matches_sorted(pip, n):
+    # test_strong.py:210-215 (host arrays)
+    a = rand_words(n + 1, n)
+    ref = np.sort(a)
+    pip.strong.quicksort_strong(a, pip.Rng(31))
+    assert np.array_equal(a, ref)
+
+
+def test_quicksort_duplicates(pip):
+    # test_strong.py:218-221
+    a = np.array([3, 1, 2] * 500, dtype=np.uint64)
+    pip.strong.quicksort_strong(a, pip.Rng(5))
+    assert np.array_equal(a, np.sort(np.array([3, 1, 2] * 500, dtype=np.uint64)))
+
+
+@pytest.mark.parametrize("case", ["random", "few_values", "all_equal", "sorted", "reversed",
+                                  "full_range_max"])
+def test_quicksort_device_large(pip, case):
+    n = 1_000_003
+    rng = np.random.default_rng(7)
+    x = {"random": rng.integers(0, 1 << 64, size=n, dtype=np.uint64),
+         "few_values": rng.integers(0, 5, size=n, dtype=np.uint64),
+         "all_equal": np.full(n, 42, dtype=np.uint64),
+         "sorted": np.arange(n, dtype=np.uint64),
+         "reversed": np.arange(n, dtype=np.uint64)[::-1].copy(),
+         "full_range_max": np.where(rng.random(n) < 0.1, np.uint64((1 << 64) - 1),
+                                    rng.integers(0, 1 << 64, size=n, dtype=np.uint64))}[case]
+    t = dev(x)
+    pip.strong.quicksort_strong(t, pip.Rng(9))
+    assert np.array_equal(host(t), np.sort(x))
+
+
+def test_quicksort_relaxed_metered(pip):
+    n = 300_000
+    x = rand_words(77, n)
+    a = x.copy()
+    meter = pip.SpaceMeter()
+    cfg = pip.EpsilonConfig(0.5)
+    b = cfg.prefix_words(n)
+    rep = pip.meter_scope(meter, 8 * b, lambda: pip.relaxed.quicksort_relaxed(a, pip.Rng(3), cfg))
+    assert meter.current_words == 0 and rep.peak_words <= 8 * b
+    assert np.array_equal(a, np.sort(x))
