@@ -42,6 +42,8 @@ EVEN = pred.even()
 ALGO_KIND = {
     "scan": "ints", "scan-blocked": "ints", "reduce": "ints", "rotate": "ints",
     "filter": "ints", "filter-relaxed": "ints",
+    "partition": "ints", "partition-relaxed": "ints",
+    "quicksort": "ints", "quicksort-relaxed": "ints",
     "merge": "ints", "merge-relaxed": "ints",
     "rp": "perm",
 }
@@ -165,6 +167,29 @@ def _make_run(cfg: BenchConfig, dev_in, host_in: np.ndarray) -> _Run:
 
         return _Run(body, verify,
                     lambda: state["s"][0].rounds if state.get("s") else 0)
+
+    if algo in ("partition", "partition-relaxed"):  # cli.py:226-247
+        def body():
+            if algo == "partition":
+                state["m"] = strong.partition_unstable(a, EVEN)
+            else:
+                state["m"] = relaxed.partition_relaxed(a, EVEN, budget,
+                                                       stats_sink=state.setdefault("s", []))
+
+        def verify():
+            m, out = state["m"], host(a)
+            ev = (out & np.uint64(1)) == 0
+            return (m == int(np.count_nonzero((host_in & np.uint64(1)) == 0))
+                    and bool(np.all(ev[:m])) and not bool(np.any(ev[m:]))
+                    and np.array_equal(np.sort(out), np.sort(host_in)))
+
+        return _Run(body, verify, lambda: state["s"][0].rounds if state.get("s") else 0)
+
+    if algo in ("quicksort", "quicksort-relaxed"):  # cli.py:249-257
+        rng = Rng(cfg.seed)
+        fn = (lambda: strong.quicksort_strong(a, rng)) if algo == "quicksort" else \
+             (lambda: relaxed.quicksort_relaxed(a, rng, budget))
+        return _Run(fn, lambda: np.array_equal(host(a), np.sort(host_in)))
 
     if algo in ("merge", "merge-relaxed"):
         split = len(host_in) // 2

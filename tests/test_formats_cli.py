@@ -94,7 +94,7 @@ def test_cli_gen_matches_reference_generators(ref):
 def test_cli_usage_errors(tmp_path, capsys):
     p = tmp_path / "x.u64"
     formats.write_ints(p, np.arange(10, dtype=np.uint64))
-    assert cli.main(["run", "--algo", "quicksort", "--input", str(p)]) == 1
+    assert cli.main(["run", "--algo", "mergesort", "--input", str(p)]) == 1
     assert cli.main(["run", "--algo", "scan", "--input", str(tmp_path / "missing.u64")]) == 2
     lst = tmp_path / "l.u64"
     lst.write_bytes(b"PIPLST\x00\x01" + struct.pack("<Q", 0))
@@ -113,8 +113,9 @@ def test_cli_reference_swap_order(orc):
     assert np.array_equal(cli._ref_knuth(h), want)
 
 
-ALGOS = ["scan", "scan-blocked", "reduce", "rotate", "filter", "filter-relaxed", "merge",
-         "merge-relaxed", "rp-naive", "rp-flat", "rp-oneres", "rp-final"]
+ALGOS = ["scan", "scan-blocked", "reduce", "rotate", "filter", "filter-relaxed", "partition",
+         "partition-relaxed", "quicksort", "quicksort-relaxed", "merge", "merge-relaxed",
+         "rp-naive", "rp-flat", "rp-oneres", "rp-final"]
 
 
 @pytest.mark.gpu
