@@ -153,6 +153,24 @@ int pip_partition_u64_host(uint64_t* host_a, uint64_t n, const pip_pred* pred, u
 int pip_sort_segments_u64(uint64_t* a, const uint64_t* seg_lo_dev, const uint32_t* seg_len_dev,
                           uint64_t nseg, void* stream);
 
+/* ---- list contraction / ranking: contraction.list_contract / list_rank ---- *
+ * (contraction.py:264-365 on detres.run_rounds, detres.py:256-307).  next /
+ * prev / p are device u64[n] (NIL = 2^64-1 ends a chain; p distinct
+ * priorities); rounds of `prefix` = b(n) active ids with the reference's
+ * structure, so committed_per_round_host[r] (host, r < rounds_cap) and
+ * *rounds_out equal its RoundStats.  rank == 0: every element splices out
+ * and keeps (prev, next) = its splice-time neighbours; trace_host (host
+ * u64[n], NULL ok) receives the committed ids round by round, splice_host
+ * (host u64[3n], NULL ok) the (v, u, x) triples (on_splice).  rank != 0:
+ * list_rank — prev receives the 0-based ranks, next bookkeeping marks.
+ * Synchronizes once per round.  PIP_ERR_LIVELOCK after 64 zero rounds.    */
+size_t pip_list_contract_workspace_bytes(uint64_t n, uint64_t prefix, int rank);
+int pip_list_contract_u64(uint64_t* next, uint64_t* prev, const uint64_t* p, uint64_t n,
+                          uint64_t prefix, int rank, uint64_t* committed_per_round_host,
+                          uint64_t rounds_cap, uint64_t* rounds_out, uint64_t* trace_host,
+                          uint64_t* splice_host, void* workspace, size_t workspace_bytes,
+                          void* stream);
+
 /* ---- merge: strong.merge_strong / relaxed.merge_relaxed ------------------ *
  * a[0:split) and a[split:n) are sorted ascending (unsigned); on return a is
  * sorted.  `workspace`/`workspace_bytes` is the metered auxiliary space

@@ -71,6 +71,10 @@ int rp_device(u64* a, const u64* h, u64 n, u64 prefix, int variant, int debug,
               u64* counts_host, u64 rounds_cap, u64* trace_dev, void* ws, size_t ws_bytes,
               pip_rp_stats* stats, cudaStream_t st);
 size_t partition_workspace_bytes(u64 n);
+size_t list_contract_workspace_bytes(u64 n, u64 prefix, int rank);
+int list_contract_device(u64* nxt, u64* prv, const u64* p, u64 n, u64 prefix, int rank,
+                         u64* committed_per_round_host, u64 rounds_cap, u64* rounds_out,
+                         u64* trace_host, u64* splice_host, void* ws, size_t ws_bytes, cudaStream_t st);
 int sort_segments_device(u64* a, const u64* seg_lo, const u32* seg_len, u64 nseg, cudaStream_t st);
 int partition_device(u64* a, u64 n, const pip_pred* pred, u64* m_dev, void* ws, size_t ws_bytes,
                      cudaStream_t st);
@@ -372,6 +376,21 @@ int pip_rotate_u64(uint64_t* a, uint64_t n, uint64_t o, void* scratch, size_t sc
 }
 
 size_t pip_partition_workspace_bytes(uint64_t n) { return partition_workspace_bytes(n); }
+
+size_t pip_list_contract_workspace_bytes(uint64_t n, uint64_t prefix, int rank) {
+  return list_contract_workspace_bytes(n, prefix, rank);
+}
+
+int pip_list_contract_u64(uint64_t* next, uint64_t* prev, const uint64_t* p, uint64_t n,
+                          uint64_t prefix, int rank, uint64_t* committed_per_round_host,
+                          uint64_t rounds_cap, uint64_t* rounds_out, uint64_t* trace_host,
+                          uint64_t* splice_host, void* workspace, size_t workspace_bytes,
+                          void* stream) {
+  return list_contract_device((u64*)next, (u64*)prev, (const u64*)p, n, prefix, rank,
+                              (u64*)committed_per_round_host, rounds_cap, (u64*)rounds_out,
+                              (u64*)trace_host, (u64*)splice_host, workspace, workspace_bytes,
+                              (cudaStream_t)stream);
+}
 
 int pip_sort_segments_u64(uint64_t* a, const uint64_t* seg_lo_dev, const uint32_t* seg_len_dev,
                           uint64_t nseg, void* stream) {

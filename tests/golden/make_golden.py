@@ -87,6 +87,50 @@ def make_partition():
     np.savez_compressed(OUT / "partition.npz", **d)
 
 
+def make_contraction():
+    from pipal.contraction import LinkedList, list_contract, list_rank, make_priorities
+    from pipal.runtime import NIL, POWER_ONLY_FRACTION
+
+    def random_chains(rng, n, nchains):  # test_contraction.py:45-59
+        order = rng.permutation(n)
+        cuts = np.sort(rng.choice(np.arange(1, n), size=nchains - 1, replace=False)) \
+            if nchains > 1 else np.array([], dtype=np.int64)
+        nxt = np.full(n, NIL, dtype=np.uint64)
+        prv = np.full(n, NIL, dtype=np.uint64)
+        prev_cut = 0
+        for cut in list(cuts) + [n]:
+            seg = order[prev_cut:cut]
+            for a, b in zip(seg, seg[1:]):
+                nxt[a] = b
+                prv[b] = a
+            prev_cut = cut
+        return nxt, prv
+
+    d = {}
+    cases = [("c1", 1, 1, 0.5, 1.0), ("c9", 9, 1, 0.5, 1.0), ("c4000", 4000, 7, 0.5, 0.02),
+             ("c2000p3", 2000, 40, 0.3, POWER_ONLY_FRACTION),
+             ("c50000", 50_000, 3, 0.5, POWER_ONLY_FRACTION)]
+    for name, n, nch, eps, frac in cases:
+        rng = np.random.default_rng(n + nch)
+        nxt, prv = random_chains(rng, n, nch)
+        p = make_priorities(n, Rng(n))
+        budget = EpsilonConfig(eps, prefix_fraction=frac)
+        d[f"next_{name}"], d[f"prev_{name}"], d[f"p_{name}"] = nxt.copy(), prv.copy(), p.copy()
+        d[f"budget_{name}"] = np.array([eps, frac])
+        lst = LinkedList(nxt.copy(), prv.copy())
+        trace = []
+        st = list_contract(lst, p, budget=budget, trace=trace)
+        d[f"cnext_{name}"], d[f"cprev_{name}"] = lst.next, lst.prev
+        d[f"ccounts_{name}"] = np.array(st.committed_per_round, dtype=np.uint64)
+        d[f"ctrace_{name}"] = np.concatenate(trace) if trace else np.zeros(0, dtype=np.uint64)
+        lst = LinkedList(nxt.copy(), prv.copy())
+        sink = []
+        ranks = list_rank(lst, p, budget=budget, stats_sink=sink)
+        d[f"ranks_{name}"] = ranks.copy()
+        d[f"rcounts_{name}"] = np.array(sink[0].committed_per_round, dtype=np.uint64)
+    np.savez_compressed(OUT / "contraction.npz", **d)
+
+
 def make_merge():
     d = {}
     pairs = [(1, 1), (5, 3), (100, 1), (1, 100), (1000, 1000), (4096, 999)]  # test_strong.py:248
@@ -163,6 +207,7 @@ if __name__ == "__main__":
     make_scan()
     make_filter()
     make_partition()
+    make_contraction()
     make_merge()
     make_rp()
     make_rng()

@@ -1,0 +1,155 @@
+"""GPU parity: list contraction and list ranking (contraction.py:264-365)
+against the reference's own outputs (tests/golden/contraction.npz, made by
+tests/golden/make_golden.py): identical final slots, ranks, RoundStats and
+per-round committed sets; plus the reference's known answers
+(test_contraction.py:110-210)."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import golden
+
+pytestmark = pytest.mark.gpu
+
+NIL = (1 << 64) - 1
+
+
+@pytest.fixture(scope="module")
+def pip():
+    import paper_2103_01216_b200 as pip
+
+    return pip
+
+
+def words(vals):
+    return np.array([NIL if v is None else v for v in vals], dtype=np.uint64)
+
+
+def chain_list(pip, order):
+    n = len(order)
+    nxt = np.full(n, NIL, dtype=np.uint64)
+    prv = np.full(n, NIL, dtype=np.uint64)
+    for a, b in zip(order, order[1:]):
+        nxt[a] = b
+        prv[b] = a
+    return pip.contraction.LinkedList(nxt, prv)
+
+
+def seq_list_rank(nxt, prv):  # baselines.py:57-72
+    n = len(nxt)
+    ranks = np.zeros(n, dtype=np.uint64)
+    for head in np.flatnonzero(prv == np.uint64(NIL)):
+        r, v = 0, int(head)
+        while v != NIL:
+            ranks[v] = r
+            r += 1
+            v = int(nxt[v])
+    return ranks
+
+
+CASES = ["c1", "c9", "c4000", "c2000p3", "c50000"]
+
+
+@pytest.mark.parametrize("name", CASES)
+@pytest.mark.parametrize("where", ["host", "device"])
+def test_list_contract_golden(pip, name, where):
+    import torch
+
+    g = golden("contraction")
+    eps, frac = g[f"budget_{name}"]
+    budget = pip.EpsilonConfig(float(eps), float(frac))
+    nxt, prv, p = g[f"next_{name}"].copy(), g[f"prev_{name}"].copy(), g[f"p_{name}"]
+    if where == "device":
+        lst = pip.contraction.LinkedList(torch.from_numpy(nxt.view(np.int64)).cuda(),
+                                         torch.from_numpy(prv.view(np.int64)).cuda())
+    else:
+        lst = pip.contraction.LinkedList(nxt, prv)
+    trace: list = []
+    st = pip.contraction.list_contract(lst, p, budget=budget, trace=trace)
+    out_n = lst.next if where == "host" else lst.next.cpu().numpy().view(np.uint64)
+    out_p = lst.prev if where == "host" else lst.prev.cpu().numpy().view(np.uint64)
+    assert np.array_equal(out_n, g[f"cnext_{name}"]) and np.array_equal(out_p, g[f"cprev_{name}"])
+    assert st.committed_per_round == g[f"ccounts_{name}"].tolist()
+    assert st.rounds == len(g[f"ccounts_{name}"])
+    assert np.array_equal(np.concatenate(trace), g[f"ctrace_{name}"])
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_list_rank_golden(pip, name):
+    g = golden("contraction")
+    eps, frac = g[f"budget_{name}"]
+    budget = pip.EpsilonConfig(float(eps), float(frac))
+    lst = pip.contraction.LinkedList(g[f"next_{name}"].copy(), g[f"prev_{name}"].copy())
+    sink: list = []
+    ranks = pip.contraction.list_rank(lst, g[f"p_{name}"], budget=budget, stats_sink=sink)
+    assert np.array_equal(ranks, g[f"ranks_{name}"])
+    assert np.array_equal(ranks, seq_list_rank(g[f"next_{name}"], g[f"prev_{name}"]))
+    assert sink[0].committed_per_round == g[f"rcounts_{name}"].tolist()
+
+
+def test_make_priorities_matches_reference(pip):
+    g = golden("contraction")
+    for name in CASES:
+        n = len(g[f"p_{name}"])
+        assert np.array_equal(pip.contraction.make_priorities(n, pip.Rng(n)), g[f"p_{name}"])
+
+
+def test_known_answers(pip):
+    FULL = pip.EpsilonConfig(0.5, 1.0)
+    C = pip.contraction
+    # test_contraction.py:110-113
+    st = C.list_contract(C.LinkedList(words([None]), words([None])), words([0]), budget=FULL)
+    assert st.rounds == 1 and st.committed_per_round == [1]
+    # :116-128 worked instance: first round contracts priorities {1,2,3,4}; 4 rounds
+    lst = chain_list(pip, list(range(9)))
+    p = words([v - 1 for v in [5, 1, 6, 2, 9, 3, 7, 4, 8]])
+    trace: list = []
+    st = C.list_contract(lst, p, budget=FULL, trace=trace)
+    assert sorted((p[trace[0]] + np.uint64(1)).tolist()) == [1, 2, 3, 4]
+    assert st.rounds == 4 and st.total_committed == 9
+    # :131-147 splice-time context
+    lst = chain_list(pip, [3, 1, 4, 0, 2])
+    observed = {}
+
+    def on_splice(v, u, x):
+        for vi, ui, xi in zip(v.tolist(), u.tolist(), x.tolist()):
+            observed[vi] = (ui, xi)
+
+    C.list_contract(lst, words([4, 0, 3, 2, 1]), on_splice=on_splice, budget=FULL)
+    assert observed[1] == (3, 4) and set(observed) == {0, 1, 2, 3, 4}
+    for v, (u, x) in observed.items():
+        assert lst.prev[v] == u and lst.next[v] == x
+    # :161-169 ranks
+    assert C.list_rank(C.LinkedList(words([None]), words([None])), words([0]), budget=FULL).tolist() == [0]
+    assert C.list_rank(chain_list(pip, [0, 1, 2]), words([2, 0, 1]), budget=FULL).tolist() == [0, 1, 2]
+
+
+def test_validate_rejects(pip):
+    C = pip.contraction
+    with pytest.raises(ValueError):
+        C.validate_linked_list(C.LinkedList(words([1, None]), words([None, None])))
+    with pytest.raises(ValueError, match="cycle"):
+        C.validate_linked_list(C.LinkedList(words([1, 0]), words([1, 0])))
+
+
+def test_rank_budget_metered_large(pip):
+    # test_contraction.py:193-210 at a larger size: charged <= 8 b, ranks exact
+    rng = np.random.default_rng(8)
+    n = 400_000
+    order = rng.permutation(n)
+    nxt = np.full(n, NIL, dtype=np.uint64)
+    prv = np.full(n, NIL, dtype=np.uint64)
+    nxt[order[:-1]] = order[1:]
+    prv[order[1:]] = order[:-1]
+    ref = np.empty(n, dtype=np.uint64)
+    ref[order] = np.arange(n, dtype=np.uint64)
+    p = pip.contraction.make_priorities(n, pip.Rng(10))
+    cfg = pip.EpsilonConfig(0.5, 1e-12)
+    b = cfg.prefix_words(n)
+    meter = pip.SpaceMeter()
+    out = {}
+    rep = pip.meter_scope(meter, 8 * b, lambda: out.__setitem__(
+        "r", pip.contraction.list_rank(pip.contraction.LinkedList(nxt, prv), p, cfg)))
+    assert rep.peak_words <= 8 * b and meter.current_words == 0
+    assert np.array_equal(out["r"], ref)
