@@ -171,6 +171,23 @@ int pip_list_contract_u64(uint64_t* next, uint64_t* prev, const uint64_t* p, uin
                           uint64_t* splice_host, void* workspace, size_t workspace_bytes,
                           void* stream);
 
+/* ---- tree contraction: contraction.tree_contract (contraction.py:368-559) *
+ * The frontier queue / cursor bookkeeping (O(prefix) per round) is the
+ * caller's; one call runs one device step of a round on the device-resident
+ * forest (parent/left/right/p/values, NIL = 2^64-1):
+ *   step 0: flags[v - lo] = contractible-when-swept, v in [lo, hi)
+ *   step 1: flags[k] = eligibility of ids[k], k < fill (sorted_ids: the same
+ *           ids ascending, for the active-neighbour test)
+ *   step 2: gathered[6k..6k+5] = (parent, child, is_left, parent's child
+ *           count, grandparent, value) of the committing ids[k] before any
+ *           surgery
+ *   step 3: fold values (combine 0 add, 1 max, 2 min, 3 xor; mod 2^64) and
+ *           re-link, from step 2's gathered state.  Stream-ordered.        */
+int pip_tree_round_u64(int step, uint64_t* parent, uint64_t* left, uint64_t* right,
+                       const uint64_t* p, uint64_t* values, uint64_t lo, uint64_t hi,
+                       const uint32_t* ids, uint64_t fill, const uint32_t* sorted_ids,
+                       uint8_t* flags, uint64_t* gathered, int combine, void* stream);
+
 /* ---- merge: strong.merge_strong / relaxed.merge_relaxed ------------------ *
  * a[0:split) and a[split:n) are sorted ascending (unsigned); on return a is
  * sorted.  `workspace`/`workspace_bytes` is the metered auxiliary space

@@ -72,6 +72,9 @@ int rp_device(u64* a, const u64* h, u64 n, u64 prefix, int variant, int debug,
               pip_rp_stats* stats, cudaStream_t st);
 size_t partition_workspace_bytes(u64 n);
 size_t list_contract_workspace_bytes(u64 n, u64 prefix, int rank);
+int tree_round_device(int step, u64* pa, u64* lf, u64* rt, const u64* p, u64* values, u64 lo, u64 hi,
+                      const u32* ids, u64 fill, const u32* sorted, unsigned char* flags, u64* gathered,
+                      int op, cudaStream_t st);
 int list_contract_device(u64* nxt, u64* prv, const u64* p, u64 n, u64 prefix, int rank,
                          u64* committed_per_round_host, u64 rounds_cap, u64* rounds_out,
                          u64* trace_host, u64* splice_host, void* ws, size_t ws_bytes, cudaStream_t st);
@@ -376,6 +379,15 @@ int pip_rotate_u64(uint64_t* a, uint64_t n, uint64_t o, void* scratch, size_t sc
 }
 
 size_t pip_partition_workspace_bytes(uint64_t n) { return partition_workspace_bytes(n); }
+
+int pip_tree_round_u64(int step, uint64_t* parent, uint64_t* left, uint64_t* right,
+                       const uint64_t* p, uint64_t* values, uint64_t lo, uint64_t hi,
+                       const uint32_t* ids, uint64_t fill, const uint32_t* sorted_ids,
+                       uint8_t* flags, uint64_t* gathered, int combine, void* stream) {
+  return tree_round_device(step, (u64*)parent, (u64*)left, (u64*)right, (const u64*)p, (u64*)values, lo,
+                           hi, ids, fill, sorted_ids, flags, (u64*)gathered, combine,
+                           (cudaStream_t)stream);
+}
 
 size_t pip_list_contract_workspace_bytes(uint64_t n, uint64_t prefix, int rank) {
   return list_contract_workspace_bytes(n, prefix, rank);

@@ -202,6 +202,133 @@ __global__ void __launch_bounds__(LC_T) lc_wave_kernel(u64* nxt, u64* dist, u64 
 }
 
 // ---------------------------------------------------------------------------
+// tree contraction (contraction.py:368-525): the frontier queue and cursor
+// (control plane, O(prefix) per round) stay on the host; these kernels do
+// the per-node work of a round on the device-resident tree.
+
+// contractible-when-swept flags for ids [lo, hi) (contraction.py:417-421)
+__global__ void __launch_bounds__(LC_T) tc_ready_kernel(const u64* __restrict__ pa, const u64* __restrict__ lf,
+                                                        const u64* __restrict__ rt, u64 lo, u64 hi,
+                                                        unsigned char* flags) {
+  for (u64 v = lo + (u64)blockIdx.x * LC_T + threadIdx.x; v < hi; v += (u64)gridDim.x * LC_T) {
+    const bool l = lf[v] != LC_NIL, r = rt[v] != LC_NIL;
+    const bool zero = !l && !r, unary = !l || !r;
+    flags[v - lo] = (zero || (unary && pa[v] != LC_NIL)) ? 1 : 0;
+  }
+}
+
+__device__ __forceinline__ bool tc_active(const u32* __restrict__ sorted, u64 fill, u64 x) {
+  if (x == LC_NIL) return false;
+  u64 lo = 0, hi = fill;
+  while (lo < hi) {
+    const u64 mid = (lo + hi) >> 1;
+    if ((u64)sorted[mid] < x) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo < fill && (u64)sorted[lo] == x;
+}
+
+// eligibility (contraction.py:451-462)
+__global__ void __launch_bounds__(LC_T) tc_elig_kernel(const u64* __restrict__ pa, const u64* __restrict__ lf,
+                                                       const u64* __restrict__ rt, const u64* __restrict__ p,
+                                                       const u32* __restrict__ ids, u64 fill,
+                                                       const u32* __restrict__ sorted, unsigned char* elig) {
+  for (u64 k = (u64)blockIdx.x * LC_T + threadIdx.x; k < fill; k += (u64)gridDim.x * LC_T) {
+    const u64 v = ids[k];
+    const u64 a = pa[v], l = lf[v], r = rt[v], pv = p[v];
+    bool ok = (l == LC_NIL && r == LC_NIL) || a != LC_NIL;
+    if (tc_active(sorted, fill, a)) ok = ok && pv < p[a];
+    if (tc_active(sorted, fill, l)) ok = ok && pv < p[l];
+    if (tc_active(sorted, fill, r)) ok = ok && pv < p[r];
+    elig[k] = ok ? 1 : 0;
+  }
+}
+
+// pre-surgery state of each committing node: parent, child, is_left, the
+// parent's child count, the grandparent, the node's value
+// (contraction.py:475-493)
+static constexpr int TC_G = 6;  // gathered words per committing node
+
+__global__ void __launch_bounds__(LC_T) tc_gather_kernel(const u64* __restrict__ pa, const u64* __restrict__ lf,
+                                                         const u64* __restrict__ rt,
+                                                         const u64* __restrict__ values,
+                                                         const u32* __restrict__ vs, u64 nv, u64* out) {
+  for (u64 k = (u64)blockIdx.x * LC_T + threadIdx.x; k < nv; k += (u64)gridDim.x * LC_T) {
+    const u64 v = vs[k];
+    const u64 a = pa[v], l = lf[v], r = rt[v];
+    const u64 child = l != LC_NIL ? l : r;
+    u64 is_left = 0, pre = 0, gp = LC_NIL;
+    if (a != LC_NIL) {
+      is_left = lf[a] == v;
+      pre = (u64)(lf[a] != LC_NIL) + (u64)(rt[a] != LC_NIL);
+      gp = pa[a];
+    }
+    out[TC_G * k] = a;
+    out[TC_G * k + 1] = child;
+    out[TC_G * k + 2] = is_left;
+    out[TC_G * k + 3] = pre;
+    out[TC_G * k + 4] = gp;
+    out[TC_G * k + 5] = values[v];
+  }
+}
+
+// value folding (rakes into the parent, compresses into the child) and the
+// pointer surgery; writes are disjoint per committed node
+__device__ __forceinline__ void tc_combine(u64* t, u64 x, int op) {
+  unsigned long long* q = (unsigned long long*)t;
+  if (op == 0) atomicAdd(q, (unsigned long long)x);
+  else if (op == 1) atomicMax(q, (unsigned long long)x);
+  else if (op == 2) atomicMin(q, (unsigned long long)x);
+  else atomicXor(q, (unsigned long long)x);
+}
+
+__global__ void __launch_bounds__(LC_T) tc_commit_kernel(u64* pa, u64* lf, u64* rt, u64* values,
+                                                         const u32* __restrict__ vs, u64 nv,
+                                                         const u64* __restrict__ g, int op) {
+  for (u64 k = (u64)blockIdx.x * LC_T + threadIdx.x; k < nv; k += (u64)gridDim.x * LC_T) {
+    const u64 v = vs[k];
+    const u64 a = g[TC_G * k], child = g[TC_G * k + 1], is_left = g[TC_G * k + 2];
+    const u64 val = g[TC_G * k + 5];
+    if (child != LC_NIL) tc_combine(values + child, val, op);
+    else if (a != LC_NIL) tc_combine(values + a, val, op);
+    if (a != LC_NIL) {
+      if (is_left) lf[a] = child;
+      else rt[a] = child;
+    }
+    if (child != LC_NIL) pa[child] = a;
+  }
+}
+
+int tree_round_device(int step, u64* pa, u64* lf, u64* rt, const u64* p, u64* values, u64 lo, u64 hi,
+                      const u32* ids, u64 fill, const u32* sorted, unsigned char* flags, u64* gathered,
+                      int op, cudaStream_t st) {
+  const int sms = num_sms(current_device());
+  auto grid_for = [&](u64 items) {
+    u64 g = (items + LC_T - 1) / LC_T;
+    const u64 cap = (u64)sms * 8;
+    return (unsigned)(g < 1 ? 1 : (g > cap ? cap : g));
+  };
+  switch (step) {
+    case 0:  // ready flags of [lo, hi)
+      if (hi > lo) tc_ready_kernel<<<grid_for(hi - lo), LC_T, 0, st>>>(pa, lf, rt, lo, hi, flags);
+      break;
+    case 1:  // eligibility of ids[0:fill)
+      if (fill) tc_elig_kernel<<<grid_for(fill), LC_T, 0, st>>>(pa, lf, rt, p, ids, fill, sorted, flags);
+      break;
+    case 2:  // gather for the committing ids[0:fill)
+      if (fill) tc_gather_kernel<<<grid_for(fill), LC_T, 0, st>>>(pa, lf, rt, values, ids, fill, gathered);
+      break;
+    case 3:  // fold + surgery
+      if (fill) tc_commit_kernel<<<grid_for(fill), LC_T, 0, st>>>(pa, lf, rt, values, ids, fill, gathered, op);
+      break;
+    default:
+      return PIP_ERR_INVALID_ARG;
+  }
+  PIP_CHECK_LAUNCH();
+  return PIP_OK;
+}
+
+// ---------------------------------------------------------------------------
 // host
 
 struct LcLayout {

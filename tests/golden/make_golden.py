@@ -128,6 +128,48 @@ def make_contraction():
         ranks = list_rank(lst, p, budget=budget, stats_sink=sink)
         d[f"ranks_{name}"] = ranks.copy()
         d[f"rcounts_{name}"] = np.array(sink[0].committed_per_round, dtype=np.uint64)
+    # tree contraction (contraction.py:528-559): random full binary trees
+    from pipal.contraction import BinaryTree, tree_contract
+
+    def random_full_binary_tree(rng, n):  # test_contraction.py:63-83
+        ids = rng.permutation(n)
+        parent = np.full(n, NIL, dtype=np.uint64)
+        left = np.full(n, NIL, dtype=np.uint64)
+        right = np.full(n, NIL, dtype=np.uint64)
+        leaves = [int(ids[0])]
+        used = 1
+        while used < n:
+            pick = int(rng.integers(0, len(leaves)))
+            node = leaves.pop(pick)
+            l, r = int(ids[used]), int(ids[used + 1])
+            used += 2
+            left[node] = l
+            right[node] = r
+            parent[l] = node
+            parent[r] = node
+            leaves.extend([l, r])
+        return parent, left, right
+
+    tcases = [("t1", 1, 0.5, 1.0), ("t3", 3, 0.5, 1.0), ("t999", 999, 0.3, POWER_ONLY_FRACTION),
+              ("t5001", 5001, 0.5, POWER_ONLY_FRACTION), ("t20001", 20001, 0.5, 0.02)]
+    for name, n, eps, frac in tcases:
+        rng = np.random.default_rng(n)
+        pa, lf, rt = random_full_binary_tree(rng, n)
+        vals = rng.integers(0, 1 << 64, size=n, dtype=np.uint64)
+        p = make_priorities(n, Rng(n + 1))
+        budget = EpsilonConfig(eps, prefix_fraction=frac)
+        d[f"tpa_{name}"], d[f"tlf_{name}"], d[f"trt_{name}"] = pa.copy(), lf.copy(), rt.copy()
+        d[f"tval_{name}"], d[f"tp_{name}"] = vals.copy(), p.copy()
+        d[f"tbudget_{name}"] = np.array([eps, frac])
+        t = BinaryTree(pa, lf, rt)
+        v = vals.copy()
+        trace = []
+        roots, st = tree_contract(t, p, v, budget=budget, trace=trace, debug=True)
+        d[f"troots_{name}"] = np.array(sorted(roots.items()), dtype=np.uint64).reshape(-1, 2)
+        d[f"tcounts_{name}"] = np.array(st.committed_per_round, dtype=np.uint64)
+        d[f"ttrace_{name}"] = np.concatenate(trace) if trace else np.zeros(0, dtype=np.uint64)
+        d[f"tvout_{name}"] = v
+        d[f"tpaout_{name}"], d[f"tlfout_{name}"], d[f"trtout_{name}"] = t.parent, t.left, t.right
     np.savez_compressed(OUT / "contraction.npz", **d)
 
 

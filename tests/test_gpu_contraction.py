@@ -153,3 +153,105 @@ def test_rank_budget_metered_large(pip):
         "r", pip.contraction.list_rank(pip.contraction.LinkedList(nxt, prv), p, cfg)))
     assert rep.peak_words <= 8 * b and meter.current_words == 0
     assert np.array_equal(out["r"], ref)
+
+
+# ----------------------------------------------------------------- trees
+
+TCASES = ["t1", "t3", "t999", "t5001", "t20001"]
+
+
+@pytest.mark.parametrize("name", TCASES)
+@pytest.mark.parametrize("where", ["host", "device"])
+def test_tree_contract_golden(pip, name, where):
+    import torch
+
+    g = golden("contraction")
+    eps, frac = g[f"tbudget_{name}"]
+    budget = pip.EpsilonConfig(float(eps), float(frac))
+    arrs = [g[f"tpa_{name}"].copy(), g[f"tlf_{name}"].copy(), g[f"trt_{name}"].copy()]
+    vals = g[f"tval_{name}"].copy()
+    if where == "device":
+        arrs = [torch.from_numpy(x.view(np.int64)).cuda() for x in arrs]
+        vals = torch.from_numpy(vals.view(np.int64)).cuda()
+    tree = pip.contraction.BinaryTree(*arrs)
+    trace: list = []
+    roots, st = pip.contraction.tree_contract(tree, g[f"tp_{name}"], vals, budget=budget,
+                                              trace=trace, debug=True)
+    want = {int(a): int(b) for a, b in g[f"troots_{name}"].tolist()}
+    assert roots == want
+    assert st.committed_per_round == g[f"tcounts_{name}"].tolist()
+    assert np.array_equal(np.concatenate(trace), g[f"ttrace_{name}"])
+
+    def h(x):
+        return x if isinstance(x, np.ndarray) else x.cpu().numpy().view(np.uint64)
+
+    assert np.array_equal(h(vals), g[f"tvout_{name}"])
+    for arr, key in zip((tree.parent, tree.left, tree.right), ("tpaout", "tlfout", "trtout")):
+        assert np.array_equal(h(arr), g[f"{key}_{name}"])
+
+
+def test_tree_known_answers(pip):
+    C = pip.contraction
+    FULL = pip.EpsilonConfig(0.5, 1.0)
+    # test_contraction.py:213-246
+    t = C.BinaryTree(words([None]), words([None]), words([None]))
+    roots, st = C.tree_contract(t, words([0]), words([42]), budget=FULL)
+    assert roots == {0: 42} and st.rounds == 1
+    t = C.BinaryTree(words([None, 0, 0]), words([1, None, None]), words([2, None, None]))
+    roots, _ = C.tree_contract(t, words([2, 0, 1]), words([10, 20, 30]), budget=FULL, debug=True)
+    assert roots == {0: 60}
+    t = C.BinaryTree(words([None, None, None]), words([None] * 3), words([None] * 3))
+    roots, _ = C.tree_contract(t, words([2, 0, 1]), words([5, 6, 7]), budget=FULL)
+    assert roots == {0: 5, 1: 6, 2: 7}
+    with pytest.raises(ValueError, match="exactly two children"):
+        C.validate_binary_tree(C.BinaryTree(words([None, 0]), words([1, None]), words([None, None])))
+
+
+def _random_full_binary_tree(rng, n):  # test_contraction.py:63-83
+    ids = rng.permutation(n)
+    parent = np.full(n, NIL, dtype=np.uint64)
+    left = np.full(n, NIL, dtype=np.uint64)
+    right = np.full(n, NIL, dtype=np.uint64)
+    leaves = [int(ids[0])]
+    used = 1
+    while used < n:
+        node = leaves.pop(int(rng.integers(0, len(leaves))))
+        lc, rc = int(ids[used]), int(ids[used + 1])
+        used += 2
+        left[node], right[node] = lc, rc
+        parent[lc] = parent[rc] = node
+        leaves.extend([lc, rc])
+    return parent, left, right
+
+
+def _seq_tree_eval(parent, left, right, values):  # baselines.py:75-96
+    out = {}
+    for root in np.flatnonzero(parent == np.uint64(NIL)).tolist():
+        total, stack = 0, [root]
+        while stack:
+            v = stack.pop()
+            total = (total + int(values[v])) & NIL
+            for c in (left[v], right[v]):
+                if c != np.uint64(NIL):
+                    stack.append(int(c))
+        out[root] = total
+    return out
+
+
+def test_tree_budget_metered(pip):
+    # test_contraction.py:249-265: n = 50_001, pure budget, charged <= 8 b
+    rng = np.random.default_rng(3)
+    n = 50_001
+    pa, lf, rt = _random_full_binary_tree(rng, n)
+    vals = rng.integers(0, 1 << 64, size=n, dtype=np.uint64)
+    ref = _seq_tree_eval(pa, lf, rt, vals)
+    cfg = pip.EpsilonConfig(0.5, 1e-12)
+    b = cfg.prefix_words(n)
+    p = pip.contraction.make_priorities(n, pip.Rng(2))
+    meter = pip.SpaceMeter()
+    out = {}
+    tree = pip.contraction.BinaryTree(pa, lf, rt)
+    rep = pip.meter_scope(meter, 8 * b, lambda: out.__setitem__("r", pip.contraction.tree_contract(
+        tree, p, vals, cfg, debug=True)))
+    assert rep.peak_words <= 8 * b and meter.current_words == 0
+    assert out["r"][0] == ref
