@@ -81,7 +81,8 @@ struct MergeGlobal {
 
 struct MergeArgs {
   u32 dbg;  // PIP_MERGE_DBG: bit0 skip the dataflow wait (profiling), bit1 no merge (profiling), bit2 CTA 0 cycle counters,
-            // bit3 mapped staging, bit4 global dataflow rule, bit5 pointer jumping for cut-free cycles (tests)
+            // bit3 mapped staging, bit4 global dataflow rule, bit5 pointer jumping for cut-free cycles (tests),
+            // bit6 8-byte write-out stores, bit8 bisect the whole diagonal (no gallop)
   u64* a;
   u64 n, na, nb;
   u64 hA, hB, KA, KB, K, NB, D, ncuts, L;
@@ -727,6 +728,29 @@ __global__ void __launch_bounds__(MG_THREADS, MG_CTAS_PER_SM) merge_kernel(Merge
         if (r0 < r1) {
           u32 lo = r0 > nb ? r0 - nb : 0, hi = r0 < na ? r0 : na;
           const u32 bq = sB + r0 - 1;  // B word of merge-path step mid: bq - mid
+          // gallop from the proportional estimate r0 * na / total (the
+          // co-rank of interleaved runs sits within a few tens of it), then
+          // bisect the bracket: fewer dependent shared loads than bisecting
+          // the whole diagonal; any input stays correct (brackets only grow)
+          if (lo < hi && !(M.dbg & 256)) {
+            u32 g = (u32)(((u64)r0 * na) / (total ? total : 1u));
+            g = g < lo ? lo : (g >= hi ? hi - 1 : g);
+            if (sp[sA + g] <= sp[bq - g]) {  // co-rank in (g, hi]
+              lo = g + 1;
+              for (u32 st = 16; lo + st <= hi; st <<= 1) {
+                const u32 j = lo + st - 1;
+                if (sp[sA + j] <= sp[bq - j]) lo = j + 1;
+                else { hi = j; break; }
+              }
+            } else {  // co-rank in [lo, g]
+              hi = g;
+              for (u32 st = 16; hi >= lo + st; st <<= 1) {
+                const u32 j = hi - st;
+                if (!(sp[sA + j] <= sp[bq - j])) hi = j;
+                else { lo = j + 1; break; }
+              }
+            }
+          }
           while (lo < hi) {
             const u32 mid = (lo + hi) >> 1;
             if (sp[sA + mid] <= sp[bq - mid]) lo = mid + 1;
