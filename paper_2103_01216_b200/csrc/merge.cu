@@ -118,11 +118,43 @@ __device__ __forceinline__ u64 phys_b(const MergeArgs& M, u64 y) {
   return M.hA + ((u64)__ldcg(M.dest + M.KA + (y >> MG_LOGC)) << MG_LOGC) + (y & (MG_C - 1));
 }
 
+// smallest i in [lo, hi] with !pred(i), pred monotone (true, then false):
+// gallop from the estimate g in steps st, 2st, ..., then bisect the bracket
+// (random probes go to HBM in P0: a close estimate saves most of them)
+template <class P>
+__device__ __forceinline__ u64 gallop_lb(u64 lo, u64 hi, u64 g, u64 st, P pred) {
+  if (lo < hi) {
+    g = g < lo ? lo : (g >= hi ? hi - 1 : g);
+    if (pred(g)) {
+      lo = g + 1;
+      for (; lo + st <= hi; st <<= 1) {
+        if (pred(lo + st - 1)) lo += st;
+        else { hi = lo + st - 1; break; }
+      }
+    } else {
+      hi = g;
+      for (; hi >= lo + st; st <<= 1) {
+        if (!pred(hi - st)) hi -= st;
+        else { lo = hi - st + 1; break; }
+      }
+    }
+  }
+  while (lo < hi) {
+    const u64 mid = (lo + hi) >> 1;
+    if (pred(mid)) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
 // merge path over the original runs A = a[0:na), B = a[na:n) (A first on ties)
 __device__ __forceinline__ u64 corank2_global(const MergeArgs& M, u64 q) {
   const u64* A = M.a;
   const u64* B = M.a + M.na;
-  u64 lo = q > M.nb ? q - M.nb : 0, hi = q < M.na ? q : M.na;
+  const u64 lo0 = q > M.nb ? q - M.nb : 0, hi0 = q < M.na ? q : M.na;
+  if (!(M.dbg & 256))
+    return gallop_lb(lo0, hi0, (u64)(((unsigned __int128)q * M.na) / M.n), 64,
+                     [&](u64 i) { return __ldcg(A + i) <= __ldcg(B + (q - i - 1)); });
+  u64 lo = lo0, hi = hi0;
   while (lo < hi) {
     const u64 mid = (lo + hi) >> 1;
     if (__ldcg(A + mid) <= __ldcg(B + (q - mid - 1))) lo = mid + 1;
@@ -211,21 +243,17 @@ __global__ void __launch_bounds__(MG_THREADS, MG_CTAS_PER_SM) merge_kernel(Merge
       u64 d;
       if (x < M.KA) {
         const u64 last = __ldcg(a + M.hA + ((x + 1) << MG_LOGC) - 1);
-        u64 lo = 0, hi = M.KB;  // #B' chunks with last < this last
-        while (lo < hi) {
-          const u64 mid = (lo + hi) >> 1;
-          if (__ldcg(a + M.na + ((mid + 1) << MG_LOGC) - 1) < last) lo = mid + 1; else hi = mid;
-        }
-        d = x + lo;
+        // #B' chunks with last < this last (estimate: proportional position)
+        const u64 c = gallop_lb(0, M.KB, (u64)(((unsigned __int128)x * M.KB) / (M.KA ? M.KA : 1)), 4,
+                                [&](u64 mid) { return __ldcg(a + M.na + ((mid + 1) << MG_LOGC) - 1) < last; });
+        d = x + c;
       } else {
         const u64 y = x - M.KA;
         const u64 last = __ldcg(a + M.na + ((y + 1) << MG_LOGC) - 1);
-        u64 lo = 0, hi = M.KA;  // #A' chunks with last <= this last
-        while (lo < hi) {
-          const u64 mid = (lo + hi) >> 1;
-          if (__ldcg(a + M.hA + ((mid + 1) << MG_LOGC) - 1) <= last) lo = mid + 1; else hi = mid;
-        }
-        d = y + lo;
+        // #A' chunks with last <= this last
+        const u64 c = gallop_lb(0, M.KA, (u64)(((unsigned __int128)y * M.KA) / (M.KB ? M.KB : 1)), 4,
+                                [&](u64 mid) { return __ldcg(a + M.hA + ((mid + 1) << MG_LOGC) - 1) <= last; });
+        d = y + c;
       }
       M.dest[x] = (u32)d;
       M.inv[d] = (u32)x;
