@@ -337,31 +337,31 @@ __global__ void __launch_bounds__(MG_THREADS, MG_CTAS_PER_SM) merge_kernel(Merge
   {
     u64 s, e;
     mpart(M.K, G, b, s, e);
-    u32 cnt = 0;
-    for (u64 x = s + tid; x < e; x += MG_THREADS)
-      cnt += !__ldcg(M.visited + x) && __ldcg(M.inv + x) != (u32)x;
-    cnt = __reduce_add_sync(0xffffffffu, cnt);
-    if ((tid & 31) == 0 && cnt) atomicAdd(&g->uncut, cnt);
+    // count the slots on cut-free cycles and list them (warp-aggregated
+    // appends into the pointer-jumping array, unused by the serial path)
+    const u64 cap = M.K < MG_UNCUT_SERIAL ? M.K : MG_UNCUT_SERIAL;
+    const u32 lane = tid & 31;
+    for (u64 x0 = s; x0 < e; x0 += MG_THREADS) {
+      const u64 x = x0 + tid;
+      const bool cand = x < e && !__ldcg(M.visited + x) && __ldcg(M.inv + x) != (u32)x;
+      const unsigned bal = __ballot_sync(0xffffffffu, cand);
+      if (!bal) continue;
+      u32 base = 0;
+      if (lane == 0) base = atomicAdd(&g->uncut, (u32)__popc(bal));
+      base = __shfl_sync(0xffffffffu, base, 0);
+      const u64 idx = base + (u32)__popc(bal & ((1u << lane) - 1u));
+      if (cand && idx < cap) M.lab[0][idx] = (u32)x;
+    }
   }
   if (!grid_barrier(&g->sync, gen)) return;
   const u32 n_uncut = ld_relaxed_u32(&g->uncut);
   if (n_uncut && n_uncut <= MG_UNCUT_SERIAL && !(M.dbg & 32)) {
-    // few slots (the usual case with a cut buffer): CTA 0 collects them and
-    // rotates each cycle through shared memory — no pointer-jumping rounds
+    // few slots (the usual case with a cut buffer): CTA 0 rotates each cycle
+    // of the listed slots through shared memory — no pointer-jumping rounds
     if (b == 0) {
-      __shared__ u32 s_ucnt;
-      u32* s_list = reinterpret_cast<u32*>(smem + MG_C);
-      if (tid == 0) s_ucnt = 0;
-      __syncthreads();
-      for (u64 x = tid; x < M.K; x += MG_THREADS)
-        if (!__ldcg(M.visited + x) && __ldcg(M.inv + x) != (u32)x) {
-          const u32 i = atomicAdd(&s_ucnt, 1u);
-          if (i < MG_UNCUT_SERIAL) s_list[i] = (u32)x;
-        }
-      __syncthreads();
-      const u32 cnt = s_ucnt < MG_UNCUT_SERIAL ? s_ucnt : MG_UNCUT_SERIAL;
+      const u32 cnt = n_uncut;  // <= min(K, MG_UNCUT_SERIAL): all listed in P1b
       for (u32 c = 0; c < cnt; ++c) {
-        const u64 x0 = s_list[c];
+        const u64 x0 = __ldcg(M.lab[0] + c);
         // thread 0 alone reads and writes `visited` here (program order)
         if (tid == 0) s_flag = !__ldcg(M.visited + x0);
         __syncthreads();
