@@ -241,14 +241,36 @@ __global__ void __launch_bounds__(256) part_bounds_kernel(const u64* __restrict_
     const u64 r = baseL[k];
     const u64 rn = k + 1 < ntiles ? baseL[k + 1] : X;
     if (rn <= r) continue;  // no misfits in this left tile
-    // right tile j: largest j in [kb, ntiles) with baseR[j] <= r
-    u64 lo = kb, hi = ntiles;  // invariant: baseR[lo] <= r (baseR[kb] == 0)
-    while (hi - lo > 1) {
-      const u64 mid = (lo + hi) >> 1;
-      if (__ldcg(baseR + mid) <= r) lo = mid;
-      else hi = mid;
+    // right tile j: largest j in [kb, ntiles) with baseR[j] <= r, i.e. the
+    // first j' in (kb, ntiles] with baseR[j'] > r, minus one; gallop from
+    // the proportional estimate (misfits spread over the right tiles)
+    u64 lo = kb + 1, hi = ntiles;
+    {
+      u64 g = kb + (u64)(((unsigned __int128)r * (ntiles - kb)) / X);
+      g = g < lo ? lo : (g >= hi ? (hi > lo ? hi - 1 : lo) : g);
+      u64 st = 4;
+      if (lo < hi) {
+        if (__ldcg(baseR + g) <= r) {
+          lo = g + 1;
+          for (; lo + st <= hi; st <<= 1) {
+            if (__ldcg(baseR + lo + st - 1) <= r) lo += st;
+            else { hi = lo + st - 1; break; }
+          }
+        } else {
+          hi = g;
+          for (; hi >= lo + st; st <<= 1) {
+            if (!(__ldcg(baseR + hi - st) <= r)) hi -= st;
+            else { lo = hi - st + 1; break; }
+          }
+        }
+      }
+      while (lo < hi) {
+        const u64 mid = (lo + hi) >> 1;
+        if (__ldcg(baseR + mid) <= r) lo = mid + 1;
+        else hi = mid;
+      }
     }
-    const u64 j = lo;
+    const u64 j = lo - 1;
     u64 q = r - __ldcg(baseR + j);  // rank inside tile j
     const u64 s0 = j * PT > m ? j * PT : m, s1 = (j + 1) * PT < n ? (j + 1) * PT : n;
     u64 pos = ~0ull;
