@@ -82,7 +82,8 @@ struct MergeGlobal {
 struct MergeArgs {
   u32 dbg;  // PIP_MERGE_DBG: bit0 skip the dataflow wait (profiling), bit1 no merge (profiling), bit2 CTA 0 cycle counters,
             // bit3 mapped staging, bit4 global dataflow rule, bit5 pointer jumping for cut-free cycles (tests),
-            // bit6 8-byte write-out stores, bit8 bisect the whole diagonal (no gallop)
+            // bit6 8-byte write-out stores, bit8 bisect the whole diagonal (no gallop),
+            // bit9 16-byte LSU write-out stores instead of one bulk copy per warp
   u64* a;
   u64 n, na, nb;
   u64 hA, hB, KA, KB, K, NB, D, ncuts, L;
@@ -739,6 +740,7 @@ __global__ void __launch_bounds__(MG_THREADS, MG_CTAS_PER_SM) merge_kernel(Merge
     const u32 t = tid - 64, w = t >> 5, lane = t & 31;
     const u32 r0_all = (u32)(((u64)t * MG_C) / NMW), r1_all = (u32)(((u64)(t + 1) * MG_C) / NMW);
     const u32 wr0 = (u32)(((u64)(w * 32) * MG_C) / NMW), wr1 = (u32)(((u64)(w * 32 + 32) * MG_C) / NMW);
+    bool bulk_pending = false;  // this warp's last bulk store may still read its tile
     for (u64 j = 0; j < nblk; ++j) {
       const u64 m = b + j * G;
       const int sb = (int)(j & 1);
@@ -861,15 +863,37 @@ __global__ void __launch_bounds__(MG_THREADS, MG_CTAS_PER_SM) merge_kernel(Merge
       u64* gd = ((keep0 && j == 0) ? M.head_save : a + m * MG_C) + wr0;
       const u32 head = (u32)(((uintptr_t)gd >> 3) & 1u);
       u64* scr = s_scr + w * MG_SCR + head - wr0;  // indexed by block-relative rank
+      // the tile may still be read by this warp's previous bulk store
+      if (bulk_pending) {
+        if (lane == 0) bulk_wait_read_all();
+        __syncwarp();
+        bulk_pending = false;
+      }
 #pragma unroll
       for (int q = 0; q < MO; ++q)
         if (r0 + q < r1) scr[r0 + q] = o[q];
-      __syncwarp();
       const u32 cnt = (wr1 < total ? wr1 : total) - (wr0 < total ? wr0 : total);
       const u64* sw = scr + wr0;  // sw[k] = output word gd[k]; gd + k, sw + k 16-byte aligned iff k = head mod 2
-      if (M.dbg & 64) {
+      if (!(M.dbg & (64 | 512))) {
+        // one bulk copy per warp (the LSU issues no global stores); the
+        // ragged first / last word by hand
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0 && cnt) {
+          const u32 body = (cnt - head) & ~1u;
+          if (head) __stcs(gd, sw[0]);
+          if (head + body < cnt) __stcs(gd + cnt - 1, sw[cnt - 1]);
+          if (body) {
+            tma_store_1d(gd + head, sw + head, body * 8u);
+            bulk_commit();
+          }
+        }
+        bulk_pending = true;
+      } else if (M.dbg & 64) {
+        __syncwarp();
         for (u32 k = lane; k < cnt; k += 32) gd[k] = sw[k];
       } else {
+        __syncwarp();
         for (u32 k = head + 2 * lane; k + 1 < cnt; k += 64)
           __stcs(reinterpret_cast<ulonglong2*>(gd + k), *reinterpret_cast<const ulonglong2*>(sw + k));
         if (lane == 0 && cnt) {
@@ -880,6 +904,8 @@ __global__ void __launch_bounds__(MG_THREADS, MG_CTAS_PER_SM) merge_kernel(Merge
       __syncwarp();
       mark(2);
     }
+    if (lane == 0) bulk_wait_all();  // the stores have landed (head_save is read below)
+    __syncwarp();
   }
   if (prof && tid == 64) {
     g->sec[0] = cyc[3];  // waiting for the block's loads to land
