@@ -578,14 +578,15 @@ filter_ws_kernel(u64* __restrict__ a, DevPred p, u64* m_out, LookbackCtx c, u64 
 // Split-role pipeline (see scan_ws2_kernel): warp 0 streams tiles in, LBW
 // look-back warps take tiles round-robin so consecutive look-backs overlap,
 // NWC compute warps count tile k and compact + store tile k - D.
-template <int NWC, int S, int PC, int LBW, int D>
+template <int NWC, int S, int PC, int LBW, int D, int J>
 __global__ void __launch_bounds__(32 * (NWC + 1 + LBW), 1)
 filter_ws2_kernel(u64* __restrict__ a, DevPred p, u64* m_out, LookbackCtx c, u64 num_tiles) {
   using O = Op<PIP_OP_ADD>;
-  constexpr u64 TILE = (u64)NWC * 512;
+  constexpr u64 TILE = (u64)NWC * 64 * J;  // J word pairs per lane
   constexpr u32 TILE_BYTES = (u32)(TILE * 8);
   constexpr u64 STRIDE = TILE + 2;  // + 2 words: the compacted output may start one word in
   static_assert(S >= D + 2, "stages");
+  static_assert(J >= 1 && J <= 8, "keep bits fit a u32");
   extern __shared__ __align__(128) u64 ring[];
   __shared__ __align__(8) u64 full[S], reduced[S], pready[S], empty[S];
   __shared__ u64 s_wtot[S][NWC];
@@ -679,11 +680,11 @@ filter_ws2_kernel(u64* __restrict__ a, DevPred p, u64* m_out, LookbackCtx c, u64
     const u32 par = (u32)(((uintptr_t)(a + prefix) >> 3) & 1u);
     u32 run = (u32)s_wexc[s][w] + par;
     const u32 keep = s_keep[s][w * 32 + lane];
-    const u64* src = stage + w * 512;
-    u64 vx[8], vy[8];
-    u32 pos[8];
+    const u64* src = stage + w * (64 * J);
+    u64 vx[J], vy[J];
+    u32 pos[J];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
+    for (int j = 0; j < J; ++j) {
       const bool f0 = (keep >> (2 * j)) & 1u, f1 = (keep >> (2 * j + 1)) & 1u;
       const u32 m0 = __ballot_sync(0xffffffffu, f0);
       const u32 m1 = __ballot_sync(0xffffffffu, f1);
@@ -695,7 +696,7 @@ filter_ws2_kernel(u64* __restrict__ a, DevPred p, u64* m_out, LookbackCtx c, u64
     }
     named_bar(1, NWC * 32);  // the whole tile is in registers
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
+    for (int j = 0; j < J; ++j) {
       const bool f0 = (keep >> (2 * j)) & 1u, f1 = (keep >> (2 * j + 1)) & 1u;
       if (f0) stage[pos[j]] = vx[j];
       if (f1) stage[pos[j] + (f0 ? 1u : 0u)] = vy[j];
@@ -724,10 +725,10 @@ filter_ws2_kernel(u64* __restrict__ a, DevPred p, u64* m_out, LookbackCtx c, u64
       break;
     }
     if (!wait_or_abort(&full[s], ph(k))) break;
-    const u64* src = ring + s * STRIDE + w * 512;
+    const u64* src = ring + s * STRIDE + w * (64 * J);
     u32 keep = 0;
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
+    for (int j = 0; j < J; ++j) {
       const ulonglong2 v = lds2(src + 64 * j + 2 * lane);
       keep |= ((u32)pred_eval_t<PC>(p, v.x) << (2 * j)) | ((u32)pred_eval_t<PC>(p, v.y) << (2 * j + 1));
     }
@@ -942,13 +943,13 @@ static int launch_filter_ws_pc(u64* a, u64 n, const DevPred& p, u64* m_dev,
   return PIP_OK;
 }
 
-template <int NWC, int S, int PC, int LBW, int D>
+template <int NWC, int S, int PC, int LBW, int D, int J>
 static int launch_filter_ws2_pc(u64* a, u64 n, const DevPred& p, u64* m_dev,
                                 const ScratchLayoutF& L, cudaStream_t st, int dev) {
-  constexpr u64 TILE = (u64)NWC * 512;
+  constexpr u64 TILE = (u64)NWC * 64 * J;
   constexpr int THREADS = 32 * (NWC + 1 + LBW);
   const u64 full_tiles = n / TILE, rem = n - full_tiles * TILE;
-  auto k = filter_ws2_kernel<NWC, S, PC, LBW, D>;
+  auto k = filter_ws2_kernel<NWC, S, PC, LBW, D, J>;
   const int smem = (int)(S * (TILE + 2) * 8);
   PIP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   int per_sm = 0;
@@ -970,15 +971,15 @@ static int launch_filter_ws2_pc(u64* a, u64 n, const DevPred& p, u64* m_dev,
   return PIP_OK;
 }
 
-template <int NWC, int S, int LBW, int D>
+template <int NWC, int S, int LBW, int D, int J = 8>
 static int launch_filter_ws2(u64* a, u64 n, const DevPred& p, u64* m_dev, const ScratchLayoutF& L,
                              cudaStream_t st, int dev) {
   switch (pred_class(p)) {
-    case PC_MASK: return launch_filter_ws2_pc<NWC, S, PC_MASK, LBW, D>(a, n, p, m_dev, L, st, dev);
-    case PC_MOD: return launch_filter_ws2_pc<NWC, S, PC_MOD, LBW, D>(a, n, p, m_dev, L, st, dev);
-    case PC_MODODD: return launch_filter_ws2_pc<NWC, S, PC_MODODD, LBW, D>(a, n, p, m_dev, L, st, dev);
-    case PC_MODODD0: return launch_filter_ws2_pc<NWC, S, PC_MODODD0, LBW, D>(a, n, p, m_dev, L, st, dev);
-    default: return launch_filter_ws2_pc<NWC, S, PC_GEN, LBW, D>(a, n, p, m_dev, L, st, dev);
+    case PC_MASK: return launch_filter_ws2_pc<NWC, S, PC_MASK, LBW, D, J>(a, n, p, m_dev, L, st, dev);
+    case PC_MOD: return launch_filter_ws2_pc<NWC, S, PC_MOD, LBW, D, J>(a, n, p, m_dev, L, st, dev);
+    case PC_MODODD: return launch_filter_ws2_pc<NWC, S, PC_MODODD, LBW, D, J>(a, n, p, m_dev, L, st, dev);
+    case PC_MODODD0: return launch_filter_ws2_pc<NWC, S, PC_MODODD0, LBW, D, J>(a, n, p, m_dev, L, st, dev);
+    default: return launch_filter_ws2_pc<NWC, S, PC_GEN, LBW, D, J>(a, n, p, m_dev, L, st, dev);
   }
 }
 
@@ -1029,6 +1030,12 @@ int filter_device(u64* a, u64 n, const pip_pred* pred, u64* m_dev, void* scratch
     if (cfg == 10) return launch_filter_ws<12, 4, false, true>(a, n, p, m_dev, L, st, dev);
     if (cfg == 17) return launch_filter_ws2<13, 4, 3, 2>(a, n, p, m_dev, L, st, dev);  // default
     if (cfg == 18) return launch_filter_ws2<12, 4, 3, 2>(a, n, p, m_dev, L, st, dev);
+    // half-size tiles (8 words per lane) with twice the stages, so more tile
+    // loads are in flight: 14.3 ms (cfg 19) and 12.4 ms (cfg 20: 4 look-back
+    // warps, compaction 3 behind) at 2^32 against 9.0 -- the per-tile
+    // pipeline, not the loads in flight, paces the filter
+    if (cfg == 19) return launch_filter_ws2<13, 8, 3, 2, 4>(a, n, p, m_dev, L, st, dev);
+    if (cfg == 20) return launch_filter_ws2<13, 8, 4, 3, 4>(a, n, p, m_dev, L, st, dev);
 
     if (cfg == 11) return launch_filter_ws<14, 4>(a, n, p, m_dev, L, st, dev);
     if (cfg == 12) return launch_filter_ws<12, 4>(a, n, p, m_dev, L, st, dev);
