@@ -203,6 +203,14 @@ int pip_merge_u64(uint64_t* a, uint64_t n, uint64_t split, int check_sorted,
 /* device workspace (bytes) the relaxed merge uses for n, split and budget
  * b = budget_words (b(n) of the caller's EpsilonConfig); 0 = strong path. */
 size_t pip_merge_workspace_bytes(uint64_t n, uint64_t split, uint64_t budget_words);
+/* the same contract on a host array (synchronous).  Streamed: the output is
+ * produced in chunks of 2^24 words (PIP_HOST_CHUNK_LOG2; the ring of
+ * PIP_HOST_NBUF chunk buffers stays within budget_words when it is > 0),
+ * each merged out of place on the device from the uploaded runs and copied
+ * straight back, so uploads, merges and write-backs overlap; the host array
+ * is still updated in place (every word is uploaded before the write-back
+ * that overwrites it).  PIP_MERGE_HOST_INPLACE=1: upload all, in-place
+ * device merge, copy back. */
 int pip_merge_u64_host(uint64_t* host_a, uint64_t n, uint64_t split, uint64_t budget_words,
                        int device);
 

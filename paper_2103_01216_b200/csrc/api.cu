@@ -82,6 +82,7 @@ int sort_segments_device(u64* a, const u64* seg_lo, const u32* seg_len, u64 nseg
 int partition_device(u64* a, u64 n, const pip_pred* pred, u64* m_dev, void* ws, size_t ws_bytes,
                      cudaStream_t st);
 size_t merge_workspace_bytes(u64 n, u64 split, u64 budget_words);
+int merge_copy_device(const u64* a, u64 na, const u64* b, u64 nb, u64* out, cudaStream_t st);
 int merge_device(u64* a, u64 n, u64 split, int check_sorted, void* ws, size_t ws_bytes,
                  void* scratch, size_t scratch_bytes, cudaStream_t st);
 
@@ -301,6 +302,84 @@ int filter_host(u64* host, u64 n, const pip_pred* pred, u64* m_out, int device) 
   return PIP_OK;
 }
 
+// merge over host memory, streamed: output chunk k (C words) is merged on the
+// device from A[i_k, i_k+1) and B[j_k, j_k+1) into a ring buffer and copied
+// back to host[kC, (k+1)C).  Uploads run in chunk order: before chunk k the
+// device holds A up to min(na, (k+1)C) (every A word its host region will
+// overwrite; A words only move right) and B up to j_k+1 (B words only move
+// left, so that covers the B part of the region).  Every host word is read
+// by an upload before the write-back that overwrites it: the write-back of
+// chunk k waits for its merge, which waits for its uploads, and later
+// uploads read only host[(k+1)C, n).  Co-ranks are taken on the host array
+// before anything moves.
+static u64 host_corank(const u64* a, u64 na, const u64* b, u64 nb, u64 r) {
+  u64 lo = r > nb ? r - nb : 0, hi = r < na ? r : na;
+  while (lo < hi) {
+    const u64 mid = (lo + hi) >> 1;
+    if (b[r - mid - 1] >= a[mid]) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+int merge_host_stream(u64* host, u64 n, u64 split, u64 budget_words, int device) {
+  const u64 na = split, nb = n - split;
+  u64 chunk = host_chunk();
+  const int nbuf = host_nbuf();
+  // the ring is the only device memory besides the uploaded runs: keep it
+  // within a relaxed budget (>= 2^16 words per buffer)
+  if (budget_words && chunk * (u64)nbuf > budget_words) {
+    chunk = budget_words / (u64)nbuf;
+    if (chunk < (1ull << 16)) chunk = 1ull << 16;
+  }
+  if (chunk > n) chunk = n;
+  const u64 nchunks = (n + chunk - 1) / chunk;
+  std::vector<u64> ci(nchunks + 1);
+  for (u64 k = 0; k <= nchunks; ++k) {
+    const u64 r = k * chunk < n ? k * chunk : n;
+    ci[k] = host_corank(host, na, host + na, nb, r);
+  }
+  DevBuf d, ring[8];
+  PIP_CUDA(d.alloc(n * 8));
+  const int nr = nchunks < (u64)nbuf ? (int)nchunks : nbuf;
+  for (int i = 0; i < nr; ++i) PIP_CUDA(ring[i].alloc(chunk * 8));
+  Stream cin, comp, cout;
+  PIP_CUDA(cin.create());
+  PIP_CUDA(comp.create());
+  PIP_CUDA(cout.create());
+  std::vector<Event> in_done(nchunks), comp_done(nchunks), out_done(nchunks);
+  u64* dv = (u64*)d.p;
+  u64 ua = 0, ub = 0;
+  for (u64 k = 0; k < nchunks; ++k) {
+    PIP_CUDA(in_done[k].create());
+    PIP_CUDA(comp_done[k].create());
+    PIP_CUDA(out_done[k].create());
+    const u64 r0 = k * chunk, r1 = (k + 1) * chunk < n ? (k + 1) * chunk : n;
+    const u64 i0 = ci[k], i1 = ci[k + 1], j0 = r0 - i0, j1 = r1 - i1;
+    const u64 ta = r1 < na ? r1 : na;
+    if (ta > ua) {
+      PIP_CUDA(cudaMemcpyAsync(dv + ua, host + ua, (ta - ua) * 8, cudaMemcpyHostToDevice, cin.s));
+      ua = ta;
+    }
+    if (j1 > ub) {
+      PIP_CUDA(cudaMemcpyAsync(dv + na + ub, host + na + ub, (j1 - ub) * 8,
+                               cudaMemcpyHostToDevice, cin.s));
+      ub = j1;
+    }
+    PIP_CUDA(cudaEventRecord(in_done[k].e, cin.s));
+    PIP_CUDA(cudaStreamWaitEvent(comp.s, in_done[k].e, 0));
+    if (k >= (u64)nr) PIP_CUDA(cudaStreamWaitEvent(comp.s, out_done[k - nr].e, 0));
+    u64* o = (u64*)ring[k % nr].p;
+    if (int rc = merge_copy_device(dv + i0, i1 - i0, dv + na + j0, j1 - j0, o, comp.s)) return rc;
+    PIP_CUDA(cudaEventRecord(comp_done[k].e, comp.s));
+    PIP_CUDA(cudaStreamWaitEvent(cout.s, comp_done[k].e, 0));
+    PIP_CUDA(cudaMemcpyAsync(host + r0, o, (r1 - r0) * 8, cudaMemcpyDeviceToHost, cout.s));
+    PIP_CUDA(cudaEventRecord(out_done[k].e, cout.s));
+  }
+  PIP_CUDA(cudaStreamSynchronize(cout.s));
+  return PIP_OK;
+}
+
 }  // namespace pip
 
 using namespace pip;
@@ -454,21 +533,25 @@ int pip_merge_u64_host(uint64_t* host_a, uint64_t n, uint64_t split, uint64_t bu
                        int device) {
   if (split > n || (n && !host_a)) return PIP_ERR_INVALID_ARG;
   PIP_CUDA(cudaSetDevice(device));
-  if (n == 0) return PIP_OK;
-  Stream s;
-  PIP_CUDA(s.create());
-  DevBuf a, ws, scratch;
-  PIP_CUDA(a.alloc(n * 8));
-  const size_t wb = merge_workspace_bytes(n, split, budget_words);
-  PIP_CUDA(ws.alloc(wb));
-  const size_t sb = scratch_bytes_for(num_sms(device));
-  PIP_CUDA(scratch.alloc(sb));
-  PIP_CUDA(cudaMemcpyAsync(a.p, host_a, n * 8, cudaMemcpyHostToDevice, s.s));
-  int rc = merge_device((u64*)a.p, n, split, 0, wb ? ws.p : nullptr, wb, scratch.p, sb, s.s);
-  if (rc) return rc;
-  PIP_CUDA(cudaMemcpyAsync(host_a, a.p, n * 8, cudaMemcpyDeviceToHost, s.s));
-  PIP_CUDA(cudaStreamSynchronize(s.s));
-  return PIP_OK;
+  if (n < 2 || split == 0 || split == n) return PIP_OK;
+  const char* e = getenv("PIP_MERGE_HOST_INPLACE");
+  if (e && atoi(e)) {  // upload everything, merge in place on the device, copy back
+    Stream s;
+    PIP_CUDA(s.create());
+    DevBuf a, ws, scratch;
+    PIP_CUDA(a.alloc(n * 8));
+    const size_t wb = merge_workspace_bytes(n, split, budget_words);
+    PIP_CUDA(ws.alloc(wb));
+    const size_t sb = scratch_bytes_for(num_sms(device));
+    PIP_CUDA(scratch.alloc(sb));
+    PIP_CUDA(cudaMemcpyAsync(a.p, host_a, n * 8, cudaMemcpyHostToDevice, s.s));
+    int rc = merge_device((u64*)a.p, n, split, 0, wb ? ws.p : nullptr, wb, scratch.p, sb, s.s);
+    if (rc) return rc;
+    PIP_CUDA(cudaMemcpyAsync(host_a, a.p, n * 8, cudaMemcpyDeviceToHost, s.s));
+    PIP_CUDA(cudaStreamSynchronize(s.s));
+    return PIP_OK;
+  }
+  return merge_host_stream((u64*)host_a, n, split, budget_words, device);
 }
 
 size_t pip_rp_workspace_bytes(uint64_t n, uint64_t prefix, int variant) {

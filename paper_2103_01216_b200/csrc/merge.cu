@@ -1009,6 +1009,81 @@ static MergeLayout merge_layout(u64 n, u64 na, u64 budget_words, int grid) {
   return L;
 }
 
+// ---------------------------------------------------------------------------
+// Streaming host merge (pip_merge_u64_host): the runs arrive over PCIe, so
+// the device merges each output chunk out of place from the uploaded runs
+// into a ring buffer that is copied straight back.  Chunk co-ranks come from
+// the host (all computed before anything is written back), so a chunk only
+// ever reads the part of the runs that has been uploaded.
+//
+// merge_copy_kernel: out[0 : na+nb) = merge(a[0:na), b[0:nb)), equal keys
+// from a first (the co-rank rule of strong.py:474-488); one CTA per
+// MC_TILE outputs, runs staged in shared memory, MC_ITEMS outputs per thread.
+static constexpr int MC_THREADS = 256, MC_ITEMS = 8, MC_TILE = MC_THREADS * MC_ITEMS;
+
+__device__ __forceinline__ u64 mc_corank(const u64* a, u64 na, const u64* b, u64 nb, u64 r) {
+  u64 lo = r > nb ? r - nb : 0, hi = r < na ? r : na;
+  while (lo < hi) {  // smallest i with not (b[r-i-1] >= a[i])
+    const u64 mid = (lo + hi) >> 1;
+    if (b[r - mid - 1] >= a[mid]) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+__global__ void __launch_bounds__(MC_THREADS)
+merge_copy_kernel(const u64* __restrict__ a, u64 na, const u64* __restrict__ b, u64 nb,
+                  u64* __restrict__ out) {
+  __shared__ u64 s[MC_TILE + 1];
+  __shared__ u64 s_i[2];
+  const u64 n = na + nb;
+  const u64 r0 = (u64)blockIdx.x * MC_TILE;
+  const u64 r1 = r0 + MC_TILE < n ? r0 + MC_TILE : n;
+  if (threadIdx.x == 0) s_i[0] = mc_corank(a, na, b, nb, r0);
+  if (threadIdx.x == 32) s_i[1] = mc_corank(a, na, b, nb, r1);
+  __syncthreads();
+  const u64 i0 = s_i[0], i1 = s_i[1], j0 = r0 - i0;
+  const u32 la = (u32)(i1 - i0), len = (u32)(r1 - r0), lb = len - la;
+  for (u32 t = threadIdx.x; t < la; t += MC_THREADS) s[t] = a[i0 + t];
+  for (u32 t = threadIdx.x; t < lb; t += MC_THREADS) s[la + t] = b[j0 + t];
+  __syncthreads();
+  const u32 q0 = threadIdx.x * MC_ITEMS;
+  u64 v[MC_ITEMS];
+  if (q0 < len) {
+    u32 lo = q0 > lb ? q0 - lb : 0, hi = q0 < la ? q0 : la;
+    while (lo < hi) {
+      const u32 mid = (lo + hi) >> 1;
+      if (s[la + q0 - mid - 1] >= s[mid]) lo = mid + 1;
+      else hi = mid;
+    }
+    u32 ia = lo, ib = q0 - lo;
+#pragma unroll
+    for (int k = 0; k < MC_ITEMS; ++k) {
+      const u64 x = s[ia < la ? ia : 0], y = s[la + (ib < lb ? ib : 0)];
+      const bool ta = ia < la && (ib >= lb || x <= y);
+      v[k] = ta ? x : y;
+      ia += ta ? 1u : 0u;
+      ib += ta ? 0u : 1u;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < MC_ITEMS; ++k)
+    if (q0 + k < len) s[q0 + k] = v[k];
+  __syncthreads();
+  for (u32 t = threadIdx.x; t < len; t += MC_THREADS) out[r0 + t] = s[t];
+}
+
+int merge_copy_device(const u64* a, u64 na, const u64* b, u64 nb, u64* out, cudaStream_t st) {
+  const u64 n = na + nb;
+  if (n == 0) return PIP_OK;
+  const u64 blocks = (n + MC_TILE - 1) / MC_TILE;
+  if (blocks > 0x7fffffffull) return PIP_ERR_UNSUPPORTED;
+  merge_copy_kernel<<<(unsigned)blocks, MC_THREADS, 0, st>>>(a, na, b, nb, out);
+  PIP_CHECK_LAUNCH();
+  return PIP_OK;
+}
+
 static int merge_grid() { return num_sms(current_device()) * MG_CTAS_PER_SM; }
 
 size_t merge_workspace_bytes(u64 n, u64 split, u64 budget_words) {
