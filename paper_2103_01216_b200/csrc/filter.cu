@@ -1036,6 +1036,10 @@ int filter_device(u64* a, u64 n, const pip_pred* pred, u64* m_dev, void* scratch
     // pipeline, not the loads in flight, paces the filter
     if (cfg == 19) return launch_filter_ws2<13, 8, 3, 2, 4>(a, n, p, m_dev, L, st, dev);
     if (cfg == 20) return launch_filter_ws2<13, 8, 4, 3, 4>(a, n, p, m_dev, L, st, dev);
+    // compaction one tile behind the count (one more load in flight, the
+    // look-back gets one tile time): 11.0 ms with 3 or 4 look-back warps
+    if (cfg == 23) return launch_filter_ws2<13, 4, 3, 1>(a, n, p, m_dev, L, st, dev);
+    if (cfg == 24) return launch_filter_ws2<13, 4, 4, 1>(a, n, p, m_dev, L, st, dev);
 
     if (cfg == 11) return launch_filter_ws<14, 4>(a, n, p, m_dev, L, st, dev);
     if (cfg == 12) return launch_filter_ws<12, 4>(a, n, p, m_dev, L, st, dev);
