@@ -69,7 +69,7 @@ int bench_random_rmw(u64* buf, u64 n, u64 updates, u64 seed, float* ms, cudaStre
 size_t rp_workspace_bytes(u64 n, u64 prefix, int variant);
 int rp_device(u64* a, const u64* h, u64 n, u64 prefix, int variant, int debug,
               u64* counts_host, u64 rounds_cap, u64* trace_dev, void* ws, size_t ws_bytes,
-              pip_rp_stats* stats, cudaStream_t st);
+              pip_rp_stats* stats, cudaStream_t st, const RpProgress* prog = nullptr);
 size_t partition_workspace_bytes(u64 n);
 size_t list_contract_workspace_bytes(u64 n, u64 prefix, int rank);
 int tree_round_device(int step, u64* pa, u64* lf, u64* rt, const u64* p, u64* values, u64 lo, u64 hi,
@@ -582,8 +582,9 @@ int pip_random_permutation_u64_host(uint64_t* host_a, const uint64_t* host_h, ui
     if (stats_host) memset(stats_host, 0, sizeof(*stats_host));
     return PIP_OK;
   }
-  Stream s;
+  Stream s, cout;
   PIP_CUDA(s.create());
+  PIP_CUDA(cout.create());
   DevBuf a, h, ws;
   PIP_CUDA(a.alloc(n * 8));
   PIP_CUDA(h.alloc(n * 8));
@@ -591,11 +592,51 @@ int pip_random_permutation_u64_host(uint64_t* host_a, const uint64_t* host_h, ui
   PIP_CUDA(ws.alloc(wb));
   PIP_CUDA(cudaMemcpyAsync(a.p, host_a, n * 8, cudaMemcpyHostToDevice, s.s));
   PIP_CUDA(cudaMemcpyAsync(h.p, host_h, n * 8, cudaMemcpyHostToDevice, s.s));
+  // the final suffix a[top + 1 : n) goes back while the rounds run (in
+  // pieces of >= 2^22 words; PIP_RP_HOST_OVERLAP=0 turns it off)
+  const char* e = getenv("PIP_RP_HOST_OVERLAP");
+  const bool overlap = !(e && atoi(e) == 0) && n >= (1ull << 23);
+  struct Drain {
+    u64* host;
+    const u64* dev;
+    cudaStream_t st;
+    u64 lo;  // a[lo : n) has been queued
+    cudaError_t err;
+    static void hook(void* c, unsigned long long top) {
+      Drain* d = (Drain*)c;
+      const u64 from = top + 1;
+      if (from < d->lo && d->lo - from >= (1ull << 22) && d->err == cudaSuccess) {
+        d->err = cudaMemcpyAsync(d->host + from, d->dev + from, (d->lo - from) * 8,
+                                 cudaMemcpyDeviceToHost, d->st);
+        d->lo = from;
+      }
+    }
+  } drain{(u64*)host_a, (const u64*)a.p, cout.s, n, cudaSuccess};
+  unsigned long long* ph = nullptr;
+  RpProgress prog{};
+  if (overlap) {
+    PIP_CUDA(cudaHostAlloc((void**)&ph, 8, cudaHostAllocMapped));
+    *ph = n;
+    unsigned long long* pd = nullptr;
+    PIP_CUDA(cudaHostGetDevicePointer((void**)&pd, ph, 0));
+    prog = RpProgress{pd, ph, &Drain::hook, &drain};
+  }
+  struct HostFree {
+    unsigned long long* p;
+    ~HostFree() {
+      if (p) cudaFreeHost(p);
+    }
+  } hf{ph};
   int rc = rp_device((u64*)a.p, (const u64*)h.p, n, prefix, variant, 0, nullptr, 0, nullptr, ws.p,
-                     wb, stats_host, s.s);
-  if (rc) return rc;
-  PIP_CUDA(cudaMemcpyAsync(host_a, a.p, n * 8, cudaMemcpyDeviceToHost, s.s));
+                     wb, stats_host, s.s, overlap ? &prog : nullptr);
+  if (rc) {
+    cudaStreamSynchronize(cout.s);  // pending copies hold only final words
+    return rc;
+  }
+  PIP_CUDA(drain.err);
+  PIP_CUDA(cudaMemcpyAsync(host_a, a.p, drain.lo * 8, cudaMemcpyDeviceToHost, s.s));
   PIP_CUDA(cudaStreamSynchronize(s.s));
+  PIP_CUDA(cudaStreamSynchronize(cout.s));
   return PIP_OK;
 }
 

@@ -9,6 +9,18 @@ typedef unsigned int u32;
 
 namespace pip {
 
+// random permutation progress reporting (host-buffer entry point): the
+// kernel writes the highest pending id to `dev` (host-mapped; `host` is the
+// same word seen from the host) after every round; rp_device calls
+// hook(ctx, *host) while the rounds run
+struct RpProgress {
+  unsigned long long* dev;
+  volatile unsigned long long* host;
+  void (*hook)(void* ctx, unsigned long long top);
+  void* ctx;
+};
+
+
 // ---------------------------------------------------------------------------
 // error plumbing (host)
 void set_cuda_error(cudaError_t e);

@@ -71,6 +71,10 @@ struct RpArgs {
   u32* wcnt;
   u32* claimcnt;
   u64* round_counts;  // RP_ROUND_CHUNK
+  // host-mapped word (NULL = off): after every round, the highest id still
+  // pending; a[id + 1 : n) is final (iterate i only touches a[i] and
+  // a[H[i]] with H[i] <= i) and may be copied out while the rounds go on
+  u64* progress;
   u64* trace;
   RpGlobal* g;
   RpResume* resume;
@@ -759,6 +763,14 @@ __global__ void __launch_bounds__(RP_THREADS, 4) rp_kernel(RpArgs A) {
     }
     if (!grid_barrier(&g->sync, gen)) break;
     tick(3);
+    if (A.progress && b == 0 && tid == 0) {
+      // this round's list is descending (failures first, then the fresh
+      // window), so its head bounds every pending id; every CTA's swaps
+      // are ordered before the barrier above
+      const u64 top = R.fill ? (u64)__ldcg(ids_n) : (R.cursor >= 0 ? (u64)R.cursor : 0);
+      __threadfence_system();
+      *(volatile u64*)A.progress = top;
+    }
     if (++rounds_here >= A.rounds_limit) break;  // pause: host drains counts
   }
   if (b == 0 && tid == 0) {
@@ -860,7 +872,7 @@ int validate_counts(const u64* h, u64 n, u64* nonself, u64* invalid, void* scrat
 
 int rp_device(u64* a, const u64* h, u64 n, u64 prefix, int variant, int debug,
               u64* counts_host, u64 rounds_cap, u64* trace_dev, void* ws, size_t ws_bytes,
-              pip_rp_stats* stats, cudaStream_t st) {
+              pip_rp_stats* stats, cudaStream_t st, const RpProgress* prog) {
   if (variant < 0 || variant > 3 || prefix < 1) return PIP_ERR_INVALID_ARG;
   if (n >= 0xffffffffull) return PIP_ERR_UNSUPPORTED;
   pip_rp_stats S{};
@@ -914,6 +926,7 @@ int rp_device(u64* a, const u64* h, u64 n, u64 prefix, int variant, int debug,
   A.wcnt = (u32*)(w + Lrun.wcnt);
   A.claimcnt = (u32*)(w + Lrun.claimcnt);
   A.round_counts = (u64*)(w + Lrun.rcounts);
+  A.progress = prog ? prog->dev : nullptr;
   A.trace = trace_dev;
   A.g = (RpGlobal*)(w + Lrun.global);
   A.resume = (RpResume*)(w + Lrun.resume);
@@ -975,6 +988,11 @@ int rp_device(u64* a, const u64* h, u64 n, u64 prefix, int variant, int debug,
       default: rc = rp_run<PIP_RP_NAIVE>(A, (int)grid, st); break;
     }
     if (rc) return rc;
+    if (prog) {  // hand the final suffix to the caller while the rounds run
+      cudaError_t q;
+      while ((q = cudaStreamQuery(st)) == cudaErrorNotReady) prog->hook(prog->ctx, *prog->host);
+      if (q != cudaSuccess) PIP_CUDA(q);
+    }
     PIP_CUDA(cudaMemcpyAsync(&R, A.resume, sizeof(R), cudaMemcpyDeviceToHost, st));
     PIP_CUDA(cudaMemcpyAsync(&Gh, A.g, sizeof(Gh), cudaMemcpyDeviceToHost, st));
     PIP_CUDA(cudaStreamSynchronize(st));
