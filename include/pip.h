@@ -138,7 +138,13 @@ int pip_rotate_u64(uint64_t* a, uint64_t n, uint64_t o, void* scratch, size_t sc
  * return a[0:m) holds the words with keep(x), a[m:n) the others (multiset
  * preserved); m is written to device m_dev.  workspace holds
  * pip_partition_workspace_bytes(n) (O(n/4096) descriptors).  Stream-ordered.
- * pip_partition_u64_host: same on a host array (copies in/out; sync).     */
+ * pip_partition_u64_host: same on a host array (synchronous).  Above one
+ * host chunk (2^24 words) it is streamed: chunks are uploaded from both
+ * ends, partitioned on the device one by one, and their kept / dropped
+ * words written back to the front / back of the array as soon as the host
+ * range they land in has been uploaded (the arrangement inside each side
+ * differs from the device entry point's; the contract is the same).
+ * PIP_PARTITION_HOST_INPLACE=1: upload all, device partition, copy back. */
 size_t pip_partition_workspace_bytes(uint64_t n);
 int pip_partition_u64(uint64_t* a, uint64_t n, const pip_pred* pred, uint64_t* m_dev,
                       void* workspace, size_t workspace_bytes, void* stream);

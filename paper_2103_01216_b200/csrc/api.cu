@@ -380,6 +380,115 @@ int merge_host_stream(u64* host, u64 n, u64 split, u64 budget_words, int device)
   return PIP_OK;
 }
 
+// unstable partition over host memory, streamed: chunks are uploaded from
+// both ends of the array into a full device copy and partitioned there one
+// by one (partition_device on the chunk); trues go back to host[0 : m) from
+// the front, falses to host[m : n) from the back.  A word is written back
+// only into a host range whose upload has completed (front chunks open
+// [0, f), back chunks [bk, n)), so every host word is read before it is
+// overwritten; the next chunk is taken from the side whose open room is
+// smaller than the kept (resp. dropped) words expected to land there.
+int partition_host_stream(u64* host, u64 n, const pip_pred* pred, u64* m_out, int device) {
+  u64 chunk = host_chunk();
+  if (chunk > n) chunk = n;
+  const u64 nchunks = (n + chunk - 1) / chunk;
+  DevBuf d, ws, cnt;
+  PIP_CUDA(d.alloc(n * 8));
+  const size_t wb = partition_workspace_bytes(chunk);
+  PIP_CUDA(ws.alloc(wb));
+  PIP_CUDA(cnt.alloc(nchunks * 8));
+  u64* hc = nullptr;
+  PIP_CUDA(cudaMallocHost(&hc, nchunks * 8));
+  struct HostFree {
+    u64* p;
+    ~HostFree() { cudaFreeHost(p); }
+  } hf{hc};
+  Stream cin, comp, cout;
+  PIP_CUDA(cin.create());
+  PIP_CUDA(comp.create());
+  PIP_CUDA(cout.create());
+  std::vector<Event> in_done(nchunks), cnt_done(nchunks);
+  std::vector<u64> off_of(nchunks), len_of(nchunks), gate_f(nchunks), gate_b(nchunks);
+  u64* dv = (u64*)d.p;
+  u64 fi = 0, bi = nchunks - 1, issued = 0;  // next front / back chunk index
+  u64 f = 0, bk = n;                          // issued upload bounds
+  u64 t_known = 0, f_known = 0, w_known = 0, w_flight = 0;
+  auto issue = [&]() -> int {
+    const double rho = w_known ? (double)t_known / (double)w_known : 0.5;
+    const double t_est = (double)t_known + rho * (double)w_flight;
+    const double f_est = (double)f_known + (1.0 - rho) * (double)w_flight;
+    const bool front = (double)f - t_est <= (double)(n - bk) - f_est;
+    const u64 j = front ? fi++ : bi--;
+    const u64 off = j * chunk, len = (n - off) < chunk ? (n - off) : chunk;
+    const u64 k = issued++;
+    PIP_CUDA(in_done[k].create());
+    PIP_CUDA(cnt_done[k].create());
+    PIP_CUDA(cudaMemcpyAsync(dv + off, host + off, len * 8, cudaMemcpyHostToDevice, cin.s));
+    PIP_CUDA(cudaEventRecord(in_done[k].e, cin.s));
+    PIP_CUDA(cudaStreamWaitEvent(comp.s, in_done[k].e, 0));
+    if (int rc = partition_device(dv + off, len, pred, (u64*)cnt.p + k, ws.p, wb, comp.s)) return rc;
+    PIP_CUDA(cudaMemcpyAsync(hc + k, (u64*)cnt.p + k, 8, cudaMemcpyDeviceToHost, comp.s));
+    PIP_CUDA(cudaEventRecord(cnt_done[k].e, comp.s));
+    if (front) f = off + len;
+    else bk = off;
+    off_of[k] = off;
+    len_of[k] = len;
+    gate_f[k] = f == bk ? n : f;  // once both ends meet every word is open
+    gate_b[k] = f == bk ? 0 : bk;
+    w_flight += len;
+    return PIP_OK;
+  };
+  struct Piece {
+    u64 off, len;
+  };
+  std::vector<Piece> pt, pf;  // pending trues / falses, in production order
+  size_t pt_head = 0, pf_head = 0;
+  u64 wt = 0, wf = 0;  // words written back: trues from 0 up, falses from n down
+  auto flush = [&](u64 gf, u64 gb) -> int {
+    while (pt_head < pt.size() && wt < gf) {
+      Piece& q = pt[pt_head];
+      const u64 x = q.len < gf - wt ? q.len : gf - wt;
+      PIP_CUDA(cudaMemcpyAsync(host + wt, dv + q.off, x * 8, cudaMemcpyDeviceToHost, cout.s));
+      wt += x;
+      q.off += x;
+      q.len -= x;
+      if (q.len == 0) ++pt_head;
+    }
+    while (pf_head < pf.size() && n - wf > gb) {
+      Piece& q = pf[pf_head];
+      const u64 room = n - wf - gb;
+      const u64 x = q.len < room ? q.len : room;
+      PIP_CUDA(cudaMemcpyAsync(host + (n - wf - x), dv + q.off + (q.len - x), x * 8,
+                               cudaMemcpyDeviceToHost, cout.s));
+      wf += x;
+      q.len -= x;
+      if (q.len == 0) ++pf_head;
+    }
+    return PIP_OK;
+  };
+  const u64 ahead = (u64)host_nbuf();
+  while (issued < nchunks && issued < ahead)
+    if (int rc = issue()) return rc;
+  for (u64 k = 0; k < nchunks; ++k) {
+    PIP_CUDA(cudaEventSynchronize(cnt_done[k].e));
+    const u64 t = hc[k], len = len_of[k];
+    t_known += t;
+    f_known += len - t;
+    w_known += len;
+    w_flight -= len;
+    if (t) pt.push_back(Piece{off_of[k], t});
+    if (len - t) pf.push_back(Piece{off_of[k] + t, len - t});
+    // chunk k's partition has finished, so every upload issued up to it has landed
+    if (int rc = flush(gate_f[k], gate_b[k])) return rc;
+    if (issued < nchunks)
+      if (int rc = issue()) return rc;
+  }
+  if (wt != t_known || wf != f_known) return PIP_ERR_CUDA;  // every word placed
+  PIP_CUDA(cudaStreamSynchronize(cout.s));
+  *m_out = t_known;
+  return PIP_OK;
+}
+
 }  // namespace pip
 
 using namespace pip;
@@ -503,6 +612,8 @@ int pip_partition_u64_host(uint64_t* host_a, uint64_t n, const pip_pred* pred, u
     *m_out = 0;
     return PIP_OK;
   }
+  const char* e = getenv("PIP_PARTITION_HOST_INPLACE");
+  if (!(e && atoi(e)) && n > host_chunk()) return partition_host_stream((u64*)host_a, n, pred, (u64*)m_out, device);
   Stream s;
   PIP_CUDA(s.create());
   DevBuf a, ws, m;
