@@ -1,5 +1,5 @@
 set -u
-o=gpurun_out/v2
+o=gpurun_out/${OUT:-v2}
 mkdir -p $o
 nvidia-smi > $o/gpu.txt 2>&1
 timeout 1500 python -m pytest tests -m gpu -x -q > $o/gpu_tests.log 2>&1; echo "tests rc=$?" >> $o/gpu_tests.log
