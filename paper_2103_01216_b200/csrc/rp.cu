@@ -33,6 +33,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
+#include <chrono>
+#include <thread>
 #include "sync.cuh"
 
 namespace pip {
@@ -990,7 +992,11 @@ int rp_device(u64* a, const u64* h, u64 n, u64 prefix, int variant, int debug,
     if (rc) return rc;
     if (prog) {  // hand the final suffix to the caller while the rounds run
       cudaError_t q;
-      while ((q = cudaStreamQuery(st)) == cudaErrorNotReady) prog->hook(prog->ctx, *prog->host);
+      static const int poll_us = getenv("PIP_RP_POLL_US") ? atoi(getenv("PIP_RP_POLL_US")) : 50;
+      while ((q = cudaStreamQuery(st)) == cudaErrorNotReady) {
+        prog->hook(prog->ctx, *prog->host);
+        if (poll_us > 0) std::this_thread::sleep_for(std::chrono::microseconds(poll_us));
+      }
       if (q != cudaSuccess) PIP_CUDA(q);
     }
     PIP_CUDA(cudaMemcpyAsync(&R, A.resume, sizeof(R), cudaMemcpyDeviceToHost, st));
