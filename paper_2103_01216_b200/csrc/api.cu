@@ -159,6 +159,12 @@ struct Event {
   cudaError_t create() { return cudaEventCreateWithFlags(&e, cudaEventDisableTiming); }
 };
 
+// the device entry points' predicate checks, made before a host entry point
+// queues any transfer (so an invalid predicate never leaves copies in flight)
+static bool pred_ok(const pip_pred* p) {
+  return p && p->kind <= PIP_PRED_EQ && !(p->kind == PIP_PRED_MOD_EQ && p->a == 0);
+}
+
 // words per pipeline stage of the host-buffer entry points (PIP_HOST_CHUNK_LOG2)
 static u64 host_chunk() {
   static u64 c = 0;
@@ -555,7 +561,7 @@ int pip_count_u64(const uint64_t* a, uint64_t n, const pip_pred* pred, uint64_t*
 
 int pip_filter_u64_host(uint64_t* host_a, uint64_t n, const pip_pred* pred, uint64_t* m_out,
                         int device) {
-  if (!pred || (n && !host_a)) return PIP_ERR_INVALID_ARG;
+  if (!pred_ok(pred) || (n && !host_a)) return PIP_ERR_INVALID_ARG;
   return filter_host((u64*)host_a, n, pred, (u64*)m_out, device);
 }
 
@@ -606,7 +612,7 @@ int pip_partition_u64(uint64_t* a, uint64_t n, const pip_pred* pred, uint64_t* m
 
 int pip_partition_u64_host(uint64_t* host_a, uint64_t n, const pip_pred* pred, uint64_t* m_out,
                            int device) {
-  if (!pred || !m_out || (n && !host_a)) return PIP_ERR_INVALID_ARG;
+  if (!pred_ok(pred) || !m_out || (n && !host_a)) return PIP_ERR_INVALID_ARG;
   PIP_CUDA(cudaSetDevice(device));
   if (n == 0) {
     *m_out = 0;

@@ -80,3 +80,19 @@ def test_workspace_sizing_is_sublinear():
         b = EpsilonConfig(0.5).prefix_words(n)
         words = lib.pip_merge_workspace_bytes(n, n // 2, b) / 8
         assert 0 < words <= b, (n, words / b)
+
+
+def test_host_entry_points_reject_bad_predicates_before_any_transfer():
+    # checked before the device is touched, so this runs without a GPU
+    import numpy as np
+
+    from paper_2103_01216_b200 import _lib
+
+    lib = _lib.load()
+    a = np.arange(10, dtype=np.uint64)
+    m = C.c_uint64(0)
+    for kind, pa in ((99, 0), (2, 0)):  # unknown kind; x % 0
+        p = _lib.PipPred(kind, 0, pa, 0)
+        assert lib.pip_filter_u64_host(a.ctypes.data, len(a), C.byref(p), C.byref(m), 0) == 1
+        assert lib.pip_partition_u64_host(a.ctypes.data, len(a), C.byref(p), C.byref(m), 0) == 1
+    assert np.array_equal(a, np.arange(10, dtype=np.uint64))
