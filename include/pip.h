@@ -151,10 +151,22 @@ int pip_partition_u64(uint64_t* a, uint64_t n, const pip_pred* pred, uint64_t* m
 int pip_partition_u64_host(uint64_t* host_a, uint64_t n, const pip_pred* pred, uint64_t* m_out,
                            int device);
 
+/* ---- one quicksort level: pip_partition_u64 over nseg disjoint segments
+ * (strong.py:431-452, relaxed.py:347-369, one call per level of the
+ * recursion instead of one per node).  Segment g = a[seg_lo[g] :
+ * seg_lo[g] + seg_len[g]) is partitioned by (x kind operand[g]) with kind in
+ * PIP_PRED_LT..PIP_PRED_EQ; its kept count goes to device m_dev[g].
+ * seg_lo / seg_len / operand are HOST arrays; workspace holds
+ * pip_partition_workspace_bytes(max seg_len).  Stream-ordered.            */
+int pip_partition_segments_u64(uint64_t* a, const uint64_t* seg_lo, const uint64_t* seg_len,
+                               const uint64_t* operand, uint32_t kind, uint64_t* m_dev,
+                               uint64_t nseg, void* workspace, size_t workspace_bytes,
+                               void* stream);
+
 /* ---- quicksort leaves: the base case of strong.quicksort_strong /
  * relaxed.quicksort_relaxed (strong.py:453-454, relaxed.py:370-371):
  * sorts a[seg_lo[g] : seg_lo[g] + seg_len[g]) ascending (unsigned) for every
- * g < nseg; seg_len[g] <= 8192, segments disjoint; device arrays.  The
+ * g < nseg; seg_len[g] <= 65536, segments disjoint; device arrays.  The
  * recursion above it partitions with pip_partition_u64.                   */
 int pip_sort_segments_u64(uint64_t* a, const uint64_t* seg_lo_dev, const uint32_t* seg_len_dev,
                           uint64_t nseg, void* stream);

@@ -610,6 +610,21 @@ int pip_partition_u64(uint64_t* a, uint64_t n, const pip_pred* pred, uint64_t* m
                           (cudaStream_t)stream);
 }
 
+int pip_partition_segments_u64(uint64_t* a, const uint64_t* seg_lo, const uint64_t* seg_len,
+                               const uint64_t* operand, uint32_t kind, uint64_t* m_dev,
+                               uint64_t nseg, void* workspace, size_t workspace_bytes,
+                               void* stream) {
+  if (nseg && (!a || !seg_lo || !seg_len || !operand || !m_dev)) return PIP_ERR_INVALID_ARG;
+  if (kind < PIP_PRED_LT || kind > PIP_PRED_EQ) return PIP_ERR_INVALID_ARG;
+  for (uint64_t g = 0; g < nseg; ++g) {
+    pip_pred p{kind, 0, operand[g], 0};
+    const int rc = partition_device((u64*)a + seg_lo[g], seg_len[g], &p, (u64*)m_dev + g,
+                                    workspace, workspace_bytes, (cudaStream_t)stream);
+    if (rc) return rc;
+  }
+  return PIP_OK;
+}
+
 int pip_partition_u64_host(uint64_t* host_a, uint64_t n, const pip_pred* pred, uint64_t* m_out,
                            int device) {
   if (!pred_ok(pred) || !m_out || (n && !host_a)) return PIP_ERR_INVALID_ARG;

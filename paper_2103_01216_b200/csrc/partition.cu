@@ -409,9 +409,68 @@ __global__ void __launch_bounds__(PT_THREADS) part_swap_kernel(u64* a, u64 n, De
 
 // ---------------------------------------------------------------- leaf sort
 // quicksort leaves (strong.quicksort_strong's base case a[lo:hi].sort(),
-// strong.py:453-454): one CTA per segment of <= 8192 words, bitonic sort in
-// shared memory (padded to a power of two with 2^64-1: ties are invisible)
-static constexpr u32 SEG_MAX = 8192;
+// strong.py:453-454): one CTA per segment of <= 65536 words.  Bitonic sort
+// in its all-ascending "flip" form: every compare-exchange puts the max at
+// the higher index, so the virtual +inf padding above the segment's length
+// never moves and partners past the end are simply skipped.  Stages whose
+// pairs lie inside an aligned 8192-word chunk run in shared memory (one
+// chunk at a time); the wider flip / half-cleaner stages of segments longer
+// than one chunk run on global memory (L2-resident: the CTA owns the
+// segment, __syncthreads orders the passes).
+static constexpr u32 SEG_CHUNK = 8192;
+static constexpr u32 SEG_MAX = 65536;
+
+__device__ __forceinline__ void cas_smem(u64* ss, u32 l, u32 r) {
+  const u64 x = ss[l], y = ss[r];
+  if (x > y) {
+    ss[l] = y;
+    ss[r] = x;
+  }
+}
+
+// stages [k0 .. C] of the flip network on one chunk in shared memory
+// (k0 = 2: full local sort; k0 > C: only the half-cleaners below C)
+__device__ void seg_chunk_pass(u64* base, u32 c0, u32 L, u32 C, u32 k_lo, u32 k_hi, u64* ss) {
+  const u32 tid = threadIdx.x;
+  for (u32 i = tid; i < C; i += 1024) ss[i] = c0 + i < L ? base[c0 + i] : ~0ull;
+  __syncthreads();
+  for (u32 k = k_lo; k <= k_hi; k <<= 1) {
+    const u32 half = k >> 1;
+    for (u32 i = tid; i < C / 2; i += 1024) {
+      const u32 pos = i & (half - 1), blk = (i - pos) << 1;
+      cas_smem(ss, blk + pos, blk + k - 1 - pos);
+    }
+    __syncthreads();
+    for (u32 j = k >> 2; j > 0; j >>= 1) {
+      for (u32 i = tid; i < C / 2; i += 1024) {
+        const u32 l = 2 * i - (i & (j - 1));
+        cas_smem(ss, l, l + j);
+      }
+      __syncthreads();
+    }
+  }
+  if (k_lo > k_hi) {  // half-cleaners j = C/2 .. 1 only
+    for (u32 j = C >> 1; j > 0; j >>= 1) {
+      for (u32 i = tid; i < C / 2; i += 1024) {
+        const u32 l = 2 * i - (i & (j - 1));
+        cas_smem(ss, l, l + j);
+      }
+      __syncthreads();
+    }
+  }
+  for (u32 i = tid; c0 + i < L && i < C; i += 1024) base[c0 + i] = ss[i];
+  __syncthreads();
+}
+
+__device__ __forceinline__ void cas_glob(u64* base, u32 l, u32 r, u32 L) {
+  if (r < L) {
+    const u64 x = base[l], y = base[r];
+    if (x > y) {
+      base[l] = y;
+      base[r] = x;
+    }
+  }
+}
 
 __global__ void __launch_bounds__(1024) segsort_kernel(u64* a, const u64* __restrict__ seg_lo,
                                                        const u32* __restrict__ seg_len, u64 nseg) {
@@ -419,34 +478,35 @@ __global__ void __launch_bounds__(1024) segsort_kernel(u64* a, const u64* __rest
   const u32 tid = threadIdx.x;
   for (u64 g = blockIdx.x; g < nseg; g += gridDim.x) {
     const u32 L = seg_len[g];
+    if (L < 2) continue;
     u64* base = a + seg_lo[g];
     u32 P = 2;
     while (P < L) P <<= 1;
-    for (u32 i = tid; i < P; i += 1024) ss[i] = i < L ? base[i] : ~0ull;
-    __syncthreads();
-    for (u32 k = 2; k <= P; k <<= 1) {
-      for (u32 j = k >> 1; j > 0; j >>= 1) {
+    const u32 C = P < SEG_CHUNK ? P : SEG_CHUNK;
+    for (u32 c0 = 0; c0 < L; c0 += C) seg_chunk_pass(base, c0, L, C, 2, C, ss);
+    for (u32 k = 2 * C; k <= P; k <<= 1) {
+      const u32 half = k >> 1;
+      for (u32 i = tid; i < P / 2; i += 1024) {
+        const u32 pos = i & (half - 1), blk = (i - pos) << 1;
+        cas_glob(base, blk + pos, blk + k - 1 - pos, L);
+      }
+      __syncthreads();
+      for (u32 j = k >> 2; j >= C; j >>= 1) {
         for (u32 i = tid; i < P / 2; i += 1024) {
-          const u32 l = 2 * i - (i & (j - 1)), r = l + j;
-          const bool up = (l & k) == 0;
-          const u64 x = ss[l], y = ss[r];
-          if ((x > y) == up) {
-            ss[l] = y;
-            ss[r] = x;
-          }
+          const u32 l = 2 * i - (i & (j - 1));
+          cas_glob(base, l, l + j, L);
         }
         __syncthreads();
       }
+      for (u32 c0 = 0; c0 < L; c0 += C) seg_chunk_pass(base, c0, L, C, 2 * C, C, ss);
     }
-    for (u32 i = tid; i < L; i += 1024) base[i] = ss[i];
-    __syncthreads();
   }
 }
 
 int sort_segments_device(u64* a, const u64* seg_lo, const u32* seg_len, u64 nseg, cudaStream_t st) {
   if (nseg == 0) return PIP_OK;
   if (!a || !seg_lo || !seg_len) return PIP_ERR_INVALID_ARG;
-  const size_t smem = SEG_MAX * 8;
+  const size_t smem = SEG_CHUNK * 8;
   PIP_CUDA(cudaFuncSetAttribute(segsort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int sms = num_sms(current_device());
   const u64 g = nseg < (u64)sms * 3 ? nseg : (u64)sms * 3;

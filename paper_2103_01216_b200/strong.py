@@ -255,7 +255,7 @@ def partition_unstable(a, pred, n: int | None = None) -> int:
     return _partition_impl(a, pred, n, meter_workspace=False)
 
 
-QS_LEAF = 8192  # leaves: one CTA sorts each in shared memory (pip_sort_segments_u64)
+QS_LEAF = 65536  # leaves: one CTA sorts each (pip_sort_segments_u64, shared-memory chunks)
 
 
 def _quicksort_impl(a, rng, salt_of, meter_workspace: bool) -> None:
@@ -286,38 +286,52 @@ def _quicksort_impl(a, rng, salt_of, meter_workspace: bool) -> None:
             keep = torch.empty(max(wb, 16), dtype=torch.uint8, device=f"cuda:{w.device}")
             ws_ptr, buf = keep.data_ptr(), None
         try:
-            m = small_device_words(1, w.device)
             words = w.obj.view(torch.int64) if w.obj.dtype != torch.int64 else w.obj
+            dev = f"cuda:{w.device}"
 
-            def part(lo: int, hi: int, p) -> int:
-                d = p.descriptor()
-                _lib.check(lib.pip_partition_u64(w.ptr + 8 * lo, hi - lo, C.byref(d), m.data_ptr(),
-                                                 ws_ptr, wb, st), "partition")
-                return int(m.item())
+            def part_all(los, lens, pvs, kind, mbuf) -> list[int]:
+                # every partition of the level in one call (they share the
+                # workspace stream-ordered); one read of all counts
+                k = len(los)
+                arr = (C.c_uint64 * k)
+                _lib.check(lib.pip_partition_segments_u64(w.ptr, arr(*los), arr(*lens), arr(*pvs),
+                                                          kind, mbuf.data_ptr(), k, ws_ptr, wb, st),
+                           "partition")
+                return mbuf.cpu().tolist()
 
             leaves_lo: list[int] = []
             leaves_len: list[int] = []
-            stack = [(0, n, 0)]
-            while stack:
-                lo, hi, depth = stack.pop()
-                while hi - lo > QS_LEAF:
-                    salt = salt_of(depth)
-                    pv = int(words[lo + rng.word(((lo << 21) ^ hi) + salt) % (hi - lo)].item()) & M64
-                    less = part(lo, hi, lt(pv))
-                    equal = part(lo + less, hi, eq(pv))
-                    left_hi, right_lo = lo + less, lo + less + equal
-                    depth += 1
-                    if left_hi - lo < hi - right_lo:
-                        stack.append((right_lo, hi, depth))
-                        hi = left_hi
-                    else:
-                        stack.append((lo, left_hi, depth))
-                        lo = right_lo
-                if hi - lo > 1:
-                    leaves_lo.append(lo)
-                    leaves_len.append(hi - lo)
+            # Level-batched recursion: the segments of one depth are disjoint,
+            # so their pivots are gathered with one read and their partitions
+            # queued back to back -- three host syncs per level, not per
+            # segment.  Pivot rule and per-segment depth as in the sequential
+            # recursion (strong.py:431-454).
+            level = [(0, n, 0)]
+            while level:
+                big = []
+                for lo, hi, depth in level:
+                    if hi - lo > QS_LEAF:
+                        big.append((lo, hi, depth))
+                    elif hi - lo > 1:
+                        leaves_lo.append(lo)
+                        leaves_len.append(hi - lo)
+                if not big:
+                    break
+                idx = [lo + rng.word(((lo << 21) ^ hi) + salt_of(depth)) % (hi - lo)
+                       for lo, hi, depth in big]
+                pvs = [int(v) & M64 for v in
+                       words[torch.tensor(idx, dtype=torch.int64, device=dev)].cpu().tolist()]
+                mbuf = torch.empty(len(big), dtype=torch.int64, device=dev)
+                less = part_all([lo for lo, _, _ in big], [hi - lo for lo, hi, _ in big], pvs,
+                                lt(0).descriptor().kind, mbuf)
+                equal = part_all([lo + le for (lo, _, _), le in zip(big, less)],
+                                 [hi - lo - le for (lo, hi, _), le in zip(big, less)], pvs,
+                                 eq(0).descriptor().kind, mbuf)
+                level = []
+                for (lo, hi, depth), le, eqn in zip(big, less, equal):
+                    level.append((lo, lo + le, depth + 1))
+                    level.append((lo + le + eqn, hi, depth + 1))
             if leaves_lo:
-                dev = f"cuda:{w.device}"
                 slo = torch.tensor(leaves_lo, dtype=torch.int64, device=dev)
                 sln = torch.tensor(leaves_len, dtype=torch.int32, device=dev)
                 _lib.check(lib.pip_sort_segments_u64(w.ptr, slo.data_ptr(), sln.data_ptr(),
@@ -335,8 +349,8 @@ def quicksort_strong(a, rng) -> None:
 
     ``rng`` is a :class:`~paper_2103_01216_b200.runtime.Rng`; pivots follow
     the reference's rule (its depth-cap restarts only change pivots, never
-    the sorted output).  Leaves of <= 8192 words are sorted on the GPU in
-    shared memory (the reference's base case is ``a[lo:hi].sort()``).
+    the sorted output).  Leaves of <= 65536 words are sorted on the GPU by
+    one CTA each (the reference's base case is ``a[lo:hi].sort()``).
     """
     _quicksort_impl(a, rng, lambda depth: 0, meter_workspace=False)
 

@@ -181,3 +181,36 @@ def test_quicksort_relaxed_metered(pip):
     rep = pip.meter_scope(meter, 8 * b, lambda: pip.relaxed.quicksort_relaxed(a, pip.Rng(3), cfg))
     assert meter.current_words == 0 and rep.peak_words <= 8 * b
     assert np.array_equal(a, np.sort(x))
+
+
+def test_sort_segments_ragged(pip):
+    # the quicksort base case (strong.py:453-454) on its own: disjoint ragged
+    # segments of 2 .. 65536 words (one and several shared-memory chunks,
+    # non-powers of two), words between them untouched
+    import ctypes as C
+
+    import torch
+
+    from paper_2103_01216_b200 import _lib
+
+    lens = [2, 3, 255, 8191, 8192, 8193, 12345, 16384, 40000, 65535, 65536, 1]
+    gap = 7
+    los, pos = [], 0
+    for ln in lens:
+        los.append(pos)
+        pos += ln + gap
+    rng = np.random.default_rng(11)
+    x = rng.integers(0, 1 << 64, size=pos, dtype=np.uint64)
+    x[: pos // 3] = rng.integers(0, 4, size=pos // 3, dtype=np.uint64)
+    x[pos // 2: pos // 2 + 5000] = np.uint64((1 << 64) - 1)
+    ref = x.copy()
+    for lo, ln in zip(los, lens):
+        ref[lo: lo + ln] = np.sort(ref[lo: lo + ln])
+    t = dev(x)
+    slo = torch.tensor(los, dtype=torch.int64, device="cuda")
+    sln = torch.tensor(lens, dtype=torch.int32, device="cuda")
+    lib = _lib.load()
+    st = torch.cuda.current_stream().cuda_stream
+    assert lib.pip_sort_segments_u64(t.data_ptr(), slo.data_ptr(), sln.data_ptr(),
+                                     C.c_uint64(len(lens)), st) == 0
+    assert np.array_equal(host(t), ref)

@@ -84,6 +84,6 @@ pip.strong.quicksort_strong(t, pip.Rng(5))
 u = t.cpu().numpy().view(np.uint64)
 print(json.dumps({"op": "quicksort_strong", "n": n, "ms": ms, "elements_per_s": n / (ms / 1e3),
                   "verified": bool(np.all(u[1:] >= u[:-1])),
-                  "note": "host recursion over the GPU partition (one sync per partition) + "
+                  "note": "level-batched host recursion over the GPU partition (3 syncs per level) + "
                           "one shared-memory bitonic launch for the <= 8192-word leaves"}),
       flush=True)
