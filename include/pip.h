@@ -166,7 +166,7 @@ int pip_partition_segments_u64(uint64_t* a, const uint64_t* seg_lo, const uint64
 /* ---- quicksort leaves: the base case of strong.quicksort_strong /
  * relaxed.quicksort_relaxed (strong.py:453-454, relaxed.py:370-371):
  * sorts a[seg_lo[g] : seg_lo[g] + seg_len[g]) ascending (unsigned) for every
- * g < nseg; seg_len[g] <= 65536, segments disjoint; device arrays.  The
+ * g < nseg; seg_len[g] <= 2^20, segments disjoint; device arrays.  The
  * recursion above it partitions with pip_partition_u64.                   */
 int pip_sort_segments_u64(uint64_t* a, const uint64_t* seg_lo_dev, const uint32_t* seg_len_dev,
                           uint64_t nseg, void* stream);

@@ -409,7 +409,7 @@ __global__ void __launch_bounds__(PT_THREADS) part_swap_kernel(u64* a, u64 n, De
 
 // ---------------------------------------------------------------- leaf sort
 // quicksort leaves (strong.quicksort_strong's base case a[lo:hi].sort(),
-// strong.py:453-454): one CTA per segment of <= 65536 words.  Bitonic sort
+// strong.py:453-454): one CTA per segment of <= 2^20 words.  Bitonic sort
 // in its all-ascending "flip" form: every compare-exchange puts the max at
 // the higher index, so the virtual +inf padding above the segment's length
 // never moves and partners past the end are simply skipped.  Stages whose
@@ -418,7 +418,7 @@ __global__ void __launch_bounds__(PT_THREADS) part_swap_kernel(u64* a, u64 n, De
 // than one chunk run on global memory (L2-resident: the CTA owns the
 // segment, __syncthreads orders the passes).
 static constexpr u32 SEG_CHUNK = 8192;
-static constexpr u32 SEG_MAX = 65536;
+static constexpr u32 SEG_MAX = 1u << 20;
 
 __device__ __forceinline__ void cas_smem(u64* ss, u32 l, u32 r) {
   const u64 x = ss[l], y = ss[r];

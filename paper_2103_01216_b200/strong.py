@@ -21,6 +21,7 @@ descriptors plus one 64 KiB chunk per SM of unmetered device scratch
 from __future__ import annotations
 
 import ctypes as C
+import os
 import operator
 from dataclasses import dataclass
 
@@ -255,7 +256,8 @@ def partition_unstable(a, pred, n: int | None = None) -> int:
     return _partition_impl(a, pred, n, meter_workspace=False)
 
 
-QS_LEAF = 65536  # leaves: one CTA sorts each (pip_sort_segments_u64, shared-memory chunks)
+# leaves: one CTA sorts each (pip_sort_segments_u64, <= 2^20 words)
+QS_LEAF = int(os.environ.get("PIP_QS_LEAF", 1 << 19))
 
 
 def _quicksort_impl(a, rng, salt_of, meter_workspace: bool) -> None:
@@ -349,7 +351,7 @@ def quicksort_strong(a, rng) -> None:
 
     ``rng`` is a :class:`~paper_2103_01216_b200.runtime.Rng`; pivots follow
     the reference's rule (its depth-cap restarts only change pivots, never
-    the sorted output).  Leaves of <= 65536 words are sorted on the GPU by
+    the sorted output).  Leaves of <= 2^19 words are sorted on the GPU by
     one CTA each (the reference's base case is ``a[lo:hi].sort()``).
     """
     _quicksort_impl(a, rng, lambda depth: 0, meter_workspace=False)

@@ -185,7 +185,7 @@ def test_quicksort_relaxed_metered(pip):
 
 def test_sort_segments_ragged(pip):
     # the quicksort base case (strong.py:453-454) on its own: disjoint ragged
-    # segments of 2 .. 65536 words (one and several shared-memory chunks,
+    # segments of 2 .. 2^20 words (one and several shared-memory chunks,
     # non-powers of two), words between them untouched
     import ctypes as C
 
@@ -193,7 +193,7 @@ def test_sort_segments_ragged(pip):
 
     from paper_2103_01216_b200 import _lib
 
-    lens = [2, 3, 255, 8191, 8192, 8193, 12345, 16384, 40000, 65535, 65536, 1]
+    lens = [2, 3, 255, 8191, 8192, 8193, 12345, 16384, 40000, 65535, 65536, 1, 262147, 1 << 20]
     gap = 7
     los, pos = [], 0
     for ln in lens:
