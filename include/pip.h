@@ -171,6 +171,13 @@ int pip_partition_segments_u64(uint64_t* a, const uint64_t* seg_lo, const uint64
 int pip_sort_segments_u64(uint64_t* a, const uint64_t* seg_lo_dev, const uint32_t* seg_len_dev,
                           uint64_t nseg, void* stream);
 
+/* pip_sort_segments_grid_u64: the same contract for segments of up to
+ * 2^28 words; max_len >= every seg_len[g] (host value).  The network is
+ * spread over the grid (one launch per stage wider than 8192 words), so a
+ * few long segments still use every SM.                                   */
+int pip_sort_segments_grid_u64(uint64_t* a, const uint64_t* seg_lo_dev, const uint32_t* seg_len_dev,
+                               uint64_t nseg, uint64_t max_len, void* stream);
+
 /* ---- list contraction / ranking: contraction.list_contract / list_rank ---- *
  * (contraction.py:264-365 on detres.run_rounds, detres.py:256-307).  next /
  * prev / p are device u64[n] (NIL = 2^64-1 ends a chain; p distinct

@@ -79,6 +79,8 @@ int list_contract_device(u64* nxt, u64* prv, const u64* p, u64 n, u64 prefix, in
                          u64* committed_per_round_host, u64 rounds_cap, u64* rounds_out,
                          u64* trace_host, u64* splice_host, void* ws, size_t ws_bytes, cudaStream_t st);
 int sort_segments_device(u64* a, const u64* seg_lo, const u32* seg_len, u64 nseg, cudaStream_t st);
+int sort_segments_grid_device(u64* a, const u64* seg_lo, const u32* seg_len, u64 nseg,
+                              u64 max_len, cudaStream_t st);
 int partition_device(u64* a, u64 n, const pip_pred* pred, u64* m_dev, void* ws, size_t ws_bytes,
                      cudaStream_t st);
 size_t merge_workspace_bytes(u64 n, u64 split, u64 budget_words);
@@ -602,6 +604,12 @@ int pip_sort_segments_u64(uint64_t* a, const uint64_t* seg_lo_dev, const uint32_
                           uint64_t nseg, void* stream) {
   return sort_segments_device((u64*)a, (const u64*)seg_lo_dev, seg_len_dev, nseg,
                               (cudaStream_t)stream);
+}
+
+int pip_sort_segments_grid_u64(uint64_t* a, const uint64_t* seg_lo_dev, const uint32_t* seg_len_dev,
+                               uint64_t nseg, uint64_t max_len, void* stream) {
+  return sort_segments_grid_device((u64*)a, (const u64*)seg_lo_dev, seg_len_dev, nseg, max_len,
+                                   (cudaStream_t)stream);
 }
 
 int pip_partition_u64(uint64_t* a, uint64_t n, const pip_pred* pred, uint64_t* m_dev,

@@ -419,6 +419,7 @@ __global__ void __launch_bounds__(PT_THREADS) part_swap_kernel(u64* a, u64 n, De
 // segment, __syncthreads orders the passes).
 static constexpr u32 SEG_CHUNK = 8192;
 static constexpr u32 SEG_MAX = 1u << 20;
+static constexpr u64 SEG_MAX_GRID = 1ull << 28;
 
 __device__ __forceinline__ void cas_smem(u64* ss, u32 l, u32 r) {
   const u64 x = ss[l], y = ss[r];
@@ -501,6 +502,83 @@ __global__ void __launch_bounds__(1024) segsort_kernel(u64* a, const u64* __rest
       for (u32 c0 = 0; c0 < L; c0 += C) seg_chunk_pass(base, c0, L, C, 2 * C, C, ss);
     }
   }
+}
+
+// The same network spread over the grid (for leaves longer than one chunk):
+// blockIdx.x = segment, blockIdx.y = chunk / pair range inside it.  One
+// launch sorts every chunk of every segment locally, then each wider stage
+// k is one launch for the flip stage, one per half-cleaner distance >= one
+// chunk, and one for the chunk-local cleaners -- every SM busy whatever the
+// number of segments.
+__device__ __forceinline__ u32 seg_pow2(u32 L) {
+  u32 P = 2;
+  while (P < L) P <<= 1;
+  return P;
+}
+
+__global__ void __launch_bounds__(1024) segsort_local_kernel(u64* a, const u64* __restrict__ seg_lo,
+                                                             const u32* __restrict__ seg_len, u32 k) {
+  extern __shared__ __align__(16) u64 ss[];
+  const u32 L = seg_len[blockIdx.x];
+  if (L < 2) return;
+  const u32 P = seg_pow2(L);
+  const u32 C = P < SEG_CHUNK ? P : SEG_CHUNK;
+  const u32 c0 = blockIdx.y * C;
+  if (c0 >= L) return;
+  if (k == 0) {
+    seg_chunk_pass(a + seg_lo[blockIdx.x], c0, L, C, 2, C, ss);
+  } else if (k <= P) {
+    seg_chunk_pass(a + seg_lo[blockIdx.x], c0, L, C, 2 * C, C, ss);
+  }
+}
+
+__global__ void __launch_bounds__(1024) segsort_global_kernel(u64* a, const u64* __restrict__ seg_lo,
+                                                              const u32* __restrict__ seg_len, u32 k,
+                                                              u32 j) {
+  const u32 L = seg_len[blockIdx.x];
+  if (L < 2) return;
+  const u32 P = seg_pow2(L);
+  if (k > P) return;
+  const u32 i0 = blockIdx.y * (SEG_CHUNK / 2);
+  if (i0 >= P / 2) return;
+  u64* base = a + seg_lo[blockIdx.x];
+  const u32 half = k >> 1;
+  for (u32 i = i0 + threadIdx.x; i < i0 + SEG_CHUNK / 2; i += 1024) {
+    if (j == 0) {
+      const u32 pos = i & (half - 1), blk = (i - pos) << 1;
+      cas_glob(base, blk + pos, blk + k - 1 - pos, L);
+    } else {
+      const u32 l = 2 * i - (i & (j - 1));
+      cas_glob(base, l, l + j, L);
+    }
+  }
+}
+
+int sort_segments_grid_device(u64* a, const u64* seg_lo, const u32* seg_len, u64 nseg,
+                              u64 max_len, cudaStream_t st) {
+  if (nseg == 0) return PIP_OK;
+  if (!a || !seg_lo || !seg_len || max_len > SEG_MAX_GRID || nseg > 0x7fffffffull)
+    return PIP_ERR_INVALID_ARG;
+  u32 Pmax = 2;
+  while (Pmax < max_len) Pmax <<= 1;
+  const size_t smem = SEG_CHUNK * 8;
+  PIP_CUDA(cudaFuncSetAttribute(segsort_local_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)smem));
+  const u32 C = Pmax < SEG_CHUNK ? Pmax : SEG_CHUNK;
+  const dim3 grid((unsigned)nseg, Pmax / C);
+  segsort_local_kernel<<<grid, 1024, smem, st>>>(a, seg_lo, seg_len, 0);
+  PIP_CHECK_LAUNCH();
+  for (u32 k = 2 * SEG_CHUNK; k <= Pmax; k <<= 1) {
+    segsort_global_kernel<<<grid, 1024, 0, st>>>(a, seg_lo, seg_len, k, 0);
+    PIP_CHECK_LAUNCH();
+    for (u32 j = k >> 2; j >= SEG_CHUNK; j >>= 1) {
+      segsort_global_kernel<<<grid, 1024, 0, st>>>(a, seg_lo, seg_len, k, j);
+      PIP_CHECK_LAUNCH();
+    }
+    segsort_local_kernel<<<grid, 1024, smem, st>>>(a, seg_lo, seg_len, k);
+    PIP_CHECK_LAUNCH();
+  }
+  return PIP_OK;
 }
 
 int sort_segments_device(u64* a, const u64* seg_lo, const u32* seg_len, u64 nseg, cudaStream_t st) {

@@ -256,8 +256,8 @@ def partition_unstable(a, pred, n: int | None = None) -> int:
     return _partition_impl(a, pred, n, meter_workspace=False)
 
 
-# leaves: one CTA sorts each (pip_sort_segments_u64, <= 2^20 words)
-QS_LEAF = int(os.environ.get("PIP_QS_LEAF", 1 << 19))
+# leaves: sorted by one grid-wide bitonic network (pip_sort_segments_grid_u64)
+QS_LEAF = int(os.environ.get("PIP_QS_LEAF", 1 << 22))
 
 
 def _quicksort_impl(a, rng, salt_of, meter_workspace: bool) -> None:
@@ -336,8 +336,9 @@ def _quicksort_impl(a, rng, salt_of, meter_workspace: bool) -> None:
             if leaves_lo:
                 slo = torch.tensor(leaves_lo, dtype=torch.int64, device=dev)
                 sln = torch.tensor(leaves_len, dtype=torch.int32, device=dev)
-                _lib.check(lib.pip_sort_segments_u64(w.ptr, slo.data_ptr(), sln.data_ptr(),
-                                                     len(leaves_lo), st), "sort")
+                _lib.check(lib.pip_sort_segments_grid_u64(w.ptr, slo.data_ptr(), sln.data_ptr(),
+                                                          len(leaves_lo), max(leaves_len), st),
+                           "sort")
                 torch.cuda.current_stream(w.device).synchronize()
         finally:
             if buf is not None:
@@ -351,8 +352,9 @@ def quicksort_strong(a, rng) -> None:
 
     ``rng`` is a :class:`~paper_2103_01216_b200.runtime.Rng`; pivots follow
     the reference's rule (its depth-cap restarts only change pivots, never
-    the sorted output).  Leaves of <= 2^19 words are sorted on the GPU by
-    one CTA each (the reference's base case is ``a[lo:hi].sort()``).
+    the sorted output).  Leaves of <= 2^22 words (``PIP_QS_LEAF``) are sorted on the
+    GPU by one grid-wide bitonic network (the reference's base case is
+    ``a[lo:hi].sort()``).
     """
     _quicksort_impl(a, rng, lambda depth: 0, meter_workspace=False)
 

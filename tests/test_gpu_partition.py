@@ -214,3 +214,60 @@ def test_sort_segments_ragged(pip):
     assert lib.pip_sort_segments_u64(t.data_ptr(), slo.data_ptr(), sln.data_ptr(),
                                      C.c_uint64(len(lens)), st) == 0
     assert np.array_equal(host(t), ref)
+
+
+@pytest.mark.parametrize("big", [1 << 13, (1 << 16) + 3, (1 << 21) + 5])
+def test_sort_segments_grid_ragged(pip, big):
+    # the grid-wide leaf sort (pip_sort_segments_grid_u64): ragged segments
+    # below, at and above one chunk next to one long segment
+    import ctypes as C
+
+    import torch
+
+    from paper_2103_01216_b200 import _lib
+
+    lens = [2, 3, 255, 8191, 8192, 8193, 40000, 1, big, 65536, 5]
+    los, pos = [], 0
+    for ln in lens:
+        los.append(pos)
+        pos += ln + 3
+    rng = np.random.default_rng(big)
+    x = rng.integers(0, 1 << 64, size=pos, dtype=np.uint64)
+    x[: pos // 4] = rng.integers(0, 3, size=pos // 4, dtype=np.uint64)
+    x[pos // 2: pos // 2 + 3000] = np.uint64((1 << 64) - 1)
+    ref = x.copy()
+    for lo, ln in zip(los, lens):
+        ref[lo: lo + ln] = np.sort(ref[lo: lo + ln])
+    t = dev(x)
+    slo = torch.tensor(los, dtype=torch.int64, device="cuda")
+    sln = torch.tensor(lens, dtype=torch.int32, device="cuda")
+    lib = _lib.load()
+    st = torch.cuda.current_stream().cuda_stream
+    assert lib.pip_sort_segments_grid_u64(t.data_ptr(), slo.data_ptr(), sln.data_ptr(),
+                                          C.c_uint64(len(lens)), C.c_uint64(max(lens)), st) == 0
+    assert np.array_equal(host(t), ref)
+
+
+@pytest.mark.parametrize("leaf", [8192, 65536, 1 << 19])
+@pytest.mark.parametrize("case", ["random", "few_values", "full_range_max"])
+def test_quicksort_recursion_small_leaves(pip, monkeypatch, leaf, case):
+    # the level-batched recursion itself (many levels of partitions) at leaf
+    # sizes below the default
+    monkeypatch.setattr(pip.strong, "QS_LEAF", leaf)
+    n = 3_000_017
+    rng = np.random.default_rng(leaf + len(case))
+    x = {"random": rng.integers(0, 1 << 64, size=n, dtype=np.uint64),
+         "few_values": rng.integers(0, 7, size=n, dtype=np.uint64),
+         "full_range_max": np.where(rng.random(n) < 0.2, np.uint64((1 << 64) - 1),
+                                    rng.integers(0, 1 << 64, size=n, dtype=np.uint64))}[case]
+    t = dev(x)
+    pip.strong.quicksort_strong(t, pip.Rng(13))
+    assert np.array_equal(host(t), np.sort(x))
+
+
+def test_quicksort_above_default_leaf(pip):
+    n = (1 << 23) + 11
+    x = pip.Rng(21).words(0, n) >> np.uint64(20)
+    t = dev(x)
+    pip.strong.quicksort_strong(t, pip.Rng(4))
+    assert np.array_equal(host(t), np.sort(x))
