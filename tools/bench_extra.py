@@ -2,7 +2,7 @@
 line each): list ranking / contraction (rows 4) and quicksort (row 3), CUDA
 events around the call on device-resident inputs, setup untimed.
 
-usage: python tools/bench_extra.py [--log2n 24] [--reps 3]
+usage: python tools/bench_extra.py [--log2n 24] [--reps 3] [--only list|quicksort]
 """
 import argparse
 import json
@@ -20,6 +20,7 @@ import paper_2103_01216_b200 as pip  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--log2n", type=int, default=24)
 ap.add_argument("--reps", type=int, default=3)
+ap.add_argument("--only", choices=["list", "quicksort"], default=None)
 args = ap.parse_args()
 n = 1 << args.log2n
 dev = "cuda:0"
@@ -41,49 +42,51 @@ def timed(setup, body):
     return ts[1:]
 
 
-# one random chain over n elements (order = a GPU random permutation)
-order = torch.arange(n, dtype=torch.int64, device=dev)
-h = pip.Rng(1).swaps_device(0, n)
-pip.relaxed.random_permutation(order, h)
-p = torch.arange(n, dtype=torch.int64, device=dev)
-pip.relaxed.random_permutation(p, pip.Rng(2).swaps_device(0, n))
+if args.only != "quicksort":
+    # one random chain over n elements (order = a GPU random permutation)
+    order = torch.arange(n, dtype=torch.int64, device=dev)
+    h = pip.Rng(1).swaps_device(0, n)
+    pip.relaxed.random_permutation(order, h)
+    p = torch.arange(n, dtype=torch.int64, device=dev)
+    pip.relaxed.random_permutation(p, pip.Rng(2).swaps_device(0, n))
 
 
-def chain():
-    nxt = torch.full((n,), NIL, dtype=torch.int64, device=dev)
-    prv = torch.full((n,), NIL, dtype=torch.int64, device=dev)
-    nxt[order[:-1]] = order[1:]
-    prv[order[1:]] = order[:-1]
-    return pip.contraction.LinkedList(nxt, prv)
+    def chain():
+        nxt = torch.full((n,), NIL, dtype=torch.int64, device=dev)
+        prv = torch.full((n,), NIL, dtype=torch.int64, device=dev)
+        nxt[order[:-1]] = order[1:]
+        prv[order[1:]] = order[:-1]
+        return pip.contraction.LinkedList(nxt, prv)
 
 
-budget = pip.EpsilonConfig(0.5)
-for name in ("list_rank", "list_contract"):
-    fn = pip.contraction.list_rank if name == "list_rank" else pip.contraction.list_contract
-    res = timed(chain, lambda l, fn=fn: fn(l, p, budget=budget))
+    budget = pip.EpsilonConfig(0.5)
+    for name in ("list_rank", "list_contract"):
+        fn = pip.contraction.list_rank if name == "list_rank" else pip.contraction.list_contract
+        res = timed(chain, lambda l, fn=fn: fn(l, p, budget=budget))
+        ms = sorted(r[0] for r in res)[len(res) // 2]
+        line = {"op": name, "n": n, "ms": ms, "elements_per_s": n / (ms / 1e3),
+                "rounds": None, "budget": "EpsilonConfig(0.5) (f=0.02)",
+                "note": "host-driven rounds (one sync per round) + in-place rank waves; single chain, "
+                        "random order and priorities from the GPU permutation"}
+        if name == "list_contract":
+            line["rounds"] = res[-1][2].rounds
+        if name == "list_rank":
+            lst = chain()
+            r = pip.contraction.list_rank(lst, p, budget=budget)
+            ref = torch.empty(n, dtype=torch.int64, device=dev)
+            ref[order] = torch.arange(n, dtype=torch.int64, device=dev)
+            line["verified"] = bool(torch.equal(r, ref))
+        print(json.dumps(line), flush=True)
+
+if args.only != "list":
+    x0 = pip.Rng(3).words_device(0, n)
+    res = timed(lambda: x0.clone(), lambda t: pip.strong.quicksort_strong(t, pip.Rng(5)))
     ms = sorted(r[0] for r in res)[len(res) // 2]
-    line = {"op": name, "n": n, "ms": ms, "elements_per_s": n / (ms / 1e3),
-            "rounds": None, "budget": "EpsilonConfig(0.5) (f=0.02)",
-            "note": "host-driven rounds (one sync per round) + in-place rank waves; single chain, "
-                    "random order and priorities from the GPU permutation"}
-    if name == "list_contract":
-        line["rounds"] = res[-1][2].rounds
-    if name == "list_rank":
-        lst = chain()
-        r = pip.contraction.list_rank(lst, p, budget=budget)
-        ref = torch.empty(n, dtype=torch.int64, device=dev)
-        ref[order] = torch.arange(n, dtype=torch.int64, device=dev)
-        line["verified"] = bool(torch.equal(r, ref))
-    print(json.dumps(line), flush=True)
-
-x0 = pip.Rng(3).words_device(0, n)
-res = timed(lambda: x0.clone(), lambda t: pip.strong.quicksort_strong(t, pip.Rng(5)))
-ms = sorted(r[0] for r in res)[len(res) // 2]
-t = x0.clone()
-pip.strong.quicksort_strong(t, pip.Rng(5))
-u = t.cpu().numpy().view(np.uint64)
-print(json.dumps({"op": "quicksort_strong", "n": n, "ms": ms, "elements_per_s": n / (ms / 1e3),
-                  "verified": bool(np.all(u[1:] >= u[:-1])),
-                  "note": "level-batched host recursion over the GPU partition (3 syncs per level) + "
-                          "one shared-memory bitonic launch for the <= 8192-word leaves"}),
-      flush=True)
+    t = x0.clone()
+    pip.strong.quicksort_strong(t, pip.Rng(5))
+    u = t.cpu().numpy().view(np.uint64)
+    print(json.dumps({"op": "quicksort_strong", "n": n, "ms": ms, "elements_per_s": n / (ms / 1e3),
+                      "verified": bool(np.all(u[1:] >= u[:-1])),
+                      "note": "level-batched host recursion over the GPU partition (3 syncs per level) + "
+                              "one grid-wide bitonic network for the <= 2^22-word leaves"}),
+          flush=True)
