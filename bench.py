@@ -309,6 +309,63 @@ def regen_timed(step, regen, steps, torch, st):
     return total
 
 
+def _windows(n: int, w: int = 1 << 20):
+    w = min(w, n)
+    mid = max(0, n // 2 - w // 2)
+    return sorted({(0, w), (mid, mid + w), (n - w, n)})
+
+
+def check_filter_windows(a, src, m, pred, lib, desc, sp, sb, sptr, torch):
+    """Oracle parity of a filtered array on sampled input windows."""
+    from oracle import oracle
+
+    n = src.numel()
+    cnt = torch.zeros(1, dtype=torch.int64, device=src.device)
+    assert lib.pip_count_u64(src.data_ptr(), n, C.byref(desc), cnt.data_ptr(), sp, sb, sptr) == 0
+    assert int(cnt.item()) == m, "filter count parity failed"
+    for lo, hi in _windows(n):
+        pos = 0
+        if lo:
+            assert lib.pip_count_u64(src.data_ptr(), lo, C.byref(desc), cnt.data_ptr(), sp, sb,
+                                     sptr) == 0
+            pos = int(cnt.item())
+        kept = oracle.seq_filter(src[lo:hi].cpu().numpy().view(np.uint64), pred)
+        got = a[pos:pos + len(kept)].cpu().numpy().view(np.uint64)
+        assert np.array_equal(got, kept), f"filter parity failed on input window [{lo}, {hi})"
+
+
+def merge_coranks(A, B, ranks, torch):
+    """Merge-path co-ranks (ties from A, strong.py:474-488) of several output
+    ranks at once (vectorised bisection on the device)."""
+    na, nb = A.numel(), B.numel()
+    r = torch.tensor(ranks, dtype=torch.int64, device=A.device)
+    lo = torch.clamp(r - nb, min=0)
+    hi = torch.clamp(r, max=na)
+    flip = -(1 << 63)
+    while bool((lo < hi).any()):
+        act = lo < hi
+        mid = torch.where(act, (lo + hi) // 2, torch.zeros_like(lo))
+        bj = torch.where(act, r - mid - 1, torch.zeros_like(lo))
+        go = act & ((B[bj.clamp(0, nb - 1)] ^ flip) >= (A[mid.clamp(0, na - 1)] ^ flip))
+        lo = torch.where(go, mid + 1, lo)
+        hi = torch.where(act & ~go, mid, hi)
+    return lo.tolist()
+
+
+def check_merge_windows(a, orig, na, torch):
+    """Oracle parity of a merged array on sampled output windows."""
+    from oracle import oracle
+
+    n = a.numel()
+    A, B = orig[:na], orig[na:]
+    for r0, r1 in _windows(n):
+        i0, i1 = merge_coranks(A, B, [r0, r1], torch)
+        want = oracle.seq_merge(A[i0:i1].cpu().numpy().view(np.uint64),
+                                B[r0 - i0:r1 - i1].cpu().numpy().view(np.uint64))
+        got = a[r0:r1].cpu().numpy().view(np.uint64)
+        assert np.array_equal(got, want), f"merge parity failed on output window [{r0}, {r1})"
+
+
 def run_filter(args, ws, rank, local, torch, pip, lib):
     if ws > 1:
         raise SystemExit("filter is benchmarked on one GPU in this round")
@@ -327,15 +384,21 @@ def run_filter(args, ws, rank, local, torch, pip, lib):
         rc = lib.pip_filter_u64(a.data_ptr(), n, C.byref(desc), mdev.data_ptr(), sp, sb, sptr)
         assert rc == 0, rc
 
-    for _ in range(args.warmup):
+    # parity of the first (warm-up) step against the oracle on sampled
+    # windows (start, middle, end of the input): the kept words of input
+    # window [lo, hi) must sit at a[count(src[0:lo)) : ...], in order
+    regen()
+    src = a.clone()
+    step()
+    torch.cuda.synchronize()
+    pip._lib.check_stall(sp, sptr, "filter")
+    m = int(mdev.item())
+    check_filter_windows(a, src, m, pip.pred.mod_eq(3, 0), lib, desc, sp, sb, sptr, torch)
+    del src
+    for _ in range(max(args.warmup - 1, 0)):
         regen()
         step()
     torch.cuda.synchronize()
-    m = int(mdev.item())
-    regen()
-    cnt = torch.zeros(1, dtype=torch.int64, device=f"cuda:{dev}")
-    lib.pip_count_u64(a.data_ptr(), n, C.byref(desc), cnt.data_ptr(), sp, sb, sptr)
-    assert int(cnt.item()) == m
     clk = ClockSampler(dev)
     ms = regen_timed(step, regen, args.steps, torch, st)
     clocks = clk.stop()
@@ -456,9 +519,15 @@ def run_merge(args, ws, rank, local, torch, pip, lib):
         assert rc == 0, rc
 
     regen()
+    orig = a.clone()
     step()
     torch.cuda.synchronize()
+    # parity of the first (warm-up) step: sampled output windows against the
+    # oracle's sequential merge of the matching input ranges, plus global
+    # sortedness (values < 2^30: signed order = unsigned)
+    check_merge_windows(a, orig, na, torch)
     assert bool((a[1:] >= a[:-1]).all().item())
+    del orig
     for _ in range(max(args.warmup - 1, 0)):
         regen()
         step()
@@ -519,12 +588,14 @@ def run_rp(args, ws, rank, local, torch, pip, lib, small: bool):
 
     step()
     torch.cuda.synchronize()
-    if small or n <= (1 << 26):
-        from oracle import oracle
+    # parity of the first step, every word, at every size (C4 included):
+    # the oracle's sequential Knuth shuffle (baselines.py:44-54) in C
+    from oracle import oracle
 
-        ref = np.arange(n, dtype=np.uint64)
-        oracle.seq_knuth_shuffle(ref, h.cpu().numpy().view(np.uint64))
-        assert np.array_equal(a.cpu().numpy().view(np.uint64), ref)
+    ref = np.arange(n, dtype=np.uint64)
+    oracle.seq_knuth_shuffle(ref, h.cpu().numpy().view(np.uint64))
+    assert np.array_equal(a.cpu().numpy().view(np.uint64), ref), "permutation parity failed"
+    a.copy_(torch.arange(n, dtype=torch.int64, device=f"cuda:{dev}"))
     for _ in range(max(args.warmup - 1, 0)):
         step()
     torch.cuda.synchronize()
@@ -553,7 +624,8 @@ def run_rp(args, ws, rank, local, torch, pip, lib, small: bool):
                     f"{bufn} words ({rmw_rate / 1e9:.2f} G RMW/s)"}
     e2e = None
     if not args.no_e2e:
-        e2e = e2e_host(lib, "rp", n, args, torch, dev, ws, h=h, prefix=prefix)
+        e2e = e2e_host(lib, "rp", n, args, torch, dev, ws, h=h, prefix=prefix, ref=ref)
+    del ref
     cpu = None if args.no_cpu else cpu_baseline("rp0" if small else "rp", args)
     cfg = {"workload": ("random permutation n=10^6, BASELINE configs[0]" if small else
                         "random permutation n=2^30, BASELINE configs[4]"),
@@ -601,6 +673,7 @@ def e2e_host(lib, op, n, args, torch, dev, ws, **kw):
         hh.copy_(kw["h"])
     total = 0.0
     bi = bo = 0
+    out = C.c_uint64(0)
     for it in range(steps + 1):  # the first call is an untimed warm-up (pools, pinned staging)
         fill()
         t0 = time.perf_counter()
@@ -635,11 +708,55 @@ def e2e_host(lib, op, n, args, torch, dev, ws, **kw):
         if it > 0:
             total += time.perf_counter() - t0
         assert rc == 0, rc
+    # parity of the last timed call's output (d still holds its input)
+    check_e2e(op, host, d, out.value if op in ("scan", "filter", "partition") else None, n,
+              torch, kw)
     del d
     return {"value": n * steps / total, "unit": "elements/s", "h2d_bytes_per_step": bi,
-            "d2h_bytes_per_step": bo, "steps": steps,
+            "d2h_bytes_per_step": bo, "steps": steps, "checked": True,
             "note": "synchronous C-ABI *_host call on pinned host memory; wall clock "
-                    "around the call (H2D + kernels + D2H)"}
+                    "around the call (H2D + kernels + D2H); the last call's output is "
+                    "checked against the oracle on sampled windows (the permutation: "
+                    "every word)"}
+
+
+def check_e2e(op, host, d, result, n, torch, kw):
+    import paper_2103_01216_b200 as pip
+    from oracle import oracle
+
+    if op == "scan":
+        src = d
+        for lo, hi in _windows(n):
+            carry = 0 if lo == 0 else int(host[lo - 1].item()) & ((1 << 64) - 1)
+            want, _ = oracle.seq_scan(src[lo:hi].cpu().numpy().view(np.uint64), init=carry,
+                                      inclusive=True)
+            got = host[lo:hi].numpy().view(np.uint64)
+            assert np.array_equal(got, want), f"e2e scan parity failed on window [{lo}, {hi})"
+        assert int(host[n - 1].item()) & ((1 << 64) - 1) == result, "e2e scan total"
+    elif op in ("filter", "partition"):
+        dev = d.device.index
+        st = torch.cuda.current_stream().cuda_stream
+        sp, sb = pip.runtime.scratch_for(dev, st)
+        lib = pip._lib.load()
+        p = pip.pred.mod_eq(3, 0)
+        desc = p.descriptor()
+        if op == "filter":
+            check_filter_windows(host, d, result, p, lib, desc, sp, sb, st, torch)
+        else:
+            cnt = torch.zeros(1, dtype=torch.int64, device=d.device)
+            assert lib.pip_count_u64(d.data_ptr(), n, C.byref(desc), cnt.data_ptr(), sp, sb, st) == 0
+            m = int(cnt.item())
+            assert m == result, "e2e partition count"
+            for lo, hi in _windows(n):
+                x = host[lo:hi].numpy().view(np.uint64)
+                keep = (x % np.uint64(3)) == 0
+                assert bool(np.all(keep[: max(0, m - lo)])) and not bool(np.any(keep[max(0, m - lo):])), \
+                    f"e2e partition contract failed on window [{lo}, {hi})"
+    elif op == "merge":
+        check_merge_windows(host, d, n // 2, torch)
+    else:
+        assert np.array_equal(host.numpy().view(np.uint64), kw["ref"]), "e2e permutation parity"
+
 
 
 # ---------------------------------------------------------------------------

@@ -46,7 +46,10 @@ enum pip_status {
   PIP_ERR_UNSORTED = 6,      /* reference: ValueError("unsorted input run") */
   PIP_ERR_UNSUPPORTED = 7,   /* size or option outside this build's support */
   PIP_ERR_TABLE = 8,         /* reservation table overfull (never in practice) */
-  PIP_ERR_DEBUG_SWEEP = 9    /* reference: debug sweep assertion failed */
+  PIP_ERR_DEBUG_SWEEP = 9,   /* reference: debug sweep assertion failed */
+  PIP_ERR_STALLED = 10       /* a CTA's bounded spin expired (look-back / dataflow
+                                wait): the output is incomplete; see
+                                pip_scratch_status */
 };
 
 /* scan element operations (strong.scan `op`): None/add, max, min, xor */
@@ -93,6 +96,14 @@ const char* pip_status_string(int status);
 const char* pip_last_cuda_error(void);
 /* bytes of O(#CTAs) scratch every strong op needs on `device` */
 size_t pip_scratch_bytes(int device);
+/* Status of the stream-ordered look-back ops (pip_scan_u64*, pip_reduce_u64,
+ * pip_filter_u64, pip_count_u64) that last ran on `scratch`: synchronizes
+ * `stream` and returns PIP_ERR_STALLED when a CTA of one of them gave up
+ * waiting (its spin bound expired; the output is then incomplete), else
+ * PIP_OK.  Each of those entry points clears the flag when it is queued, so
+ * call this after every call whose result is used (the Python layer does).
+ * The *_host entry points and the merge / permutation check it themselves. */
+int pip_scratch_status(const void* scratch, void* stream);
 
 /* ---- scan: strong.scan / strong.scan_blocked (strong.py:151-236) --------- *
  * Exclusive (inclusive=0) or inclusive in-place scan of a[0:n) under `op`.
@@ -127,6 +138,37 @@ int pip_count_u64(const uint64_t* a, uint64_t n, const pip_pred* pred, uint64_t*
                   void* scratch, size_t scratch_bytes, void* stream);
 int pip_filter_u64_host(uint64_t* host_a, uint64_t n, const pip_pred* pred, uint64_t* m_out,
                         int device);
+
+/* ---- runtime.compact_by_mask (runtime.py:335-355) ------------------------ *
+ * Stable in-place compaction: a[0:m) = the a[i] with keep[i] != 0 (device
+ * byte mask u8[n]), in order; m to device m_dev; a[m:n) unspecified.  The
+ * failure packing of the round engine (detres.py:303).  Same look-back
+ * scratch and status rules as pip_filter_u64.                               */
+int pip_compact_by_mask_u64(uint64_t* a, uint64_t n, const uint8_t* keep, uint64_t* m_dev,
+                            void* scratch, size_t scratch_bytes, void* stream);
+
+/* ---- detres.ReservationTable (detres.py:40-211) on the device ------------- *
+ * table_keys / table_vals: device u64[capacity], capacity a power of two
+ * >= 8, empty slots hold NIL = 2^64-1 in table_keys; home(k) =
+ * (k * 0x9E3779B97F4A7C15) >> (64 - log2 capacity), linear probing.
+ * reserve_max: per key, slot value = max(existing, written values) — the
+ * reference's batch algorithm step by step (claims of empty slots by
+ * write-min on the key word), so the slot layout equals the reference's;
+ * keys / vals device u64[n]; workspace holds pip_rt_workspace_bytes(n);
+ * *count_out (HOST) receives the occupied slots afterwards; synchronizes;
+ * PIP_ERR_TABLE on probe overflow (detres.py:126-127).
+ * lookup: vals_out (device u64[n], NIL when absent) and found_out (device
+ * u8[n]); stream-ordered.  delete: clears the keys' slots (all located
+ * before any is cleared, :165-193); *count_out (HOST) as above.           */
+size_t pip_rt_workspace_bytes(uint64_t n);
+int pip_rt_reserve_max_u64(uint64_t* table_keys, uint64_t* table_vals, uint64_t capacity,
+                           const uint64_t* keys, const uint64_t* vals, uint64_t n, void* workspace,
+                           size_t workspace_bytes, uint64_t* count_out, void* stream);
+int pip_rt_lookup_u64(const uint64_t* table_keys, const uint64_t* table_vals, uint64_t capacity,
+                      const uint64_t* keys, uint64_t n, uint64_t* vals_out, uint8_t* found_out,
+                      void* stream);
+int pip_rt_delete_u64(uint64_t* table_keys, uint64_t capacity, const uint64_t* keys, uint64_t n,
+                      void* workspace, size_t workspace_bytes, uint64_t* count_out, void* stream);
 
 /* ---- rotate: strong.rotate (strong.py:67-95) ------------------------------ *
  * Left rotation: out[i] = in[(i + o) mod n], 0 <= o <= n.                   */
@@ -245,14 +287,15 @@ int pip_merge_u64_host(uint64_t* host_a, uint64_t n, uint64_t split, uint64_t bu
  * (detres.run_rounds, detres.py:256-307), with the reference's round
  * structure (descending ids, self-swaps retired at ingestion, failures
  * packed first), so rounds / committed-per-round / trace are identical.
- *   committed_per_round_dev: device u64[rounds_cap] (NULL ok)
+ *   committed_per_round_host: HOST u64[rounds_cap] (NULL ok), written by the
+ *   call as the rounds complete (it synchronizes)
  *   trace_dev: device u64[n_iterates] of committed ids in round/packed order
  *   (NULL ok); debug != 0 runs the clean-table sweep (relaxed.py:212-217).
  * workspace must hold pip_rp_workspace_bytes(n, prefix, variant).
  * stats_host receives the round statistics (the call synchronizes).        */
 size_t pip_rp_workspace_bytes(uint64_t n, uint64_t prefix, int variant);
 int pip_random_permutation_u64(uint64_t* a, const uint64_t* h, uint64_t n, uint64_t prefix,
-                               int variant, int debug, uint64_t* committed_per_round_dev,
+                               int variant, int debug, uint64_t* committed_per_round_host,
                                uint64_t rounds_cap, uint64_t* trace_dev,
                                void* workspace, size_t workspace_bytes,
                                pip_rp_stats* stats_host, void* stream);

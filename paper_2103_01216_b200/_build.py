@@ -17,7 +17,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libpip.so"
-SOURCES = ["api.cu", "scan.cu", "filter.cu", "misc.cu", "rp.cu", "merge.cu", "partition.cu", "contraction.cu"]
+SOURCES = ["api.cu", "scan.cu", "filter.cu", "misc.cu", "rp.cu", "merge.cu", "partition.cu", "contraction.cu", "detres.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -45,8 +45,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
              "-I", str(ROOT / "include"), "--expt-relaxed-constexpr"]
     if verbose:
         flags += ["-Xptxas", "-v"]
-    objs = []
-    for src in SOURCES:
+    def compile_one(src: str) -> str:
         obj = objdir / (src + ".o")
         cmd = [nvcc(), *flags, "-c", str(CSRC / src), "-o", str(obj)]
         r = subprocess.run(cmd, capture_output=True, text=True)
@@ -54,7 +53,12 @@ def build(force: bool = False, verbose: bool = False) -> Path:
             raise RuntimeError(f"nvcc failed on {src}:\n{r.stderr}")
         if verbose and r.stderr:
             sys.stderr.write(r.stderr)
-        objs.append(str(obj))
+        return str(obj)
+
+    from concurrent.futures import ThreadPoolExecutor
+
+    with ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 1)) as ex:
+        objs = list(ex.map(compile_one, SOURCES))
     tmp = LIB.with_suffix(".so.tmp")
     cmd = [nvcc(), *ARCH, "-shared", "-cudart", "static", "-o", str(tmp), *objs]
     r = subprocess.run(cmd, capture_output=True, text=True)

@@ -30,6 +30,7 @@ PIP_ERR_UNSORTED = 6
 PIP_ERR_UNSUPPORTED = 7
 PIP_ERR_TABLE = 8
 PIP_ERR_DEBUG_SWEEP = 9
+PIP_ERR_STALLED = 10
 
 OP_ADD, OP_MAX, OP_MIN, OP_XOR = 0, 1, 2, 3
 RP_NAIVE, RP_FLAT, RP_ONERES, RP_FINAL = 0, 1, 2, 3
@@ -60,6 +61,7 @@ SIGNATURES = {
     "pip_status_string": (C.c_char_p, [i32]),
     "pip_last_cuda_error": (C.c_char_p, []),
     "pip_scratch_bytes": (sz, [i32]),
+    "pip_scratch_status": (i32, [vp, vp]),
     "pip_scan_u64": (i32, [vp, u64, i32, u64, i32, vp, vp, sz, vp]),
     "pip_scan_u64_carry": (i32, [vp, u64, i32, u64, i32, vp, vp, vp, sz, vp]),
     "pip_reduce_u64": (i32, [vp, u64, i32, vp, vp, sz, vp]),
@@ -68,6 +70,11 @@ SIGNATURES = {
     "pip_count_u64": (i32, [vp, u64, C.POINTER(PipPred), vp, vp, sz, vp]),
     "pip_filter_u64_host": (i32, [vp, u64, C.POINTER(PipPred), C.POINTER(u64), i32]),
     "pip_rotate_u64": (i32, [vp, u64, u64, vp, sz, vp]),
+    "pip_compact_by_mask_u64": (i32, [vp, u64, vp, vp, vp, sz, vp]),
+    "pip_rt_workspace_bytes": (sz, [u64]),
+    "pip_rt_reserve_max_u64": (i32, [vp, vp, u64, vp, vp, u64, vp, sz, C.POINTER(u64), vp]),
+    "pip_rt_lookup_u64": (i32, [vp, vp, u64, vp, u64, vp, vp, vp]),
+    "pip_rt_delete_u64": (i32, [vp, u64, vp, u64, vp, sz, C.POINTER(u64), vp]),
     "pip_partition_workspace_bytes": (sz, [u64]),
     "pip_partition_u64": (i32, [vp, u64, C.POINTER(PipPred), vp, vp, sz, vp]),
     "pip_partition_u64_host": (i32, [vp, u64, C.POINTER(PipPred), C.POINTER(u64), i32]),
@@ -130,6 +137,12 @@ class PipError(RuntimeError):
             msg += f" ({lib.pip_last_cuda_error().decode()})"
         super().__init__(f"{where}: {msg} [status {status}]")
         self.status = status
+
+
+def check_stall(scratch_ptr: int, stream: int, where: str) -> None:
+    """Synchronize ``stream`` and raise if a look-back op queued on this
+    scratch gave up waiting (PIP_ERR_STALLED: its output is incomplete)."""
+    check(load().pip_scratch_status(scratch_ptr, stream), where)
 
 
 def check(status: int, where: str) -> None:

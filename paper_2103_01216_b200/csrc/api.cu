@@ -84,6 +84,15 @@ int sort_segments_grid_device(u64* a, const u64* seg_lo, const u32* seg_len, u64
 int partition_device(u64* a, u64 n, const pip_pred* pred, u64* m_dev, void* ws, size_t ws_bytes,
                      cudaStream_t st);
 size_t merge_workspace_bytes(u64 n, u64 split, u64 budget_words);
+int compact_mask_device(u64* a, u64 n, const unsigned char* mask, u64* m_dev, void* scratch,
+                        size_t scratch_bytes, cudaStream_t st);
+size_t rt_workspace_bytes(u64 n);
+int rt_reserve_max(u64* tkeys, u64* tvals, u64 cap, const u64* keys, const u64* vals, u64 n,
+                   void* ws, size_t ws_bytes, u64* count_out, cudaStream_t st);
+int rt_lookup(const u64* tkeys, const u64* tvals, u64 cap, const u64* keys, u64 n, u64* out_vals,
+              unsigned char* found, cudaStream_t st);
+int rt_delete(u64* tkeys, u64 cap, const u64* keys, u64 n, void* ws, size_t ws_bytes, u64* count_out,
+              cudaStream_t st);
 int merge_copy_device(const u64* a, u64 na, const u64* b, u64 nb, u64* out, cudaStream_t st);
 int merge_device(u64* a, u64 n, u64 split, int check_sorted, void* ws, size_t ws_bytes,
                  void* scratch, size_t scratch_bytes, cudaStream_t st);
@@ -146,10 +155,17 @@ struct DevBuf {
     return pool_get(bytes, &p);
   }
 };
+// A Stream drains its queued work before it is destroyed, so an early error
+// return never hands a DevBuf back to the pool while a copy or kernel still
+// uses it.  Every function declares its DevBufs BEFORE its Streams (locals
+// are destroyed in reverse order: streams drain first, buffers return after).
 struct Stream {
   cudaStream_t s = nullptr;
   ~Stream() {
-    if (s) cudaStreamDestroy(s);
+    if (s) {
+      cudaStreamSynchronize(s);
+      cudaStreamDestroy(s);
+    }
   }
   cudaError_t create() { return cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking); }
 };
@@ -160,6 +176,25 @@ struct Event {
   }
   cudaError_t create() { return cudaEventCreateWithFlags(&e, cudaEventDisableTiming); }
 };
+
+// The look-back ops' stall flag (scratch word 0).  It is cleared once per
+// public call, never per launch: a scan's tail launch must not wipe a stall
+// its main launch raised, nor a chunk of a host scan one of an earlier chunk.
+// PIP_INJECT_STALL=1 raises it right after the clear (tests of the
+// reporting path; the kernels then bail out of their first long wait).
+static int clear_stall(void* scratch, size_t scratch_bytes, cudaStream_t st) {
+  if (!scratch || scratch_bytes < 64) return PIP_OK;  // the op reports OOM itself
+  PIP_CUDA(cudaMemsetAsync(scratch, 0, 4, st));
+  const char* e = getenv("PIP_INJECT_STALL");
+  if (e && e[0] == '1') PIP_CUDA(cudaMemsetAsync(scratch, 1, 1, st));
+  return PIP_OK;
+}
+static int read_stall(const void* scratch, cudaStream_t st) {
+  u32 h = 0;
+  PIP_CUDA(cudaMemcpyAsync(&h, scratch, 4, cudaMemcpyDeviceToHost, st));
+  PIP_CUDA(cudaStreamSynchronize(st));
+  return h ? PIP_ERR_STALLED : PIP_OK;
+}
 
 // the device entry points' predicate checks, made before a host entry point
 // queues any transfer (so an invalid predicate never leaves copies in flight)
@@ -173,7 +208,7 @@ static u64 host_chunk() {
   if (!c) {
     const char* e = getenv("PIP_HOST_CHUNK_LOG2");
     const int lg = e ? atoi(e) : 24;
-    c = 1ull << (lg >= 16 && lg <= 30 ? lg : 26);
+    c = 1ull << (lg >= 16 && lg <= 30 ? lg : 24);  // invalid values: the default
   }
   return c;
 }
@@ -208,6 +243,7 @@ int scan_host(u64* host, u64 n, int op, u64 init, int inclusive, u64* total_out,
   const u64 nchunks = (n + chunk - 1) / chunk;
   std::vector<Event> in_done(nchunks), comp_done(nchunks), out_done(nchunks);
   u64* cr = (u64*)carry.p;  // cr[k & 1] = carry into chunk k
+  if (int rc = clear_stall(scratch.p, sb, comp.s)) return rc;
   u64 ident = op == PIP_OP_MIN ? ~0ull : 0ull;
   PIP_CUDA(cudaMemcpyAsync(cr, &ident, 8, cudaMemcpyHostToDevice, comp.s));
   PIP_CUDA(cudaStreamSynchronize(comp.s));
@@ -233,9 +269,7 @@ int scan_host(u64* host, u64 n, int op, u64 init, int inclusive, u64* total_out,
   PIP_CUDA(cudaMemcpyAsync(&tot, cr + (nchunks & 1), 8, cudaMemcpyDeviceToHost, comp.s));
   PIP_CUDA(cudaStreamSynchronize(comp.s));
   PIP_CUDA(cudaStreamSynchronize(cout.s));
-  u32 abort_flag = 0;
-  PIP_CUDA(cudaMemcpy(&abort_flag, scratch.p, 4, cudaMemcpyDeviceToHost));
-  if (abort_flag) return PIP_ERR_CUDA;
+  if (int rc = read_stall(scratch.p, comp.s)) return rc;
   if (total_out) *total_out = tot;
   return PIP_OK;
 }
@@ -275,6 +309,7 @@ int filter_host(u64* host, u64 n, const pip_pred* pred, u64* m_out, int device) 
     PIP_CUDA(cnt_done[k].create());
     PIP_CUDA(out_done[k].create());
   }
+  if (int rc = clear_stall(scratch.p, sb, comp.s)) return rc;
   u64 m = 0;
   auto issue = [&](u64 k) -> int {
     const u64 off = k * chunk, len = (n - off) < chunk ? (n - off) : chunk;
@@ -303,9 +338,7 @@ int filter_host(u64* host, u64 n, const pip_pred* pred, u64* m_out, int device) 
       if (int rc = issue(k + 1 + ahead)) return rc;
   }
   PIP_CUDA(cudaStreamSynchronize(cout.s));
-  u32 abort_flag = 0;
-  PIP_CUDA(cudaMemcpy(&abort_flag, scratch.p, 4, cudaMemcpyDeviceToHost));
-  if (abort_flag) return PIP_ERR_CUDA;
+  if (int rc = read_stall(scratch.p, comp.s)) return rc;
   if (m_out) *m_out = m;
   return PIP_OK;
 }
@@ -517,6 +550,7 @@ const char* pip_status_string(int s) {
     case PIP_ERR_UNSUPPORTED: return "unsupported size or option";
     case PIP_ERR_TABLE: return "reservation table overfull; presize the table";
     case PIP_ERR_DEBUG_SWEEP: return "debug sweep: reservation slots not clean after a round";
+    case PIP_ERR_STALLED: return "a CTA's bounded wait expired (look-back / dataflow stall); output incomplete";
     default: return "unknown status";
   }
 }
@@ -525,8 +559,14 @@ const char* pip_last_cuda_error(void) { return g_cuda_err; }
 
 size_t pip_scratch_bytes(int device) { return scratch_bytes_for(num_sms(device)); }
 
+int pip_scratch_status(const void* scratch, void* stream) {
+  if (!scratch) return PIP_ERR_INVALID_ARG;
+  return read_stall(scratch, (cudaStream_t)stream);
+}
+
 int pip_scan_u64(uint64_t* a, uint64_t n, int op, uint64_t init, int inclusive, uint64_t* total_dev,
                  void* scratch, size_t scratch_bytes, void* stream) {
+  if (int rc = clear_stall(scratch, scratch_bytes, (cudaStream_t)stream)) return rc;
   return scan_device((u64*)a, n, op, init, inclusive, nullptr, (u64*)total_dev, scratch,
                      scratch_bytes, (cudaStream_t)stream);
 }
@@ -534,12 +574,14 @@ int pip_scan_u64(uint64_t* a, uint64_t n, int op, uint64_t init, int inclusive, 
 int pip_scan_u64_carry(uint64_t* a, uint64_t n, int op, uint64_t init, int inclusive,
                        const uint64_t* carry_dev, uint64_t* total_dev, void* scratch,
                        size_t scratch_bytes, void* stream) {
+  if (int rc = clear_stall(scratch, scratch_bytes, (cudaStream_t)stream)) return rc;
   return scan_device((u64*)a, n, op, init, inclusive, (const u64*)carry_dev, (u64*)total_dev,
                      scratch, scratch_bytes, (cudaStream_t)stream);
 }
 
 int pip_reduce_u64(const uint64_t* a, uint64_t n, int op, uint64_t* total_dev, void* scratch,
                    size_t scratch_bytes, void* stream) {
+  if (int rc = clear_stall(scratch, scratch_bytes, (cudaStream_t)stream)) return rc;
   return reduce_device((const u64*)a, n, op, (u64*)total_dev, scratch, scratch_bytes,
                        (cudaStream_t)stream);
 }
@@ -552,11 +594,13 @@ int pip_scan_u64_host(uint64_t* host_a, uint64_t n, int op, uint64_t init, int i
 
 int pip_filter_u64(uint64_t* a, uint64_t n, const pip_pred* pred, uint64_t* m_dev, void* scratch,
                    size_t scratch_bytes, void* stream) {
+  if (int rc = clear_stall(scratch, scratch_bytes, (cudaStream_t)stream)) return rc;
   return filter_device((u64*)a, n, pred, (u64*)m_dev, scratch, scratch_bytes, (cudaStream_t)stream);
 }
 
 int pip_count_u64(const uint64_t* a, uint64_t n, const pip_pred* pred, uint64_t* m_dev,
                   void* scratch, size_t scratch_bytes, void* stream) {
+  if (int rc = clear_stall(scratch, scratch_bytes, (cudaStream_t)stream)) return rc;
   return count_device((const u64*)a, n, pred, (u64*)m_dev, scratch, scratch_bytes,
                       (cudaStream_t)stream);
 }
@@ -565,6 +609,36 @@ int pip_filter_u64_host(uint64_t* host_a, uint64_t n, const pip_pred* pred, uint
                         int device) {
   if (!pred_ok(pred) || (n && !host_a)) return PIP_ERR_INVALID_ARG;
   return filter_host((u64*)host_a, n, pred, (u64*)m_out, device);
+}
+
+int pip_compact_by_mask_u64(uint64_t* a, uint64_t n, const uint8_t* keep, uint64_t* m_dev,
+                            void* scratch, size_t scratch_bytes, void* stream) {
+  if (int rc = clear_stall(scratch, scratch_bytes, (cudaStream_t)stream)) return rc;
+  return compact_mask_device((u64*)a, n, keep, (u64*)m_dev, scratch, scratch_bytes,
+                             (cudaStream_t)stream);
+}
+
+size_t pip_rt_workspace_bytes(uint64_t n) { return rt_workspace_bytes(n); }
+
+int pip_rt_reserve_max_u64(uint64_t* table_keys, uint64_t* table_vals, uint64_t capacity,
+                           const uint64_t* keys, const uint64_t* vals, uint64_t n, void* workspace,
+                           size_t workspace_bytes, uint64_t* count_out, void* stream) {
+  return rt_reserve_max((u64*)table_keys, (u64*)table_vals, capacity, (const u64*)keys,
+                        (const u64*)vals, n, workspace, workspace_bytes, (u64*)count_out,
+                        (cudaStream_t)stream);
+}
+
+int pip_rt_lookup_u64(const uint64_t* table_keys, const uint64_t* table_vals, uint64_t capacity,
+                      const uint64_t* keys, uint64_t n, uint64_t* vals_out, uint8_t* found_out,
+                      void* stream) {
+  return rt_lookup((const u64*)table_keys, (const u64*)table_vals, capacity, (const u64*)keys, n,
+                   (u64*)vals_out, found_out, (cudaStream_t)stream);
+}
+
+int pip_rt_delete_u64(uint64_t* table_keys, uint64_t capacity, const uint64_t* keys, uint64_t n,
+                      void* workspace, size_t workspace_bytes, uint64_t* count_out, void* stream) {
+  return rt_delete((u64*)table_keys, capacity, (const u64*)keys, n, workspace, workspace_bytes,
+                   (u64*)count_out, (cudaStream_t)stream);
 }
 
 int pip_rotate_u64(uint64_t* a, uint64_t n, uint64_t o, void* scratch, size_t scratch_bytes,
@@ -643,9 +717,9 @@ int pip_partition_u64_host(uint64_t* host_a, uint64_t n, const pip_pred* pred, u
   }
   const char* e = getenv("PIP_PARTITION_HOST_INPLACE");
   if (!(e && atoi(e)) && n > host_chunk()) return partition_host_stream((u64*)host_a, n, pred, (u64*)m_out, device);
+  DevBuf a, ws, m;
   Stream s;
   PIP_CUDA(s.create());
-  DevBuf a, ws, m;
   PIP_CUDA(a.alloc(n * 8));
   const size_t wb = partition_workspace_bytes(n);
   PIP_CUDA(ws.alloc(wb));
@@ -676,9 +750,9 @@ int pip_merge_u64_host(uint64_t* host_a, uint64_t n, uint64_t split, uint64_t bu
   if (n < 2 || split == 0 || split == n) return PIP_OK;
   const char* e = getenv("PIP_MERGE_HOST_INPLACE");
   if (e && atoi(e)) {  // upload everything, merge in place on the device, copy back
+    DevBuf a, ws, scratch;
     Stream s;
     PIP_CUDA(s.create());
-    DevBuf a, ws, scratch;
     PIP_CUDA(a.alloc(n * 8));
     const size_t wb = merge_workspace_bytes(n, split, budget_words);
     PIP_CUDA(ws.alloc(wb));
@@ -722,10 +796,10 @@ int pip_random_permutation_u64_host(uint64_t* host_a, const uint64_t* host_h, ui
     if (stats_host) memset(stats_host, 0, sizeof(*stats_host));
     return PIP_OK;
   }
+  DevBuf a, h, ws;
   Stream s, cout;
   PIP_CUDA(s.create());
   PIP_CUDA(cout.create());
-  DevBuf a, h, ws;
   PIP_CUDA(a.alloc(n * 8));
   PIP_CUDA(h.alloc(n * 8));
   const size_t wb = rp_workspace_bytes(n, prefix, variant);
@@ -770,7 +844,14 @@ int pip_random_permutation_u64_host(uint64_t* host_a, const uint64_t* host_h, ui
   int rc = rp_device((u64*)a.p, (const u64*)h.p, n, prefix, variant, 0, nullptr, 0, nullptr, ws.p,
                      wb, stats_host, s.s, overlap ? &prog : nullptr);
   if (rc) {
-    cudaStreamSynchronize(cout.s);  // pending copies hold only final words
+    // The drain already wrote final words of a[top+1 : n) back while the
+    // host prefix still holds the input: bring the whole device state back
+    // (the rounds run so far, a permutation of the input) so the caller's
+    // array stays a permutation, as the reference's in-place swaps do.
+    cudaStreamSynchronize(cout.s);
+    if (cudaStreamSynchronize(s.s) == cudaSuccess &&
+        cudaMemcpy(host_a, a.p, n * 8, cudaMemcpyDeviceToHost) != cudaSuccess)
+      cudaGetLastError();
     return rc;
   }
   PIP_CUDA(drain.err);

@@ -141,6 +141,44 @@ filter_kernel(u64* __restrict__ a, u64 n, DevPred p, u64* m_out, LookbackCtx c, 
   }
 }
 
+// runtime.compact_by_mask (runtime.py:335-355): the same look-back tile
+// body with the keep flags read from a byte mask instead of a predicate
+// (the reference's failure packing in detres.run_rounds, detres.py:303).
+template <bool VEC>
+__global__ void __launch_bounds__(FILTER_THREADS, 2)
+compact_mask_kernel(u64* __restrict__ a, u64 n, const unsigned char* __restrict__ mask, u64* m_out,
+                    LookbackCtx c, u64 num_tiles) {
+  __shared__ u64 s_warp[4 * (FILTER_THREADS / 32) + 4];
+  __shared__ int s_abort;
+  const u32 lane = lane_id(), warp = warp_id();
+  for (u64 tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+    const u64 wbase = tile * FILTER_TILE + (u64)warp * 512;
+    const bool full = VEC && (tile * FILTER_TILE + FILTER_TILE <= n);
+    u64 x[16];
+    u32 keep = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const u64 i0 = wbase + 64 * j + 2 * lane;
+      if (full) {
+        const ulonglong2 v = ldg_stream2(a + wbase + 64 * j + 2 * lane);
+        x[2 * j] = v.x;
+        x[2 * j + 1] = v.y;
+        const unsigned short mk = *(const unsigned short*)(mask + i0);
+        keep |= (u32)((mk & 0xff) != 0) << (2 * j);
+        keep |= (u32)((mk >> 8) != 0) << (2 * j + 1);
+      } else {
+        x[2 * j] = i0 < n ? a[i0] : 0;
+        x[2 * j + 1] = i0 + 1 < n ? a[i0 + 1] : 0;
+        keep |= (u32)(i0 < n && mask[i0] != 0) << (2 * j);
+        keep |= (u32)(i0 + 1 < n && mask[i0 + 1] != 0) << (2 * j + 1);
+      }
+    }
+    if (!filter_tile_body<FILTER_THREADS>(x, keep, a, tile, m_out, c, num_tiles, s_warp, &s_abort,
+                                          nullptr))
+      return;
+  }
+}
+
 // TMA ring variant (16-byte aligned base), as scan_tma_kernel
 template <int THREADS, int STAGES>
 __global__ void __launch_bounds__(THREADS, 1)
@@ -851,7 +889,7 @@ static int launch_filter_pc(u64* a, u64 n, const DevPred& p, u64* m_dev, const S
   u64 g = (u64)per_sm * num_sms(dev);
   if (g > tiles) g = tiles;
   int grid = (int)g;
-  PIP_CUDA(cudaMemsetAsync(L.abort, 0, 64, st));
+  PIP_CUDA(cudaMemsetAsync(L.counter, 0, 60, st));
   PIP_CUDA(cudaMemsetAsync(L.slots, 0, sizeof(TileSlot) * 4 * (size_t)grid * lb_stride(num_sms(current_device()), grid), st));
   LookbackCtx c{L.slots, L.abort, (u32)(4 * grid), lb_stride(num_sms(current_device()), grid)};
   DevPred pp = p;
@@ -876,7 +914,7 @@ static int launch_filter_tma(u64* a, u64 n, const DevPred& p, u64* m_dev, const 
   u64 g = (u64)per_sm * num_sms(dev);
   if (g > tiles) g = tiles;
   int grid = (int)g;
-  PIP_CUDA(cudaMemsetAsync(L.abort, 0, 64, st));
+  PIP_CUDA(cudaMemsetAsync(L.counter, 0, 60, st));
   PIP_CUDA(cudaMemsetAsync(L.slots, 0, sizeof(TileSlot) * 4 * (size_t)grid * lb_stride(num_sms(current_device()), grid), st));
   LookbackCtx c{L.slots, L.abort, (u32)(4 * grid), lb_stride(num_sms(current_device()), grid)};
   DevPred pp = p;
@@ -902,7 +940,7 @@ static int launch_filter_ahead(u64* a, u64 n, const DevPred& p, u64* m_dev,
   if (g > full_tiles) g = full_tiles;
   int grid = (int)g;
   u64* mid = rem ? L.carry : m_dev;
-  PIP_CUDA(cudaMemsetAsync(L.abort, 0, 64, st));
+  PIP_CUDA(cudaMemsetAsync(L.counter, 0, 60, st));
   PIP_CUDA(cudaMemsetAsync(L.slots, 0, sizeof(TileSlot) * 4 * (size_t)grid * lb_stride(num_sms(current_device()), grid), st));
   LookbackCtx c{L.slots, L.abort, (u32)(4 * grid), lb_stride(num_sms(current_device()), grid)};
   DevPred pp = p;
@@ -932,7 +970,7 @@ static int launch_filter_ws_pc(u64* a, u64 n, const DevPred& p, u64* m_dev,
   if (g > full_tiles) g = full_tiles;
   int grid = (int)g;
   u64* mid = rem ? L.carry : m_dev;
-  PIP_CUDA(cudaMemsetAsync(L.abort, 0, 64, st));
+  PIP_CUDA(cudaMemsetAsync(L.counter, 0, 60, st));
   PIP_CUDA(cudaMemsetAsync(L.slots, 0, sizeof(TileSlot) * 4 * (size_t)grid * lb_stride(num_sms(current_device()), grid), st));
   LookbackCtx c{L.slots, L.abort, (u32)(4 * grid), lb_stride(num_sms(current_device()), grid)};
   DevPred pp = p;
@@ -961,7 +999,7 @@ static int launch_filter_ws2_pc(u64* a, u64 n, const DevPred& p, u64* m_dev,
   int grid = (int)g;
   u64* mid = rem ? L.carry : m_dev;
   const u32 stride = lb_stride(num_sms(dev), grid);
-  PIP_CUDA(cudaMemsetAsync(L.abort, 0, 64, st));
+  PIP_CUDA(cudaMemsetAsync(L.counter, 0, 60, st));
   PIP_CUDA(cudaMemsetAsync(L.slots, 0, sizeof(TileSlot) * 4 * (size_t)grid * stride, st));
   LookbackCtx c{L.slots, L.abort, (u32)(4 * grid), stride};
   DevPred pp = p;
@@ -1058,6 +1096,37 @@ int filter_device(u64* a, u64 n, const pip_pred* pred, u64* m_dev, void* scratch
              : launch_filter<false>(a, n, p, m_dev, L, st, dev);
 }
 
+int compact_mask_device(u64* a, u64 n, const unsigned char* mask, u64* m_dev, void* scratch,
+                        size_t scratch_bytes, cudaStream_t st) {
+  const int dev = current_device();
+  const int sms = num_sms(dev);
+  if ((n && (!a || !mask)) || !m_dev) return PIP_ERR_INVALID_ARG;
+  if (!scratch || scratch_bytes < scratch_bytes_for(sms)) return PIP_ERR_OOM;
+  if (n == 0) {
+    PIP_CUDA(cudaMemsetAsync(m_dev, 0, 8, st));
+    return PIP_OK;
+  }
+  ScratchLayoutF L = carve_f(scratch, sms);
+  // the vector path needs 16-byte aligned words and 2-byte aligned flags
+  const bool vec = ((uintptr_t)a & 15) == 0 && ((uintptr_t)mask & 1) == 0;
+  const u64 tiles = (n + FILTER_TILE - 1) / FILTER_TILE;
+  const void* k = vec ? (const void*)compact_mask_kernel<true> : (const void*)compact_mask_kernel<false>;
+  int per_sm = 0;
+  PIP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, FILTER_THREADS, 0));
+  if (per_sm < 1) return PIP_ERR_UNSUPPORTED;
+  if (per_sm > 8) per_sm = 8;
+  u64 g = (u64)per_sm * sms;
+  if (g > tiles) g = tiles;
+  int grid = (int)g;
+  const u32 stride = lb_stride(sms, grid);
+  PIP_CUDA(cudaMemsetAsync(L.counter, 0, 60, st));
+  PIP_CUDA(cudaMemsetAsync(L.slots, 0, sizeof(TileSlot) * 4 * (size_t)grid * stride, st));
+  LookbackCtx c{L.slots, L.abort, (u32)(4 * grid), stride};
+  void* args[] = {&a, &n, (void*)&mask, &m_dev, &c, (void*)&tiles};
+  PIP_CUDA(cudaLaunchCooperativeKernel(k, dim3(grid), dim3(FILTER_THREADS), args, 0, st));
+  return PIP_OK;
+}
+
 int count_device(const u64* a, u64 n, const pip_pred* pred, u64* m_dev, void* scratch,
                  size_t scratch_bytes, cudaStream_t st) {
   const int dev = current_device();
@@ -1070,7 +1139,7 @@ int count_device(const u64* a, u64 n, const pip_pred* pred, u64* m_dev, void* sc
   int grid = sms * 2;
   u64 need = (n + 1023) / 1024;
   if ((u64)grid > need) grid = (int)(need ? need : 1);
-  PIP_CUDA(cudaMemsetAsync(L.abort, 0, 64, st));
+  PIP_CUDA(cudaMemsetAsync(L.counter, 0, 60, st));
   switch (pred_class(p)) {
     case PC_MASK: count_kernel<PC_MASK><<<grid, 512, 0, st>>>(a, n, p, L.partials, L.counter, m_dev); break;
     case PC_MOD: count_kernel<PC_MOD><<<grid, 512, 0, st>>>(a, n, p, L.partials, L.counter, m_dev); break;

@@ -1180,7 +1180,7 @@ int merge_device(u64* a, u64 n, u64 split, int check_sorted, void* ws, size_t ws
   MergeGlobal gh{};
   PIP_CUDA(cudaMemcpyAsync(&gh, M.g, sizeof(gh), cudaMemcpyDeviceToHost, st));
   PIP_CUDA(cudaStreamSynchronize(st));
-  if (gh.sync.abort) return PIP_ERR_CUDA;
+  if (gh.sync.abort) return PIP_ERR_STALLED;
   if (timing_enabled() && (M.dbg & 4))
     fprintf(stderr, "[pip merge] CTA0 cycles: merge warps: wait data %llu | merge %llu | wait output buffer %llu | write-out %llu ; "
             "loader: refills/publishes %llu | watcher: dataflow wait %llu | missing-reader polls after m %llu before m %llu\n",

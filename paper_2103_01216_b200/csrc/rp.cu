@@ -1002,7 +1002,7 @@ int rp_device(u64* a, const u64* h, u64 n, u64 prefix, int variant, int debug,
     PIP_CUDA(cudaMemcpyAsync(&R, A.resume, sizeof(R), cudaMemcpyDeviceToHost, st));
     PIP_CUDA(cudaMemcpyAsync(&Gh, A.g, sizeof(Gh), cudaMemcpyDeviceToHost, st));
     PIP_CUDA(cudaStreamSynchronize(st));
-    if (Gh.sync.abort) return PIP_ERR_CUDA;
+    if (Gh.sync.abort) return PIP_ERR_STALLED;
     // counts are recorded in P1 of the following round: all rounds but the
     // last completed one are available (all of them once done)
     const u64 have = R.done ? R.rounds : (R.rounds ? R.rounds - 1 : 0);

@@ -860,7 +860,7 @@ static int launch_scan_t(u64* a, u64 n, u64 init, const u64* carry, u64* total,
   int grid = 0;
   int rc = persistent_grid(k, SCAN_THREADS, device, tiles, &grid);
   if (rc) return rc;
-  PIP_CUDA(cudaMemsetAsync(L.abort, 0, 64, st));
+  PIP_CUDA(cudaMemsetAsync(L.counter, 0, 60, st));
   PIP_CUDA(cudaMemsetAsync(L.slots, 0, sizeof(TileSlot) * 4 * (size_t)grid * lb_stride(num_sms(current_device()), grid), st));
   LookbackCtx c{L.slots, L.abort, (u32)(4 * grid), lb_stride(num_sms(current_device()), grid)};
   u32* counter = L.counter;
@@ -885,7 +885,7 @@ static int launch_scan_tma(u64* a, u64 n, u64 init, const u64* carry, u64* total
   u64 g = (u64)per_sm * num_sms(device);
   if (g > tiles) g = tiles;
   int grid = (int)g;
-  PIP_CUDA(cudaMemsetAsync(L.abort, 0, 64, st));
+  PIP_CUDA(cudaMemsetAsync(L.counter, 0, 60, st));
   PIP_CUDA(cudaMemsetAsync(L.slots, 0, sizeof(TileSlot) * 4 * (size_t)grid * lb_stride(num_sms(current_device()), grid), st));
   LookbackCtx c{L.slots, L.abort, (u32)(4 * grid), lb_stride(num_sms(current_device()), grid)};
   u32* counter = L.counter;
@@ -912,7 +912,7 @@ static int launch_scan_ahead(u64* a, u64 n, u64 init, const u64* carry, u64* tot
   int grid = (int)g;
   // the whole-tile part writes its inclusive fold to `mid` when a tail follows
   u64* mid = rem ? L.carry : total;
-  PIP_CUDA(cudaMemsetAsync(L.abort, 0, 64, st));
+  PIP_CUDA(cudaMemsetAsync(L.counter, 0, 60, st));
   PIP_CUDA(cudaMemsetAsync(L.slots, 0, sizeof(TileSlot) * 4 * (size_t)grid * lb_stride(num_sms(current_device()), grid), st));
   LookbackCtx c{L.slots, L.abort, (u32)(4 * grid), lb_stride(num_sms(current_device()), grid)};
   void* args[] = {&a, &init, &carry, &mid, &c, (void*)&full_tiles};
@@ -942,7 +942,7 @@ static int launch_scan_ws(u64* a, u64 n, u64 init, const u64* carry, u64* total,
   if (g > full_tiles) g = full_tiles;
   int grid = (int)g;
   u64* mid = rem ? L.carry : total;
-  PIP_CUDA(cudaMemsetAsync(L.abort, 0, 64, st));
+  PIP_CUDA(cudaMemsetAsync(L.counter, 0, 60, st));
   PIP_CUDA(cudaMemsetAsync(L.slots, 0, sizeof(TileSlot) * 4 * (size_t)grid * lb_stride(num_sms(current_device()), grid), st));
   LookbackCtx c{L.slots, L.abort, (u32)(4 * grid), lb_stride(num_sms(current_device()), grid)};
   u32* counter = L.counter;
@@ -995,7 +995,7 @@ static int launch_scan_ws2(u64* a, u64 n, u64 init, const u64* carry, u64* total
   int grid = (int)g;
   u64* mid = rem ? L.carry : total;
   const u32 stride = lb_stride(num_sms(device), grid);
-  PIP_CUDA(cudaMemsetAsync(L.abort, 0, 64, st));
+  PIP_CUDA(cudaMemsetAsync(L.counter, 0, 60, st));
   PIP_CUDA(cudaMemsetAsync(L.slots, 0, sizeof(TileSlot) * 4 * (size_t)grid * stride, st));
   LookbackCtx c{L.slots, L.abort, (u32)(4 * grid), stride};
   void* args[] = {&a, &init, &carry, &mid, &c, (void*)&full_tiles};
@@ -1075,13 +1075,6 @@ static int launch_scan_op(u64* a, u64 n, u64 init, int inclusive, const u64* car
              : launch_scan_t<OP, false, false>(a, n, init, carry, total, L, st, device);
 }
 
-int check_abort(void* scratch, cudaStream_t st) {
-  u32 h = 0;
-  PIP_CUDA(cudaMemcpyAsync(&h, scratch, sizeof(u32), cudaMemcpyDeviceToHost, st));
-  PIP_CUDA(cudaStreamSynchronize(st));
-  return h ? PIP_ERR_CUDA : PIP_OK;
-}
-
 int scan_device(u64* a, u64 n, int op, u64 init, int inclusive, const u64* carry_dev,
                 u64* total_dev, void* scratch, size_t scratch_bytes, cudaStream_t st) {
   const int dev = current_device();
@@ -1112,7 +1105,7 @@ static int launch_reduce(const u64* a, u64 n, u64* total, const ScratchLayout& L
   int grid = sms * 2;
   u64 need = (n + 1023) / 1024;
   if ((u64)grid > need) grid = (int)(need ? need : 1);
-  PIP_CUDA(cudaMemsetAsync(L.abort, 0, 64, st));
+  PIP_CUDA(cudaMemsetAsync(L.counter, 0, 60, st));
   reduce_kernel<OP><<<grid, 512, 0, st>>>(a, n, L.partials, L.counter, total);
   PIP_CHECK_LAUNCH();
   return PIP_OK;

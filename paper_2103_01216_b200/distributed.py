@@ -80,6 +80,7 @@ class CudaOps(LocalOps):
         out = torch.zeros(1, dtype=torch.int64, device=self.device)
         _lib.check(self.lib.pip_reduce_u64(t.data_ptr(), t.numel(), 0, out.data_ptr(), sp, sb, st),
                    "reduce")
+        _lib.check_stall(sp, st, "reduce")
         return out
 
     def scan_carry(self, t, carry, inclusive):
@@ -90,6 +91,7 @@ class CudaOps(LocalOps):
         _lib.check(self.lib.pip_scan_u64_carry(t.data_ptr(), t.numel(), 0, 0, int(inclusive),
                                                carry.data_ptr(), tot.data_ptr(), sp, sb, st),
                    "scan")
+        _lib.check_stall(sp, st, "scan")
 
     def filter(self, t, pred):
         from . import strong

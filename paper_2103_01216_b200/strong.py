@@ -86,6 +86,7 @@ def _scan_impl(a, op, identity, inclusive: bool) -> ScanResult:
             tot = small_device_words(1, w.device)
             _lib.check(lib.pip_scan_u64(w.ptr, n, code, init, 1 if inclusive else 0, tot.data_ptr(),
                                         sp, sb, st), "scan")
+            _lib.check_stall(sp, st, "scan")
             total = int(tot.item()) & M64
     else:
         out = C.c_uint64(0)
@@ -129,6 +130,7 @@ def reduce(a, op=None, identity: int = 0) -> int:
             sp, sb = scratch_for(w.device, st)
             tot = small_device_words(1, w.device)
             _lib.check(lib.pip_reduce_u64(w.ptr, w.n, code, tot.data_ptr(), sp, sb, st), "reduce")
+            _lib.check_stall(sp, st, "reduce")
             return int(tot.item()) & M64
     # host array: stream it through the device with a read-only scan copy
     import torch
@@ -190,6 +192,7 @@ def filter_kway(a, pred, n: int | None = None) -> int:
             m = small_device_words(1, w.device)
             _lib.check(lib.pip_filter_u64(w.ptr, n, C.byref(desc), m.data_ptr(), sp, sb, st),
                        "filter")
+            _lib.check_stall(sp, st, "filter")
             return int(m.item())
     out = C.c_uint64(0)
     _lib.check(lib.pip_filter_u64_host(w.ptr, n, C.byref(desc), C.byref(out), _device_index()),

@@ -17,6 +17,7 @@ GOLDEN = ROOT / "tests" / "golden"
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200)")
+    config.addinivalue_line("markers", "fullsize: BASELINE configs at full size (GPU, minutes)")
     config.addinivalue_line("markers", "reference: needs the reference package (build container only)")
 
 

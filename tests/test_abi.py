@@ -46,7 +46,7 @@ def test_status_strings_and_version():
 
     lib = _lib.load()
     assert lib.pip_version() == 1
-    for code in range(10):
+    for code in range(11):
         assert lib.pip_status_string(code)
     assert b"unsorted" in lib.pip_status_string(_lib.PIP_ERR_UNSORTED)
 
