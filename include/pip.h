@@ -280,6 +280,10 @@ size_t pip_merge_workspace_bytes(uint64_t n, uint64_t split, uint64_t budget_wor
  * device merge, copy back. */
 int pip_merge_u64_host(uint64_t* host_a, uint64_t n, uint64_t split, uint64_t budget_words,
                        int device);
+/* device workspace (bytes) pip_merge_u64_host uses besides its staging copy
+ * of the array: the output ring (or, with PIP_MERGE_HOST_INPLACE=1, the
+ * device merge's workspace) — what a relaxed caller charges to its meter. */
+size_t pip_merge_host_workspace_bytes(uint64_t n, uint64_t split, uint64_t budget_words);
 
 /* ---- random permutation: relaxed.random_permutation (relaxed.py:220-251) - *
  * Applies the Knuth swap sequence H (swap a[i], a[H[i]] for i = n-1..0) as

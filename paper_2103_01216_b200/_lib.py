@@ -87,6 +87,7 @@ SIGNATURES = {
     "pip_merge_u64": (i32, [vp, u64, u64, i32, vp, sz, vp, sz, vp]),
     "pip_merge_workspace_bytes": (sz, [u64, u64, u64]),
     "pip_merge_u64_host": (i32, [vp, u64, u64, u64, i32]),
+    "pip_merge_host_workspace_bytes": (sz, [u64, u64, u64]),
     "pip_rp_workspace_bytes": (sz, [u64, u64, i32]),
     "pip_random_permutation_u64": (
         i32, [vp, vp, u64, u64, i32, i32, vp, u64, vp, vp, sz, C.POINTER(PipRpStats), vp]),

@@ -214,7 +214,7 @@ def tree_contract(tree: BinaryTree, p, values, budget: EpsilonConfig = DEFAULT_B
     from .runtime import charge, uncharge
 
     qwords = qcap
-    charge(qwords)
+    _charged = charge(qwords)
     base = buf.ptr
     d_ids, d_sorted = base, base + ids_bytes
     d_flags = base + 2 * ids_bytes
@@ -357,7 +357,7 @@ def tree_contract(tree: BinaryTree, p, values, budget: EpsilonConfig = DEFAULT_B
         torch.cuda.current_stream(dev).synchronize()
     finally:
         release(buf)
-        uncharge(qwords)
+        uncharge(qwords, _charged)
     if host_mode:
         tree.parent[:] = pa.cpu().numpy().view(np.uint64)
         tree.left[:] = lf.cpu().numpy().view(np.uint64)

@@ -363,17 +363,44 @@ static u64 host_corank(const u64* a, u64 na, const u64* b, u64 nb, u64 r) {
   return lo;
 }
 
-int merge_host_stream(u64* host, u64 n, u64 split, u64 budget_words, int device) {
-  const u64 na = split, nb = n - split;
+// the streamed merge's output ring: the only device memory besides the
+// uploaded runs (the array's device copy is staging, like every *_host
+// path's); kept within a relaxed budget (>= 2^16 words per buffer)
+static u64 merge_host_chunk(u64 n, u64 budget_words, int nbuf) {
   u64 chunk = host_chunk();
-  const int nbuf = host_nbuf();
-  // the ring is the only device memory besides the uploaded runs: keep it
-  // within a relaxed budget (>= 2^16 words per buffer)
   if (budget_words && chunk * (u64)nbuf > budget_words) {
     chunk = budget_words / (u64)nbuf;
     if (chunk < (1ull << 16)) chunk = 1ull << 16;
   }
-  if (chunk > n) chunk = n;
+  return chunk > n ? n : chunk;
+}
+static bool merge_host_inplace() {
+  const char* e = getenv("PIP_MERGE_HOST_INPLACE");
+  return e && atoi(e);
+}
+static u64 merge_host_ring_words(u64 n, u64 budget_words) {
+  const int nbuf = host_nbuf();
+  const u64 chunk = merge_host_chunk(n, budget_words, nbuf);
+  const u64 nchunks = (n + chunk - 1) / chunk;
+  const u64 nr = nchunks < (u64)nbuf ? nchunks : (u64)nbuf;
+  return nr * chunk;
+}
+// a relaxed call whose budget the ring would exceed (small n: one chunk of
+// n words; tiny budgets: the 2^16-word floor) merges in place on the device
+// with the budgeted workspace instead
+static bool merge_host_use_inplace(u64 n, u64 budget_words) {
+  return merge_host_inplace() || (budget_words && merge_host_ring_words(n, budget_words) > budget_words);
+}
+size_t merge_host_workspace_bytes(u64 n, u64 split, u64 budget_words) {
+  if (split > n || n < 2 || split == 0 || split == n) return 0;
+  if (merge_host_use_inplace(n, budget_words)) return merge_workspace_bytes(n, split, budget_words);
+  return (size_t)(merge_host_ring_words(n, budget_words) * 8);
+}
+
+int merge_host_stream(u64* host, u64 n, u64 split, u64 budget_words, int device) {
+  const u64 na = split, nb = n - split;
+  const int nbuf = host_nbuf();
+  const u64 chunk = merge_host_chunk(n, budget_words, nbuf);
   const u64 nchunks = (n + chunk - 1) / chunk;
   std::vector<u64> ci(nchunks + 1);
   for (u64 k = 0; k <= nchunks; ++k) {
@@ -743,13 +770,16 @@ int pip_merge_u64(uint64_t* a, uint64_t n, uint64_t split, int check_sorted, voi
                       scratch_bytes, (cudaStream_t)stream);
 }
 
+size_t pip_merge_host_workspace_bytes(uint64_t n, uint64_t split, uint64_t budget_words) {
+  return merge_host_workspace_bytes(n, split, budget_words);
+}
+
 int pip_merge_u64_host(uint64_t* host_a, uint64_t n, uint64_t split, uint64_t budget_words,
                        int device) {
   if (split > n || (n && !host_a)) return PIP_ERR_INVALID_ARG;
   PIP_CUDA(cudaSetDevice(device));
   if (n < 2 || split == 0 || split == n) return PIP_OK;
-  const char* e = getenv("PIP_MERGE_HOST_INPLACE");
-  if (e && atoi(e)) {  // upload everything, merge in place on the device, copy back
+  if (merge_host_use_inplace(n, budget_words)) {  // upload all, in-place device merge, copy back
     DevBuf a, ws, scratch;
     Stream s;
     PIP_CUDA(s.create());

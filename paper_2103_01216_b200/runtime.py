@@ -35,7 +35,7 @@ __all__ = [
     "as_words", "make_words", "Words",
     "set_num_threads", "num_threads",
     "SpaceMeter", "MeterReport", "meter_scope", "metered", "alloc", "release", "aux",
-    "Rng", "EpsilonConfig", "POWER_ONLY_FRACTION",
+    "Rng", "EpsilonConfig", "POWER_ONLY_FRACTION", "compact_by_mask",
 ]
 
 
@@ -191,10 +191,33 @@ def _charge_words(nbytes: int) -> int:
     return (nbytes + 7) // 8
 
 
+def _caller_meter():
+    """The reference's own active meter, when the caller runs inside
+    ``pipal.runtime.metered`` / ``meter_scope`` (runtime.py:194-207): GPU
+    workspace is charged to it too, so a pipal user measuring a drop-in call
+    sees its words (not only users of this package's meter)."""
+    import sys
+
+    ref = sys.modules.get("pipal.runtime")
+    stack = getattr(ref, "_meter_stack", None) if ref is not None else None
+    return stack[-1] if stack else None
+
+
+def _active_meters() -> list:
+    out = []
+    m = _active_meter()
+    if m is not None:
+        out.append(m)
+    c = _caller_meter()
+    if c is not None and all(c is not x for x in out):
+        out.append(c)
+    return out
+
+
 class DeviceBuffer:
     """Charged device workspace (the GPU counterpart of runtime.alloc)."""
 
-    __slots__ = ("tensor", "nbytes", "words", "_released")
+    __slots__ = ("tensor", "nbytes", "words", "_released", "_meters")
 
     def __init__(self, nbytes: int, device: int):
         torch = _torch()
@@ -202,8 +225,8 @@ class DeviceBuffer:
         self.tensor = torch.empty(max(self.nbytes, 16), dtype=torch.uint8, device=f"cuda:{device}")
         self.words = _charge_words(self.nbytes)
         self._released = False
-        m = _active_meter()
-        if m is not None:
+        self._meters = _active_meters()
+        for m in self._meters:
             m.acquire(self.words)
 
     @property
@@ -215,16 +238,17 @@ def alloc(nbytes: int, device: int) -> DeviceBuffer:
     return DeviceBuffer(nbytes, device)
 
 
-def charge(words: int) -> None:
-    """Charge words for workspace allocated inside a host-path C call."""
-    m = _active_meter()
-    if m is not None:
+def charge(words: int) -> list:
+    """Charge words for workspace allocated inside a host-path C call;
+    returns the meters charged (pass them to ``uncharge``)."""
+    ms = _active_meters()
+    for m in ms:
         m.acquire(words)
+    return ms
 
 
-def uncharge(words: int) -> None:
-    m = _active_meter()
-    if m is not None:
+def uncharge(words: int, meters: list | None = None) -> None:
+    for m in (meters if meters is not None else _active_meters()):
         m.release(words)
 
 
@@ -232,8 +256,7 @@ def release(buf: DeviceBuffer) -> None:
     if buf._released:
         return
     buf._released = True
-    m = _active_meter()
-    if m is not None:
+    for m in buf._meters:
         m.release(buf.words)
     buf.tensor = None
 
@@ -361,3 +384,47 @@ class EpsilonConfig:
             return 1
         b = max(math.ceil(n ** (1.0 - self.epsilon)), math.floor(self.prefix_fraction * n))
         return min(max(b, 1), n)
+
+
+# ---------------------------------------------------------------------------
+# shared in-place primitive (runtime.py:335-355)
+
+def compact_by_mask(arr, keep, n: int | None = None) -> int:
+    """Stable in-place compaction of arr[i] with keep[i]; returns the new count.
+
+    Runs on the device (``pip_compact_by_mask_u64``: the look-back filter
+    with the keep flags read from a byte mask, O(#CTAs) scratch, zero heap
+    like the reference's SCRATCH_WORDS blocks).  ``arr``: numpy uint64 (copied
+    through the device and back in place) or a CUDA int64/uint64 tensor;
+    ``keep``: a bool / uint8 array of at least ``n`` flags (numpy or CUDA).
+    Only arr[0:n) is compacted; arr[m:n) is unspecified afterwards.
+    """
+    w: Words = as_words(arr, _wrap=True)
+    n = w.n if n is None else int(n)
+    if n < 0 or n > w.n or len(keep) < n:
+        raise ValueError("n out of range")
+    if n == 0:
+        return 0
+    torch = _torch()
+    lib = _lib.load()
+    if not w.is_device:
+        dev = torch.cuda.current_device()
+        t = torch.from_numpy(w.obj[:n].view(np.int64)).to(f"cuda:{dev}")
+        m = compact_by_mask(t, keep, n)
+        w.obj[:m] = t[:m].cpu().numpy().view(np.uint64)
+        return m
+    if isinstance(keep, np.ndarray):
+        k = torch.from_numpy(np.ascontiguousarray(keep[:n]).view(np.uint8)).to(f"cuda:{w.device}")
+    else:
+        k = keep[:n]
+        if k.device != w.obj.device:
+            raise ValueError("keep mask must live on the array's device")
+        k = (k.view(torch.uint8) if k.dtype == torch.bool else k.to(torch.uint8)).contiguous()
+    with torch.cuda.device(w.device):
+        st = w.stream()
+        sp, sb = scratch_for(w.device, st)
+        out = small_device_words(1, w.device)
+        _lib.check(lib.pip_compact_by_mask_u64(w.ptr, n, k.data_ptr(), out.data_ptr(), sp, sb, st),
+                   "compact_by_mask")
+        _lib.check_stall(sp, st, "compact_by_mask")
+        return int(out.item())

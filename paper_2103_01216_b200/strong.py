@@ -216,13 +216,13 @@ def _partition_impl(a, pred, n: int | None, meter_workspace: bool) -> int:
         if meter_workspace:
             from .runtime import charge, uncharge
 
-            charge((wb + 7) // 8)
+            _charged = charge((wb + 7) // 8)
         try:
             _lib.check(lib.pip_partition_u64_host(w.ptr, n, C.byref(desc), C.byref(out),
                                                   _device_index()), "partition")
         finally:
             if meter_workspace:
-                uncharge((wb + 7) // 8)
+                uncharge((wb + 7) // 8, _charged)
         return int(out.value)
     import torch
 
@@ -376,17 +376,20 @@ def _merge_impl(a, split: int, debug: bool, budget_words: int, meter_workspace: 
                                                              meter_workspace))
         if split == 0 or split == n or n < 2:
             return None
-        wb = lib.pip_merge_workspace_bytes(n, split, budget_words)
+        # the streamed host merge's auxiliary device memory is its output
+        # ring (the device copy of the array is staging, as on every host
+        # path); that ring is what a relaxed call charges
+        wb = lib.pip_merge_host_workspace_bytes(n, split, budget_words)
         words = (wb + 7) // 8
         if meter_workspace:
             from .runtime import charge, uncharge
 
-            charge(words)
+            _charged = charge(words)
             try:
                 _lib.check(lib.pip_merge_u64_host(w.ptr, n, split, budget_words, _device_index()),
                            "merge")
             finally:
-                uncharge(words)
+                uncharge(words, _charged)
         else:
             _lib.check(lib.pip_merge_u64_host(w.ptr, n, split, budget_words, _device_index()),
                        "merge")

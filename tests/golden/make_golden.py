@@ -245,7 +245,53 @@ def make_rng():
     np.savez_compressed(OUT / "rng.npz", **d)
 
 
+def make_detres():
+    """ReservationTable slot layouts after seeded batches (detres.py:40-211):
+    the device table reproduces the reference's probe steps, so its key and
+    value arrays must equal these word for word; plus compact_by_mask."""
+    from pipal import detres
+    from pipal.runtime import compact_by_mask
+
+    d = {}
+    cases = {
+        "small": (16, [(np.array([5, 5, 5], dtype=np.uint64), np.array([3, 9, 5], dtype=np.uint64))]),
+        "collide": (32, [(np.array([1, 9, 17, 25, 33], dtype=np.uint64),) * 2]),
+    }
+    rng = np.random.default_rng(42)
+    keys = rng.integers(0, 500, size=10_000, dtype=np.uint64)
+    vals = rng.integers(0, 1 << 63, size=10_000, dtype=np.uint64)
+    cases["batches"] = (2048, [(keys[s:s + 700], vals[s:s + 700]) for s in range(0, 10_000, 700)])
+    big_k = rng.integers(0, 1 << 64, size=7_000, dtype=np.uint64)
+    big_v = rng.integers(0, 1 << 64, size=7_000, dtype=np.uint64)
+    cases["dense"] = (1 << 14, [(big_k[:5_000], big_v[:5_000]), (big_k[3_000:], big_v[3_000:])])
+    for name, (cap, batches) in cases.items():
+        t = detres.ReservationTable(cap)
+        for i, (k, v) in enumerate(batches):
+            d[f"{name}_k{i}"] = k
+            d[f"{name}_v{i}"] = v
+            t.reserve_max(k, v)
+        d[f"{name}_cap"] = np.array([cap, len(batches), t.count], dtype=np.uint64)
+        d[f"{name}_peak"] = np.array([t.peak_load])
+        d[f"{name}_keys"] = t.keys.copy()
+        d[f"{name}_vals"] = np.where(t.keys != np.uint64((1 << 64) - 1), t.vals, 0).astype(np.uint64)
+        dk = batches[0][0][::2]
+        t.delete(dk)
+        d[f"{name}_delk"] = dk
+        d[f"{name}_keys_after_delete"] = t.keys.copy()
+        d[f"{name}_count_after_delete"] = np.array([t.count], dtype=np.uint64)
+    for n in (1, 255, 256, 257, 10_000, 20_011):
+        a = rand_words(n + 1, n)
+        keep = np.random.default_rng(n).random(n) < 0.37
+        b = a.copy()
+        m = compact_by_mask(b, keep, n)
+        d[f"compact_in_{n}"] = a
+        d[f"compact_keep_{n}"] = keep
+        d[f"compact_out_{n}"] = b[:m]
+    np.savez_compressed(OUT / "detres.npz", **d)
+
+
 if __name__ == "__main__":
+    make_detres()
     make_scan()
     make_filter()
     make_partition()

@@ -83,3 +83,26 @@ def test_host_logic_vs_reference(ref):
         assert R.Rng(seed).derive(5).seed == ref.runtime.Rng(seed).derive(5).seed
         assert np.array_equal(make_swap_sequence(1000, R.Rng(seed)),
                               ref.relaxed.make_swap_sequence(1000, ref.runtime.Rng(seed)))
+
+
+def test_charges_reach_the_callers_pipal_meter(ref):
+    """A pipal user measuring a drop-in call inside pipal.runtime.metered
+    sees the GPU workspace words (runtime.py:194-253 of the reference)."""
+    from paper_2103_01216_b200 import runtime as rt
+
+    pm = ref.runtime.SpaceMeter()
+    own = rt.SpaceMeter()
+    with ref.runtime.metered(pm):
+        ms = rt.charge(123)
+        assert pm.current_words == 123
+        rt.uncharge(123, ms)
+        with rt.metered(own):
+            ms = rt.charge(7)
+            assert own.current_words == 7 and pm.current_words == 7
+            rt.uncharge(7, ms)
+    assert pm.current_words == 0 and pm.peak_words == 123 and own.peak_words == 7
+    # no pipal meter active: only the drop-in's own meter is charged
+    with rt.metered(own):
+        ms = rt.charge(5)
+        assert len(ms) == 1 and own.current_words == 5
+        rt.uncharge(5, ms)
