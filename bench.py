@@ -11,9 +11,11 @@ resident in HBM.  `--op` selects the other configs for our own measurements:
   rp0     configs[0]  random permutation, n = 10^6, H from PCG64(seed)
   partition  SURVEY 8(f) row 3 (not a BASELINE config): unstable in-place
           partition, 2^32 words with the configs[2] inputs and predicate
-Multi-GPU (torchrun, WORLD_SIZE = N > 1): scan is sharded (strong scaling,
-2^32 / N words per rank; local reduce -> NCCL all_gather of shard totals ->
-scan with a device carry-in).  `--impl reference` times the CPU reference
+Multi-GPU (torchrun, WORLD_SIZE = N > 1), strong scaling over 2^32 / N words
+per rank: scan (local reduce -> NCCL all_gather of shard totals -> scan with
+a device carry-in), filter (local filter -> in-place NCCL P2P moves to the
+global packed prefix) and merge (collective co-ranks -> in-place rotations
+of shard pieces -> local merge); see paper_2103_01216_b200/distributed.py.  `--impl reference` times the CPU reference
 path (the C port of the reference's own algorithm in oracle/) instead.
 """
 from __future__ import annotations
@@ -68,8 +70,17 @@ def dist_init():
         import torch
         import torch.distributed as dist
 
+        # PIP_DIST_BACKEND=gloo + PIP_ONE_GPU=1: every rank on cuda:0 with
+        # gloo (functional test of the sharded paths on a one-GPU box; the
+        # numbers of such a run are not bench values)
+        if os.environ.get("PIP_ONE_GPU") == "1":
+            local = 0
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        backend = os.environ.get("PIP_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        else:
+            dist.init_process_group(backend)
     return ws, rank, local
 
 
@@ -227,11 +238,17 @@ def run_scan(args, ws, rank, local, torch, pip, lib):
     else:
         import torch.distributed as dist
 
+        nccl = dist.get_backend() == "nccl"
+
         def step():
             # shard total -> all ranks' totals -> exclusive carry -> scan with carry
             rc = lib.pip_reduce_u64(a.data_ptr(), n, 0, tot.data_ptr(), sp, sb, sptr)
             assert rc == 0, rc
-            dist.all_gather_into_tensor(gathered, tot[:1])
+            if nccl:
+                dist.all_gather_into_tensor(gathered, tot[:1])
+            else:  # gloo (functional one-GPU runs): list form
+                parts = list(gathered.split(1))
+                dist.all_gather(parts, tot[:1].clone())
             torch.sum(gathered[:rank], dim=0, keepdim=True, out=carry) if rank else carry.zero_()
             rc = lib.pip_scan_u64_carry(a.data_ptr(), n, 0, 0, 1, carry.data_ptr(),
                                         tot[1:].data_ptr(), sp, sb, sptr)
@@ -292,15 +309,17 @@ def run_scan(args, ws, rank, local, torch, pip, lib):
                 clocks=clocks, launches=launches * args.steps, extra=extra)
 
 
-def regen_timed(step, regen, steps, torch, st):
+def regen_timed(step, regen, steps, torch, st, ws: int = 1):
     """Per-step CUDA-event timing for destructive in-place ops: the input is
-    regenerated between steps OUTSIDE the timed events."""
+    regenerated between steps OUTSIDE the timed events (ranks meet at a
+    barrier before each timed step)."""
     total = 0.0
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     for _ in range(steps):
         regen()
         torch.cuda.synchronize()
+        barrier(ws)
         e0.record(st)
         step()
         e1.record(st)
@@ -366,9 +385,169 @@ def check_merge_windows(a, orig, na, torch):
         assert np.array_equal(got, want), f"merge parity failed on output window [{r0}, {r1})"
 
 
+def _wsum(t, w, torch):
+    """sum(t * w) mod 2^64 (int64 wrap-around) as a python int."""
+    return int((t * w).sum().item()) & ((1 << 64) - 1)
+
+
+def run_filter_sharded(args, ws, rank, local, torch, pip, lib):
+    """configs[2] over ws GPUs (strong scaling): rank r filters its 2^32/ws
+    words, then the kept words move in place to the global packed prefix
+    (distributed.sharded_filter)."""
+    import torch.distributed as dist
+
+    from paper_2103_01216_b200 import distributed as D
+
+    n_total = 1 << (args.log2n or 32)
+    lo, hi = D.shard_bounds(n_total, ws, rank)
+    n = hi - lo
+    dev = local
+    st = torch.cuda.current_stream()
+    a = torch.empty(n, dtype=torch.int64, device=f"cuda:{dev}")
+    rng = pip.Rng(args.seed)
+    regen = lambda: rng.words_device(lo, hi, shift=1, device=dev, out=a)  # noqa: E731
+    p = pip.pred.mod_eq(3, 0)
+    ops = D.CudaOps()
+    res = {}
+
+    def step():
+        res["m"] = D.sharded_filter(a, n_total, p, ops)
+
+    # parity of the first step by an order-sensitive checksum: every kept
+    # word x with global kept rank k contributes x * (k + 1) (mod 2^64);
+    # computed from the input shards and from the packed output
+    regen()
+    keep = (a % 3) == 0
+    c = int(keep.sum().item())
+    cnt = torch.tensor([c], dtype=torch.int64, device=a.device)
+    allc = [torch.zeros_like(cnt) for _ in range(ws)]
+    dist.all_gather(allc, cnt)
+    off = sum(int(x.item()) for x in allc[:rank])
+    kept = a[keep]
+    w_in = torch.tensor([_wsum(kept, torch.arange(off + 1, off + 1 + c, device=a.device), torch),
+                         _wsum(kept, 1, torch)], dtype=torch.int64, device=a.device)
+    del kept, keep
+    step()
+    torch.cuda.synchronize()
+    m = res["m"]
+    assert m == sum(int(x.item()) for x in allc), "sharded filter count"
+    top = max(0, min(hi, m) - lo)
+    out = a[:top]
+    w_out = torch.tensor([_wsum(out, torch.arange(lo + 1, lo + 1 + top, device=a.device), torch),
+                          _wsum(out, 1, torch)], dtype=torch.int64, device=a.device)
+    both = torch.stack([w_in, w_out])
+    dist.all_reduce(both)
+    assert torch.equal(both[0], both[1]), "sharded filter checksum parity failed"
+    for _ in range(max(args.warmup - 1, 0)):
+        regen()
+        step()
+    torch.cuda.synchronize()
+    barrier(ws)
+    clk = ClockSampler(dev)
+    ms = regen_timed(step, regen, args.steps, torch, st, ws=ws)
+    clocks = clk.stop()
+    ms = max_over_ranks(ms, ws)
+    per_step = ms / args.steps
+    value = n_total * args.steps / (ms / 1e3)
+    pk = peaks()
+    algo = 8 * n + 8 * (m / ws)  # per GPU: read my shard once, write my share of the prefix
+    achieved = algo / (per_step / 1e3) / 1e9
+    roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": pk["hbm_gbs"], "unit": "GB/s",
+            "frac": round(achieved / pk["hbm_gbs"], 4), "traffic": None,
+            "note": "per GPU: 8 B/word of its shard + 8 B per word of its share of the packed "
+                    "prefix; the step also moves the kept words across GPUs (NCCL P2P)"}
+    cfg = {"workload": "stable in-place filter x % 3 == 0, BASELINE configs[2]", "n": n_total,
+           "n_per_rank": n, "values": f"Rng({args.seed}).words >> 1, in [0,2^63)", "kept": m,
+           "l2": "inputs larger than L2; input regenerated between steps (untimed)",
+           "parallelism": f"shard{ws}: local filter + in-place P2P moves to the global prefix",
+           "check": "order-sensitive checksum of the packed prefix vs the inputs",
+           "seed": args.seed}
+    return dict(value=value, per_step=per_step, roof=roof, e2e=None, cpu=None, cfg=cfg,
+                clocks=clocks, launches=2 * args.steps, extra={})
+
+
+def run_merge_sharded(args, ws, rank, local, torch, pip, lib):
+    """configs[3] over ws GPUs (strong scaling): each rank holds 2^32/ws words
+    of the two sorted runs; co-ranks by a collective 4096-ary search, the
+    shard interleave by in-place rotations (P2P mirror swaps), local merge
+    (distributed.sharded_merge)."""
+    import torch.distributed as dist
+
+    from paper_2103_01216_b200 import distributed as D
+
+    n_total = 1 << (args.log2n or 32)
+    na = n_total // 2
+    lo, hi = D.shard_bounds(n_total, ws, rank)
+    n = hi - lo
+    dev = local
+    st = torch.cuda.current_stream()
+    # every rank builds the same global sorted runs (same generator and sort
+    # as one GPU), keeps its shard as the pristine input, and checks its
+    # output window against the oracle from the global runs
+    g = torch.empty(n_total, dtype=torch.int64, device=f"cuda:{dev}")
+    pip.Rng(args.seed).words_device(0, n_total, shift=34, device=dev, out=g)
+    sort_run(g[:na], torch, pip)
+    sort_run(g[na:], torch, pip)
+    orig = g[lo:hi].clone()
+    A, B = g[:na], g[na:]
+    a = torch.empty(n, dtype=torch.int64, device=f"cuda:{dev}")
+    regen = lambda: a.copy_(orig)  # noqa: E731
+    ops = D.CudaOps()
+
+    def step():
+        D.sharded_merge(a, n_total, na, ops)
+
+    regen()
+    step()
+    torch.cuda.synchronize()
+    from oracle import oracle
+
+    w = min(n, 1 << 20)
+    for r0 in sorted({lo, lo + n // 2 - w // 2, hi - w}):
+        i0, i1 = merge_coranks(A, B, [r0, r0 + w], torch)
+        want = oracle.seq_merge(A[i0:i1].cpu().numpy().view(np.uint64),
+                                B[r0 - i0:r0 + w - i1].cpu().numpy().view(np.uint64))
+        got = a[r0 - lo:r0 - lo + w].cpu().numpy().view(np.uint64)
+        assert np.array_equal(got, want), f"sharded merge parity failed at {r0}"
+    assert bool((a[1:] >= a[:-1]).all().item())
+    ends = torch.stack([a[0], a[-1]])
+    alle = [torch.zeros_like(ends) for _ in range(ws)]
+    dist.all_gather(alle, ends)
+    assert all(int(alle[r][1]) <= int(alle[r + 1][0]) for r in range(ws - 1)), "shard order"
+    del g, A, B
+    torch.cuda.empty_cache()
+    for _ in range(max(args.warmup - 1, 0)):
+        regen()
+        step()
+    torch.cuda.synchronize()
+    barrier(ws)
+    clk = ClockSampler(dev)
+    ms = regen_timed(step, regen, args.steps, torch, st, ws=ws)
+    clocks = clk.stop()
+    ms = max_over_ranks(ms, ws)
+    per_step = ms / args.steps
+    value = n_total * args.steps / (ms / 1e3)
+    pk = peaks()
+    achieved = 16 * n / (per_step / 1e3) / 1e9
+    roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": pk["hbm_gbs"], "unit": "GB/s",
+            "frac": round(achieved / pk["hbm_gbs"], 4), "traffic": None,
+            "note": "per GPU: 16 B/word of its shard algorithmic; the step also rotates shard "
+                    "pieces across GPUs (log2(G) levels of P2P mirror swaps)"}
+    cfg = {"workload": "in-place merge of two sorted runs, BASELINE configs[3]", "n": n_total,
+           "n_per_rank": n, "split": na,
+           "values": f"Rng({args.seed}).words >> 34, in [0,2^30), runs sorted (untimed)",
+           "l2": "inputs larger than L2; shard restored from a pristine copy between steps "
+                 "(untimed)",
+           "parallelism": f"shard{ws}: co-ranks + in-place rotations + local merge",
+           "check": "oracle windows of each rank's output + global shard order",
+           "seed": args.seed}
+    return dict(value=value, per_step=per_step, roof=roof, e2e=None, cpu=None, cfg=cfg,
+                clocks=clocks, launches=args.steps, extra={})
+
+
 def run_filter(args, ws, rank, local, torch, pip, lib):
     if ws > 1:
-        raise SystemExit("filter is benchmarked on one GPU in this round")
+        return run_filter_sharded(args, ws, rank, local, torch, pip, lib)
     n = 1 << (args.log2n or 32)
     dev = local
     st = torch.cuda.current_stream()
@@ -494,7 +673,7 @@ def run_partition(args, ws, rank, local, torch, pip, lib):
 
 def run_merge(args, ws, rank, local, torch, pip, lib):
     if ws > 1:
-        raise SystemExit("merge is benchmarked on one GPU in this round")
+        return run_merge_sharded(args, ws, rank, local, torch, pip, lib)
     n = 1 << (args.log2n or 32)
     na = n // 2
     dev = local

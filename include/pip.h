@@ -175,6 +175,16 @@ int pip_rt_delete_u64(uint64_t* table_keys, uint64_t capacity, const uint64_t* k
 int pip_rotate_u64(uint64_t* a, uint64_t n, uint64_t o, void* scratch, size_t scratch_bytes,
                    void* stream);
 
+/* In-place reversal of a[0:n) (strong.py:67-82, the rotation's step). */
+int pip_reverse_u64(uint64_t* a, uint64_t n, void* stream);
+/* memmove inside one device array: a[dst : dst+len) = the old a[src :
+ * src+len).  Overlapping left moves run in ONE pass on the look-back
+ * machinery (scratch as pip_filter_u64; pip_scratch_status applies);
+ * disjoint ranges copy; overlapping right moves rotate a[src : dst+len).
+ * The sharded filter's local shift (distributed.py).                       */
+int pip_move_u64(uint64_t* a, uint64_t dst, uint64_t src, uint64_t len, void* scratch,
+                 size_t scratch_bytes, void* stream);
+
 /* ---- partition: strong.partition_unstable / relaxed.partition_relaxed ---- *
  * Unstable in-place partition (strong.py:394-419, relaxed.py:312-344): on
  * return a[0:m) holds the words with keep(x), a[m:n) the others (multiset

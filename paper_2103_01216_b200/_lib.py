@@ -70,6 +70,8 @@ SIGNATURES = {
     "pip_count_u64": (i32, [vp, u64, C.POINTER(PipPred), vp, vp, sz, vp]),
     "pip_filter_u64_host": (i32, [vp, u64, C.POINTER(PipPred), C.POINTER(u64), i32]),
     "pip_rotate_u64": (i32, [vp, u64, u64, vp, sz, vp]),
+    "pip_reverse_u64": (i32, [vp, u64, vp]),
+    "pip_move_u64": (i32, [vp, u64, u64, u64, vp, sz, vp]),
     "pip_compact_by_mask_u64": (i32, [vp, u64, vp, vp, vp, sz, vp]),
     "pip_rt_workspace_bytes": (sz, [u64]),
     "pip_rt_reserve_max_u64": (i32, [vp, vp, u64, vp, vp, u64, vp, sz, C.POINTER(u64), vp]),

@@ -61,6 +61,9 @@ int filter_device(u64* a, u64 n, const pip_pred* pred, u64* m_dev, void* scratch
 int count_device(const u64* a, u64 n, const pip_pred* pred, u64* m_dev, void* scratch,
                  size_t scratch_bytes, cudaStream_t st);
 int rotate_device(u64* a, u64 n, u64 o, cudaStream_t st);
+int reverse_device(u64* a, u64 n, cudaStream_t st);
+int move_device(u64* a, u64 dst, u64 src, u64 len, void* scratch, size_t scratch_bytes,
+                cudaStream_t st);
 int validate_device(const u64* h, u64 n, u64* nonself_dev, void* scratch, size_t scratch_bytes,
                     cudaStream_t st);
 int rng_words(u64* out, u64 lo, u64 count, u64 seed, u32 shift, cudaStream_t st);
@@ -666,6 +669,17 @@ int pip_rt_delete_u64(uint64_t* table_keys, uint64_t capacity, const uint64_t* k
                       void* workspace, size_t workspace_bytes, uint64_t* count_out, void* stream) {
   return rt_delete((u64*)table_keys, capacity, (const u64*)keys, n, workspace, workspace_bytes,
                    (u64*)count_out, (cudaStream_t)stream);
+}
+
+int pip_reverse_u64(uint64_t* a, uint64_t n, void* stream) {
+  if (n && !a) return PIP_ERR_INVALID_ARG;
+  return reverse_device((u64*)a, n, (cudaStream_t)stream);
+}
+
+int pip_move_u64(uint64_t* a, uint64_t dst, uint64_t src, uint64_t len, void* scratch,
+                 size_t scratch_bytes, void* stream) {
+  if (int rc = clear_stall(scratch, scratch_bytes, (cudaStream_t)stream)) return rc;
+  return move_device((u64*)a, dst, src, len, scratch, scratch_bytes, (cudaStream_t)stream);
 }
 
 int pip_rotate_u64(uint64_t* a, uint64_t n, uint64_t o, void* scratch, size_t scratch_bytes,

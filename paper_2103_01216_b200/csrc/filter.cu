@@ -1096,6 +1096,34 @@ int filter_device(u64* a, u64 n, const pip_pred* pred, u64* m_dev, void* scratch
              : launch_filter<false>(a, n, p, m_dev, L, st, dev);
 }
 
+// memmove inside one array: a[dst : dst+len) = a[src : src+len) (old
+// contents).  A left move runs the look-back filter with an always-true
+// predicate reading a[src:] and writing from a[dst:] — every tile writes only
+// below its own reads, after every earlier tile has read (the in-place
+// filter's argument), so overlapping ranges are safe in one pass; disjoint
+// ranges are a plain copy; an overlapping right move is a rotation of
+// a[src : dst+len) (in place, two passes).
+int rotate_device(u64* a, u64 n, u64 o, cudaStream_t st);
+int move_device(u64* a, u64 dst, u64 src, u64 len, void* scratch, size_t scratch_bytes,
+                cudaStream_t st) {
+  const int dev = current_device();
+  const int sms = num_sms(dev);
+  if (len == 0 || dst == src) return PIP_OK;
+  if (!a) return PIP_ERR_INVALID_ARG;
+  if (dst + len <= src || src + len <= dst) {
+    PIP_CUDA(cudaMemcpyAsync(a + dst, a + src, len * 8, cudaMemcpyDeviceToDevice, st));
+    return PIP_OK;
+  }
+  if (dst > src) return rotate_device(a + src, dst + len - src, len, st);
+  if (!scratch || scratch_bytes < scratch_bytes_for(sms)) return PIP_ERR_OOM;
+  ScratchLayoutF L = carve_f(scratch, sms);
+  const pip_pred all{PIP_PRED_MASK_EQ, 0, 0, 0};
+  const DevPred p = make_dev_pred(all);
+  u64* from = a + src;
+  if (((uintptr_t)from & 15) == 0) return launch_filter<true>(from, len, p, nullptr, L, st, dev, nullptr, a + dst);
+  return launch_filter<false>(from, len, p, nullptr, L, st, dev, nullptr, a + dst);
+}
+
 int compact_mask_device(u64* a, u64 n, const unsigned char* mask, u64* m_dev, void* scratch,
                         size_t scratch_bytes, cudaStream_t st) {
   const int dev = current_device();

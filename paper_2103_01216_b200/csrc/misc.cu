@@ -32,6 +32,8 @@ static int reverse(u64* a, u64 s, u64 t, cudaStream_t st) {
   return PIP_OK;
 }
 
+int reverse_device(u64* a, u64 n, cudaStream_t st) { return reverse(a, 0, n, st); }
+
 int rotate_device(u64* a, u64 n, u64 o, cudaStream_t st) {
   if (o > n) return PIP_ERR_INVALID_ARG;
   if (o == 0 || o == n || n < 2) return PIP_OK;

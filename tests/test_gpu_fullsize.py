@@ -62,6 +62,37 @@ def host_u64(t) -> np.ndarray:
     return t.cpu().numpy().view(np.uint64)
 
 
+class Pinned:
+    """Reusable pinned host windows: D2H at PCIe speed, no per-window allocation."""
+
+    def __init__(self, k: int = 2):
+        import torch
+
+        self.bufs = [torch.empty(WIN, dtype=torch.int64, pin_memory=True) for _ in range(k)]
+
+    def get(self, t, slot: int = 0) -> np.ndarray:
+        b = self.bufs[slot][: t.numel()]
+        b.copy_(t)
+        return b.numpy().view(np.uint64)
+
+
+def sort_run(t, pip):
+    """Sort a device run longer than torch.sort's INT_MAX limit: pieces of
+    2^30 sorted by torch, then merged in place pairwise with merge_relaxed."""
+    import torch
+
+    n, piece = t.numel(), 1 << 30
+    for s in range(0, n, piece):
+        t[s:s + piece] = torch.sort(t[s:s + piece]).values
+    width = piece
+    while width < n:
+        for s in range(0, n, 2 * width):
+            e = min(s + 2 * width, n)
+            if s + width < e:
+                pip.relaxed.merge_relaxed(t[s:e], width)
+        width *= 2
+
+
 def test_c1_scan_2_32(pip, orc):
     """configs[1]: inclusive scan of 2^32 words Rng(1) >> 44, every word."""
     import torch
@@ -73,12 +104,13 @@ def test_c1_scan_2_32(pip, orc):
     rng.words_device(0, n, shift=44, out=a)
     r = pip.strong.scan_inclusive(a)
     buf = torch.empty(WIN, dtype=torch.int64, device="cuda")
+    pin = Pinned()
     carry = 0
     for lo in range(0, n, WIN):
         hi = min(n, lo + WIN)
-        x = host_u64(rng.words_device(lo, hi, shift=44, out=buf[: hi - lo]))
+        x = pin.get(rng.words_device(lo, hi, shift=44, out=buf[: hi - lo]), 0)
         want, _ = orc.seq_scan(x, init=carry, inclusive=True)
-        got = host_u64(a[lo:hi])
+        got = pin.get(a[lo:hi], 1)
         assert np.array_equal(got, want), f"window [{lo}, {hi})"
         carry = int(want[-1])
     assert r.total == carry
@@ -97,12 +129,13 @@ def test_c2_filter_2_32(pip, orc):
     rng.words_device(0, n, shift=1, out=a)
     m = pip.strong.filter_kway(a, p)
     buf = torch.empty(WIN, dtype=torch.int64, device="cuda")
+    pin = Pinned()
     pos = 0
     for lo in range(0, n, WIN):
         hi = min(n, lo + WIN)
-        x = host_u64(rng.words_device(lo, hi, shift=1, out=buf[: hi - lo]))
+        x = pin.get(rng.words_device(lo, hi, shift=1, out=buf[: hi - lo]), 0)
         kept = orc.seq_filter(x, p)
-        got = host_u64(a[pos: pos + len(kept)])
+        got = pin.get(a[pos: pos + len(kept)], 1)
         assert np.array_equal(got, kept), f"input window [{lo}, {hi}), output at {pos}"
         pos += len(kept)
     assert m == pos
@@ -142,19 +175,20 @@ def test_c3_merge_2x2_31(pip, orc):
     n, split = 1 << 32, 1 << 31
     a = torch.empty(n, dtype=torch.int64, device="cuda")
     pip.Rng(1).words_device(0, n, shift=34, out=a)
-    a[:split] = torch.sort(a[:split]).values
-    a[split:] = torch.sort(a[split:]).values
+    sort_run(a[:split], pip)
+    sort_run(a[split:], pip)
     orig = a.clone()
     pip.relaxed.merge_relaxed(a, split)
     A, B = orig[:split], orig[split:]
     bounds = list(range(0, n, WIN)) + [n]
     ci = _coranks(A, B, bounds)
+    pin = Pinned(3)
     for k in range(len(bounds) - 1):
         r0, r1 = bounds[k], bounds[k + 1]
         i0, i1 = ci[k], ci[k + 1]
         j0, j1 = r0 - i0, r1 - i1
-        want = orc.seq_merge(host_u64(A[i0:i1]), host_u64(B[j0:j1]))
-        got = host_u64(a[r0:r1])
+        want = orc.seq_merge(pin.get(A[i0:i1], 0), pin.get(B[j0:j1], 1))
+        got = pin.get(a[r0:r1], 2)
         assert np.array_equal(got, want), f"output window [{r0}, {r1})"
 
 
@@ -168,8 +202,8 @@ def test_c3_merge_strong_2x2_31(pip):
     n, split = 1 << 32, 1 << 31
     a = torch.empty(n, dtype=torch.int64, device="cuda")
     pip.Rng(3).words_device(0, n, shift=34, out=a)
-    a[:split] = torch.sort(a[:split]).values
-    a[split:] = torch.sort(a[split:]).values
+    sort_run(a[:split], pip)
+    sort_run(a[split:], pip)
     b = a.clone()
     pip.strong.merge_strong(a, split)
     pip.relaxed.merge_relaxed(b, split)
@@ -221,16 +255,20 @@ def test_scan_host_2_32(pip, orc):
     """pip_scan_u64_host (the e2e path) on a 32 GiB host array: 256 chunks,
     carry handed from chunk to chunk; every word checked."""
     need_host(72)
+    import torch
+
     n = 1 << 32
     x = np.empty(n, dtype=np.uint64)
     rng = pip.Rng(1)
+    buf = torch.empty(WIN, dtype=torch.int64, device="cuda")
+    pin = Pinned(1)
     for lo in range(0, n, WIN):
-        x[lo: lo + WIN] = rng.words(lo, min(n, lo + WIN)) >> np.uint64(44)
+        x[lo: lo + WIN] = pin.get(rng.words_device(lo, min(n, lo + WIN), shift=44, out=buf))
     r = pip.strong.scan_inclusive(x)
     carry = 0
     for lo in range(0, n, WIN):
         hi = min(n, lo + WIN)
-        src = rng.words(lo, hi) >> np.uint64(44)
+        src = pin.get(rng.words_device(lo, hi, shift=44, out=buf[: hi - lo]))
         want, _ = orc.seq_scan(src, init=carry, inclusive=True)
         assert np.array_equal(x[lo:hi], want), f"window [{lo}, {hi})"
         carry = int(want[-1])
@@ -242,17 +280,21 @@ def test_filter_host_2_32(pip, orc):
     chunk's kept words written back behind the upload front; every kept word
     checked in order."""
     need_host(72)
+    import torch
+
     n = 1 << 32
     x = np.empty(n, dtype=np.uint64)
     rng = pip.Rng(1)
+    buf = torch.empty(WIN, dtype=torch.int64, device="cuda")
+    pin = Pinned(1)
     for lo in range(0, n, WIN):
-        x[lo: lo + WIN] = rng.words(lo, min(n, lo + WIN)) >> np.uint64(1)
+        x[lo: lo + WIN] = pin.get(rng.words_device(lo, min(n, lo + WIN), shift=1, out=buf))
     p = pip.pred.mod_eq(3, 0)
     m = pip.strong.filter_kway(x, p)
     pos = 0
     for lo in range(0, n, WIN):
         hi = min(n, lo + WIN)
-        kept = orc.seq_filter(rng.words(lo, hi) >> np.uint64(1), p)
+        kept = orc.seq_filter(pin.get(rng.words_device(lo, hi, shift=1, out=buf[: hi - lo])), p)
         assert np.array_equal(x[pos: pos + len(kept)], kept), f"input window [{lo}, {hi})"
         pos += len(kept)
     assert m == pos
