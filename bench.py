@@ -386,8 +386,9 @@ def check_merge_windows(a, orig, na, torch):
 
 
 def _wsum(t, w, torch):
-    """sum(t * w) mod 2^64 (int64 wrap-around) as a python int."""
-    return int((t * w).sum().item()) & ((1 << 64) - 1)
+    """sum(t * w) mod 2^64 (int64 wrap-around), as a signed int64 value."""
+    v = int((t * w).sum().item()) & ((1 << 64) - 1)
+    return v - (1 << 64) if v >> 63 else v
 
 
 def run_filter_sharded(args, ws, rank, local, torch, pip, lib):

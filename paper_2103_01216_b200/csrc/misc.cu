@@ -62,11 +62,55 @@ __global__ void validate_kernel(const u64* __restrict__ h, u64 n, u64* counters)
   }
 }
 
+// the same pass, also writing the non-self count of every 4096-id block
+// (bcnt[c] for ids [4096c, 4096c + 4096)): the permutation's window counts
+// then come from these instead of a second read of H
+static constexpr u32 VBLK_SHIFT = 12;
+__global__ void __launch_bounds__(256) validate_blocks_kernel(const u64* __restrict__ h, u64 n,
+                                                              u64* counters, u32* bcnt) {
+  __shared__ u32 s_w[8];
+  const u64 nblk = (n + (1ull << VBLK_SHIFT) - 1) >> VBLK_SHIFT;
+  u64 ns_all = 0, bad_all = 0;
+  for (u64 c = blockIdx.x; c < nblk; c += gridDim.x) {
+    const u64 base = c << VBLK_SHIFT;
+    u32 ns = 0;
+#pragma unroll 4
+    for (u32 q = threadIdx.x; q < (1u << VBLK_SHIFT); q += 256) {
+      const u64 i = base + q;
+      if (i < n) {
+        const u64 v = __ldcs(h + i);
+        ns += v != i;
+        bad_all += v > i;
+      }
+    }
+    ns = __reduce_add_sync(0xffffffffu, ns);
+    if (lane_id() == 0) s_w[warp_id()] = ns;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      u32 t = 0;
+      for (int w = 0; w < 8; ++w) t += s_w[w];
+      bcnt[c] = t;
+      ns_all += t;
+    }
+    __syncthreads();
+  }
+  bad_all = warp_reduce<Op<PIP_OP_ADD>>(bad_all);
+  if (lane_id() == 0 && bad_all) atomicAdd(counters + 1, bad_all);
+  if (threadIdx.x == 0 && ns_all) atomicAdd(counters, ns_all);
+}
+
 int validate_counts(const u64* h, u64 n, u64* nonself, u64* invalid, void* scratch16,
-                    cudaStream_t st) {
+                    cudaStream_t st, u32* bcnt) {
   u64* cnt = (u64*)scratch16;
   PIP_CUDA(cudaMemsetAsync(cnt, 0, 16, st));
-  if (n) {
+  if (n && bcnt) {
+    const u64 nblk = (n + (1ull << VBLK_SHIFT) - 1) >> VBLK_SHIFT;
+    u64 blocks = nblk;
+    const u64 cap = (u64)num_sms(current_device()) * 8;
+    if (blocks > cap) blocks = cap;
+    validate_blocks_kernel<<<(unsigned)blocks, 256, 0, st>>>(h, n, cnt, bcnt);
+    PIP_CHECK_LAUNCH();
+  } else if (n) {
     u64 blocks = (n + 255) / 256;
     const u64 cap = (u64)num_sms(current_device()) * 8;
     if (blocks > cap) blocks = cap;
@@ -85,7 +129,7 @@ int validate_device(const u64* h, u64 n, u64* nonself_dev, void* scratch, size_t
                     cudaStream_t st) {
   if (!scratch || scratch_bytes < 16) return PIP_ERR_OOM;
   u64 ns = 0, bad = 0;
-  int rc = validate_counts(h, n, &ns, &bad, scratch, st);
+  int rc = validate_counts(h, n, &ns, &bad, scratch, st, nullptr);
   if (rc) return rc;
   if (nonself_dev) {
     PIP_CUDA(cudaMemcpyAsync(nonself_dev, &ns, 8, cudaMemcpyHostToDevice, st));

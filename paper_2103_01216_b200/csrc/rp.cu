@@ -56,6 +56,7 @@ struct RpResume {
   u64 dlo, dhi;
   u32 ping, done, first, logcap_c;  // logcap_c: BM collided-table size of the last round
   u32 wpre, pad;                     // wpre: wcnt already holds the counts of the window at `cursor`
+  u64 rlo, rhi;                      // BM 3: id range of the last round's active list (marked in B)
 };
 
 struct RpArgs {
@@ -85,7 +86,17 @@ struct RpArgs {
   u32* lc;   // BM 2: per-CTA lists of iterates whose target was already marked
   u32* lccnt;  // BM: list lengths [G]
   u64 bm_words;
+  // BM 3: collisions are detected on a FOLDED bitmap bmF of 2^logf bits
+  // (bit t & (2^logf - 1), L2-resident); B only receives the targets inside
+  // the active id range (the own checks), a narrow, L2-resident band of it
+  u32* bmF;
+  u32 logf, pad3;
+  u32* claim2;  // BM 3: per-CTA correction of the distinct-target count
+  // non-self count of every 2^RP_BLK_SHIFT-id block of H (from the validation
+  // pass), so the window counts need no second read of H (NULL = read H)
+  const u32* bcnt;
 };
+static constexpr u32 RP_BLK_SHIFT = 12;
 
 __device__ __forceinline__ void part(u64 total, u32 G, u32 b, u64& s, u64& e) {
   s = total * b / G;
@@ -114,6 +125,21 @@ __device__ __forceinline__ u32 block_rank(bool f, u32* s_cnt, u32* tot) {
   __syncthreads();
   const u32 r = s_cnt[warp] + wr;
   *tot = s_cnt[32];
+  __syncthreads();
+  return r;
+}
+
+// signed sum of the int32 words cnt[0..G) (all threads get it)
+__device__ __forceinline__ long long sum_counts_signed(const u32* cnt, u32 G, u64* s_red) {
+  if (threadIdx.x < 32) {
+    long long t = 0;
+    for (u32 i = threadIdx.x; i < G; i += 32) t += (int)__ldcg(cnt + i);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) t += __shfl_down_sync(0xffffffffu, t, o);
+    if (threadIdx.x == 0) s_red[35] = (u64)t;
+  }
+  __syncthreads();
+  const long long r = (long long)s_red[35];
   __syncthreads();
   return r;
 }
@@ -187,6 +213,24 @@ __device__ __forceinline__ void sum_counts(const u32* cnt, u32 G, u32 b, u64* s_
   total = s_red[33];
   before = s_red[34];
   __syncthreads();
+}
+
+// non-self ids in [x, y] (inclusive), summed over the CTA: whole blocks from
+// the block counts, the ragged ends from H itself
+__device__ __forceinline__ u64 count_nonself_range(const RpArgs& A, u64 x, u64 y) {
+  if (x > y) return 0;
+  u64 c = 0;
+  const u64 B = 1ull << RP_BLK_SHIFT;
+  const u64 fb = (x + B - 1) >> RP_BLK_SHIFT, lb = (y + 1) >> RP_BLK_SHIFT;  // full blocks [fb, lb)
+  if (A.bcnt && fb < lb) {
+    for (u64 q = fb + threadIdx.x; q < lb; q += blockDim.x) c += __ldg(A.bcnt + q);
+    const u64 e1 = fb << RP_BLK_SHIFT, s2 = lb << RP_BLK_SHIFT;
+    for (u64 id = x + threadIdx.x; id < e1; id += blockDim.x) c += __ldcs(A.h + id) != id;
+    for (u64 id = s2 + threadIdx.x; id <= y; id += blockDim.x) c += __ldcs(A.h + id) != id;
+  } else {
+    for (u64 id = x + threadIdx.x; id <= y; id += blockDim.x) c += __ldcs(A.h + id) != id;
+  }
+  return c;
 }
 
 // ---------------------------------------------------------------------------
@@ -340,14 +384,25 @@ __global__ void __launch_bounds__(RP_THREADS, 4) rp_kernel(RpArgs A) {
             const u32 sl = __ldcg(A.slot + k);
             if (sl != RP_NOSLOT) A.table[sl] = RP_EMPTY;
           }
-          if (BM && F * 256 < A.n) {  // sparse round: clear the touched words
+          if (BM && BM != 3 && F * 256 < A.n) {  // sparse round: clear the touched words
             A.bmB[tv[q] >> 5] = 0u;
             if (BM == 1) A.bmC[tv[q] >> 5] = 0u;
           }
         }
       }
       R.trace_pos += ncommit;
-      if (BM && F * 256 >= A.n) {  // dense round: clear the bitmaps wholesale
+      if (BM == 3) {
+        // the folded bitmap wholesale (L2-resident); B only over the band of
+        // ids the last round marked
+        u64 ts, te;
+        part(1ull << (A.logf - 5), G, b, ts, te);
+        for (u64 x = ts + tid; x < te; x += T) A.bmF[x] = 0u;
+        if (R.rhi >= R.rlo) {
+          part((R.rhi >> 5) - (R.rlo >> 5) + 1, G, b, ts, te);
+          for (u64 x = ts + tid; x < te; x += T) A.bmB[(R.rlo >> 5) + x] = 0u;
+        }
+      }
+      if (BM && BM != 3 && F * 256 >= A.n) {  // dense round: clear the bitmaps wholesale
         u64 ts, te;
         part(A.bm_words, G, b, ts, te);
         for (u64 x = ts + tid; x < te; x += T) {
@@ -355,7 +410,7 @@ __global__ void __launch_bounds__(RP_THREADS, 4) rp_kernel(RpArgs A) {
           if (BM == 1) A.bmC[x] = 0u;
         }
       }
-      if (BM == 2 && R.logcap_c) {  // the collided table used only its first 2^logcap_c slots
+      if ((BM == 2 || BM == 3) && R.logcap_c) {  // the collided table used only its first 2^logcap_c slots
         u64 ts, te;
         part(1ull << R.logcap_c, G, b, ts, te);
         for (u64 x = ts + tid; x < te; x += T) A.table[x] = RP_EMPTY;
@@ -384,12 +439,7 @@ __global__ void __launch_bounds__(RP_THREADS, 4) rp_kernel(RpArgs A) {
       wd = hi - lo + 1;
       u64 s, e;
       part(wd, G, b, s, e);
-      u64 c = 0;
-#pragma unroll 4
-      for (u64 q = s + tid; q < e; q += T) {
-        const u64 id = hi - q;
-        c += __ldcs(A.h + id) != id;
-      }
+      u64 c = e > s ? count_nonself_range(A, hi - (e - 1), hi - s) : 0;
       c = block_sum(c, s_red);
       if (tid == 0) A.wcnt[b] = (u32)c;
     };
@@ -427,6 +477,11 @@ __global__ void __launch_bounds__(RP_THREADS, 4) rp_kernel(RpArgs A) {
         part(A.bm_words, G, b, ts, te);
         for (u64 x = ts + tid; x < te; x += T)
           if (__ldcg(A.bmB + x) | (BM == 1 ? __ldcg(A.bmC + x) : 0u)) atomicExch(&g->sync.error, (u32)PIP_ERR_DEBUG_SWEEP);
+        if (BM == 3) {
+          part(1ull << (A.logf - 5), G, b, ts, te);
+          for (u64 x = ts + tid; x < te; x += T)
+            if (__ldcg(A.bmF + x)) atomicExch(&g->sync.error, (u32)PIP_ERR_DEBUG_SWEEP);
+        }
       }
     }
     u64 total_ns = 0, wbefore = 0;
@@ -491,6 +546,13 @@ __global__ void __launch_bounds__(RP_THREADS, 4) rp_kernel(RpArgs A) {
     const u64 dlo = ld_relaxed_u64(reinterpret_cast<const u64*>(&g->dlo));
     const u64 dhi = ld_relaxed_u64(reinterpret_cast<const u64*>(&g->dhi));
     if (fresh > 0) cursor = (long long)dlo - 1;
+    // BM 3: the active list is descending, so its ids span [band_lo, band_hi];
+    // only targets inside that band can be some active iterate's own slot
+    u64 band_lo = 1, band_hi = 0;
+    if (BM == 3) {
+      band_hi = __ldcg(ids_n);
+      band_lo = __ldcg(ids_n + newF - 1);
+    }
     {
       u64 s, e;
       part(newF, G, b, s, e);
@@ -530,6 +592,35 @@ __global__ void __launch_bounds__(RP_THREADS, 4) rp_kernel(RpArgs A) {
           for (int q = 0; q < RB; ++q) {
             const u64 k = k0 + q * T;
             if (k >= e) continue;
+            const bool coll = (old[q] >> (t[q] & 31)) & 1u;
+            if (coll) A.lc[s + atomicAdd(s_cnt + 32, 1u)] = (u32)(k - s);
+            else if (t[q] < dlo || t[q] > dhi) claims += 1;
+            A.cflag[k] = coll ? 2 : 0;
+          }
+        }
+        __syncthreads();
+        if (tid == 0) A.lccnt[b] = s_cnt[32];
+      } else if (BM == 3) {
+        // mark: the first toucher of FOLDED bit (t mod 2^logf) is its
+        // "first marker"; later touchers go to the list (every reserver of
+        // a target other than its first marker lands there, plus a few that
+        // only share the folded bit).  Targets inside the active band also
+        // set B[t] for the own checks.
+        if (tid == 0) s_cnt[32] = 0;
+        __syncthreads();
+        const u32 fmask = (u32)((1ull << A.logf) - 1ull);
+        for (u64 k0 = s + tid; k0 < e; k0 += (u64)RB * T) {
+          u32 t[RB], old[RB];
+#pragma unroll
+          for (int q = 0; q < RB; ++q) t[q] = k0 + q * T < e ? __ldcs(tg_n + k0 + q * T) : 0u;
+#pragma unroll
+          for (int q = 0; q < RB; ++q)
+            old[q] = k0 + q * T < e ? atomicOr(A.bmF + ((t[q] & fmask) >> 5), 1u << (t[q] & 31)) : 0u;
+#pragma unroll
+          for (int q = 0; q < RB; ++q) {
+            const u64 k = k0 + q * T;
+            if (k >= e) continue;
+            if (t[q] >= band_lo && t[q] <= band_hi) atomicOr(A.bmB + (t[q] >> 5), 1u << (t[q] & 31));
             const bool coll = (old[q] >> (t[q] & 31)) & 1u;
             if (coll) A.lc[s + atomicAdd(s_cnt + 32, 1u)] = (u32)(k - s);
             else if (t[q] < dlo || t[q] > dhi) claims += 1;
@@ -603,7 +694,7 @@ __global__ void __launch_bounds__(RP_THREADS, 4) rp_kernel(RpArgs A) {
       }
       const u64 f = block_sum(fails, s_red);
       if (tid == 0) A.failcnt[b] = (u32)f;
-    } else if (BM == 2) {
+    } else if (BM == 2 || BM == 3) {
       // P3b: the iterates that found their target already marked (list lc)
       // reserve in a write-max table sized for them alone (L2-resident);
       // then every first marker looks its target up there: absent => it is
@@ -612,15 +703,20 @@ __global__ void __launch_bounds__(RP_THREADS, 4) rp_kernel(RpArgs A) {
       if (!grid_barrier(&g->sync, gen)) break;
       tick(2);
       u64 claims_total, dummy, lc_total, lc_before;
-      sum_counts(A.claimcnt, G, b, s_red, claims_total, dummy);
-      if (claims_total > R.peak) R.peak = claims_total;
+      if (BM == 2) {  // BM 3 counts distinct targets at the end of the round
+        sum_counts(A.claimcnt, G, b, s_red, claims_total, dummy);
+        if (claims_total > R.peak) R.peak = claims_total;
+      }
       sum_counts(A.lccnt, G, b, s_red, lc_total, lc_before);
       u32 lg = 0;
       if (lc_total) {
         lg = 8;
-        while ((1ull << lg) < 4 * lc_total) ++lg;  // load <= 1/4: short probes
+        // load <= 1/4 (BM 2) or 1/2 (BM 3: the list is longer, the table
+        // must stay in L2 next to the folded bitmap)
+        while ((1ull << lg) < (BM == 3 ? 2 : 4) * lc_total) ++lg;
         if (lg > A.logcap) lg = A.logcap;
       }
+      int c2 = 0;  // BM 3: listed claims of new targets - first markers that joined
       R.logcap_c = lg;
       u64 s, e;
       part(newF, G, b, s, e);
@@ -629,7 +725,10 @@ __global__ void __launch_bounds__(RP_THREADS, 4) rp_kernel(RpArgs A) {
         const u32 mine = __ldcg(A.lccnt + b);
         for (u32 q = tid; q < mine; q += T) {
           const u64 k = s + __ldcg(A.lc + s + q);
-          table_reserve(A.table, lg, __ldcs(tg_n + k), __ldcs(ids_n + k), dclaim, &g->sync.error);
+          const u32 t = __ldcs(tg_n + k);
+          const u32 before = dclaim;
+          table_reserve(A.table, lg, t, __ldcs(ids_n + k), dclaim, &g->sync.error);
+          if (BM == 3 && dclaim != before && (t < dlo || t > dhi)) c2 += 1;
         }
         if (!grid_barrier(&g->sync, gen)) break;
       }
@@ -660,6 +759,7 @@ __global__ void __launch_bounds__(RP_THREADS, 4) rp_kernel(RpArgs A) {
         if (w0 != RP_EMPTY && ((u32)(w0 >> 32) == t || table_lookup(A.table, lg, t, v))) {
           table_reserve(A.table, lg, t, i, dclaim, &g->sync.error);
           A.cflag[k] = 2;
+          if (BM == 3 && (t < dlo || t > dhi)) c2 -= 1;  // its target was counted as listed
           continue;
         }
         const bool c = !((bw >> (i & 31)) & 1u);
@@ -693,6 +793,10 @@ __global__ void __launch_bounds__(RP_THREADS, 4) rp_kernel(RpArgs A) {
       }
       const u64 f = block_sum(fails, s_red);
       if (tid == 0) A.failcnt[b] = (u32)f;
+      if (BM == 3) {
+        const u64 c2s = block_sum((u64)(long long)c2, s_red);
+        if (tid == 0) A.claim2[b] = (u32)c2s;
+      }
     } else {
     if (!grid_barrier(&g->sync, gen)) break;
     tick(2);
@@ -747,24 +851,30 @@ __global__ void __launch_bounds__(RP_THREADS, 4) rp_kernel(RpArgs A) {
     R.dhi = dhi;
     R.cursor = cursor;
     R.wpre = 0;
+    R.rlo = band_lo;
+    R.rhi = band_hi;
     if (V == PIP_RP_FINAL && cursor >= 0) {  // count the next round's window now
       hi = (u64)cursor;
       lo = hi + 1 >= A.span_cap ? hi + 1 - A.span_cap : 0;
       wd = hi - lo + 1;
       u64 ws, we;
       part(wd, G, b, ws, we);
-      u64 c = 0;
-#pragma unroll 4
-      for (u64 q = ws + tid; q < we; q += T) {
-        const u64 id = hi - q;
-        c += __ldcs(A.h + id) != id;
-      }
+      u64 c = we > ws ? count_nonself_range(A, hi - (we - 1), hi - ws) : 0;
       c = block_sum(c, s_red);
       if (tid == 0) A.wcnt[b] = (u32)c;
       R.wpre = 1;
     }
     if (!grid_barrier(&g->sync, gen)) break;
     tick(3);
+    if (BM == 3) {
+      // distinct out-of-window targets of the round (the reference table's
+      // keys): first markers outside the window + listed targets no first
+      // marker holds (listed claims - joined first markers)
+      u64 fm, dummy;
+      sum_counts(A.claimcnt, G, b, s_red, fm, dummy);
+      const long long d = (long long)fm + sum_counts_signed(A.claim2, G, s_red);
+      if (d > 0 && (u64)d > R.peak) R.peak = (u64)d;
+    }
     if (A.progress && b == 0 && tid == 0) {
       // this round's list is descending (failures first, then the fresh
       // window), so its head bounds every pending id; every CTA's swaps
@@ -788,7 +898,10 @@ struct RpLayout {
   size_t ids[2], tg[2], slot, cflag, dense, table, failcnt, wcnt, claimcnt, rcounts, global,
       resume, bmB, bmC, lc, lccnt, total;
   u64 bm_words;
-  int bm;  // 0 table (+dense window), 1 bitmaps B and C, 2 bitmap B + collided lists
+  int bm;  // 0 table (+dense window), 1 bitmaps B and C, 2 bitmap B + collided lists,
+          // 3 folded collision bitmap + own band of B + collided lists + H block counts
+  size_t bmF, claim2, bcnt;
+  u32 logf;
 };
 
 static u64 pow2_at_least(u64 x) {
@@ -825,8 +938,19 @@ static RpLayout rp_layout_mode(u64 n, u64 prefix, int variant, u64 cap, int gmax
   L.bm_words = bm ? (n + 31) / 32 : 0;
   L.bmB = take(L.bm_words * 4);
   L.bmC = take(bm == 1 ? L.bm_words * 4 : 0);
-  L.lc = take(bm == 2 ? prefix * 4 : 0);
-  L.lccnt = take(bm == 2 ? (size_t)gmax * 4 : 0);
+  L.lc = take(bm >= 2 ? prefix * 4 : 0);
+  L.lccnt = take(bm >= 2 ? (size_t)gmax * 4 : 0);
+  L.logf = 0;
+  if (bm == 3) {
+    u32 lf = 10;
+    while (lf < 28 && (1ull << lf) < n) ++lf;
+    if (const char* e = getenv("PIP_RP_FOLD_LOG2")) lf = (u32)atoi(e) < 10 ? 10 : (u32)atoi(e);
+    if (lf > 31) lf = 31;
+    L.logf = lf;
+  }
+  L.bmF = take(bm == 3 ? (1ull << L.logf) / 8 : 0);
+  L.claim2 = take(bm == 3 ? (size_t)gmax * 4 : 0);
+  L.bcnt = take(bm == 3 ? ((n >> RP_BLK_SHIFT) + 1) * 4 : 0);
   L.total = off;
   return L;
 }
@@ -843,13 +967,16 @@ static u64 rp_capacity(u64 prefix, int variant) {
 // that, where the random C reads would go to HBM.  PIP_RP_BM=0/1/2 forces.
 static RpLayout rp_layout(u64 n, u64 prefix, int variant, u64 cap, int gmax) {
   if (variant == PIP_RP_FINAL) {
-    int want = n <= (1ull << 28) ? 1 : 2;
+    int want = n <= (1ull << 28) ? 1 : 3;
     if (const char* e = getenv("PIP_RP_BM")) want = atoi(e);
-    if (want == 1 || want == 2) {
+    if (want >= 1 && want <= 3) {
       const RpLayout Lb = rp_layout_mode(n, prefix, variant, cap, gmax, want);
       if ((Lb.total + 7) / 8 <= 8 * prefix || getenv("PIP_RP_BM")) return Lb;
-      const RpLayout Lo = rp_layout_mode(n, prefix, variant, cap, gmax, 3 - want);
-      if ((Lo.total + 7) / 8 <= 8 * prefix) return Lo;
+      for (int alt : {3, 2, 1}) {
+        if (alt == want) continue;
+        const RpLayout Lo = rp_layout_mode(n, prefix, variant, cap, gmax, alt);
+        if ((Lo.total + 7) / 8 <= 8 * prefix) return Lo;
+      }
     }
   }
   return rp_layout_mode(n, prefix, variant, cap, gmax, 0);
@@ -870,7 +997,7 @@ static int rp_run(RpArgs& A, int grid, cudaStream_t st) {
 }
 
 int validate_counts(const u64* h, u64 n, u64* nonself, u64* invalid, void* scratch16,
-                    cudaStream_t st);
+                    cudaStream_t st, u32* bcnt);
 
 int rp_device(u64* a, const u64* h, u64 n, u64 prefix, int variant, int debug,
               u64* counts_host, u64 rounds_cap, u64* trace_dev, void* ws, size_t ws_bytes,
@@ -895,7 +1022,8 @@ int rp_device(u64* a, const u64* h, u64 n, u64 prefix, int variant, int debug,
   char* w = (char*)ws;
   // validate H and count the non-self iterates (relaxed.py:233, :239)
   u64 n_iter = 0, invalid = 0;
-  int vrc = validate_counts(h, n, &n_iter, &invalid, w + Lrun.global, st);
+  int vrc = validate_counts(h, n, &n_iter, &invalid, w + Lrun.global, st,
+                            Lrun.bm == 3 ? (u32*)(w + Lrun.bcnt) : nullptr);
   if (vrc) return vrc;
   if (invalid) return PIP_ERR_INVALID_SWAPS;
   S.n_iterates = n_iter;
@@ -935,14 +1063,19 @@ int rp_device(u64* a, const u64* h, u64 n, u64 prefix, int variant, int debug,
   A.bm_words = Lrun.bm_words;
   A.bmB = Lrun.bm ? (u32*)(w + Lrun.bmB) : nullptr;
   A.bmC = Lrun.bm == 1 ? (u32*)(w + Lrun.bmC) : nullptr;
-  A.lc = Lrun.bm == 2 ? (u32*)(w + Lrun.lc) : nullptr;
-  A.lccnt = Lrun.bm == 2 ? (u32*)(w + Lrun.lccnt) : nullptr;
+  A.lc = Lrun.bm >= 2 ? (u32*)(w + Lrun.lc) : nullptr;
+  A.lccnt = Lrun.bm >= 2 ? (u32*)(w + Lrun.lccnt) : nullptr;
+  A.bmF = Lrun.bm == 3 ? (u32*)(w + Lrun.bmF) : nullptr;
+  A.logf = Lrun.logf;
+  A.claim2 = Lrun.bm == 3 ? (u32*)(w + Lrun.claim2) : nullptr;
+  A.bcnt = Lrun.bm == 3 ? (const u32*)(w + Lrun.bcnt) : nullptr;
 
   PIP_CUDA(cudaMemsetAsync(A.table, 0xff, cap * 8, st));
   if (variant == PIP_RP_FINAL && !Lrun.bm) PIP_CUDA(cudaMemsetAsync(A.dense, 0, A.span_cap * 4, st));
   if (Lrun.bm) {
     PIP_CUDA(cudaMemsetAsync(A.bmB, 0, Lrun.bm_words * 4, st));
     if (Lrun.bm == 1) PIP_CUDA(cudaMemsetAsync(A.bmC, 0, Lrun.bm_words * 4, st));
+    if (Lrun.bm == 3) PIP_CUDA(cudaMemsetAsync(A.bmF, 0, (1ull << Lrun.logf) / 8, st));
   }
   PIP_CUDA(cudaMemsetAsync(A.failcnt, 0, (size_t)gmax * 4, st));
   PIP_CUDA(cudaMemsetAsync(A.g, 0, sizeof(RpGlobal), st));
@@ -951,6 +1084,8 @@ int rp_device(u64* a, const u64* h, u64 n, u64 prefix, int variant, int debug,
   R0.first = 1;
   R0.dlo = 1;
   R0.dhi = 0;
+  R0.rlo = 1;
+  R0.rhi = 0;
   PIP_CUDA(cudaMemcpyAsync(A.resume, &R0, sizeof(R0), cudaMemcpyHostToDevice, st));
   PIP_CUDA(cudaStreamSynchronize(st));  // R0 lives on this stack frame
 
@@ -958,6 +1093,7 @@ int rp_device(u64* a, const u64* h, u64 n, u64 prefix, int variant, int debug,
   int per_sm = 0;
   const void* kp = variant == PIP_RP_FINAL ? (Lrun.bm == 1   ? (const void*)rp_kernel<PIP_RP_FINAL, 1>
                                                  : Lrun.bm == 2 ? (const void*)rp_kernel<PIP_RP_FINAL, 2>
+                                                 : Lrun.bm == 3 ? (const void*)rp_kernel<PIP_RP_FINAL, 3>
                                                                 : (const void*)rp_kernel<PIP_RP_FINAL, 0>)
                    : variant == PIP_RP_ONERES ? (const void*)rp_kernel<PIP_RP_ONERES, 0>
                    : variant == PIP_RP_FLAT ? (const void*)rp_kernel<PIP_RP_FLAT, 0>
@@ -983,6 +1119,7 @@ int rp_device(u64* a, const u64* h, u64 n, u64 prefix, int variant, int debug,
       case PIP_RP_FINAL:
         rc = Lrun.bm == 1   ? rp_run<PIP_RP_FINAL, 1>(A, (int)grid, st)
              : Lrun.bm == 2 ? rp_run<PIP_RP_FINAL, 2>(A, (int)grid, st)
+             : Lrun.bm == 3 ? rp_run<PIP_RP_FINAL, 3>(A, (int)grid, st)
                             : rp_run<PIP_RP_FINAL, 0>(A, (int)grid, st);
         break;
       case PIP_RP_ONERES: rc = rp_run<PIP_RP_ONERES>(A, (int)grid, st); break;
