@@ -90,7 +90,8 @@ struct RpArgs {
   // (bit t & (2^logf - 1), L2-resident); B only receives the targets inside
   // the active id range (the own checks), a narrow, L2-resident band of it
   u32* bmF;
-  u32 logf, pad3;
+  u32 logf, dbg;
+  u32 tload, pad4;  // collided table: slots per listed iterate (BM 2/3)
   u32* claim2;  // BM 3: per-CTA correction of the distinct-target count
   // non-self count of every 2^RP_BLK_SHIFT-id block of H (from the validation
   // pass), so the window counts need no second read of H (NULL = read H)
@@ -667,9 +668,11 @@ __global__ void __launch_bounds__(RP_THREADS, 4) rp_kernel(RpArgs A) {
           const bool c = !((__ldcg(A.bmB + (i >> 5)) >> (i & 31)) & 1u);
           A.cflag[k] = c;
           if (c) {
-            const u64 x = __ldcg(A.a + i), y = __ldcg(A.a + t);
-            A.a[i] = y;
-            A.a[t] = x;
+            if (!(A.dbg & 1)) {
+              const u64 x = __ldcg(A.a + i), y = __ldcg(A.a + t);
+              A.a[i] = y;
+              A.a[t] = x;
+            }
           } else {
             fails += 1;
           }
@@ -685,9 +688,11 @@ __global__ void __launch_bounds__(RP_THREADS, 4) rp_kernel(RpArgs A) {
         const bool c = own && w != RP_EMPTY && (u32)(w >> 32) == t && (u32)w == i;
         A.cflag[k] = c;
         if (c) {
-          const u64 x = __ldcg(A.a + i), y = __ldcg(A.a + t);
-          A.a[i] = y;
-          A.a[t] = x;
+          if (!(A.dbg & 1)) {  // PIP_RP_DBG=1: measurement only, no swaps
+            const u64 x = __ldcg(A.a + i), y = __ldcg(A.a + t);
+            A.a[i] = y;
+            A.a[t] = x;
+          }
         } else {
           fails += 1;
         }
@@ -713,7 +718,7 @@ __global__ void __launch_bounds__(RP_THREADS, 4) rp_kernel(RpArgs A) {
         lg = 8;
         // load <= 1/4 (BM 2) or 1/2 (BM 3: the list is longer, the table
         // must stay in L2 next to the folded bitmap)
-        while ((1ull << lg) < (BM == 3 ? 2 : 4) * lc_total) ++lg;
+        while ((1ull << lg) < (u64)A.tload * lc_total) ++lg;
         if (lg > A.logcap) lg = A.logcap;
       }
       int c2 = 0;  // BM 3: listed claims of new targets - first markers that joined
@@ -765,9 +770,11 @@ __global__ void __launch_bounds__(RP_THREADS, 4) rp_kernel(RpArgs A) {
         const bool c = !((bw >> (i & 31)) & 1u);
         A.cflag[k] = c;
         if (c) {
-          const u64 x = __ldcg(A.a + i), y = __ldcg(A.a + t);
-          A.a[i] = y;
-          A.a[t] = x;
+          if (!(A.dbg & 1)) {  // PIP_RP_DBG=1: measurement only, no swaps
+            const u64 x = __ldcg(A.a + i), y = __ldcg(A.a + t);
+            A.a[i] = y;
+            A.a[t] = x;
+          }
         } else {
           fails += 1;
         }
@@ -783,9 +790,11 @@ __global__ void __launch_bounds__(RP_THREADS, 4) rp_kernel(RpArgs A) {
           const bool c = own && table_lookup(A.table, lg, t, v) && v == i;
           A.cflag[k] = c;
           if (c) {
-            const u64 x = __ldcg(A.a + i), y = __ldcg(A.a + t);
-            A.a[i] = y;
-            A.a[t] = x;
+            if (!(A.dbg & 1)) {
+              const u64 x = __ldcg(A.a + i), y = __ldcg(A.a + t);
+              A.a[i] = y;
+              A.a[t] = x;
+            }
           } else {
             fails += 1;
           }
@@ -831,9 +840,11 @@ __global__ void __launch_bounds__(RP_THREADS, 4) rp_kernel(RpArgs A) {
         const bool c = own && tgt;
         A.cflag[k] = c;
         if (c) {
-          const u64 x = __ldcg(A.a + i), y = __ldcg(A.a + t);
-          A.a[i] = y;
-          A.a[t] = x;
+          if (!(A.dbg & 1)) {  // PIP_RP_DBG=1: measurement only, no swaps
+            const u64 x = __ldcg(A.a + i), y = __ldcg(A.a + t);
+            A.a[i] = y;
+            A.a[t] = x;
+          }
         } else {
           fails += 1;
         }
@@ -982,10 +993,20 @@ static RpLayout rp_layout(u64 n, u64 prefix, int variant, u64 cap, int gmax) {
   return rp_layout_mode(n, prefix, variant, cap, gmax, 0);
 }
 
+size_t rp_cluster_workspace_bytes(u64 n, u64 prefix);
+bool rp_cluster_eligible(u64 n, u64 prefix, u64 span_cap, int* K_out);
+int rp_cluster_run(u64* a, const u64* h, u64 n, u64 prefix, u64 span_cap, void* ws, size_t ws_bytes,
+                   u64* counts_host, u64 rounds_cap, pip_rp_stats* S, cudaStream_t st, int K);
+
 size_t rp_workspace_bytes(u64 n, u64 prefix, int variant) {
   if (prefix < 1 || variant < 0 || variant > 3) return 0;
   if (prefix > n && n > 0) prefix = n;
-  return rp_layout(n, prefix, variant, rp_capacity(prefix, variant), rp_gmax()).total;
+  size_t t = rp_layout(n, prefix, variant, rp_capacity(prefix, variant), rp_gmax()).total;
+  if (variant == PIP_RP_FINAL) {  // the small-n cluster path (rp_cluster.cu) may run instead
+    const size_t c = rp_cluster_workspace_bytes(n, prefix);
+    if (c > t) t = c;
+  }
+  return t;
 }
 
 template <int V, int BM = 0>
@@ -1034,6 +1055,20 @@ int rp_device(u64* a, const u64* h, u64 n, u64 prefix, int variant, int debug,
   }
   // ... while run_rounds clamps the active prefix to n_iterates (detres.py:267)
   const u64 P = prefix < n_iter ? prefix : n_iter;
+  // small n: the whole round loop on one thread-block cluster (rp_cluster.cu)
+  {
+    int K = 0;
+    const u64 span = prefix + prefix / 4 + 8;
+    if (variant == PIP_RP_FINAL && !debug && !trace_dev && !prog && rp_cluster_eligible(n, P, span, &K)) {
+      const int rc = rp_cluster_run(a, h, n, P, span, ws, ws_bytes, counts_host, rounds_cap, &S, st, K);
+      if (rc != PIP_ERR_UNSUPPORTED) {
+        S.table_capacity = cap;
+        S.workspace_words = (rp_cluster_workspace_bytes(n, P) + 7) / 8;
+        if (stats) *stats = S;
+        return rc;
+      }
+    }
+  }
   RpArgs A{};
   A.a = a;
   A.h = h;
@@ -1067,6 +1102,9 @@ int rp_device(u64* a, const u64* h, u64 n, u64 prefix, int variant, int debug,
   A.lccnt = Lrun.bm >= 2 ? (u32*)(w + Lrun.lccnt) : nullptr;
   A.bmF = Lrun.bm == 3 ? (u32*)(w + Lrun.bmF) : nullptr;
   A.logf = Lrun.logf;
+  A.dbg = getenv("PIP_RP_DBG") ? (u32)atoi(getenv("PIP_RP_DBG")) : 0u;
+  A.tload = Lrun.bm == 3 ? 2u : 4u;
+  if (const char* e = getenv("PIP_RP_TLOAD")) A.tload = (u32)atoi(e) < 2 ? 2u : (u32)atoi(e);
   A.claim2 = Lrun.bm == 3 ? (u32*)(w + Lrun.claim2) : nullptr;
   A.bcnt = Lrun.bm == 3 ? (const u32*)(w + Lrun.bcnt) : nullptr;
 
