@@ -719,10 +719,16 @@ def run_merge(args, ws, rank, local, torch, pip, lib):
     pk = peaks()
     achieved = 16 * n / (per_step / 1e3) / 1e9
     tb = ncu_traffic("merge")
+    two_pass = 32 * n / (per_step / 1e3) / 1e9
     roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": pk["hbm_gbs"], "unit": "GB/s",
             "frac": round(achieved / pk["hbm_gbs"], 4), "traffic": (tb * n) if tb else None,
-            "note": "16 B/word algorithmic (each word read once, written once); the in-place "
-                    "schedule moves ~32 B/word (chunk permutation + block merge)"}
+            "two_pass_achieved": round(two_pass, 1),
+            "two_pass_frac": round(two_pass / pk["hbm_gbs"], 4),
+            "note": "frac: 16 B/word algorithmic (each word read once, written once).  An "
+                    "in-place merge with b(n) = 0.02 n words of workspace cannot run in one "
+                    "pass (DESIGN.md 3.3: a single pass would hold ~n/4 words in flight), so "
+                    "it moves >= 32 B/word (chunk permutation + block merge); two_pass_frac is "
+                    "against that floor"}
     e2e = None if args.no_e2e else e2e_host(lib, "merge", n, args, torch, dev, ws, budget=b)
     cpu = None if args.no_cpu else cpu_baseline("merge", args)
     cfg = {"workload": "in-place merge of two sorted runs (merge_relaxed, eps=0.5, f=0.02), "

@@ -91,13 +91,18 @@ struct RpArgs {
   // the active id range (the own checks), a narrow, L2-resident band of it
   u32* bmF;
   u32 logf, dbg;
-  u32 tload, pad4;  // collided table: slots per listed iterate (BM 2/3)
+  u32 tload, fmb;  // collided table: slots per listed iterate (BM 2/3); items in flight per thread
+  // BM 2/3: listed-key filter, bit (t mod 2^RP_LF_LOG2) set for every listed
+  // target, so a first marker probes the collided table only when its bit
+  // is set (NULL = probe always)
+  u32* lf;
   u32* claim2;  // BM 3: per-CTA correction of the distinct-target count
   // non-self count of every 2^RP_BLK_SHIFT-id block of H (from the validation
   // pass), so the window counts need no second read of H (NULL = read H)
   const u32* bcnt;
 };
 static constexpr u32 RP_BLK_SHIFT = 12;
+static constexpr u32 RP_LF_LOG2 = 24;  // 2 MiB filter
 
 __device__ __forceinline__ void part(u64 total, u32 G, u32 b, u64& s, u64& e) {
   s = total * b / G;
@@ -410,6 +415,11 @@ __global__ void __launch_bounds__(RP_THREADS, 4) rp_kernel(RpArgs A) {
           A.bmB[x] = 0u;
           if (BM == 1) A.bmC[x] = 0u;
         }
+      }
+      if ((BM == 2 || BM == 3) && R.logcap_c && A.lf) {
+        u64 ts, te;
+        part(1ull << (RP_LF_LOG2 - 5), G, b, ts, te);
+        for (u64 x = ts + tid; x < te; x += T) A.lf[x] = 0u;
       }
       if ((BM == 2 || BM == 3) && R.logcap_c) {  // the collided table used only its first 2^logcap_c slots
         u64 ts, te;
@@ -733,6 +743,7 @@ __global__ void __launch_bounds__(RP_THREADS, 4) rp_kernel(RpArgs A) {
           const u32 t = __ldcs(tg_n + k);
           const u32 before = dclaim;
           table_reserve(A.table, lg, t, __ldcs(ids_n + k), dclaim, &g->sync.error);
+          if (A.lf) atomicOr(A.lf + ((t & ((1u << RP_LF_LOG2) - 1u)) >> 5), 1u << (t & 31));
           if (BM == 3 && dclaim != before && (t < dlo || t > dhi)) c2 += 1;
         }
         if (!grid_barrier(&g->sync, gen)) break;
@@ -743,6 +754,65 @@ __global__ void __launch_bounds__(RP_THREADS, 4) rp_kernel(RpArgs A) {
       // issued in two waves instead of a chain: {cflag, target, id} of the
       // next item travel while this one finishes (software pipeline), and the
       // table probe and the own-check word go out together.
+      if (A.fmb >= 2) {
+        // FMB items per thread in flight: their stream loads, then their
+        // filter / own-check words, then the swaps' loads go out together
+        constexpr int FB = 2;
+        const u32 lfm = (1u << RP_LF_LOG2) - 1u;
+        for (u64 k0 = s + tid; k0 < e; k0 += (u64)FB * T) {
+          u32 cf[FB], t[FB], iv[FB], fw[FB], bw[FB];
+#pragma unroll
+          for (int q = 0; q < FB; ++q) {
+            const u64 k = k0 + (u64)q * T;
+            cf[q] = 1;
+            if (k < e) {
+              cf[q] = __ldcs(A.cflag + k);
+              t[q] = __ldcs(tg_n + k);
+              iv[q] = __ldcs(ids_n + k);
+            }
+          }
+#pragma unroll
+          for (int q = 0; q < FB; ++q) {
+            fw[q] = 0;
+            bw[q] = 0;
+            if (!cf[q]) {
+              fw[q] = !lc_total ? 0u : A.lf ? __ldcg(A.lf + ((t[q] & lfm) >> 5)) : 0xffffffffu;
+              bw[q] = __ldcg(A.bmB + (iv[q] >> 5));
+            }
+          }
+          bool go[FB];
+#pragma unroll
+          for (int q = 0; q < FB; ++q) {
+            go[q] = false;
+            if (cf[q]) continue;
+            const u64 k = k0 + (u64)q * T;
+            u32 v;
+            if (((fw[q] >> (t[q] & 31)) & 1u) && table_lookup(A.table, lg, t[q], v)) {
+              table_reserve(A.table, lg, t[q], iv[q], dclaim, &g->sync.error);
+              A.cflag[k] = 2;
+              if (BM == 3 && (t[q] < dlo || t[q] > dhi)) c2 -= 1;
+              continue;
+            }
+            const bool c = !((bw[q] >> (iv[q] & 31)) & 1u);
+            A.cflag[k] = c;
+            go[q] = c && !(A.dbg & 1);
+            if (!c) fails += 1;
+          }
+          u64 x[FB], y[FB];
+#pragma unroll
+          for (int q = 0; q < FB; ++q)
+            if (go[q]) {
+              x[q] = __ldcg(A.a + iv[q]);
+              y[q] = __ldcg(A.a + t[q]);
+            }
+#pragma unroll
+          for (int q = 0; q < FB; ++q)
+            if (go[q]) {
+              A.a[iv[q]] = y[q];
+              A.a[t[q]] = x[q];
+            }
+        }
+      } else {
       u64 k = s + tid;
       u32 ncf = 1, nt = 0, ni = 0;
       if (k < e) {
@@ -758,7 +828,8 @@ __global__ void __launch_bounds__(RP_THREADS, 4) rp_kernel(RpArgs A) {
           ni = __ldcs(ids_n + k + T);
         }
         if (cf) continue;
-        const u64 w0 = lc_total ? __ldcg(A.table + rp_home(t, lg)) : RP_EMPTY;
+        const bool maybe = lc_total && (!A.lf || ((__ldcg(A.lf + ((t & ((1u << RP_LF_LOG2) - 1u)) >> 5)) >> (t & 31)) & 1u));
+        const u64 w0 = maybe ? __ldcg(A.table + rp_home(t, lg)) : RP_EMPTY;
         const u32 bw = __ldcg(A.bmB + (i >> 5));
         u32 v;
         if (w0 != RP_EMPTY && ((u32)(w0 >> 32) == t || table_lookup(A.table, lg, t, v))) {
@@ -778,6 +849,7 @@ __global__ void __launch_bounds__(RP_THREADS, 4) rp_kernel(RpArgs A) {
         } else {
           fails += 1;
         }
+      }
       }
       if (lc_total) {
         if (!grid_barrier(&g->sync, gen)) break;
@@ -911,7 +983,7 @@ struct RpLayout {
   u64 bm_words;
   int bm;  // 0 table (+dense window), 1 bitmaps B and C, 2 bitmap B + collided lists,
           // 3 folded collision bitmap + own band of B + collided lists + H block counts
-  size_t bmF, claim2, bcnt;
+  size_t bmF, claim2, bcnt, lf;
   u32 logf;
 };
 
@@ -962,6 +1034,7 @@ static RpLayout rp_layout_mode(u64 n, u64 prefix, int variant, u64 cap, int gmax
   L.bmF = take(bm == 3 ? (1ull << L.logf) / 8 : 0);
   L.claim2 = take(bm == 3 ? (size_t)gmax * 4 : 0);
   L.bcnt = take(bm == 3 ? ((n >> RP_BLK_SHIFT) + 1) * 4 : 0);
+  L.lf = take(bm >= 2 ? (1ull << RP_LF_LOG2) / 8 : 0);
   L.total = off;
   return L;
 }
@@ -1103,7 +1176,10 @@ int rp_device(u64* a, const u64* h, u64 n, u64 prefix, int variant, int debug,
   A.bmF = Lrun.bm == 3 ? (u32*)(w + Lrun.bmF) : nullptr;
   A.logf = Lrun.logf;
   A.dbg = getenv("PIP_RP_DBG") ? (u32)atoi(getenv("PIP_RP_DBG")) : 0u;
-  A.tload = Lrun.bm == 3 ? 2u : 4u;
+  A.tload = 4u;
+  A.fmb = getenv("PIP_RP_FMB") ? (u32)atoi(getenv("PIP_RP_FMB")) : 1u;
+  const bool use_lf = !(getenv("PIP_RP_LF") && atoi(getenv("PIP_RP_LF")) == 0);
+  A.lf = Lrun.bm >= 2 && use_lf ? (u32*)(w + Lrun.lf) : nullptr;
   if (const char* e = getenv("PIP_RP_TLOAD")) A.tload = (u32)atoi(e) < 2 ? 2u : (u32)atoi(e);
   A.claim2 = Lrun.bm == 3 ? (u32*)(w + Lrun.claim2) : nullptr;
   A.bcnt = Lrun.bm == 3 ? (const u32*)(w + Lrun.bcnt) : nullptr;
@@ -1114,6 +1190,7 @@ int rp_device(u64* a, const u64* h, u64 n, u64 prefix, int variant, int debug,
     PIP_CUDA(cudaMemsetAsync(A.bmB, 0, Lrun.bm_words * 4, st));
     if (Lrun.bm == 1) PIP_CUDA(cudaMemsetAsync(A.bmC, 0, Lrun.bm_words * 4, st));
     if (Lrun.bm == 3) PIP_CUDA(cudaMemsetAsync(A.bmF, 0, (1ull << Lrun.logf) / 8, st));
+    if (Lrun.bm >= 2) PIP_CUDA(cudaMemsetAsync(w + Lrun.lf, 0, (1ull << RP_LF_LOG2) / 8, st));
   }
   PIP_CUDA(cudaMemsetAsync(A.failcnt, 0, (size_t)gmax * 4, st));
   PIP_CUDA(cudaMemsetAsync(A.g, 0, sizeof(RpGlobal), st));

@@ -35,11 +35,15 @@
 // stay in their CTA), which only the trace would show: calls that want a
 // trace (or debug sweeps) use rp.cu.
 #include <cooperative_groups.h>
+#include <cstdio>
+#include <cstdlib>
 #include "common.cuh"
 
 namespace cg = cooperative_groups;
 
 namespace pip {
+
+bool timing_enabled();
 
 static constexpr int RC_THREADS = 1024;
 static constexpr int RC_MAXK = 16;
@@ -56,6 +60,7 @@ struct RcArgs {
   u64* round_counts;
   u64 rounds_cap;
   u64* out;  // [0] rounds [1] total committed [2] peak distinct targets [3] status
+             // [4..8] ns per phase (CTA 0): B refill, C marks, D commits, E resolve, A pack+count
 };
 
 // published values, written into every CTA's copy by DSMEM stores; the
@@ -171,6 +176,16 @@ __global__ void __launch_bounds__(RC_THREADS, 1) rp_cluster_kernel(RcArgs A) {
 
   u32 ncur = 0, nfail_me = 0;
   u64 rounds = 0, total = 0, peak = 0, zero_rounds = 0;
+  const bool tm = me == 0 && tid == 0;
+  u64 tacc[5] = {0, 0, 0, 0, 0};
+  u64 tlast = tm ? globaltimer_ns() : 0;
+  auto tick = [&](int ph) {
+    if (tm) {
+      const u64 now = globaltimer_ns();
+      tacc[ph] += now - tlast;
+      tlast = now;
+    }
+  };
   u32 wc0 = cursor >= 0 ? count_window() : 0;
   publish(pub.nfail[0], 0u);
   publish(pub.wcnt[0], wc0);
@@ -254,6 +269,7 @@ __global__ void __launch_bounds__(RC_THREADS, 1) rp_cluster_kernel(RcArgs A) {
     if (newF == 0) break;  // every CTA sees the same counts
     const u32 nmine = nfail_me + q[me];
     cl.sync();
+    tick(0);
 
     // ============ C: marks ============
     const u64 dlo = pub.dlo, dhi = pub.dhi;
@@ -269,6 +285,7 @@ __global__ void __launch_bounds__(RC_THREADS, 1) rp_cluster_kernel(RcArgs A) {
     }
     publish(pub.claims, rc_block_sum(claims, s_w));
     cl.sync();
+    tick(1);
 
     // ============ D: commits on single-reserver targets; C targets reserve ============
     {
@@ -299,6 +316,7 @@ __global__ void __launch_bounds__(RC_THREADS, 1) rp_cluster_kernel(RcArgs A) {
       }
     }
     cl.sync();
+    tick(2);
 
     // ============ E: C targets resolve ============
     for (u32 k = tid; k < nmine; k += T) {
@@ -320,6 +338,7 @@ __global__ void __launch_bounds__(RC_THREADS, 1) rp_cluster_kernel(RcArgs A) {
     }
     // ---- A of the next round: pack my failures (in order), count the next window
     __syncthreads();
+    tick(3);
     {
       u32 nf2 = 0;
       for (u32 k0 = 0; k0 < nmine; k0 += T) {
@@ -349,6 +368,7 @@ __global__ void __launch_bounds__(RC_THREADS, 1) rp_cluster_kernel(RcArgs A) {
     publish(pub.nfail[nx], nfail_me);
     publish(pub.wcnt[nx], wc);
     cl.sync();
+    tick(4);
     u64 tf = 0;
 #pragma unroll
     for (int c = 0; c < K; ++c) tf += pub.fails[nx][c];
@@ -371,6 +391,7 @@ __global__ void __launch_bounds__(RC_THREADS, 1) rp_cluster_kernel(RcArgs A) {
     A.out[0] = rounds;
     A.out[1] = total;
     A.out[2] = peak;
+    for (int i = 0; i < 5; ++i) A.out[4 + i] = tacc[i];
   }
 }
 
@@ -399,7 +420,7 @@ size_t rp_cluster_workspace_bytes(u64 n, u64 prefix) {
   u64 cap = 8;
   while (cap < 2 * prefix) cap <<= 1;
   const u64 rcap = 4 * (n / (prefix ? prefix : 1)) + 4096;
-  return (size_t)(cap * 8 + rcap * 8 + 64);
+  return (size_t)(cap * 8 + rcap * 8 + 128);
 }
 
 // eligible: final variant, no trace / debug, state fits the cluster's smem
@@ -451,8 +472,11 @@ int rp_cluster_run(u64* a, const u64* h, u64 n, u64 prefix, u64 span_cap, void* 
     cap <<= 1;
     ++logcap;
   }
-  const u64 rcap = 4 * (n / prefix) + 4096;
-  if (!ws || ws_bytes < rp_cluster_workspace_bytes(n, prefix)) return PIP_ERR_OOM;
+  // round counts: as many as the workspace holds after the table (at least
+  // 4 n / b + 4096 when sized by pip_rp_workspace_bytes); a longer run keeps
+  // the first ones (rounds_recorded tells)
+  if (!ws || ws_bytes < cap * 8 + 128 + 4096 * 8) return PIP_ERR_OOM;
+  const u64 rcap = (ws_bytes - cap * 8 - 128) / 8;
   RcArgs A{};
   A.a = a;
   A.h = h;
@@ -469,25 +493,32 @@ int rp_cluster_run(u64* a, const u64* h, u64 n, u64 prefix, u64 span_cap, void* 
   A.cap = p.cap;
   A.part_cap = p.part_cap;
   PIP_CUDA(cudaMemsetAsync(A.table, 0xff, cap * 8, st));
-  PIP_CUDA(cudaMemsetAsync(A.out, 0, 64, st));
+  PIP_CUDA(cudaMemsetAsync(A.out, 0, 128, st));
   int rc = K == 16 ? rc_launch<16>(A, p.smem, st) : rc_launch<8>(A, p.smem, st);
   if (rc) {
-    cudaGetLastError();
+    const cudaError_t e = cudaGetLastError();
+    if (timing_enabled())
+      fprintf(stderr, "[pip rp] cluster launch (K=%d, smem %zu) failed: %s; grid kernel instead\n", K,
+              p.smem, cudaGetErrorString(e));
+    if (getenv("PIP_RP_CLUSTER") && atoi(getenv("PIP_RP_CLUSTER")) == 2) return PIP_ERR_CUDA;
     return PIP_ERR_UNSUPPORTED;
   }
-  u64 out[4];
+  u64 out[9];
   PIP_CUDA(cudaMemcpyAsync(out, A.out, sizeof(out), cudaMemcpyDeviceToHost, st));
   PIP_CUDA(cudaStreamSynchronize(st));
   const u64 rounds = out[0];
-  if (rounds > rcap) return PIP_ERR_UNSUPPORTED;
-  if (counts_host && rounds) {
-    const u64 m = rounds < rounds_cap ? rounds : rounds_cap;
-    PIP_CUDA(cudaMemcpy(counts_host, A.round_counts, m * 8, cudaMemcpyDeviceToHost));
-  }
+  u64 rec = rounds < rounds_cap ? rounds : rounds_cap;
+  if (rec > rcap) rec = rcap;
+  if (counts_host && rec) PIP_CUDA(cudaMemcpy(counts_host, A.round_counts, rec * 8, cudaMemcpyDeviceToHost));
+  if (timing_enabled())
+    fprintf(stderr, "[pip rp] cluster path: K=%d CTAs x %d threads, smem %zu B, %llu rounds | "
+            "refill %.3f marks %.3f commit %.3f resolve %.3f pack+count %.3f ms\n", K, RC_THREADS,
+            p.smem, (unsigned long long)rounds, out[4] * 1e-6, out[5] * 1e-6, out[6] * 1e-6,
+            out[7] * 1e-6, out[8] * 1e-6);
   S->rounds = rounds;
   S->total_committed = out[1];
   S->peak_table_count = out[2];
-  S->rounds_recorded = rounds < rounds_cap ? rounds : rounds_cap;
+  S->rounds_recorded = rec;
   if (out[3]) return (int)out[3];
   return PIP_OK;
 }
