@@ -298,7 +298,7 @@ def test_merge_full_range_unsigned(pip):
     assert np.array_equal(host(t), np.sort(a))
 
 
-@pytest.mark.parametrize("mode", ["0", "1", "2", "3", "3f"])
+@pytest.mark.parametrize("mode", ["0", "1", "2", "3", "3f", "c16", "c8"])
 @pytest.mark.parametrize("n,seed,frac,debug", [(100_000, 55, 0.02, False), (1_000_000, 1, 0.02, False),
                                                (20_000, 3, 1e-12, True), (3000, 0, 0.05, True),
                                                (3_000_017, 7, 0.05, False)])
@@ -308,7 +308,12 @@ def test_rp_reservation_modes(pip, orc, monkeypatch, mode, n, seed, frac, debug)
     # bitmap + own band of B + H block counts ("3f": a 1024-bit fold, so most
     # iterates share folded bits with others and go through the list).  All
     # must reproduce the reference's rounds exactly (relaxed.py:176-227).
-    monkeypatch.setenv("PIP_RP_BM", mode[0])
+    # "c16" / "c8": the one-cluster kernel (rp_cluster.cu, 16 or 8 CTAs;
+    # it takes only the sizes that fit a cluster's shared memory)
+    if mode.startswith("c"):
+        monkeypatch.setenv("PIP_RP_CLUSTER", "1" if mode == "c16" else "8")
+    else:
+        monkeypatch.setenv("PIP_RP_BM", mode[0])
     if mode == "3f":
         monkeypatch.setenv("PIP_RP_FOLD_LOG2", "10")
     h = (np.zeros(n, dtype=np.uint64) if seed == 0
