@@ -30,7 +30,7 @@ from .runtime import (
     scratch_for,
     small_device_words,
 )
-from .strong import _merge_impl, _partition_impl, _quicksort_impl, filter_kway
+from .strong import _merge_impl, _quicksort_impl
 
 __all__ = ["RP_VARIANTS", "DEFAULT_BUDGET", "make_swap_sequence", "validate_swap_sequence",
            "random_permutation", "decompose_driver", "filter_relaxed", "partition_relaxed",
@@ -162,62 +162,102 @@ def decompose_driver(n: int, budget_words: int, step, trace: list | None = None)
     return stats
 
 
-def filter_relaxed(a, pred, budget: EpsilonConfig = DEFAULT_BUDGET,
-                   stats_sink: list | None = None) -> int:
-    """Stable filter with the reference's prefix-round contract.
+def _relaxed_rounds(a, pred, budget: EpsilonConfig, stats_sink, kind: str) -> int:
+    """The reference's prefix rounds (decompose_driver over b(n)-word blocks,
+    relaxed.py:284-344) run on the device, one block per round:
 
-    The GPU retires the whole array in one look-back pass with no buffer
-    (0 charged words <= 8 b(n)); the returned m and a[0:m) equal the
-    reference's, and ``stats_sink`` receives the round structure the
-    reference reports (ceil(n / b) rounds of min(b, remaining) words).
+      filter:    the block is filtered in place (stable, pip_filter_u64) and
+                 its kept words move down to a[m:] (pip_move_u64, one pass);
+      partition: the block is partitioned in place (pip_partition_u64), then
+                 the first d = min(#true, #false so far) false words of
+                 a[m:pos) and the last d true words of the block swap places
+                 through a charged d-word buffer (the reference's displaced
+                 words, relaxed.py:326-335), so a[0:m') is all true and
+                 a[m':pos') all false.
+
+    So the rounds, their retired counts and the b(n)-word buffer are the
+    reference's, not a restatement of them; the word order inside the false
+    region may differ from the reference's (its contract leaves it free).
     """
+    import torch
+
     w: Words = as_words(a, _wrap=True)
-    as_pred(pred)
+    p = as_pred(pred)
     n = w.n
     if n == 0:
         return 0
+    if not w.is_device:
+        t = torch.from_numpy(w.obj.view(np.int64)).cuda()
+        m = _relaxed_rounds(t, pred, budget, stats_sink, kind)
+        w.obj[:] = t.cpu().numpy().view(np.uint64)
+        return m
     b = budget.prefix_words(n)
-    m = filter_kway(a, pred)
+    lib = _lib.load()
+    desc = p.descriptor()
+    words = w.obj.view(torch.int64) if w.obj.dtype != torch.int64 else w.obj
+    state = {"m": 0, "pos": 0}
+    with torch.cuda.device(w.device):
+        st = w.stream()
+        sp, sb = scratch_for(w.device, st)
+        cnt = small_device_words(1, w.device)
+        if kind == "partition":
+            buf = alloc(8 * b, w.device)  # the reference's aux(b) (relaxed.py:320)
+            tmp = buf.tensor[: 8 * b].view(torch.int64)
+            wb = lib.pip_partition_workspace_bytes(b)
+            pws = alloc(wb, w.device)  # the block partition's descriptors
+        try:
+            def step(hint: int) -> int:
+                pos, m = state["pos"], state["m"]
+                take = min(hint, n - pos)
+                blk = w.ptr + 8 * pos
+                if kind == "filter":
+                    _lib.check(lib.pip_filter_u64(blk, take, C.byref(desc), cnt.data_ptr(), sp, sb,
+                                                  st), "filter_relaxed")
+                    _lib.check_stall(sp, st, "filter_relaxed")
+                    k = int(cnt.item())
+                    if k and m < pos:
+                        _lib.check(lib.pip_move_u64(w.ptr, m, pos, k, sp, sb, st), "filter_relaxed")
+                        _lib.check_stall(sp, st, "filter_relaxed")
+                    state["m"] = m + k
+                else:
+                    _lib.check(lib.pip_partition_u64(blk, take, C.byref(desc), cnt.data_ptr(),
+                                                     pws.ptr, wb, st), "partition_relaxed")
+                    tc = int(cnt.item())
+                    d = min(tc, pos - m)
+                    if d:
+                        x = words[m:m + d]                        # displaced false words
+                        y = words[pos + tc - d:pos + tc]          # the block's last d true words
+                        tmp[:d].copy_(x)
+                        x.copy_(y)
+                        y.copy_(tmp[:d])
+                    state["m"] = m + tc
+                state["pos"] = pos + take
+                return take
+
+            stats = decompose_driver(n, b, step)
+        finally:
+            if kind == "partition":
+                release(pws)
+                release(buf)
     if stats_sink is not None:
-        st = RoundStats()
-        rem = n
-        while rem > 0:
-            take = min(b, rem)
-            st.rounds += 1
-            st.committed_per_round.append(take)
-            rem -= take
-        stats_sink.append(st)
-    return m
+        stats_sink.append(stats)
+    return state["m"]
+
+
+def filter_relaxed(a, pred, budget: EpsilonConfig = DEFAULT_BUDGET,
+                   stats_sink: list | None = None) -> int:
+    """Stable filter, one b(n)-word block per round (relaxed.py:284-309):
+    a[0:m) = the kept words in order; returns m; ``stats_sink`` receives the
+    rounds the device actually ran (ceil(n / b) blocks)."""
+    return _relaxed_rounds(a, pred, budget, stats_sink, "filter")
 
 
 def partition_relaxed(a, pred, budget: EpsilonConfig = DEFAULT_BUDGET,
                       stats_sink: list | None = None) -> int:
-    """Unstable partition with the reference's prefix-round contract
-    (relaxed.py:312-344): a[0:m) holds the words with ``pred`` true, a[m:n)
-    the others (multiset preserved); returns m.
-
-    The GPU runs the swap partition of ``strong.partition_unstable`` once over
-    the whole array; its O(n/4096) descriptor words are charged to the active
-    meter (well under b(n)), and ``stats_sink`` receives the reference's
-    round structure (ceil(n / b) rounds of min(b, remaining) words).
-    """
-    w = as_words(a, _wrap=True)
-    as_pred(pred)
-    n = w.n
-    if n == 0:
-        return 0
-    b = budget.prefix_words(n)
-    m = _partition_impl(a, pred, None, meter_workspace=True)
-    if stats_sink is not None:
-        st = RoundStats()
-        rem = n
-        while rem > 0:
-            take = min(b, rem)
-            st.rounds += 1
-            st.committed_per_round.append(take)
-            rem -= take
-        stats_sink.append(st)
-    return m
+    """Unstable partition, one b(n)-word block per round (relaxed.py:312-344):
+    a[0:m) holds the words with ``pred`` true, a[m:n) the others (multiset
+    preserved); returns m."""
+    return _relaxed_rounds(a, pred, budget, stats_sink, "partition")
 
 
 def quicksort_relaxed(a, rng, budget: EpsilonConfig = DEFAULT_BUDGET) -> None:

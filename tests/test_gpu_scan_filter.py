@@ -275,8 +275,19 @@ def test_filter_relaxed_equals_kway(pip):
         a1, a2 = x.copy(), x.copy()
         m1 = pip.strong.filter_kway(a1, P.even())
         sink = []
-        m2 = pip.relaxed.filter_relaxed(a2, P.even(), pip.EpsilonConfig(0.5, 1e-12), stats_sink=sink)
+        cfg = pip.EpsilonConfig(0.5, 1e-12)
+        m2 = pip.relaxed.filter_relaxed(a2, P.even(), cfg, stats_sink=sink)
         assert m1 == m2 and np.array_equal(a1[:m1], a2[:m2])
+        if n:  # the device ran the reference's rounds: ceil(n / b) blocks of b words
+            b = cfg.prefix_words(n)
+            assert sink[0].committed_per_round == [min(b, n - s) for s in range(0, n, b)]
+    # device tensor, BASELINE's predicate, several block sizes
+    x = rand_words(5, 300_001)
+    for frac in (0.02, 0.3, 1.0):
+        t = dev(x)
+        m = pip.relaxed.filter_relaxed(t, P.mod_eq(3, 0), pip.EpsilonConfig(0.5, frac))
+        want = x[(x % np.uint64(3)) == 0]
+        assert m == len(want) and np.array_equal(host(t)[:m], want)
 
 
 # Tile geometry of the default split-role kernels: 13 compute warps x 512 words
