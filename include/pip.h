@@ -248,7 +248,27 @@ int pip_list_contract_u64(uint64_t* next, uint64_t* prev, const uint64_t* p, uin
                           uint64_t* splice_host, void* workspace, size_t workspace_bytes,
                           void* stream);
 
-/* ---- tree contraction: contraction.tree_contract (contraction.py:368-559) *
+/* ---- tree contraction, whole round loop: contraction.tree_contract
+ * (contraction.py:368-559 on detres.run_rounds).  parent / left / right /
+ * p / values: device u64[n] (NIL = 2^64-1), rewritten in place (values
+ * folded with combine 0 add, 1 max, 2 min, 3 xor, mod 2^64).  The frontier
+ * queue, sweep cursor, active list and rake-parent map live in `workspace`
+ * (pip_tree_contract_workspace_bytes(n, prefix), O(prefix)); the host loop
+ * reads a few counts per round.  HOST outputs: committed_per_round_host
+ * [rounds_cap], trace_host (u64[n], NULL ok: committed ids per round in
+ * packed order), roots_host (u64[2n]: (root, folded value) pairs, count in
+ * *nroots_out), *violations_out (debug != 0: parent-child pairs contracted
+ * together, contraction.py:481-485).  PIP_ERR_TABLE = frontier overflow,
+ * PIP_ERR_LIVELOCK after 64 zero rounds.  Synchronizes.                    */
+size_t pip_tree_contract_workspace_bytes(uint64_t n, uint64_t prefix);
+int pip_tree_contract_u64(uint64_t* parent, uint64_t* left, uint64_t* right, const uint64_t* p,
+                          uint64_t* values, uint64_t n, uint64_t prefix, int combine, int debug,
+                          uint64_t* committed_per_round_host, uint64_t rounds_cap, uint64_t* rounds_out,
+                          uint64_t* trace_host, uint64_t* roots_host, uint64_t* nroots_out,
+                          uint64_t* violations_out, void* workspace, size_t workspace_bytes,
+                          void* stream);
+
+/* ---- tree contraction, one round step: contraction.tree_contract (contraction.py:368-559) *
  * The frontier queue / cursor bookkeeping (O(prefix) per round) is the
  * caller's; one call runs one device step of a round on the device-resident
  * forest (parent/left/right/p/values, NIL = 2^64-1):

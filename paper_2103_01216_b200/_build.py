@@ -17,7 +17,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libpip.so"
-SOURCES = ["api.cu", "scan.cu", "filter.cu", "misc.cu", "rp.cu", "merge.cu", "partition.cu", "contraction.cu", "detres.cu", "rp_cluster.cu"]
+SOURCES = ["api.cu", "scan.cu", "filter.cu", "misc.cu", "rp.cu", "merge.cu", "partition.cu", "contraction.cu", "detres.cu", "rp_cluster.cu", "tree.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

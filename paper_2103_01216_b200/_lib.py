@@ -84,6 +84,9 @@ SIGNATURES = {
     "pip_sort_segments_u64": (i32, [vp, vp, vp, u64, vp]),
     "pip_sort_segments_grid_u64": (i32, [vp, vp, vp, u64, u64, vp]),
     "pip_list_contract_workspace_bytes": (sz, [u64, u64, i32]),
+    "pip_tree_contract_workspace_bytes": (sz, [u64, u64]),
+    "pip_tree_contract_u64": (i32, [vp, vp, vp, vp, vp, u64, u64, i32, i32, vp, u64, C.POINTER(u64), vp,
+                                    vp, C.POINTER(u64), C.POINTER(u64), vp, sz, vp]),
     "pip_tree_round_u64": (i32, [i32, vp, vp, vp, vp, vp, u64, u64, vp, u64, vp, vp, vp, i32, vp]),
     "pip_list_contract_u64": (i32, [vp, vp, vp, u64, u64, i32, vp, u64, vp, vp, vp, vp, sz, vp]),
     "pip_merge_u64": (i32, [vp, u64, u64, i32, vp, sz, vp, sz, vp]),

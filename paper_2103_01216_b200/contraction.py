@@ -7,10 +7,11 @@ ascending, b(n) in all) is checked for local priority minima among active
 neighbours, which splice out (``csrc/contraction.cu``).  ``RoundStats``
 (rounds, committed-per-round) and ``trace`` equal the reference's; list
 ranking finishes with in-place dependence waves over the contraction forest.
-Tree contraction (``contraction.py:368-559``) keeps the reference's frontier
-queue and cursor (the round's control plane, O(prefix) per round) on the
-host and runs every per-node step of a round on the device-resident forest
-(``pip_tree_round_u64``), so its rounds and traces equal the reference's.
+Tree contraction (``contraction.py:368-559``) runs its whole round loop on
+the device (``csrc/tree.cu``): the frontier ring, the sweep cursor, the
+active list, the active-id set and the rake-parent map live in the charged
+workspace, and per round the host reads a few counts; rounds, traces,
+roots and folded values equal the reference's.
 
 Arrays may be numpy (host: copied to the device and back in place) or torch
 CUDA tensors (processed in place on the current stream).  Validation
@@ -167,8 +168,6 @@ def tree_contract(tree: BinaryTree, p, values, budget: EpsilonConfig = DEFAULT_B
     np.add (default, mod 2^64), np.maximum, np.minimum, np.bitwise_xor."""
     import torch
 
-    from .detres import LivelockError
-
     as_words(p)
     as_words(values)
     n = len(tree)
@@ -201,171 +200,47 @@ def tree_contract(tree: BinaryTree, p, values, budget: EpsilonConfig = DEFAULT_B
     pt, vt = to_dev(p), to_dev(values)
     lib = _lib.load()
     prefix = budget.prefix_words(n)
-    qcap = 2 * prefix + 8
-    # device scratch of one round, charged to the active meter (with the host
-    # frontier queue, as the reference charges its own): ids, sorted ids,
-    # flags (a sweep span or the round's eligibility), gathered state of a
-    # chunk of committing nodes
-    GCH = 64
-    span = max(_SCAN_BLOCK, min(n, 2 * prefix * 8))
-    fl_bytes = ((max(span, prefix) + 15) // 16) * 16
-    ids_bytes = ((prefix * 4 + 15) // 16) * 16
-    buf = alloc(2 * ids_bytes + fl_bytes + GCH * 6 * 8, dev)
-    from .runtime import charge, uncharge
-
-    qwords = qcap
-    _charged = charge(qwords)
-    base = buf.ptr
-    d_ids, d_sorted = base, base + ids_bytes
-    d_flags = base + 2 * ids_bytes
-    d_gath = d_flags + fl_bytes
-    st = torch.cuda.current_stream(dev).cuda_stream
-
-    def step(k, lo=0, hi=0, fill=0):
-        _lib.check(lib.pip_tree_round_u64(k, pa.data_ptr(), lf.data_ptr(), rt.data_ptr(),
-                                          pt.data_ptr(), vt.data_ptr(), lo, hi, d_ids, fill,
-                                          d_sorted, d_flags, d_gath, op, st), "tree contraction")
-
-    tb = buf.tensor  # uint8 view of the scratch: bookkeeping transfers go through torch
-
-    def d2h(ptr, nbytes, dtype):
-        off = ptr - base
-        return tb[off:off + nbytes].cpu().numpy().view(dtype)
-
-    def h2d(ptr, arr):
-        arr = np.ascontiguousarray(arr)
-        off = ptr - base
-        if arr.nbytes:
-            tb[off:off + arr.nbytes].copy_(torch.from_numpy(arr.reshape(-1).view(np.uint8)))
-
-    # frontier queue and cursor (contraction.py:400-446), host control plane
-    queue = np.zeros(qcap, dtype=np.uint64)
-    qs = {"head": 0, "size": 0, "cursor": 0}
-    roots: dict[int, int] = {}
-    violations = 0
-
-    def push(ids):
-        cnt = len(ids)
-        if cnt == 0:
-            return
-        if qs["size"] + cnt > qcap:
-            raise RuntimeError("tree contraction frontier overflow")
-        tail = (qs["head"] + qs["size"]) % qcap
-        first = min(cnt, qcap - tail)
-        queue[tail:tail + first] = ids[:first]
-        if first < cnt:
-            queue[:cnt - first] = ids[first:]
-        qs["size"] += cnt
-
-    def scan_fill():
-        while qs["size"] < prefix and qs["cursor"] < n:
-            # ready flags of up to cap_scan ids ahead, then the block sweep
-            lo = qs["cursor"]
-            hi_span = min(n, lo + span)
-            step(0, lo, hi_span)
-            flags = d2h(d_flags, hi_span - lo, np.uint8)
-            while qs["size"] < prefix and qs["cursor"] < hi_span:
-                c0 = qs["cursor"]
-                hi = min(c0 + _SCAN_BLOCK, n)
-                if hi > hi_span:
-                    break  # the block runs past the evaluated span: refetch
-                ids = (np.flatnonzero(flags[c0 - lo:hi - lo]) + c0).astype(np.uint64)
-                need = prefix - qs["size"]
-                if len(ids) > need:
-                    ids = ids[:need]
-                    qs["cursor"] = int(ids[-1]) + 1
-                else:
-                    qs["cursor"] = hi
-                push(ids)
-
-    def next_ids(count):
-        scan_fill()
-        cnt = min(count, qs["size"])
-        if cnt <= 0:
-            return np.empty(0, dtype=np.uint64)
-        h = qs["head"]
-        first = min(cnt, qcap - h)
-        out = np.empty(cnt, dtype=np.uint64)
-        out[:first] = queue[h:h + first]
-        if first < cnt:
-            out[first:] = queue[:cnt - first]
-        qs["head"] = (h + cnt) % qcap
-        qs["size"] -= cnt
-        return out
-
+    # the whole round loop on the device (csrc/tree.cu): frontier ring,
+    # sweep cursor, active list, active-id set and rake-parent map in the
+    # charged workspace; per round the host reads a few counts
+    cap = max(16, 4 * n // max(prefix, 1) + 4096)
+    counts = np.zeros(cap, dtype=np.uint64)
+    tr = np.zeros(n if trace is not None else 0, dtype=np.uint64)
+    roots_buf = np.zeros(2 * n, dtype=np.uint64)
+    rounds, nroots, viol = C.c_uint64(0), C.c_uint64(0), C.c_uint64(0)
+    with torch.cuda.device(dev):
+        st = torch.cuda.current_stream(dev).cuda_stream
+        wb = lib.pip_tree_contract_workspace_bytes(n, prefix)
+        buf = alloc(wb, dev)
+        try:
+            rc = lib.pip_tree_contract_u64(
+                pa.data_ptr(), lf.data_ptr(), rt.data_ptr(), pt.data_ptr(), vt.data_ptr(), n, prefix, op,
+                1 if debug else 0, counts.ctypes.data, cap, C.byref(rounds),
+                tr.ctypes.data if len(tr) else None, roots_buf.ctypes.data, C.byref(nroots),
+                C.byref(viol), buf.ptr, wb, st)
+            if rc == _lib.PIP_ERR_TABLE:
+                raise RuntimeError("tree contraction frontier overflow")
+            _lib.check(rc, "tree contraction")
+        finally:
+            release(buf)
     stats = RoundStats()
-    ids = np.zeros(0, dtype=np.uint64)
-    zero_rounds = 0
-    try:
-        while True:
-            fresh = next_ids(prefix - len(ids))
-            ids = np.concatenate([ids, fresh])
-            fill = len(ids)
-            if fill == 0:
-                break
-            h2d(d_ids, ids.astype(np.uint32))
-            h2d(d_sorted, np.sort(ids).astype(np.uint32))
-            step(1, fill=fill)
-            c = d2h(d_flags, fill, np.uint8).astype(bool)
-            v = ids[c]
-            nv = len(v)
-            if nv:
-                v32 = v.astype(np.uint32)
-                g = np.empty((nv, 6), dtype=np.uint64)
-                for c0 in range(0, nv, GCH):  # every gather precedes any surgery
-                    c1 = min(nv, c0 + GCH)
-                    h2d(d_ids, v32[c0:c1])
-                    step(2, fill=c1 - c0)
-                    g[c0:c1] = d2h(d_gath, (c1 - c0) * 6 * 8, np.uint64).reshape(c1 - c0, 6)
-                par, child, pre, gp, val = g[:, 0], g[:, 1], g[:, 3], g[:, 4], g[:, 5]
-                has_child, has_parent = child != _NILW, par != _NILW
-                if debug and nv > 1:
-                    vs = np.sort(v)
-                    hits = np.minimum(np.searchsorted(vs, par[has_parent]), len(vs) - 1)
-                    violations += int(np.count_nonzero(vs[hits] == par[has_parent]))
-                rake = ~has_child & has_parent
-                rp = par[rake]
-                if len(rp):
-                    uniq_p, first_idx, rake_cnt = np.unique(rp, return_index=True,
-                                                            return_counts=True)
-                    pre_cnt = pre[rake][first_idx].astype(np.int64)
-                    p_is_root = gp[rake][first_idx] == _NILW
-                for c0 in range(0, nv, GCH):
-                    c1 = min(nv, c0 + GCH)
-                    h2d(d_ids, v32[c0:c1])
-                    h2d(d_gath, g[c0:c1])
-                    step(3, fill=c1 - c0)
-                if len(rp):
-                    post_cnt = pre_cnt - rake_cnt
-                    want = np.where(p_is_root, post_cnt == 0, pre_cnt == 2)
-                    push(uniq_p[want & (uniq_p < np.uint64(qs["cursor"]))])
-                done = ~has_child & ~has_parent
-                for node, x in zip(v[done].tolist(), val[done].tolist()):
-                    roots[int(node)] = int(x)
-            stats.rounds += 1
-            stats.committed_per_round.append(nv)
-            if trace is not None:
-                trace.append(v.copy())
-            if nv == 0:
-                zero_rounds += 1
-                if zero_rounds >= 64:
-                    raise LivelockError(f"no iterate committed for 64 rounds ({fill} active); "
-                                        "the client's commit rule cannot make progress")
-            else:
-                zero_rounds = 0
-                ids = ids[~c]
-        torch.cuda.current_stream(dev).synchronize()
-    finally:
-        release(buf)
-        uncharge(qwords, _charged)
+    stats.rounds = int(rounds.value)
+    stats.committed_per_round = [int(x) for x in counts[:min(stats.rounds, cap)]]
+    if trace is not None:
+        pos = 0
+        for c in stats.committed_per_round:
+            trace.append(tr[pos:pos + c].copy())
+            pos += c
+    k = int(nroots.value)
+    roots = {int(r): int(v) for r, v in zip(roots_buf[0:2 * k:2].tolist(), roots_buf[1:2 * k:2].tolist())}
     if host_mode:
         tree.parent[:] = pa.cpu().numpy().view(np.uint64)
         tree.left[:] = lf.cpu().numpy().view(np.uint64)
         tree.right[:] = rt.cpu().numpy().view(np.uint64)
     if isinstance(values, np.ndarray):
         values[:] = vt.cpu().numpy().view(np.uint64)
-    if debug and violations:
-        raise AssertionError(f"{violations} parent-child pairs contracted together")
+    if debug and int(viol.value):
+        raise AssertionError(f"{int(viol.value)} parent-child pairs contracted together")
     return roots, stats
 
 

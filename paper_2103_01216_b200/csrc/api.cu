@@ -75,6 +75,11 @@ int rp_device(u64* a, const u64* h, u64 n, u64 prefix, int variant, int debug,
               pip_rp_stats* stats, cudaStream_t st, const RpProgress* prog = nullptr);
 size_t partition_workspace_bytes(u64 n);
 size_t list_contract_workspace_bytes(u64 n, u64 prefix, int rank);
+size_t tree_contract_workspace_bytes(u64 n, u64 prefix);
+int tree_contract_device(u64* pa, u64* lf, u64* rt, const u64* p, u64* values, u64 n, u64 prefix, int op,
+                         int debug, u64* committed_per_round_host, u64 rounds_cap, u64* rounds_out,
+                         u64* trace_host, u64* roots_host, u64* nroots_out, u64* violations_out, void* ws,
+                         size_t ws_bytes, cudaStream_t st);
 int tree_round_device(int step, u64* pa, u64* lf, u64* rt, const u64* p, u64* values, u64 lo, u64 hi,
                       const u32* ids, u64 fill, const u32* sorted, unsigned char* flags, u64* gathered,
                       int op, cudaStream_t st);
@@ -698,6 +703,22 @@ int pip_tree_round_u64(int step, uint64_t* parent, uint64_t* left, uint64_t* rig
   return tree_round_device(step, (u64*)parent, (u64*)left, (u64*)right, (const u64*)p, (u64*)values, lo,
                            hi, ids, fill, sorted_ids, flags, (u64*)gathered, combine,
                            (cudaStream_t)stream);
+}
+
+size_t pip_tree_contract_workspace_bytes(uint64_t n, uint64_t prefix) {
+  return tree_contract_workspace_bytes(n, prefix);
+}
+
+int pip_tree_contract_u64(uint64_t* parent, uint64_t* left, uint64_t* right, const uint64_t* p,
+                          uint64_t* values, uint64_t n, uint64_t prefix, int combine, int debug,
+                          uint64_t* committed_per_round_host, uint64_t rounds_cap, uint64_t* rounds_out,
+                          uint64_t* trace_host, uint64_t* roots_host, uint64_t* nroots_out,
+                          uint64_t* violations_out, void* workspace, size_t workspace_bytes,
+                          void* stream) {
+  return tree_contract_device((u64*)parent, (u64*)left, (u64*)right, (const u64*)p, (u64*)values, n, prefix,
+                              combine, debug, (u64*)committed_per_round_host, rounds_cap, (u64*)rounds_out,
+                              (u64*)trace_host, (u64*)roots_host, (u64*)nroots_out, (u64*)violations_out,
+                              workspace, workspace_bytes, (cudaStream_t)stream);
 }
 
 size_t pip_list_contract_workspace_bytes(uint64_t n, uint64_t prefix, int rank) {

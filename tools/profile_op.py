@@ -55,5 +55,12 @@ elif args.op == "rp":
     for _ in range(args.reps):
         assert lib.pip_random_permutation_u64(a.data_ptr(), h.data_ptr(), n, prefix, 3, 0, None, 0,
                                               None, ws.data_ptr(), wb, C.byref(stats), st) == 0
+elif args.op == "rmw":
+    # the permutation's roofline denominator: random 8-byte read-modify-writes
+    # over an array of the C4 size (bench.py run_rp)
+    ms = C.c_float(0)
+    for _ in range(args.reps):
+        assert lib.pip_bench_random_rmw(a.data_ptr(), n, n, 7, C.byref(ms), st) == 0
+    print("rmw", n, "updates in", ms.value, "ms ->", n / (ms.value / 1e3) / 1e9, "G RMW/s")
 torch.cuda.synchronize()
 print("ok", args.op, n)
