@@ -21,8 +21,10 @@ Differences from the reference, all on purpose:
 * ``--verify`` checks with numpy on the host (cumsum, sort, mask, roll, the
   sequential swap order) — the reference's oracles in ``baselines.py`` —
   never with the library under test.
-Algorithms outside this path (sorts, partition, sets, contraction, graphs)
-are not registered here; asking for them is a usage error (exit 1).
+Registered: scan, scan-blocked, reduce, rotate, filter(-relaxed),
+partition(-relaxed), quicksort(-relaxed), merge(-relaxed) and rp (all four
+variants).  Algorithms outside this path (mergesort, sets, contraction,
+graphs) are not registered here; asking for them is a usage error (exit 1).
 """
 from __future__ import annotations
 
