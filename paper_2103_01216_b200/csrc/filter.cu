@@ -616,8 +616,8 @@ filter_ws_kernel(u64* __restrict__ a, DevPred p, u64* m_out, LookbackCtx c, u64 
 // Split-role pipeline (see scan_ws2_kernel): warp 0 streams tiles in, LBW
 // look-back warps take tiles round-robin so consecutive look-backs overlap,
 // NWC compute warps count tile k and compact + store tile k - D.
-template <int NWC, int S, int PC, int LBW, int D, int J>
-__global__ void __launch_bounds__(32 * (NWC + 1 + LBW), 1)
+template <int NWC, int S, int PC, int LBW, int D, int J, int MB = 1>
+__global__ void __launch_bounds__(32 * (NWC + 1 + LBW), MB)
 filter_ws2_kernel(u64* __restrict__ a, DevPred p, u64* m_out, LookbackCtx c, u64 num_tiles) {
   using O = Op<PIP_OP_ADD>;
   constexpr u64 TILE = (u64)NWC * 64 * J;  // J word pairs per lane
@@ -981,13 +981,13 @@ static int launch_filter_ws_pc(u64* a, u64 n, const DevPred& p, u64* m_dev,
   return PIP_OK;
 }
 
-template <int NWC, int S, int PC, int LBW, int D, int J>
+template <int NWC, int S, int PC, int LBW, int D, int J, int MB = 1>
 static int launch_filter_ws2_pc(u64* a, u64 n, const DevPred& p, u64* m_dev,
                                 const ScratchLayoutF& L, cudaStream_t st, int dev) {
   constexpr u64 TILE = (u64)NWC * 64 * J;
   constexpr int THREADS = 32 * (NWC + 1 + LBW);
   const u64 full_tiles = n / TILE, rem = n - full_tiles * TILE;
-  auto k = filter_ws2_kernel<NWC, S, PC, LBW, D, J>;
+  auto k = filter_ws2_kernel<NWC, S, PC, LBW, D, J, MB>;
   const int smem = (int)(S * (TILE + 2) * 8);
   PIP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   int per_sm = 0;
@@ -1009,15 +1009,15 @@ static int launch_filter_ws2_pc(u64* a, u64 n, const DevPred& p, u64* m_dev,
   return PIP_OK;
 }
 
-template <int NWC, int S, int LBW, int D, int J = 8>
+template <int NWC, int S, int LBW, int D, int J = 8, int MB = 1>
 static int launch_filter_ws2(u64* a, u64 n, const DevPred& p, u64* m_dev, const ScratchLayoutF& L,
                              cudaStream_t st, int dev) {
   switch (pred_class(p)) {
-    case PC_MASK: return launch_filter_ws2_pc<NWC, S, PC_MASK, LBW, D, J>(a, n, p, m_dev, L, st, dev);
-    case PC_MOD: return launch_filter_ws2_pc<NWC, S, PC_MOD, LBW, D, J>(a, n, p, m_dev, L, st, dev);
-    case PC_MODODD: return launch_filter_ws2_pc<NWC, S, PC_MODODD, LBW, D, J>(a, n, p, m_dev, L, st, dev);
-    case PC_MODODD0: return launch_filter_ws2_pc<NWC, S, PC_MODODD0, LBW, D, J>(a, n, p, m_dev, L, st, dev);
-    default: return launch_filter_ws2_pc<NWC, S, PC_GEN, LBW, D, J>(a, n, p, m_dev, L, st, dev);
+    case PC_MASK: return launch_filter_ws2_pc<NWC, S, PC_MASK, LBW, D, J, MB>(a, n, p, m_dev, L, st, dev);
+    case PC_MOD: return launch_filter_ws2_pc<NWC, S, PC_MOD, LBW, D, J, MB>(a, n, p, m_dev, L, st, dev);
+    case PC_MODODD: return launch_filter_ws2_pc<NWC, S, PC_MODODD, LBW, D, J, MB>(a, n, p, m_dev, L, st, dev);
+    case PC_MODODD0: return launch_filter_ws2_pc<NWC, S, PC_MODODD0, LBW, D, J, MB>(a, n, p, m_dev, L, st, dev);
+    default: return launch_filter_ws2_pc<NWC, S, PC_GEN, LBW, D, J, MB>(a, n, p, m_dev, L, st, dev);
   }
 }
 
@@ -1078,6 +1078,10 @@ int filter_device(u64* a, u64 n, const pip_pred* pred, u64* m_dev, void* scratch
     // look-back gets one tile time): 11.0 ms with 3 or 4 look-back warps
     if (cfg == 23) return launch_filter_ws2<13, 4, 3, 1>(a, n, p, m_dev, L, st, dev);
     if (cfg == 24) return launch_filter_ws2<13, 4, 4, 1>(a, n, p, m_dev, L, st, dev);
+    // two CTAs per SM, half-size tiles (two independent tile chains per SM)
+    if (cfg == 25) return launch_filter_ws2<12, 4, 3, 2, 4, 2>(a, n, p, m_dev, L, st, dev);
+    if (cfg == 26) return launch_filter_ws2<12, 4, 2, 2, 4, 2>(a, n, p, m_dev, L, st, dev);
+    if (cfg == 27) return launch_filter_ws2<8, 4, 3, 2, 6, 2>(a, n, p, m_dev, L, st, dev);
 
     if (cfg == 11) return launch_filter_ws<14, 4>(a, n, p, m_dev, L, st, dev);
     if (cfg == 12) return launch_filter_ws<12, 4>(a, n, p, m_dev, L, st, dev);

@@ -348,20 +348,39 @@ __global__ void __launch_bounds__(RP_THREADS, 4) rp_kernel(RpArgs A) {
       const u64 cbefore = s - fbefore;  // committed items in CTAs < b
       const bool targeted = A.targeted_clean_ok && F * 8 < (1ull << A.logcap);
       u64 runf = 0, runc = 0;
-      // RB consecutive items per thread: failures keep their order
+      // RB consecutive items per thread: failures keep their order; the
+      // next batch's loads are in flight while this batch is packed
+      u32 cn[RB], inx[RB], tnx[RB];
+#pragma unroll
+      for (int q = 0; q < RB; ++q) {
+        const u64 k = s + (u64)RB * tid + q;
+        cn[q] = 1;
+        inx[q] = tnx[q] = 0;
+        if (k < e) {
+          cn[q] = __ldcs(A.cflag + k);
+          inx[q] = __ldcs(ids_o + k);
+          tnx[q] = __ldcs(tg_o + k);
+        }
+      }
       for (u64 c0 = s; c0 < e; c0 += (u64)RB * T) {
         const u64 kb = c0 + (u64)RB * tid;
         u32 fm = 0, cm = 0, iv[RB], tv[RB];
 #pragma unroll
         for (int q = 0; q < RB; ++q) {
-          const u64 k = kb + q;
-          iv[q] = tv[q] = 0;
-          if (k < e) {
-            const bool com = __ldcs(A.cflag + k);
-            iv[q] = __ldcs(ids_o + k);
-            tv[q] = __ldcs(tg_o + k);
-            if (com) cm |= 1u << q;
+          iv[q] = inx[q];
+          tv[q] = tnx[q];
+          if (kb + q < e) {
+            if (cn[q]) cm |= 1u << q;
             else fm |= 1u << q;
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < RB; ++q) {
+          const u64 k = kb + (u64)RB * T + q;
+          if (k < e) {
+            cn[q] = __ldcs(A.cflag + k);
+            inx[q] = __ldcs(ids_o + k);
+            tnx[q] = __ldcs(tg_o + k);
           }
         }
         u32 tot;
@@ -511,18 +530,26 @@ __global__ void __launch_bounds__(RP_THREADS, 4) rp_kernel(RpArgs A) {
       u64 s, e;
       part(wd, G, b, s, e);
       u64 run = wbefore;
+      // the next batch's H words are in flight while this batch is ranked
+      u64 hn[RB];
+#pragma unroll
+      for (int q = 0; q < RB; ++q) {
+        const u64 qq = s + (u64)RB * tid + q;
+        hn[q] = qq < e ? __ldcs(A.h + (hi - qq)) : 0;
+      }
       for (u64 c0 = s; c0 < e && run < fresh; c0 += (u64)RB * T) {
         const u64 qb = c0 + (u64)RB * tid;
         u64 hv[RB];
         u32 fm = 0;
 #pragma unroll
         for (int q = 0; q < RB; ++q) {
-          hv[q] = 0;
-          if (qb + q < e) {
-            const u64 id = hi - (qb + q);
-            hv[q] = __ldcs(A.h + id);
-            if (hv[q] != id) fm |= 1u << q;
-          }
+          hv[q] = hn[q];
+          if (qb + q < e && hv[q] != hi - (qb + q)) fm |= 1u << q;
+        }
+        {
+          const u64 qn = qb + (u64)RB * T;
+#pragma unroll
+          for (int q = 0; q < RB; ++q) hn[q] = qn + q < e ? __ldcs(A.h + (hi - (qn + q))) : 0;
         }
         u32 tot;
         u64 rank = run + block_excl_sum(__popc(fm), s_cnt, &tot);
@@ -620,10 +647,17 @@ __global__ void __launch_bounds__(RP_THREADS, 4) rp_kernel(RpArgs A) {
         if (tid == 0) s_cnt[32] = 0;
         __syncthreads();
         const u32 fmask = (u32)((1ull << A.logf) - 1ull);
+        u32 tn[RB];  // the next batch's targets travel while this batch marks
+#pragma unroll
+        for (int q = 0; q < RB; ++q) tn[q] = s + tid + q * T < e ? __ldcs(tg_n + s + tid + q * T) : 0u;
         for (u64 k0 = s + tid; k0 < e; k0 += (u64)RB * T) {
           u32 t[RB], old[RB];
 #pragma unroll
-          for (int q = 0; q < RB; ++q) t[q] = k0 + q * T < e ? __ldcs(tg_n + k0 + q * T) : 0u;
+          for (int q = 0; q < RB; ++q) {
+            t[q] = tn[q];
+            const u64 kn = k0 + (u64)RB * T + q * T;
+            tn[q] = kn < e ? __ldcs(tg_n + kn) : 0u;
+          }
 #pragma unroll
           for (int q = 0; q < RB; ++q)
             old[q] = k0 + q * T < e ? atomicOr(A.bmF + ((t[q] & fmask) >> 5), 1u << (t[q] & 31)) : 0u;

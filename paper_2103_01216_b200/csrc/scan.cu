@@ -619,8 +619,8 @@ scan_ws_kernel(u64* __restrict__ a, u64 init, const u64* carry_in, u64* total, L
 // so the look-backs of consecutive tiles of this CTA overlap instead of
 // queueing behind one another (the single look-back warp of scan_ws_kernel
 // is busy ~84% of the time at 2^32).
-template <int OP, bool INCLUSIVE, int NWC, int S, int LBW, int D = 1>
-__global__ void __launch_bounds__(32 * (NWC + 1 + LBW), 1)
+template <int OP, bool INCLUSIVE, int NWC, int S, int LBW, int D = 1, int MB = 1>
+__global__ void __launch_bounds__(32 * (NWC + 1 + LBW), MB)
 scan_ws2_kernel(u64* __restrict__ a, u64 init, const u64* carry_in, u64* total, LookbackCtx c,
                 u64 num_tiles) {
   using O = Op<OP>;
@@ -976,14 +976,14 @@ static int launch_scan_ws(u64* a, u64 n, u64 init, const u64* carry, u64* total,
   return PIP_OK;
 }
 
-template <int OP, bool INCL, int NWC, int S, int LBW, int D = 1>
+template <int OP, bool INCL, int NWC, int S, int LBW, int D = 1, int MB = 1>
 static int launch_scan_ws2(u64* a, u64 n, u64 init, const u64* carry, u64* total,
                            const ScratchLayout& L, cudaStream_t st, int device) {
   constexpr u64 TILE = (u64)NWC * 512;
   constexpr int THREADS = 32 * (NWC + 1 + LBW);
   const u64 full_tiles = n / TILE;
   const u64 rem = n - full_tiles * TILE;
-  auto k = scan_ws2_kernel<OP, INCL, NWC, S, LBW, D>;
+  auto k = scan_ws2_kernel<OP, INCL, NWC, S, LBW, D, MB>;
   const int smem = (int)(S * TILE * 8);
   PIP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   int per_sm = 0;
@@ -1037,6 +1037,12 @@ static int launch_scan_op(u64* a, u64 n, u64 init, int inclusive, const u64* car
     if (cfg == 17)  // default: producer warp, 3 look-back warps, 13 compute warps 2 tiles ahead
       return inclusive ? launch_scan_ws2<OP, true, 13, 4, 3, 2>(a, n, init, carry, total, L, st, device)
                        : launch_scan_ws2<OP, false, 13, 4, 3, 2>(a, n, init, carry, total, L, st, device);
+    if (cfg == 18)  // two CTAs per SM, 3072-word tiles
+      return inclusive ? launch_scan_ws2<OP, true, 6, 4, 3, 2, 2>(a, n, init, carry, total, L, st, device)
+                       : launch_scan_ws2<OP, false, 6, 4, 3, 2, 2>(a, n, init, carry, total, L, st, device);
+    if (cfg == 19)  // two CTAs per SM, 4096-word tiles, 3 stages
+      return inclusive ? launch_scan_ws2<OP, true, 8, 3, 3, 1, 2>(a, n, init, carry, total, L, st, device)
+                       : launch_scan_ws2<OP, false, 8, 3, 3, 1, 2>(a, n, init, carry, total, L, st, device);
     if (cfg == 11)
       return inclusive ? launch_scan_ws<OP, true, 14, 4>(a, n, init, carry, total, L, st, device)
                        : launch_scan_ws<OP, false, 14, 4>(a, n, init, carry, total, L, st, device);
