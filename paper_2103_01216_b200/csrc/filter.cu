@@ -1082,6 +1082,11 @@ int filter_device(u64* a, u64 n, const pip_pred* pred, u64* m_dev, void* scratch
     if (cfg == 25) return launch_filter_ws2<12, 4, 3, 2, 4, 2>(a, n, p, m_dev, L, st, dev);
     if (cfg == 26) return launch_filter_ws2<12, 4, 2, 2, 4, 2>(a, n, p, m_dev, L, st, dev);
     if (cfg == 27) return launch_filter_ws2<8, 4, 3, 2, 6, 2>(a, n, p, m_dev, L, st, dev);
+    // 3/4-size tiles, one more stage (two tile loads in flight behind the
+    // two tiles held for the look-back)
+    if (cfg == 28) return launch_filter_ws2<13, 5, 3, 2, 6>(a, n, p, m_dev, L, st, dev);
+    if (cfg == 29) return launch_filter_ws2<13, 5, 4, 3, 6>(a, n, p, m_dev, L, st, dev);
+    if (cfg == 30) return launch_filter_ws2<16, 4, 3, 2, 6>(a, n, p, m_dev, L, st, dev);
 
     if (cfg == 11) return launch_filter_ws<14, 4>(a, n, p, m_dev, L, st, dev);
     if (cfg == 12) return launch_filter_ws<12, 4>(a, n, p, m_dev, L, st, dev);
