@@ -91,7 +91,7 @@ struct RpArgs {
   // the active id range (the own checks), a narrow, L2-resident band of it
   u32* bmF;
   u32 logf, dbg;
-  u32 tload, fmb;  // collided table: slots per listed iterate (BM 2/3); items in flight per thread
+  u32 tload, pad5;  // collided table: slots per listed iterate (BM 2/3)
   // BM 2/3: listed-key filter, bit (t mod 2^RP_LF_LOG2) set for every listed
   // target, so a first marker probes the collided table only when its bit
   // is set (NULL = probe always)
@@ -365,6 +365,17 @@ __global__ void __launch_bounds__(RP_THREADS, 4) rp_kernel(RpArgs A) {
       for (u64 c0 = s; c0 < e; c0 += (u64)RB * T) {
         const u64 kb = c0 + (u64)RB * tid;
         u32 fm = 0, cm = 0, iv[RB], tv[RB];
+        if (BM != 3 && c0 != s) {
+#pragma unroll
+          for (int q = 0; q < RB; ++q) {
+            const u64 k = kb + q;
+            if (k < e) {
+              cn[q] = __ldcs(A.cflag + k);
+              inx[q] = __ldcs(ids_o + k);
+              tnx[q] = __ldcs(tg_o + k);
+            }
+          }
+        }
 #pragma unroll
         for (int q = 0; q < RB; ++q) {
           iv[q] = inx[q];
@@ -374,13 +385,17 @@ __global__ void __launch_bounds__(RP_THREADS, 4) rp_kernel(RpArgs A) {
             else fm |= 1u << q;
           }
         }
+        // (scheme 3 only: the large rounds of C4 gain 0.8 ms; at C0's size the
+        // extra live registers spill and cost more than they hide)
+        if (BM == 3) {
 #pragma unroll
-        for (int q = 0; q < RB; ++q) {
-          const u64 k = kb + (u64)RB * T + q;
-          if (k < e) {
-            cn[q] = __ldcs(A.cflag + k);
-            inx[q] = __ldcs(ids_o + k);
-            tnx[q] = __ldcs(tg_o + k);
+          for (int q = 0; q < RB; ++q) {
+            const u64 k = kb + (u64)RB * T + q;
+            if (k < e) {
+              cn[q] = __ldcs(A.cflag + k);
+              inx[q] = __ldcs(ids_o + k);
+              tnx[q] = __ldcs(tg_o + k);
+            }
           }
         }
         u32 tot;
@@ -541,12 +556,16 @@ __global__ void __launch_bounds__(RP_THREADS, 4) rp_kernel(RpArgs A) {
         const u64 qb = c0 + (u64)RB * tid;
         u64 hv[RB];
         u32 fm = 0;
+        if (BM != 3 && c0 != s) {  // (prefetch for scheme 3 only, as in the retire loop)
+#pragma unroll
+          for (int q = 0; q < RB; ++q) hn[q] = qb + q < e ? __ldcs(A.h + (hi - (qb + q))) : 0;
+        }
 #pragma unroll
         for (int q = 0; q < RB; ++q) {
           hv[q] = hn[q];
           if (qb + q < e && hv[q] != hi - (qb + q)) fm |= 1u << q;
         }
-        {
+        if (BM == 3) {
           const u64 qn = qb + (u64)RB * T;
 #pragma unroll
           for (int q = 0; q < RB; ++q) hn[q] = qn + q < e ? __ldcs(A.h + (hi - (qn + q))) : 0;
@@ -788,65 +807,7 @@ __global__ void __launch_bounds__(RP_THREADS, 4) rp_kernel(RpArgs A) {
       // issued in two waves instead of a chain: {cflag, target, id} of the
       // next item travel while this one finishes (software pipeline), and the
       // table probe and the own-check word go out together.
-      if (A.fmb >= 2) {
-        // FMB items per thread in flight: their stream loads, then their
-        // filter / own-check words, then the swaps' loads go out together
-        constexpr int FB = 2;
-        const u32 lfm = (1u << RP_LF_LOG2) - 1u;
-        for (u64 k0 = s + tid; k0 < e; k0 += (u64)FB * T) {
-          u32 cf[FB], t[FB], iv[FB], fw[FB], bw[FB];
-#pragma unroll
-          for (int q = 0; q < FB; ++q) {
-            const u64 k = k0 + (u64)q * T;
-            cf[q] = 1;
-            if (k < e) {
-              cf[q] = __ldcs(A.cflag + k);
-              t[q] = __ldcs(tg_n + k);
-              iv[q] = __ldcs(ids_n + k);
-            }
-          }
-#pragma unroll
-          for (int q = 0; q < FB; ++q) {
-            fw[q] = 0;
-            bw[q] = 0;
-            if (!cf[q]) {
-              fw[q] = !lc_total ? 0u : A.lf ? __ldcg(A.lf + ((t[q] & lfm) >> 5)) : 0xffffffffu;
-              bw[q] = __ldcg(A.bmB + (iv[q] >> 5));
-            }
-          }
-          bool go[FB];
-#pragma unroll
-          for (int q = 0; q < FB; ++q) {
-            go[q] = false;
-            if (cf[q]) continue;
-            const u64 k = k0 + (u64)q * T;
-            u32 v;
-            if (((fw[q] >> (t[q] & 31)) & 1u) && table_lookup(A.table, lg, t[q], v)) {
-              table_reserve(A.table, lg, t[q], iv[q], dclaim, &g->sync.error);
-              A.cflag[k] = 2;
-              if (BM == 3 && (t[q] < dlo || t[q] > dhi)) c2 -= 1;
-              continue;
-            }
-            const bool c = !((bw[q] >> (iv[q] & 31)) & 1u);
-            A.cflag[k] = c;
-            go[q] = c && !(A.dbg & 1);
-            if (!c) fails += 1;
-          }
-          u64 x[FB], y[FB];
-#pragma unroll
-          for (int q = 0; q < FB; ++q)
-            if (go[q]) {
-              x[q] = __ldcg(A.a + iv[q]);
-              y[q] = __ldcg(A.a + t[q]);
-            }
-#pragma unroll
-          for (int q = 0; q < FB; ++q)
-            if (go[q]) {
-              A.a[iv[q]] = y[q];
-              A.a[t[q]] = x[q];
-            }
-        }
-      } else {
+      {
       u64 k = s + tid;
       u32 ncf = 1, nt = 0, ni = 0;
       if (k < e) {
@@ -1211,7 +1172,6 @@ int rp_device(u64* a, const u64* h, u64 n, u64 prefix, int variant, int debug,
   A.logf = Lrun.logf;
   A.dbg = getenv("PIP_RP_DBG") ? (u32)atoi(getenv("PIP_RP_DBG")) : 0u;
   A.tload = 4u;
-  A.fmb = getenv("PIP_RP_FMB") ? (u32)atoi(getenv("PIP_RP_FMB")) : 1u;
   const bool use_lf = !(getenv("PIP_RP_LF") && atoi(getenv("PIP_RP_LF")) == 0);
   A.lf = Lrun.bm >= 2 && use_lf ? (u32*)(w + Lrun.lf) : nullptr;
   if (const char* e = getenv("PIP_RP_TLOAD")) A.tload = (u32)atoi(e) < 2 ? 2u : (u32)atoi(e);
