@@ -245,6 +245,52 @@ def make_rng():
     np.savez_compressed(OUT / "rng.npz", **d)
 
 
+def make_tree_ops():
+    """Tree contraction on a forest (three random full binary trees with
+    interleaved ids, plus a bare node) under every combine the device folds
+    with (np.add / maximum / minimum / bitwise_xor): rounds, traces, roots,
+    folded values and the final forest from the reference itself."""
+    from pipal.contraction import BinaryTree, make_priorities, tree_contract
+    from pipal.runtime import NIL, POWER_ONLY_FRACTION
+
+    rng = np.random.default_rng(77)
+    sizes = [301, 1, 77, 1023]
+    n = sum(sizes)
+    ids = rng.permutation(n)
+    pa = np.full(n, NIL, dtype=np.uint64)
+    lf = np.full(n, NIL, dtype=np.uint64)
+    rt = np.full(n, NIL, dtype=np.uint64)
+    base = 0
+    for sz in sizes:
+        mine = ids[base:base + sz]
+        base += sz
+        leaves = [int(mine[0])]
+        used = 1
+        while used < sz:
+            node = leaves.pop(int(rng.integers(0, len(leaves))))
+            l, r = int(mine[used]), int(mine[used + 1])
+            used += 2
+            lf[node], rt[node] = l, r
+            pa[l] = pa[r] = node
+            leaves.extend([l, r])
+    vals = rng.integers(0, 1 << 64, size=n, dtype=np.uint64)
+    p = make_priorities(n, Rng(5))
+    d = {"pa": pa, "lf": lf, "rt": rt, "vals": vals, "p": p}
+    for cname, comb in (("add", np.add), ("max", np.maximum), ("min", np.minimum),
+                        ("xor", np.bitwise_xor)):
+        t = BinaryTree(pa.copy(), lf.copy(), rt.copy())
+        v = vals.copy()
+        trace = []
+        roots, st = tree_contract(t, p, v, budget=EpsilonConfig(0.5, POWER_ONLY_FRACTION),
+                                  combine=comb, trace=trace, debug=True)
+        d[f"roots_{cname}"] = np.array(sorted(roots.items()), dtype=np.uint64).reshape(-1, 2)
+        d[f"counts_{cname}"] = np.array(st.committed_per_round, dtype=np.uint64)
+        d[f"trace_{cname}"] = np.concatenate(trace)
+        d[f"vout_{cname}"] = v
+        d[f"paout_{cname}"], d[f"lfout_{cname}"], d[f"rtout_{cname}"] = t.parent, t.left, t.right
+    np.savez_compressed(OUT / "tree_ops.npz", **d)
+
+
 def make_detres():
     """ReservationTable slot layouts after seeded batches (detres.py:40-211):
     the device table reproduces the reference's probe steps, so its key and
@@ -291,6 +337,7 @@ def make_detres():
 
 
 if __name__ == "__main__":
+    make_tree_ops()
     make_detres()
     make_scan()
     make_filter()

@@ -255,3 +255,35 @@ def test_tree_budget_metered(pip):
         tree, p, vals, cfg, debug=True)))
     assert rep.peak_words <= 8 * b and meter.current_words == 0
     assert out["r"][0] == ref
+
+
+@pytest.mark.parametrize("cname", ["add", "max", "min", "xor"])
+@pytest.mark.parametrize("where", ["host", "device"])
+def test_tree_contract_forest_combine_ops_golden(pip, cname, where):
+    """A forest of four trees (one a bare node) under every combine the
+    device folds with: the reference's own rounds, traces, roots, folded
+    values and final forest (tests/golden/tree_ops.npz)."""
+    import torch
+
+    g = golden("tree_ops")
+    comb = {"add": np.add, "max": np.maximum, "min": np.minimum, "xor": np.bitwise_xor}[cname]
+    arrs = [g["pa"].copy(), g["lf"].copy(), g["rt"].copy()]
+    vals = g["vals"].copy()
+    if where == "device":
+        arrs = [torch.from_numpy(x.view(np.int64)).cuda() for x in arrs]
+        vals = torch.from_numpy(vals.view(np.int64)).cuda()
+    tree = pip.contraction.BinaryTree(*arrs)
+    trace: list = []
+    roots, st = pip.contraction.tree_contract(tree, g["p"], vals,
+                                              budget=pip.EpsilonConfig(0.5, 1e-12), combine=comb,
+                                              trace=trace, debug=True)
+
+    def h(x):
+        return x if isinstance(x, np.ndarray) else x.cpu().numpy().view(np.uint64)
+
+    assert roots == {int(a): int(b) for a, b in g[f"roots_{cname}"].tolist()}
+    assert st.committed_per_round == g[f"counts_{cname}"].tolist()
+    assert np.array_equal(np.concatenate(trace), g[f"trace_{cname}"])
+    assert np.array_equal(h(vals), g[f"vout_{cname}"])
+    for arr, key in zip((tree.parent, tree.left, tree.right), ("paout", "lfout", "rtout")):
+        assert np.array_equal(h(arr), g[f"{key}_{cname}"])

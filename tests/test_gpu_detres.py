@@ -323,3 +323,48 @@ def test_run_rounds_with_table_client_is_knuth_shuffle(dr, orc):
     info = orc.ref_random_permutation(np.arange(n, dtype=np.uint64), h_np, prefix, "naive")
     assert st.rounds == info["rounds"]
     assert st.committed_per_round == info["committed_per_round"]
+
+
+def test_table_grow_and_numpy_source(dr):
+    t = dr.ReservationTable(8)
+    t.grow(100)
+    assert t.capacity == 128
+    t.put_max(7, 3)
+    with pytest.raises(RuntimeError, match="only grow while empty"):
+        t.grow(1000)
+
+    # an id source that hands out numpy words (the reference's own clients do)
+    state = {"next": 0}
+
+    def source(count):
+        lo = state["next"]
+        hi = min(lo + count, 50)
+        state["next"] = hi
+        return np.arange(lo, hi, dtype=np.uint64)
+
+    def nothing(view):
+        pass
+
+    def commit(view):
+        view.committed[:] = (view.ids % 2 == 0) | (view.round_index > 0)
+
+    trace: list = []
+    st = dr.run_rounds(50, 16, nothing, commit, nothing, id_source=source, trace=trace)
+    assert sorted(int(x) for tr in trace for x in tr.tolist()) == list(range(50))
+    assert st.total_committed == 50
+
+
+def test_compact_by_mask_uint8_flags_and_meter():
+    import torch
+
+    from paper_2103_01216_b200.runtime import SpaceMeter, compact_by_mask, metered
+
+    x = np.arange(10_000, dtype=np.uint64)
+    keep = (np.arange(10_000) % 7 == 3).astype(np.uint8) * 5  # any nonzero byte keeps
+    t = torch.from_numpy(x.view(np.int64).copy()).cuda()
+    meter = SpaceMeter()
+    with metered(meter):
+        m = compact_by_mask(t, torch.from_numpy(keep).cuda())
+    assert meter.peak_words == 0  # zero heap, like the reference's (runtime.py:335-355)
+    assert m == int((keep != 0).sum())
+    assert np.array_equal(t[:m].cpu().numpy().view(np.uint64), x[keep != 0])
