@@ -771,12 +771,18 @@ filter_ws2_kernel(u64* __restrict__ a, DevPred p, u64* m_out, LookbackCtx c, u64
       keep |= ((u32)pred_eval_t<PC>(p, v.x) << (2 * j)) | ((u32)pred_eval_t<PC>(p, v.y) << (2 * j + 1));
     }
     s_keep[s][w * 32 + lane] = keep;
-    const u64 cnt = warp_reduce<O>((u64)__popc(keep));
+    const u64 cnt = __reduce_add_sync(0xffffffffu, (u32)__popc(keep));  // one REDUX, not 10 shuffles
     if (lane == 0) s_wtot[s][w] = cnt;
     named_bar(1, NWC * 32);
     if (w == 0) {
-      const u64 wv = lane < (u32)NWC ? s_wtot[s][lane] : 0;
-      const u64 winc = warp_incl_scan<O>(wv);
+      // tile counts fit 32 bits: a 32-bit shuffle scan (5 shuffles, not 10)
+      const u32 wv = lane < (u32)NWC ? (u32)s_wtot[s][lane] : 0u;
+      u32 winc = wv;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const u32 t = __shfl_up_sync(0xffffffffu, winc, o);
+        if (lane >= (u32)o) winc += t;
+      }
       if (lane < (u32)NWC) s_wexc[s][lane] = winc - wv;
       if (lane == NWC - 1) s_agg[s] = winc;
       __syncwarp();
