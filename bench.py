@@ -234,7 +234,9 @@ def run_scan(args, ws, rank, local, torch, pip, lib):
         def step():
             rc = lib.pip_scan_u64(a.data_ptr(), n, 0, 0, 1, tot.data_ptr(), sp, sb, sptr)
             assert rc == 0, rc
-        launches = 1
+        # scan_ws2_kernel over the whole 6656-word tiles + the register
+        # kernel for the ragged tail (csrc/scan.cu launch_scan_ws2)
+        launches = 1 + (1 if n % 6656 else 0)
     else:
         import torch.distributed as dist
 
@@ -597,8 +599,9 @@ def run_filter(args, ws, rank, local, torch, pip, lib):
            "values": f"Rng({args.seed}).words >> 1, in [0,2^63)", "kept": m,
            "l2": "inputs larger than L2; input regenerated between steps (untimed)",
            "parallelism": "single-GPU", "seed": args.seed}
+    # filter_ws2_kernel + the tail kernel when n is not a multiple of the tile
     return dict(value=value, per_step=per_step, roof=roof, e2e=e2e, cpu=cpu, cfg=cfg,
-                clocks=clocks, launches=args.steps, extra={})
+                clocks=clocks, launches=(1 + (1 if n % 6656 else 0)) * args.steps, extra={})
 
 
 def sort_run(t, torch, pip):
@@ -820,8 +823,9 @@ def run_rp(args, ws, rank, local, torch, pip, lib, small: bool):
            "workspace_words_over_b": round(wb / 8 / prefix, 3),
            "l2": "C0 is L2-resident by design (8 MB); C4 arrays 8 GiB >> L2",
            "parallelism": "single-GPU", "seed": args.seed}
+    # the validation pass (non-self counts) + the persistent round kernel
     return dict(value=value, per_step=per_step, roof=roof, e2e=e2e, cpu=cpu, cfg=cfg,
-                clocks=clocks, launches=args.steps, extra={})
+                clocks=clocks, launches=2 * args.steps, extra={})
 
 
 # ---------------------------------------------------------------------------

@@ -165,6 +165,20 @@ __device__ __forceinline__ bool pred_eval_t(const DevPred& p, u64 x) {
   return r != (p.negate != 0);
 }
 
+// the same test without the negate flag (callers that evaluate many words
+// apply it once to the whole keep mask); PC_GEN still applies it itself
+template <int PC>
+__device__ __forceinline__ bool pred_raw_t(const DevPred& p, u64 x) {
+  if (PC == PC_MASK) return (x & p.a) == p.b;
+  if (PC == PC_MOD) {
+    const u64 y = x - p.b;
+    return (x >= p.b) & ((y & ((1ull << p.tz) - 1ull)) == 0) & ((y >> p.tz) * p.inv <= p.lim);
+  }
+  if (PC == PC_MODODD) return (x >= p.b) & ((x - p.b) * p.inv <= p.lim);
+  if (PC == PC_MODODD0) return x * p.inv <= p.lim;
+  return pred_eval(p, x);
+}
+
 // ---------------------------------------------------------------------------
 // runtime.Rng (SplitMix64 finalizer over a golden-ratio counter)
 static constexpr u64 GOLDEN = 0x9E3779B97F4A7C15ull;

@@ -768,8 +768,9 @@ filter_ws2_kernel(u64* __restrict__ a, DevPred p, u64* m_out, LookbackCtx c, u64
 #pragma unroll
     for (int j = 0; j < J; ++j) {
       const ulonglong2 v = lds2(src + 64 * j + 2 * lane);
-      keep |= ((u32)pred_eval_t<PC>(p, v.x) << (2 * j)) | ((u32)pred_eval_t<PC>(p, v.y) << (2 * j + 1));
+      keep |= ((u32)pred_raw_t<PC>(p, v.x) << (2 * j)) | ((u32)pred_raw_t<PC>(p, v.y) << (2 * j + 1));
     }
+    if (PC != PC_GEN && p.negate) keep ^= (2 * J >= 32) ? 0xffffffffu : ((1u << (2 * J)) - 1u);
     s_keep[s][w * 32 + lane] = keep;
     const u64 cnt = __reduce_add_sync(0xffffffffu, (u32)__popc(keep));  // one REDUX, not 10 shuffles
     if (lane == 0) s_wtot[s][w] = cnt;

@@ -313,7 +313,8 @@ def test_scan_ws2_tile_boundaries(pip, orc, n):
 def test_filter_ws2_tile_boundaries(pip, orc, n):
     P = pip.pred
     x = rand_words(n + 2, n)
-    for p in (P.mod_eq(3, 0), P.mod_eq(5, 2), P.mod_eq(8, 1), P.always(), ~P.always(), P.lt(1 << 62)):
+    for p in (P.mod_eq(3, 0), P.mod_eq(5, 2), P.mod_eq(8, 1), P.always(), ~P.always(), P.lt(1 << 62),
+              ~P.mod_eq(5, 2), ~P.mod_eq(8, 1), ~P.even(), ~P.lt(1 << 62), ~P.mod_eq(3, 0)):
         want = orc.seq_filter(x, p)
         t = dev(x)
         m = pip.strong.filter_kway(t, p)
