@@ -45,6 +45,9 @@ def build(force: bool = False, verbose: bool = False) -> Path:
              "-I", str(ROOT / "include"), "--expt-relaxed-constexpr"]
     if verbose:
         flags += ["-Xptxas", "-v"]
+    extra = os.environ.get("PIP_NVCC_EXTRA")  # measurement builds (e.g. -DPIP_BAR_SPIN=...)
+    if extra:
+        flags += extra.split()
     def compile_one(src: str) -> str:
         obj = objdir / (src + ".o")
         cmd = [nvcc(), *flags, "-c", str(CSRC / src), "-o", str(obj)]

@@ -6,6 +6,10 @@
 
 namespace pip {
 
+#ifndef PIP_BAR_SPIN
+#define PIP_BAR_SPIN 16  // polls before the barrier waiter starts sleeping between polls
+#endif
+
 struct GridSync {
   u32 bar_count, bar_gen, abort, error;
 };
@@ -31,7 +35,7 @@ __device__ __forceinline__ bool grid_barrier(GridSync* g, u32& gen) {
     u32 v = atom_add_acq_rel_u32(&g->bar_count, 1u) + 1u;
     u64 spins = 0;
     while ((int)(v - target) < 0) {
-      if (++spins > 16) __nanosleep(32);
+      if (++spins > PIP_BAR_SPIN) __nanosleep(32);
       if ((spins & 1023) == 0) {
         if (ld_relaxed_u32(&g->abort)) { ok = 0; break; }
         if (spins > (1ull << 26)) { atomicExch(&g->abort, 1u); ok = 0; break; }

@@ -247,8 +247,18 @@ __global__ void __launch_bounds__(TR_T) tr_split_scatter(const u32* __restrict__
 // pre-child-count << 32 | is_left << 34.  (A committed node's own value is
 // not folded into by any other commit of its round — its parent and child
 // cannot commit with it — so the commit reads it directly.)
+// the committed ids of the round sit at nxt[fill - ncommit, fill) (tr_split_scatter);
+// their count is read on the device, so no host sync separates the split
+// from the commits
+__device__ __forceinline__ const u32* tr_committed(const u32* nxt, u64 fill, const TrDev* d, u64& nv) {
+  nv = d->ncommit;
+  return nxt + (fill - nv);
+}
+
 __global__ void tr_gather(const u64* __restrict__ pa, const u64* __restrict__ lf, const u64* __restrict__ rt,
-                          const u32* __restrict__ vs, u64 nv, u64* g) {
+                          const u32* __restrict__ nxt, u64 fill, const TrDev* __restrict__ d, u64* g) {
+  u64 nv;
+  const u32* vs = tr_committed(nxt, fill, d, nv);
   for (u64 k = (u64)blockIdx.x * TR_T + threadIdx.x; k < nv; k += (u64)gridDim.x * TR_T) {
     const u64 v = vs[k];
     const u64 a = pa[v], l = lf[v], r = rt[v];
@@ -275,8 +285,19 @@ __device__ __forceinline__ void tr_combine(u64* t, u64 x, int op) {
 }
 
 // debug sweep (contraction.py:481-485): committed ids into a set first
-__global__ void tr_violations(const u32* __restrict__ vs, u64 nv, const u64* __restrict__ g,
+__global__ void tr_hash_committed(const u32* __restrict__ nxt, u64 fill, const TrDev* __restrict__ d,
+                                  u32* keys, u32 logc) {
+  u64 nv;
+  const u32* vs = tr_committed(nxt, fill, d, nv);
+  for (u64 k = (u64)blockIdx.x * TR_T + threadIdx.x; k < nv; k += (u64)gridDim.x * TR_T)
+    tr_insert(keys, logc, vs[k]);
+}
+
+__global__ void tr_violations(const u32* __restrict__ nxt, u64 fill, const u64* __restrict__ g,
                               const u32* __restrict__ keys, u32 logc, TrDev* d) {
+  u64 nv = d->ncommit;
+  (void)nxt;
+  (void)fill;
   u32 c = 0;
   for (u64 k = (u64)blockIdx.x * TR_T + threadIdx.x; k < nv; k += (u64)gridDim.x * TR_T)
     c += tr_member(keys, logc, tr_w((u32)g[2 * k]));
@@ -286,9 +307,11 @@ __global__ void tr_violations(const u32* __restrict__ vs, u64 nv, const u64* __r
 
 // rake-parent map value: bits 0-7 rakes this round, 8-9 the parent's
 // pre-round child count, 10 "the parent is a root"
-__global__ void tr_commit(u64* pa, u64* lf, u64* rt, u64* values, const u32* __restrict__ vs, u64 nv,
+__global__ void tr_commit(u64* pa, u64* lf, u64* rt, u64* values, const u32* __restrict__ nxt, u64 fill,
                           const u64* __restrict__ g, int op, u32* mkeys, u32* mval, u32 logm, u64* roots,
                           TrDev* d) {
+  u64 nv;
+  const u32* vs = tr_committed(nxt, fill, d, nv);
   for (u64 k = (u64)blockIdx.x * TR_T + threadIdx.x; k < nv; k += (u64)gridDim.x * TR_T) {
     const u64 v = vs[k];
     const u64 w0 = g[2 * k], w1 = g[2 * k + 1], val = values[v];
@@ -513,57 +536,54 @@ int tree_contract_device(u64* pa, u64* lf, u64* rt, const u64* p, u64* values, u
     tr_split_scan<<<1, 1024, 0, st>>>(bcnt, nblk, d);
     tr_split_scatter<<<(unsigned)nblk, TR_T, 0, st>>>(act[cur], cflag, fill, bcnt, act[cur ^ 1], d);
     PIP_CHECK_LAUNCH();
+    // ---- gather, (debug) violations, fold + surgery, rake parents, roots:
+    // sized for the whole list, each kernel reads the committed count itself
+    const u32* nxt = act[cur ^ 1];
+    tr_gather<<<grid_for(fill), TR_T, 0, st>>>(pa, lf, rt, nxt, fill, d, g);
+    PIP_CHECK_LAUNCH();
+    if (debug) {
+      tr_hash_committed<<<grid_for(fill), TR_T, 0, st>>>(nxt, fill, d, hkeys, L.logh);
+      tr_violations<<<grid_for(fill), TR_T, 0, st>>>(nxt, fill, g, hkeys, L.logh, d);
+      PIP_CHECK_LAUNCH();
+      PIP_CUDA(cudaMemsetAsync(hkeys, 0xff, L.hc * 4, st));
+    }
+    tr_commit<<<grid_for(fill), TR_T, 0, st>>>(pa, lf, rt, values, nxt, fill, g, op, hkeys, mval, L.logh, roots,
+                                               d);
+    PIP_CHECK_LAUNCH();
+    tr_collect<<<grid_for(L.hc), TR_T, 0, st>>>(hkeys, mval, L.hc, cursor, list, d);
+    PIP_CHECK_LAUNCH();
+    // the round's one host sync: committed count, pushes, roots
     PIP_CUDA(cudaMemcpyAsync(&hd, d, sizeof(hd), cudaMemcpyDeviceToHost, st));
     PIP_CUDA(cudaStreamSynchronize(st));
+    PIP_CUDA(cudaMemsetAsync(hkeys, 0xff, L.hc * 4, st));
+    PIP_CUDA(cudaMemsetAsync(mval, 0, L.hc * 4, st));
     const u64 nv = hd.ncommit;
-    const u32* vs = act[cur ^ 1] + (fill - nv);
     if (committed_per_round_host && rounds < rounds_cap) committed_per_round_host[rounds] = nv;
     if (trace_host && nv) {
       std::vector<u32> t(nv);
-      PIP_CUDA(cudaMemcpy(t.data(), vs, nv * 4, cudaMemcpyDeviceToHost));
+      PIP_CUDA(cudaMemcpy(t.data(), nxt + (fill - nv), nv * 4, cudaMemcpyDeviceToHost));
       for (u64 k = 0; k < nv; ++k) trace_host[traced + k] = t[k];
     }
     traced += nv;
     ++rounds;
-    if (nv) {
-      // ---- gather, (debug) violations, fold + surgery, rake parents, roots
-      tr_gather<<<grid_for(nv), TR_T, 0, st>>>(pa, lf, rt, vs, nv, g);
-      PIP_CHECK_LAUNCH();
-      if (debug && nv > 1) {
-        tr_hash_ids<<<grid_for(nv), TR_T, 0, st>>>(vs, nv, hkeys, L.logh);
-        tr_violations<<<grid_for(nv), TR_T, 0, st>>>(vs, nv, g, hkeys, L.logh, d);
-        PIP_CHECK_LAUNCH();
-        PIP_CUDA(cudaMemsetAsync(hkeys, 0xff, L.hc * 4, st));
+    violations += hd.violations;
+    if (hd.nroots) {
+      memcpy(roots_host + 2 * nroots, hr.h, (size_t)hd.nroots * 16);
+      nroots += hd.nroots;
+    }
+    const u64 np = hd.npush;
+    if (np) {
+      if (qsize + np > Q) return PIP_ERR_TABLE;
+      if (np > 1) {  // np.unique order: ascending ids
+        const u64 sg[2] = {0, np};
+        const u32 sl = (u32)np;
+        PIP_CUDA(cudaMemcpyAsync(seg, &sg[0], 8, cudaMemcpyHostToDevice, st));
+        PIP_CUDA(cudaMemcpyAsync((u32*)(seg + 1), &sl, 4, cudaMemcpyHostToDevice, st));
+        if (int rc = sort_segments_grid_device(list, seg, (const u32*)(seg + 1), 1, np, st)) return rc;
       }
-      tr_commit<<<grid_for(nv), TR_T, 0, st>>>(pa, lf, rt, values, vs, nv, g, op, hkeys, mval, L.logh, roots,
-                                                d);
+      tr_push<<<grid_for(np), TR_T, 0, st>>>(list, np, ring, Q, (qhead + qsize) % Q);
       PIP_CHECK_LAUNCH();
-      tr_collect<<<grid_for(L.hc), TR_T, 0, st>>>(hkeys, mval, L.hc, cursor, list, d);
-      PIP_CHECK_LAUNCH();
-      PIP_CUDA(cudaMemcpyAsync(&hd, d, sizeof(hd), cudaMemcpyDeviceToHost, st));
-      PIP_CUDA(cudaStreamSynchronize(st));
-      PIP_CUDA(cudaMemsetAsync(hkeys, 0xff, L.hc * 4, st));
-      PIP_CUDA(cudaMemsetAsync(mval, 0, L.hc * 4, st));
-      violations += hd.violations;
-      if (hd.nroots) {
-        memcpy(roots_host + 2 * nroots, hr.h, (size_t)hd.nroots * 16);
-        nroots += hd.nroots;
-      }
-      const u64 np = hd.npush;
-      if (np) {
-        if (qsize + np > Q) return PIP_ERR_TABLE;
-        if (np > 1) {  // np.unique order: ascending ids
-          const u64 sg[2] = {0, np};
-          const u32 sl = (u32)np;
-          PIP_CUDA(cudaMemcpyAsync(seg, &sg[0], 8, cudaMemcpyHostToDevice, st));
-          PIP_CUDA(cudaMemcpyAsync((u32*)(seg + 1), &sl, 4, cudaMemcpyHostToDevice, st));
-          if (int rc = sort_segments_grid_device(list, seg, (const u32*)(seg + 1), 1, np, st)) return rc;
-        }
-        tr_push<<<grid_for(np), TR_T, 0, st>>>(list, np, ring, Q, (qhead + qsize) % Q);
-        PIP_CHECK_LAUNCH();
-        qsize += np;
-      }
-      PIP_CUDA(cudaStreamSynchronize(st));  // host-side seg values and roots copies
+      qsize += np;
     }
     if (nv == 0) {
       if (++zero_rounds >= 64) {
