@@ -96,3 +96,19 @@ def test_host_entry_points_reject_bad_predicates_before_any_transfer():
         assert lib.pip_filter_u64_host(a.ctypes.data, len(a), C.byref(p), C.byref(m), 0) == 1
         assert lib.pip_partition_u64_host(a.ctypes.data, len(a), C.byref(p), C.byref(m), 0) == 1
     assert np.array_equal(a, np.arange(10, dtype=np.uint64))
+
+
+def test_header_compiles_as_plain_c_and_cpp(tmp_path):
+    """A C or C++ binder includes pip.h on its own: no CUDA
+    or torch types in the signatures."""
+    import shutil
+    import subprocess
+
+    if not shutil.which("gcc"):
+        pytest.skip("gcc unavailable")
+    src = tmp_path / "use.c"
+    src.write_text('#include "pip.h"\nint main(void) { return pip_version() == 1 ? 0 : 1; }\n')
+    for cmd in (["gcc", "-std=c99", "-fsyntax-only", "-Wall", "-Werror"],
+                ["g++", "-std=c++11", "-fsyntax-only", "-Wall", "-Werror", "-x", "c++"]):
+        r = subprocess.run(cmd + ["-I", str(ROOT / "include"), str(src)], capture_output=True, text=True)
+        assert r.returncode == 0, r.stderr
