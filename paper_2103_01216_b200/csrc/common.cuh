@@ -220,18 +220,30 @@ __device__ __forceinline__ u64 warp_incl_scan(u64 v) {
 
 // ---------------------------------------------------------------------------
 // decoupled look-back tile status, O(#CTAs) and reusable (see scan.cu)
-// 16 bytes, written and read with single 128-bit accesses (as CUB's tile
-// descriptors): value and (epoch << 2 | state) are always seen together.
+// 16 bytes, written and read as ONE scalar .b128 access each (PTX ISA 8.3+):
+// a relaxed .gpu-scope b128 load or store is a single memory operation, so it
+// is single-copy atomic and value and (epoch << 2 | state) are always seen
+// together.  (A .v2.u64 vector access would be two operations to the memory
+// model even though it issues the same LDG/STG.E.128.STRONG.GPU.)
 struct __align__(16) TileSlot {
   u64 value;
   u64 flag;  // (epoch << 2) | state ; epoch = tile + 1
 };
 enum : u32 { SLOT_BUSY = 0, SLOT_AGG = 1, SLOT_INCL = 2 };
 __device__ __forceinline__ void st_slot(TileSlot* s, u64 value, u64 flag) {
-  asm volatile("st.global.cg.v2.u64 [%0], {%1, %2};" ::"l"(s), "l"(value), "l"(flag) : "memory");
+  asm volatile(
+      "{\n\t.reg .b128 t;\n\tmov.b128 t, {%1, %2};\n\t"
+      "st.relaxed.gpu.global.b128 [%0], t;\n\t}" ::"l"(s),
+      "l"(value), "l"(flag)
+      : "memory");
 }
 __device__ __forceinline__ void ld_slot(const TileSlot* s, u64& value, u64& flag) {
-  asm volatile("ld.global.cg.v2.u64 {%0, %1}, [%2];" : "=l"(value), "=l"(flag) : "l"(s) : "memory");
+  asm volatile(
+      "{\n\t.reg .b128 t;\n\tld.relaxed.gpu.global.b128 t, [%2];\n\t"
+      "mov.b128 {%0, %1}, t;\n\t}"
+      : "=l"(value), "=l"(flag)
+      : "l"(s)
+      : "memory");
 }
 
 }  // namespace pip
@@ -261,6 +273,23 @@ __device__ __forceinline__ void mbar_wait(u64* bar, u32 phase) {
       "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
       "r"(phase)
       : "memory");
+}
+#ifndef PIP_WAIT_NS
+#define PIP_WAIT_NS 0  // 0: plain try_wait in the pipelines' wait loops
+#endif
+// a probe that lets the hardware suspend the thread for up to `ns`
+// nanoseconds while the phase is incomplete (fewer issue slots spent on
+// waiting warps; callers still see their abort flag at least every `ns`)
+__device__ __forceinline__ bool mbar_try_sleep(u64* bar, u32 phase, u32 ns) {
+  u32 ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+      "selp.u32 %0, 1, 0, p;\n}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(phase), "r"(ns)
+      : "memory");
+  return ok != 0;
 }
 // one non-blocking probe of the phase with parity `phase`
 __device__ __forceinline__ bool mbar_try(u64* bar, u32 phase) {

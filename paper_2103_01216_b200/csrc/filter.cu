@@ -649,7 +649,7 @@ filter_ws2_kernel(u64* __restrict__ a, DevPred p, u64* m_out, LookbackCtx c, u64
   __syncthreads();
   auto ph = [&](u64 k) { return (u32)((k / S) & 1); };
   auto wait_or_abort = [&](u64* bar, u32 phase) -> bool {
-    while (!mbar_try(bar, phase))
+    while (!(PIP_WAIT_NS ? mbar_try_sleep(bar, phase, PIP_WAIT_NS) : mbar_try(bar, phase)))
       if (s_abort) return false;
     return true;
   };

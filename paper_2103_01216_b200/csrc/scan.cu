@@ -648,7 +648,7 @@ scan_ws2_kernel(u64* __restrict__ a, u64 init, const u64* carry_in, u64* total, 
   __syncthreads();
   auto ph = [&](u64 k) { return (u32)((k / S) & 1); };
   auto wait_or_abort = [&](u64* bar, u32 phase) -> bool {
-    while (!mbar_try(bar, phase))
+    while (!(PIP_WAIT_NS ? mbar_try_sleep(bar, phase, PIP_WAIT_NS) : mbar_try(bar, phase)))
       if (s_abort) return false;
     return true;
   };
