@@ -727,11 +727,14 @@ def run_merge(args, ws, rank, local, torch, pip, lib):
             "frac": round(achieved / pk["hbm_gbs"], 4), "traffic": (tb * n) if tb else None,
             "two_pass_achieved": round(two_pass, 1),
             "two_pass_frac": round(two_pass / pk["hbm_gbs"], 4),
-            "note": "frac: 16 B/word algorithmic (each word read once, written once).  An "
-                    "in-place merge with b(n) = 0.02 n words of workspace cannot run in one "
-                    "pass (DESIGN.md 3.3: a single pass would hold ~n/4 words in flight), so "
-                    "it moves >= 32 B/word (chunk permutation + block merge); two_pass_frac is "
-                    "against that floor"}
+            "displacement_bound_frac": round(24 * n / (per_step / 1e3) / 1e9 / pk["hbm_gbs"], 4),
+            "note": "frac: 16 B/word algorithmic (each word read once, written once).  With "
+                    "b(n) = 0.02 n words of workspace and sequential accesses every displaced "
+                    "A word must be parked once: >= 24 B/word for equal interleaved runs "
+                    "(displacement_bound_frac; DESIGN.md 3.3).  This implementation's two "
+                    "parallel passes (chunk permutation + block merge) move 32 B/word; "
+                    "two_pass_frac is the kernels' DRAM throughput on those bytes, not a "
+                    "lower bound"}
     e2e = None if args.no_e2e else e2e_host(lib, "merge", n, args, torch, dev, ws, budget=b)
     cpu = None if args.no_cpu else cpu_baseline("merge", args)
     cfg = {"workload": "in-place merge of two sorted runs (merge_relaxed, eps=0.5, f=0.02), "
