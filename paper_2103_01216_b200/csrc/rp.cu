@@ -42,6 +42,7 @@ namespace pip {
 static constexpr int RP_THREADS = 256;
 static constexpr u64 RP_EMPTY = ~0ull;
 static constexpr u32 RP_NOSLOT = 0xffffffffu;
+static constexpr u32 RP_TMASK = 0x7fffffffu;  // BM 1: tg bit 31 = first marker
 static constexpr u64 RP_ROUND_CHUNK = 512;  // committed counts per launch
 
 struct RpGlobal {
@@ -221,6 +222,33 @@ __device__ __forceinline__ void sum_counts(const u32* cnt, u32 G, u32 b, u64* s_
   __syncthreads();
 }
 
+// sum of cnt[0..G), exclusive prefix up to b, and the sum of cnt2[0..G)
+__device__ __forceinline__ void sum_counts2(const u32* cnt, const u32* cnt2, u32 G, u32 b, u64* s_red,
+                                            u64& total, u64& before, u64& total2) {
+  if (threadIdx.x < 32) {
+    u64 t = 0, bf = 0, t2 = 0;
+    for (u32 i = threadIdx.x; i < G; i += 32) {
+      const u64 v = __ldcg(cnt + i);
+      t2 += __ldcg(cnt2 + i);
+      t += v;
+      if (i < b) bf += v;
+    }
+    t = warp_reduce<Op<PIP_OP_ADD>>(t);
+    bf = warp_reduce<Op<PIP_OP_ADD>>(bf);
+    t2 = warp_reduce<Op<PIP_OP_ADD>>(t2);
+    if (threadIdx.x == 0) {
+      s_red[33] = t;
+      s_red[34] = bf;
+      s_red[35] = t2;
+    }
+  }
+  __syncthreads();
+  total = s_red[33];
+  before = s_red[34];
+  total2 = s_red[35];
+  __syncthreads();
+}
+
 // non-self ids in [x, y] (inclusive), summed over the CTA: whole blocks from
 // the block counts, the ragged ends from H itself
 __device__ __forceinline__ u64 count_nonself_range(const RpArgs& A, u64 x, u64 y) {
@@ -317,6 +345,16 @@ __global__ void __launch_bounds__(RP_THREADS, 4) rp_kernel(RpArgs A) {
   while (!R.done) {
     // ======================= P1: retire previous round =====================
     const u32 old = R.ping, nw = R.ping ^ 1u;
+    // BM 1: two bitmap pairs by round parity.  This round marks and reads
+    // (Bc, Cc); its failures mark the NEXT round's targets in (Bp, Cp) as
+    // soon as they fail, and the fresh ids mark during the refill, so no
+    // separate mark phase (and no grid barrier for it) is needed.  (Bp, Cp)
+    // held the previous round's marks and are cleared by the retire below.
+    const u64 pofs = BM == 1 ? (R.rounds & 1u) * A.bm_words : 0, qofs = BM == 1 ? A.bm_words - pofs : 0;
+    u32* const Bc = A.bmB + pofs;
+    u32* const Cc = A.bmC + pofs;
+    u32* const Bp = A.bmB + qofs;
+    u32* const Cp = A.bmC + qofs;
     const u32* ids_o = A.ids[old];
     const u32* tg_o = A.tg[old];
     u32* ids_n = A.ids[nw];
@@ -325,7 +363,14 @@ __global__ void __launch_bounds__(RP_THREADS, 4) rp_kernel(RpArgs A) {
     if (!R.first) {
       const u64 F = R.fill;
       u64 fbefore;
-      sum_counts(A.failcnt, G, b, s_red, nfail, fbefore);
+      if (BM == 1) {
+        // the previous round's distinct out-of-window targets ride along
+        u64 claims_total;
+        sum_counts2(A.failcnt, A.claimcnt, G, b, s_red, nfail, fbefore, claims_total);
+        if (claims_total > R.peak) R.peak = claims_total;
+      } else {
+        sum_counts(A.failcnt, G, b, s_red, nfail, fbefore);
+      }
       const u64 ncommit = F - nfail;
       // committed-per-round + livelock bookkeeping (identical in every CTA)
       if (b == 0 && tid == 0) {
@@ -381,10 +426,16 @@ __global__ void __launch_bounds__(RP_THREADS, 4) rp_kernel(RpArgs A) {
           iv[q] = inx[q];
           tv[q] = tnx[q];
           if (kb + q < e) {
-            if (cn[q]) cm |= 1u << q;
+            if (BM == 1 ? (cn[q] & 1u) : cn[q]) cm |= 1u << q;
             else fm |= 1u << q;
           }
+          // BM 1: bit 2 = the failure was its next-round target's first marker
+          // (tg bit 31 in the new list); bit 3 = it holds a table slot
+          if (BM == 1) tv[q] = (tv[q] & RP_TMASK) | ((u32)(cn[q] & 4u) << 29);
         }
+        u32 cf1[RB];
+#pragma unroll
+        for (int q = 0; q < RB; ++q) cf1[q] = cn[q];
         // (scheme 3 only: the large rounds of C4 gain 0.8 ms; at C0's size the
         // extra live registers spill and cost more than they hide)
         if (BM == 3) {
@@ -420,13 +471,16 @@ __global__ void __launch_bounds__(RP_THREADS, 4) rp_kernel(RpArgs A) {
         for (int q = 0; q < RB; ++q) {
           const u64 k = kb + q;
           if (k >= e) continue;
-          if (BM == 1 || (!BM && targeted)) {
+          if (BM == 1) {
+            if (cf1[q] & 8u) A.table[__ldcg(A.slot + k)] = RP_EMPTY;
+          } else if (!BM && targeted) {
             const u32 sl = __ldcg(A.slot + k);
             if (sl != RP_NOSLOT) A.table[sl] = RP_EMPTY;
           }
           if (BM && BM != 3 && F * 256 < A.n) {  // sparse round: clear the touched words
-            A.bmB[tv[q] >> 5] = 0u;
-            if (BM == 1) A.bmC[tv[q] >> 5] = 0u;
+            const u32 tq = tv[q] & RP_TMASK;
+            Bp[tq >> 5] = 0u;
+            if (BM == 1) Cp[tq >> 5] = 0u;
           }
         }
       }
@@ -446,8 +500,8 @@ __global__ void __launch_bounds__(RP_THREADS, 4) rp_kernel(RpArgs A) {
         u64 ts, te;
         part(A.bm_words, G, b, ts, te);
         for (u64 x = ts + tid; x < te; x += T) {
-          A.bmB[x] = 0u;
-          if (BM == 1) A.bmC[x] = 0u;
+          Bp[x] = 0u;
+          if (BM == 1) Cp[x] = 0u;
         }
       }
       if ((BM == 2 || BM == 3) && R.logcap_c && A.lf) {
@@ -521,7 +575,7 @@ __global__ void __launch_bounds__(RP_THREADS, 4) rp_kernel(RpArgs A) {
       if (BM) {
         part(A.bm_words, G, b, ts, te);
         for (u64 x = ts + tid; x < te; x += T)
-          if (__ldcg(A.bmB + x) | (BM == 1 ? __ldcg(A.bmC + x) : 0u)) atomicExch(&g->sync.error, (u32)PIP_ERR_DEBUG_SWEEP);
+          if (__ldcg(Bp + x) | (BM == 1 ? __ldcg(Cp + x) : 0u)) atomicExch(&g->sync.error, (u32)PIP_ERR_DEBUG_SWEEP);
         if (BM == 3) {
           part(1ull << (A.logf - 5), G, b, ts, te);
           for (u64 x = ts + tid; x < te; x += T)
@@ -572,13 +626,34 @@ __global__ void __launch_bounds__(RP_THREADS, 4) rp_kernel(RpArgs A) {
         }
         u32 tot;
         u64 rank = run + block_excl_sum(__popc(fm), s_cnt, &tot);
+        u32 mk[RB];  // BM 1: the fresh iterates mark their targets here
+        if (BM == 1) {
+          u64 rk = rank;
+#pragma unroll
+          for (int q = 0; q < RB; ++q) {
+            mk[q] = 0u;
+            if ((fm >> q) & 1u) {
+              if (rk < fresh) mk[q] = 1u;
+              ++rk;
+            }
+          }
+#pragma unroll
+          for (int q = 0; q < RB; ++q)
+            if (mk[q]) mk[q] = atomicOr(Bc + ((u32)hv[q] >> 5), 1u << (hv[q] & 31));
+        }
 #pragma unroll
         for (int q = 0; q < RB; ++q)
           if ((fm >> q) & 1u) {
             if (rank < fresh) {
               const u64 id = hi - (qb + q);
               ids_n[nfail + rank] = (u32)id;
-              tg_n[nfail + rank] = (u32)hv[q];
+              u32 tw = (u32)hv[q];
+              if (BM == 1) {
+                const u32 bit = 1u << (tw & 31);
+                if (mk[q] & bit) atomicOr(Cc + (tw >> 5), bit);
+                else tw |= 0x80000000u;  // first marker
+              }
+              tg_n[nfail + rank] = tw;
               if (rank == 0) g->dhi = id;
               if (rank == fresh - 1) g->dlo = id;
             }
@@ -615,23 +690,7 @@ __global__ void __launch_bounds__(RP_THREADS, 4) rp_kernel(RpArgs A) {
       part(newF, G, b, s, e);
       u32 claims = 0;
       if (BM == 1) {
-        for (u64 k0 = s + tid; k0 < e; k0 += (u64)RB * T) {
-          u32 t[RB], old[RB];
-#pragma unroll
-          for (int q = 0; q < RB; ++q) t[q] = k0 + q * T < e ? __ldcs(tg_n + k0 + q * T) : 0u;
-#pragma unroll
-          for (int q = 0; q < RB; ++q)
-            old[q] = k0 + q * T < e ? atomicOr(A.bmB + (t[q] >> 5), 1u << (t[q] & 31)) : 0u;
-#pragma unroll
-          for (int q = 0; q < RB; ++q) {
-            const u64 k = k0 + q * T;
-            if (k >= e) continue;
-            const u32 bit = 1u << (t[q] & 31);
-            if (old[q] & bit) atomicOr(A.bmC + (t[q] >> 5), bit);
-            else if (t[q] < dlo || t[q] > dhi) claims += 1;
-            A.slot[k] = RP_NOSLOT;
-          }
-        }
+        // marks already made (refill / previous round's failures)
       } else if (BM == 2) {
         // mark: first toucher of t sets B[t]; later ones go to the list.  The
         // reference's table holds the distinct out-of-window targets: count
@@ -707,56 +766,104 @@ __global__ void __launch_bounds__(RP_THREADS, 4) rp_kernel(RpArgs A) {
         A.slot[k] = sl;
       }
       }
-      const u64 c = block_sum(claims, s_red);
-      if (tid == 0) A.claimcnt[b] = (u32)c;
+      if (BM != 1) {
+        const u64 c = block_sum(claims, s_red);
+        if (tid == 0) A.claimcnt[b] = (u32)c;
+      }
     }
     if (BM == 1) {
       // P3b: iterates on targets hit once (no C bit) are their target's only
       // reserver and commit now; the few on C targets reserve in the
-      // write-max table and are resolved in P4 (cflag 2).
-      if (!grid_barrier(&g->sync, gen)) break;
+      // write-max table and are resolved in P4 (cflag 2).  A failure marks
+      // its target for the next round in (Bp, Cp) right away (cflag bit 2 =
+      // first marker there).  The distinct out-of-window targets
+      // (peak_table_load) are the first markers outside [dlo, dhi].
       tick(2);
-      u64 claims_total, dummy;
-      sum_counts(A.claimcnt, G, b, s_red, claims_total, dummy);
-      if (claims_total > R.peak) R.peak = claims_total;
       u64 s, e;
       part(newF, G, b, s, e);
-      u32 fails = 0, dclaim = 0;
+      u32 fails = 0, dclaim = 0, claims1 = 0;
+      // the next round's window [cursor - span + 1, cursor] is known now: its
+      // H words are loaded here, in flight with this phase's chain (<= 4 per
+      // thread; wider CTA shares count at the end of the round as before)
+      constexpr int WPT = 4;
+      u32 wnon = 0;
+      bool wdone = false;
+      u64 wv[WPT], wid[WPT];
+      u64 whi = 0, ws = 0, we = 0;
+      if (V == PIP_RP_FINAL && cursor >= 0) {
+        whi = (u64)cursor;
+        const u64 wlo = whi + 1 >= A.span_cap ? whi + 1 - A.span_cap : 0;
+        part(whi - wlo + 1, G, b, ws, we);
+        if (we - ws <= (u64)WPT * T) {
+          wdone = true;
+#pragma unroll
+          for (int q = 0; q < WPT; ++q) {
+            const u64 x = ws + tid + (u64)q * T;
+            wid[q] = x < we ? whi - x : ~0ull;
+            wv[q] = x < we ? __ldcs(A.h + wid[q]) : ~0ull;
+          }
+        }
+      }
+      auto mark_next = [&](u32 t) -> u32 {
+        const u32 bit = 1u << (t & 31);
+        if (atomicOr(Bp + (t >> 5), bit) & bit) {
+          atomicOr(Cp + (t >> 5), bit);
+          return 0u;
+        }
+        return 4u;
+      };
       for (u64 k = s + tid; k < e; k += T) {
-        const u32 t = __ldcs(tg_n + k), i = __ldcs(ids_n + k);
-        if ((__ldcg(A.bmC + (t >> 5)) >> (t & 31)) & 1u) {
+        const u32 tw = __ldcs(tg_n + k), i = __ldcs(ids_n + k);
+        const u32 t = tw & RP_TMASK;
+        if ((tw >> 31) && (t < dlo || t > dhi)) claims1 += 1;
+        const u32 cw = __ldcg(Cc + (t >> 5)), bw = __ldcg(Bc + (i >> 5));
+        if ((cw >> (t & 31)) & 1u) {
           A.slot[k] = table_reserve(A.table, A.logcap, t, i, dclaim, &g->sync.error);
           A.cflag[k] = 2;
         } else {
-          const bool c = !((__ldcg(A.bmB + (i >> 5)) >> (i & 31)) & 1u);
-          A.cflag[k] = c;
+          const bool c = !((bw >> (i & 31)) & 1u);
           if (c) {
+            A.cflag[k] = 1;
             if (!(A.dbg & 1)) {
               const u64 x = __ldcg(A.a + i), y = __ldcg(A.a + t);
               A.a[i] = y;
               A.a[t] = x;
             }
           } else {
+            A.cflag[k] = (unsigned char)mark_next(t);
             fails += 1;
           }
+        }
+      }
+      if (wdone) {
+#pragma unroll
+        for (int q = 0; q < WPT; ++q) wnon += wid[q] != ~0ull && wv[q] != wid[q];
+      }
+      {
+        // claims (summed by the next retire) and the next window's count
+        const u64 c = block_sum(((u64)wnon << 32) | claims1, s_red);
+        if (tid == 0) {
+          A.claimcnt[b] = (u32)c;
+          if (wdone) A.wcnt[b] = (u32)(c >> 32);
         }
       }
       if (!grid_barrier(&g->sync, gen)) break;
       for (u64 k = s + tid; k < e; k += T) {
         if (__ldcs(A.cflag + k) != 2) continue;
-        const u32 t = __ldcs(tg_n + k), i = __ldcs(ids_n + k);
-        const bool own = !((__ldcg(A.bmB + (i >> 5)) >> (i & 31)) & 1u);
+        const u32 t = __ldcs(tg_n + k) & RP_TMASK, i = __ldcs(ids_n + k);
+        const bool own = !((__ldcg(Bc + (i >> 5)) >> (i & 31)) & 1u);
         const u32 sl = __ldcg(A.slot + k);
         const u64 w = sl == RP_NOSLOT ? RP_EMPTY : __ldcg(A.table + sl);
         const bool c = own && w != RP_EMPTY && (u32)(w >> 32) == t && (u32)w == i;
-        A.cflag[k] = c;
         if (c) {
+          A.cflag[k] = 1u | 8u;
           if (!(A.dbg & 1)) {  // PIP_RP_DBG=1: measurement only, no swaps
             const u64 x = __ldcg(A.a + i), y = __ldcg(A.a + t);
             A.a[i] = y;
             A.a[t] = x;
           }
         } else {
+          A.cflag[k] = (unsigned char)(mark_next(t) | (sl == RP_NOSLOT ? 0u : 8u));
           fails += 1;
         }
       }
@@ -931,7 +1038,16 @@ __global__ void __launch_bounds__(RP_THREADS, 4) rp_kernel(RpArgs A) {
     R.wpre = 0;
     R.rlo = band_lo;
     R.rhi = band_hi;
-    if (V == PIP_RP_FINAL && cursor >= 0) {  // count the next round's window now
+    bool wcounted = false;
+    if (BM == 1) {  // P3b counted the next window when it fit its loads
+      const u64 whi = cursor >= 0 ? (u64)cursor : 0;
+      const u64 wlo = whi + 1 >= A.span_cap ? whi + 1 - A.span_cap : 0;
+      u64 ws, we;
+      part(whi - wlo + 1, G, b, ws, we);
+      wcounted = cursor >= 0 && we - ws <= (u64)4 * T;
+      if (wcounted) R.wpre = 1;
+    }
+    if (V == PIP_RP_FINAL && cursor >= 0 && !wcounted) {  // count the next round's window now
       hi = (u64)cursor;
       lo = hi + 1 >= A.span_cap ? hi + 1 - A.span_cap : 0;
       wd = hi - lo + 1;
@@ -1006,7 +1122,9 @@ static RpLayout rp_layout_mode(u64 n, u64 prefix, int variant, u64 cap, int gmax
   L.slot = take(bm == 2 ? 0 : prefix * 4);
   L.cflag = take(prefix);
   L.dense = take(variant == PIP_RP_FINAL && !bm ? (prefix + prefix / 4 + 8) * 4 : 0);
-  L.table = take(cap * 8);
+  // BM 1: only the iterates on twice-hit targets use the table, at most
+  // prefix / 2 distinct keys
+  L.table = take((bm == 1 ? pow2_at_least(prefix) : cap) * 8);
   L.failcnt = take((size_t)gmax * 4);
   L.wcnt = take((size_t)gmax * 4);
   L.claimcnt = take((size_t)gmax * 4);
@@ -1014,8 +1132,8 @@ static RpLayout rp_layout_mode(u64 n, u64 prefix, int variant, u64 cap, int gmax
   L.global = take(sizeof(RpGlobal));
   L.resume = take(sizeof(RpResume));
   L.bm_words = bm ? (n + 31) / 32 : 0;
-  L.bmB = take(L.bm_words * 4);
-  L.bmC = take(bm == 1 ? L.bm_words * 4 : 0);
+  L.bmB = take(L.bm_words * 4 * (bm == 1 ? 2 : 1));  // BM 1: one pair per round parity
+  L.bmC = take(bm == 1 ? L.bm_words * 4 * 2 : 0);
   L.lc = take(bm >= 2 ? prefix * 4 : 0);
   L.lccnt = take(bm >= 2 ? (size_t)gmax * 4 : 0);
   L.logf = 0;
@@ -1048,6 +1166,7 @@ static RpLayout rp_layout(u64 n, u64 prefix, int variant, u64 cap, int gmax) {
   if (variant == PIP_RP_FINAL) {
     int want = n <= (1ull << 28) ? 1 : 3;
     if (const char* e = getenv("PIP_RP_BM")) want = atoi(e);
+    if (want == 1 && n > (1ull << 31)) want = 3;  // BM 1 keeps a flag in target bit 31
     if (want >= 1 && want <= 3) {
       const RpLayout Lb = rp_layout_mode(n, prefix, variant, cap, gmax, want);
       if ((Lb.total + 7) / 8 <= 8 * prefix || getenv("PIP_RP_BM")) return Lb;
@@ -1102,11 +1221,12 @@ int rp_device(u64* a, const u64* h, u64 n, u64 prefix, int variant, int debug,
   // the client sizes its table / dense window from `prefix` (relaxed.py:84-89)
   const u64 cap = rp_capacity(prefix, variant);
   if (cap > (1ull << 31)) return PIP_ERR_UNSUPPORTED;
-  u32 logcap = 0;
-  while ((1ull << logcap) < cap) ++logcap;
   const int dev = current_device();
   const int gmax = rp_gmax();
   const RpLayout Lrun = rp_layout(n, prefix, variant, cap, gmax);
+  const u64 tcap = Lrun.bm == 1 ? pow2_at_least(prefix) : cap;  // table slots allocated
+  u32 logcap = 0;
+  while ((1ull << logcap) < tcap) ++logcap;
   if (!ws || ws_bytes < Lrun.total) return PIP_ERR_OOM;
   char* w = (char*)ws;
   // validate H and count the non-self iterates (relaxed.py:233, :239)
@@ -1178,11 +1298,11 @@ int rp_device(u64* a, const u64* h, u64 n, u64 prefix, int variant, int debug,
   A.claim2 = Lrun.bm == 3 ? (u32*)(w + Lrun.claim2) : nullptr;
   A.bcnt = Lrun.bm == 3 ? (const u32*)(w + Lrun.bcnt) : nullptr;
 
-  PIP_CUDA(cudaMemsetAsync(A.table, 0xff, cap * 8, st));
+  PIP_CUDA(cudaMemsetAsync(A.table, 0xff, tcap * 8, st));
   if (variant == PIP_RP_FINAL && !Lrun.bm) PIP_CUDA(cudaMemsetAsync(A.dense, 0, A.span_cap * 4, st));
   if (Lrun.bm) {
-    PIP_CUDA(cudaMemsetAsync(A.bmB, 0, Lrun.bm_words * 4, st));
-    if (Lrun.bm == 1) PIP_CUDA(cudaMemsetAsync(A.bmC, 0, Lrun.bm_words * 4, st));
+    PIP_CUDA(cudaMemsetAsync(A.bmB, 0, Lrun.bm_words * 4 * (Lrun.bm == 1 ? 2 : 1), st));
+    if (Lrun.bm == 1) PIP_CUDA(cudaMemsetAsync(A.bmC, 0, Lrun.bm_words * 4 * 2, st));
     if (Lrun.bm == 3) PIP_CUDA(cudaMemsetAsync(A.bmF, 0, (1ull << Lrun.logf) / 8, st));
     if (Lrun.bm >= 2) PIP_CUDA(cudaMemsetAsync(w + Lrun.lf, 0, (1ull << RP_LF_LOG2) / 8, st));
   }
