@@ -117,6 +117,7 @@ int validate_counts(const u64* h, u64 n, u64* nonself, u64* invalid, void* scrat
     validate_kernel<<<(unsigned)blocks, 256, 0, st>>>(h, n, cnt);
     PIP_CHECK_LAUNCH();
   }
+  if (!nonself) return PIP_OK;  // stream-ordered: the caller reads cnt[0..1] on the device
   u64 host[2];
   PIP_CUDA(cudaMemcpyAsync(host, cnt, 16, cudaMemcpyDeviceToHost, st));
   PIP_CUDA(cudaStreamSynchronize(st));

@@ -32,6 +32,7 @@
 // 32-bit (n < 2^32 - 1) to halve the workspace traffic.
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <vector>
 #include <chrono>
 #include <thread>
@@ -101,6 +102,10 @@ struct RpArgs {
   // non-self count of every 2^RP_BLK_SHIFT-id block of H (from the validation
   // pass), so the window counts need no second read of H (NULL = read H)
   const u32* bcnt;
+  // validation counts {non-self iterates, invalid targets}, written on the
+  // device by the validation pass just before the launch (NULL = the host
+  // read them already and set `prefix` = min(prefix, non-self))
+  const u64* vcnt;
 };
 static constexpr u32 RP_BLK_SHIFT = 12;
 static constexpr u32 RP_LF_LOG2 = 24;  // 2 MiB filter
@@ -328,6 +333,18 @@ __global__ void __launch_bounds__(RP_THREADS, 4) rp_kernel(RpArgs A) {
   const u32 b = blockIdx.x, G = gridDim.x, tid = threadIdx.x, T = blockDim.x;
   RpGlobal* g = A.g;
   RpResume R = *A.resume;
+  u64 P = A.prefix;  // run_rounds clamps the active prefix to n_iterates (detres.py:267)
+  if (A.vcnt) {
+    const u64 ns = __ldcg(A.vcnt), bad = __ldcg(A.vcnt + 1);
+    if (bad || ns == 0) {  // nothing to do, or invalid H: a[] is not touched
+      if (b == 0 && tid == 0) {
+        R.done = 1;
+        *A.resume = R;
+      }
+      return;
+    }
+    if (ns < P) P = ns;
+  }
   u32 gen = 0;
   u64 rounds_here = 0;
   const bool trace = A.trace != nullptr;
@@ -527,7 +544,7 @@ __global__ void __launch_bounds__(RP_THREADS, 4) rp_kernel(RpArgs A) {
       }
     }
     // window for the refill (next_ids)
-    const u64 count = A.prefix - nfail;
+    const u64 count = P - nfail;
     long long cursor = R.cursor;
     u64 hi = 0, lo = 0, wd = 0;
     bool win = count > 0 && cursor >= 0;
@@ -1090,7 +1107,7 @@ __global__ void __launch_bounds__(RP_THREADS, 4) rp_kernel(RpArgs A) {
 
 struct RpLayout {
   size_t ids[2], tg[2], slot, cflag, dense, table, failcnt, wcnt, claimcnt, rcounts, global,
-      resume, bmB, bmC, lc, lccnt, total;
+      resume, vcnt, bmB, bmC, lc, lccnt, total;
   u64 bm_words;
   int bm;  // 0 table (+dense window), 1 bitmaps B and C, 2 bitmap B + collided lists,
           // 3 folded collision bitmap + own band of B + collided lists + H block counts
@@ -1131,6 +1148,7 @@ static RpLayout rp_layout_mode(u64 n, u64 prefix, int variant, u64 cap, int gmax
   L.rcounts = take(RP_ROUND_CHUNK * 8);
   L.global = take(sizeof(RpGlobal));
   L.resume = take(sizeof(RpResume));
+  L.vcnt = take(16);  // (rcounts .. vcnt are read back by one copy)
   L.bm_words = bm ? (n + 31) / 32 : 0;
   L.bmB = take(L.bm_words * 4 * (bm == 1 ? 2 : 1));  // BM 1: one pair per round parity
   L.bmC = take(bm == 1 ? L.bm_words * 4 * 2 : 0);
@@ -1196,6 +1214,12 @@ size_t rp_workspace_bytes(u64 n, u64 prefix, int variant) {
   return t;
 }
 
+__global__ void rp_init_kernel(RpResume* r, RpResume r0, u32* g, u32 gwords, u32* failcnt, u32 gmax) {
+  for (u32 x = threadIdx.x; x < gwords; x += blockDim.x) g[x] = 0u;
+  for (u32 x = threadIdx.x; x < gmax; x += blockDim.x) failcnt[x] = 0u;
+  if (threadIdx.x == 0) *r = r0;
+}
+
 template <int V, int BM = 0>
 static int rp_run(RpArgs& A, int grid, cudaStream_t st) {
   auto k = rp_kernel<V, BM>;
@@ -1229,22 +1253,31 @@ int rp_device(u64* a, const u64* h, u64 n, u64 prefix, int variant, int debug,
   while ((1ull << logcap) < tcap) ++logcap;
   if (!ws || ws_bytes < Lrun.total) return PIP_ERR_OOM;
   char* w = (char*)ws;
-  // validate H and count the non-self iterates (relaxed.py:233, :239)
+  // validate H and count the non-self iterates (relaxed.py:233, :239).  The
+  // counts stay on the device for the round kernel (it clamps the prefix and
+  // refuses invalid H before touching a[]), so nothing waits for the host
+  // between the validation and the launch; only the opt-in cluster path
+  // needs them on the host first.
+  const bool cluster_req = variant == PIP_RP_FINAL && !debug && !trace_dev && !prog &&
+                           getenv("PIP_RP_CLUSTER") != nullptr;
+  u64* vcnt = (u64*)(w + Lrun.vcnt);
   u64 n_iter = 0, invalid = 0;
-  int vrc = validate_counts(h, n, &n_iter, &invalid, w + Lrun.global, st,
+  int vrc = validate_counts(h, n, cluster_req ? &n_iter : nullptr, &invalid, vcnt, st,
                             Lrun.bm == 3 ? (u32*)(w + Lrun.bcnt) : nullptr);
   if (vrc) return vrc;
-  if (invalid) return PIP_ERR_INVALID_SWAPS;
-  S.n_iterates = n_iter;
   S.table_capacity = cap;
-  if (n_iter == 0) {
-    if (stats) *stats = S;
-    return PIP_OK;
+  if (cluster_req) {
+    if (invalid) return PIP_ERR_INVALID_SWAPS;
+    S.n_iterates = n_iter;
+    if (n_iter == 0) {
+      if (stats) *stats = S;
+      return PIP_OK;
+    }
   }
   // ... while run_rounds clamps the active prefix to n_iterates (detres.py:267)
-  const u64 P = prefix < n_iter ? prefix : n_iter;
+  const u64 P = cluster_req ? (prefix < n_iter ? prefix : n_iter) : prefix;
   // small n: the whole round loop on one thread-block cluster (rp_cluster.cu)
-  {
+  if (cluster_req) {
     int K = 0;
     const u64 span = prefix + prefix / 4 + 8;
     if (variant == PIP_RP_FINAL && !debug && !trace_dev && !prog && rp_cluster_eligible(n, P, span, &K)) {
@@ -1297,6 +1330,7 @@ int rp_device(u64* a, const u64* h, u64 n, u64 prefix, int variant, int debug,
   if (const char* e = getenv("PIP_RP_TLOAD")) A.tload = (u32)atoi(e) < 2 ? 2u : (u32)atoi(e);
   A.claim2 = Lrun.bm == 3 ? (u32*)(w + Lrun.claim2) : nullptr;
   A.bcnt = Lrun.bm == 3 ? (const u32*)(w + Lrun.bcnt) : nullptr;
+  A.vcnt = cluster_req ? nullptr : vcnt;
 
   PIP_CUDA(cudaMemsetAsync(A.table, 0xff, tcap * 8, st));
   if (variant == PIP_RP_FINAL && !Lrun.bm) PIP_CUDA(cudaMemsetAsync(A.dense, 0, A.span_cap * 4, st));
@@ -1306,8 +1340,6 @@ int rp_device(u64* a, const u64* h, u64 n, u64 prefix, int variant, int debug,
     if (Lrun.bm == 3) PIP_CUDA(cudaMemsetAsync(A.bmF, 0, (1ull << Lrun.logf) / 8, st));
     if (Lrun.bm >= 2) PIP_CUDA(cudaMemsetAsync(w + Lrun.lf, 0, (1ull << RP_LF_LOG2) / 8, st));
   }
-  PIP_CUDA(cudaMemsetAsync(A.failcnt, 0, (size_t)gmax * 4, st));
-  PIP_CUDA(cudaMemsetAsync(A.g, 0, sizeof(RpGlobal), st));
   RpResume R0{};
   R0.cursor = (long long)n - 1;
   R0.first = 1;
@@ -1315,8 +1347,11 @@ int rp_device(u64* a, const u64* h, u64 n, u64 prefix, int variant, int debug,
   R0.dhi = 0;
   R0.rlo = 1;
   R0.rhi = 0;
-  PIP_CUDA(cudaMemcpyAsync(A.resume, &R0, sizeof(R0), cudaMemcpyHostToDevice, st));
-  PIP_CUDA(cudaStreamSynchronize(st));  // R0 lives on this stack frame
+  // resume state, barrier / error words and fail counts set by one kernel
+  // (parameters by value: no host staging, no sync)
+  rp_init_kernel<<<1, 256, 0, st>>>(A.resume, R0, (u32*)A.g, (u32)(sizeof(RpGlobal) / 4), A.failcnt,
+                                    (u32)gmax);
+  PIP_CHECK_LAUNCH();
 
   // grid: enough CTAs to give every thread ~2 iterates, at most co-resident
   int per_sm = 0;
@@ -1342,6 +1377,7 @@ int rp_device(u64* a, const u64* h, u64 n, u64 prefix, int variant, int debug,
   u64 recorded = 0;
   RpResume R{};
   RpGlobal Gh{};
+  std::vector<char> blob(Lrun.vcnt + 16 - Lrun.rcounts);
   for (;;) {
     int rc;
     switch (variant) {
@@ -1365,18 +1401,28 @@ int rp_device(u64* a, const u64* h, u64 n, u64 prefix, int variant, int debug,
       }
       if (q != cudaSuccess) PIP_CUDA(q);
     }
-    PIP_CUDA(cudaMemcpyAsync(&R, A.resume, sizeof(R), cudaMemcpyDeviceToHost, st));
-    PIP_CUDA(cudaMemcpyAsync(&Gh, A.g, sizeof(Gh), cudaMemcpyDeviceToHost, st));
+    // one copy brings back the round counts, the barrier / error words, the
+    // resume state and the validation counts (adjacent in the workspace)
+    PIP_CUDA(cudaMemcpyAsync(blob.data(), w + Lrun.rcounts, blob.size(), cudaMemcpyDeviceToHost, st));
     PIP_CUDA(cudaStreamSynchronize(st));
+    memcpy(&R, blob.data() + (Lrun.resume - Lrun.rcounts), sizeof(R));
+    memcpy(&Gh, blob.data() + (Lrun.global - Lrun.rcounts), sizeof(Gh));
+    if (A.vcnt) {
+      u64 vc[2];
+      memcpy(vc, blob.data() + (Lrun.vcnt - Lrun.rcounts), 16);
+      if (vc[1]) return PIP_ERR_INVALID_SWAPS;  // a[] untouched
+      S.n_iterates = vc[0];
+      if (vc[0] == 0) {
+        if (stats) *stats = S;
+        return PIP_OK;
+      }
+    }
     if (Gh.sync.abort) return PIP_ERR_STALLED;
     // counts are recorded in P1 of the following round: all rounds but the
     // last completed one are available (all of them once done)
     const u64 have = R.done ? R.rounds : (R.rounds ? R.rounds - 1 : 0);
     if (have > recorded && counts_host) {
-      std::vector<u64> chunk(RP_ROUND_CHUNK);
-      PIP_CUDA(cudaMemcpyAsync(chunk.data(), A.round_counts, RP_ROUND_CHUNK * 8,
-                               cudaMemcpyDeviceToHost, st));
-      PIP_CUDA(cudaStreamSynchronize(st));
+      const u64* chunk = (const u64*)blob.data();
       for (u64 r = recorded; r < have; ++r)
         if (r < rounds_cap) counts_host[r] = chunk[r % RP_ROUND_CHUNK];
     }
