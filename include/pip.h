@@ -342,6 +342,58 @@ int pip_random_permutation_u64_host(uint64_t* host_a, const uint64_t* host_h, ui
                                     uint64_t prefix, int variant, pip_rp_stats* stats_host,
                                     int device);
 
+/* ---- multi-GPU: sharded scan and filter on an NCCL communicator ----------- *
+ * SURVEY.md 8(b) "multi-GPU variants taking an ncclComm_t plus shard
+ * descriptors", 8(e).  The reference has no distributed code; these restate
+ * distributed.py's sharded_scan / sharded_filter over the NCCL C API.  One
+ * process per GPU; the global array of n_global words is split evenly, rank r
+ * owning global [r*S, min(n_global, (r+1)*S)), S = ceil(n_global / world).
+ * nccl_comm is an ncclComm_t of `world` ranks in which the caller is `rank`
+ * (void* here: this header needs no nccl.h).  NCCL is resolved at run time
+ * from the process's libnccl.so.2 (or PIP_NCCL_LIB): PIP_ERR_UNSUPPORTED when
+ * none can be loaded, PIP_ERR_CUDA when an NCCL call fails.  workspace:
+ * device memory of pip_sharded_workspace_bytes(world) = 8 (world + 2) bytes.
+ *
+ * pip_scan_u64_sharded: in-place scan of the GLOBAL array (strong.scan's
+ * contract, strong.py:151-166) — local fold, allgather of the shard totals,
+ * device carry, local scan with the carry; stream-ordered, no host
+ * synchronization; total_dev (device, NULL ok) receives the global total.
+ *
+ * pip_filter_u64_sharded: stable filter of the GLOBAL array, in place
+ * (strong.filter_kway's contract, strong.py:283-349): on return the packed
+ * prefix global [0, m) holds the kept words in order, *m_out (HOST) = m and
+ * *local_len_out (HOST, NULL ok) = how many words of that prefix sit in this
+ * rank's shard (local [0, len)).  Local filter, allgather of the kept counts,
+ * then pip_filter_shard_plan's moves: ncclSend of the head that lands in
+ * lower shards, one in-place shift of the rest (pip_move_u64), ncclRecv of
+ * the words of higher ranks into their final slots — destination precedes
+ * source at rank granularity (strong.py:317-327).  Synchronizes (the plan
+ * needs the counts on the host).  No rank holds a copy of its shard.
+ *
+ * pip_filter_shard_plan: the plan alone (host arithmetic, no GPU, no NCCL):
+ * counts = HOST u64[world] kept words per shard; down / up receive at most
+ * world - 1 pieces each.                                                    */
+typedef struct pip_shard_piece {
+  uint32_t peer;          /* rank the piece goes to (down) / comes from (up) */
+  uint32_t reserved;
+  uint64_t local_offset;  /* word offset inside the caller's shard */
+  uint64_t length;        /* words */
+} pip_shard_piece;
+size_t pip_sharded_workspace_bytes(int world);
+int pip_nccl_available(void); /* 1 when the NCCL entry points resolved */
+int pip_scan_u64_sharded(uint64_t* a_local, uint64_t n_local, int op, uint64_t init, int inclusive,
+                         void* nccl_comm, int rank, int world, void* workspace,
+                         size_t workspace_bytes, uint64_t* total_dev, void* scratch,
+                         size_t scratch_bytes, void* stream);
+int pip_filter_shard_plan(const uint64_t* counts, int world, int rank, uint64_t n_global,
+                          pip_shard_piece* down, int* n_down, uint64_t* stay_src,
+                          uint64_t* stay_len, pip_shard_piece* up, int* n_up);
+int pip_filter_u64_sharded(uint64_t* a_local, uint64_t n_local, uint64_t n_global,
+                           const pip_pred* pred, void* nccl_comm, int rank, int world,
+                           void* workspace, size_t workspace_bytes, uint64_t* m_out,
+                           uint64_t* local_len_out, void* scratch, size_t scratch_bytes,
+                           void* stream);
+
 /* ---- input generation (runtime.Rng, runtime.py:263-302) ------------------ *
  * out[k] = mix64(seed + (lo + k + 1) * GOLDEN) >> shift   (Rng.words)
  * swaps: out[k] = Rng.words(lo..)[k] % (lo + k + 1)      (make_swap_sequence) */

@@ -17,7 +17,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libpip.so"
-SOURCES = ["api.cu", "scan.cu", "filter.cu", "misc.cu", "rp.cu", "merge.cu", "partition.cu", "contraction.cu", "detres.cu", "rp_cluster.cu", "tree.cu"]
+SOURCES = ["api.cu", "scan.cu", "filter.cu", "misc.cu", "rp.cu", "merge.cu", "partition.cu", "contraction.cu", "detres.cu", "rp_cluster.cu", "tree.cu", "sharded.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -63,7 +63,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     with ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 1)) as ex:
         objs = list(ex.map(compile_one, SOURCES))
     tmp = LIB.with_suffix(".so.tmp")
-    cmd = [nvcc(), *ARCH, "-shared", "-cudart", "static", "-o", str(tmp), *objs]
+    cmd = [nvcc(), *ARCH, "-shared", "-cudart", "static", "-o", str(tmp), *objs, "-ldl"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr}")

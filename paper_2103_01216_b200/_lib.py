@@ -55,6 +55,10 @@ class PipRpStats(C.Structure):
     ]
 
 
+class PipShardPiece(C.Structure):
+    _fields_ = [("peer", u32), ("reserved", u32), ("local_offset", u64), ("length", u64)]
+
+
 # name -> (restype, argtypes); the full export list of include/pip.h
 SIGNATURES = {
     "pip_version": (i32, []),
@@ -102,6 +106,14 @@ SIGNATURES = {
     "pip_rng_words_u64": (i32, [vp, u64, u64, u64, u32, vp]),
     "pip_make_swaps_u64": (i32, [vp, u64, u64, u64, vp]),
     "pip_bench_random_rmw": (i32, [vp, u64, u64, u64, C.POINTER(C.c_float), vp]),
+    "pip_sharded_workspace_bytes": (sz, [i32]),
+    "pip_nccl_available": (i32, []),
+    "pip_scan_u64_sharded": (i32, [vp, u64, i32, u64, i32, vp, i32, i32, vp, sz, vp, vp, sz, vp]),
+    "pip_filter_shard_plan": (i32, [C.POINTER(u64), i32, i32, u64, C.POINTER(PipShardPiece),
+                                    C.POINTER(i32), C.POINTER(u64), C.POINTER(u64),
+                                    C.POINTER(PipShardPiece), C.POINTER(i32)]),
+    "pip_filter_u64_sharded": (i32, [vp, u64, u64, C.POINTER(PipPred), vp, i32, i32, vp, sz,
+                                     C.POINTER(u64), C.POINTER(u64), vp, sz, vp]),
 }
 
 

@@ -190,14 +190,14 @@ struct Event {
 // its main launch raised, nor a chunk of a host scan one of an earlier chunk.
 // PIP_INJECT_STALL=1 raises it right after the clear (tests of the
 // reporting path; the kernels then bail out of their first long wait).
-static int clear_stall(void* scratch, size_t scratch_bytes, cudaStream_t st) {
+int clear_stall(void* scratch, size_t scratch_bytes, cudaStream_t st) {
   if (!scratch || scratch_bytes < 64) return PIP_OK;  // the op reports OOM itself
   PIP_CUDA(cudaMemsetAsync(scratch, 0, 4, st));
   const char* e = getenv("PIP_INJECT_STALL");
   if (e && e[0] == '1') PIP_CUDA(cudaMemsetAsync(scratch, 1, 1, st));
   return PIP_OK;
 }
-static int read_stall(const void* scratch, cudaStream_t st) {
+int read_stall(const void* scratch, cudaStream_t st) {
   u32 h = 0;
   PIP_CUDA(cudaMemcpyAsync(&h, scratch, 4, cudaMemcpyDeviceToHost, st));
   PIP_CUDA(cudaStreamSynchronize(st));

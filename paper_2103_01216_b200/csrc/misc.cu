@@ -177,20 +177,36 @@ int make_swaps(u64* out, u64 lo, u64 count, u64 seed, cudaStream_t st) {
 // ---------------------------------------------------------------------------
 // random 8-byte read-modify-write microbenchmark (the RP roofline: the swap
 // phase touches 2 random 32-byte sectors per committed swap)
+template <int MODE>
 __global__ void __launch_bounds__(256)
 random_rmw_kernel(u64* __restrict__ buf, u64 n, u64 updates, u64 seed) {
   // 8 independent read-modify-writes in flight per thread; index by
-  // multiply-high range reduction (no 64-bit division on the critical path)
+  // multiply-high range reduction (no 64-bit division on the critical path).
+  // MODE 0: load + store (two requests per update); 1: one atomic exchange
+  // whose old value is consumed (the swap's form); 2: a reduction (no
+  // return value)
   const u64 stride = (u64)gridDim.x * blockDim.x;
+  u64 acc = 0;
   for (u64 k = (u64)blockIdx.x * blockDim.x + threadIdx.x; k * 8 < updates; k += stride) {
     u64 idx[8], v[8];
 #pragma unroll
     for (int q = 0; q < 8; ++q) idx[q] = __umul64hi(mix64(seed + (k * 8 + q) * GOLDEN), n);
+    if (MODE == 0) {
 #pragma unroll
-    for (int q = 0; q < 8; ++q) v[q] = __ldcg(buf + idx[q]);
+      for (int q = 0; q < 8; ++q) v[q] = __ldcg(buf + idx[q]);
 #pragma unroll
-    for (int q = 0; q < 8; ++q) buf[idx[q]] = v[q] + 1;
+      for (int q = 0; q < 8; ++q) buf[idx[q]] = v[q] + 1;
+    } else if (MODE == 1) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) v[q] = atomicExch((unsigned long long*)buf + idx[q], (unsigned long long)(k + q));
+#pragma unroll
+      for (int q = 0; q < 8; ++q) acc += v[q];
+    } else {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) atomicAdd((unsigned long long*)buf + idx[q], 1ull);
+    }
   }
+  if (MODE == 1 && acc == 0x123456789abcdefull) buf[0] = acc;  // keep the exchanges' results live
 }
 
 int bench_random_rmw(u64* buf, u64 n, u64 updates, u64 seed, float* ms, cudaStream_t st) {
@@ -199,9 +215,13 @@ int bench_random_rmw(u64* buf, u64 n, u64 updates, u64 seed, float* ms, cudaStre
   PIP_CUDA(cudaEventCreate(&e0));
   PIP_CUDA(cudaEventCreate(&e1));
   const int blocks = num_sms(current_device()) * 8;
-  random_rmw_kernel<<<blocks, 256, 0, st>>>(buf, n, updates / 8, seed ^ 0x5555);  // warm
+  // PIP_RMW_MODE (measurement knob): 0 load + store (default, the
+  // denominator bench.py reports), 1 atomic exchange, 2 reduction
+  const int mode = getenv("PIP_RMW_MODE") ? atoi(getenv("PIP_RMW_MODE")) : 0;
+  auto kern = mode == 1 ? random_rmw_kernel<1> : mode == 2 ? random_rmw_kernel<2> : random_rmw_kernel<0>;
+  kern<<<blocks, 256, 0, st>>>(buf, n, updates / 8, seed ^ 0x5555);  // warm
   PIP_CUDA(cudaEventRecord(e0, st));
-  random_rmw_kernel<<<blocks, 256, 0, st>>>(buf, n, updates, seed);
+  kern<<<blocks, 256, 0, st>>>(buf, n, updates, seed);
   PIP_CUDA(cudaEventRecord(e1, st));
   PIP_CUDA(cudaEventSynchronize(e1));
   PIP_CUDA(cudaEventElapsedTime(ms, e0, e1));

@@ -273,6 +273,23 @@ __device__ __forceinline__ u64 count_nonself_range(const RpArgs& A, u64 x, u64 y
 }
 
 // ---------------------------------------------------------------------------
+// The swap of a committed iterate.  A round's committed swaps touch disjoint
+// words (each word is reserved by exactly one committing iterate), so the
+// random side may be ONE atomic exchange (one request through the SM's
+// load/store queue and one L2 read-modify-write) instead of a load and a
+// store.  PIP_RP_DBG bit 1 selects the exchange form (measurement knob).
+__device__ __forceinline__ void rp_swap(u64* a, u32 i, u32 t, u32 dbg) {
+  if (dbg & 2u) {
+    const u64 x = __ldcg(a + i);
+    a[i] = (u64)atomicExch((unsigned long long*)a + t, (unsigned long long)x);
+  } else {
+    const u64 x = __ldcg(a + i), y = __ldcg(a + t);
+    a[i] = y;
+    a[t] = x;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // write-max reservation table: one 64-bit word per slot, key<<32 | value
 __device__ __forceinline__ u64 rp_home(u32 key, u32 logcap) {
   return ((u64)key * GOLDEN) >> (64 - logcap);
@@ -326,8 +343,11 @@ __device__ __forceinline__ bool table_lookup(const u64* table, u32 logcap, u32 k
 // iterates (plus the first marker of their targets) use the write-max table,
 // sized per round for them alone so that it stays L2-resident.  Same commit
 // rule, so the same rounds as the reference.
+#ifndef PIP_RP_MINB3
+#define PIP_RP_MINB3 4  // resident CTAs per SM asked of the scheme-3 kernel (measurement knob)
+#endif
 template <int V, int BM>
-__global__ void __launch_bounds__(RP_THREADS, 4) rp_kernel(RpArgs A) {
+__global__ void __launch_bounds__(RP_THREADS, BM == 3 ? PIP_RP_MINB3 : 4) rp_kernel(RpArgs A) {
   __shared__ u32 s_cnt[33];
   __shared__ u64 s_red[36];
   const u32 b = blockIdx.x, G = gridDim.x, tid = threadIdx.x, T = blockDim.x;
@@ -842,9 +862,7 @@ __global__ void __launch_bounds__(RP_THREADS, 4) rp_kernel(RpArgs A) {
           if (c) {
             A.cflag[k] = 1;
             if (!(A.dbg & 1)) {
-              const u64 x = __ldcg(A.a + i), y = __ldcg(A.a + t);
-              A.a[i] = y;
-              A.a[t] = x;
+              rp_swap(A.a, i, t, A.dbg);
             }
           } else {
             A.cflag[k] = (unsigned char)mark_next(t);
@@ -875,9 +893,7 @@ __global__ void __launch_bounds__(RP_THREADS, 4) rp_kernel(RpArgs A) {
         if (c) {
           A.cflag[k] = 1u | 8u;
           if (!(A.dbg & 1)) {  // PIP_RP_DBG=1: measurement only, no swaps
-            const u64 x = __ldcg(A.a + i), y = __ldcg(A.a + t);
-            A.a[i] = y;
-            A.a[t] = x;
+            rp_swap(A.a, i, t, A.dbg);
           }
         } else {
           A.cflag[k] = (unsigned char)(mark_next(t) | (sl == RP_NOSLOT ? 0u : 8u));
@@ -961,9 +977,7 @@ __global__ void __launch_bounds__(RP_THREADS, 4) rp_kernel(RpArgs A) {
         A.cflag[k] = c;
         if (c) {
           if (!(A.dbg & 1)) {  // PIP_RP_DBG=1: measurement only, no swaps
-            const u64 x = __ldcg(A.a + i), y = __ldcg(A.a + t);
-            A.a[i] = y;
-            A.a[t] = x;
+            rp_swap(A.a, i, t, A.dbg);
           }
         } else {
           fails += 1;
@@ -982,9 +996,7 @@ __global__ void __launch_bounds__(RP_THREADS, 4) rp_kernel(RpArgs A) {
           A.cflag[k] = c;
           if (c) {
             if (!(A.dbg & 1)) {
-              const u64 x = __ldcg(A.a + i), y = __ldcg(A.a + t);
-              A.a[i] = y;
-              A.a[t] = x;
+              rp_swap(A.a, i, t, A.dbg);
             }
           } else {
             fails += 1;
@@ -1032,9 +1044,7 @@ __global__ void __launch_bounds__(RP_THREADS, 4) rp_kernel(RpArgs A) {
         A.cflag[k] = c;
         if (c) {
           if (!(A.dbg & 1)) {  // PIP_RP_DBG=1: measurement only, no swaps
-            const u64 x = __ldcg(A.a + i), y = __ldcg(A.a + t);
-            A.a[i] = y;
-            A.a[t] = x;
+            rp_swap(A.a, i, t, A.dbg);
           }
         } else {
           fails += 1;
@@ -1121,7 +1131,7 @@ static u64 pow2_at_least(u64 x) {
   return c;
 }
 
-static int rp_gmax() { return num_sms(current_device()) * 4; }
+static int rp_gmax() { return num_sms(current_device()) * 8; }
 
 static RpLayout rp_layout_mode(u64 n, u64 prefix, int variant, u64 cap, int gmax, int bm) {
   RpLayout L{};
@@ -1364,7 +1374,11 @@ int rp_device(u64* a, const u64* h, u64 n, u64 prefix, int variant, int debug,
                                              : (const void*)rp_kernel<PIP_RP_NAIVE, 0>;
   PIP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kp, RP_THREADS, 0));
   if (per_sm < 1) return PIP_ERR_UNSUPPORTED;
-  if (per_sm > 4) per_sm = 4;
+  {
+    const int cap = getenv("PIP_RP_PERSM") ? atoi(getenv("PIP_RP_PERSM")) : 4;  // measurement knob
+    if (per_sm > cap && cap >= 1 && cap <= 8) per_sm = cap;
+    if (per_sm > 8) per_sm = 8;
+  }
   u64 grid = (u64)per_sm * num_sms(dev);
   // about one iterate per thread for small prefixes (measured: fewer, fuller
   // CTAs are slower — rounds are latency-bound per thread), full grid otherwise
