@@ -407,6 +407,11 @@ int pip_make_swaps_u64(uint64_t* out, uint64_t lo, uint64_t count, uint64_t seed
  * buf[0:n) (one per thread of a full grid); returns device time in ms. */
 int pip_bench_random_rmw(uint64_t* buf, uint64_t n, uint64_t updates, uint64_t seed,
                          float* ms_out, void* stream);
+/* the same with the request form chosen: 0 load + store (two requests per
+ * update), 1 atomic exchange whose old value is consumed (the form the
+ * permutation's swaps take above 2^28 words), 2 reduction (no return). */
+int pip_bench_random_update(uint64_t* buf, uint64_t n, uint64_t updates, uint64_t seed, int form,
+                            float* ms_out, void* stream);
 
 #ifdef __cplusplus
 }

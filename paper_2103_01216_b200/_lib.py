@@ -106,6 +106,7 @@ SIGNATURES = {
     "pip_rng_words_u64": (i32, [vp, u64, u64, u64, u32, vp]),
     "pip_make_swaps_u64": (i32, [vp, u64, u64, u64, vp]),
     "pip_bench_random_rmw": (i32, [vp, u64, u64, u64, C.POINTER(C.c_float), vp]),
+    "pip_bench_random_update": (i32, [vp, u64, u64, u64, i32, C.POINTER(C.c_float), vp]),
     "pip_sharded_workspace_bytes": (sz, [i32]),
     "pip_nccl_available": (i32, []),
     "pip_scan_u64_sharded": (i32, [vp, u64, i32, u64, i32, vp, i32, i32, vp, sz, vp, vp, sz, vp]),

@@ -68,7 +68,7 @@ int validate_device(const u64* h, u64 n, u64* nonself_dev, void* scratch, size_t
                     cudaStream_t st);
 int rng_words(u64* out, u64 lo, u64 count, u64 seed, u32 shift, cudaStream_t st);
 int make_swaps(u64* out, u64 lo, u64 count, u64 seed, cudaStream_t st);
-int bench_random_rmw(u64* buf, u64 n, u64 updates, u64 seed, float* ms, cudaStream_t st);
+int bench_random_rmw(u64* buf, u64 n, u64 updates, u64 seed, float* ms, cudaStream_t st, int mode);
 size_t rp_workspace_bytes(u64 n, u64 prefix, int variant);
 int rp_device(u64* a, const u64* h, u64 n, u64 prefix, int variant, int debug,
               u64* counts_host, u64 rounds_cap, u64* trace_dev, void* ws, size_t ws_bytes,
@@ -937,7 +937,13 @@ int pip_make_swaps_u64(uint64_t* out, uint64_t lo, uint64_t count, uint64_t seed
 
 int pip_bench_random_rmw(uint64_t* buf, uint64_t n, uint64_t updates, uint64_t seed, float* ms_out,
                          void* stream) {
-  return bench_random_rmw((u64*)buf, n, updates, seed, ms_out, (cudaStream_t)stream);
+  return bench_random_rmw((u64*)buf, n, updates, seed, ms_out, (cudaStream_t)stream, -1);
+}
+
+int pip_bench_random_update(uint64_t* buf, uint64_t n, uint64_t updates, uint64_t seed, int form,
+                            float* ms_out, void* stream) {
+  if (form < 0 || form > 2) return PIP_ERR_INVALID_ARG;
+  return bench_random_rmw((u64*)buf, n, updates, seed, ms_out, (cudaStream_t)stream, form);
 }
 
 }  // extern "C"

@@ -209,15 +209,15 @@ random_rmw_kernel(u64* __restrict__ buf, u64 n, u64 updates, u64 seed) {
   if (MODE == 1 && acc == 0x123456789abcdefull) buf[0] = acc;  // keep the exchanges' results live
 }
 
-int bench_random_rmw(u64* buf, u64 n, u64 updates, u64 seed, float* ms, cudaStream_t st) {
-  if (!n) return PIP_ERR_INVALID_ARG;
+int bench_random_rmw(u64* buf, u64 n, u64 updates, u64 seed, float* ms, cudaStream_t st, int mode) {
+  if (!n || mode > 2) return PIP_ERR_INVALID_ARG;
   cudaEvent_t e0, e1;
   PIP_CUDA(cudaEventCreate(&e0));
   PIP_CUDA(cudaEventCreate(&e1));
   const int blocks = num_sms(current_device()) * 8;
-  // PIP_RMW_MODE (measurement knob): 0 load + store (default, the
-  // denominator bench.py reports), 1 atomic exchange, 2 reduction
-  const int mode = getenv("PIP_RMW_MODE") ? atoi(getenv("PIP_RMW_MODE")) : 0;
+  // mode: 0 load + store, 1 atomic exchange (the form the scheme-3 swaps
+  // use), 2 reduction; < 0: PIP_RMW_MODE (measurement knob), default 0
+  if (mode < 0) mode = getenv("PIP_RMW_MODE") ? atoi(getenv("PIP_RMW_MODE")) : 0;
   auto kern = mode == 1 ? random_rmw_kernel<1> : mode == 2 ? random_rmw_kernel<2> : random_rmw_kernel<0>;
   kern<<<blocks, 256, 0, st>>>(buf, n, updates / 8, seed ^ 0x5555);  // warm
   PIP_CUDA(cudaEventRecord(e0, st));

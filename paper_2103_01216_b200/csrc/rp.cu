@@ -277,9 +277,13 @@ __device__ __forceinline__ u64 count_nonself_range(const RpArgs& A, u64 x, u64 y
 // words (each word is reserved by exactly one committing iterate), so the
 // random side may be ONE atomic exchange (one request through the SM's
 // load/store queue and one L2 read-modify-write) instead of a load and a
-// store.  PIP_RP_DBG bit 1 selects the exchange form (measurement knob).
+// store: 20.1 against 14.9 G random updates/s over 8 GiB (tools/rmw_modes.py).
+// Scheme 3 (n > 2^28, DRAM-bound swaps) exchanges; the small-n schemes keep
+// the load + store form, whose two loads travel together (C0: 1.51 against
+// 1.56 ms).  PIP_RP_DBG bit 1 flips the choice (measurement knob).
+template <int BM>
 __device__ __forceinline__ void rp_swap(u64* a, u32 i, u32 t, u32 dbg) {
-  if (dbg & 2u) {
+  if ((BM == 3) != ((dbg & 2u) != 0)) {
     const u64 x = __ldcg(a + i);
     a[i] = (u64)atomicExch((unsigned long long*)a + t, (unsigned long long)x);
   } else {
@@ -343,16 +347,47 @@ __device__ __forceinline__ bool table_lookup(const u64* table, u32 logcap, u32 k
 // iterates (plus the first marker of their targets) use the write-max table,
 // sized per round for them alone so that it stays L2-resident.  Same commit
 // rule, so the same rounds as the reference.
-#ifndef PIP_RP_MINB3
-#define PIP_RP_MINB3 4  // resident CTAs per SM asked of the scheme-3 kernel (measurement knob)
+#ifndef PIP_RP_SMALL1
+#define PIP_RP_SMALL1 0
 #endif
-template <int V, int BM>
-__global__ void __launch_bounds__(RP_THREADS, BM == 3 ? PIP_RP_MINB3 : 4) rp_kernel(RpArgs A) {
+#ifndef PIP_RP_PF3
+#define PIP_RP_PF3 0  // scheme 3: retire / refill loops load their next batch early (at 6 CTAs per SM it no longer pays: 118.9 vs 118.5 ms)
+#endif
+#ifndef PIP_RP_XPRE
+#define PIP_RP_XPRE 1
+#endif
+#ifndef PIP_RP_MINB3
+#define PIP_RP_MINB3 6  // resident CTAs per SM of the scheme-3 kernel (40 registers; 4: 64, 8: 32)
+#endif
+// MB: resident CTAs per SM the kernel is compiled for.  MB = 1 (scheme 1
+// only) is the flavour for grids of at most one CTA per SM (C0: 79 CTAs):
+// no register cap, so nothing spills into the rounds' latency chains.
+template <int V, int BM, int MB = (BM == 3 ? PIP_RP_MINB3 : 4)>
+__global__ void __launch_bounds__(RP_THREADS, MB) rp_kernel(RpArgs A) {
   __shared__ u32 s_cnt[33];
   __shared__ u64 s_red[36];
   const u32 b = blockIdx.x, G = gridDim.x, tid = threadIdx.x, T = blockDim.x;
   RpGlobal* g = A.g;
-  RpResume R = *A.resume;
+  // The round state (identical in every thread) is touched only between
+  // phases.  Scheme 3 keeps it in shared memory, written by thread 0 between
+  // two CTA barriers (RSET), so the phase loops have ~30 more registers and
+  // the kernel fits 6 CTAs per SM; the small-n schemes keep it in registers
+  // (their rounds are latency-bound: the extra barriers would show).
+  __shared__ RpResume s_R;
+  RpResume R_reg;
+  RpResume& R = (BM == 3) ? s_R : R_reg;
+  if (BM == 3) {
+    if (tid == 0) s_R = *A.resume;
+    __syncthreads();
+  } else {
+    R_reg = *A.resume;
+  }
+#define RSET(...)                              \
+  do {                                         \
+    if (BM == 3) __syncthreads();              \
+    if (BM != 3 || tid == 0) { __VA_ARGS__; }  \
+    if (BM == 3) __syncthreads();              \
+  } while (0)
   u64 P = A.prefix;  // run_rounds clamps the active prefix to n_iterates (detres.py:267)
   if (A.vcnt) {
     const u64 ns = __ldcg(A.vcnt), bad = __ldcg(A.vcnt + 1);
@@ -369,13 +404,17 @@ __global__ void __launch_bounds__(RP_THREADS, BM == 3 ? PIP_RP_MINB3 : 4) rp_ker
   u64 rounds_here = 0;
   const bool trace = A.trace != nullptr;
   const bool tm = b == 0 && tid == 0;
-  u64 tacc[4] = {0, 0, 0, 0};
-  u64 tlast = tm ? globaltimer_ns() : 0;
+  // phase timers of CTA 0 (PIP_TIMING): shared memory, so they take no registers
+  __shared__ u64 s_tacc[5];
+  if (tm) {
+    s_tacc[0] = s_tacc[1] = s_tacc[2] = s_tacc[3] = 0;
+    s_tacc[4] = globaltimer_ns();
+  }
   auto tick = [&](int ph) {
     if (tm) {
       const u64 now = globaltimer_ns();
-      tacc[ph] += now - tlast;
-      tlast = now;
+      s_tacc[ph] += now - s_tacc[4];
+      s_tacc[4] = now;
     }
   };
 
@@ -404,7 +443,7 @@ __global__ void __launch_bounds__(RP_THREADS, BM == 3 ? PIP_RP_MINB3 : 4) rp_ker
         // the previous round's distinct out-of-window targets ride along
         u64 claims_total;
         sum_counts2(A.failcnt, A.claimcnt, G, b, s_red, nfail, fbefore, claims_total);
-        if (claims_total > R.peak) R.peak = claims_total;
+        RSET(if (claims_total > R.peak) R.peak = claims_total);
       } else {
         sum_counts(A.failcnt, G, b, s_red, nfail, fbefore);
       }
@@ -414,22 +453,18 @@ __global__ void __launch_bounds__(RP_THREADS, BM == 3 ? PIP_RP_MINB3 : 4) rp_ker
         const u64 r = R.rounds - 1;
         A.round_counts[r % RP_ROUND_CHUNK] = ncommit;
       }
-      R.total_committed += ncommit;
-      if (ncommit == 0) {
-        R.zero_rounds += 1;
-        if (R.zero_rounds >= 64) {
-          if (b == 0 && tid == 0) atomicExch(&g->sync.error, (u32)PIP_ERR_LIVELOCK);
-          R.done = 1;
-          break;
-        }
-      } else {
-        R.zero_rounds = 0;
+      RSET(R.total_committed += ncommit; R.zero_rounds = ncommit == 0 ? R.zero_rounds + 1 : 0);
+      if (R.zero_rounds >= 64) {
+        if (b == 0 && tid == 0) atomicExch(&g->sync.error, (u32)PIP_ERR_LIVELOCK);
+        RSET(R.done = 1);
+        break;
       }
       u64 s, e;
       part(F, G, b, s, e);
       const u64 cbefore = s - fbefore;  // committed items in CTAs < b
       const bool targeted = A.targeted_clean_ok && F * 8 < (1ull << A.logcap);
       u64 runf = 0, runc = 0;
+      const u64 trace_pos0 = R.trace_pos;
       // RB consecutive items per thread: failures keep their order; the
       // next batch's loads are in flight while this batch is packed
       u32 cn[RB], inx[RB], tnx[RB];
@@ -447,7 +482,7 @@ __global__ void __launch_bounds__(RP_THREADS, BM == 3 ? PIP_RP_MINB3 : 4) rp_ker
       for (u64 c0 = s; c0 < e; c0 += (u64)RB * T) {
         const u64 kb = c0 + (u64)RB * tid;
         u32 fm = 0, cm = 0, iv[RB], tv[RB];
-        if (BM != 3 && c0 != s) {
+        if (!(BM == 3 && PIP_RP_PF3) && c0 != s) {
 #pragma unroll
           for (int q = 0; q < RB; ++q) {
             const u64 k = kb + q;
@@ -475,7 +510,7 @@ __global__ void __launch_bounds__(RP_THREADS, BM == 3 ? PIP_RP_MINB3 : 4) rp_ker
         for (int q = 0; q < RB; ++q) cf1[q] = cn[q];
         // (scheme 3 only: the large rounds of C4 gain 0.8 ms; at C0's size the
         // extra live registers spill and cost more than they hide)
-        if (BM == 3) {
+        if (BM == 3 && PIP_RP_PF3) {
 #pragma unroll
           for (int q = 0; q < RB; ++q) {
             const u64 k = kb + (u64)RB * T + q;
@@ -498,7 +533,7 @@ __global__ void __launch_bounds__(RP_THREADS, BM == 3 ? PIP_RP_MINB3 : 4) rp_ker
         runf += tot;
         if (trace) {
           u32 totc;
-          u64 cp = R.trace_pos + cbefore + runc + block_excl_sum(__popc(cm), s_cnt, &totc);
+          u64 cp = trace_pos0 + cbefore + runc + block_excl_sum(__popc(cm), s_cnt, &totc);
 #pragma unroll
           for (int q = 0; q < RB; ++q)
             if ((cm >> q) & 1u) A.trace[cp++] = iv[q];
@@ -521,16 +556,17 @@ __global__ void __launch_bounds__(RP_THREADS, BM == 3 ? PIP_RP_MINB3 : 4) rp_ker
           }
         }
       }
-      R.trace_pos += ncommit;
+      RSET(R.trace_pos += ncommit);
       if (BM == 3) {
         // the folded bitmap wholesale (L2-resident); B only over the band of
         // ids the last round marked
         u64 ts, te;
         part(1ull << (A.logf - 5), G, b, ts, te);
         for (u64 x = ts + tid; x < te; x += T) A.bmF[x] = 0u;
-        if (R.rhi >= R.rlo) {
-          part((R.rhi >> 5) - (R.rlo >> 5) + 1, G, b, ts, te);
-          for (u64 x = ts + tid; x < te; x += T) A.bmB[(R.rlo >> 5) + x] = 0u;
+        const u64 rlo = R.rlo, rhi = R.rhi;
+        if (rhi >= rlo) {
+          part((rhi >> 5) - (rlo >> 5) + 1, G, b, ts, te);
+          for (u64 x = ts + tid; x < te; x += T) A.bmB[(rlo >> 5) + x] = 0u;
         }
       }
       if (BM && BM != 3 && F * 256 >= A.n) {  // dense round: clear the bitmaps wholesale
@@ -548,7 +584,7 @@ __global__ void __launch_bounds__(RP_THREADS, BM == 3 ? PIP_RP_MINB3 : 4) rp_ker
       }
       if ((BM == 2 || BM == 3) && R.logcap_c) {  // the collided table used only its first 2^logcap_c slots
         u64 ts, te;
-        part(1ull << R.logcap_c, G, b, ts, te);
+        part(1ull << (u32)R.logcap_c, G, b, ts, te);
         for (u64 x = ts + tid; x < te; x += T) A.table[x] = RP_EMPTY;
       }
       if (!targeted && !BM) {
@@ -559,7 +595,8 @@ __global__ void __launch_bounds__(RP_THREADS, BM == 3 ? PIP_RP_MINB3 : 4) rp_ker
       }
       if (V == PIP_RP_FINAL && !BM && R.dhi >= R.dlo) {
         u64 ds, de;
-        part(R.dhi - R.dlo + 1, G, b, ds, de);
+        const u64 odlo = R.dlo, odhi = R.dhi;
+        part(odhi - odlo + 1, G, b, ds, de);
         for (u64 x = ds + tid; x < de; x += T) A.dense[x] = 0;
       }
     }
@@ -636,6 +673,55 @@ __global__ void __launch_bounds__(RP_THREADS, BM == 3 ? PIP_RP_MINB3 : 4) rp_ker
       u64 s, e;
       part(wd, G, b, s, e);
       u64 run = wbefore;
+      if (BM == 3 && A.bcnt && !(A.dbg & 4u)) {
+        // The window holds span_cap ids but only its first `fresh` non-self
+        // ids are taken (about a third of it), so with the window split
+        // evenly two thirds of the CTAs would have nothing to rank.  Split
+        // the NEEDED stretch instead: the old parts 0..bl hold the first
+        // `fresh` non-self ids (their counts are in wcnt); its whole
+        // 4096-id blocks are dealt evenly to all CTAs, and a CTA's first
+        // rank is the non-self count of the ids above its blocks (block
+        // counts of the validation pass + the window's ragged top from H).
+        const u32 per = (G + T - 1) / T;
+        const u32 q0 = tid * per, q1 = q0 + per < G ? q0 + per : G;
+        u32 mysum = 0;
+        for (u32 q = q0; q < q1; ++q) mysum += __ldcg(A.wcnt + q);
+        u32 tot0;
+        const u64 pre = block_excl_sum(mysum, s_cnt, &tot0);
+        if (tid == 0) s_red[32] = G - 1;
+        __syncthreads();
+        if (pre < fresh && pre + mysum >= fresh) {
+          u64 c = pre;
+          for (u32 q = q0; q < q1; ++q) {
+            c += __ldcg(A.wcnt + q);
+            if (c >= fresh) {
+              s_red[32] = q;
+              break;
+            }
+          }
+        }
+        __syncthreads();
+        const u32 bl = (u32)s_red[32];
+        __syncthreads();
+        u64 ps, pe;
+        part(wd, G, bl, ps, pe);  // positions [0, pe) cover the needed ids
+        const u64 low_id = hi - (pe - 1);
+        const u64 bhi = hi >> RP_BLK_SHIFT, blo = low_id >> RP_BLK_SHIFT;
+        u64 bs, be;
+        part(bhi - blo + 1, G, b, bs, be);  // my blocks, counted from the top
+        if (be > bs) {
+          u64 top = ((bhi - bs) << RP_BLK_SHIFT) + ((1ull << RP_BLK_SHIFT) - 1);
+          if (top > hi) top = hi;
+          u64 bot = (bhi - (be - 1)) << RP_BLK_SHIFT;
+          if (bot < low_id) bot = low_id;
+          s = hi - top;
+          e = hi - bot + 1;
+          run = block_sum(count_nonself_range(A, top + 1, hi), s_red);
+        } else {
+          s = e = 0;
+          run = fresh;
+        }
+      }
       // the next batch's H words are in flight while this batch is ranked
       u64 hn[RB];
 #pragma unroll
@@ -647,7 +733,7 @@ __global__ void __launch_bounds__(RP_THREADS, BM == 3 ? PIP_RP_MINB3 : 4) rp_ker
         const u64 qb = c0 + (u64)RB * tid;
         u64 hv[RB];
         u32 fm = 0;
-        if (BM != 3 && c0 != s) {  // (prefetch for scheme 3 only, as in the retire loop)
+        if (!(BM == 3 && PIP_RP_PF3) && c0 != s) {  // (prefetch for scheme 3 only, as in the retire loop)
 #pragma unroll
           for (int q = 0; q < RB; ++q) hn[q] = qb + q < e ? __ldcs(A.h + (hi - (qb + q))) : 0;
         }
@@ -656,7 +742,7 @@ __global__ void __launch_bounds__(RP_THREADS, BM == 3 ? PIP_RP_MINB3 : 4) rp_ker
           hv[q] = hn[q];
           if (qb + q < e && hv[q] != hi - (qb + q)) fm |= 1u << q;
         }
-        if (BM == 3) {
+        if (BM == 3 && PIP_RP_PF3) {
           const u64 qn = qb + (u64)RB * T;
 #pragma unroll
           for (int q = 0; q < RB; ++q) hn[q] = qn + q < e ? __ldcs(A.h + (hi - (qn + q))) : 0;
@@ -704,8 +790,7 @@ __global__ void __launch_bounds__(RP_THREADS, BM == 3 ? PIP_RP_MINB3 : 4) rp_ker
     }
     const u64 newF = nfail + fresh;
     if (newF == 0) {
-      R.done = 1;
-      R.cursor = cursor;
+      RSET(R.done = 1; R.cursor = cursor);
       break;
     }
     if (!grid_barrier(&g->sync, gen)) break;
@@ -862,7 +947,7 @@ __global__ void __launch_bounds__(RP_THREADS, BM == 3 ? PIP_RP_MINB3 : 4) rp_ker
           if (c) {
             A.cflag[k] = 1;
             if (!(A.dbg & 1)) {
-              rp_swap(A.a, i, t, A.dbg);
+              rp_swap<BM>(A.a, i, t, A.dbg);
             }
           } else {
             A.cflag[k] = (unsigned char)mark_next(t);
@@ -893,7 +978,7 @@ __global__ void __launch_bounds__(RP_THREADS, BM == 3 ? PIP_RP_MINB3 : 4) rp_ker
         if (c) {
           A.cflag[k] = 1u | 8u;
           if (!(A.dbg & 1)) {  // PIP_RP_DBG=1: measurement only, no swaps
-            rp_swap(A.a, i, t, A.dbg);
+            rp_swap<BM>(A.a, i, t, A.dbg);
           }
         } else {
           A.cflag[k] = (unsigned char)(mark_next(t) | (sl == RP_NOSLOT ? 0u : 8u));
@@ -913,7 +998,7 @@ __global__ void __launch_bounds__(RP_THREADS, BM == 3 ? PIP_RP_MINB3 : 4) rp_ker
       u64 claims_total, dummy, lc_total, lc_before;
       if (BM == 2) {  // BM 3 counts distinct targets at the end of the round
         sum_counts(A.claimcnt, G, b, s_red, claims_total, dummy);
-        if (claims_total > R.peak) R.peak = claims_total;
+        RSET(if (claims_total > R.peak) R.peak = claims_total);
       }
       sum_counts(A.lccnt, G, b, s_red, lc_total, lc_before);
       u32 lg = 0;
@@ -925,7 +1010,7 @@ __global__ void __launch_bounds__(RP_THREADS, BM == 3 ? PIP_RP_MINB3 : 4) rp_ker
         if (lg > A.logcap) lg = A.logcap;
       }
       int c2 = 0;  // BM 3: listed claims of new targets - first markers that joined
-      R.logcap_c = lg;
+      RSET(R.logcap_c = lg);
       u64 s, e;
       part(newF, G, b, s, e);
       u32 dclaim = 0;
@@ -966,6 +1051,12 @@ __global__ void __launch_bounds__(RP_THREADS, BM == 3 ? PIP_RP_MINB3 : 4) rp_ker
         const bool maybe = lc_total && (!A.lf || ((__ldcg(A.lf + ((t & ((1u << RP_LF_LOG2) - 1u)) >> 5)) >> (t & 31)) & 1u));
         const u64 w0 = maybe ? __ldcg(A.table + rp_home(t, lg)) : RP_EMPTY;
         const u32 bw = __ldcg(A.bmB + (i >> 5));
+#if PIP_RP_XPRE
+        // a[i] travels with the decision loads (ids are dense and descending,
+        // so these reads are near-coalesced): a committing iterate's exchange
+        // can leave as soon as the decision is made
+        const u64 xpre = (BM == 3) ? __ldcg(A.a + i) : 0ull;
+#endif
         u32 v;
         if (w0 != RP_EMPTY && ((u32)(w0 >> 32) == t || table_lookup(A.table, lg, t, v))) {
           table_reserve(A.table, lg, t, i, dclaim, &g->sync.error);
@@ -977,7 +1068,14 @@ __global__ void __launch_bounds__(RP_THREADS, BM == 3 ? PIP_RP_MINB3 : 4) rp_ker
         A.cflag[k] = c;
         if (c) {
           if (!(A.dbg & 1)) {  // PIP_RP_DBG=1: measurement only, no swaps
-            rp_swap(A.a, i, t, A.dbg);
+#if PIP_RP_XPRE
+            if (BM == 3 && !(A.dbg & 2u))
+              A.a[i] = (u64)atomicExch((unsigned long long*)A.a + t, (unsigned long long)xpre);
+            else
+              rp_swap<BM>(A.a, i, t, A.dbg);
+#else
+            rp_swap<BM>(A.a, i, t, A.dbg);
+#endif
           }
         } else {
           fails += 1;
@@ -996,7 +1094,7 @@ __global__ void __launch_bounds__(RP_THREADS, BM == 3 ? PIP_RP_MINB3 : 4) rp_ker
           A.cflag[k] = c;
           if (c) {
             if (!(A.dbg & 1)) {
-              rp_swap(A.a, i, t, A.dbg);
+              rp_swap<BM>(A.a, i, t, A.dbg);
             }
           } else {
             fails += 1;
@@ -1017,7 +1115,7 @@ __global__ void __launch_bounds__(RP_THREADS, BM == 3 ? PIP_RP_MINB3 : 4) rp_ker
     {
       u64 claims_total, dummy;
       sum_counts(A.claimcnt, G, b, s_red, claims_total, dummy);
-      if (claims_total > R.peak) R.peak = claims_total;
+      RSET(if (claims_total > R.peak) R.peak = claims_total);
       u64 s, e;
       part(newF, G, b, s, e);
       u32 fails = 0;
@@ -1044,7 +1142,7 @@ __global__ void __launch_bounds__(RP_THREADS, BM == 3 ? PIP_RP_MINB3 : 4) rp_ker
         A.cflag[k] = c;
         if (c) {
           if (!(A.dbg & 1)) {  // PIP_RP_DBG=1: measurement only, no swaps
-            rp_swap(A.a, i, t, A.dbg);
+            rp_swap<BM>(A.a, i, t, A.dbg);
           }
         } else {
           fails += 1;
@@ -1054,17 +1152,8 @@ __global__ void __launch_bounds__(RP_THREADS, BM == 3 ? PIP_RP_MINB3 : 4) rp_ker
       if (tid == 0) A.failcnt[b] = (u32)f;
     }
     }
-    R.fill = newF;
-    R.nfail_prev = nfail;
-    R.ping = nw;
-    R.rounds += 1;
-    R.first = 0;
-    R.dlo = dlo;
-    R.dhi = dhi;
-    R.cursor = cursor;
-    R.wpre = 0;
-    R.rlo = band_lo;
-    R.rhi = band_hi;
+    RSET(R.fill = newF; R.nfail_prev = nfail; R.ping = nw; R.rounds += 1; R.first = 0; R.dlo = dlo;
+         R.dhi = dhi; R.cursor = cursor; R.wpre = 0; R.rlo = band_lo; R.rhi = band_hi);
     bool wcounted = false;
     if (BM == 1) {  // P3b counted the next window when it fit its loads
       const u64 whi = cursor >= 0 ? (u64)cursor : 0;
@@ -1072,7 +1161,7 @@ __global__ void __launch_bounds__(RP_THREADS, BM == 3 ? PIP_RP_MINB3 : 4) rp_ker
       u64 ws, we;
       part(whi - wlo + 1, G, b, ws, we);
       wcounted = cursor >= 0 && we - ws <= (u64)4 * T;
-      if (wcounted) R.wpre = 1;
+      if (wcounted) RSET(R.wpre = 1);
     }
     if (V == PIP_RP_FINAL && cursor >= 0 && !wcounted) {  // count the next round's window now
       hi = (u64)cursor;
@@ -1083,7 +1172,7 @@ __global__ void __launch_bounds__(RP_THREADS, BM == 3 ? PIP_RP_MINB3 : 4) rp_ker
       u64 c = we > ws ? count_nonself_range(A, hi - (we - 1), hi - ws) : 0;
       c = block_sum(c, s_red);
       if (tid == 0) A.wcnt[b] = (u32)c;
-      R.wpre = 1;
+      RSET(R.wpre = 1);
     }
     if (!grid_barrier(&g->sync, gen)) break;
     tick(3);
@@ -1094,7 +1183,7 @@ __global__ void __launch_bounds__(RP_THREADS, BM == 3 ? PIP_RP_MINB3 : 4) rp_ker
       u64 fm, dummy;
       sum_counts(A.claimcnt, G, b, s_red, fm, dummy);
       const long long d = (long long)fm + sum_counts_signed(A.claim2, G, s_red);
-      if (d > 0 && (u64)d > R.peak) R.peak = (u64)d;
+      RSET(if (d > 0 && (u64)d > R.peak) R.peak = (u64)d);
     }
     if (A.progress && b == 0 && tid == 0) {
       // this round's list is descending (failures first, then the fresh
@@ -1108,7 +1197,7 @@ __global__ void __launch_bounds__(RP_THREADS, BM == 3 ? PIP_RP_MINB3 : 4) rp_ker
   }
   if (b == 0 && tid == 0) {
     *A.resume = R;
-    for (int i = 0; i < 4; ++i) g->t[i] += tacc[i];
+    for (int i = 0; i < 4; ++i) g->t[i] += s_tacc[i];
   }
 }
 
@@ -1233,6 +1322,7 @@ __global__ void rp_init_kernel(RpResume* r, RpResume r0, u32* g, u32 gwords, u32
 template <int V, int BM = 0>
 static int rp_run(RpArgs& A, int grid, cudaStream_t st) {
   auto k = rp_kernel<V, BM>;
+  if (BM == 1 && PIP_RP_SMALL1 && grid <= num_sms(current_device())) k = rp_kernel<V, BM == 1 ? BM : 0, BM == 1 ? 1 : 4>;
   void* args[] = {&A};
   PIP_CUDA(cudaLaunchCooperativeKernel((const void*)k, dim3(grid), dim3(RP_THREADS), args, 0, st));
   return PIP_OK;
@@ -1375,7 +1465,11 @@ int rp_device(u64* a, const u64* h, u64 n, u64 prefix, int variant, int debug,
   PIP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kp, RP_THREADS, 0));
   if (per_sm < 1) return PIP_ERR_UNSUPPORTED;
   {
-    const int cap = getenv("PIP_RP_PERSM") ? atoi(getenv("PIP_RP_PERSM")) : 4;  // measurement knob
+    // scheme 3 is compiled for PIP_RP_MINB3 CTAs per SM: its commit pass is
+    // latency-bound and gains from every resident warp (C4: 130.6 ms at 4,
+    // 121.2 at 5, 118.4 at 6, 120.5 at 8, where the other phases spill)
+    const int cap = getenv("PIP_RP_PERSM") ? atoi(getenv("PIP_RP_PERSM"))
+                                           : (Lrun.bm == 3 ? PIP_RP_MINB3 : 4);
     if (per_sm > cap && cap >= 1 && cap <= 8) per_sm = cap;
     if (per_sm > 8) per_sm = 8;
   }

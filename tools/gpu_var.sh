@@ -7,7 +7,7 @@ cp paper_2103_01216_b200/libpip.so /tmp/libpip_base.so
 for rep in 1 2; do
 for t in base $tags; do
   if [ $t = base ]; then cp /tmp/libpip_base.so paper_2103_01216_b200/libpip.so; else cp build/var/libpip_$t.so paper_2103_01216_b200/libpip.so; fi
-  persm=4; case $t in m[0-9]) persm=${t#m};; esac
+  persm=; case $t in m[0-9]*) persm=${t:1:1};; esac
   PIP_RP_PERSM=$persm PIP_TIMING=1 timeout 600 python bench.py "$@" >> $o/$t.json 2>> $o/$t.err
 done
 done
