@@ -347,8 +347,11 @@ __device__ __forceinline__ bool table_lookup(const u64* table, u32 logcap, u32 k
 // iterates (plus the first marker of their targets) use the write-max table,
 // sized per round for them alone so that it stays L2-resident.  Same commit
 // rule, so the same rounds as the reference.
+#ifndef PIP_RP_SPEC1
+#define PIP_RP_SPEC1 1
+#endif
 #ifndef PIP_RP_SMALL1
-#define PIP_RP_SMALL1 0
+#define PIP_RP_SMALL1 1
 #endif
 #ifndef PIP_RP_PF3
 #define PIP_RP_PF3 0  // scheme 3: retire / refill loops load their next batch early (at 6 CTAs per SM it no longer pays: 118.9 vs 118.5 ms)
@@ -939,6 +942,14 @@ __global__ void __launch_bounds__(RP_THREADS, MB) rp_kernel(RpArgs A) {
         const u32 t = tw & RP_TMASK;
         if ((tw >> 31) && (t < dlo || t > dhi)) claims1 += 1;
         const u32 cw = __ldcg(Cc + (t >> 5)), bw = __ldcg(Bc + (i >> 5));
+        // small grids (MB == 1, L2-resident a[]): both words of the swap
+        // travel with the bitmap words, one L2 round trip less per round
+        // (a committing iterate's words are touched by nobody else this round)
+        u64 xs = 0, ys = 0;
+        if (MB == 1 && PIP_RP_SPEC1) {
+          xs = __ldcg(A.a + i);
+          ys = __ldcg(A.a + t);
+        }
         if ((cw >> (t & 31)) & 1u) {
           A.slot[k] = table_reserve(A.table, A.logcap, t, i, dclaim, &g->sync.error);
           A.cflag[k] = 2;
@@ -947,7 +958,12 @@ __global__ void __launch_bounds__(RP_THREADS, MB) rp_kernel(RpArgs A) {
           if (c) {
             A.cflag[k] = 1;
             if (!(A.dbg & 1)) {
-              rp_swap<BM>(A.a, i, t, A.dbg);
+              if (MB == 1 && PIP_RP_SPEC1) {
+                A.a[i] = ys;
+                A.a[t] = xs;
+              } else {
+                rp_swap<BM>(A.a, i, t, A.dbg);
+              }
             }
           } else {
             A.cflag[k] = (unsigned char)mark_next(t);
