@@ -62,5 +62,11 @@ elif args.op == "rmw":
     for _ in range(args.reps):
         assert lib.pip_bench_random_rmw(a.data_ptr(), n, n, 7, C.byref(ms), st) == 0
     print("rmw", n, "updates in", ms.value, "ms ->", n / (ms.value / 1e3) / 1e9, "G RMW/s")
+elif args.op == "rmwx":
+    # the same updates as one atomic exchange each (the form the swaps take above 2^28 words)
+    ms = C.c_float(0)
+    for _ in range(args.reps):
+        assert lib.pip_bench_random_update(a.data_ptr(), n, n, 7, 1, C.byref(ms), st) == 0
+    print("rmwx", n, "updates in", ms.value, "ms ->", n / (ms.value / 1e3) / 1e9, "G exchanges/s")
 torch.cuda.synchronize()
 print("ok", args.op, n)

@@ -31,6 +31,7 @@ full scan 28 scan_ws2
 full filter 28 filter_ws2
 full merge 28 merge_kernel
 full rmw 30 random_rmw
+full rmwx 30 random_rmw
 cmd="python tools/profile_op.py --op rp --log2n 30 --reps 1"
 $cmd > $out/profile_op_rp.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_sector_hit_rate.pct \
