@@ -347,9 +347,6 @@ __device__ __forceinline__ bool table_lookup(const u64* table, u32 logcap, u32 k
 // iterates (plus the first marker of their targets) use the write-max table,
 // sized per round for them alone so that it stays L2-resident.  Same commit
 // rule, so the same rounds as the reference.
-#ifndef PIP_RP_NI
-#define PIP_RP_NI 1  // scheme 3: items per thread per step of the commit loop
-#endif
 #ifndef PIP_RP_SPEC1
 #define PIP_RP_SPEC1 1
 #endif
@@ -1047,77 +1044,15 @@ __global__ void __launch_bounds__(RP_THREADS, MB) rp_kernel(RpArgs A) {
       }
       u32 fails = 0;
       // One item per thread per step (4 CTAs/SM of 64 registers beat 2 CTAs/SM
-      // with 4-item batches: 110 vs 175 ms at 2^30), but the step's loads are
+      // with 4-item batches: 110 vs 175 ms at 2^30; with the round state out
+      // of the registers, 2 / 4 items per step with every wave of loads
+      // issued for all items first: 142 / 179 ms at 4 CTAs per SM against
+      // 128, 132 at 6 against 117 -- resident warps, not loads per thread,
+      // are what this pass wants), but the step's loads are
       // issued in two waves instead of a chain: {cflag, target, id} of the
       // next item travel while this one finishes (software pipeline), and the
       // table probe and the own-check word go out together.
-      if (BM == 3 && PIP_RP_NI > 1 && !(A.dbg & 2u)) {
-        // scheme 3: NI items per thread per step, each wave of loads issued
-        // for all of them before any is used ({cflag, target, id}, then
-        // {filter word, own word, a[i]}, then the rare table probes, then
-        // the exchanges, then the stores of the exchanged words)
-        constexpr int NI = PIP_RP_NI > 1 ? PIP_RP_NI : 1;
-        const bool uself = lc_total != 0;
-        for (u64 k0 = s + tid; k0 < e; k0 += (u64)NI * T) {
-          u32 cf[NI], t[NI], i[NI], lfw[NI], bw[NI];
-          u64 x[NI], w0[NI], y[NI];
-          bool sw[NI];
-#pragma unroll
-          for (int q = 0; q < NI; ++q) {
-            const u64 k = k0 + (u64)q * T;
-            cf[q] = 1;
-            t[q] = i[q] = 0;
-            if (k < e) {
-              cf[q] = __ldcs(A.cflag + k);
-              t[q] = __ldcs(tg_n + k);
-              i[q] = __ldcs(ids_n + k);
-            }
-          }
-#pragma unroll
-          for (int q = 0; q < NI; ++q) {
-            lfw[q] = 0xFFFFFFFFu;
-            bw[q] = 0;
-            x[q] = 0;
-            if (!cf[q]) {
-              if (uself && A.lf) lfw[q] = __ldcg(A.lf + ((t[q] & ((1u << RP_LF_LOG2) - 1u)) >> 5));
-              bw[q] = __ldcg(A.bmB + (i[q] >> 5));
-              x[q] = __ldcg(A.a + i[q]);
-            }
-          }
-#pragma unroll
-          for (int q = 0; q < NI; ++q) {
-            const bool maybe = !cf[q] && uself && ((lfw[q] >> (t[q] & 31)) & 1u);
-            w0[q] = maybe ? __ldcg(A.table + rp_home(t[q], lg)) : RP_EMPTY;
-          }
-#pragma unroll
-          for (int q = 0; q < NI; ++q) {
-            sw[q] = false;
-            y[q] = 0;
-            if (cf[q]) continue;
-            const u64 k = k0 + (u64)q * T;
-            u32 v;
-            if (w0[q] != RP_EMPTY && ((u32)(w0[q] >> 32) == t[q] || table_lookup(A.table, lg, t[q], v))) {
-              table_reserve(A.table, lg, t[q], i[q], dclaim, &g->sync.error);
-              A.cflag[k] = 2;
-              if (t[q] < dlo || t[q] > dhi) c2 -= 1;  // its target was counted as listed
-              continue;
-            }
-            const bool c = !((bw[q] >> (i[q] & 31)) & 1u);
-            A.cflag[k] = c;
-            if (c) {
-              if (!(A.dbg & 1)) {  // PIP_RP_DBG=1: measurement only, no swaps
-                y[q] = (u64)atomicExch((unsigned long long*)A.a + t[q], (unsigned long long)x[q]);
-                sw[q] = true;
-              }
-            } else {
-              fails += 1;
-            }
-          }
-#pragma unroll
-          for (int q = 0; q < NI; ++q)
-            if (sw[q]) A.a[i[q]] = y[q];
-        }
-      } else {
+      {
       u64 k = s + tid;
       u32 ncf = 1, nt = 0, ni = 0;
       if (k < e) {
