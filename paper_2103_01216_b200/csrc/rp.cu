@@ -187,7 +187,10 @@ __device__ __forceinline__ u32 block_excl_sum(u32 v, u32* s_cnt, u32* tot) {
 }
 
 // items per thread per pass in the latency-bound loops (independent loads in flight)
-static constexpr int RB = 4;
+static constexpr int RB_DEFAULT = 4;
+#ifndef PIP_RP_RB3
+#define PIP_RP_RB3 2  // the same for scheme 3: at 8 CTAs per SM (32 registers) 2 spill least (C4 116.7 ms; 4: 120.5, 1: 120.7)
+#endif
 
 __device__ __forceinline__ u64 block_sum(u64 v, u64* s_red) {
   v = warp_reduce<Op<PIP_OP_ADD>>(v);
@@ -360,7 +363,7 @@ __device__ __forceinline__ bool table_lookup(const u64* table, u32 logcap, u32 k
 #define PIP_RP_XPRE 1
 #endif
 #ifndef PIP_RP_MINB3
-#define PIP_RP_MINB3 6  // resident CTAs per SM of the scheme-3 kernel (40 registers; 4: 64, 8: 32)
+#define PIP_RP_MINB3 8  // resident CTAs per SM of the scheme-3 kernel (32 registers; 6: 40, 4: 64)
 #endif
 // MB: resident CTAs per SM the kernel is compiled for.  MB = 1 (scheme 1
 // only) is the flavour for grids of at most one CTA per SM (C0: 79 CTAs):
@@ -369,6 +372,7 @@ template <int V, int BM, int MB = (BM == 3 ? PIP_RP_MINB3 : 4)>
 __global__ void __launch_bounds__(RP_THREADS, MB) rp_kernel(RpArgs A) {
   __shared__ u32 s_cnt[33];
   __shared__ u64 s_red[36];
+  constexpr int RB = BM == 3 ? PIP_RP_RB3 : RB_DEFAULT;
   const u32 b = blockIdx.x, G = gridDim.x, tid = threadIdx.x, T = blockDim.x;
   RpGlobal* g = A.g;
   // The round state (identical in every thread) is touched only between
