@@ -1305,7 +1305,7 @@ static u64 rp_capacity(u64 prefix, int variant) {
 // that, where the random C reads would go to HBM.  PIP_RP_BM=0/1/2 forces.
 static RpLayout rp_layout(u64 n, u64 prefix, int variant, u64 cap, int gmax) {
   if (variant == PIP_RP_FINAL) {
-    int want = n <= (1ull << 28) ? 1 : 3;
+    int want = n < (1ull << 28) ? 1 : 3;  // measured crossover (2^27: 16.4 vs 18.2 ms, 2^28: 33.8 vs 32.0)
     if (const char* e = getenv("PIP_RP_BM")) want = atoi(e);
     if (want == 1 && n > (1ull << 31)) want = 3;  // BM 1 keeps a flag in target bit 31
     if (want >= 1 && want <= 3) {
