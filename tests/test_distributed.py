@@ -70,10 +70,12 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, cases, q, cuda=False):
+def _worker(rank, world, port, cases, q, cuda=False, backend="gloo"):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    if backend == "nccl":
+        torch.cuda.set_device(0)
+    dist.init_process_group(backend, rank=rank, world_size=world)
     try:
         if cuda:
             torch.cuda.set_device(0)
@@ -111,13 +113,13 @@ def _split(case):
     return {"half": n // 2 + 3, "zero": 0, "all": n, "small": 5}[kind]
 
 
-def _run(world, cases, cuda=False):
+def _run(world, cases, cuda=False, backend="gloo"):
     """Run every case in one process group; returns, per case, the ranks'
     (result, final shard) in rank order."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, cases, q, cuda))
+    procs = [ctx.Process(target=_worker, args=(r, world, port, cases, q, cuda, backend))
              for r in range(world)]
     for p in procs:
         p.start()
@@ -209,6 +211,18 @@ def test_sharded_cuda_gloo():
     cases = [("filter", 300_007, 2, "mod3"), ("scan", 200_003, 1),
              ("merge", 400_009, 1, "half", 1 << 12), ("merge", 300_001, 4, "half", 1000)]
     for case, per_rank in zip(cases, _run(2, cases, cuda=True)):
+        _check(case, per_rank)
+
+
+@pytest.mark.gpu
+def test_sharded_cuda_nccl_world1():
+    """The sharded plans over the NCCL backend itself (the backend the SCALE
+    run uses), as far as one GPU allows: a process group of one rank, so
+    every collective (all_gather of totals / counts, the co-rank search's
+    all_reduce on int64 words) really goes through NCCL on device buffers."""
+    cases = [("filter", 300_007, 2, "mod3"), ("scan", 200_003, 1),
+             ("merge", 400_009, 1, "half", 1 << 12), ("merge", 100_001, 4, "small", 1000)]
+    for case, per_rank in zip(cases, _run(1, cases, cuda=True, backend="nccl")):
         _check(case, per_rank)
 
 
