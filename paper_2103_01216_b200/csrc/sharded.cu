@@ -242,9 +242,11 @@ int pip_filter_u64_sharded(uint64_t* a_local, uint64_t n_local, uint64_t n_globa
   // 1. the head of my kept words goes to lower shards, straight from the array
   if (!down.empty()) {
     PIP_NCCL(N.GroupStart());
+    int bad = 0;  // a failed call must not leave the group open
     for (const pip_shard_piece& p : down)
-      PIP_NCCL(N.Send(a_local + p.local_offset, p.length, NCCL_U64, (int)p.peer, nccl_comm, st));
-    PIP_NCCL(N.GroupEnd());
+      bad |= N.Send(a_local + p.local_offset, p.length, NCCL_U64, (int)p.peer, nccl_comm, st);
+    bad |= N.GroupEnd();
+    if (bad) return PIP_ERR_CUDA;
   }
   // 2. what stays moves down to local 0 (one in-place pass)
   if (sl && ss)
@@ -252,9 +254,11 @@ int pip_filter_u64_sharded(uint64_t* a_local, uint64_t n_local, uint64_t n_globa
   // 3. higher ranks' words land above what I kept, in their final slots
   if (!up.empty()) {
     PIP_NCCL(N.GroupStart());
+    int bad = 0;
     for (const pip_shard_piece& p : up)
-      PIP_NCCL(N.Recv(a_local + p.local_offset, p.length, NCCL_U64, (int)p.peer, nccl_comm, st));
-    PIP_NCCL(N.GroupEnd());
+      bad |= N.Recv(a_local + p.local_offset, p.length, NCCL_U64, (int)p.peer, nccl_comm, st);
+    bad |= N.GroupEnd();
+    if (bad) return PIP_ERR_CUDA;
   }
   u64 m = 0;
   for (int r = 0; r < world; ++r) m += counts[r];
