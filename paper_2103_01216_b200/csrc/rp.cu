@@ -93,6 +93,7 @@ struct RpArgs {
   // the active id range (the own checks), a narrow, L2-resident band of it
   u32* bmF;
   u32 logf, dbg;
+  u32 wf, wn;  // scheme 3: weights of a carried-over failure / a fresh iterate in the list split
   u32 tload, pad5;  // collided table: slots per listed iterate (BM 2/3)
   // BM 2/3: listed-key filter, bit (t mod 2^RP_LF_LOG2) set for every listed
   // target, so a first marker probes the collided table only when its bit
@@ -113,6 +114,24 @@ static constexpr u32 RP_LF_LOG2 = 24;  // 2 MiB filter
 __device__ __forceinline__ void part(u64 total, u32 G, u32 b, u64& s, u64& e) {
   s = total * b / G;
   e = total * (b + 1) / G;
+}
+
+// The round's list is [failures of the previous round | fresh iterates].
+// Split it among the CTAs by WEIGHT (wf per failure, wn per fresh iterate):
+// a fresh iterate commits -- and pays for a DRAM exchange -- more often than
+// one that has already failed, so an even split leaves the CTAs of the
+// failure part idle at the end of the commit pass.  Every phase of a round
+// (marks, commit, resolve and the next round's retire) uses the same split.
+__device__ __forceinline__ void lpart(u64 total, u64 nf, u32 wf, u32 wn, u32 G, u32 b, u64& s, u64& e) {
+  if (wf == wn) {
+    part(total, G, b, s, e);
+    return;
+  }
+  if (nf > total) nf = total;
+  const u64 Wf = nf * wf, W = Wf + (total - nf) * wn;
+  auto at = [&](u64 w) -> u64 { return w <= Wf ? w / wf : nf + (w - Wf) / wn; };
+  s = at(W * b / G);
+  e = b + 1 == G ? total : at(W * (b + 1) / G);
 }
 
 // block-wide stable exclusive rank of `f`; *tot = number of set flags
@@ -350,6 +369,10 @@ __device__ __forceinline__ bool table_lookup(const u64* table, u32 logcap, u32 k
 // iterates (plus the first marker of their targets) use the write-max table,
 // sized per round for them alone so that it stays L2-resident.  Same commit
 // rule, so the same rounds as the reference.
+#ifndef PIP_RP_WF_DEFAULT
+#define PIP_RP_WF_DEFAULT 5  // measured at C4: 5:4 116.05 ms, 4:4 116.7, 6:4 116.7, 4:5 121.0
+#define PIP_RP_WN_DEFAULT 4
+#endif
 #ifndef PIP_RP_SPEC1
 #define PIP_RP_SPEC1 1
 #endif
@@ -467,7 +490,8 @@ __global__ void __launch_bounds__(RP_THREADS, MB) rp_kernel(RpArgs A) {
         break;
       }
       u64 s, e;
-      part(F, G, b, s, e);
+      if (BM == 3) lpart(F, R.nfail_prev, A.wf, A.wn, G, b, s, e);
+      else part(F, G, b, s, e);
       const u64 cbefore = s - fbefore;  // committed items in CTAs < b
       const bool targeted = A.targeted_clean_ok && F * 8 < (1ull << A.logcap);
       u64 runf = 0, runc = 0;
@@ -816,7 +840,8 @@ __global__ void __launch_bounds__(RP_THREADS, MB) rp_kernel(RpArgs A) {
     }
     {
       u64 s, e;
-      part(newF, G, b, s, e);
+      if (BM == 3) lpart(newF, nfail, A.wf, A.wn, G, b, s, e);
+      else part(newF, G, b, s, e);
       u32 claims = 0;
       if (BM == 1) {
         // marks already made (refill / previous round's failures)
@@ -1032,7 +1057,8 @@ __global__ void __launch_bounds__(RP_THREADS, MB) rp_kernel(RpArgs A) {
       int c2 = 0;  // BM 3: listed claims of new targets - first markers that joined
       RSET(R.logcap_c = lg);
       u64 s, e;
-      part(newF, G, b, s, e);
+      if (BM == 3) lpart(newF, nfail, A.wf, A.wn, G, b, s, e);
+      else part(newF, G, b, s, e);
       u32 dclaim = 0;
       if (lc_total) {
         const u32 mine = __ldcg(A.lccnt + b);
@@ -1448,6 +1474,9 @@ int rp_device(u64* a, const u64* h, u64 n, u64 prefix, int variant, int debug,
   A.bmF = Lrun.bm == 3 ? (u32*)(w + Lrun.bmF) : nullptr;
   A.logf = Lrun.logf;
   A.dbg = getenv("PIP_RP_DBG") ? (u32)atoi(getenv("PIP_RP_DBG")) : 0u;
+  A.wf = getenv("PIP_RP_WF") ? (u32)atoi(getenv("PIP_RP_WF")) : PIP_RP_WF_DEFAULT;
+  A.wn = getenv("PIP_RP_WN") ? (u32)atoi(getenv("PIP_RP_WN")) : PIP_RP_WN_DEFAULT;
+  if (A.wf < 1 || A.wf > 64 || A.wn < 1 || A.wn > 64) A.wf = A.wn = 1;
   A.tload = 4u;
   const bool use_lf = !(getenv("PIP_RP_LF") && atoi(getenv("PIP_RP_LF")) == 0);
   A.lf = Lrun.bm >= 2 && use_lf ? (u32*)(w + Lrun.lf) : nullptr;
