@@ -50,6 +50,8 @@ struct RpGlobal {
   GridSync sync;  // barrier + abort + kernel error (PIP_ERR_*)
   u64 dlo, dhi;
   u64 t[4];       // ns accumulated per phase by CTA 0 (P1 retire, P2 refill, P3 reserve, P4 commit)
+  u64 ticket;     // scheme 3: next shared piece of the commit pass
+  u64 wsum[5];    // -DPIP_RP_WAITSTAT: ns every CTA spent inside each of scheme 3's 5 barriers, summed
 };
 
 struct RpResume {
@@ -93,6 +95,7 @@ struct RpArgs {
   // the active id range (the own checks), a narrow, L2-resident band of it
   u32* bmF;
   u32 logf, dbg;
+  u32 steal_pct, pad2;  // scheme 3: share of every part handed out by ticket in the commit pass
   u32 wf, wn;  // scheme 3: weights of a carried-over failure / a fresh iterate in the list split
   u32 tload, pad5;  // collided table: slots per listed iterate (BM 2/3)
   // BM 2/3: listed-key filter, bit (t mod 2^RP_LF_LOG2) set for every listed
@@ -373,6 +376,16 @@ __device__ __forceinline__ bool table_lookup(const u64* table, u32 logcap, u32 k
 #define PIP_RP_WF_DEFAULT 5  // measured at C4: 5:4 116.05 ms, 4:4 116.7, 6:4 116.7, 4:5 121.0
 #define PIP_RP_WN_DEFAULT 4
 #endif
+#ifndef PIP_RP_STEAL_DEFAULT
+#define PIP_RP_STEAL_DEFAULT 30
+#endif
+#ifndef PIP_RP_STEAL_STEPS
+#define PIP_RP_STEAL_STEPS 4  // steps of 256 items per shared piece (C4: 1: 115.7 ms, 2: 113.3, 4: 112.5, 8: 113.2)
+#endif
+static constexpr int RP_STEAL_STEPS = PIP_RP_STEAL_STEPS;
+#ifndef PIP_RP_WAITSTAT
+#define PIP_RP_WAITSTAT 0  // measurement build: time every CTA spends inside the barriers
+#endif
 #ifndef PIP_RP_SPEC1
 #define PIP_RP_SPEC1 1
 #endif
@@ -431,6 +444,14 @@ __global__ void __launch_bounds__(RP_THREADS, MB) rp_kernel(RpArgs A) {
     if (ns < P) P = ns;
   }
   u32 gen = 0;
+#if PIP_RP_WAITSTAT
+  u64 wacc[5] = {0, 0, 0, 0, 0}, wt0 = 0;
+#define WSTAT_T0() do { if (tid == 0) wt0 = globaltimer_ns(); } while (0)
+#define WSTAT_T1(i) do { if (tid == 0) wacc[i] += globaltimer_ns() - wt0; } while (0)
+#else
+#define WSTAT_T0() do { } while (0)
+#define WSTAT_T1(i) do { } while (0)
+#endif
   u64 rounds_here = 0;
   const bool trace = A.trace != nullptr;
   const bool tm = b == 0 && tid == 0;
@@ -824,7 +845,9 @@ __global__ void __launch_bounds__(RP_THREADS, MB) rp_kernel(RpArgs A) {
       RSET(R.done = 1; R.cursor = cursor);
       break;
     }
+    WSTAT_T0();
     if (!grid_barrier(&g->sync, gen)) break;
+    WSTAT_T1(0);
     tick(1);
 
     // ======================= P3: reserve ====================================
@@ -876,7 +899,11 @@ __global__ void __launch_bounds__(RP_THREADS, MB) rp_kernel(RpArgs A) {
         // a target other than its first marker lands there, plus a few that
         // only share the folded bit).  Targets inside the active band also
         // set B[t] for the own checks.
-        if (tid == 0) s_cnt[32] = 0;
+        if (tid == 0) {
+          s_cnt[32] = 0;
+          A.failcnt[b] = 0u;           // this round's failures are ADDED (work stealing in the commit pass)
+          if (b == 0) g->ticket = 0;  // nobody draws a ticket before the barriers below
+        }
         __syncthreads();
         const u32 fmask = (u32)((1ull << A.logf) - 1ull);
         u32 tn[RB];  // the next batch's targets travel while this batch marks
@@ -1038,7 +1065,9 @@ __global__ void __launch_bounds__(RP_THREADS, MB) rp_kernel(RpArgs A) {
       // then every first marker looks its target up there: absent => it is
       // the only reserver and commits right away, present => it joins the
       // write-max and is resolved in the short P4 with the others (cflag 2).
-      if (!grid_barrier(&g->sync, gen)) break;
+      WSTAT_T0();
+    if (!grid_barrier(&g->sync, gen)) break;
+    WSTAT_T1(1);
       tick(2);
       u64 claims_total, dummy, lc_total, lc_before;
       if (BM == 2) {  // BM 3 counts distinct targets at the end of the round
@@ -1070,7 +1099,9 @@ __global__ void __launch_bounds__(RP_THREADS, MB) rp_kernel(RpArgs A) {
           if (A.lf) atomicOr(A.lf + ((t & ((1u << RP_LF_LOG2) - 1u)) >> 5), 1u << (t & 31));
           if (BM == 3 && dclaim != before && (t < dlo || t > dhi)) c2 += 1;
         }
-        if (!grid_barrier(&g->sync, gen)) break;
+        WSTAT_T0();
+    if (!grid_barrier(&g->sync, gen)) break;
+    WSTAT_T1(2);
       }
       u32 fails = 0;
       // One item per thread per step (4 CTAs/SM of 64 registers beat 2 CTAs/SM
@@ -1082,7 +1113,7 @@ __global__ void __launch_bounds__(RP_THREADS, MB) rp_kernel(RpArgs A) {
       // issued in two waves instead of a chain: {cflag, target, id} of the
       // next item travel while this one finishes (software pipeline), and the
       // table probe and the own-check word go out together.
-      {
+      auto commit_range = [&](const u64 s, const u64 e) {
       u64 k = s + tid;
       u32 ncf = 1, nt = 0, ni = 0;
       if (k < e) {
@@ -1131,9 +1162,64 @@ __global__ void __launch_bounds__(RP_THREADS, MB) rp_kernel(RpArgs A) {
           fails += 1;
         }
       }
+      };
+      // Scheme 3: the last RP_STEAL_PCT % of every part is not the part
+      // owner's alone: it is cut into pieces of RP_STEAL_STEPS steps that
+      // whichever CTA has finished its own share takes by ticket (round-robin
+      // over the parts), so the CTAs reach the barrier together instead of
+      // waiting ~9% of the pass for the slowest.  A piece lies inside one part;
+      // its failures are added to that part's count (the next round's retire
+      // packs by part).
+      u64 ms = e;  // my part: [s, ms) mine, [ms, e) shared
+      const bool steal = BM == 3 && A.steal_pct && G > 1;
+      u64 plen = 0;
+      if (steal) {
+        // every part keeps the same shared length (parts differ by <= a few items)
+        plen = (newF / G) * A.steal_pct / 100;
+        plen -= plen % T;
+        ms = e - s > plen ? e - plen : s;
+      }
+      {
+        // one call site: first my own share, then pieces by ticket
+        const u64 piece = (u64)RP_STEAL_STEPS * T;
+        const u64 npieces = steal && plen ? ((plen + piece - 1) / piece) * G : 0;
+        u64 lo = s, hi = ms;
+        u32 own_fails = 0, pcur = b;
+        bool mine = true;
+        for (;;) {
+          commit_range(lo, hi);
+          if (!npieces) {
+            own_fails = fails;
+            break;
+          }
+          if (mine) {
+            own_fails = fails;
+            mine = false;
+          } else {
+            const u64 fp = block_sum(fails, s_red);
+            if (tid == 0 && fp) atomicAdd(A.failcnt + pcur, (u32)fp);
+          }
+          fails = 0;
+          __syncthreads();
+          if (tid == 0) s_red[33] = atomicAdd((unsigned long long*)&g->ticket, 1ull);
+          __syncthreads();
+          const u64 tk = s_red[33];
+          if (tk >= npieces) break;
+          // tickets go round-robin over the parts (ticket -> piece is one-to-one)
+          pcur = (u32)(tk % G);
+          u64 ps, pe;
+          lpart(newF, nfail, A.wf, A.wn, G, pcur, ps, pe);
+          const u64 pms = pe - ps > plen ? pe - plen : ps;
+          lo = pms + (tk / G) * piece;
+          hi = lo + piece < pe ? lo + piece : pe;
+          if (lo > hi) lo = hi;
+        }
+        fails = own_fails;
       }
       if (lc_total) {
-        if (!grid_barrier(&g->sync, gen)) break;
+        WSTAT_T0();
+    if (!grid_barrier(&g->sync, gen)) break;
+    WSTAT_T1(3);
         // P4: iterates on collided targets
         for (u64 k = s + tid; k < e; k += T) {
           if (__ldcs(A.cflag + k) != 2) continue;
@@ -1152,7 +1238,10 @@ __global__ void __launch_bounds__(RP_THREADS, MB) rp_kernel(RpArgs A) {
         }
       }
       const u64 f = block_sum(fails, s_red);
-      if (tid == 0) A.failcnt[b] = (u32)f;
+      if (tid == 0) {
+        if (BM == 3) atomicAdd(A.failcnt + b, (u32)f);  // zeroed in the mark phase; others may have added
+        else A.failcnt[b] = (u32)f;
+      }
       if (BM == 3) {
         const u64 c2s = block_sum((u64)(long long)c2, s_red);
         if (tid == 0) A.claim2[b] = (u32)c2s;
@@ -1224,7 +1313,9 @@ __global__ void __launch_bounds__(RP_THREADS, MB) rp_kernel(RpArgs A) {
       if (tid == 0) A.wcnt[b] = (u32)c;
       RSET(R.wpre = 1);
     }
+    WSTAT_T0();
     if (!grid_barrier(&g->sync, gen)) break;
+    WSTAT_T1(4);
     tick(3);
     if (BM == 3) {
       // distinct out-of-window targets of the round (the reference table's
@@ -1249,6 +1340,10 @@ __global__ void __launch_bounds__(RP_THREADS, MB) rp_kernel(RpArgs A) {
     *A.resume = R;
     for (int i = 0; i < 4; ++i) g->t[i] += s_tacc[i];
   }
+#if PIP_RP_WAITSTAT
+  if (tid == 0)
+    for (int i = 0; i < 5; ++i) atomicAdd((unsigned long long*)&g->wsum[i], (unsigned long long)wacc[i]);
+#endif
 }
 
 // ---------------------------------------------------------------------------
@@ -1474,6 +1569,8 @@ int rp_device(u64* a, const u64* h, u64 n, u64 prefix, int variant, int debug,
   A.bmF = Lrun.bm == 3 ? (u32*)(w + Lrun.bmF) : nullptr;
   A.logf = Lrun.logf;
   A.dbg = getenv("PIP_RP_DBG") ? (u32)atoi(getenv("PIP_RP_DBG")) : 0u;
+  A.steal_pct = getenv("PIP_RP_STEAL") ? (u32)atoi(getenv("PIP_RP_STEAL")) : PIP_RP_STEAL_DEFAULT;
+  if (A.steal_pct > 100) A.steal_pct = 100;
   A.wf = getenv("PIP_RP_WF") ? (u32)atoi(getenv("PIP_RP_WF")) : PIP_RP_WF_DEFAULT;
   A.wn = getenv("PIP_RP_WN") ? (u32)atoi(getenv("PIP_RP_WN")) : PIP_RP_WN_DEFAULT;
   if (A.wf < 1 || A.wf > 64 || A.wn < 1 || A.wn > 64) A.wf = A.wn = 1;
@@ -1604,6 +1701,13 @@ int rp_device(u64* a, const u64* h, u64 n, u64 prefix, int variant, int debug,
             (unsigned long long)n, (unsigned long long)P, (unsigned long long)R.rounds,
             (unsigned long long)grid, Gh.t[0] * 1e-6, Gh.t[1] * 1e-6, Gh.t[2] * 1e-6,
             Gh.t[3] * 1e-6);
+#if PIP_RP_WAITSTAT
+  if (timing_enabled())
+    fprintf(stderr, "[pip rp] mean ms per CTA inside barriers: after refill %.3f | after marks %.3f | after listed "
+            "reserve %.3f | before resolve %.3f | end of round %.3f\n",
+            Gh.wsum[0] * 1e-6 / grid, Gh.wsum[1] * 1e-6 / grid, Gh.wsum[2] * 1e-6 / grid,
+            Gh.wsum[3] * 1e-6 / grid, Gh.wsum[4] * 1e-6 / grid);
+#endif
   S.rounds = R.rounds;
   S.total_committed = R.total_committed;
   S.peak_table_count = R.peak;
