@@ -619,10 +619,13 @@ scan_ws_kernel(u64* __restrict__ a, u64 init, const u64* carry_in, u64* total, L
 // so the look-backs of consecutive tiles of this CTA overlap instead of
 // queueing behind one another (the single look-back warp of scan_ws_kernel
 // is busy ~84% of the time at 2^32).
-template <int OP, bool INCLUSIVE, int NWC, int S, int LBW, int D = 1, int MB = 1>
+// TK: tiles are handed out by ticket (one atomic per tile, drawn by the
+// producer one tile ahead) instead of round-robin B + k G: a CTA on a slower
+// SM then takes fewer tiles instead of holding every look-back chain up.
+template <int OP, bool INCLUSIVE, int NWC, int S, int LBW, int D = 1, int MB = 1, bool TK = false>
 __global__ void __launch_bounds__(32 * (NWC + 1 + LBW), MB)
 scan_ws2_kernel(u64* __restrict__ a, u64 init, const u64* carry_in, u64* total, LookbackCtx c,
-                u64 num_tiles) {
+                u64 num_tiles, u32* ticket) {
   using O = Op<OP>;
   constexpr u64 TILE = (u64)NWC * 512;
   constexpr u32 TILE_BYTES = (u32)(TILE * 8);
@@ -633,6 +636,8 @@ scan_ws2_kernel(u64* __restrict__ a, u64 init, const u64* carry_in, u64* total, 
   __shared__ u64 s_agg[S];
   __shared__ u64 s_prefix[S];
   __shared__ volatile int s_abort;
+  __shared__ volatile u64 s_tile[S];  // TK: the tile in each stage (>= num_tiles: the stream's end)
+  __shared__ volatile int s_done;     // TK: every tile of this CTA is stored; look-back warps leave
   const u32 tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const u64 G = gridDim.x, B = blockIdx.x;
   if (tid == 0) {
@@ -643,39 +648,56 @@ scan_ws2_kernel(u64* __restrict__ a, u64 init, const u64* carry_in, u64* total, 
       mbar_init(&empty[s], 1);
     }
     s_abort = 0;
+    s_done = 0;
     mbar_fence_init();
   }
   __syncthreads();
   auto ph = [&](u64 k) { return (u32)((k / S) & 1); };
   auto wait_or_abort = [&](u64* bar, u32 phase) -> bool {
     while (!(PIP_WAIT_NS ? mbar_try_sleep(bar, phase, PIP_WAIT_NS) : mbar_try(bar, phase)))
-      if (s_abort) return false;
+      if (s_abort || (TK && s_done)) return false;
     return true;
   };
+  auto tile_of = [&](u64 k) -> u64 { return TK ? s_tile[k % S] : B + k * G; };
   if (warp == 0) {
     // ------------------------------------------------------------ producer
-    for (u64 k = 0; B + k * G < num_tiles; ++k) {
+    u64 tnext = 0;
+    if (TK && lane == 0) tnext = atomicAdd(ticket, 1u);
+    for (u64 k = 0; TK || B + k * G < num_tiles; ++k) {
       const int s = (int)(k % S);
       if (k >= (u64)S && !wait_or_abort(&empty[s], (u32)(((k / S) - 1) & 1))) return;
+      bool end = false;
       if (lane == 0) {
         fence_proxy_async_smem();
-        const u64 t = B + k * G;
+        const u64 t = TK ? tnext : B + k * G;
+        if (TK) {
+          s_tile[s] = t;
+          if (t >= num_tiles) {  // the end of the stream: hand the stage over empty
+            mbar_arrive(&full[s]);
+            end = true;
+          } else {
+            tnext = atomicAdd(ticket, 1u);  // the next ticket travels while this tile loads
+          }
+        }
+        if (!end) {
         mbar_expect_tx(&full[s], TILE_BYTES);
 #pragma unroll
         for (int q = 0; q < 4; ++q)
           tma_load_1d(ring + s * TILE + q * (TILE / 4), a + t * TILE + q * (TILE / 4), TILE_BYTES / 4,
                       &full[s]);
+        }
       }
+      if (TK && __shfl_sync(0xffffffffu, end ? 1 : 0, 0)) return;
       __syncwarp();
     }
     return;
   }
   if (warp <= (u32)LBW) {
     // ------------------------------------------------ look-back, k = warp-1 mod LBW
-    for (u64 k = warp - 1; B + k * G < num_tiles; k += LBW) {
+    for (u64 k = warp - 1; TK || B + k * G < num_tiles; k += LBW) {
       const int s = (int)(k % S);
-      const u64 t = B + k * G;
       if (!wait_or_abort(&reduced[s], ph(k))) return;
+      const u64 t = tile_of(k);
       const u64 agg = s_agg[s];
       u64 prefix = (t == 0 && carry_in) ? *carry_in : O::identity;
       int ok = 1;
@@ -708,7 +730,7 @@ scan_ws2_kernel(u64* __restrict__ a, u64 init, const u64* carry_in, u64* total, 
     if (!wait_or_abort(&pready[s], ph(k))) return false;
     u64 run = O::apply(s_prefix[s], s_wexc[s][w]);
     const u64* src = ring + s * TILE + w * 512;
-    const u64 wbase = (B + k * G) * TILE + (u64)w * 512;
+    const u64 wbase = tile_of(k) * TILE + (u64)w * 512;
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       const ulonglong2 v = lds2(src + 64 * j + 2 * lane);
@@ -737,12 +759,17 @@ scan_ws2_kernel(u64* __restrict__ a, u64 init, const u64* carry_in, u64* total, 
   static_assert(S >= D + 2, "stages");
   for (u64 k = 0;; ++k) {
     const int s = (int)(k % S);
-    if (B + k * G >= num_tiles) {
+    if (TK && !wait_or_abort(&full[s], ph(k))) return;
+    if (TK ? tile_of(k) >= num_tiles : B + k * G >= num_tiles) {
       for (u64 q = k > (u64)D ? k - D : 0; q < k; ++q)
         if (!scan_store(q)) return;
+      if (TK) {
+        named_bar(1, NWC * 32);
+        if (w == 0 && lane == 0) s_done = 1;  // every tile stored: the look-back warps may leave
+      }
       break;
     }
-    if (!wait_or_abort(&full[s], ph(k))) return;
+    if (!TK && !wait_or_abort(&full[s], ph(k))) return;
     const u64* src = ring + s * TILE + w * 512;
     u64 acc = O::identity;
 #pragma unroll
@@ -976,14 +1003,14 @@ static int launch_scan_ws(u64* a, u64 n, u64 init, const u64* carry, u64* total,
   return PIP_OK;
 }
 
-template <int OP, bool INCL, int NWC, int S, int LBW, int D = 1, int MB = 1>
+template <int OP, bool INCL, int NWC, int S, int LBW, int D = 1, int MB = 1, bool TK = false>
 static int launch_scan_ws2(u64* a, u64 n, u64 init, const u64* carry, u64* total,
                            const ScratchLayout& L, cudaStream_t st, int device) {
   constexpr u64 TILE = (u64)NWC * 512;
   constexpr int THREADS = 32 * (NWC + 1 + LBW);
   const u64 full_tiles = n / TILE;
   const u64 rem = n - full_tiles * TILE;
-  auto k = scan_ws2_kernel<OP, INCL, NWC, S, LBW, D, MB>;
+  auto k = scan_ws2_kernel<OP, INCL, NWC, S, LBW, D, MB, TK>;
   const int smem = (int)(S * TILE * 8);
   PIP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   int per_sm = 0;
@@ -998,7 +1025,8 @@ static int launch_scan_ws2(u64* a, u64 n, u64 init, const u64* carry, u64* total
   PIP_CUDA(cudaMemsetAsync(L.counter, 0, 60, st));
   PIP_CUDA(cudaMemsetAsync(L.slots, 0, sizeof(TileSlot) * 4 * (size_t)grid * stride, st));
   LookbackCtx c{L.slots, L.abort, (u32)(4 * grid), stride};
-  void* args[] = {&a, &init, &carry, &mid, &c, (void*)&full_tiles};
+  u32* ticket = L.counter + 2;  // zeroed with the counters above
+  void* args[] = {&a, &init, &carry, &mid, &c, (void*)&full_tiles, &ticket};
   PIP_CUDA(cudaLaunchCooperativeKernel((const void*)k, dim3(grid), dim3(THREADS), args, smem, st));
   if (rem) return launch_scan_t<OP, INCL, true>(a + full_tiles * TILE, rem, init, L.carry, total, L, st, device);
   return PIP_OK;
@@ -1037,6 +1065,9 @@ static int launch_scan_op(u64* a, u64 n, u64 init, int inclusive, const u64* car
     if (cfg == 17)  // default: producer warp, 3 look-back warps, 13 compute warps 2 tiles ahead
       return inclusive ? launch_scan_ws2<OP, true, 13, 4, 3, 2>(a, n, init, carry, total, L, st, device)
                        : launch_scan_ws2<OP, false, 13, 4, 3, 2>(a, n, init, carry, total, L, st, device);
+    if (cfg == 21)  // 17 with tiles handed out by ticket
+      return inclusive ? launch_scan_ws2<OP, true, 13, 4, 3, 2, 1, true>(a, n, init, carry, total, L, st, device)
+                       : launch_scan_ws2<OP, false, 13, 4, 3, 2, 1, true>(a, n, init, carry, total, L, st, device);
     if (cfg == 18)  // two CTAs per SM, 3072-word tiles
       return inclusive ? launch_scan_ws2<OP, true, 6, 4, 3, 2, 2>(a, n, init, carry, total, L, st, device)
                        : launch_scan_ws2<OP, false, 6, 4, 3, 2, 2>(a, n, init, carry, total, L, st, device);
