@@ -616,9 +616,11 @@ filter_ws_kernel(u64* __restrict__ a, DevPred p, u64* m_out, LookbackCtx c, u64 
 // Split-role pipeline (see scan_ws2_kernel): warp 0 streams tiles in, LBW
 // look-back warps take tiles round-robin so consecutive look-backs overlap,
 // NWC compute warps count tile k and compact + store tile k - D.
-template <int NWC, int S, int PC, int LBW, int D, int J, int MB = 1>
+// TK: tiles handed out by ticket instead of round-robin (see scan_ws2_kernel).
+template <int NWC, int S, int PC, int LBW, int D, int J, int MB = 1, bool TK = false>
 __global__ void __launch_bounds__(32 * (NWC + 1 + LBW), MB)
-filter_ws2_kernel(u64* __restrict__ a, DevPred p, u64* m_out, LookbackCtx c, u64 num_tiles) {
+filter_ws2_kernel(u64* __restrict__ a, DevPred p, u64* m_out, LookbackCtx c, u64 num_tiles,
+                  u32* ticket) {
   using O = Op<PIP_OP_ADD>;
   constexpr u64 TILE = (u64)NWC * 64 * J;  // J word pairs per lane
   constexpr u32 TILE_BYTES = (u32)(TILE * 8);
@@ -633,6 +635,8 @@ filter_ws2_kernel(u64* __restrict__ a, DevPred p, u64* m_out, LookbackCtx c, u64
   __shared__ u64 s_prefix[S];
   __shared__ u32 s_keep[S][NWC * 32];
   __shared__ volatile int s_abort;
+  __shared__ volatile u64 s_tile[S];  // TK: the tile in each stage (>= num_tiles: the stream's end)
+  __shared__ volatile int s_done;     // TK: every tile of this CTA is stored; look-back warps leave
   const u32 tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const u32 lt = (1u << lane) - 1u;
   const u64 G = gridDim.x, B = blockIdx.x;
@@ -644,39 +648,56 @@ filter_ws2_kernel(u64* __restrict__ a, DevPred p, u64* m_out, LookbackCtx c, u64
       mbar_init(&empty[s], 1);
     }
     s_abort = 0;
+    s_done = 0;
     mbar_fence_init();
   }
   __syncthreads();
   auto ph = [&](u64 k) { return (u32)((k / S) & 1); };
   auto wait_or_abort = [&](u64* bar, u32 phase) -> bool {
     while (!(PIP_WAIT_NS ? mbar_try_sleep(bar, phase, PIP_WAIT_NS) : mbar_try(bar, phase)))
-      if (s_abort) return false;
+      if (s_abort || (TK && s_done)) return false;
     return true;
   };
+  auto tile_of = [&](u64 k) -> u64 { return TK ? s_tile[k % S] : B + k * G; };
   if (warp == 0) {
     // ------------------------------------------------------------ producer
-    for (u64 k = 0; B + k * G < num_tiles; ++k) {
+    u64 tnext = 0;
+    if (TK && lane == 0) tnext = atomicAdd(ticket, 1u);
+    for (u64 k = 0; TK || B + k * G < num_tiles; ++k) {
       const int s = (int)(k % S);
       if (k >= (u64)S && !wait_or_abort(&empty[s], (u32)(((k / S) - 1) & 1))) return;
+      bool end = false;
       if (lane == 0) {
         fence_proxy_async_smem();
-        const u64 t = B + k * G;
+        const u64 t = TK ? tnext : B + k * G;
+        if (TK) {
+          s_tile[s] = t;
+          if (t >= num_tiles) {  // the end of the stream: hand the stage over empty
+            mbar_arrive(&full[s]);
+            end = true;
+          } else {
+            tnext = atomicAdd(ticket, 1u);  // the next ticket travels while this tile loads
+          }
+        }
+        if (!end) {
         mbar_expect_tx(&full[s], TILE_BYTES);
 #pragma unroll
         for (int q = 0; q < 4; ++q)
           tma_load_1d(ring + s * STRIDE + q * (TILE / 4), a + t * TILE + q * (TILE / 4), TILE_BYTES / 4,
                       &full[s]);
+        }
       }
+      if (TK && __shfl_sync(0xffffffffu, end ? 1 : 0, 0)) return;
       __syncwarp();
     }
     return;
   }
   if (warp <= (u32)LBW) {
     // ------------------------------------------------ look-back, k = warp-1 mod LBW
-    for (u64 k = warp - 1; B + k * G < num_tiles; k += LBW) {
+    for (u64 k = warp - 1; TK || B + k * G < num_tiles; k += LBW) {
       const int s = (int)(k % S);
-      const u64 t = B + k * G;
       if (!wait_or_abort(&reduced[s], ph(k))) return;
+      const u64 t = tile_of(k);
       const u64 agg = s_agg[s];
       u64 prefix = 0;
       int ok = 1;
@@ -757,12 +778,17 @@ filter_ws2_kernel(u64* __restrict__ a, DevPred p, u64* m_out, LookbackCtx c, u64
   };
   for (u64 k = 0;; ++k) {
     const int s = (int)(k % S);
-    if (B + k * G >= num_tiles) {
+    if (TK && !wait_or_abort(&full[s], ph(k))) break;
+    if (TK ? tile_of(k) >= num_tiles : B + k * G >= num_tiles) {
       for (u64 q = k > (u64)D ? k - D : 0; q < k; ++q)
         if (!scatter(q)) break;
+      if (TK) {
+        named_bar(1, NWC * 32);
+        if (w == 0 && lane == 0) s_done = 1;  // every tile stored: the look-back warps may leave
+      }
       break;
     }
-    if (!wait_or_abort(&full[s], ph(k))) break;
+    if (!TK && !wait_or_abort(&full[s], ph(k))) break;
     const u64* src = ring + s * STRIDE + w * (64 * J);
     u32 keep = 0;
 #pragma unroll
@@ -988,13 +1014,13 @@ static int launch_filter_ws_pc(u64* a, u64 n, const DevPred& p, u64* m_dev,
   return PIP_OK;
 }
 
-template <int NWC, int S, int PC, int LBW, int D, int J, int MB = 1>
+template <int NWC, int S, int PC, int LBW, int D, int J, int MB = 1, bool TK = false>
 static int launch_filter_ws2_pc(u64* a, u64 n, const DevPred& p, u64* m_dev,
                                 const ScratchLayoutF& L, cudaStream_t st, int dev) {
   constexpr u64 TILE = (u64)NWC * 64 * J;
   constexpr int THREADS = 32 * (NWC + 1 + LBW);
   const u64 full_tiles = n / TILE, rem = n - full_tiles * TILE;
-  auto k = filter_ws2_kernel<NWC, S, PC, LBW, D, J, MB>;
+  auto k = filter_ws2_kernel<NWC, S, PC, LBW, D, J, MB, TK>;
   const int smem = (int)(S * (TILE + 2) * 8);
   PIP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   int per_sm = 0;
@@ -1010,21 +1036,22 @@ static int launch_filter_ws2_pc(u64* a, u64 n, const DevPred& p, u64* m_dev,
   PIP_CUDA(cudaMemsetAsync(L.slots, 0, sizeof(TileSlot) * 4 * (size_t)grid * stride, st));
   LookbackCtx c{L.slots, L.abort, (u32)(4 * grid), stride};
   DevPred pp = p;
-  void* args[] = {&a, &pp, &mid, &c, (void*)&full_tiles};
+  u32* ticket = L.counter + 2;  // zeroed with the counters above
+  void* args[] = {&a, &pp, &mid, &c, (void*)&full_tiles, &ticket};
   PIP_CUDA(cudaLaunchCooperativeKernel((const void*)k, dim3(grid), dim3(THREADS), args, smem, st));
   if (rem) return launch_filter<true>(a + full_tiles * TILE, rem, p, m_dev, L, st, dev, L.carry, a);
   return PIP_OK;
 }
 
-template <int NWC, int S, int LBW, int D, int J = 8, int MB = 1>
+template <int NWC, int S, int LBW, int D, int J = 8, int MB = 1, bool TK = false>
 static int launch_filter_ws2(u64* a, u64 n, const DevPred& p, u64* m_dev, const ScratchLayoutF& L,
                              cudaStream_t st, int dev) {
   switch (pred_class(p)) {
-    case PC_MASK: return launch_filter_ws2_pc<NWC, S, PC_MASK, LBW, D, J, MB>(a, n, p, m_dev, L, st, dev);
-    case PC_MOD: return launch_filter_ws2_pc<NWC, S, PC_MOD, LBW, D, J, MB>(a, n, p, m_dev, L, st, dev);
-    case PC_MODODD: return launch_filter_ws2_pc<NWC, S, PC_MODODD, LBW, D, J, MB>(a, n, p, m_dev, L, st, dev);
-    case PC_MODODD0: return launch_filter_ws2_pc<NWC, S, PC_MODODD0, LBW, D, J, MB>(a, n, p, m_dev, L, st, dev);
-    default: return launch_filter_ws2_pc<NWC, S, PC_GEN, LBW, D, J, MB>(a, n, p, m_dev, L, st, dev);
+    case PC_MASK: return launch_filter_ws2_pc<NWC, S, PC_MASK, LBW, D, J, MB, TK>(a, n, p, m_dev, L, st, dev);
+    case PC_MOD: return launch_filter_ws2_pc<NWC, S, PC_MOD, LBW, D, J, MB, TK>(a, n, p, m_dev, L, st, dev);
+    case PC_MODODD: return launch_filter_ws2_pc<NWC, S, PC_MODODD, LBW, D, J, MB, TK>(a, n, p, m_dev, L, st, dev);
+    case PC_MODODD0: return launch_filter_ws2_pc<NWC, S, PC_MODODD0, LBW, D, J, MB, TK>(a, n, p, m_dev, L, st, dev);
+    default: return launch_filter_ws2_pc<NWC, S, PC_GEN, LBW, D, J, MB, TK>(a, n, p, m_dev, L, st, dev);
   }
 }
 
@@ -1074,6 +1101,7 @@ int filter_device(u64* a, u64 n, const pip_pred* pred, u64* m_dev, void* scratch
     if (cfg == 9) return launch_filter_ws<16, 3, true>(a, n, p, m_dev, L, st, dev);
     if (cfg == 10) return launch_filter_ws<12, 4, false, true>(a, n, p, m_dev, L, st, dev);
     if (cfg == 17) return launch_filter_ws2<13, 4, 3, 2>(a, n, p, m_dev, L, st, dev);  // default
+    if (cfg == 35) return launch_filter_ws2<13, 4, 3, 2, 8, 1, true>(a, n, p, m_dev, L, st, dev);  // 17, tiles by ticket
     if (cfg == 18) return launch_filter_ws2<12, 4, 3, 2>(a, n, p, m_dev, L, st, dev);
     // half-size tiles (8 words per lane) with twice the stages, so more tile
     // loads are in flight: 14.3 ms (cfg 19) and 12.4 ms (cfg 20: 4 look-back

@@ -1041,8 +1041,12 @@ static int scan_cfg() {
     // 12.9 ms; 2 look-back warps, 3 stages: 12.2; <12,4,2,2>: 11.6;
     // <10,5,3,3>: 11.7); 6/7/9-12 = other scan_ws variants; 4/5 =
     // aggregate-ahead TMA; 1-3 = plain TMA rings; 0 = registers
+    // 21 = 17 with the tiles handed out by ticket instead of round-robin
+    // (default since the end of round 2: 11.33 vs 11.54 ms over 10 steps,
+    // 11.65 vs 11.80 over 20; the same change on the filter, PIP_FILTER_CFG=35,
+    // measured 9.02 vs 8.95 ms and is not its default)
     const char* e = getenv("PIP_SCAN_CFG");
-    cfg = e ? atoi(e) : 17;
+    cfg = e ? atoi(e) : 21;
   }
   return cfg;
 }
