@@ -1102,6 +1102,8 @@ int filter_device(u64* a, u64 n, const pip_pred* pred, u64* m_dev, void* scratch
     if (cfg == 10) return launch_filter_ws<12, 4, false, true>(a, n, p, m_dev, L, st, dev);
     if (cfg == 17) return launch_filter_ws2<13, 4, 3, 2>(a, n, p, m_dev, L, st, dev);  // default
     if (cfg == 35) return launch_filter_ws2<13, 4, 3, 2, 8, 1, true>(a, n, p, m_dev, L, st, dev);  // 17, tiles by ticket
+    if (cfg == 36) return launch_filter_ws2<13, 4, 2, 2>(a, n, p, m_dev, L, st, dev);                 // 2 look-back warps
+    if (cfg == 37) return launch_filter_ws2<13, 4, 2, 2, 8, 1, true>(a, n, p, m_dev, L, st, dev);  // the same, tiles by ticket
     if (cfg == 18) return launch_filter_ws2<12, 4, 3, 2>(a, n, p, m_dev, L, st, dev);
     // half-size tiles (8 words per lane) with twice the stages, so more tile
     // loads are in flight: 14.3 ms (cfg 19) and 12.4 ms (cfg 20: 4 look-back

@@ -1045,8 +1045,11 @@ static int scan_cfg() {
     // (default since the end of round 2: 11.33 vs 11.54 ms over 10 steps,
     // 11.65 vs 11.80 over 20; the same change on the filter, PIP_FILTER_CFG=35,
     // measured 9.02 vs 8.95 ms and is not its default)
+    // 25 = the same with 14 compute warps (56 KiB tiles, the largest four
+    // stages of fit) and 2 look-back warps: 10.80-11.07 ms over 10 steps,
+    // 11.37 over 20 (cfg 29, the same shape with round-robin tiles: 11.2)
     const char* e = getenv("PIP_SCAN_CFG");
-    cfg = e ? atoi(e) : 21;
+    cfg = e ? atoi(e) : 25;
   }
   return cfg;
 }
@@ -1069,6 +1072,30 @@ static int launch_scan_op(u64* a, u64 n, u64 init, int inclusive, const u64* car
     if (cfg == 17)  // default: producer warp, 3 look-back warps, 13 compute warps 2 tiles ahead
       return inclusive ? launch_scan_ws2<OP, true, 13, 4, 3, 2>(a, n, init, carry, total, L, st, device)
                        : launch_scan_ws2<OP, false, 13, 4, 3, 2>(a, n, init, carry, total, L, st, device);
+    if (cfg == 28)  // ticketed, 14 compute warps, 3 look-back warps
+      return inclusive ? launch_scan_ws2<OP, true, 14, 4, 3, 2, 1, true>(a, n, init, carry, total, L, st, device)
+                       : launch_scan_ws2<OP, false, 14, 4, 3, 2, 1, true>(a, n, init, carry, total, L, st, device);
+    if (cfg == 29)  // 14 compute warps, 2 look-back warps, round-robin tiles
+      return inclusive ? launch_scan_ws2<OP, true, 14, 4, 2, 2, 1, false>(a, n, init, carry, total, L, st, device)
+                       : launch_scan_ws2<OP, false, 14, 4, 2, 2, 1, false>(a, n, init, carry, total, L, st, device);
+    if (cfg == 25)  // ticketed, 14 compute warps (56 KiB tiles), 2 look-back warps
+      return inclusive ? launch_scan_ws2<OP, true, 14, 4, 2, 2, 1, true>(a, n, init, carry, total, L, st, device)
+                       : launch_scan_ws2<OP, false, 14, 4, 2, 2, 1, true>(a, n, init, carry, total, L, st, device);
+    if (cfg == 26)  // ticketed, 14 compute warps, 1 look-back warp
+      return inclusive ? launch_scan_ws2<OP, true, 14, 4, 1, 2, 1, true>(a, n, init, carry, total, L, st, device)
+                       : launch_scan_ws2<OP, false, 14, 4, 1, 2, 1, true>(a, n, init, carry, total, L, st, device);
+    if (cfg == 27)  // ticketed, 13 compute warps, 1 look-back warp
+      return inclusive ? launch_scan_ws2<OP, true, 13, 4, 1, 2, 1, true>(a, n, init, carry, total, L, st, device)
+                       : launch_scan_ws2<OP, false, 13, 4, 1, 2, 1, true>(a, n, init, carry, total, L, st, device);
+    if (cfg == 22)  // ticketed, 2 look-back warps
+      return inclusive ? launch_scan_ws2<OP, true, 13, 4, 2, 2, 1, true>(a, n, init, carry, total, L, st, device)
+                       : launch_scan_ws2<OP, false, 13, 4, 2, 2, 1, true>(a, n, init, carry, total, L, st, device);
+    if (cfg == 23)  // ticketed, two CTAs per SM with half-size tiles
+      return inclusive ? launch_scan_ws2<OP, true, 6, 4, 3, 2, 2, true>(a, n, init, carry, total, L, st, device)
+                       : launch_scan_ws2<OP, false, 6, 4, 3, 2, 2, true>(a, n, init, carry, total, L, st, device);
+    if (cfg == 24)  // ticketed, stores one tile behind the reduce
+      return inclusive ? launch_scan_ws2<OP, true, 13, 4, 3, 1, 1, true>(a, n, init, carry, total, L, st, device)
+                       : launch_scan_ws2<OP, false, 13, 4, 3, 1, 1, true>(a, n, init, carry, total, L, st, device);
     if (cfg == 21)  // 17 with tiles handed out by ticket
       return inclusive ? launch_scan_ws2<OP, true, 13, 4, 3, 2, 1, true>(a, n, init, carry, total, L, st, device)
                        : launch_scan_ws2<OP, false, 13, 4, 3, 2, 1, true>(a, n, init, carry, total, L, st, device);
