@@ -633,7 +633,8 @@ filter_ws2_kernel(u64* __restrict__ a, DevPred p, u64* m_out, LookbackCtx c, u64
   __shared__ u64 s_wexc[S][NWC];
   __shared__ u64 s_agg[S];
   __shared__ u64 s_prefix[S];
-  __shared__ u32 s_keep[S][NWC * 32];
+  // (each lane's keep bits of the tiles between count and compaction stay in
+  // its registers: the same lane compacts the words it counted)
   __shared__ volatile int s_abort;
   __shared__ volatile u64 s_tile[S];  // TK: the tile in each stage (>= num_tiles: the stream's end)
   __shared__ volatile int s_done;     // TK: every tile of this CTA is stored; look-back warps leave
@@ -728,7 +729,7 @@ filter_ws2_kernel(u64* __restrict__ a, DevPred p, u64* m_out, LookbackCtx c, u64
   // the kept words of a tile are compacted inside its own stage buffer (every
   // warp first pulls its 16 words per lane into registers) and leave with one
   // bulk store; only <= 2 ragged words go through the LSU
-  auto scatter = [&](u64 k) -> bool {
+  auto scatter = [&](u64 k, const u32 keep) -> bool {
     const int s = (int)(k % S);
     if (!wait_or_abort(&pready[s], ph(k))) return false;
     const u64 prefix = s_prefix[s];
@@ -738,7 +739,6 @@ filter_ws2_kernel(u64* __restrict__ a, DevPred p, u64* m_out, LookbackCtx c, u64
     // so that shared and global addresses agree modulo 16 bytes
     const u32 par = (u32)(((uintptr_t)(a + prefix) >> 3) & 1u);
     u32 run = (u32)s_wexc[s][w] + par;
-    const u32 keep = s_keep[s][w * 32 + lane];
     const u64* src = stage + w * (64 * J);
     u64 vx[J], vy[J];
     u32 pos[J];
@@ -776,12 +776,17 @@ filter_ws2_kernel(u64* __restrict__ a, DevPred p, u64* m_out, LookbackCtx c, u64
     }
     return true;
   };
+  u32 kq[D + 1];  // kq[j]: keep bits of tile k - j
+#pragma unroll
+  for (int j = 0; j <= D; ++j) kq[j] = 0;
   for (u64 k = 0;; ++k) {
     const int s = (int)(k % S);
     if (TK && !wait_or_abort(&full[s], ph(k))) break;
     if (TK ? tile_of(k) >= num_tiles : B + k * G >= num_tiles) {
-      for (u64 q = k > (u64)D ? k - D : 0; q < k; ++q)
-        if (!scatter(q)) break;
+      // the last D tiles (fewer at the start): tile k - j counted j steps ago
+#pragma unroll
+      for (int j = D; j >= 1; --j)
+        if (k >= (u64)j && !scatter(k - j, kq[j - 1])) break;
       if (TK) {
         named_bar(1, NWC * 32);
         if (w == 0 && lane == 0) s_done = 1;  // every tile stored: the look-back warps may leave
@@ -797,7 +802,9 @@ filter_ws2_kernel(u64* __restrict__ a, DevPred p, u64* m_out, LookbackCtx c, u64
       keep |= ((u32)pred_raw_t<PC>(p, v.x) << (2 * j)) | ((u32)pred_raw_t<PC>(p, v.y) << (2 * j + 1));
     }
     if (PC != PC_GEN && p.negate) keep ^= (2 * J >= 32) ? 0xffffffffu : ((1u << (2 * J)) - 1u);
-    s_keep[s][w * 32 + lane] = keep;
+#pragma unroll
+    for (int j = D; j >= 1; --j) kq[j] = kq[j - 1];
+    kq[0] = keep;
     const u64 cnt = __reduce_add_sync(0xffffffffu, (u32)__popc(keep));  // one REDUX, not 10 shuffles
     if (lane == 0) s_wtot[s][w] = cnt;
     named_bar(1, NWC * 32);
@@ -815,7 +822,7 @@ filter_ws2_kernel(u64* __restrict__ a, DevPred p, u64* m_out, LookbackCtx c, u64
       __syncwarp();
       if (lane == 0) mbar_arrive(&reduced[s]);
     }
-    if (k >= (u64)D && !scatter(k - D)) break;
+    if (k >= (u64)D && !scatter(k - D, kq[D])) break;
   }
   if (w == 0 && lane == 0) bulk_wait_all();  // the bulk stores have landed
 }
@@ -1074,8 +1081,12 @@ static int filter_cfg() {
     // compaction 2 tiles behind the count> (best measured: 10.36 ms at 2^32;
     // cfg 8 = filter_ws_kernel<16,3> 12.5 ms; <12,4,3,2> 10.66; <13,4,4,2>
     // 10.39; <16,3,3,1> 11.04); 0 = register path; 4/5 = aggregate-ahead TMA
+    // 38 (default since the end of round 2) = 14 compute warps (56 KiB tiles,
+    // the largest four stages of fit once each lane's keep bits stay in its
+    // registers instead of shared memory), 2 look-back warps: 8.40 ms at
+    // 2^32 against 8.82 for 17 (39, the same with tiles by ticket: 8.49)
     const char* e = getenv("PIP_FILTER_CFG");
-    cfg = e ? atoi(e) : 17;
+    cfg = e ? atoi(e) : 38;
   }
   return cfg;
 }
@@ -1102,6 +1113,9 @@ int filter_device(u64* a, u64 n, const pip_pred* pred, u64* m_dev, void* scratch
     if (cfg == 10) return launch_filter_ws<12, 4, false, true>(a, n, p, m_dev, L, st, dev);
     if (cfg == 17) return launch_filter_ws2<13, 4, 3, 2>(a, n, p, m_dev, L, st, dev);  // default
     if (cfg == 35) return launch_filter_ws2<13, 4, 3, 2, 8, 1, true>(a, n, p, m_dev, L, st, dev);  // 17, tiles by ticket
+    if (cfg == 38) return launch_filter_ws2<14, 4, 2, 2>(a, n, p, m_dev, L, st, dev);                 // default: 14 compute warps (56 KiB tiles)
+    if (cfg == 40) return launch_filter_ws2<14, 4, 3, 2>(a, n, p, m_dev, L, st, dev);                 // the same with 3 look-back warps
+    if (cfg == 39) return launch_filter_ws2<14, 4, 2, 2, 8, 1, true>(a, n, p, m_dev, L, st, dev);  // the same, tiles by ticket
     if (cfg == 36) return launch_filter_ws2<13, 4, 2, 2>(a, n, p, m_dev, L, st, dev);                 // 2 look-back warps
     if (cfg == 37) return launch_filter_ws2<13, 4, 2, 2, 8, 1, true>(a, n, p, m_dev, L, st, dev);  // the same, tiles by ticket
     if (cfg == 18) return launch_filter_ws2<12, 4, 3, 2>(a, n, p, m_dev, L, st, dev);
