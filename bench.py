@@ -294,7 +294,9 @@ def run_scan(args, ws, rank, local, torch, pip, lib):
             "traffic": (tb * n) if tb else None,
             "note": f"{'16' if ws == 1 else '24'} B/word algorithmic (read+write"
                     f"{'' if ws == 1 else ' + shard reduce'}); peak = {pk['source']}; "
-                    "kernel time = CUDA-event step time (1 launch/step)"}
+                    "kernel time = CUDA-event step time (1 launch/step); the peak is the "
+                    "bandwidth a torch copy measured on this pool, not the HBM limit, so a "
+                    "short run of this kernel can reach or pass 1.0 of it"}
     extra = {"n_per_rank": n}
     e2e = None
     if not args.no_e2e:
