@@ -112,7 +112,10 @@ struct RpArgs {
   const u64* vcnt;
 };
 static constexpr u32 RP_BLK_SHIFT = 12;
-static constexpr u32 RP_LF_LOG2 = 24;  // 2 MiB filter
+#ifndef PIP_RP_LF_LOG2
+#define PIP_RP_LF_LOG2 24
+#endif
+static constexpr u32 RP_LF_LOG2 = PIP_RP_LF_LOG2;  // 2 MiB filter
 
 __device__ __forceinline__ void part(u64 total, u32 G, u32 b, u64& s, u64& e) {
   s = total * b / G;
