@@ -617,7 +617,11 @@ filter_ws_kernel(u64* __restrict__ a, DevPred p, u64* m_out, LookbackCtx c, u64 
 // look-back warps take tiles round-robin so consecutive look-backs overlap,
 // NWC compute warps count tile k and compact + store tile k - D.
 // TK: tiles handed out by ticket instead of round-robin (see scan_ws2_kernel).
-template <int NWC, int S, int PC, int LBW, int D, int J, int MB = 1, bool TK = false>
+// BLK: each lane owns 16 CONSECUTIVE words of its warp's 1024 (read at a lane
+// rotation, so the 16-byte shared-memory loads stay conflict-free): a kept
+// word's place is the lane's base (one 5-step warp scan of the lane counts)
+// plus the kept words below it in the lane's own mask -- no ballots.
+template <int NWC, int S, int PC, int LBW, int D, int J, int MB = 1, bool TK = false, bool BLK = false>
 __global__ void __launch_bounds__(32 * (NWC + 1 + LBW), MB)
 filter_ws2_kernel(u64* __restrict__ a, DevPred p, u64* m_out, LookbackCtx c, u64 num_tiles,
                   u32* ticket) {
@@ -742,6 +746,23 @@ filter_ws2_kernel(u64* __restrict__ a, DevPred p, u64* m_out, LookbackCtx c, u64
     const u64* src = stage + w * (64 * J);
     u64 vx[J], vy[J];
     u32 pos[J];
+    if (BLK) {
+      const u32 cl = __popc(keep);
+      u32 inc = cl;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const u32 t = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= (u32)o) inc += t;
+      }
+      run += inc - cl;  // the lane's first kept word
+#pragma unroll
+      for (int j = 0; j < J; ++j) {
+        const u32 pj = ((u32)j + lane) & (J - 1);
+        const ulonglong2 v = lds2(src + 2 * J * lane + 2 * pj);
+        vx[j] = v.x;
+        vy[j] = v.y;
+      }
+    } else {
 #pragma unroll
     for (int j = 0; j < J; ++j) {
       const bool f0 = (keep >> (2 * j)) & 1u, f1 = (keep >> (2 * j + 1)) & 1u;
@@ -753,12 +774,24 @@ filter_ws2_kernel(u64* __restrict__ a, DevPred p, u64* m_out, LookbackCtx c, u64
       vy[j] = v.y;
       run += __popc(m0) + __popc(m1);
     }
+    }
     named_bar(1, NWC * 32);  // the whole tile is in registers
+    if (BLK) {
+#pragma unroll
+      for (int j = 0; j < J; ++j) {
+        const u32 b0 = 2 * (((u32)j + lane) & (J - 1));
+        const bool f0 = (keep >> b0) & 1u, f1 = (keep >> (b0 + 1)) & 1u;
+        const u32 at = run + __popc(keep & ((1u << b0) - 1u));
+        if (f0) stage[at] = vx[j];
+        if (f1) stage[at + (f0 ? 1u : 0u)] = vy[j];
+      }
+    } else {
 #pragma unroll
     for (int j = 0; j < J; ++j) {
       const bool f0 = (keep >> (2 * j)) & 1u, f1 = (keep >> (2 * j + 1)) & 1u;
       if (f0) stage[pos[j]] = vx[j];
       if (f1) stage[pos[j] + (f0 ? 1u : 0u)] = vy[j];
+    }
     }
     fence_proxy_async_smem();
     named_bar(1, NWC * 32);
@@ -796,10 +829,20 @@ filter_ws2_kernel(u64* __restrict__ a, DevPred p, u64* m_out, LookbackCtx c, u64
     if (!TK && !wait_or_abort(&full[s], ph(k))) break;
     const u64* src = ring + s * STRIDE + w * (64 * J);
     u32 keep = 0;
+    if (BLK) {
+      static_assert(!BLK || (J & (J - 1)) == 0, "lane rotation needs a power-of-two J");
+#pragma unroll
+      for (int j = 0; j < J; ++j) {
+        const u32 pj = ((u32)j + lane) & (J - 1);
+        const ulonglong2 v = lds2(src + 2 * J * lane + 2 * pj);
+        keep |= ((u32)pred_raw_t<PC>(p, v.x) << (2 * pj)) | ((u32)pred_raw_t<PC>(p, v.y) << (2 * pj + 1));
+      }
+    } else {
 #pragma unroll
     for (int j = 0; j < J; ++j) {
       const ulonglong2 v = lds2(src + 64 * j + 2 * lane);
       keep |= ((u32)pred_raw_t<PC>(p, v.x) << (2 * j)) | ((u32)pred_raw_t<PC>(p, v.y) << (2 * j + 1));
+    }
     }
     if (PC != PC_GEN && p.negate) keep ^= (2 * J >= 32) ? 0xffffffffu : ((1u << (2 * J)) - 1u);
 #pragma unroll
@@ -1021,13 +1064,13 @@ static int launch_filter_ws_pc(u64* a, u64 n, const DevPred& p, u64* m_dev,
   return PIP_OK;
 }
 
-template <int NWC, int S, int PC, int LBW, int D, int J, int MB = 1, bool TK = false>
+template <int NWC, int S, int PC, int LBW, int D, int J, int MB = 1, bool TK = false, bool BLK = false>
 static int launch_filter_ws2_pc(u64* a, u64 n, const DevPred& p, u64* m_dev,
                                 const ScratchLayoutF& L, cudaStream_t st, int dev) {
   constexpr u64 TILE = (u64)NWC * 64 * J;
   constexpr int THREADS = 32 * (NWC + 1 + LBW);
   const u64 full_tiles = n / TILE, rem = n - full_tiles * TILE;
-  auto k = filter_ws2_kernel<NWC, S, PC, LBW, D, J, MB, TK>;
+  auto k = filter_ws2_kernel<NWC, S, PC, LBW, D, J, MB, TK, BLK>;
   const int smem = (int)(S * (TILE + 2) * 8);
   PIP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   int per_sm = 0;
@@ -1050,15 +1093,15 @@ static int launch_filter_ws2_pc(u64* a, u64 n, const DevPred& p, u64* m_dev,
   return PIP_OK;
 }
 
-template <int NWC, int S, int LBW, int D, int J = 8, int MB = 1, bool TK = false>
+template <int NWC, int S, int LBW, int D, int J = 8, int MB = 1, bool TK = false, bool BLK = false>
 static int launch_filter_ws2(u64* a, u64 n, const DevPred& p, u64* m_dev, const ScratchLayoutF& L,
                              cudaStream_t st, int dev) {
   switch (pred_class(p)) {
-    case PC_MASK: return launch_filter_ws2_pc<NWC, S, PC_MASK, LBW, D, J, MB, TK>(a, n, p, m_dev, L, st, dev);
-    case PC_MOD: return launch_filter_ws2_pc<NWC, S, PC_MOD, LBW, D, J, MB, TK>(a, n, p, m_dev, L, st, dev);
-    case PC_MODODD: return launch_filter_ws2_pc<NWC, S, PC_MODODD, LBW, D, J, MB, TK>(a, n, p, m_dev, L, st, dev);
-    case PC_MODODD0: return launch_filter_ws2_pc<NWC, S, PC_MODODD0, LBW, D, J, MB, TK>(a, n, p, m_dev, L, st, dev);
-    default: return launch_filter_ws2_pc<NWC, S, PC_GEN, LBW, D, J, MB, TK>(a, n, p, m_dev, L, st, dev);
+    case PC_MASK: return launch_filter_ws2_pc<NWC, S, PC_MASK, LBW, D, J, MB, TK, BLK>(a, n, p, m_dev, L, st, dev);
+    case PC_MOD: return launch_filter_ws2_pc<NWC, S, PC_MOD, LBW, D, J, MB, TK, BLK>(a, n, p, m_dev, L, st, dev);
+    case PC_MODODD: return launch_filter_ws2_pc<NWC, S, PC_MODODD, LBW, D, J, MB, TK, BLK>(a, n, p, m_dev, L, st, dev);
+    case PC_MODODD0: return launch_filter_ws2_pc<NWC, S, PC_MODODD0, LBW, D, J, MB, TK, BLK>(a, n, p, m_dev, L, st, dev);
+    default: return launch_filter_ws2_pc<NWC, S, PC_GEN, LBW, D, J, MB, TK, BLK>(a, n, p, m_dev, L, st, dev);
   }
 }
 
@@ -1115,6 +1158,7 @@ int filter_device(u64* a, u64 n, const pip_pred* pred, u64* m_dev, void* scratch
     if (cfg == 35) return launch_filter_ws2<13, 4, 3, 2, 8, 1, true>(a, n, p, m_dev, L, st, dev);  // 17, tiles by ticket
     if (cfg == 38) return launch_filter_ws2<14, 4, 2, 2>(a, n, p, m_dev, L, st, dev);                 // default: 14 compute warps (56 KiB tiles)
     if (cfg == 40) return launch_filter_ws2<14, 4, 3, 2>(a, n, p, m_dev, L, st, dev);                 // the same with 3 look-back warps
+    if (cfg == 41) return launch_filter_ws2<14, 4, 2, 2, 8, 1, false, true>(a, n, p, m_dev, L, st, dev);  // 38 with lane-blocked words (no ballots)
     if (cfg == 39) return launch_filter_ws2<14, 4, 2, 2, 8, 1, true>(a, n, p, m_dev, L, st, dev);  // the same, tiles by ticket
     if (cfg == 36) return launch_filter_ws2<13, 4, 2, 2>(a, n, p, m_dev, L, st, dev);                 // 2 look-back warps
     if (cfg == 37) return launch_filter_ws2<13, 4, 2, 2, 8, 1, true>(a, n, p, m_dev, L, st, dev);  // the same, tiles by ticket
