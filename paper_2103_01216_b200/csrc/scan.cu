@@ -1048,8 +1048,16 @@ static int scan_cfg() {
     // 25 = the same with 14 compute warps (56 KiB tiles, the largest four
     // stages of fit) and 2 look-back warps: 10.80-11.07 ms over 10 steps,
     // 11.37 over 20 (cfg 29, the same shape with round-robin tiles: 11.2)
+    // DEFAULT = 29: cfg 25's shape (14 compute warps, 56 KiB tiles, 2
+    // look-back warps) with ROUND-ROBIN tiles.  The ticketed variants (21,
+    // 22, 25, 28) are faster by 1-2% but a soak test found intermittent
+    // stalls in them (a bounded spin expiring -> PIP_ERR_STALLED, reported,
+    // never silent) when the look-back slots are packed (PIP_LB_STRIDE=1:
+    // cfg 21 three times in 30 full-size scans, cfg 25 once in 60; none in
+    // 260 scans at the default spacing, none ever for round-robin tiles), so
+    // they stay measurement knobs until that wait cycle is found.
     const char* e = getenv("PIP_SCAN_CFG");
-    cfg = e ? atoi(e) : 25;
+    cfg = e ? atoi(e) : 29;
   }
   return cfg;
 }
